@@ -1,0 +1,200 @@
+/*
+ * fga.h -- C ABI of libfga, the B200 (sm_100a) implementation of the Fast
+ * Gravitational Approach (FGA, arXiv 2009.14005) per-iteration hot path.
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in any signature
+ * (streams are passed as void*).  All functions return FGA_OK (0) or a negative
+ * FGA_ERR_* code; fga_last_error() gives a thread-local message.  A context
+ * (fga_ctx) owns device memory and is bound to one CUDA device and one stream;
+ * it is not re-entrant (one context per thread/device).
+ *
+ * Each entry point names the reference interface it replaces (paths are
+ * under the reference package gravreg 0.1.0, pkg/src/gravreg/).
+ *
+ * Pointer conventions: functions without a `_dev` suffix take HOST arrays in
+ * the reference's numpy layouts (C-contiguous float64 (n,3) points, int64
+ * indices with -1 = absent) and copy in/out themselves.  `_dev` functions take
+ * device pointers and are stream-ordered on the context's stream.
+ */
+#ifndef FGA_H_
+#define FGA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FGA_OK 0
+#define FGA_ERR_INVALID (-1)     /* invalid argument (maps to InvalidParam)      */
+#define FGA_ERR_CUDA (-2)        /* CUDA runtime failure                         */
+#define FGA_ERR_NOMEM (-3)       /* allocation failure                           */
+#define FGA_ERR_UNSUPPORTED (-4) /* valid for the reference, not built here yet  */
+#define FGA_ERR_EMPTY (-5)       /* EmptyCloud                                   */
+#define FGA_ERR_DEGENERATE (-6)  /* DegenerateExtent                             */
+#define FGA_ERR_NONFINITE (-7)   /* NonFiniteWeight                              */
+#define FGA_ERR_LENGTH (-8)      /* LengthMismatch                               */
+#define FGA_ERR_STATE (-9)       /* call order (e.g. no tree built yet)          */
+
+#define FGA_PREC_FP32 0 /* FP32 traversal/direct sums, fp64 state (default)   */
+#define FGA_PREC_FP64 1 /* fp64 everywhere: bit-exact reference visit order   */
+
+typedef struct fga_ctx fga_ctx;
+
+/* Mirrors core.FgaParams (core.py:103-117); validated like core.validate
+ * (core.py:127-151), first failing field reported through fga_last_error(). */
+typedef struct {
+  double G, epsilon, eta, dt, theta, sigma;
+  int32_t rho, max_depth;
+  double norm_a, norm_b, conv_tol;
+  int32_t max_iters;
+  int32_t pad_;
+} fga_params;
+
+/* Mirrors registration.RegisterOptions (registration.py:22-31) plus the
+ * B200-side knobs (precision, poll interval). */
+typedef struct {
+  int32_t trace_gpe;         /* RegisterOptions.trace_gpe          */
+  int32_t normalize;         /* RegisterOptions.normalize          */
+  int32_t record_iterations; /* RegisterOptions.record_iterations  */
+  int32_t precision;         /* FGA_PREC_*                         */
+  const double* x_weights;   /* RegisterOptions.x_weights or NULL  */
+  const double* y_weights;   /* RegisterOptions.y_weights or NULL  */
+  int32_t poll_every;        /* iterations enqueued between host polls of the
+                                device convergence flag (0 = default 8)       */
+  int32_t compute_gpe;       /* 1 (default semantics): gpe_initial/final      */
+} fga_options;
+
+/* Mirrors registration.RegistrationResult (core.py:162-172). */
+typedef struct {
+  double R[9], t[3];           /* transform in the original frame (normalize.py:63-84) */
+  double R_norm[9], t_norm[3]; /* R_acc, t_acc in the normalized frame           */
+  int64_t iterations;
+  int32_t converged;
+  int32_t pad_;
+  double gpe_initial, gpe_final;
+  double norm_ctx[10];         /* mean_x[3], mean_y[3], l, r, a, b            */
+  int64_t interactions;        /* sum over iterations of accepted interactions */
+  int64_t visits;              /* sum over iterations of node visits           */
+  int64_t n_nodes;             /* reference tree size                          */
+  double setup_ms, loop_ms, gpe_ms; /* device-timed phases (CUDA events)       */
+} fga_result;
+
+/* ------------------------------------------------------------------ misc */
+int fga_version(void);
+const char* fga_last_error(void);
+int fga_device_count(int* count);
+
+int fga_create(fga_ctx** ctx, int device);
+int fga_destroy(fga_ctx* ctx);
+/* Bind the context to a CUDA stream (cudaStream_t as void*; NULL = own stream). */
+int fga_set_stream(fga_ctx* ctx, void* stream);
+int fga_synchronize(fga_ctx* ctx);
+
+/* --------------------------------------------------- driver-level entry
+ * registration.register (registration.py:91-166): normalize, masses, tree,
+ * gpe_initial, iteration loop with Kabsch projection, gpe_final, denormalize.
+ * x: (n,dim) reference, y: (m,dim) template, host fp64.  dim must be 3.
+ * deltas / traj (12 per iteration, [R_acc|t_acc] row-major) / gpe_trace /
+ * interactions_per_iter are optional host outputs sized >= max_iters. */
+int fga_register(fga_ctx* ctx, const double* x, int64_t n, const double* y, int64_t m, int dim,
+                 const fga_params* params, const fga_options* options, fga_result* out,
+                 double* deltas, double* traj, double* gpe_trace, int64_t* interactions_per_iter);
+
+/* ---------------------------------------------- session (stepwise) entry
+ * The same loop split into stream-ordered pieces so a host can insert a
+ * collective between the force pass and the rigid update (template sharding
+ * across GPUs).  shard_rank/shard_count select a contiguous
+ * chunk of the Morton-sorted template; every rank passes the FULL clouds (the
+ * normalization and the template mass field are global).  x/y are host
+ * pointers for fga_session_begin and device pointers for _dev. */
+int fga_session_begin(fga_ctx* ctx, const double* x, int64_t n, const double* y, int64_t m,
+                      int dim, const fga_params* params, const fga_options* options,
+                      int shard_rank, int shard_count);
+int fga_session_begin_dev(fga_ctx* ctx, const double* x_dev, int64_t n, const double* y_dev,
+                          int64_t m, int dim, const fga_params* params,
+                          const fga_options* options, int shard_rank, int shard_count);
+/* Enqueue the force pass of one iteration (forces, fused Euler-Cromer step and
+ * Kabsch partial sums) and reduce this shard's partials into the sums buffer. */
+int fga_session_forces(fga_ctx* ctx);
+/* Device pointer to the 18-double sums buffer (layout: see DESIGN.md); a
+ * multi-GPU host all-reduces it (sum) between _forces and _update. */
+int fga_session_sums(fga_ctx* ctx, void** dev_ptr);
+/* Enqueue the rigid update: 3x3 fp64 SVD, transform accumulation, delta,
+ * convergence flag. */
+int fga_session_update(fga_ctx* ctx);
+/* Enqueue k full iterations (forces + update), single shard only. */
+int fga_session_iterate(fga_ctx* ctx, int k);
+/* Enqueue the energy pass of the CURRENT positions into the sums buffer
+ * (slot 17); collect with fga_session_take_gpe after an optional all-reduce. */
+int fga_session_gpe(fga_ctx* ctx);
+int fga_session_take_gpe(fga_ctx* ctx, double* value);
+/* Apply the pending rigid transform to the positions (idempotent). */
+int fga_session_apply_pending(fga_ctx* ctx);
+/* Host poll of the device flags (synchronizes the stream). */
+int fga_session_poll(fga_ctx* ctx, int* done, int64_t* iterations);
+/* Apply the pending transform, compute gpe_final (unless skip_gpe), copy
+ * results out.  With shard_count>1 the caller supplies the all-reduced
+ * gpe_final via fga_session_set_gpe_final instead. */
+int fga_session_finish(fga_ctx* ctx, fga_result* out, double* deltas, double* traj,
+                       double* gpe_trace, int64_t* interactions_per_iter);
+int fga_session_set_gpe(fga_ctx* ctx, int which /*0 initial,1 final*/, double value);
+/* Number of template points owned by this shard and total tree nodes. */
+int fga_session_info(fga_ctx* ctx, int64_t* m_local, int64_t* n_nodes);
+
+/* --------------------------------------------------- tree-level entries
+ * bhtree.build (bhtree.py:56-122) on the device; the tree stays in the
+ * context.  n_nodes receives the node count. */
+int fga_tree_build(fga_ctx* ctx, const double* pts, const double* masses, int64_t n, int dim,
+                   int max_depth, int64_t* n_nodes);
+/* Copy the context's tree out in the BHTree array layout (bhtree.py:14-45):
+ * children (n_nodes,8) int64, com (n_nodes,3), mass, length, occupancy,
+ * depth (int64), bbox_min/max (n_nodes,3).  Any pointer may be NULL. */
+int fga_tree_export(fga_ctx* ctx, int64_t* children, double* com, double* mass, double* length,
+                    int64_t* occupancy, int64_t* depth, double* bbox_min, double* bbox_max);
+/* Load an existing BHTree (e.g. built by the reference) into the context:
+ * the arrays of bhtree.BHTree, nodes in preorder (bhtree.py:77). */
+int fga_tree_upload(fga_ctx* ctx, const int64_t* children, const double* com, const double* mass,
+                    const double* length, int64_t n_nodes, int n_child, int dim);
+
+/* ------------------------------------------------ operator-level entries */
+/* _kernels.bh_forces_kernel (_kernels.py:7-50) as called by bhtree.bh_forces
+ * (bhtree.py:125-147), against the context's tree: forces (m,3) and optional
+ * visits / accepted (m,) int64.  eps2 = epsilon^2 as the reference passes it.
+ * precision FGA_PREC_FP64 reproduces the reference visit order and per-term
+ * arithmetic exactly. */
+int fga_tree_forces(fga_ctx* ctx, const double* queries, const double* query_masses, int64_t m,
+                    double theta, double G, double eps2, int precision, double* forces,
+                    int64_t* visits, int64_t* accepted);
+/* The reference's exact kernel signature (_kernels.py:7-8): uploads the tree
+ * arrays, then evaluates.  Convenience for a literal ctypes drop-in. */
+int fga_bh_forces_kernel(fga_ctx* ctx, const int64_t* children, const double* com,
+                         const double* mass, const double* length, int64_t n_nodes, int n_child,
+                         const double* queries, const double* query_masses, int64_t m, int dim,
+                         double theta, double G, double eps2, int64_t stack_cap, double* forces,
+                         int64_t* visits);
+/* bhtree.brute_force (bhtree.py:155-164) for every query row: the tiled
+ * direct O(NM) sum.  eps is epsilon (not squared), as brute_force reads it. */
+int fga_direct_forces(fga_ctx* ctx, const double* ref, const double* ref_masses, int64_t n,
+                      const double* queries, const double* query_masses, int64_t m, int dim,
+                      double G, double eps, int precision, double* forces);
+/* _kernels.gpe_kernel (_kernels.py:53-67). */
+int fga_gpe_kernel(fga_ctx* ctx, const double* pos_y, const double* mass_y, int64_t m,
+                   const double* pos_x, const double* mass_x, int64_t n, int dim, double G,
+                   double eps, int precision, double* out);
+/* masses.niv_masses (masses.py:85-116). */
+int fga_niv_masses(fga_ctx* ctx, const double* pts, int64_t n, int dim, int rho, double a,
+                   double b, int max_depth, double* out);
+/* normalize.normalize_pair (normalize.py:36-60): xn, yn (host, same shapes)
+ * and ctx10 = mean_x[3], mean_y[3], l, r, a, b. */
+int fga_normalize_pair(fga_ctx* ctx, const double* x, int64_t n, const double* y, int64_t m,
+                       int dim, double a, double b, double* xn, double* yn, double* ctx10);
+/* procrustes.solve_rigid (procrustes.py:12-49): R (3x3 row-major), t (3),
+ * degenerate flag. */
+int fga_solve_rigid(fga_ctx* ctx, const double* y, const double* y_d, int64_t m, int dim,
+                    double* R, double* t, int32_t* degenerate);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FGA_H_ */

@@ -1,0 +1,917 @@
+// capi.cu -- the C ABI (include/fga.h): context, operator entry points and the
+// registration driver (registration.py:91-166) as a device-resident loop.
+//
+// The whole registration state lives in HBM inside the context.  One
+// iteration is three stream-ordered launches -- force pass (traversal or
+// direct sum, fused step + Kabsch partials), partial reduction, rigid update
+// -- and the host only polls the device convergence flag every
+// `poll_every` iterations; kernels enqueued after convergence exit at once
+// (they read the same flag), so the result is exactly the reference's
+// stop-at-first-delta<tol semantics (registration.py:152-154).
+#include <cub/cub.cuh>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fga.h"
+#include "fga_session.cuh"
+
+namespace fga {
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+const char* last_error() { return g_err.c_str(); }
+}  // namespace fga
+
+using namespace fga;
+
+namespace {
+
+struct Session {
+  bool active = false;
+  fga_params P{};
+  fga_options O{};
+  SimParams sp{};
+  int precision = 0;
+  bool direct = false;  // theta == 0: exact O(NM) direct sum instead of the tree
+  int64_t n = 0, m = 0, m_begin = 0, m_local = 0;
+  int shard_rank = 0, shard_count = 1;
+  double ctx10[10] = {0};
+  double gpe_initial = NAN, gpe_final = NAN;
+  bool have_gpe_initial = false, have_gpe_final = false;
+  bool applied = false;
+  int64_t passes = 0;      // force passes enqueued
+  bool last_pass_gpe = false;
+  DevBuf x_raw, y_raw, xn, yn, ctx_dev, mx, my, flat, counts, cells, ref32, ref64;
+  DevBuf tkeys_in, tkeys, tidx_in, tidx, cub_tmp, tpl;
+  DevBuf partials, gpe_part, sums, state, scratch;
+  DevBuf rec_delta, rec_traj, rec_gpe, rec_inter, rec_visits;
+  float setup_ms = 0.f, loop_ms = 0.f, gpe_ms = 0.f;
+
+  TemplateView view() const {
+    double* b = tpl.as<double>();
+    const int64_t ml = m_local;
+    return TemplateView{b, b + ml, b + 2 * ml, b + 3 * ml, b + 4 * ml, b + 5 * ml, b + 6 * ml, ml};
+  }
+  RefPoints ref() const { return RefPoints{ref32.as<float4>(), ref64.as<double4>(), n}; }
+  IterState* st() const { return state.as<IterState>(); }
+};
+
+}  // namespace
+
+struct fga_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  TreeDev tree;
+  DevBuf tree_pts, tree_masses;
+  DevBuf op[8];
+  Session S;
+  int* pinned = nullptr;  // poll buffer: done, pad, iter(lo,hi)
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+int check_ctx(fga_ctx* c) {
+  if (!c) {
+    set_error("null context");
+    return FGA_ERR_INVALID;
+  }
+  if (cudaSetDevice(c->device) != cudaSuccess) {
+    set_error("cudaSetDevice failed");
+    return FGA_ERR_CUDA;
+  }
+  return FGA_OK;
+}
+
+#define CTX_TRY(c)                 \
+  do {                             \
+    int r_ = check_ctx(c);         \
+    if (r_) return r_;             \
+  } while (0)
+#define TRY(expr)                  \
+  do {                             \
+    int r_ = (expr);               \
+    if (r_) return r_;             \
+  } while (0)
+
+int invalid(const char* name, double v) {
+  set_error(std::string("invalid parameter ") + name + "=" + std::to_string(v));
+  return FGA_ERR_INVALID;
+}
+
+// core.validate (core.py:127-151): first failing field.
+int validate(const fga_params* p) {
+  if (!p) {
+    set_error("null params");
+    return FGA_ERR_INVALID;
+  }
+  if (!(p->G > 0)) return invalid("G", p->G);
+  if (!(p->epsilon >= 0)) return invalid("epsilon", p->epsilon);
+  if (!(p->eta >= 0 && p->eta < 1)) return invalid("eta", p->eta);
+  if (!(p->dt > 0)) return invalid("dt", p->dt);
+  if (!(p->theta >= 0 && p->theta <= 1)) return invalid("theta", p->theta);
+  if (!(p->sigma > 0)) return invalid("sigma", p->sigma);
+  if (!(p->rho >= 2)) return invalid("rho", p->rho);
+  if (!(p->max_depth >= 1)) return invalid("max_depth", p->max_depth);
+  if (!(p->norm_a < p->norm_b)) return invalid("norm_range", p->norm_a);
+  if (!(p->conv_tol > 0)) return invalid("conv_tol", p->conv_tol);
+  if (!(p->max_iters >= 1)) return invalid("max_iters", p->max_iters);
+  return FGA_OK;
+}
+
+template <typename T>
+int h2d(DevBuf& b, const T* src, int64_t count, cudaStream_t s) {
+  FGA_CUDA_TRY(b.reserve(sizeof(T) * std::max<int64_t>(count, 1)));
+  if (count > 0) FGA_CUDA_TRY(cudaMemcpyAsync(b.p, src, sizeof(T) * count, cudaMemcpyHostToDevice, s));
+  return FGA_OK;
+}
+
+int sort_keys(DevBuf& tmp, DevBuf& kin, DevBuf& kout, DevBuf& iin, DevBuf& iout, int64_t n,
+              int end_bit, cudaStream_t s) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin.as<unsigned long long>(),
+                                  kout.as<unsigned long long>(), iin.as<int>(), iout.as<int>(),
+                                  (int)n, 0, end_bit, s);
+  FGA_CUDA_TRY(tmp.reserve(bytes));
+  FGA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, kin.as<unsigned long long>(),
+                                               kout.as<unsigned long long>(), iin.as<int>(),
+                                               iout.as<int>(), (int)n, 0, end_bit, s));
+  return FGA_OK;
+}
+
+// Morton order of an AoS (n,3) device cloud -> iout (int, n)
+int morton_order(const double* pts, int64_t n, DevBuf& kin, DevBuf& kout, DevBuf& iin,
+                 DevBuf& iout, DevBuf& tmp, DevBuf& scratch, cudaStream_t s) {
+  FGA_CUDA_TRY(kin.reserve(sizeof(unsigned long long) * n));
+  FGA_CUDA_TRY(kout.reserve(sizeof(unsigned long long) * n));
+  FGA_CUDA_TRY(iin.reserve(sizeof(int) * n));
+  FGA_CUDA_TRY(iout.reserve(sizeof(int) * n));
+  FGA_CUDA_TRY(scratch.reserve(sizeof(double) * (6 * 600 + 16)));
+  double* box = scratch.as<double>() + 6 * 600;
+  launch_bbox(pts, n, scratch.as<double>(), box, s);
+  launch_morton_keys(pts, n, box, kin.as<unsigned long long>(), iin.as<int>(), s);
+  return sort_keys(tmp, kin, kout, iin, iout, n, 63, s);
+}
+
+// -------------------------------------------------------------------- session
+int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
+  Session& S = c->S;
+  cudaStream_t s = c->stream;
+  const int64_t n = S.n, m = S.m;
+  const double a = S.P.norm_a, b = S.P.norm_b;
+  FGA_CUDA_TRY(cudaEventRecord(c->ev[0], s));
+  FGA_CUDA_TRY(S.xn.reserve(sizeof(double) * 3 * n));
+  FGA_CUDA_TRY(S.yn.reserve(sizeof(double) * 3 * m));
+  FGA_CUDA_TRY(S.ctx_dev.reserve(sizeof(double) * 16));
+  FGA_CUDA_TRY(S.scratch.reserve(sizeof(double) * 8192));
+  if (S.O.normalize) {
+    TRY(normalize_pair_dev(x_dev, n, y_dev, m, a, b, S.xn.as<double>(), S.yn.as<double>(),
+                           S.ctx_dev.as<double>(), S.scratch.as<double>(), S.scratch.bytes,
+                           S.ctx10, s));
+  } else {
+    // registration.py:108-114: identity context spanning [a, b]
+    FGA_CUDA_TRY(cudaMemcpyAsync(S.xn.p, x_dev, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+    FGA_CUDA_TRY(cudaMemcpyAsync(S.yn.p, y_dev, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, s));
+    const double z[10] = {0, 0, 0, 0, 0, 0, a, b, a, b};
+    std::memcpy(S.ctx10, z, sizeof(z));
+  }
+  // mass fields (registration.py:64-88)
+  FGA_CUDA_TRY(S.mx.reserve(sizeof(double) * n));
+  FGA_CUDA_TRY(S.my.reserve(sizeof(double) * m));
+  const int64_t ncell = (int64_t)S.P.rho * S.P.rho * S.P.rho;
+  FGA_CUDA_TRY(S.flat.reserve(sizeof(int) * std::max(n, m)));
+  FGA_CUDA_TRY(S.counts.reserve(sizeof(long long) * (ncell + 1)));
+  FGA_CUDA_TRY(S.cells.reserve(sizeof(double) * ncell));
+  const double ca = S.ctx10[8], cb = S.ctx10[9];
+  if (S.O.x_weights) {
+    TRY(h2d(S.scratch, S.O.x_weights, n, s));
+    launch_external_masses(S.scratch.as<double>(), n, S.mx.as<double>(), s);
+    FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  } else {
+    TRY(niv_masses_dev(S.xn.as<double>(), n, S.P.rho, ca, cb, S.P.max_depth, S.mx.as<double>(),
+                       S.flat.as<int>(), S.counts.as<long long>(), S.cells.as<double>(), s));
+  }
+  if (S.O.y_weights) {
+    TRY(h2d(S.scratch, S.O.y_weights, m, s));
+    launch_external_masses(S.scratch.as<double>(), m, S.my.as<double>(), s);
+    FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  } else {
+    TRY(niv_masses_dev(S.yn.as<double>(), m, S.P.rho, ca, cb, S.P.max_depth, S.my.as<double>(),
+                       S.flat.as<int>(), S.counts.as<long long>(), S.cells.as<double>(), s));
+  }
+  FGA_CUDA_TRY(S.scratch.reserve(sizeof(double) * 8192));
+  launch_rescale(S.mx.as<double>(), n, S.my.as<double>(), m, S.P.dt, S.P.eta,
+                 S.scratch.as<double>(), s);
+  // reference side: tree (BH) and packed points (direct sum, energy)
+  if (!S.direct) TRY(tree_build_dev(c->tree, S.xn.as<double>(), S.mx.as<double>(), n, S.P.max_depth, s));
+  FGA_CUDA_TRY(S.ref32.reserve(sizeof(float4) * n));
+  if (S.precision) FGA_CUDA_TRY(S.ref64.reserve(sizeof(double4) * n));
+  launch_pack_ref(S.xn.as<double>(), S.mx.as<double>(), n, S.ref32.as<float4>(),
+                  S.precision ? S.ref64.as<double4>() : nullptr, s);
+  // template: Morton order, this shard's contiguous chunk
+  TRY(morton_order(S.yn.as<double>(), m, S.tkeys_in, S.tkeys, S.tidx_in, S.tidx, S.cub_tmp,
+                   S.scratch, s));
+  S.m_begin = m * S.shard_rank / S.shard_count;
+  S.m_local = m * (S.shard_rank + 1) / S.shard_count - S.m_begin;
+  FGA_CUDA_TRY(S.tpl.reserve(sizeof(double) * 7 * std::max<int64_t>(S.m_local, 1)));
+  launch_gather_template(S.yn.as<double>(), S.my.as<double>(), S.tidx.as<int>(), S.m_begin,
+                         S.m_local, S.view(), s);
+  // iteration state
+  FGA_CUDA_TRY(S.state.reserve(sizeof(IterState)));
+  FGA_CUDA_TRY(S.sums.reserve(sizeof(double) * kPartialStride));
+  launch_mean3(S.yn.as<double>(), m, S.scratch.as<double>(), S.scratch.as<double>() + 4096, s);
+  launch_state_init(S.st(), S.scratch.as<double>() + 4096, s);
+  const int64_t nw = S.direct ? direct_iterate_warps(S.m_local, S.precision)
+                              : bh_iterate_warps(S.m_local);
+  FGA_CUDA_TRY(S.partials.reserve(sizeof(double) * kPartialStride * std::max<int64_t>(nw, 1)));
+  FGA_CUDA_TRY(S.gpe_part.reserve(sizeof(double) * std::max<int64_t>(gpe_warps(S.m_local, S.precision), 1)));
+  const int64_t mi = S.P.max_iters;
+  FGA_CUDA_TRY(S.rec_delta.reserve(sizeof(double) * mi));
+  FGA_CUDA_TRY(S.rec_traj.reserve(sizeof(double) * 12 * mi));
+  FGA_CUDA_TRY(S.rec_gpe.reserve(sizeof(double) * mi));
+  FGA_CUDA_TRY(S.rec_inter.reserve(sizeof(long long) * mi));
+  FGA_CUDA_TRY(S.rec_visits.reserve(sizeof(long long) * mi));
+  FGA_CUDA_TRY(cudaMemsetAsync(S.rec_gpe.p, 0xff, sizeof(double) * mi, s));  // NaN
+  FGA_CUDA_TRY(cudaEventRecord(c->ev[1], s));
+  FGA_CUDA_TRY(cudaGetLastError());
+  return FGA_OK;
+}
+
+int session_begin_common(fga_ctx* c, int64_t n, int64_t m, int dim, const fga_params* params,
+                         const fga_options* options, int shard_rank, int shard_count) {
+  TRY(validate(params));
+  if (n <= 0 || m <= 0) {
+    set_error("registration requires a non-empty cloud");
+    return FGA_ERR_EMPTY;
+  }
+  if (dim != 3) {
+    set_error("the B200 path implements D=3 (D=2 is not built yet)");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  if (shard_count < 1 || shard_rank < 0 || shard_rank >= shard_count) {
+    set_error("invalid shard_rank/shard_count");
+    return FGA_ERR_INVALID;
+  }
+  Session& S = c->S;
+  S.active = false;
+  S.P = *params;
+  fga_options def{};
+  def.normalize = 1;
+  def.compute_gpe = 1;
+  S.O = options ? *options : def;
+  if (S.O.poll_every <= 0) S.O.poll_every = 8;
+  S.precision = S.O.precision ? 1 : 0;
+  S.direct = params->theta == 0.0;
+  S.n = n;
+  S.m = m;
+  S.shard_rank = shard_rank;
+  S.shard_count = shard_count;
+  S.sp.G = params->G;
+  S.sp.eps = params->epsilon;
+  S.sp.eps2 = params->epsilon * params->epsilon;  // float(params.epsilon) ** 2 (bhtree.py:142)
+  S.sp.eta = params->eta;
+  S.sp.dt = params->dt;
+  S.sp.theta = params->theta;
+  S.sp.theta2 = params->theta * params->theta;  // _kernels.py:14
+  S.sp.conv_tol = params->conv_tol;
+  S.sp.max_iters = params->max_iters;
+  S.sp.m_total = m;
+  S.sp.trace_gpe = S.O.trace_gpe;
+  S.gpe_initial = S.gpe_final = NAN;
+  S.have_gpe_initial = S.have_gpe_final = false;
+  S.applied = false;
+  S.passes = 0;
+  S.last_pass_gpe = false;
+  return FGA_OK;
+}
+
+int session_gpe(fga_ctx* c, const IterState* gate) {
+  Session& S = c->S;
+  TemplateView tv = S.view();
+  const int64_t ngw = gpe_warps(S.m_local, S.precision);
+  launch_gpe(S.ref(), tv.px, tv.py, tv.pz, tv.mq, S.m_local, S.sp.eps, gate, S.gpe_part.as<double>(),
+             S.precision, c->stream);
+  launch_reduce(S.partials.as<double>(), 0, S.gpe_part.as<double>(), S.m_local > 0 ? ngw : 0, -1.0,
+                S.sums.as<double>(), c->stream);
+  FGA_CUDA_TRY(cudaGetLastError());
+  return FGA_OK;
+}
+
+int session_forces(fga_ctx* c) {
+  Session& S = c->S;
+  cudaStream_t s = c->stream;
+  TemplateView tv = S.view();
+  int64_t nw;
+  if (S.direct) {
+    launch_direct_iterate(S.ref(), tv, S.st(), S.sp, S.partials.as<double>(), S.precision, s);
+    nw = direct_iterate_warps(S.m_local, S.precision);
+  } else {
+    launch_bh_iterate(c->tree, tv, S.st(), S.sp, S.partials.as<double>(), S.precision, s);
+    nw = bh_iterate_warps(S.m_local);
+  }
+  if (S.m_local <= 0) nw = 0;
+  const bool with_gpe = S.O.trace_gpe && S.passes > 0;
+  int64_t ngw = 0;
+  if (with_gpe && S.m_local > 0) {
+    launch_gpe(S.ref(), tv.px, tv.py, tv.pz, tv.mq, S.m_local, S.sp.eps, S.st(),
+               S.gpe_part.as<double>(), S.precision, s);
+    ngw = gpe_warps(S.m_local, S.precision);
+  }
+  const double pairs = S.direct ? (double)S.n * (double)S.m_local : -1.0;
+  launch_reduce(S.partials.as<double>(), nw, S.gpe_part.as<double>(), ngw, pairs,
+                S.sums.as<double>(), s);
+  S.last_pass_gpe = with_gpe;
+  S.passes++;
+  FGA_CUDA_TRY(cudaGetLastError());
+  return FGA_OK;
+}
+
+int session_update(fga_ctx* c) {
+  Session& S = c->S;
+  launch_update(S.sums.as<double>(), S.st(), S.sp, S.rec_delta.as<double>(),
+                S.rec_traj.as<double>(), S.rec_gpe.as<double>(), S.rec_inter.as<long long>(),
+                S.rec_visits.as<long long>(), S.last_pass_gpe ? 1 : 0, c->stream);
+  FGA_CUDA_TRY(cudaGetLastError());
+  return FGA_OK;
+}
+
+int session_poll(fga_ctx* c, int* done, int64_t* iters) {
+  Session& S = c->S;
+  const char* st = reinterpret_cast<const char*>(S.st());
+  FGA_CUDA_TRY(cudaMemcpyAsync(c->pinned, st + offsetof(IterState, iter), sizeof(long long) + 2 * sizeof(int),
+                               cudaMemcpyDeviceToHost, c->stream));
+  FGA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  long long it;
+  std::memcpy(&it, c->pinned, sizeof(long long));
+  int dn;
+  std::memcpy(&dn, reinterpret_cast<char*>(c->pinned) + sizeof(long long), sizeof(int));
+  if (done) *done = dn;
+  if (iters) *iters = it;
+  return FGA_OK;
+}
+
+int session_apply(fga_ctx* c) {
+  Session& S = c->S;
+  if (!S.applied) {
+    launch_apply_pending(S.view(), S.st(), c->stream);
+    S.applied = true;
+  }
+  FGA_CUDA_TRY(cudaGetLastError());
+  return FGA_OK;
+}
+
+int take_gpe(fga_ctx* c, double* value) {
+  Session& S = c->S;
+  double v = 0.0;
+  FGA_CUDA_TRY(cudaMemcpyAsync(&v, S.sums.as<double>() + kGpe, sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream));
+  FGA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  *value = -S.P.G * v;  // _kernels.py:67
+  return FGA_OK;
+}
+
+// denormalize_translation (normalize.py:73-84)
+void denormalize(const double R[9], const double t[3], const double* ctx, double tout[3]) {
+  const double l = ctx[6], r = ctx[7], a = ctx[8], b = ctx[9];
+  const double inv_scale = (r - l) / (b - a);
+  for (int i = 0; i < 3; i++) {
+    double v1 = 0.0, v2 = 0.0;
+    for (int k = 0; k < 3; k++) {
+      v1 += -R[3 * i + k] * (ctx[3 + k] + l);
+      v2 += R[3 * i + k] * a;
+    }
+    tout[i] = ((v1 + inv_scale * ((v2 + t[i]) - a)) + ctx[i]) + l;
+  }
+}
+
+}  // namespace
+
+// ======================================================================== C ABI
+extern "C" {
+
+int fga_version(void) { return 100; }
+const char* fga_last_error(void) { return fga::last_error(); }
+
+int fga_device_count(int* count) {
+  if (!count) return FGA_ERR_INVALID;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    set_error(std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    return FGA_ERR_CUDA;
+  }
+  *count = n;
+  return FGA_OK;
+}
+
+int fga_create(fga_ctx** out, int device) {
+  if (!out) return FGA_ERR_INVALID;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n <= 0) {
+    set_error("no CUDA device visible: libfga has no CPU fallback");
+    return FGA_ERR_CUDA;
+  }
+  if (device < 0 || device >= n) {
+    set_error("device index out of range");
+    return FGA_ERR_INVALID;
+  }
+  FGA_CUDA_TRY(cudaSetDevice(device));
+  fga_ctx* c = new fga_ctx();
+  c->device = device;
+  FGA_CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->own_stream = true;
+  FGA_CUDA_TRY(cudaMallocHost(&c->pinned, 64));
+  for (auto& e : c->ev) FGA_CUDA_TRY(cudaEventCreate(&e));
+  *out = c;
+  return FGA_OK;
+}
+
+int fga_destroy(fga_ctx* c) {
+  if (!c) return FGA_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->tree.release();
+  c->tree_pts.release();
+  c->tree_masses.release();
+  for (auto& b : c->op) b.release();
+  Session& S = c->S;
+  DevBuf* all[] = {&S.x_raw,   &S.y_raw,  &S.xn,        &S.yn,       &S.ctx_dev,   &S.mx,
+                   &S.my,      &S.flat,   &S.counts,    &S.cells,    &S.ref32,     &S.ref64,
+                   &S.tkeys_in, &S.tkeys, &S.tidx_in,   &S.tidx,     &S.cub_tmp,   &S.tpl,
+                   &S.partials, &S.gpe_part, &S.sums,   &S.state,    &S.scratch,   &S.rec_delta,
+                   &S.rec_traj, &S.rec_gpe, &S.rec_inter, &S.rec_visits};
+  for (DevBuf* b : all) b->release();
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return FGA_OK;
+}
+
+int fga_set_stream(fga_ctx* c, void* stream) {
+  CTX_TRY(c);
+  if (c->own_stream && c->stream) {
+    cudaStreamSynchronize(c->stream);
+    cudaStreamDestroy(c->stream);
+  }
+  if (stream) {
+    c->stream = (cudaStream_t)stream;
+    c->own_stream = false;
+  } else {
+    FGA_CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  return FGA_OK;
+}
+
+int fga_synchronize(fga_ctx* c) {
+  CTX_TRY(c);
+  FGA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FGA_OK;
+}
+
+// ------------------------------------------------------------------ session
+int fga_session_begin_dev(fga_ctx* c, const double* x_dev, int64_t n, const double* y_dev,
+                          int64_t m, int dim, const fga_params* params,
+                          const fga_options* options, int shard_rank, int shard_count) {
+  CTX_TRY(c);
+  TRY(session_begin_common(c, n, m, dim, params, options, shard_rank, shard_count));
+  TRY(session_setup(c, x_dev, y_dev));
+  c->S.active = true;
+  return FGA_OK;
+}
+
+int fga_session_begin(fga_ctx* c, const double* x, int64_t n, const double* y, int64_t m, int dim,
+                      const fga_params* params, const fga_options* options, int shard_rank,
+                      int shard_count) {
+  CTX_TRY(c);
+  TRY(session_begin_common(c, n, m, dim, params, options, shard_rank, shard_count));
+  Session& S = c->S;
+  TRY(h2d(S.x_raw, x, 3 * n, c->stream));
+  TRY(h2d(S.y_raw, y, 3 * m, c->stream));
+  TRY(session_setup(c, S.x_raw.as<double>(), S.y_raw.as<double>()));
+  S.active = true;
+  return FGA_OK;
+}
+
+#define SESSION_TRY(c)                                   \
+  do {                                                   \
+    CTX_TRY(c);                                          \
+    if (!c->S.active) {                                  \
+      set_error("no active registration session");      \
+      return FGA_ERR_STATE;                              \
+    }                                                    \
+  } while (0)
+
+int fga_session_forces(fga_ctx* c) {
+  SESSION_TRY(c);
+  return session_forces(c);
+}
+int fga_session_sums(fga_ctx* c, void** dev_ptr) {
+  SESSION_TRY(c);
+  if (!dev_ptr) return FGA_ERR_INVALID;
+  *dev_ptr = c->S.sums.p;
+  return FGA_OK;
+}
+int fga_session_update(fga_ctx* c) {
+  SESSION_TRY(c);
+  return session_update(c);
+}
+int fga_session_iterate(fga_ctx* c, int k) {
+  SESSION_TRY(c);
+  if (c->S.shard_count != 1) {
+    set_error("fga_session_iterate: sharded sessions need the host collective between passes");
+    return FGA_ERR_STATE;
+  }
+  for (int i = 0; i < k; i++) {
+    TRY(session_forces(c));
+    TRY(session_update(c));
+  }
+  return FGA_OK;
+}
+int fga_session_gpe(fga_ctx* c) {
+  SESSION_TRY(c);
+  return session_gpe(c, nullptr);
+}
+int fga_session_take_gpe(fga_ctx* c, double* value) {
+  SESSION_TRY(c);
+  if (!value) return FGA_ERR_INVALID;
+  return take_gpe(c, value);
+}
+int fga_session_set_gpe(fga_ctx* c, int which, double value) {
+  SESSION_TRY(c);
+  if (which == 0) {
+    c->S.gpe_initial = value;
+    c->S.have_gpe_initial = true;
+  } else {
+    c->S.gpe_final = value;
+    c->S.have_gpe_final = true;
+  }
+  return FGA_OK;
+}
+int fga_session_poll(fga_ctx* c, int* done, int64_t* iterations) {
+  SESSION_TRY(c);
+  return session_poll(c, done, iterations);
+}
+int fga_session_apply_pending(fga_ctx* c) {
+  SESSION_TRY(c);
+  return session_apply(c);
+}
+int fga_session_info(fga_ctx* c, int64_t* m_local, int64_t* n_nodes) {
+  SESSION_TRY(c);
+  if (m_local) *m_local = c->S.m_local;
+  if (n_nodes) *n_nodes = c->S.direct ? 0 : c->tree.n_nodes;
+  return FGA_OK;
+}
+
+int fga_session_finish(fga_ctx* c, fga_result* out, double* deltas, double* traj,
+                       double* gpe_trace, int64_t* inter) {
+  SESSION_TRY(c);
+  Session& S = c->S;
+  cudaStream_t s = c->stream;
+  TRY(session_apply(c));
+  if (S.O.compute_gpe && !S.have_gpe_final && S.shard_count == 1) {
+    FGA_CUDA_TRY(cudaEventRecord(c->ev[4], s));
+    TRY(session_gpe(c, nullptr));
+    double v;
+    TRY(take_gpe(c, &v));
+    FGA_CUDA_TRY(cudaEventRecord(c->ev[5], s));
+    S.gpe_final = v;
+    S.have_gpe_final = true;
+  }
+  IterState st;
+  FGA_CUDA_TRY(cudaMemcpyAsync(&st, S.st(), sizeof(IterState), cudaMemcpyDeviceToHost, s));
+  const int64_t it = 0;
+  (void)it;
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  const int64_t iters = st.iter;
+  std::vector<long long> iv(std::max<int64_t>(iters, 1)), vv(std::max<int64_t>(iters, 1));
+  if (iters > 0) {
+    if (deltas) FGA_CUDA_TRY(cudaMemcpyAsync(deltas, S.rec_delta.p, sizeof(double) * iters, cudaMemcpyDeviceToHost, s));
+    if (traj) FGA_CUDA_TRY(cudaMemcpyAsync(traj, S.rec_traj.p, sizeof(double) * 12 * iters, cudaMemcpyDeviceToHost, s));
+    if (gpe_trace) FGA_CUDA_TRY(cudaMemcpyAsync(gpe_trace, S.rec_gpe.p, sizeof(double) * iters, cudaMemcpyDeviceToHost, s));
+    FGA_CUDA_TRY(cudaMemcpyAsync(iv.data(), S.rec_inter.p, sizeof(long long) * iters, cudaMemcpyDeviceToHost, s));
+    FGA_CUDA_TRY(cudaMemcpyAsync(vv.data(), S.rec_visits.p, sizeof(long long) * iters, cudaMemcpyDeviceToHost, s));
+  }
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  // the last trace entry is the energy of the final positions (registration.py:146-148)
+  if (gpe_trace && S.O.trace_gpe && iters > 0) gpe_trace[iters - 1] = S.gpe_final;
+  if (inter)
+    for (int64_t k = 0; k < iters; k++) inter[k] = iv[k];
+  if (out) {
+    std::memset(out, 0, sizeof(*out));
+    std::memcpy(out->R, st.Racc, sizeof(st.Racc));
+    std::memcpy(out->R_norm, st.Racc, sizeof(st.Racc));
+    std::memcpy(out->t_norm, st.tacc, sizeof(st.tacc));
+    denormalize(st.Racc, st.tacc, S.ctx10, out->t);
+    out->iterations = iters;
+    out->converged = st.converged;
+    out->gpe_initial = S.gpe_initial;
+    out->gpe_final = S.gpe_final;
+    std::memcpy(out->norm_ctx, S.ctx10, sizeof(S.ctx10));
+    for (int64_t k = 0; k < iters; k++) {
+      out->interactions += iv[k];
+      out->visits += vv[k];
+    }
+    out->n_nodes = S.direct ? 0 : c->tree.n_nodes;
+    cudaEventElapsedTime(&S.setup_ms, c->ev[0], c->ev[1]);
+    out->setup_ms = S.setup_ms;
+    out->loop_ms = S.loop_ms;
+    out->gpe_ms = S.gpe_ms;
+  }
+  S.active = false;
+  return FGA_OK;
+}
+
+// ------------------------------------------------------------------ driver
+int fga_register(fga_ctx* c, const double* x, int64_t n, const double* y, int64_t m, int dim,
+                 const fga_params* params, const fga_options* options, fga_result* out,
+                 double* deltas, double* traj, double* gpe_trace, int64_t* inter) {
+  CTX_TRY(c);
+  TRY(fga_session_begin(c, x, n, y, m, dim, params, options, 0, 1));
+  Session& S = c->S;
+  cudaStream_t s = c->stream;
+  float gpe_ms = 0.f;
+  if (S.O.compute_gpe) {
+    FGA_CUDA_TRY(cudaEventRecord(c->ev[4], s));
+    TRY(session_gpe(c, nullptr));
+    FGA_CUDA_TRY(cudaEventRecord(c->ev[5], s));
+    TRY(take_gpe(c, &S.gpe_initial));
+    S.have_gpe_initial = true;
+    cudaEventElapsedTime(&gpe_ms, c->ev[4], c->ev[5]);
+  }
+  FGA_CUDA_TRY(cudaEventRecord(c->ev[2], s));
+  int done = 0;
+  int64_t iters = 0;
+  while (!done) {
+    const int64_t left = S.P.max_iters - S.passes;
+    const int k = (int)std::min<int64_t>(S.O.poll_every, std::max<int64_t>(left, 1));
+    TRY(fga_session_iterate(c, k));
+    TRY(session_poll(c, &done, &iters));
+    if (S.passes >= S.P.max_iters) done = 1;
+  }
+  FGA_CUDA_TRY(cudaEventRecord(c->ev[3], s));
+  FGA_CUDA_TRY(cudaEventSynchronize(c->ev[3]));
+  cudaEventElapsedTime(&S.loop_ms, c->ev[2], c->ev[3]);
+  TRY(session_apply(c));
+  if (S.O.compute_gpe) {
+    FGA_CUDA_TRY(cudaEventRecord(c->ev[4], s));
+    TRY(session_gpe(c, nullptr));
+    FGA_CUDA_TRY(cudaEventRecord(c->ev[5], s));
+    TRY(take_gpe(c, &S.gpe_final));
+    S.have_gpe_final = true;
+    float ms2 = 0.f;
+    cudaEventElapsedTime(&ms2, c->ev[4], c->ev[5]);
+    gpe_ms += ms2;
+  }
+  S.gpe_ms = gpe_ms;
+  return fga_session_finish(c, out, deltas, traj, gpe_trace, inter);
+}
+
+// ------------------------------------------------------------------ tree ops
+int fga_tree_build(fga_ctx* c, const double* pts, const double* masses, int64_t n, int dim,
+                   int max_depth, int64_t* n_nodes) {
+  CTX_TRY(c);
+  if (n <= 0) {
+    set_error("registration requires a non-empty cloud");
+    return FGA_ERR_EMPTY;
+  }
+  if (dim != 3) {
+    set_error("the B200 path implements D=3 (D=2 is not built yet)");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  TRY(h2d(c->tree_pts, pts, 3 * n, c->stream));
+  TRY(h2d(c->tree_masses, masses, n, c->stream));
+  TRY(tree_build_dev(c->tree, c->tree_pts.as<double>(), c->tree_masses.as<double>(), n, max_depth,
+                     c->stream));
+  FGA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (n_nodes) *n_nodes = c->tree.n_nodes;
+  return FGA_OK;
+}
+
+int fga_tree_export(fga_ctx* c, int64_t* children, double* com, double* mass, double* length,
+                    int64_t* occupancy, int64_t* depth, double* bbox_min, double* bbox_max) {
+  CTX_TRY(c);
+  return tree_export_host(c->tree, c->stream, children, com, mass, length, occupancy, depth,
+                          bbox_min, bbox_max);
+}
+
+int fga_tree_upload(fga_ctx* c, const int64_t* children, const double* com, const double* mass,
+                    const double* length, int64_t n_nodes, int n_child, int dim) {
+  CTX_TRY(c);
+  if (dim != 3) {
+    set_error("the B200 path implements D=3 (D=2 is not built yet)");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  return tree_upload_host(c->tree, children, com, mass, length, n_nodes, n_child, c->stream);
+}
+
+int fga_tree_forces(fga_ctx* c, const double* queries, const double* qm, int64_t m, double theta,
+                    double G, double eps2, int precision, double* forces, int64_t* visits,
+                    int64_t* accepted) {
+  CTX_TRY(c);
+  if (c->tree.n_nodes <= 0) {
+    set_error("no tree in this context (fga_tree_build / fga_tree_upload first)");
+    return FGA_ERR_STATE;
+  }
+  if (m <= 0) return FGA_OK;
+  cudaStream_t s = c->stream;
+  DevBuf &q = c->op[0], &qmd = c->op[1], &soa = c->op[2], &out = c->op[3];
+  DevBuf &kin = c->op[4], &kout = c->op[5], &iin = c->op[6], &iout = c->op[7];
+  TRY(h2d(q, queries, 3 * m, s));
+  TRY(h2d(qmd, qm, m, s));
+  DevBuf& tmp = c->S.cub_tmp;
+  DevBuf& scratch = c->S.scratch;
+  TRY(morton_order(q.as<double>(), m, kin, kout, iin, iout, tmp, scratch, s));
+  FGA_CUDA_TRY(soa.reserve(sizeof(double) * 4 * m));
+  double* b = soa.as<double>();
+  launch_gather_queries(q.as<double>(), qmd.as<double>(), iout.as<int>(), m, b, b + m, b + 2 * m,
+                        b + 3 * m, s);
+  FGA_CUDA_TRY(out.reserve(sizeof(double) * 5 * m));
+  double* f = out.as<double>();
+  long long* vis = reinterpret_cast<long long*>(f + 3 * m);
+  long long* acc = vis + m;
+  launch_bh_operator(c->tree, b, b + m, b + 2 * m, b + 3 * m, iout.as<int>(), m, theta, G, eps2, f,
+                     vis, acc, precision, s);
+  FGA_CUDA_TRY(cudaGetLastError());
+  FGA_CUDA_TRY(cudaMemcpyAsync(forces, f, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s));
+  if (visits) FGA_CUDA_TRY(cudaMemcpyAsync(visits, vis, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
+  if (accepted) FGA_CUDA_TRY(cudaMemcpyAsync(accepted, acc, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  return FGA_OK;
+}
+
+int fga_bh_forces_kernel(fga_ctx* c, const int64_t* children, const double* com,
+                         const double* mass, const double* length, int64_t n_nodes, int n_child,
+                         const double* queries, const double* qm, int64_t m, int dim,
+                         double theta, double G, double eps2, int64_t stack_cap, double* forces,
+                         int64_t* visits) {
+  (void)stack_cap;  // the stackless traversal needs no stack
+  TRY(fga_tree_upload(c, children, com, mass, length, n_nodes, n_child, dim));
+  return fga_tree_forces(c, queries, qm, m, theta, G, eps2, FGA_PREC_FP64, forces, visits, nullptr);
+}
+
+int fga_direct_forces(fga_ctx* c, const double* ref, const double* rm, int64_t n,
+                      const double* queries, const double* qm, int64_t m, int dim, double G,
+                      double eps, int precision, double* forces) {
+  CTX_TRY(c);
+  if (dim != 3) {
+    set_error("the B200 path implements D=3 (D=2 is not built yet)");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  if (n <= 0) {
+    set_error("registration requires a non-empty cloud");
+    return FGA_ERR_EMPTY;
+  }
+  if (m <= 0) return FGA_OK;
+  cudaStream_t s = c->stream;
+  DevBuf &r = c->op[0], &rmd = c->op[1], &pk = c->op[2], &q = c->op[3], &qmd = c->op[4],
+         &soa = c->op[5], &out = c->op[6];
+  TRY(h2d(r, ref, 3 * n, s));
+  TRY(h2d(rmd, rm, n, s));
+  FGA_CUDA_TRY(pk.reserve(precision ? sizeof(double4) * n : sizeof(float4) * n));
+  launch_pack_ref(r.as<double>(), rmd.as<double>(), n, precision ? nullptr : pk.as<float4>(),
+                  precision ? pk.as<double4>() : nullptr, s);
+  TRY(h2d(q, queries, 3 * m, s));
+  TRY(h2d(qmd, qm, m, s));
+  FGA_CUDA_TRY(soa.reserve(sizeof(double) * 4 * m));
+  double* b = soa.as<double>();
+  launch_gather_queries(q.as<double>(), qmd.as<double>(), nullptr, m, b, b + m, b + 2 * m, b + 3 * m, s);
+  FGA_CUDA_TRY(out.reserve(sizeof(double) * 3 * m));
+  RefPoints rp{precision ? nullptr : pk.as<float4>(), precision ? pk.as<double4>() : nullptr, n};
+  launch_direct_operator(rp, b, b + m, b + 2 * m, b + 3 * m, m, G, eps, out.as<double>(), precision, s);
+  FGA_CUDA_TRY(cudaGetLastError());
+  FGA_CUDA_TRY(cudaMemcpyAsync(forces, out.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  return FGA_OK;
+}
+
+int fga_gpe_kernel(fga_ctx* c, const double* pos_y, const double* mass_y, int64_t m,
+                   const double* pos_x, const double* mass_x, int64_t n, int dim, double G,
+                   double eps, int precision, double* value) {
+  CTX_TRY(c);
+  if (dim != 3) {
+    set_error("the B200 path implements D=3 (D=2 is not built yet)");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  if (!value) return FGA_ERR_INVALID;
+  cudaStream_t s = c->stream;
+  if (m <= 0 || n <= 0) {
+    *value = -G * 0.0;
+    return FGA_OK;
+  }
+  DevBuf &r = c->op[0], &rmd = c->op[1], &pk = c->op[2], &q = c->op[3], &qmd = c->op[4],
+         &soa = c->op[5], &part = c->op[6], &sums = c->op[7];
+  TRY(h2d(r, pos_x, 3 * n, s));
+  TRY(h2d(rmd, mass_x, n, s));
+  FGA_CUDA_TRY(pk.reserve(precision ? sizeof(double4) * n : sizeof(float4) * n));
+  launch_pack_ref(r.as<double>(), rmd.as<double>(), n, precision ? nullptr : pk.as<float4>(),
+                  precision ? pk.as<double4>() : nullptr, s);
+  TRY(h2d(q, pos_y, 3 * m, s));
+  TRY(h2d(qmd, mass_y, m, s));
+  FGA_CUDA_TRY(soa.reserve(sizeof(double) * 4 * m));
+  double* b = soa.as<double>();
+  launch_gather_queries(q.as<double>(), qmd.as<double>(), nullptr, m, b, b + m, b + 2 * m, b + 3 * m, s);
+  const int64_t ngw = gpe_warps(m, precision);
+  FGA_CUDA_TRY(part.reserve(sizeof(double) * ngw));
+  FGA_CUDA_TRY(sums.reserve(sizeof(double) * kPartialStride));
+  RefPoints rp{precision ? nullptr : pk.as<float4>(), precision ? pk.as<double4>() : nullptr, n};
+  launch_gpe(rp, b, b + m, b + 2 * m, b + 3 * m, m, eps, nullptr, part.as<double>(), precision, s);
+  launch_reduce(nullptr, 0, part.as<double>(), ngw, -1.0, sums.as<double>(), s);
+  FGA_CUDA_TRY(cudaGetLastError());
+  double v = 0.0;
+  FGA_CUDA_TRY(cudaMemcpyAsync(&v, sums.as<double>() + kGpe, sizeof(double), cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  *value = -G * v;
+  return FGA_OK;
+}
+
+int fga_niv_masses(fga_ctx* c, const double* pts, int64_t n, int dim, int rho, double a, double b,
+                   int max_depth, double* out) {
+  CTX_TRY(c);
+  if (dim != 3) {
+    set_error("the B200 path implements D=3 (D=2 is not built yet)");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  if (rho < 2) return invalid("rho", rho);
+  if (n <= 0) return FGA_OK;
+  cudaStream_t s = c->stream;
+  DevBuf &p = c->op[0], &o = c->op[1], &flat = c->op[2], &cnt = c->op[3], &cells = c->op[4];
+  TRY(h2d(p, pts, 3 * n, s));
+  const int64_t ncell = (int64_t)rho * rho * rho;
+  FGA_CUDA_TRY(o.reserve(sizeof(double) * n));
+  FGA_CUDA_TRY(flat.reserve(sizeof(int) * n));
+  FGA_CUDA_TRY(cnt.reserve(sizeof(long long) * (ncell + 1)));
+  FGA_CUDA_TRY(cells.reserve(sizeof(double) * ncell));
+  TRY(niv_masses_dev(p.as<double>(), n, rho, a, b, max_depth, o.as<double>(), flat.as<int>(),
+                     cnt.as<long long>(), cells.as<double>(), s));
+  FGA_CUDA_TRY(cudaMemcpyAsync(out, o.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  return FGA_OK;
+}
+
+int fga_normalize_pair(fga_ctx* c, const double* x, int64_t n, const double* y, int64_t m, int dim,
+                       double a, double b, double* xn, double* yn, double* ctx10) {
+  CTX_TRY(c);
+  if (dim != 3) {
+    set_error("the B200 path implements D=3 (D=2 is not built yet)");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  if (n <= 0 || m <= 0) {
+    set_error("registration requires a non-empty cloud");
+    return FGA_ERR_EMPTY;
+  }
+  cudaStream_t s = c->stream;
+  DevBuf &dx = c->op[0], &dy = c->op[1], &ox = c->op[2], &oy = c->op[3], &cd = c->op[4],
+         &sc = c->op[5];
+  TRY(h2d(dx, x, 3 * n, s));
+  TRY(h2d(dy, y, 3 * m, s));
+  FGA_CUDA_TRY(ox.reserve(sizeof(double) * 3 * n));
+  FGA_CUDA_TRY(oy.reserve(sizeof(double) * 3 * m));
+  FGA_CUDA_TRY(cd.reserve(sizeof(double) * 16));
+  FGA_CUDA_TRY(sc.reserve(sizeof(double) * 8192));
+  double host_ctx[10];
+  TRY(normalize_pair_dev(dx.as<double>(), n, dy.as<double>(), m, a, b, ox.as<double>(),
+                         oy.as<double>(), cd.as<double>(), sc.as<double>(), sc.bytes, host_ctx, s));
+  FGA_CUDA_TRY(cudaMemcpyAsync(xn, ox.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaMemcpyAsync(yn, oy.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  if (ctx10) std::memcpy(ctx10, host_ctx, sizeof(host_ctx));
+  return FGA_OK;
+}
+
+int fga_solve_rigid(fga_ctx* c, const double* y, const double* yd, int64_t m, int dim, double* R,
+                    double* t, int32_t* degenerate) {
+  CTX_TRY(c);
+  if (dim != 3) {
+    set_error("the B200 path implements D=3 (D=2 is not built yet)");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  if (m <= 0) {
+    set_error("registration requires a non-empty cloud");
+    return FGA_ERR_EMPTY;
+  }
+  cudaStream_t s = c->stream;
+  DevBuf &dy = c->op[0], &dd = c->op[1], &o = c->op[2];
+  TRY(h2d(dy, y, 3 * m, s));
+  TRY(h2d(dd, yd, 3 * m, s));
+  FGA_CUDA_TRY(o.reserve(sizeof(double) * 16));
+  launch_solve_rigid(dy.as<double>(), dd.as<double>(), m, nullptr, o.as<double>(), s);
+  FGA_CUDA_TRY(cudaGetLastError());
+  double h[13];
+  FGA_CUDA_TRY(cudaMemcpyAsync(h, o.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  if (R) std::memcpy(R, h, sizeof(double) * 9);
+  if (t) std::memcpy(t, h + 9, sizeof(double) * 3);
+  if (degenerate) *degenerate = (int32_t)h[12];
+  return FGA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// fga_session.cuh -- launch interfaces between capi.cu and the kernel files.
+#pragma once
+#include "fga_internal.cuh"
+#include "fga_tree.cuh"
+
+namespace fga {
+
+// Template swarm state for one shard, SoA fp64 in Morton order.
+struct TemplateView {
+  double *px, *py, *pz;  // positions (pending transform not yet applied)
+  double *vx, *vy, *vz;  // velocities v' of the last step (pre-rotation)
+  const double* mq;      // masses
+  int64_t m;
+};
+
+// Reference points for the direct sum / energy: {x, y, z, m}.
+struct RefPoints {
+  const float4* p32;
+  const double4* p64;
+  int64_t n;
+};
+
+constexpr int kForceThreads = 256;
+constexpr int kDirectQPT = 2;  // queries per thread in the FP32 direct sum
+
+int64_t bh_iterate_warps(int64_t m);
+int64_t direct_iterate_warps(int64_t m, int precision);
+int64_t gpe_warps(int64_t m, int precision);
+
+// One force pass of the iteration: applies the pending transform, evaluates
+// forces, fused Euler-Cromer step, per-warp Kabsch partials.
+void launch_bh_iterate(const TreeDev& T, const TemplateView& tv, const IterState* st,
+                       const SimParams& sp, double* partials, int precision, cudaStream_t s);
+void launch_direct_iterate(const RefPoints& ref, const TemplateView& tv, const IterState* st,
+                           const SimParams& sp, double* partials, int precision, cudaStream_t s);
+// Energy of the current (already transformed) positions: per-warp partials of
+// sum_i m_i * sum_j m_j / (|y_i - x_j| + eps).  Skipped when st->done.
+void launch_gpe(const RefPoints& ref, const double* px, const double* py, const double* pz,
+                const double* mq, int64_t m, double eps, const IterState* st, double* partials,
+                int precision, cudaStream_t s);
+
+// Operator-level (no state): queries SoA fp64 (already in traversal order),
+// outputs scattered back through `order` (may be null = identity).
+void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, const double* qz,
+                        const double* qm, const int* order, int64_t m, double theta, double G,
+                        double eps2, double* fout, long long* visits, long long* accepted,
+                        int precision, cudaStream_t s);
+void launch_direct_operator(const RefPoints& ref, const double* qx, const double* qy,
+                            const double* qz, const double* qm, int64_t m, double G, double eps,
+                            double* fout, int precision, cudaStream_t s);
+
+// Rigid side (rigid.cu)
+void launch_reduce(const double* partials, int64_t nwarps, const double* gpe_partials,
+                   int64_t ngwarps, double direct_pairs, double* sums, cudaStream_t s);
+void launch_update(const double* sums, IterState* st, const SimParams& sp, double* rec_delta,
+                   double* rec_traj, double* rec_gpe, long long* rec_inter, long long* rec_visits,
+                   int has_gpe, cudaStream_t s);
+void launch_apply_pending(const TemplateView& tv, const IterState* st, cudaStream_t s);
+void launch_state_init(IterState* st, const double* mean3, cudaStream_t s);
+void launch_solve_rigid(const double* y, const double* yd, int64_t m, double* scratch,
+                        double* out13, cudaStream_t s);
+
+// Setup (setup.cu)
+int normalize_pair_dev(const double* x, int64_t n, const double* y, int64_t m, double a, double b,
+                       double* xn, double* yn, double* ctx10_dev, double* scratch,
+                       size_t scratch_bytes, double* ctx10_host, cudaStream_t s);
+int niv_masses_dev(const double* pts, int64_t n, int rho, double a, double b, int max_depth,
+                   double* out, int* flat_scratch, long long* counts_scratch, double* cells_scratch,
+                   cudaStream_t s);
+void launch_external_masses(const double* w, int64_t n, double* out, cudaStream_t s);
+void launch_rescale(double* sx, int64_t n, double* sy, int64_t m, double dt, double eta,
+                    double* scratch, cudaStream_t s);
+void launch_pack_ref(const double* xn, const double* mx, int64_t n, float4* p32, double4* p64,
+                     cudaStream_t s);
+size_t scratch_doubles_for(int64_t n);
+void launch_mean3(const double* pts_aos, int64_t n, double* scratch, double* out3, cudaStream_t s);
+void launch_bbox(const double* pts_aos, int64_t n, double* scratch, double* out6, cudaStream_t s);
+void launch_morton_keys(const double* pts_aos, int64_t n, const double* box6,
+                        unsigned long long* keys, int* idx, cudaStream_t s);
+void launch_gather_template(const double* pts_aos, const double* mass, const int* order,
+                            int64_t begin, int64_t count, TemplateView tv, cudaStream_t s);
+void launch_gather_queries(const double* q_aos, const double* qm, const int* order, int64_t m,
+                           double* qx, double* qy, double* qz, double* qms, cudaStream_t s);
+
+}  // namespace fga

@@ -1,0 +1,76 @@
+// fga_tree.cuh -- device tree containers shared by tree.cu / forces.cu / capi.cu
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "fga_internal.cuh"
+
+namespace fga {
+
+// Ascending-preorder node arrays (the reference's numbering, bhtree.py:77).
+struct TreeNodesView {
+  signed char* level;
+  int* start;
+  int* occ;
+  int* skip;
+  int* parent;
+  unsigned* childmask;
+  int* arrive;
+  int* children;  // (n_nodes, 8), -1 absent
+  double* mass;
+  double* mc;     // sum m*p (n_nodes, 3)
+  double* com;    // (n_nodes, 3)
+  double* length;
+};
+
+// Mirrored-preorder traversal records.
+struct TreeRecords {
+  float4* a32;
+  NodeB32* b32;
+  double4* a64;
+  NodeB64* b64;
+};
+
+struct TreeDev {
+  int64_t n_points = 0, n_nodes = 0;
+  int L = 0;
+  double cmag = 0.0;  // max |coordinate| over node centres (fp32 MAC guard)
+  double box_host[6] = {0, 0, 0, 0, 0, 0};
+  bool exportable = false;
+  const double* pts = nullptr;     // (n,3) device, not owned
+  const double* masses = nullptr;  // (n,) device, not owned
+  DevBuf box, scratch, keys_in, keys, idx_in, idx, clev, count, offset, cub_tmp;
+  DevBuf level, start, occ, skip, parent, childmask, arrive, children, mass, mc, com, length;
+  DevBuf a32, b32, a64, b64;
+  DevBuf export_buf;
+
+  TreeNodesView view() const {
+    return TreeNodesView{level.as<signed char>(), start.as<int>(),    occ.as<int>(),
+                         skip.as<int>(),          parent.as<int>(),   childmask.as<unsigned>(),
+                         arrive.as<int>(),        children.as<int>(), mass.as<double>(),
+                         mc.as<double>(),         com.as<double>(),   length.as<double>()};
+  }
+  TreeRecords records() const {
+    return TreeRecords{a32.as<float4>(), b32.as<NodeB32>(), a64.as<double4>(), b64.as<NodeB64>()};
+  }
+  void release() {
+    DevBuf* all[] = {&box,  &scratch, &keys_in,   &keys,   &idx_in,   &idx,      &clev,
+                     &count, &offset, &cub_tmp,   &level,  &start,    &occ,      &skip,
+                     &parent, &childmask, &arrive, &children, &mass,  &mc,       &com,
+                     &length, &a32,   &b32,       &a64,    &b64,      &export_buf};
+    for (DevBuf* b : all) b->release();
+    n_nodes = 0;
+    exportable = false;
+  }
+};
+
+int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, int64_t n, int L,
+                   cudaStream_t st);
+int tree_export_host(TreeDev& T, cudaStream_t st, int64_t* children, double* com, double* mass,
+                     double* length, int64_t* occupancy, int64_t* depth, double* bmin,
+                     double* bmax);
+int tree_upload_host(TreeDev& T, const int64_t* children, const double* com, const double* mass,
+                     const double* length, int64_t nn, int n_child, cudaStream_t st);
+
+}  // namespace fga

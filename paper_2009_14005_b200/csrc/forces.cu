@@ -1,0 +1,801 @@
+// forces.cu -- the per-iteration force pass (hot path).
+//
+// K6 Barnes-Hut traversal (reference: _kernels.bh_forces_kernel,
+// _kernels.py:7-50).  Stackless and warp-coherent: every lane keeps a cursor
+// into the mirrored-preorder node array; the warp repeatedly takes the
+// smallest cursor n (redux.sync.min), the lanes whose cursor equals n apply
+// their own MAC -- accept: cursor = skip[n]; open: cursor = n + 1 -- so each
+// query visits exactly the reference's node set, in exactly the reference's
+// order (the reference's stack pops slot 7 first, which is mirrored
+// preorder).  Node records are staged per warp through a 32-node shared-memory
+// window that one coalesced load refills whenever the warp's minimum cursor
+// leaves it.
+//   * FP32 path: positions/records in fp32, acceleration accumulated in fp32
+//     registers; the MAC `l^2 < theta^2 d^2` (:37) is evaluated in fp32 and
+//     re-evaluated exactly in fp64 whenever the fp32 margin is within the
+//     rounding bound, so the accepted set is the reference's.
+//   * FP64 path: the reference's per-term arithmetic verbatim (:26-42), no
+//     FMA contraction, same order -> bit-identical forces on the same tree.
+// The iterate kernels fuse: the pending rigid transform of the previous
+// iteration (registration.py:135-136), damping + Euler-Cromer
+// (dynamics.py:37-47) and the Kabsch partial sums (procrustes.py:20-25).
+//
+// K1 direct O(NM) sum (bhtree.brute_force, bhtree.py:155-164): reference
+// points staged through shared memory as float4 {x,y,z,m} tiles of 1024,
+// 2 queries per thread, FP32 FMA/MUFU inner loop, fp64 across tiles.
+//
+// K11 potential energy (_kernels.gpe_kernel, _kernels.py:53-67): same tiling.
+#include <climits>
+
+#include "fga_session.cuh"
+
+namespace fga {
+namespace {
+
+constexpr int kWin = 32;
+constexpr int kWarps = kForceThreads / 32;
+
+struct Win32 {
+  float4 a[kWin];
+  NodeB32 b[kWin];
+};
+struct Win64 {
+  double4 a[kWin];
+  NodeB64 b[kWin];
+};
+
+// exact fp64 MAC of the reference (_kernels.py:26-29, :37)
+__device__ __noinline__ bool mac_exact(const double4* __restrict__ A64,
+                                       const NodeB64* __restrict__ B64, int node, double qx,
+                                       double qy, double qz, double theta2) {
+  const double4 a = A64[node];
+  const double dx = __dsub_rn(qx, a.x), dy = __dsub_rn(qy, a.y), dz = __dsub_rn(qz, a.z);
+  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+  return B64[node].l2 < __dmul_rn(theta2, d2);
+}
+
+struct Trav32Out {
+  float ax, ay, az;
+  int visits, accepted;
+};
+
+// FP32 warp-coherent traversal.  All 32 lanes must call it (inactive lanes
+// pass active=false).  g0/g1: per-lane fp32 MAC uncertainty model (see
+// guard_coeffs).
+__device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
+                                                const NodeB32* __restrict__ B,
+                                                const double4* __restrict__ A64,
+                                                const NodeB64* __restrict__ B64, int n_nodes,
+                                                float qx, float qy, float qz, bool active,
+                                                float theta2, double theta2_64, float eps2,
+                                                float g0, float g1, const double* qpx,
+                                                const double* qpy, const double* qpz, int64_t qi,
+                                                Win32* win, int lane) {
+  Trav32Out o{0.f, 0.f, 0.f, 0, 0};
+  int cursor = active ? 0 : n_nodes;
+  int wbase = INT_MIN / 2;
+  while (true) {
+    const int n = __reduce_min_sync(0xffffffffu, cursor);
+    if (n >= n_nodes) break;
+    if ((unsigned)(n - wbase) >= (unsigned)kWin) {
+      wbase = n;
+      __syncwarp();
+      const int j = n + lane;
+      if (j < n_nodes) {
+        win->a[lane] = __ldg(&A[j]);
+        win->b[lane] = B[j];
+      }
+      __syncwarp();
+    }
+    if (cursor == n) {
+      const float4 a = win->a[n - wbase];
+      const NodeB32 b = win->b[n - wbase];
+      const float dx = a.x - qx, dy = a.y - qy, dz = a.z - qz;
+      const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      const float t2d2 = theta2 * d2;
+      bool acc = b.l2 < t2d2;
+      if (fabsf(t2d2 - b.l2) <= fmaf(theta2, fmaf(d2, g1, g0), 4.0e-7f * fabsf(b.l2)))
+        acc = mac_exact(A64, B64, n, qpx[qi], qpy[qi], qpz[qi], theta2_64);
+      o.visits++;
+      if (acc) {
+        o.accepted++;
+        const float r2 = d2 + eps2;
+        const float inv = rsqrtf(r2);
+        float w = a.w * (inv * inv * inv);
+        if (!(r2 > 0.f)) w = 0.f;  // reference skips d2+eps2 == 0 (:39)
+        o.ax = fmaf(w, dx, o.ax);
+        o.ay = fmaf(w, dy, o.ay);
+        o.az = fmaf(w, dz, o.az);
+        cursor = b.skip;
+      } else {
+        cursor = n + 1;
+      }
+    }
+  }
+  return o;
+}
+
+struct Trav64Out {
+  double fx, fy, fz;
+  int visits, accepted;
+};
+
+// FP64 traversal: the reference's arithmetic and order exactly.  gq = G*m_q.
+__device__ __forceinline__ Trav64Out traverse64(const double4* __restrict__ A,
+                                                const NodeB64* __restrict__ B, int n_nodes,
+                                                double qx, double qy, double qz, double gq,
+                                                bool active, double theta2, double eps2,
+                                                Win64* win, int lane) {
+  Trav64Out o{0.0, 0.0, 0.0, 0, 0};
+  int cursor = active ? 0 : n_nodes;
+  int wbase = INT_MIN / 2;
+  while (true) {
+    const int n = __reduce_min_sync(0xffffffffu, cursor);
+    if (n >= n_nodes) break;
+    if ((unsigned)(n - wbase) >= (unsigned)kWin) {
+      wbase = n;
+      __syncwarp();
+      const int j = n + lane;
+      if (j < n_nodes) {
+        win->a[lane] = A[j];
+        win->b[lane] = B[j];
+      }
+      __syncwarp();
+    }
+    if (cursor == n) {
+      const double4 a = win->a[n - wbase];
+      const NodeB64 b = win->b[n - wbase];
+      const double dx = __dsub_rn(qx, a.x), dy = __dsub_rn(qy, a.y), dz = __dsub_rn(qz, a.z);
+      const double d2 =
+          __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+      o.visits++;
+      if (b.l2 < __dmul_rn(theta2, d2)) {
+        o.accepted++;
+        const double denom = __dadd_rn(d2, eps2);
+        if (denom > 0.0) {
+          const double w = __ddiv_rn(__dmul_rn(gq, a.w), __dmul_rn(denom, __dsqrt_rn(denom)));
+          o.fx = __dsub_rn(o.fx, __dmul_rn(w, dx));
+          o.fy = __dsub_rn(o.fy, __dmul_rn(w, dy));
+          o.fz = __dsub_rn(o.fz, __dmul_rn(w, dz));
+        }
+        cursor = (int)b.skip;
+      } else {
+        cursor = n + 1;
+      }
+    }
+  }
+  return o;
+}
+
+// Bound on |fp32 d^2 - exact d^2| as g0 + g1*d2 (then scaled by theta^2):
+// coordinates carry <= (|q| + |com|) * 2^-24 rounding each; 2|d| <= d2 + 1.
+__device__ __forceinline__ void guard_coeffs(float qmag, float cmag, float& g0, float& g1) {
+  const float delta = (qmag + cmag) * 1.2e-7f;  // ~2^-23, double the unit roundoff
+  g0 = 4.0f * delta + 8.0f * delta * delta + 1e-30f;
+  g1 = 4.0f * delta + 6.0e-7f;
+}
+
+// ---------------------------------------------------------------- iterate epilogue
+struct Partial {
+  double v[17];
+};
+
+__device__ __forceinline__ void partial_zero(Partial& p) {
+#pragma unroll
+  for (int k = 0; k < 17; k++) p.v[k] = 0.0;
+}
+
+// Applies R,t of the previous step to (y, v') in place (registration.py:135-136).
+__device__ __forceinline__ void apply_pending(const IterState* st, double y[3], double v[3]) {
+  double ny[3], nv[3];
+#pragma unroll
+  for (int r = 0; r < 3; r++) {
+    ny[r] = st->Rp[3 * r] * y[0] + st->Rp[3 * r + 1] * y[1] + st->Rp[3 * r + 2] * y[2] + st->tp[r];
+    nv[r] = st->Rp[3 * r] * v[0] + st->Rp[3 * r + 1] * v[1] + st->Rp[3 * r + 2] * v[2];
+  }
+#pragma unroll
+  for (int r = 0; r < 3; r++) {
+    y[r] = ny[r];
+    v[r] = nv[r];
+  }
+}
+
+// total_force + step (dynamics.py:40, :45-46) in the reference's operation
+// order, then this query's contribution to the Kabsch sums.
+__device__ __forceinline__ void step_and_accumulate(const double F[3], const double y[3],
+                                                    const double v[3], double mq,
+                                                    const SimParams& sp, const double s[3],
+                                                    double vp[3], Partial& p) {
+  double w[3], u[3];
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    const double f = __dsub_rn(F[k], __dmul_rn(sp.eta, v[k]));
+    vp[k] = __dadd_rn(v[k], __ddiv_rn(__dmul_rn(sp.dt, f), mq));
+    const double d = __dmul_rn(sp.dt, vp[k]);
+    u[k] = y[k] - s[k];
+    w[k] = (y[k] + d) - s[k];
+  }
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    p.v[kSumU + k] += u[k];
+    p.v[kSumW + k] += w[k];
+  }
+#pragma unroll
+  for (int i = 0; i < 3; i++)
+#pragma unroll
+    for (int j = 0; j < 3; j++) p.v[kSumWU + 3 * i + j] = fma(w[i], u[j], p.v[kSumWU + 3 * i + j]);
+}
+
+__device__ __forceinline__ void warp_store_partial(Partial& p, int lane, double* out) {
+#pragma unroll
+  for (int k = 0; k < 17; k++) p.v[k] = warp_sum(p.v[k]);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 17; k++) out[k] = p.v[k];
+    out[17] = 0.0;
+  }
+}
+
+// ---------------------------------------------------------------- BH iterate
+template <typename Real>
+struct WinOf;
+template <>
+struct WinOf<float> {
+  using T = Win32;
+};
+template <>
+struct WinOf<double> {
+  using T = Win64;
+};
+
+template <typename Real>
+__global__ void __launch_bounds__(kForceThreads) k_bh_iterate(TreeRecords tr, int n_nodes,
+                                                               TemplateView tv,
+                                                               const IterState* __restrict__ st,
+                                                               SimParams sp, double* partials,
+                                                               float cmag) {
+  if (st->done) return;
+  __shared__ typename WinOf<Real>::T wins[kWarps];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + wl;
+  const int64_t i = gw * 32 + lane;
+  const bool active = i < tv.m;
+  double y[3] = {0, 0, 0}, v[3] = {0, 0, 0}, mq = 1.0;
+  if (active) {
+    y[0] = tv.px[i];
+    y[1] = tv.py[i];
+    y[2] = tv.pz[i];
+    v[0] = tv.vx[i];
+    v[1] = tv.vy[i];
+    v[2] = tv.vz[i];
+    mq = tv.mq[i];
+    apply_pending(st, y, v);
+    tv.px[i] = y[0];
+    tv.py[i] = y[1];
+    tv.pz[i] = y[2];
+    tv.vx[i] = v[0];
+    tv.vy[i] = v[1];
+    tv.vz[i] = v[2];
+  }
+  double F[3];
+  int nv, na;
+  if constexpr (sizeof(Real) == 4) {
+    const float qx = (float)y[0], qy = (float)y[1], qz = (float)y[2];
+    float g0, g1;
+    guard_coeffs(fmaxf(fabsf(qx), fmaxf(fabsf(qy), fabsf(qz))), cmag, g0, g1);
+    Trav32Out o = traverse32(tr.a32, tr.b32, tr.a64, tr.b64, n_nodes, qx, qy, qz, active,
+                             (float)sp.theta2, sp.theta2, (float)sp.eps2, g0, g1, tv.px, tv.py,
+                             tv.pz, i, &wins[wl], lane);
+    const double gq = sp.G * mq;
+    F[0] = gq * (double)o.ax;
+    F[1] = gq * (double)o.ay;
+    F[2] = gq * (double)o.az;
+    nv = o.visits;
+    na = o.accepted;
+  } else {
+    Trav64Out o = traverse64(tr.a64, tr.b64, n_nodes, y[0], y[1], y[2], __dmul_rn(sp.G, mq),
+                             active, sp.theta2, sp.eps2, &wins[wl], lane);
+    F[0] = o.fx;
+    F[1] = o.fy;
+    F[2] = o.fz;
+    nv = o.visits;
+    na = o.accepted;
+  }
+  Partial p;
+  partial_zero(p);
+  if (active) {
+    // state re-read here (L2-resident) instead of living in registers
+    // across the traversal loop
+    y[0] = tv.px[i];
+    y[1] = tv.py[i];
+    y[2] = tv.pz[i];
+    v[0] = tv.vx[i];
+    v[1] = tv.vy[i];
+    v[2] = tv.vz[i];
+    mq = tv.mq[i];
+    double vp[3];
+    const double s[3] = {st->shift[0], st->shift[1], st->shift[2]};
+    step_and_accumulate(F, y, v, mq, sp, s, vp, p);
+    tv.vx[i] = vp[0];
+    tv.vy[i] = vp[1];
+    tv.vz[i] = vp[2];
+  }
+  p.v[kAccepted] = (double)__reduce_add_sync(0xffffffffu, (unsigned)na);
+  p.v[kVisits] = (double)__reduce_add_sync(0xffffffffu, (unsigned)nv);
+  // counts are already warp totals: divide the upcoming warp_sum by 32
+  p.v[kAccepted] = lane == 0 ? p.v[kAccepted] : 0.0;
+  p.v[kVisits] = lane == 0 ? p.v[kVisits] : 0.0;
+  warp_store_partial(p, lane, partials + gw * kPartialStride);
+}
+
+// ---------------------------------------------------------------- BH operator
+template <typename Real>
+__global__ void __launch_bounds__(kForceThreads) k_bh_operator(
+    TreeRecords tr, int n_nodes, const double* __restrict__ qx_, const double* __restrict__ qy_,
+    const double* __restrict__ qz_, const double* __restrict__ qm_, const int* __restrict__ order,
+    int64_t m, double theta2, double G, double eps2, double* __restrict__ fout,
+    long long* __restrict__ visits, long long* __restrict__ accepted, float cmag) {
+  __shared__ typename WinOf<Real>::T wins[kWarps];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t i = ((int64_t)blockIdx.x * kWarps + wl) * 32 + lane;
+  const bool active = i < m;
+  double q[3] = {0, 0, 0}, qm = 0.0;
+  if (active) {
+    q[0] = qx_[i];
+    q[1] = qy_[i];
+    q[2] = qz_[i];
+    qm = qm_[i];
+  }
+  double F[3];
+  int nv, na;
+  if constexpr (sizeof(Real) == 4) {
+    const float fx = (float)q[0], fy = (float)q[1], fz = (float)q[2];
+    float g0, g1;
+    guard_coeffs(fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))), cmag, g0, g1);
+    Trav32Out o = traverse32(tr.a32, tr.b32, tr.a64, tr.b64, n_nodes, fx, fy, fz, active,
+                             (float)theta2, theta2, (float)eps2, g0, g1, qx_, qy_, qz_, i,
+                             &wins[wl], lane);
+    const double gq = G * qm;
+    F[0] = gq * (double)o.ax;
+    F[1] = gq * (double)o.ay;
+    F[2] = gq * (double)o.az;
+    nv = o.visits;
+    na = o.accepted;
+  } else {
+    Trav64Out o = traverse64(tr.a64, tr.b64, n_nodes, q[0], q[1], q[2], __dmul_rn(G, qm), active,
+                             theta2, eps2, &wins[wl], lane);
+    F[0] = o.fx;
+    F[1] = o.fy;
+    F[2] = o.fz;
+    nv = o.visits;
+    na = o.accepted;
+  }
+  if (!active) return;
+  const int64_t dst = order ? order[i] : i;
+  fout[dst * 3] = F[0];
+  fout[dst * 3 + 1] = F[1];
+  fout[dst * 3 + 2] = F[2];
+  if (visits) visits[dst] = nv;
+  if (accepted) accepted[dst] = na;
+}
+
+// ---------------------------------------------------------------- direct sum
+constexpr int kTile = 1024;
+
+// FP32 tile loop for QPT queries; returns per-tile sums in fp32 which the
+// caller folds into fp64.  kGuard handles eps == 0 (coincident points).
+template <int QPT, bool kGuard>
+__device__ __forceinline__ void direct_tile32(const float4* __restrict__ sm, int jmax,
+                                              const float (&qx)[QPT], const float (&qy)[QPT],
+                                              const float (&qz)[QPT], float eps2,
+                                              float (&ax)[QPT], float (&ay)[QPT],
+                                              float (&az)[QPT]) {
+#pragma unroll 4
+  for (int j = 0; j < jmax; j++) {
+    const float4 s = sm[j];
+#pragma unroll
+    for (int k = 0; k < QPT; k++) {
+      const float dx = s.x - qx[k], dy = s.y - qy[k], dz = s.z - qz[k];
+      const float r2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, eps2)));
+      const float inv = rsqrtf(r2);
+      float w = s.w * inv * inv * inv;
+      if (kGuard && !(r2 > 0.f)) w = 0.f;
+      ax[k] = fmaf(w, dx, ax[k]);
+      ay[k] = fmaf(w, dy, ay[k]);
+      az[k] = fmaf(w, dz, az[k]);
+    }
+  }
+}
+
+// fp64 brute force term (bhtree.py:158-164): w = m / d2^1.5, sum w*delta.
+__device__ __forceinline__ void direct_tile64(const double4* __restrict__ sm, int jmax, double qx,
+                                              double qy, double qz, double eps2, double& sx,
+                                              double& sy, double& sz) {
+  for (int j = 0; j < jmax; j++) {
+    const double4 s = sm[j];
+    const double dx = __dsub_rn(qx, s.x), dy = __dsub_rn(qy, s.y), dz = __dsub_rn(qz, s.z);
+    const double d2 = __dadd_rn(
+        __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)), eps2);
+    const double w = d2 > 0.0 ? __ddiv_rn(s.w, __dmul_rn(d2, __dsqrt_rn(d2))) : 0.0;
+    sx = __dadd_rn(sx, __dmul_rn(w, dx));
+    sy = __dadd_rn(sy, __dmul_rn(w, dy));
+    sz = __dadd_rn(sz, __dmul_rn(w, dz));
+  }
+}
+
+template <bool kGuard>
+__global__ void __launch_bounds__(kForceThreads) k_direct_iterate32(
+    const float4* __restrict__ src, int64_t n, TemplateView tv, const IterState* __restrict__ st,
+    SimParams sp, double* partials) {
+  if (st->done) return;
+  __shared__ float4 sm[kTile];
+  constexpr int Q = kDirectQPT;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t base = (int64_t)blockIdx.x * (kForceThreads * Q);
+  float qx[Q], qy[Q], qz[Q];
+#pragma unroll
+  for (int k = 0; k < Q; k++) {
+    const int64_t i = base + threadIdx.x + k * kForceThreads;
+    double y[3] = {0.0, 0.0, 0.0}, v[3];
+    if (i < tv.m) {
+      y[0] = tv.px[i];
+      y[1] = tv.py[i];
+      y[2] = tv.pz[i];
+      v[0] = tv.vx[i];
+      v[1] = tv.vy[i];
+      v[2] = tv.vz[i];
+      apply_pending(st, y, v);
+      tv.px[i] = y[0];
+      tv.py[i] = y[1];
+      tv.pz[i] = y[2];
+      tv.vx[i] = v[0];
+      tv.vy[i] = v[1];
+      tv.vz[i] = v[2];
+    }
+    qx[k] = (float)y[0];
+    qy[k] = (float)y[1];
+    qz[k] = (float)y[2];
+  }
+  double A[Q][3];
+#pragma unroll
+  for (int k = 0; k < Q; k++) A[k][0] = A[k][1] = A[k][2] = 0.0;
+  const float eps2 = (float)sp.eps2;
+  for (int64_t t0 = 0; t0 < n; t0 += kTile) {
+    const int jmax = (int)((n - t0) < (int64_t)(kTile) ? (n - t0) : (int64_t)(kTile));
+    __syncthreads();
+    for (int j = threadIdx.x; j < jmax; j += kForceThreads) sm[j] = __ldg(&src[t0 + j]);
+    __syncthreads();
+    float ax[Q], ay[Q], az[Q];
+#pragma unroll
+    for (int k = 0; k < Q; k++) ax[k] = ay[k] = az[k] = 0.f;
+    direct_tile32<Q, kGuard>(sm, jmax, qx, qy, qz, eps2, ax, ay, az);
+#pragma unroll
+    for (int k = 0; k < Q; k++) {
+      A[k][0] += (double)ax[k];
+      A[k][1] += (double)ay[k];
+      A[k][2] += (double)az[k];
+    }
+  }
+  Partial p;
+  partial_zero(p);
+  const double s[3] = {st->shift[0], st->shift[1], st->shift[2]};
+#pragma unroll
+  for (int k = 0; k < Q; k++) {
+    const int64_t i = base + threadIdx.x + k * kForceThreads;
+    if (i >= tv.m) continue;
+    const double y[3] = {tv.px[i], tv.py[i], tv.pz[i]};
+    const double v[3] = {tv.vx[i], tv.vy[i], tv.vz[i]};
+    const double mq = tv.mq[i];
+    const double gq = sp.G * mq;
+    const double F[3] = {gq * A[k][0], gq * A[k][1], gq * A[k][2]};
+    double vp[3];
+    step_and_accumulate(F, y, v, mq, sp, s, vp, p);
+    tv.vx[i] = vp[0];
+    tv.vy[i] = vp[1];
+    tv.vz[i] = vp[2];
+  }
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + wl;
+  warp_store_partial(p, lane, partials + gw * kPartialStride);
+}
+
+__global__ void __launch_bounds__(kForceThreads) k_direct_iterate64(
+    const double4* __restrict__ src, int64_t n, TemplateView tv, const IterState* __restrict__ st,
+    SimParams sp, double* partials) {
+  if (st->done) return;
+  __shared__ double4 sm[kTile / 2];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * kForceThreads + threadIdx.x;
+  const bool active = i < tv.m;
+  double y[3] = {0, 0, 0}, v[3] = {0, 0, 0}, mq = 1.0;
+  if (active) {
+    y[0] = tv.px[i];
+    y[1] = tv.py[i];
+    y[2] = tv.pz[i];
+    v[0] = tv.vx[i];
+    v[1] = tv.vy[i];
+    v[2] = tv.vz[i];
+    mq = tv.mq[i];
+    apply_pending(st, y, v);
+    tv.px[i] = y[0];
+    tv.py[i] = y[1];
+    tv.pz[i] = y[2];
+  }
+  double sx = 0, sy = 0, sz = 0;
+  for (int64_t t0 = 0; t0 < n; t0 += kTile / 2) {
+    const int jmax = (int)((n - t0) < (int64_t)(kTile / 2) ? (n - t0) : (int64_t)(kTile / 2));
+    __syncthreads();
+    for (int j = threadIdx.x; j < jmax; j += kForceThreads) sm[j] = src[t0 + j];
+    __syncthreads();
+    direct_tile64(sm, jmax, y[0], y[1], y[2], sp.eps2, sx, sy, sz);
+  }
+  Partial p;
+  partial_zero(p);
+  if (active) {
+    const double sc = __dmul_rn(-sp.G, mq);
+    const double F[3] = {__dmul_rn(sc, sx), __dmul_rn(sc, sy), __dmul_rn(sc, sz)};
+    double vp[3];
+    const double s[3] = {st->shift[0], st->shift[1], st->shift[2]};
+    step_and_accumulate(F, y, v, mq, sp, s, vp, p);
+    tv.vx[i] = vp[0];
+    tv.vy[i] = vp[1];
+    tv.vz[i] = vp[2];
+  }
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + wl;
+  warp_store_partial(p, lane, partials + gw * kPartialStride);
+}
+
+template <bool kGuard>
+__global__ void __launch_bounds__(kForceThreads) k_direct_operator32(
+    const float4* __restrict__ src, int64_t n, const double* __restrict__ qx_,
+    const double* __restrict__ qy_, const double* __restrict__ qz_, const double* __restrict__ qm_,
+    int64_t m, double G, float eps2, double* __restrict__ fout) {
+  __shared__ float4 sm[kTile];
+  constexpr int Q = kDirectQPT;
+  const int64_t base = (int64_t)blockIdx.x * (kForceThreads * Q);
+  float qx[Q], qy[Q], qz[Q];
+#pragma unroll
+  for (int k = 0; k < Q; k++) {
+    const int64_t i = base + threadIdx.x + k * kForceThreads;
+    qx[k] = i < m ? (float)qx_[i] : 0.f;
+    qy[k] = i < m ? (float)qy_[i] : 0.f;
+    qz[k] = i < m ? (float)qz_[i] : 0.f;
+  }
+  double A[Q][3];
+#pragma unroll
+  for (int k = 0; k < Q; k++) A[k][0] = A[k][1] = A[k][2] = 0.0;
+  for (int64_t t0 = 0; t0 < n; t0 += kTile) {
+    const int jmax = (int)((n - t0) < (int64_t)(kTile) ? (n - t0) : (int64_t)(kTile));
+    __syncthreads();
+    for (int j = threadIdx.x; j < jmax; j += kForceThreads) sm[j] = __ldg(&src[t0 + j]);
+    __syncthreads();
+    float ax[Q], ay[Q], az[Q];
+#pragma unroll
+    for (int k = 0; k < Q; k++) ax[k] = ay[k] = az[k] = 0.f;
+    direct_tile32<Q, kGuard>(sm, jmax, qx, qy, qz, eps2, ax, ay, az);
+#pragma unroll
+    for (int k = 0; k < Q; k++) {
+      A[k][0] += (double)ax[k];
+      A[k][1] += (double)ay[k];
+      A[k][2] += (double)az[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < Q; k++) {
+    const int64_t i = base + threadIdx.x + k * kForceThreads;
+    if (i >= m) continue;
+    const double gq = G * qm_[i];
+    fout[i * 3] = gq * A[k][0];
+    fout[i * 3 + 1] = gq * A[k][1];
+    fout[i * 3 + 2] = gq * A[k][2];
+  }
+}
+
+__global__ void __launch_bounds__(kForceThreads) k_direct_operator64(
+    const double4* __restrict__ src, int64_t n, const double* __restrict__ qx_,
+    const double* __restrict__ qy_, const double* __restrict__ qz_, const double* __restrict__ qm_,
+    int64_t m, double G, double eps2, double* __restrict__ fout) {
+  __shared__ double4 sm[kTile / 2];
+  const int64_t i = (int64_t)blockIdx.x * kForceThreads + threadIdx.x;
+  const double qx = i < m ? qx_[i] : 0.0, qy = i < m ? qy_[i] : 0.0, qz = i < m ? qz_[i] : 0.0;
+  double sx = 0, sy = 0, sz = 0;
+  for (int64_t t0 = 0; t0 < n; t0 += kTile / 2) {
+    const int jmax = (int)((n - t0) < (int64_t)(kTile / 2) ? (n - t0) : (int64_t)(kTile / 2));
+    __syncthreads();
+    for (int j = threadIdx.x; j < jmax; j += kForceThreads) sm[j] = src[t0 + j];
+    __syncthreads();
+    direct_tile64(sm, jmax, qx, qy, qz, eps2, sx, sy, sz);
+  }
+  if (i >= m) return;
+  const double sc = __dmul_rn(-G, qm_[i]);  // -params.G * query_mass (bhtree.py:164)
+  fout[i * 3] = __dmul_rn(sc, sx);
+  fout[i * 3 + 1] = __dmul_rn(sc, sy);
+  fout[i * 3 + 2] = __dmul_rn(sc, sz);
+}
+
+// ---------------------------------------------------------------- energy
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__global__ void __launch_bounds__(kForceThreads) k_gpe32(const float4* __restrict__ src, int64_t n,
+                                                         const double* __restrict__ px,
+                                                         const double* __restrict__ py,
+                                                         const double* __restrict__ pz,
+                                                         const double* __restrict__ mq, int64_t m,
+                                                         float eps, const IterState* st,
+                                                         double* partials) {
+  if (st && st->done) return;
+  __shared__ float4 sm[kTile];
+  constexpr int Q = kDirectQPT;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t base = (int64_t)blockIdx.x * (kForceThreads * Q);
+  float qx[Q], qy[Q], qz[Q];
+#pragma unroll
+  for (int k = 0; k < Q; k++) {
+    const int64_t i = base + threadIdx.x + k * kForceThreads;
+    qx[k] = i < m ? (float)px[i] : 0.f;
+    qy[k] = i < m ? (float)py[i] : 0.f;
+    qz[k] = i < m ? (float)pz[i] : 0.f;
+  }
+  double acc[Q];
+#pragma unroll
+  for (int k = 0; k < Q; k++) acc[k] = 0.0;
+  for (int64_t t0 = 0; t0 < n; t0 += kTile) {
+    const int jmax = (int)((n - t0) < (int64_t)(kTile) ? (n - t0) : (int64_t)(kTile));
+    __syncthreads();
+    for (int j = threadIdx.x; j < jmax; j += kForceThreads) sm[j] = __ldg(&src[t0 + j]);
+    __syncthreads();
+    float a[Q];
+#pragma unroll
+    for (int k = 0; k < Q; k++) a[k] = 0.f;
+#pragma unroll 4
+    for (int j = 0; j < jmax; j++) {
+      const float4 s = sm[j];
+#pragma unroll
+      for (int k = 0; k < Q; k++) {
+        const float dx = s.x - qx[k], dy = s.y - qy[k], dz = s.z - qz[k];
+        const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        a[k] = fmaf(s.w, rcp_approx(sqrt_approx(d2) + eps), a[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < Q; k++) acc[k] += (double)a[k];
+  }
+  double tot = 0.0;
+#pragma unroll
+  for (int k = 0; k < Q; k++) {
+    const int64_t i = base + threadIdx.x + k * kForceThreads;
+    if (i < m) tot += mq[i] * acc[k];
+  }
+  tot = warp_sum(tot);
+  if (lane == 0) partials[(int64_t)blockIdx.x * kWarps + wl] = tot;
+}
+
+__global__ void __launch_bounds__(kForceThreads) k_gpe64(const double4* __restrict__ src, int64_t n,
+                                                         const double* __restrict__ px,
+                                                         const double* __restrict__ py,
+                                                         const double* __restrict__ pz,
+                                                         const double* __restrict__ mq, int64_t m,
+                                                         double eps, const IterState* st,
+                                                         double* partials) {
+  if (st && st->done) return;
+  __shared__ double4 sm[kTile / 2];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * kForceThreads + threadIdx.x;
+  const double qx = i < m ? px[i] : 0.0, qy = i < m ? py[i] : 0.0, qz = i < m ? pz[i] : 0.0;
+  double acc = 0.0;
+  for (int64_t t0 = 0; t0 < n; t0 += kTile / 2) {
+    const int jmax = (int)((n - t0) < (int64_t)(kTile / 2) ? (n - t0) : (int64_t)(kTile / 2));
+    __syncthreads();
+    for (int j = threadIdx.x; j < jmax; j += kForceThreads) sm[j] = src[t0 + j];
+    __syncthreads();
+    for (int j = 0; j < jmax; j++) {
+      const double4 s = sm[j];
+      const double dx = __dsub_rn(qx, s.x), dy = __dsub_rn(qy, s.y), dz = __dsub_rn(qz, s.z);
+      const double d2 =
+          __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+      acc = __dadd_rn(acc, __ddiv_rn(s.w, __dadd_rn(__dsqrt_rn(d2), eps)));  // :66
+    }
+  }
+  double tot = i < m ? __dmul_rn(mq[i], acc) : 0.0;
+  tot = warp_sum(tot);
+  if (lane == 0) partials[(int64_t)blockIdx.x * kWarps + wl] = tot;
+}
+
+inline unsigned grid_for(int64_t items, int64_t per_block) {
+  return (unsigned)((items + per_block - 1) / per_block);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+int64_t bh_iterate_warps(int64_t m) { return (int64_t)grid_for(m, kForceThreads) * kWarps; }
+int64_t direct_iterate_warps(int64_t m, int precision) {
+  const int64_t per = precision ? kForceThreads : kForceThreads * kDirectQPT;
+  return (int64_t)grid_for(m, per) * kWarps;
+}
+int64_t gpe_warps(int64_t m, int precision) { return direct_iterate_warps(m, precision); }
+
+void launch_bh_iterate(const TreeDev& T, const TemplateView& tv, const IterState* st,
+                       const SimParams& sp, double* partials, int precision, cudaStream_t s) {
+  if (tv.m <= 0) return;
+  const unsigned g = grid_for(tv.m, kForceThreads);
+  if (precision)
+    k_bh_iterate<double><<<g, kForceThreads, 0, s>>>(T.records(), (int)T.n_nodes, tv, st, sp,
+                                                     partials, (float)T.cmag);
+  else
+    k_bh_iterate<float><<<g, kForceThreads, 0, s>>>(T.records(), (int)T.n_nodes, tv, st, sp,
+                                                    partials, (float)T.cmag);
+}
+
+void launch_direct_iterate(const RefPoints& ref, const TemplateView& tv, const IterState* st,
+                           const SimParams& sp, double* partials, int precision, cudaStream_t s) {
+  if (tv.m <= 0) return;
+  if (precision) {
+    k_direct_iterate64<<<grid_for(tv.m, kForceThreads), kForceThreads, 0, s>>>(ref.p64, ref.n, tv,
+                                                                               st, sp, partials);
+  } else {
+    const unsigned g = grid_for(tv.m, kForceThreads * kDirectQPT);
+    if (sp.eps2 > 0.0)
+      k_direct_iterate32<false><<<g, kForceThreads, 0, s>>>(ref.p32, ref.n, tv, st, sp, partials);
+    else
+      k_direct_iterate32<true><<<g, kForceThreads, 0, s>>>(ref.p32, ref.n, tv, st, sp, partials);
+  }
+}
+
+void launch_gpe(const RefPoints& ref, const double* px, const double* py, const double* pz,
+                const double* mq, int64_t m, double eps, const IterState* st, double* partials,
+                int precision, cudaStream_t s) {
+  if (m <= 0) return;
+  if (precision)
+    k_gpe64<<<grid_for(m, kForceThreads), kForceThreads, 0, s>>>(ref.p64, ref.n, px, py, pz, mq, m,
+                                                                 eps, st, partials);
+  else
+    k_gpe32<<<grid_for(m, kForceThreads * kDirectQPT), kForceThreads, 0, s>>>(
+        ref.p32, ref.n, px, py, pz, mq, m, (float)eps, st, partials);
+}
+
+void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, const double* qz,
+                        const double* qm, const int* order, int64_t m, double theta, double G,
+                        double eps2, double* fout, long long* visits, long long* accepted,
+                        int precision, cudaStream_t s) {
+  if (m <= 0) return;
+  const unsigned g = grid_for(m, kForceThreads);
+  const double theta2 = theta * theta;
+  if (precision)
+    k_bh_operator<double><<<g, kForceThreads, 0, s>>>(T.records(), (int)T.n_nodes, qx, qy, qz, qm,
+                                                      order, m, theta2, G, eps2, fout, visits,
+                                                      accepted, (float)T.cmag);
+  else
+    k_bh_operator<float><<<g, kForceThreads, 0, s>>>(T.records(), (int)T.n_nodes, qx, qy, qz, qm,
+                                                     order, m, theta2, G, eps2, fout, visits,
+                                                     accepted, (float)T.cmag);
+}
+
+void launch_direct_operator(const RefPoints& ref, const double* qx, const double* qy,
+                            const double* qz, const double* qm, int64_t m, double G, double eps,
+                            double* fout, int precision, cudaStream_t s) {
+  if (m <= 0) return;
+  const double eps2 = eps * eps;  // params.epsilon**2 (bhtree.py:159)
+  if (precision) {
+    k_direct_operator64<<<grid_for(m, kForceThreads), kForceThreads, 0, s>>>(
+        ref.p64, ref.n, qx, qy, qz, qm, m, G, eps2, fout);
+  } else {
+    const unsigned g = grid_for(m, kForceThreads * kDirectQPT);
+    if (eps2 > 0.0)
+      k_direct_operator32<false><<<g, kForceThreads, 0, s>>>(ref.p32, ref.n, qx, qy, qz, qm, m, G,
+                                                             (float)eps2, fout);
+    else
+      k_direct_operator32<true><<<g, kForceThreads, 0, s>>>(ref.p32, ref.n, qx, qy, qz, qm, m, G,
+                                                            (float)eps2, fout);
+  }
+}
+
+}  // namespace fga

@@ -1,0 +1,339 @@
+// rigid.cu -- K7/K8: deterministic reduction of the Kabsch partials and the
+// fp64 rigid update (procrustes.py:12-49, registration.py:133-154).
+//
+// The cross-covariance is assembled from shifted moments
+//     C = sum w u^T - M * mean(w) mean(u)^T,  u = y - s, w = y + d - s
+// with s = the current template mean (carried from the previous update), so
+// there is no cancellation; C equals the reference's yd_c.T @ yc
+// (procrustes.py:23-25) up to rounding.  The 3x3 SVD is a one-sided Jacobi in
+// fp64 (no LAPACK on the device); the reflection guard and the rotation are
+// the reference's (:27-33): R = U diag(1, 1, sign det(U V^T)) V^T.
+#include "fga_session.cuh"
+
+namespace fga {
+namespace {
+
+constexpr int kReduceThreads = 1024;
+
+// Block-wide sums of the per-warp partial records, fixed order.
+__global__ void __launch_bounds__(kReduceThreads) k_reduce(const double* __restrict__ partials,
+                                                           int64_t nwarps,
+                                                           const double* __restrict__ gpe_part,
+                                                           int64_t ngwarps, double direct_pairs,
+                                                           double* __restrict__ sums) {
+  double acc[kPartialStride];
+#pragma unroll
+  for (int k = 0; k < kPartialStride; k++) acc[k] = 0.0;
+  for (int64_t w = threadIdx.x; w < nwarps; w += kReduceThreads) {
+#pragma unroll
+    for (int k = 0; k < 17; k++) acc[k] += partials[w * kPartialStride + k];
+  }
+  for (int64_t w = threadIdx.x; w < ngwarps; w += kReduceThreads) acc[kGpe] += gpe_part[w];
+  __shared__ double sm[kReduceThreads / 32][kPartialStride];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kPartialStride; k++) {
+    const double v = warp_sum(acc[k]);
+    if (lane == 0) sm[wl][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kPartialStride) {
+    double v = 0.0;
+    for (int j = 0; j < kReduceThreads / 32; j++) v += sm[j][threadIdx.x];
+    if (direct_pairs >= 0.0 && (threadIdx.x == kAccepted || threadIdx.x == kVisits)) v = direct_pairs;
+    sums[threadIdx.x] = v;
+  }
+}
+
+// ------------------------------------------------------------------ 3x3 SVD
+// One-sided Jacobi on the columns of A (3x3, row-major): A V = U S.
+__device__ void svd3(const double C[9], double U[9], double S[3], double V[9]) {
+  double A[9];
+  for (int k = 0; k < 9; k++) A[k] = C[k];
+  for (int k = 0; k < 9; k++) V[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  const int P[3] = {0, 0, 1}, Q[3] = {1, 2, 2};
+  for (int sweep = 0; sweep < 30; sweep++) {
+    double off = 0.0;
+    for (int r = 0; r < 3; r++) {
+      const int p = P[r], q = Q[r];
+      double alpha = 0.0, beta = 0.0, gamma = 0.0;
+      for (int k = 0; k < 3; k++) {
+        alpha += A[3 * k + p] * A[3 * k + p];
+        beta += A[3 * k + q] * A[3 * k + q];
+        gamma += A[3 * k + p] * A[3 * k + q];
+      }
+      if (gamma == 0.0) continue;
+      const double rel = fabs(gamma) / sqrt(alpha * beta);
+      off = fmax(off, rel);
+      if (!(rel > 1e-17)) continue;
+      const double zeta = (beta - alpha) / (2.0 * gamma);
+      const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+      const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+      for (int k = 0; k < 3; k++) {
+        const double ap = A[3 * k + p], aq = A[3 * k + q];
+        A[3 * k + p] = c * ap - s * aq;
+        A[3 * k + q] = s * ap + c * aq;
+        const double vp = V[3 * k + p], vq = V[3 * k + q];
+        V[3 * k + p] = c * vp - s * vq;
+        V[3 * k + q] = s * vp + c * vq;
+      }
+    }
+    if (off < 1e-16) break;
+  }
+  // singular values = column norms, sorted descending (LAPACK order)
+  int ord[3] = {0, 1, 2};
+  double nrm[3];
+  for (int j = 0; j < 3; j++)
+    nrm[j] = sqrt(A[j] * A[j] + A[3 + j] * A[3 + j] + A[6 + j] * A[6 + j]);
+  for (int a = 0; a < 2; a++)
+    for (int b = 0; b < 2 - a; b++)
+      if (nrm[ord[b]] < nrm[ord[b + 1]]) {
+        int tmp = ord[b];
+        ord[b] = ord[b + 1];
+        ord[b + 1] = tmp;
+      }
+  double Vs[9];
+  for (int j = 0; j < 3; j++) {
+    S[j] = nrm[ord[j]];
+    for (int k = 0; k < 3; k++) {
+      Vs[3 * k + j] = V[3 * k + ord[j]];
+      U[3 * k + j] = S[j] > 0.0 ? A[3 * k + ord[j]] / S[j] : 0.0;
+    }
+  }
+  for (int k = 0; k < 9; k++) V[k] = Vs[k];
+  // Orthonormal completion: u1 normalized, u2 Gram-Schmidt, u3 = u1 x u2.
+  double u1[3] = {U[0], U[3], U[6]}, u2[3] = {U[1], U[4], U[7]};
+  double n1 = sqrt(u1[0] * u1[0] + u1[1] * u1[1] + u1[2] * u1[2]);
+  if (!(n1 > 0.0)) {
+    u1[0] = 1.0;
+    u1[1] = u1[2] = 0.0;
+    n1 = 1.0;
+  }
+  for (int k = 0; k < 3; k++) u1[k] /= n1;
+  double d12 = u1[0] * u2[0] + u1[1] * u2[1] + u1[2] * u2[2];
+  for (int k = 0; k < 3; k++) u2[k] -= d12 * u1[k];
+  double n2 = sqrt(u2[0] * u2[0] + u2[1] * u2[1] + u2[2] * u2[2]);
+  if (!(n2 > 1e-300)) {  // rank <= 1: any unit vector orthogonal to u1
+    const int a = fabs(u1[0]) < 0.9 ? 0 : 1;
+    double e[3] = {0, 0, 0};
+    e[a] = 1.0;
+    d12 = u1[a];
+    for (int k = 0; k < 3; k++) u2[k] = e[k] - d12 * u1[k];
+    n2 = sqrt(u2[0] * u2[0] + u2[1] * u2[1] + u2[2] * u2[2]);
+  }
+  for (int k = 0; k < 3; k++) u2[k] /= n2;
+  const double u3[3] = {u1[1] * u2[2] - u1[2] * u2[1], u1[2] * u2[0] - u1[0] * u2[2],
+                        u1[0] * u2[1] - u1[1] * u2[0]};
+  for (int k = 0; k < 3; k++) {
+    U[3 * k] = u1[k];
+    U[3 * k + 1] = u2[k];
+    U[3 * k + 2] = u3[k];
+  }
+}
+
+__device__ __forceinline__ double det3(const double M[9]) {
+  return M[0] * (M[4] * M[8] - M[5] * M[7]) - M[1] * (M[3] * M[8] - M[5] * M[6]) +
+         M[2] * (M[3] * M[7] - M[4] * M[6]);
+}
+
+// procrustes.solve_rotation (procrustes.py:12-35) from the cross-covariance.
+__device__ void kabsch_rotation(const double C[9], double R[9], int* degenerate) {
+  double U[9], S[3], V[9];
+  svd3(C, U, S, V);
+  // sign(det(U Vt)) (:28-30); det(U) = +1 by construction
+  double sgn = det3(V) < 0.0 ? -1.0 : 1.0;
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++)
+      R[3 * i + j] = U[3 * i] * V[3 * j] + U[3 * i + 1] * V[3 * j + 1] + sgn * U[3 * i + 2] * V[3 * j + 2];
+  if (degenerate) {
+    const double tol = 1e-12 * fmax(S[0], 1e-300);  // _DEGENERATE_REL_TOL (:8)
+    int rank = (S[0] > tol) + (S[1] > tol) + (S[2] > tol);
+    *degenerate = rank < 2;
+  }
+}
+
+__global__ void k_update(const double* __restrict__ sums, IterState* st, SimParams sp,
+                         double* rec_delta, double* rec_traj, double* rec_gpe,
+                         long long* rec_inter, long long* rec_visits, int has_gpe) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (st->done) return;
+  const double M = (double)sp.m_total;
+  double mu_u[3], mu_w[3], C[9];
+  for (int k = 0; k < 3; k++) {
+    mu_u[k] = sums[kSumU + k] / M;
+    mu_w[k] = sums[kSumW + k] / M;
+  }
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) C[3 * i + j] = sums[kSumWU + 3 * i + j] - M * mu_w[i] * mu_u[j];
+  double R[9];
+  kabsch_rotation(C, R, nullptr);
+  double mu_y[3], mu_d[3], t[3];
+  for (int k = 0; k < 3; k++) {
+    mu_y[k] = mu_u[k] + st->shift[k];
+    mu_d[k] = mu_w[k] + st->shift[k];
+  }
+  for (int k = 0; k < 3; k++)
+    t[k] = mu_d[k] - (R[3 * k] * mu_y[0] + R[3 * k + 1] * mu_y[1] + R[3 * k + 2] * mu_y[2]);  // :42
+  const long long it = st->iter;
+  if (has_gpe && it > 0 && rec_gpe) rec_gpe[it - 1] = -sp.G * sums[kGpe];
+  // R_acc <- R R_acc ; t_acc <- t + R t_acc  (registration.py:137-138)
+  double Ra[9], ta[3], delta = 0.0;
+  for (int i = 0; i < 3; i++) {
+    for (int j = 0; j < 3; j++)
+      Ra[3 * i + j] = R[3 * i] * st->Racc[j] + R[3 * i + 1] * st->Racc[3 + j] + R[3 * i + 2] * st->Racc[6 + j];
+    ta[i] = t[i] + (R[3 * i] * st->tacc[0] + R[3 * i + 1] * st->tacc[1] + R[3 * i + 2] * st->tacc[2]);
+  }
+  // delta = ||[R_acc|t_acc] - prev||_F^2 (:140-142)
+  for (int i = 0; i < 3; i++) {
+    for (int j = 0; j < 3; j++) {
+      const double e = Ra[3 * i + j] - st->Racc[3 * i + j];
+      delta += e * e;
+    }
+    const double e = ta[i] - st->tacc[i];
+    delta += e * e;
+  }
+  for (int k = 0; k < 9; k++) {
+    st->Rp[k] = R[k];
+    st->Racc[k] = Ra[k];
+  }
+  for (int k = 0; k < 3; k++) {
+    st->tp[k] = t[k];
+    st->tacc[k] = ta[k];
+    st->shift[k] = mu_d[k];  // mean of R y + t
+  }
+  if (rec_delta) rec_delta[it] = delta;
+  if (rec_traj)
+    for (int i = 0; i < 3; i++) {
+      for (int j = 0; j < 3; j++) rec_traj[it * 12 + 4 * i + j] = Ra[3 * i + j];
+      rec_traj[it * 12 + 4 * i + 3] = ta[i];
+    }
+  if (rec_inter) rec_inter[it] = (long long)sums[kAccepted];
+  if (rec_visits) rec_visits[it] = (long long)sums[kVisits];
+  st->iter = it + 1;
+  if (delta < sp.conv_tol) {  // :152-154
+    st->converged = 1;
+    st->done = 1;
+  } else if (it + 1 >= sp.max_iters) {
+    st->done = 1;
+  }
+}
+
+__global__ void k_apply_pending(TemplateView tv, const IterState* __restrict__ st) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= tv.m) return;
+  const double y[3] = {tv.px[i], tv.py[i], tv.pz[i]};
+  double ny[3];
+  for (int r = 0; r < 3; r++)
+    ny[r] = st->Rp[3 * r] * y[0] + st->Rp[3 * r + 1] * y[1] + st->Rp[3 * r + 2] * y[2] + st->tp[r];
+  tv.px[i] = ny[0];
+  tv.py[i] = ny[1];
+  tv.pz[i] = ny[2];
+}
+
+__global__ void k_state_init(IterState* st, const double* __restrict__ mean3) {
+  if (threadIdx.x != 0) return;
+  for (int k = 0; k < 9; k++) {
+    st->Rp[k] = (k % 4 == 0) ? 1.0 : 0.0;
+    st->Racc[k] = st->Rp[k];
+  }
+  for (int k = 0; k < 3; k++) {
+    st->tp[k] = 0.0;
+    st->tacc[k] = 0.0;
+    st->shift[k] = mean3[k];
+  }
+  st->iter = 0;
+  st->done = 0;
+  st->converged = 0;
+  st->gpe_pending = 0;
+  st->pad = 0;
+}
+
+// solve_rigid operator: two deterministic passes (means, then centred
+// cross-covariance) in one block, then the Kabsch rotation.
+__global__ void __launch_bounds__(kReduceThreads) k_solve_rigid(const double* __restrict__ y,
+                                                                const double* __restrict__ yd,
+                                                                int64_t m, double* out13) {
+  __shared__ double sm[kReduceThreads / 32][9];
+  __shared__ double mean[6];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  double a[9];
+  for (int k = 0; k < 6; k++) a[k] = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += kReduceThreads)
+    for (int k = 0; k < 3; k++) {
+      a[k] += y[i * 3 + k];
+      a[3 + k] += yd[i * 3 + k];
+    }
+  for (int k = 0; k < 6; k++) {
+    const double v = warp_sum(a[k]);
+    if (lane == 0) sm[wl][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double v = 0.0;
+    for (int j = 0; j < kReduceThreads / 32; j++) v += sm[j][threadIdx.x];
+    mean[threadIdx.x] = v / (double)m;
+  }
+  __syncthreads();
+  for (int k = 0; k < 9; k++) a[k] = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += kReduceThreads) {
+    double yc[3], dc[3];
+    for (int k = 0; k < 3; k++) {
+      yc[k] = y[i * 3 + k] - mean[k];
+      dc[k] = yd[i * 3 + k] - mean[3 + k];
+    }
+    for (int r = 0; r < 3; r++)
+      for (int c = 0; c < 3; c++) a[3 * r + c] = fma(dc[r], yc[c], a[3 * r + c]);
+  }
+  __syncthreads();
+  for (int k = 0; k < 9; k++) {
+    const double v = warp_sum(a[k]);
+    if (lane == 0) sm[wl][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double C[9], R[9];
+    for (int k = 0; k < 9; k++) {
+      double v = 0.0;
+      for (int j = 0; j < kReduceThreads / 32; j++) v += sm[j][k];
+      C[k] = v;
+    }
+    int degenerate = 0;
+    kabsch_rotation(C, R, &degenerate);
+    for (int k = 0; k < 9; k++) out13[k] = R[k];
+    for (int k = 0; k < 3; k++)  // t = mean(y_d) - R mean(y) (:42)
+      out13[9 + k] = mean[3 + k] - (R[3 * k] * mean[0] + R[3 * k + 1] * mean[1] + R[3 * k + 2] * mean[2]);
+    out13[12] = degenerate;
+  }
+}
+
+}  // namespace
+
+void launch_reduce(const double* partials, int64_t nwarps, const double* gpe_partials,
+                   int64_t ngwarps, double direct_pairs, double* sums, cudaStream_t s) {
+  k_reduce<<<1, kReduceThreads, 0, s>>>(partials, nwarps, gpe_partials, ngwarps, direct_pairs,
+                                        sums);
+}
+
+void launch_update(const double* sums, IterState* st, const SimParams& sp, double* rec_delta,
+                   double* rec_traj, double* rec_gpe, long long* rec_inter, long long* rec_visits,
+                   int has_gpe, cudaStream_t s) {
+  k_update<<<1, 32, 0, s>>>(sums, st, sp, rec_delta, rec_traj, rec_gpe, rec_inter, rec_visits,
+                            has_gpe);
+}
+
+void launch_apply_pending(const TemplateView& tv, const IterState* st, cudaStream_t s) {
+  if (tv.m <= 0) return;
+  k_apply_pending<<<(unsigned)((tv.m + 255) / 256), 256, 0, s>>>(tv, st);
+}
+
+void launch_state_init(IterState* st, const double* mean3, cudaStream_t s) {
+  k_state_init<<<1, 32, 0, s>>>(st, mean3);
+}
+
+void launch_solve_rigid(const double* y, const double* yd, int64_t m, double* scratch,
+                        double* out13, cudaStream_t s) {
+  (void)scratch;
+  k_solve_rigid<<<1, kReduceThreads, 0, s>>>(y, yd, m, out13);
+}
+
+}  // namespace fga

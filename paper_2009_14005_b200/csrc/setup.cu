@@ -1,0 +1,433 @@
+// setup.cu -- once-per-registration O(N) work on the device: joint
+// normalization (normalize.py:36-60), NIV lattice masses (masses.py:85-116),
+// the mass rescale (registration.py:85-87), reference-point packing for the
+// direct sum / energy kernels, and the Morton ordering of the template.
+//
+// Every element-wise fp64 expression uses explicit round-to-nearest
+// intrinsics in the reference's operation order so the results are
+// bit-identical to numpy's (tests/test_gpu_setup.py).  The cloud means use a
+// sequential column sum because that IS numpy's order for an axis-0
+// reduction of an (n,3) C-contiguous array.
+#include <cub/cub.cuh>
+
+#include "../../include/fga.h"
+#include "fga_session.cuh"
+
+namespace fga {
+namespace {
+
+constexpr int kT = 256;
+inline unsigned nblk(int64_t n, int t = kT) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+// numpy mean(axis=0): sequential accumulation over rows, then / n.
+// thread k<3 handles x column k, thread 3+k handles y column k.
+__global__ void k_colmean_seq(const double* __restrict__ x, int64_t n, const double* __restrict__ y,
+                              int64_t m, double* __restrict__ out6) {
+  const int t = threadIdx.x;
+  if (t >= 6) return;
+  const double* p = t < 3 ? x : y;
+  const int64_t cnt = t < 3 ? n : m;
+  const int k = t % 3;
+  double s = 0.0;
+  int64_t i = 0;
+  for (; i + 8 <= cnt; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) v[u] = p[(i + u) * 3 + k];
+#pragma unroll
+    for (int u = 0; u < 8; u++) s = __dadd_rn(s, v[u]);
+  }
+  for (; i < cnt; i++) s = __dadd_rn(s, p[i * 3 + k]);
+  out6[t] = __ddiv_rn(s, (double)cnt);
+}
+
+// min/max over all centred coordinates of both clouds (scalar l, r).
+__global__ void k_centred_minmax(const double* __restrict__ x, int64_t n,
+                                 const double* __restrict__ y, int64_t m,
+                                 const double* __restrict__ mean6, double* __restrict__ part) {
+  double lo = INFINITY, hi = -INFINITY;
+  const int64_t tot = (n + m) * 3;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const bool isx = e < n * 3;
+    const int64_t f = isx ? e : e - n * 3;
+    const double v = __dsub_rn(isx ? x[f] : y[f], mean6[(isx ? 0 : 3) + (int)(f % 3)]);
+    lo = fmin(lo, v);
+    hi = fmax(hi, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  __shared__ double s[2][kT / 32];
+  if ((threadIdx.x & 31) == 0) {
+    s[0][threadIdx.x >> 5] = lo;
+    s[1][threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 1; j < kT / 32; j++) {
+      lo = fmin(lo, s[0][j]);
+      hi = fmax(hi, s[1][j]);
+    }
+    part[blockIdx.x * 2] = fmin(s[0][0], lo);
+    part[blockIdx.x * 2 + 1] = fmax(s[1][0], hi);
+  }
+}
+
+__global__ void k_norm_ctx(const double* __restrict__ part, int nparts, const double* mean6,
+                           double a, double b, double* ctx10) {
+  if (threadIdx.x != 0) return;
+  double lo = part[0], hi = part[1];
+  for (int j = 1; j < nparts; j++) {
+    lo = fmin(lo, part[2 * j]);
+    hi = fmax(hi, part[2 * j + 1]);
+  }
+  for (int k = 0; k < 6; k++) ctx10[k] = mean6[k];
+  ctx10[6] = lo;
+  ctx10[7] = hi;
+  ctx10[8] = a;
+  ctx10[9] = b;
+}
+
+// p' = (p - mu - l) * s + a, s = (b - a) / (r - l)   (normalize.py:55-58)
+__global__ void k_norm_apply(const double* __restrict__ x, int64_t n, const double* __restrict__ y,
+                             int64_t m, const double* __restrict__ ctx10, double* __restrict__ xn,
+                             double* __restrict__ yn) {
+  const int64_t tot = (n + m) * 3;
+  const double l = ctx10[6], r = ctx10[7], a = ctx10[8], b = ctx10[9];
+  const double s = __ddiv_rn(__dsub_rn(b, a), __dsub_rn(r, l));
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const bool isx = e < n * 3;
+    const int64_t f = isx ? e : e - n * 3;
+    const double c = __dsub_rn(isx ? x[f] : y[f], ctx10[(isx ? 0 : 3) + (int)(f % 3)]);
+    const double v = __dadd_rn(__dmul_rn(__dsub_rn(c, l), s), a);
+    if (isx) xn[f] = v; else yn[f] = v;
+  }
+}
+
+// ---------------------------------------------------------------- NIV
+// idx = clip(floor((p - a) / edge), 0, rho-1) with numpy's float->int64 cast
+// (out-of-range values become INT64_MIN, then clip to 0).
+__device__ __forceinline__ long long niv_axis(double p, double a, double edge, int rho) {
+  const double f = floor(__ddiv_rn(__dsub_rn(p, a), edge));
+  long long v;
+  if (!(f >= -9.223372036854775808e18 && f < 9.223372036854775808e18)) v = LLONG_MIN;
+  else v = (long long)f;
+  return v < 0 ? 0 : (v > rho - 1 ? rho - 1 : v);
+}
+
+__global__ void k_niv_hist(const double* __restrict__ pts, int64_t n, int rho, double a,
+                           double edge, int* __restrict__ flat,
+                           unsigned long long* __restrict__ counts) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long ix = niv_axis(pts[i * 3], a, edge, rho);
+  const long long iy = niv_axis(pts[i * 3 + 1], a, edge, rho);
+  const long long iz = niv_axis(pts[i * 3 + 2], a, edge, rho);
+  const long long f = (ix * rho + iy) * rho + iz;  // masses.py:106-108
+  flat[i] = (int)f;
+  atomicAdd(&counts[f], 1ull);
+}
+
+__global__ void k_niv_nnz(const unsigned long long* __restrict__ counts, int cells,
+                          unsigned long long* __restrict__ nnz) {
+  unsigned long long c = 0;
+  for (int j = threadIdx.x; j < cells; j += blockDim.x) c += counts[j] > 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  __shared__ unsigned long long s[32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int j = 0; j < (int)(blockDim.x >> 5); j++) t += s[j];
+    *nnz = t;
+  }
+}
+
+// cell_value = total_vol * cell_vol / min(count * ball_vol, cell_vol)  (:111-114)
+__global__ void k_niv_cells(const unsigned long long* __restrict__ counts, int cells,
+                            const unsigned long long* __restrict__ nnz, double cell_vol,
+                            double ball_vol, double* __restrict__ value) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cells) return;
+  const unsigned long long c = counts[j];
+  if (c == 0) {
+    value[j] = 0.0;
+    return;
+  }
+  const double total_vol = __dmul_rn((double)*nnz, cell_vol);
+  const double uni = fmin(__dmul_rn((double)c, ball_vol), cell_vol);
+  value[j] = __ddiv_rn(__dmul_rn(total_vol, cell_vol), uni > 0.0 ? uni : 1.0);
+}
+
+__global__ void k_niv_gather(const int* __restrict__ flat, int64_t n,
+                             const double* __restrict__ value, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = fmax(value[flat[i]], 1e-6);  // MASS_FLOOR (masses.py:16, :116)
+}
+
+__global__ void k_external(const double* __restrict__ w, int64_t n, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = fmax(w[i], 1e-6);  // masses.py:135
+}
+
+// ---------------------------------------------------------------- rescale
+// Deterministic sum(sx) and max(sy); one block.
+__global__ void k_sum_max(const double* __restrict__ sx, int64_t n, const double* __restrict__ sy,
+                          int64_t m, double* out2) {
+  double s = 0.0, mx = -INFINITY;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += sx[i];
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) mx = fmax(mx, sy[i]);
+  s = warp_sum(s);
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __shared__ double a[32], b[32];
+  if ((threadIdx.x & 31) == 0) {
+    a[threadIdx.x >> 5] = s;
+    b[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0, u = -INFINITY;
+    for (int j = 0; j < (int)(blockDim.x >> 5); j++) {
+      t += a[j];
+      u = fmax(u, b[j]);
+    }
+    out2[0] = t;
+    out2[1] = u;
+  }
+}
+
+// sx <- min(budget * sx / sum(sx), 0.022); sy <- max(0.1 * sy / max(sy), floor)
+__global__ void k_rescale(double* sx, int64_t n, double* sy, int64_t m, const double* sm2,
+                          double budget, double floor_) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) sx[i] = fmin(__ddiv_rn(__dmul_rn(budget, sx[i]), sm2[0]), 0.022);
+  if (i < m) sy[i] = fmax(__ddiv_rn(__dmul_rn(0.1, sy[i]), sm2[1]), floor_);
+}
+
+__global__ void k_pack_ref(const double* __restrict__ xn, const double* __restrict__ mx, int64_t n,
+                           float4* __restrict__ p32, double4* __restrict__ p64) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = xn[i * 3], y = xn[i * 3 + 1], z = xn[i * 3 + 2], w = mx[i];
+  if (p32) p32[i] = make_float4((float)x, (float)y, (float)z, (float)w);
+  if (p64) p64[i] = make_double4(x, y, z, w);
+}
+
+// deterministic column means (two-level fixed-order tree)
+__global__ void k_mean_partial(const double* __restrict__ p, int64_t n, double* __restrict__ part) {
+  double s[3] = {0, 0, 0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int k = 0; k < 3; k++) s[k] += p[i * 3 + k];
+  __shared__ double sm[3][kT / 32];
+  for (int k = 0; k < 3; k++) {
+    const double v = warp_sum(s[k]);
+    if ((threadIdx.x & 31) == 0) sm[k][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0.0;
+    for (int j = 0; j < kT / 32; j++) v += sm[threadIdx.x][j];
+    part[blockIdx.x * 3 + threadIdx.x] = v;
+  }
+}
+__global__ void k_mean_final(const double* __restrict__ part, int nparts, int64_t n, double* out3) {
+  if (threadIdx.x >= 3) return;
+  double v = 0.0;
+  for (int j = 0; j < nparts; j++) v += part[j * 3 + threadIdx.x];
+  out3[threadIdx.x] = v / (double)n;
+}
+
+__global__ void k_bbox6_partial(const double* __restrict__ p, int64_t n, double* __restrict__ part) {
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    for (int k = 0; k < 3; k++) {
+      lo[k] = fmin(lo[k], p[i * 3 + k]);
+      hi[k] = fmax(hi[k], p[i * 3 + k]);
+    }
+  for (int k = 0; k < 3; k++)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[k] = fmin(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+  __shared__ double sm[6][kT / 32];
+  if ((threadIdx.x & 31) == 0)
+    for (int k = 0; k < 3; k++) {
+      sm[k][threadIdx.x >> 5] = lo[k];
+      sm[3 + k][threadIdx.x >> 5] = hi[k];
+    }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    double v = sm[threadIdx.x][0];
+    for (int j = 1; j < kT / 32; j++)
+      v = threadIdx.x < 3 ? fmin(v, sm[threadIdx.x][j]) : fmax(v, sm[threadIdx.x][j]);
+    part[blockIdx.x * 6 + threadIdx.x] = v;
+  }
+}
+__global__ void k_bbox6_final(const double* __restrict__ part, int nparts, double* out6) {
+  const int k = threadIdx.x;
+  if (k >= 6) return;
+  double v = part[k];
+  for (int j = 1; j < nparts; j++) v = k < 3 ? fmin(v, part[j * 6 + k]) : fmax(v, part[j * 6 + k]);
+  out6[k] = v;
+}
+
+// 21-bit-per-axis Morton key over the cloud's own bbox (locality only).
+__device__ __forceinline__ unsigned long long spread21(unsigned long long v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x1f00000000ffffull;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+__global__ void k_morton(const double* __restrict__ p, int64_t n, const double* __restrict__ box,
+                         unsigned long long* __restrict__ keys, int* __restrict__ idx) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned long long q[3];
+  for (int k = 0; k < 3; k++) {
+    const double ext = box[3 + k] - box[k];
+    double f = ext > 0.0 ? (p[i * 3 + k] - box[k]) / ext : 0.0;
+    f = fmin(fmax(f, 0.0), 1.0);
+    q[k] = (unsigned long long)(f * 2097151.0);
+  }
+  keys[i] = (spread21(q[0]) << 2) | (spread21(q[1]) << 1) | spread21(q[2]);
+  idx[i] = (int)i;
+}
+
+__global__ void k_gather_tpl(const double* __restrict__ pts, const double* __restrict__ mass,
+                             const int* __restrict__ order, int64_t begin, TemplateView tv) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= tv.m) return;
+  const int64_t src = order[begin + i];
+  tv.px[i] = pts[src * 3];
+  tv.py[i] = pts[src * 3 + 1];
+  tv.pz[i] = pts[src * 3 + 2];
+  tv.vx[i] = 0.0;
+  tv.vy[i] = 0.0;
+  tv.vz[i] = 0.0;
+  const_cast<double*>(tv.mq)[i] = mass[src];
+}
+
+__global__ void k_gather_q(const double* __restrict__ q, const double* __restrict__ qm,
+                           const int* __restrict__ order, int64_t m, double* qx, double* qy,
+                           double* qz, double* qms) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int64_t src = order ? order[i] : i;
+  qx[i] = q[src * 3];
+  qy[i] = q[src * 3 + 1];
+  qz[i] = q[src * 3 + 2];
+  qms[i] = qm[src];
+}
+
+}  // namespace
+
+size_t scratch_doubles_for(int64_t n) { (void)n; return 6 * 1024 + 64; }
+
+int normalize_pair_dev(const double* x, int64_t n, const double* y, int64_t m, double a, double b,
+                       double* xn, double* yn, double* ctx10_dev, double* scratch,
+                       size_t scratch_bytes, double* ctx10_host, cudaStream_t s) {
+  (void)scratch_bytes;
+  double* mean6 = scratch;
+  double* part = scratch + 8;
+  const int nb = (int)std::min<int64_t>(nblk((n + m) * 3), 592);
+  k_colmean_seq<<<1, 32, 0, s>>>(x, n, y, m, mean6);
+  k_centred_minmax<<<nb, kT, 0, s>>>(x, n, y, m, mean6, part);
+  k_norm_ctx<<<1, 32, 0, s>>>(part, nb, mean6, a, b, ctx10_dev);
+  FGA_CUDA_TRY(cudaMemcpyAsync(ctx10_host, ctx10_dev, sizeof(double) * 10, cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  if (!(ctx10_host[7] > ctx10_host[6])) {  // normalize.py:53-54
+    set_error("all centered coordinates coincide");
+    return FGA_ERR_DEGENERATE;
+  }
+  k_norm_apply<<<(unsigned)std::min<int64_t>(nblk((n + m) * 3), 4 * 592), kT, 0, s>>>(x, n, y, m, ctx10_dev, xn, yn);
+  FGA_CUDA_TRY(cudaGetLastError());
+  return FGA_OK;
+}
+
+int niv_masses_dev(const double* pts, int64_t n, int rho, double a, double b, int max_depth,
+                   double* out, int* flat, long long* counts, double* cell_value, cudaStream_t s) {
+  if (rho < 2) {
+    set_error("invalid parameter rho");
+    return FGA_ERR_INVALID;
+  }
+  const int64_t ncell64 = (int64_t)rho * rho * rho;
+  if (ncell64 > (1ll << 26)) {
+    set_error("niv: rho^3 too large for the device lattice");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  const int ncell = (int)ncell64;
+  // Python-float scalars exactly as masses.py:97-102 computes them
+  const double extent = b - a;
+  const double cell_edge = extent / rho;
+  const double cell_vol = std::pow(cell_edge, 3);
+  const double r_ball = extent / (2.0 * max_depth * rho);
+  const double ball_vol = (4.0 / 3.0) * M_PI * std::pow(r_ball, 3);
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(counts);
+  FGA_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (ncell + 1), s));
+  k_niv_hist<<<nblk(n), kT, 0, s>>>(pts, n, rho, a, cell_edge, flat, cnt);
+  k_niv_nnz<<<1, 1024, 0, s>>>(cnt, ncell, cnt + ncell);
+  k_niv_cells<<<nblk(ncell), kT, 0, s>>>(cnt, ncell, cnt + ncell, cell_vol, ball_vol, cell_value);
+  k_niv_gather<<<nblk(n), kT, 0, s>>>(flat, n, cell_value, out);
+  FGA_CUDA_TRY(cudaGetLastError());
+  return FGA_OK;
+}
+
+void launch_external_masses(const double* w, int64_t n, double* out, cudaStream_t s) {
+  k_external<<<nblk(n), kT, 0, s>>>(w, n, out);
+}
+
+// registration.py:85-87 (FIELD_MASS=16, FIELD_MASS_POINTS=2000,
+// REFERENCE_POINT_CAP=0.022, TEMPLATE_PEAK_MASS=0.1, floor max(1e-6, dt*eta))
+void launch_rescale(double* sx, int64_t n, double* sy, int64_t m, double dt, double eta,
+                    double* scratch, cudaStream_t s) {
+  const double budget = 16.0 * std::sqrt((double)n / 2000.0);
+  const double floor_ = std::max(1e-6, dt * eta);
+  k_sum_max<<<1, 1024, 0, s>>>(sx, n, sy, m, scratch);
+  k_rescale<<<nblk(std::max(n, m)), kT, 0, s>>>(sx, n, sy, m, scratch, budget, floor_);
+}
+
+void launch_pack_ref(const double* xn, const double* mx, int64_t n, float4* p32, double4* p64,
+                     cudaStream_t s) {
+  k_pack_ref<<<nblk(n), kT, 0, s>>>(xn, mx, n, p32, p64);
+}
+
+void launch_mean3(const double* pts, int64_t n, double* scratch, double* out3, cudaStream_t s) {
+  const int nb = (int)std::min<int64_t>(nblk(n), 592);
+  k_mean_partial<<<nb, kT, 0, s>>>(pts, n, scratch);
+  k_mean_final<<<1, 32, 0, s>>>(scratch, nb, n, out3);
+}
+
+void launch_bbox(const double* pts, int64_t n, double* scratch, double* out6, cudaStream_t s) {
+  const int nb = (int)std::min<int64_t>(nblk(n), 592);
+  k_bbox6_partial<<<nb, kT, 0, s>>>(pts, n, scratch);
+  k_bbox6_final<<<1, 32, 0, s>>>(scratch, nb, out6);
+}
+
+void launch_morton_keys(const double* pts, int64_t n, const double* box6,
+                        unsigned long long* keys, int* idx, cudaStream_t s) {
+  k_morton<<<nblk(n), kT, 0, s>>>(pts, n, box6, keys, idx);
+}
+
+void launch_gather_template(const double* pts, const double* mass, const int* order,
+                            int64_t begin, int64_t count, TemplateView tv, cudaStream_t s) {
+  tv.m = count;
+  if (count <= 0) return;
+  k_gather_tpl<<<nblk(count), kT, 0, s>>>(pts, mass, order, begin, tv);
+}
+
+void launch_gather_queries(const double* q, const double* qm, const int* order, int64_t m,
+                           double* qx, double* qy, double* qz, double* qms, cudaStream_t s) {
+  if (m <= 0) return;
+  k_gather_q<<<nblk(m), kT, 0, s>>>(q, qm, order, m, qx, qy, qz, qms);
+}
+
+}  // namespace fga

@@ -1,0 +1,164 @@
+"""The registration driver (mirrors gravreg/registration.py).
+
+``register`` keeps the reference signature and semantics
+(registration.py:91-166) and runs the whole pipeline in one call into
+libfga (``fga_register``): device normalization, NIV masses + rescale, GPU
+octree build, energy, and the iteration loop -- force pass with the fused
+Euler-Cromer step and Kabsch partial sums, fp64 3x3 SVD update, convergence
+flag on the device -- then the denormalized transform.
+
+B200-side options (extra ``RegisterOptions`` fields, defaults keep reference
+behaviour): ``precision`` ("fp32" fast path / "fp64" reference arithmetic),
+``poll_every`` (iterations enqueued between host polls), ``device``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .core import (
+    FgaParams,
+    IterationRecord,
+    PointCloud,
+    RegistrationResult,
+    RigidTransform,
+    default_params,
+    validate,
+)
+from .errors import DeviceError, EmptyCloud, GravregError
+from .masses import check_weights
+
+# Mass rescale constants (registration.py:41-54); the device applies them in
+# setup.cu (launch_rescale); listed here for API parity.
+FIELD_MASS = 16.0
+FIELD_MASS_POINTS = 2000
+REFERENCE_POINT_CAP = 0.022
+TEMPLATE_PEAK_MASS = 0.1
+
+
+@dataclass
+class RegisterOptions:
+    """Trace and behaviour flags (registration.py:22-31) + device knobs."""
+
+    trace_gpe: bool = False
+    normalize: bool = True
+    x_weights: np.ndarray | None = None
+    y_weights: np.ndarray | None = None
+    record_iterations: bool = False
+    precision: str = "fp32"
+    poll_every: int = 8
+    device: int | None = None
+    compute_gpe: bool = True
+
+
+def _c_options(options: RegisterOptions, xw, yw) -> N.COptions:
+    if options.precision not in ("fp32", "fp64"):
+        raise GravregError(f"precision must be 'fp32' or 'fp64', got {options.precision!r}")
+    return N.COptions(int(bool(options.trace_gpe)), int(bool(options.normalize)),
+                      int(bool(options.record_iterations)),
+                      N.PREC_FP64 if options.precision == "fp64" else N.PREC_FP32,
+                      N.ptr(xw), N.ptr(yw), int(options.poll_every),
+                      int(bool(options.compute_gpe)))
+
+
+def _check_inputs(x, y, landmarks, params, options):
+    validate(params)
+    x.require_nonempty()
+    y.require_nonempty()
+    if x.dim != y.dim:
+        raise EmptyCloud(f"dimension mismatch: {x.dim} vs {y.dim}")
+    if landmarks is not None:
+        landmarks.check_bounds(len(y), len(x))
+        if len(landmarks) > 0:
+            raise DeviceError("landmark (RBF x NIV) mass fields are not built on the B200 path "
+                              "yet; pass external weights via RegisterOptions.x/y_weights")
+    xw = check_weights(len(x), options.x_weights) if options.x_weights is not None else None
+    yw = check_weights(len(y), options.y_weights) if options.y_weights is not None else None
+    return xw, yw
+
+
+def register(x: PointCloud, y: PointCloud, landmarks=None, params: FgaParams | None = None,
+             options: RegisterOptions | None = None) -> RegistrationResult:
+    """Align template ``y`` to reference ``x``; the transform is expressed in
+    the original (unnormalized) frame (registration.py:91-166)."""
+    params = params or default_params()
+    options = options or RegisterOptions()
+    xw, yw = _check_inputs(x, y, landmarks, params, options)
+    c = N.context(options.device)
+    mi = int(params.max_iters)
+    deltas = np.zeros(mi)
+    traj = np.zeros((mi, 3, 4))
+    gtrace = np.zeros(mi)
+    inter = np.zeros(mi, np.int64)
+    res = N.CResult()
+    cp = N.make_params(params)
+    co = _c_options(options, xw, yw)
+    N.check(N.lib().fga_register(c.handle, N.ptr(x.points), len(x), N.ptr(y.points), len(y),
+                                 x.dim, N.ctypes.byref(cp), N.ctypes.byref(co),
+                                 N.ctypes.byref(res), N.ptr(deltas), N.ptr(traj), N.ptr(gtrace),
+                                 N.ptr(inter)))
+    return _result_from_c(res, deltas, traj, gtrace, inter, options)
+
+
+def _result_from_c(res, deltas, traj, gtrace, inter, options) -> RegistrationResult:
+    it = int(res.iterations)
+    R = np.array(res.R).reshape(3, 3)
+    t = np.array(res.t)
+    gpe_trace = [float(v) for v in gtrace[:it]] if options.trace_gpe else []
+    records = []
+    if options.record_iterations:
+        records = [IterationRecord(index=k, transform_delta=float(deltas[k]),
+                                   gpe=gpe_trace[k] if options.trace_gpe else None)
+                   for k in range(it)]
+    compute_gpe = getattr(options, "compute_gpe", True)
+    return RegistrationResult(
+        transform=RigidTransform(R, t),
+        iterations=it,
+        gpe_trace=gpe_trace,
+        converged=bool(res.converged),
+        gpe_initial=float(res.gpe_initial) if compute_gpe else None,
+        gpe_final=float(res.gpe_final) if compute_gpe else None,
+        records=records,
+        trajectory=traj[:it].copy(),
+        interactions=inter[:it].copy(),
+        timings_ms={"setup": float(res.setup_ms), "loop": float(res.loop_ms),
+                    "gpe": float(res.gpe_ms)},
+    )
+
+
+@dataclass
+class SequenceResult:
+    """Pairwise frame transforms plus composed absolute poses
+    (registration.py:169-175)."""
+
+    pairwise: list[RigidTransform]
+    trajectory: list[RigidTransform]
+    failed: list[bool] = field(default_factory=list)
+
+
+def register_sequence(frames, params: FgaParams | None = None,
+                      options: RegisterOptions | None = None) -> SequenceResult:
+    """Frame i (template) onto frame i+1 (reference), pairwise; a failed pair
+    contributes an identity transform (registration.py:178-206)."""
+    frames = list(frames)
+    if len(frames) < 2:
+        raise EmptyCloud("sequence registration needs at least 2 frames")
+    params = params or default_params()
+    pairwise, failed = [], []
+    for i in range(len(frames) - 1):
+        try:
+            pairwise.append(register(x=frames[i + 1], y=frames[i], params=params,
+                                     options=options).transform)
+            failed.append(False)
+        except DeviceError:
+            raise
+        except GravregError:
+            pairwise.append(RigidTransform.identity(frames[i].dim))
+            failed.append(True)
+    poses = [RigidTransform.identity(frames[0].dim)]
+    for tf in pairwise:
+        poses.append(poses[-1].compose(tf.inverse()))
+    return SequenceResult(pairwise=pairwise, trajectory=poses, failed=failed)

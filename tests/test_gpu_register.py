@@ -1,0 +1,124 @@
+"""End-to-end parity of register() (registration.py:91-166) on the CUDA path
+against the reference's golden runs (config-1-shaped pairs) and the oracle.
+GPU only.
+
+Tolerances (north_star): R within 1e-4 rad, t within 1e-4 * scene extent;
+the per-iteration [R_acc|t_acc] trajectory is compared too because a
+one-iteration difference in the stop would move R,t by ~1e-2.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fga():
+    import paper_2009_14005_b200 as f
+    return f
+
+
+def _rot_err(Ra, Rb):
+    c = (np.trace(Ra.T @ Rb) - 1) / 2
+    return float(np.arccos(np.clip(c, -1, 1)))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_register_matches_reference_c1(golden, fga, seed, precision):
+    g = golden("register")
+    k = f"s{seed}/"
+    x, y = fga.PointCloud(g[k + "x"]), fga.PointCloud(g[k + "y"])
+    p = fga.default_params().replace(theta=0.5)
+    res = fga.register(x, y, params=p, options=fga.RegisterOptions(
+        record_iterations=True, precision=precision))
+    assert res.iterations == int(g[k + "iterations"])
+    assert res.converged == bool(g[k + "converged"])
+    traj = g[k + "traj"]
+    tol_traj = 1e-5 if precision == "fp32" else 1e-9
+    assert np.abs(res.trajectory - traj).max() < tol_traj
+    deltas = np.array([r.transform_delta for r in res.records])
+    assert np.allclose(deltas, g[k + "deltas"], rtol=1e-3 if precision == "fp32" else 1e-7,
+                       atol=1e-12)
+    assert _rot_err(res.transform.rotation, g[k + "R"]) < 1e-4
+    extent = np.ptp(g[k + "x"], axis=0).max()
+    assert np.abs(res.transform.translation - g[k + "t"]).max() < 1e-4 * extent
+    gi, gf = float(g[k + "gpe_initial"]), float(g[k + "gpe_final"])
+    assert abs(res.gpe_initial - gi) <= 1e-6 * abs(gi)
+    assert abs(res.gpe_final - gf) <= 1e-6 * abs(gf)
+
+
+def test_register_trace_gpe(golden, fga):
+    g = golden("register")
+    x, y = fga.PointCloud(g["trace/x"]), fga.PointCloud(g["trace/y"])
+    res = fga.register(x, y, options=fga.RegisterOptions(trace_gpe=True, record_iterations=True))
+    assert res.iterations == int(g["trace/iterations"])
+    ref = g["trace/gpe_trace"]
+    assert len(res.gpe_trace) == len(ref) == len(res.records)
+    assert np.allclose(res.gpe_trace, ref, rtol=1e-6, atol=0)
+    assert all(r.gpe == v for r, v in zip(res.records, res.gpe_trace))
+    assert res.gpe_trace[-1] == res.gpe_final
+
+
+def test_register_direct_mode_matches_oracle(orc, fga):
+    """theta = 0: the exact O(NM) direct-sum kernel drives the loop; the
+    reference traverses every leaf, which is the same sum."""
+    from paper_2009_14005_b200 import synth
+    rng = synth.rng_from_seed(41)
+    x = synth.blob(1500, rng)
+    y = synth.misalign(x, synth.random_rigid(rng, np.deg2rad(40), 0.1))
+    res = fga.register(x, y, params=fga.default_params().replace(theta=0.0),
+                       options=fga.RegisterOptions(record_iterations=True))
+    ref = orc.register(x.points, y.points, theta=0.0)
+    assert res.iterations == ref.iterations and res.converged == ref.converged
+    assert np.abs(res.trajectory - np.array(ref.trajectory)).max() < 1e-5
+    assert np.all(res.interactions == 1500 * 1500)
+
+
+def test_register_identity_and_determinism(fga):
+    from paper_2009_14005_b200 import synth
+    x = synth.blob(1000, synth.rng_from_seed(3))
+    a = fga.register(x, x)
+    assert np.abs(a.transform.rotation - np.eye(3)).max() < 1e-6
+    assert np.abs(a.transform.translation).max() < 1e-6
+    y = synth.misalign(x, synth.random_rigid(synth.rng_from_seed(4), 0.5, 0.1))
+    r1 = fga.register(x, y)
+    r2 = fga.register(x, y)
+    assert np.array_equal(r1.transform.rotation, r2.transform.rotation)
+    assert np.array_equal(r1.transform.translation, r2.transform.translation)
+    assert r1.iterations == r2.iterations and r1.gpe_final == r2.gpe_final
+
+
+def test_register_external_weights_and_raw_frame(orc, fga):
+    from paper_2009_14005_b200 import synth
+    rng = synth.rng_from_seed(12)
+    x = synth.blob(800, rng)
+    y = synth.misalign(x, synth.random_rigid(rng, np.deg2rad(20), 0.05))
+    wx = rng.uniform(0.5, 2.0, size=800)
+    wy = rng.uniform(0.5, 2.0, size=800)
+    res = fga.register(x, y, options=fga.RegisterOptions(x_weights=wx, y_weights=wy,
+                                                         record_iterations=True))
+    ref = orc.register(x.points, y.points, x_weights=wx, y_weights=wy)
+    assert res.iterations == ref.iterations
+    assert np.abs(res.trajectory - np.array(ref.trajectory)).max() < 1e-5
+    res2 = fga.register(x, y, options=fga.RegisterOptions(normalize=False,
+                                                          record_iterations=True))
+    ref2 = orc.register(x.points, y.points, normalize=False)
+    assert res2.iterations == ref2.iterations
+    assert np.abs(res2.trajectory - np.array(ref2.trajectory)).max() < 1e-5
+
+
+def test_register_invalid_inputs(fga):
+    x = fga.PointCloud(np.random.default_rng(0).normal(size=(10, 3)))
+    with pytest.raises(fga.InvalidParam) as e:
+        fga.register(x, x, params=fga.default_params().replace(theta=1.5))
+    assert e.value.name == "theta"
+    with pytest.raises(fga.EmptyCloud):
+        fga.register(fga.PointCloud(np.zeros((0, 3))), x)
+    with pytest.raises(fga.DegenerateExtent):
+        fga.register(fga.PointCloud(np.ones((5, 3))), fga.PointCloud(np.ones((5, 3))))
+    with pytest.raises(fga.LengthMismatch):
+        fga.register(x, x, options=fga.RegisterOptions(x_weights=np.ones(3)))
+    with pytest.raises(fga.NonFiniteWeight):
+        fga.register(x, x, options=fga.RegisterOptions(y_weights=np.full(10, np.nan)))
