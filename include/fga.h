@@ -120,6 +120,9 @@ int fga_session_forces(fga_ctx* ctx);
 /* Device pointer to the 18-double sums buffer (layout: see DESIGN.md); a
  * multi-GPU host all-reduces it (sum) between _forces and _update. */
 int fga_session_sums(fga_ctx* ctx, void** dev_ptr);
+/* Use a caller-owned device buffer of >= 18 doubles (e.g. a torch tensor that
+ * torch.distributed all-reduces in place) as the sums buffer. */
+int fga_session_bind_sums(fga_ctx* ctx, void* dev_ptr);
 /* Enqueue the rigid update: 3x3 fp64 SVD, transform accumulation, delta,
  * convergence flag. */
 int fga_session_update(fga_ctx* ctx);
@@ -137,7 +140,8 @@ int fga_session_poll(fga_ctx* ctx, int* done, int64_t* iterations);
  * results out.  With shard_count>1 the caller supplies the all-reduced
  * gpe_final via fga_session_set_gpe_final instead. */
 int fga_session_finish(fga_ctx* ctx, fga_result* out, double* deltas, double* traj,
-                       double* gpe_trace, int64_t* interactions_per_iter);
+                       double* gpe_trace, int64_t* interactions_per_iter,
+                       int64_t* visits_per_iter);
 int fga_session_set_gpe(fga_ctx* ctx, int which /*0 initial,1 final*/, double value);
 /* Number of template points owned by this shard and total tree nodes. */
 int fga_session_info(fga_ctx* ctx, int64_t* m_local, int64_t* n_nodes);

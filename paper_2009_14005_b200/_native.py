@@ -91,13 +91,14 @@ SIGNATURES = {
                                        _c_int]),
     "fga_session_forces": (_c_int, [_vp]),
     "fga_session_sums": (_c_int, [_vp, ctypes.POINTER(_vp)]),
+    "fga_session_bind_sums": (_c_int, [_vp, _vp]),
     "fga_session_update": (_c_int, [_vp]),
     "fga_session_iterate": (_c_int, [_vp, _c_int]),
     "fga_session_gpe": (_c_int, [_vp]),
     "fga_session_take_gpe": (_c_int, [_vp, ctypes.POINTER(_dbl)]),
     "fga_session_apply_pending": (_c_int, [_vp]),
     "fga_session_poll": (_c_int, [_vp, ctypes.POINTER(_c_int), ctypes.POINTER(_i64)]),
-    "fga_session_finish": (_c_int, [_vp, ctypes.POINTER(CResult), _vp, _vp, _vp, _vp]),
+    "fga_session_finish": (_c_int, [_vp, ctypes.POINTER(CResult), _vp, _vp, _vp, _vp, _vp]),
     "fga_session_set_gpe": (_c_int, [_vp, _c_int, _dbl]),
     "fga_session_info": (_c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "fga_tree_build": (_c_int, [_vp, _vp, _vp, _i64, _c_int, _c_int, ctypes.POINTER(_i64)]),

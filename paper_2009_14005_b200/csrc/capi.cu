@@ -55,6 +55,8 @@ struct Session {
     const int64_t ml = m_local;
     return TemplateView{b, b + ml, b + 2 * ml, b + 3 * ml, b + 4 * ml, b + 5 * ml, b + 6 * ml, ml};
   }
+  double* sums_ext = nullptr;  // caller-owned sums buffer (fga_session_bind_sums)
+  double* sums_ptr() const { return sums_ext ? sums_ext : sums.as<double>(); }
   RefPoints ref() const { return RefPoints{ref32.as<float4>(), ref64.as<double4>(), n}; }
   IterState* st() const { return state.as<IterState>(); }
 };
@@ -286,6 +288,7 @@ int session_begin_common(fga_ctx* c, int64_t n, int64_t m, int dim, const fga_pa
   S.applied = false;
   S.passes = 0;
   S.last_pass_gpe = false;
+  S.sums_ext = nullptr;
   return FGA_OK;
 }
 
@@ -296,7 +299,7 @@ int session_gpe(fga_ctx* c, const IterState* gate) {
   launch_gpe(S.ref(), tv.px, tv.py, tv.pz, tv.mq, S.m_local, S.sp.eps, gate, S.gpe_part.as<double>(),
              S.precision, c->stream);
   launch_reduce(S.partials.as<double>(), 0, S.gpe_part.as<double>(), S.m_local > 0 ? ngw : 0, -1.0,
-                S.sums.as<double>(), c->stream);
+                S.sums_ptr(), c->stream);
   FGA_CUDA_TRY(cudaGetLastError());
   return FGA_OK;
 }
@@ -323,7 +326,7 @@ int session_forces(fga_ctx* c) {
   }
   const double pairs = S.direct ? (double)S.n * (double)S.m_local : -1.0;
   launch_reduce(S.partials.as<double>(), nw, S.gpe_part.as<double>(), ngw, pairs,
-                S.sums.as<double>(), s);
+                S.sums_ptr(), s);
   S.last_pass_gpe = with_gpe;
   S.passes++;
   FGA_CUDA_TRY(cudaGetLastError());
@@ -332,7 +335,7 @@ int session_forces(fga_ctx* c) {
 
 int session_update(fga_ctx* c) {
   Session& S = c->S;
-  launch_update(S.sums.as<double>(), S.st(), S.sp, S.rec_delta.as<double>(),
+  launch_update(S.sums_ptr(), S.st(), S.sp, S.rec_delta.as<double>(),
                 S.rec_traj.as<double>(), S.rec_gpe.as<double>(), S.rec_inter.as<long long>(),
                 S.rec_visits.as<long long>(), S.last_pass_gpe ? 1 : 0, c->stream);
   FGA_CUDA_TRY(cudaGetLastError());
@@ -367,7 +370,7 @@ int session_apply(fga_ctx* c) {
 int take_gpe(fga_ctx* c, double* value) {
   Session& S = c->S;
   double v = 0.0;
-  FGA_CUDA_TRY(cudaMemcpyAsync(&v, S.sums.as<double>() + kGpe, sizeof(double), cudaMemcpyDeviceToHost,
+  FGA_CUDA_TRY(cudaMemcpyAsync(&v, S.sums_ptr() + kGpe, sizeof(double), cudaMemcpyDeviceToHost,
                                c->stream));
   FGA_CUDA_TRY(cudaStreamSynchronize(c->stream));
   *value = -S.P.G * v;  // _kernels.py:67
@@ -517,7 +520,12 @@ int fga_session_forces(fga_ctx* c) {
 int fga_session_sums(fga_ctx* c, void** dev_ptr) {
   SESSION_TRY(c);
   if (!dev_ptr) return FGA_ERR_INVALID;
-  *dev_ptr = c->S.sums.p;
+  *dev_ptr = c->S.sums_ptr();
+  return FGA_OK;
+}
+int fga_session_bind_sums(fga_ctx* c, void* dev_ptr) {
+  SESSION_TRY(c);
+  c->S.sums_ext = static_cast<double*>(dev_ptr);
   return FGA_OK;
 }
 int fga_session_update(fga_ctx* c) {
@@ -572,7 +580,7 @@ int fga_session_info(fga_ctx* c, int64_t* m_local, int64_t* n_nodes) {
 }
 
 int fga_session_finish(fga_ctx* c, fga_result* out, double* deltas, double* traj,
-                       double* gpe_trace, int64_t* inter) {
+                       double* gpe_trace, int64_t* inter, int64_t* visits) {
   SESSION_TRY(c);
   Session& S = c->S;
   cudaStream_t s = c->stream;
@@ -605,6 +613,8 @@ int fga_session_finish(fga_ctx* c, fga_result* out, double* deltas, double* traj
   if (gpe_trace && S.O.trace_gpe && iters > 0) gpe_trace[iters - 1] = S.gpe_final;
   if (inter)
     for (int64_t k = 0; k < iters; k++) inter[k] = iv[k];
+  if (visits)
+    for (int64_t k = 0; k < iters; k++) visits[k] = vv[k];
   if (out) {
     std::memset(out, 0, sizeof(*out));
     std::memcpy(out->R, st.Racc, sizeof(st.Racc));
@@ -672,7 +682,7 @@ int fga_register(fga_ctx* c, const double* x, int64_t n, const double* y, int64_
     gpe_ms += ms2;
   }
   S.gpe_ms = gpe_ms;
-  return fga_session_finish(c, out, deltas, traj, gpe_trace, inter);
+  return fga_session_finish(c, out, deltas, traj, gpe_trace, inter, nullptr);
 }
 
 // ------------------------------------------------------------------ tree ops
