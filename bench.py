@@ -140,8 +140,8 @@ def run_ours(args, rank, world, local_rank):
     params = fga.default_params().replace(theta=args.theta, conv_tol=1e-300,
                                           max_iters=W + K + 1)
     opts = fga.RegisterOptions(compute_gpe=False)
-    x_t = torch.from_numpy(np.ascontiguousarray(x.points)).to(dev)
-    y_t = torch.from_numpy(np.ascontiguousarray(y.points)).to(dev)
+    x_t = torch.from_numpy(np.array(x.points)).to(dev)
+    y_t = torch.from_numpy(np.array(y.points)).to(dev)
     stream = torch.cuda.current_stream()
     sess = Session(None, None, params, opts, shard_rank=rank, shard_count=world,
                    device=local_rank, stream=stream.cuda_stream,
@@ -256,8 +256,8 @@ def run_direct(args, x, y, dev, stream, peak, peak_src, fmax):
     from paper_2009_14005_b200.engine import Session
     S = args.direct_steps
     params = fga.default_params().replace(theta=0.0, conv_tol=1e-300, max_iters=S + 2)
-    x_t = torch.from_numpy(np.ascontiguousarray(x.points)).to(dev)
-    y_t = torch.from_numpy(np.ascontiguousarray(y.points)).to(dev)
+    x_t = torch.from_numpy(np.array(x.points)).to(dev)
+    y_t = torch.from_numpy(np.array(y.points)).to(dev)
     sess = Session(None, None, params, fga.RegisterOptions(compute_gpe=False),
                    device=dev.index, stream=stream.cuda_stream,
                    device_inputs=(x_t.data_ptr(), len(x), y_t.data_ptr(), len(y)))

@@ -87,7 +87,8 @@ int fga_device_count(int* count);
 
 int fga_create(fga_ctx** ctx, int device);
 int fga_destroy(fga_ctx* ctx);
-/* Bind the context to a CUDA stream (cudaStream_t as void*; NULL = own stream). */
+/* Bind the context to a CUDA stream (cudaStream_t as void*; NULL = the legacy
+ * default stream).  A new context owns a private non-blocking stream. */
 int fga_set_stream(fga_ctx* ctx, void* stream);
 int fga_synchronize(fga_ctx* ctx);
 

@@ -464,13 +464,8 @@ int fga_set_stream(fga_ctx* c, void* stream) {
     cudaStreamSynchronize(c->stream);
     cudaStreamDestroy(c->stream);
   }
-  if (stream) {
-    c->stream = (cudaStream_t)stream;
-    c->own_stream = false;
-  } else {
-    FGA_CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    c->own_stream = true;
-  }
+  c->stream = (cudaStream_t)stream;  // NULL = the legacy default stream (torch's default)
+  c->own_stream = false;
   return FGA_OK;
 }
 
