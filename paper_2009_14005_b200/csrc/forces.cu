@@ -54,6 +54,12 @@ __device__ __noinline__ bool mac_exact(const double4* __restrict__ A64,
   return B64[node].l2 < __dmul_rn(theta2, d2);
 }
 
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 struct Trav32Out {
   float ax, ay, az;
   int visits, accepted;
@@ -100,7 +106,7 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
       if (acc) {
         o.accepted++;
         const float r2 = d2 + eps2;
-        const float inv = rsqrtf(r2);
+        const float inv = rsqrt_approx(r2);
         float w = a.w * (inv * inv * inv);
         if (!(r2 > 0.f)) w = 0.f;  // reference skips d2+eps2 == 0 (:39)
         o.ax = fmaf(w, dx, o.ax);
@@ -249,7 +255,7 @@ struct WinOf<double> {
 };
 
 template <typename Real>
-__global__ void __launch_bounds__(kForceThreads) k_bh_iterate(TreeRecords tr, int n_nodes,
+__global__ void __launch_bounds__(kForceThreads, 5) k_bh_iterate(TreeRecords tr, int n_nodes,
                                                                TemplateView tv,
                                                                const IterState* __restrict__ st,
                                                                SimParams sp, double* partials,
@@ -397,7 +403,7 @@ __device__ __forceinline__ void direct_tile32(const float4* __restrict__ sm, int
     for (int k = 0; k < QPT; k++) {
       const float dx = s.x - qx[k], dy = s.y - qy[k], dz = s.z - qz[k];
       const float r2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, eps2)));
-      const float inv = rsqrtf(r2);
+      const float inv = rsqrt_approx(r2);
       float w = s.w * inv * inv * inv;
       if (kGuard && !(r2 > 0.f)) w = 0.f;
       ax[k] = fmaf(w, dx, ax[k]);
@@ -424,7 +430,7 @@ __device__ __forceinline__ void direct_tile64(const double4* __restrict__ sm, in
 }
 
 template <bool kGuard>
-__global__ void __launch_bounds__(kForceThreads) k_direct_iterate32(
+__global__ void __launch_bounds__(kForceThreads, 3) k_direct_iterate32(
     const float4* __restrict__ src, int64_t n, TemplateView tv, const IterState* __restrict__ st,
     SimParams sp, double* partials) {
   if (st->done) return;

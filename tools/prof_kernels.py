@@ -1,0 +1,35 @@
+"""Small driver for ncu: one 1M x 1M session, a few iterations of the BH or
+direct force pass (plus the energy kernel).  Not a benchmark (numbers printed
+under a profiler are never reported)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2009_14005_b200 as fga
+from paper_2009_14005_b200 import synth
+from paper_2009_14005_b200.engine import Session
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--mode", default="bh", choices=["bh", "direct", "gpe"])
+ap.add_argument("--n", type=int, default=1_000_000)
+ap.add_argument("--iters", type=int, default=3)
+a = ap.parse_args()
+rng = synth.rng_from_seed(3)
+x = synth.blob(a.n, rng)
+y = synth.misalign(x, synth.random_rigid(rng, np.deg2rad(60), 0.1))
+theta = 0.0 if a.mode == "direct" else 0.5
+p = fga.default_params().replace(theta=theta, conv_tol=1e-300, max_iters=a.iters + 2)
+s = Session(x, y, p, fga.RegisterOptions(compute_gpe=False), stream=0)
+if a.mode == "gpe":
+    for _ in range(a.iters):
+        s.gpe()
+        print("gpe", s.take_gpe())
+else:
+    s.iterate(a.iters)
+r = s.finish()
+torch.cuda.synchronize()
+print("ok", r.iterations, r.interactions, getattr(r, "visits_per_iter", None))
