@@ -21,7 +21,7 @@ struct RefPoints {
 };
 
 constexpr int kForceThreads = 256;
-constexpr int kDirectQPT = 2;  // queries per thread in the FP32 direct sum
+constexpr int kDirectQPT = 4;  // queries per thread in the FP32 direct sum (2 FFMA2 packs)
 
 int64_t bh_iterate_warps(int64_t m);
 int64_t direct_iterate_warps(int64_t m, int precision);

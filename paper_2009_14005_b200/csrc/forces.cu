@@ -66,20 +66,29 @@ struct Trav32Out {
 };
 
 // FP32 warp-coherent traversal.  All 32 lanes must call it (inactive lanes
-// pass active=false).  g0/g1: per-lane fp32 MAC uncertainty model (see
-// guard_coeffs).
+// pass active=false).
+//
+// Exact-MAC guard: with q and com rounded to fp32 (each coordinate off by at
+// most delta = (|q|max + |com|max) * 2^-24) the fp32 d^2 differs from the
+// fp64 one by at most 2*delta*(|dx|+|dy|+|dz|) + 3*delta^2 + 4u*d^2.  When
+// |theta^2 d^2 - l^2| is inside that bound (plus the rounding of l^2 and of
+// theta^2 d^2) the decision is re-made exactly in fp64 from the fp64 records,
+// so the accepted set always equals the reference's (_kernels.py:37).
+// gA = 2*delta*theta^2*1.25, gB = 3*delta^2*theta^2*1.25 (per lane).
+template <bool kGuardZero>
 __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
                                                 const NodeB32* __restrict__ B,
                                                 const double4* __restrict__ A64,
                                                 const NodeB64* __restrict__ B64, int n_nodes,
                                                 float qx, float qy, float qz, bool active,
                                                 float theta2, double theta2_64, float eps2,
-                                                float g0, float g1, const double* qpx,
+                                                float gA, float gB, const double* qpx,
                                                 const double* qpy, const double* qpz, int64_t qi,
                                                 Win32* win, int lane) {
   Trav32Out o{0.f, 0.f, 0.f, 0, 0};
   int cursor = active ? 0 : n_nodes;
   int wbase = INT_MIN / 2;
+  constexpr float kRel = 8.0f * 5.97e-8f;  // 8 unit roundoffs: d^2, theta^2 d^2, l^2
   while (true) {
     const int n = __reduce_min_sync(0xffffffffu, cursor);
     if (n >= n_nodes) break;
@@ -100,7 +109,9 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
       const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
       const float t2d2 = theta2 * d2;
       bool acc = b.l2 < t2d2;
-      if (fabsf(t2d2 - b.l2) <= fmaf(theta2, fmaf(d2, g1, g0), 4.0e-7f * fabsf(b.l2)))
+      const float s1 = fabsf(dx) + fabsf(dy) + fabsf(dz);
+      const float band = fmaf(gA, s1, gB) + kRel * (t2d2 + fabsf(b.l2));
+      if (fabsf(t2d2 - b.l2) <= band)
         acc = mac_exact(A64, B64, n, qpx[qi], qpy[qi], qpz[qi], theta2_64);
       o.visits++;
       if (acc) {
@@ -108,7 +119,7 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
         const float r2 = d2 + eps2;
         const float inv = rsqrt_approx(r2);
         float w = a.w * (inv * inv * inv);
-        if (!(r2 > 0.f)) w = 0.f;  // reference skips d2+eps2 == 0 (:39)
+        if (kGuardZero && !(r2 > 0.f)) w = 0.f;  // reference skips d2+eps2 == 0 (:39)
         o.ax = fmaf(w, dx, o.ax);
         o.ay = fmaf(w, dy, o.ay);
         o.az = fmaf(w, dz, o.az);
@@ -173,12 +184,12 @@ __device__ __forceinline__ Trav64Out traverse64(const double4* __restrict__ A,
   return o;
 }
 
-// Bound on |fp32 d^2 - exact d^2| as g0 + g1*d2 (then scaled by theta^2):
-// coordinates carry <= (|q| + |com|) * 2^-24 rounding each; 2|d| <= d2 + 1.
-__device__ __forceinline__ void guard_coeffs(float qmag, float cmag, float& g0, float& g1) {
-  const float delta = (qmag + cmag) * 1.2e-7f;  // ~2^-23, double the unit roundoff
-  g0 = 4.0f * delta + 8.0f * delta * delta + 1e-30f;
-  g1 = 4.0f * delta + 6.0e-7f;
+// Per-lane guard coefficients (see traverse32).
+__device__ __forceinline__ void guard_coeffs(float qmag, float cmag, float theta2, float& gA,
+                                             float& gB) {
+  const float delta = (qmag + cmag) * 5.97e-8f;
+  gA = 2.5f * delta * theta2;
+  gB = 3.75f * delta * delta * theta2 + 1e-37f;
 }
 
 // ---------------------------------------------------------------- iterate epilogue
@@ -254,12 +265,16 @@ struct WinOf<double> {
   using T = Win64;
 };
 
-template <typename Real>
+struct F32Params {
+  float theta2, eps2;
+};
+
+template <typename Real, bool kGuardZero>
 __global__ void __launch_bounds__(kForceThreads, 5) k_bh_iterate(TreeRecords tr, int n_nodes,
                                                                TemplateView tv,
                                                                const IterState* __restrict__ st,
-                                                               SimParams sp, double* partials,
-                                                               float cmag) {
+                                                               SimParams sp, F32Params f,
+                                                               double* partials, float cmag) {
   if (st->done) return;
   __shared__ typename WinOf<Real>::T wins[kWarps];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -287,11 +302,11 @@ __global__ void __launch_bounds__(kForceThreads, 5) k_bh_iterate(TreeRecords tr,
   int nv, na;
   if constexpr (sizeof(Real) == 4) {
     const float qx = (float)y[0], qy = (float)y[1], qz = (float)y[2];
-    float g0, g1;
-    guard_coeffs(fmaxf(fabsf(qx), fmaxf(fabsf(qy), fabsf(qz))), cmag, g0, g1);
-    Trav32Out o = traverse32(tr.a32, tr.b32, tr.a64, tr.b64, n_nodes, qx, qy, qz, active,
-                             (float)sp.theta2, sp.theta2, (float)sp.eps2, g0, g1, tv.px, tv.py,
-                             tv.pz, i, &wins[wl], lane);
+    float gA, gB;
+    guard_coeffs(fmaxf(fabsf(qx), fmaxf(fabsf(qy), fabsf(qz))), cmag, f.theta2, gA, gB);
+    Trav32Out o = traverse32<kGuardZero>(tr.a32, tr.b32, tr.a64, tr.b64, n_nodes, qx, qy, qz,
+                                         active, f.theta2, sp.theta2, f.eps2, gA, gB, tv.px,
+                                         tv.py, tv.pz, i, &wins[wl], lane);
     const double gq = sp.G * mq;
     F[0] = gq * (double)o.ax;
     F[1] = gq * (double)o.ay;
@@ -335,11 +350,11 @@ __global__ void __launch_bounds__(kForceThreads, 5) k_bh_iterate(TreeRecords tr,
 }
 
 // ---------------------------------------------------------------- BH operator
-template <typename Real>
+template <typename Real, bool kGuardZero>
 __global__ void __launch_bounds__(kForceThreads) k_bh_operator(
     TreeRecords tr, int n_nodes, const double* __restrict__ qx_, const double* __restrict__ qy_,
     const double* __restrict__ qz_, const double* __restrict__ qm_, const int* __restrict__ order,
-    int64_t m, double theta2, double G, double eps2, double* __restrict__ fout,
+    int64_t m, double theta2, double G, double eps2, F32Params f, double* __restrict__ fout,
     long long* __restrict__ visits, long long* __restrict__ accepted, float cmag) {
   __shared__ typename WinOf<Real>::T wins[kWarps];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -356,11 +371,11 @@ __global__ void __launch_bounds__(kForceThreads) k_bh_operator(
   int nv, na;
   if constexpr (sizeof(Real) == 4) {
     const float fx = (float)q[0], fy = (float)q[1], fz = (float)q[2];
-    float g0, g1;
-    guard_coeffs(fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))), cmag, g0, g1);
-    Trav32Out o = traverse32(tr.a32, tr.b32, tr.a64, tr.b64, n_nodes, fx, fy, fz, active,
-                             (float)theta2, theta2, (float)eps2, g0, g1, qx_, qy_, qz_, i,
-                             &wins[wl], lane);
+    float gA, gB;
+    guard_coeffs(fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))), cmag, f.theta2, gA, gB);
+    Trav32Out o = traverse32<kGuardZero>(tr.a32, tr.b32, tr.a64, tr.b64, n_nodes, fx, fy, fz,
+                                         active, f.theta2, theta2, f.eps2, gA, gB, qx_, qy_, qz_,
+                                         i, &wins[wl], lane);
     const double gq = G * qm;
     F[0] = gq * (double)o.ax;
     F[1] = gq * (double)o.ay;
@@ -388,27 +403,76 @@ __global__ void __launch_bounds__(kForceThreads) k_bh_operator(
 // ---------------------------------------------------------------- direct sum
 constexpr int kTile = 1024;
 
-// FP32 tile loop for QPT queries; returns per-tile sums in fp32 which the
-// caller folds into fp64.  kGuard handles eps == 0 (coincident points).
-template <int QPT, bool kGuard>
+// ---- packed FP32x2 arithmetic (sm_100 FFMA2/FADD2/FMUL2): two queries per
+// instruction, which halves the issue slots of the FP32 inner loops (they are
+// issue-bound with scalar FP32: ncu showed 84% issue-slot utilisation at 56%
+// of FP32 peak).  A scalar operand {s, s} becomes the .F32 broadcast form.
+__device__ __forceinline__ float2 sub2s(float s, float2 q) {  // s - q
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%2};\n\tmov.b64 rb, {%3,%4};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(s), "f"(q.x), "f"(q.y));
+  return d;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "mov.b64 rc, {%6,%7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 mul2s(float s, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%2};\n\tmov.b64 rb, {%3,%4};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(s), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 add2s(float2 a, float s) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%4};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(s));
+  return d;
+}
+
+// FP32 tile loop: P packs of 2 queries against jmax staged sources
+// {x, y, z, m}.  Per source and pack: 3 FADD2, 3 FFMA2 (r^2 + eps^2),
+// 2 MUFU.RSQ, 3 FMUL2 (m r^-3), 3 FFMA2 (accumulate) = 20 FLOP per pair in
+// 7 issue slots per pair.  kGuard handles eps == 0 (coincident points).
+template <int P, bool kGuard>
 __device__ __forceinline__ void direct_tile32(const float4* __restrict__ sm, int jmax,
-                                              const float (&qx)[QPT], const float (&qy)[QPT],
-                                              const float (&qz)[QPT], float eps2,
-                                              float (&ax)[QPT], float (&ay)[QPT],
-                                              float (&az)[QPT]) {
+                                              const float2 (&qx)[P], const float2 (&qy)[P],
+                                              const float2 (&qz)[P], float eps2,
+                                              float2 (&ax)[P], float2 (&ay)[P],
+                                              float2 (&az)[P]) {
+  const float2 e2 = make_float2(eps2, eps2);
 #pragma unroll 4
   for (int j = 0; j < jmax; j++) {
     const float4 s = sm[j];
 #pragma unroll
-    for (int k = 0; k < QPT; k++) {
-      const float dx = s.x - qx[k], dy = s.y - qy[k], dz = s.z - qz[k];
-      const float r2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, eps2)));
-      const float inv = rsqrt_approx(r2);
-      float w = s.w * inv * inv * inv;
-      if (kGuard && !(r2 > 0.f)) w = 0.f;
-      ax[k] = fmaf(w, dx, ax[k]);
-      ay[k] = fmaf(w, dy, ay[k]);
-      az[k] = fmaf(w, dz, az[k]);
+    for (int k = 0; k < P; k++) {
+      const float2 dx = sub2s(s.x, qx[k]), dy = sub2s(s.y, qy[k]), dz = sub2s(s.z, qz[k]);
+      const float2 r2 = fma2(dx, dx, fma2(dy, dy, fma2(dz, dz, e2)));
+      float2 inv;
+      inv.x = rsqrt_approx(r2.x);
+      inv.y = rsqrt_approx(r2.y);
+      float2 w = mul2(mul2s(s.w, inv), mul2(inv, inv));
+      if (kGuard) {
+        if (!(r2.x > 0.f)) w.x = 0.f;
+        if (!(r2.y > 0.f)) w.y = 0.f;
+      }
+      ax[k] = fma2(w, dx, ax[k]);
+      ay[k] = fma2(w, dy, ay[k]);
+      az[k] = fma2(w, dz, az[k]);
     }
   }
 }
@@ -432,13 +496,13 @@ __device__ __forceinline__ void direct_tile64(const double4* __restrict__ sm, in
 template <bool kGuard>
 __global__ void __launch_bounds__(kForceThreads, 3) k_direct_iterate32(
     const float4* __restrict__ src, int64_t n, TemplateView tv, const IterState* __restrict__ st,
-    SimParams sp, double* partials) {
+    SimParams sp, float eps2, double* partials) {
   if (st->done) return;
   __shared__ float4 sm[kTile];
-  constexpr int Q = kDirectQPT;
+  constexpr int Q = kDirectQPT, P = Q / 2;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t base = (int64_t)blockIdx.x * (kForceThreads * Q);
-  float qx[Q], qy[Q], qz[Q];
+  float2 qx[P], qy[P], qz[P];
 #pragma unroll
   for (int k = 0; k < Q; k++) {
     const int64_t i = base + threadIdx.x + k * kForceThreads;
@@ -458,28 +522,33 @@ __global__ void __launch_bounds__(kForceThreads, 3) k_direct_iterate32(
       tv.vy[i] = v[1];
       tv.vz[i] = v[2];
     }
-    qx[k] = (float)y[0];
-    qy[k] = (float)y[1];
-    qz[k] = (float)y[2];
+    float* fx = reinterpret_cast<float*>(&qx[k / 2]);
+    float* fy = reinterpret_cast<float*>(&qy[k / 2]);
+    float* fz = reinterpret_cast<float*>(&qz[k / 2]);
+    fx[k % 2] = (float)y[0];
+    fy[k % 2] = (float)y[1];
+    fz[k % 2] = (float)y[2];
   }
   double A[Q][3];
 #pragma unroll
   for (int k = 0; k < Q; k++) A[k][0] = A[k][1] = A[k][2] = 0.0;
-  const float eps2 = (float)sp.eps2;
   for (int64_t t0 = 0; t0 < n; t0 += kTile) {
-    const int jmax = (int)((n - t0) < (int64_t)(kTile) ? (n - t0) : (int64_t)(kTile));
+    const int jmax = (int)((n - t0) < (int64_t)kTile ? (n - t0) : (int64_t)kTile);
     __syncthreads();
     for (int j = threadIdx.x; j < jmax; j += kForceThreads) sm[j] = __ldg(&src[t0 + j]);
     __syncthreads();
-    float ax[Q], ay[Q], az[Q];
+    float2 ax[P], ay[P], az[P];
 #pragma unroll
-    for (int k = 0; k < Q; k++) ax[k] = ay[k] = az[k] = 0.f;
-    direct_tile32<Q, kGuard>(sm, jmax, qx, qy, qz, eps2, ax, ay, az);
+    for (int k = 0; k < P; k++) ax[k] = ay[k] = az[k] = make_float2(0.f, 0.f);
+    direct_tile32<P, kGuard>(sm, jmax, qx, qy, qz, eps2, ax, ay, az);
 #pragma unroll
-    for (int k = 0; k < Q; k++) {
-      A[k][0] += (double)ax[k];
-      A[k][1] += (double)ay[k];
-      A[k][2] += (double)az[k];
+    for (int k = 0; k < P; k++) {
+      A[2 * k][0] += (double)ax[k].x;
+      A[2 * k][1] += (double)ay[k].x;
+      A[2 * k][2] += (double)az[k].x;
+      A[2 * k + 1][0] += (double)ax[k].y;
+      A[2 * k + 1][1] += (double)ay[k].y;
+      A[2 * k + 1][2] += (double)az[k].y;
     }
   }
   Partial p;
@@ -551,38 +620,41 @@ __global__ void __launch_bounds__(kForceThreads) k_direct_iterate64(
 }
 
 template <bool kGuard>
-__global__ void __launch_bounds__(kForceThreads) k_direct_operator32(
+__global__ void __launch_bounds__(kForceThreads, 3) k_direct_operator32(
     const float4* __restrict__ src, int64_t n, const double* __restrict__ qx_,
     const double* __restrict__ qy_, const double* __restrict__ qz_, const double* __restrict__ qm_,
     int64_t m, double G, float eps2, double* __restrict__ fout) {
   __shared__ float4 sm[kTile];
-  constexpr int Q = kDirectQPT;
+  constexpr int Q = kDirectQPT, P = Q / 2;
   const int64_t base = (int64_t)blockIdx.x * (kForceThreads * Q);
-  float qx[Q], qy[Q], qz[Q];
+  float2 qx[P], qy[P], qz[P];
 #pragma unroll
   for (int k = 0; k < Q; k++) {
     const int64_t i = base + threadIdx.x + k * kForceThreads;
-    qx[k] = i < m ? (float)qx_[i] : 0.f;
-    qy[k] = i < m ? (float)qy_[i] : 0.f;
-    qz[k] = i < m ? (float)qz_[i] : 0.f;
+    reinterpret_cast<float*>(&qx[k / 2])[k % 2] = i < m ? (float)qx_[i] : 0.f;
+    reinterpret_cast<float*>(&qy[k / 2])[k % 2] = i < m ? (float)qy_[i] : 0.f;
+    reinterpret_cast<float*>(&qz[k / 2])[k % 2] = i < m ? (float)qz_[i] : 0.f;
   }
   double A[Q][3];
 #pragma unroll
   for (int k = 0; k < Q; k++) A[k][0] = A[k][1] = A[k][2] = 0.0;
   for (int64_t t0 = 0; t0 < n; t0 += kTile) {
-    const int jmax = (int)((n - t0) < (int64_t)(kTile) ? (n - t0) : (int64_t)(kTile));
+    const int jmax = (int)((n - t0) < (int64_t)kTile ? (n - t0) : (int64_t)kTile);
     __syncthreads();
     for (int j = threadIdx.x; j < jmax; j += kForceThreads) sm[j] = __ldg(&src[t0 + j]);
     __syncthreads();
-    float ax[Q], ay[Q], az[Q];
+    float2 ax[P], ay[P], az[P];
 #pragma unroll
-    for (int k = 0; k < Q; k++) ax[k] = ay[k] = az[k] = 0.f;
-    direct_tile32<Q, kGuard>(sm, jmax, qx, qy, qz, eps2, ax, ay, az);
+    for (int k = 0; k < P; k++) ax[k] = ay[k] = az[k] = make_float2(0.f, 0.f);
+    direct_tile32<P, kGuard>(sm, jmax, qx, qy, qz, eps2, ax, ay, az);
 #pragma unroll
-    for (int k = 0; k < Q; k++) {
-      A[k][0] += (double)ax[k];
-      A[k][1] += (double)ay[k];
-      A[k][2] += (double)az[k];
+    for (int k = 0; k < P; k++) {
+      A[2 * k][0] += (double)ax[k].x;
+      A[2 * k][1] += (double)ay[k].x;
+      A[2 * k][2] += (double)az[k].x;
+      A[2 * k + 1][0] += (double)ax[k].y;
+      A[2 * k + 1][1] += (double)ay[k].y;
+      A[2 * k + 1][2] += (double)az[k].y;
     }
   }
 #pragma unroll
@@ -733,12 +805,19 @@ void launch_bh_iterate(const TreeDev& T, const TemplateView& tv, const IterState
                        const SimParams& sp, double* partials, int precision, cudaStream_t s) {
   if (tv.m <= 0) return;
   const unsigned g = grid_for(tv.m, kForceThreads);
+  const F32Params f{(float)sp.theta2, (float)sp.eps2};
+  const bool gz = !(sp.eps2 > 0.0);
+  const int nn = (int)T.n_nodes;
+  const float cm = (float)T.cmag;
   if (precision)
-    k_bh_iterate<double><<<g, kForceThreads, 0, s>>>(T.records(), (int)T.n_nodes, tv, st, sp,
-                                                     partials, (float)T.cmag);
+    k_bh_iterate<double, false><<<g, kForceThreads, 0, s>>>(T.records(), nn, tv, st, sp, f,
+                                                            partials, cm);
+  else if (gz)
+    k_bh_iterate<float, true><<<g, kForceThreads, 0, s>>>(T.records(), nn, tv, st, sp, f,
+                                                          partials, cm);
   else
-    k_bh_iterate<float><<<g, kForceThreads, 0, s>>>(T.records(), (int)T.n_nodes, tv, st, sp,
-                                                    partials, (float)T.cmag);
+    k_bh_iterate<float, false><<<g, kForceThreads, 0, s>>>(T.records(), nn, tv, st, sp, f,
+                                                           partials, cm);
 }
 
 void launch_direct_iterate(const RefPoints& ref, const TemplateView& tv, const IterState* st,
@@ -750,9 +829,9 @@ void launch_direct_iterate(const RefPoints& ref, const TemplateView& tv, const I
   } else {
     const unsigned g = grid_for(tv.m, kForceThreads * kDirectQPT);
     if (sp.eps2 > 0.0)
-      k_direct_iterate32<false><<<g, kForceThreads, 0, s>>>(ref.p32, ref.n, tv, st, sp, partials);
+      k_direct_iterate32<false><<<g, kForceThreads, 0, s>>>(ref.p32, ref.n, tv, st, sp, (float)sp.eps2, partials);
     else
-      k_direct_iterate32<true><<<g, kForceThreads, 0, s>>>(ref.p32, ref.n, tv, st, sp, partials);
+      k_direct_iterate32<true><<<g, kForceThreads, 0, s>>>(ref.p32, ref.n, tv, st, sp, (float)sp.eps2, partials);
   }
 }
 
@@ -775,14 +854,21 @@ void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, co
   if (m <= 0) return;
   const unsigned g = grid_for(m, kForceThreads);
   const double theta2 = theta * theta;
+  const F32Params f{(float)theta2, (float)eps2};
+  const int nn = (int)T.n_nodes;
+  const float cm = (float)T.cmag;
   if (precision)
-    k_bh_operator<double><<<g, kForceThreads, 0, s>>>(T.records(), (int)T.n_nodes, qx, qy, qz, qm,
-                                                      order, m, theta2, G, eps2, fout, visits,
-                                                      accepted, (float)T.cmag);
+    k_bh_operator<double, false><<<g, kForceThreads, 0, s>>>(T.records(), nn, qx, qy, qz, qm,
+                                                             order, m, theta2, G, eps2, f, fout,
+                                                             visits, accepted, cm);
+  else if (!(eps2 > 0.0))
+    k_bh_operator<float, true><<<g, kForceThreads, 0, s>>>(T.records(), nn, qx, qy, qz, qm,
+                                                           order, m, theta2, G, eps2, f, fout,
+                                                           visits, accepted, cm);
   else
-    k_bh_operator<float><<<g, kForceThreads, 0, s>>>(T.records(), (int)T.n_nodes, qx, qy, qz, qm,
-                                                     order, m, theta2, G, eps2, fout, visits,
-                                                     accepted, (float)T.cmag);
+    k_bh_operator<float, false><<<g, kForceThreads, 0, s>>>(T.records(), nn, qx, qy, qz, qm,
+                                                            order, m, theta2, G, eps2, f, fout,
+                                                            visits, accepted, cm);
 }
 
 void launch_direct_operator(const RefPoints& ref, const double* qx, const double* qy,
