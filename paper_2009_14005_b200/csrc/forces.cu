@@ -66,7 +66,10 @@ struct Trav32Out {
 };
 
 // FP32 warp-coherent traversal.  All 32 lanes must call it (inactive lanes
-// pass active=false).
+// pass active=false).  Branch-free step: every lane evaluates the node at the
+// warp-minimum cursor and the results are committed only on the lanes whose
+// cursor is that node (SIMT issues the instructions once per warp either way,
+// so predication is cheaper than divergent branches + reconvergence).
 //
 // Exact-MAC guard: with q and com rounded to fp32 (each coordinate off by at
 // most delta = (|q|max + |com|max) * 2^-24) the fp32 d^2 differs from the
@@ -75,6 +78,14 @@ struct Trav32Out {
 // theta^2 d^2) the decision is re-made exactly in fp64 from the fp64 records,
 // so the accepted set always equals the reference's (_kernels.py:37).
 // gA = 2*delta*theta^2*1.25, gB = 3*delta^2*theta^2*1.25 (per lane).
+struct WinRec32 {
+  float4 a;  // com.xyz, mass
+  float4 b;  // l2 | -inf, skip (int bits), unused, unused
+};
+struct WinBuf32 {
+  WinRec32 r[kWin];
+};
+
 template <bool kGuardZero>
 __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
                                                 const NodeB32* __restrict__ B,
@@ -84,8 +95,9 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
                                                 float theta2, double theta2_64, float eps2,
                                                 float gA, float gB, const double* qpx,
                                                 const double* qpy, const double* qpz, int64_t qi,
-                                                Win32* win, int lane) {
-  Trav32Out o{0.f, 0.f, 0.f, 0, 0};
+                                                WinBuf32* win, int lane) {
+  float ax = 0.f, ay = 0.f, az = 0.f;
+  int visits = 0, accepted = 0;
   int cursor = active ? 0 : n_nodes;
   int wbase = INT_MIN / 2;
   constexpr float kRel = 8.0f * 5.97e-8f;  // 8 unit roundoffs: d^2, theta^2 d^2, l^2
@@ -97,39 +109,44 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
       __syncwarp();
       const int j = n + lane;
       if (j < n_nodes) {
-        win->a[lane] = __ldg(&A[j]);
-        win->b[lane] = B[j];
+        const float4 a = __ldg(&A[j]);
+        const NodeB32 b = B[j];
+        win->r[lane].a = a;
+        win->r[lane].b = make_float4(b.l2, __int_as_float(b.skip),
+                                     b.l2 > -INFINITY ? 4.776e-7f * fabsf(b.l2) : 0.f, 0.f);
       }
       __syncwarp();
     }
-    if (cursor == n) {
-      const float4 a = win->a[n - wbase];
-      const NodeB32 b = win->b[n - wbase];
-      const float dx = a.x - qx, dy = a.y - qy, dz = a.z - qz;
-      const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-      const float t2d2 = theta2 * d2;
-      bool acc = b.l2 < t2d2;
-      const float s1 = fabsf(dx) + fabsf(dy) + fabsf(dz);
-      const float band = fmaf(gA, s1, gB) + kRel * (t2d2 + fabsf(b.l2));
-      if (fabsf(t2d2 - b.l2) <= band)
-        acc = mac_exact(A64, B64, n, qpx[qi], qpy[qi], qpz[qi], theta2_64);
-      o.visits++;
-      if (acc) {
-        o.accepted++;
-        const float r2 = d2 + eps2;
-        const float inv = rsqrt_approx(r2);
-        float w = a.w * (inv * inv * inv);
-        if (kGuardZero && !(r2 > 0.f)) w = 0.f;  // reference skips d2+eps2 == 0 (:39)
-        o.ax = fmaf(w, dx, o.ax);
-        o.ay = fmaf(w, dy, o.ay);
-        o.az = fmaf(w, dz, o.az);
-        cursor = b.skip;
-      } else {
-        cursor = n + 1;
-      }
+    const WinRec32& rec = win->r[n - wbase];
+    const float4 a = rec.a;
+    const float4 b = rec.b;
+    const bool mine = cursor == n;
+    const float dx = a.x - qx, dy = a.y - qy, dz = a.z - qz;
+    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float t2d2 = theta2 * d2;
+    bool acc = b.x < t2d2;
+    const float s1 = fabsf(dx) + fabsf(dy) + fabsf(dz);
+    const float band = fmaf(gA, s1, fmaf(kRel, t2d2, b.z));  // b.z = gB-free kRel*|l2|
+    const bool near = mine && fabsf(t2d2 - b.x) <= band + gB;
+    if (__any_sync(0xffffffffu, near)) {  // warp-uniform branch, rarely taken
+      if (near) acc = mac_exact(A64, B64, n, qpx[qi], qpy[qi], qpz[qi], theta2_64);
     }
+    const bool take = mine && acc;
+    const float r2 = d2 + eps2;
+    const float inv = rsqrt_approx(r2);
+    float w = a.w * (inv * inv * inv);
+    if (!take) w = 0.f;
+    if (kGuardZero && !(r2 > 0.f)) w = 0.f;  // reference skips d2+eps2 == 0 (:39)
+    ax = fmaf(w, dx, ax);
+    ay = fmaf(w, dy, ay);
+    az = fmaf(w, dz, az);
+    asm("{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %2, 0;\n\tsetp.ne.b32 q, %3, 0;\n\t"
+        "@p add.s32 %0, %0, 1;\n\t@q add.s32 %1, %1, 1;\n\t}"
+        : "+r"(visits), "+r"(accepted) : "r"((int)mine), "r"((int)take));
+    const int next = acc ? __float_as_int(b.y) : n + 1;
+    cursor = mine ? next : cursor;
   }
-  return o;
+  return Trav32Out{ax, ay, az, visits, accepted};
 }
 
 struct Trav64Out {
@@ -258,7 +275,7 @@ template <typename Real>
 struct WinOf;
 template <>
 struct WinOf<float> {
-  using T = Win32;
+  using T = WinBuf32;
 };
 template <>
 struct WinOf<double> {
@@ -270,7 +287,7 @@ struct F32Params {
 };
 
 template <typename Real, bool kGuardZero>
-__global__ void __launch_bounds__(kForceThreads, 5) k_bh_iterate(TreeRecords tr, int n_nodes,
+__global__ void __launch_bounds__(kForceThreads, 4) k_bh_iterate(TreeRecords tr, int n_nodes,
                                                                TemplateView tv,
                                                                const IterState* __restrict__ st,
                                                                SimParams sp, F32Params f,
