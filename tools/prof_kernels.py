@@ -14,10 +14,14 @@ from paper_2009_14005_b200 import synth
 from paper_2009_14005_b200.engine import Session
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--mode", default="bh", choices=["bh", "direct", "gpe"])
+ap.add_argument("--mode", default="bh", choices=["bh", "direct", "gpe", "all"])
 ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--iters", type=int, default=3)
 a = ap.parse_args()
+if a.mode == "all":
+    for m in ("bh", "direct", "gpe"):
+        os.system(f"{sys.executable} {__file__} --mode {m} --n {a.n} --iters {a.iters}")
+    sys.exit(0)
 rng = synth.rng_from_seed(3)
 x = synth.blob(a.n, rng)
 y = synth.misalign(x, synth.random_rigid(rng, np.deg2rad(60), 0.1))
