@@ -719,49 +719,100 @@ __device__ __forceinline__ float sqrt_approx(float x) {
   return r;
 }
 
-__global__ void __launch_bounds__(kForceThreads) k_gpe32(const float4* __restrict__ src, int64_t n,
-                                                         const double* __restrict__ px,
-                                                         const double* __restrict__ py,
-                                                         const double* __restrict__ pz,
-                                                         const double* __restrict__ mq, int64_t m,
-                                                         float eps, const IterState* st,
-                                                         double* partials) {
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 fma2s(float s, float2 b, float2 c) {  // s*b + c
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2,%2};\n\tmov.b64 rb, {%3,%4};\n\t"
+      "mov.b64 rc, {%5,%6};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y) : "f"(s), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
+// K11 energy.  Per pair: |y - x| (MUFU.SQRT) and 1/(|y - x| + eps).  The two
+// MUFU ops per pair make the scalar kernel MUFU-bound (16/clk/SM), so half of
+// the pairs (pack 1) compute the reciprocal on the FMA pipe instead: a
+// bit-trick seed and three Newton steps on w = -1/x (w' = w (2 + x w), error
+// 0.125^8 ~ 6e-8), in packed FP32x2 arithmetic.  FP32 within a tile, fp64
+// across tiles and across queries (<= 1e-6 relative, tested).
+template <bool kNewton>
+__global__ void __launch_bounds__(kForceThreads, 3) k_gpe32(const float4* __restrict__ src,
+                                                            int64_t n,
+                                                            const double* __restrict__ px,
+                                                            const double* __restrict__ py,
+                                                            const double* __restrict__ pz,
+                                                            const double* __restrict__ mq,
+                                                            int64_t m, float eps,
+                                                            const IterState* st,
+                                                            double* partials) {
   if (st && st->done) return;
   __shared__ float4 sm[kTile];
-  constexpr int Q = kDirectQPT;
+  constexpr int Q = kDirectQPT;  // 4 queries = pack 0 (MUFU) + pack 1 (Newton)
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t base = (int64_t)blockIdx.x * (kForceThreads * Q);
-  float qx[Q], qy[Q], qz[Q];
+  float2 qx[2], qy[2], qz[2];
 #pragma unroll
   for (int k = 0; k < Q; k++) {
     const int64_t i = base + threadIdx.x + k * kForceThreads;
-    qx[k] = i < m ? (float)px[i] : 0.f;
-    qy[k] = i < m ? (float)py[i] : 0.f;
-    qz[k] = i < m ? (float)pz[i] : 0.f;
+    reinterpret_cast<float*>(&qx[k / 2])[k % 2] = i < m ? (float)px[i] : 0.f;
+    reinterpret_cast<float*>(&qy[k / 2])[k % 2] = i < m ? (float)py[i] : 0.f;
+    reinterpret_cast<float*>(&qz[k / 2])[k % 2] = i < m ? (float)pz[i] : 0.f;
   }
   double acc[Q];
 #pragma unroll
   for (int k = 0; k < Q; k++) acc[k] = 0.0;
+  const float2 e2 = make_float2(eps, eps);
+  const float2 two = make_float2(2.f, 2.f);
   for (int64_t t0 = 0; t0 < n; t0 += kTile) {
-    const int jmax = (int)((n - t0) < (int64_t)(kTile) ? (n - t0) : (int64_t)(kTile));
+    const int jmax = (int)((n - t0) < (int64_t)kTile ? (n - t0) : (int64_t)kTile);
     __syncthreads();
     for (int j = threadIdx.x; j < jmax; j += kForceThreads) sm[j] = __ldg(&src[t0 + j]);
     __syncthreads();
-    float a[Q];
-#pragma unroll
-    for (int k = 0; k < Q; k++) a[k] = 0.f;
+    float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
 #pragma unroll 4
     for (int j = 0; j < jmax; j++) {
       const float4 s = sm[j];
+      {  // pack 0: MUFU reciprocal
+        const float2 dx = sub2s(s.x, qx[0]), dy = sub2s(s.y, qy[0]), dz = sub2s(s.z, qz[0]);
+        const float2 d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+        float2 den;
+        den.x = sqrt_approx(d2.x);
+        den.y = sqrt_approx(d2.y);
+        den = add2(den, e2);
+        float2 r;
+        r.x = rcp_approx(den.x);
+        r.y = rcp_approx(den.y);
+        a0 = fma2s(s.w, r, a0);
+      }
+      {  // pack 1: Newton reciprocal (accumulates -m/x)
+        const float2 dx = sub2s(s.x, qx[1]), dy = sub2s(s.y, qy[1]), dz = sub2s(s.z, qz[1]);
+        const float2 d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+        float2 den;
+        den.x = sqrt_approx(d2.x);
+        den.y = sqrt_approx(d2.y);
+        den = add2(den, e2);
+        float2 w;
+        if (kNewton) {
+          w.x = __int_as_float(0xFEF311C3u - __float_as_uint(den.x));
+          w.y = __int_as_float(0xFEF311C3u - __float_as_uint(den.y));
 #pragma unroll
-      for (int k = 0; k < Q; k++) {
-        const float dx = s.x - qx[k], dy = s.y - qy[k], dz = s.z - qz[k];
-        const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        a[k] = fmaf(s.w, rcp_approx(sqrt_approx(d2) + eps), a[k]);
+          for (int it = 0; it < 3; it++) w = mul2(w, fma2(den, w, two));
+        } else {
+          w.x = -rcp_approx(den.x);
+          w.y = -rcp_approx(den.y);
+        }
+        a1 = fma2s(s.w, w, a1);
       }
     }
-#pragma unroll
-    for (int k = 0; k < Q; k++) acc[k] += (double)a[k];
+    acc[0] += (double)a0.x;
+    acc[1] += (double)a0.y;
+    acc[2] -= (double)a1.x;
+    acc[3] -= (double)a1.y;
   }
   double tot = 0.0;
 #pragma unroll
@@ -859,8 +910,11 @@ void launch_gpe(const RefPoints& ref, const double* px, const double* py, const 
   if (precision)
     k_gpe64<<<grid_for(m, kForceThreads), kForceThreads, 0, s>>>(ref.p64, ref.n, px, py, pz, mq, m,
                                                                  eps, st, partials);
-  else
-    k_gpe32<<<grid_for(m, kForceThreads * kDirectQPT), kForceThreads, 0, s>>>(
+  else if (eps > 0.0)
+    k_gpe32<true><<<grid_for(m, kForceThreads * kDirectQPT), kForceThreads, 0, s>>>(
+        ref.p32, ref.n, px, py, pz, mq, m, (float)eps, st, partials);
+  else  // eps == 0: keep IEEE rcp semantics (1/0 = inf) on every pair
+    k_gpe32<false><<<grid_for(m, kForceThreads * kDirectQPT), kForceThreads, 0, s>>>(
         ref.p32, ref.n, px, py, pz, mq, m, (float)eps, st, partials);
 }
 

@@ -19,26 +19,52 @@ namespace {
 constexpr int kT = 256;
 inline unsigned nblk(int64_t n, int t = kT) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
 
-// numpy mean(axis=0): sequential accumulation over rows, then / n.
-// thread k<3 handles x column k, thread 3+k handles y column k.
-__global__ void k_colmean_seq(const double* __restrict__ x, int64_t n, const double* __restrict__ y,
-                              int64_t m, double* __restrict__ out6) {
-  const int t = threadIdx.x;
-  if (t >= 6) return;
-  const double* p = t < 3 ? x : y;
-  const int64_t cnt = t < 3 ? n : m;
-  const int k = t % 3;
+// numpy mean(axis=0): sequential accumulation over rows, then / n.  One warp
+// per column (x0, x1, x2, y0, y1, y2): the warp streams 256-row chunks of its
+// column into shared memory with cp.async (double-buffered) while lane 0 adds
+// the previous chunk in row order, so the serial fp64 add chain -- which IS
+// numpy's rounding order -- runs at DADD latency instead of load latency.
+constexpr int kColChunk = 256;
+__global__ void __launch_bounds__(192) k_colmean_seq(const double* __restrict__ x, int64_t n,
+                                                     const double* __restrict__ y, int64_t m,
+                                                     double* __restrict__ out6) {
+  __shared__ double buf[6][2][kColChunk];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* p = w < 3 ? x : y;
+  const int64_t cnt = w < 3 ? n : m;
+  const int k = w % 3;
+  const int64_t nch = (cnt + kColChunk - 1) / kColChunk;
+  auto issue = [&](int64_t c) {
+    const int64_t r0 = c * kColChunk;
+    double* dst = buf[w][c & 1];
+    for (int j = lane; j < kColChunk; j += 32) {
+      const int64_t r = r0 + j;
+      if (r < cnt) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + j);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(p + r * 3 + k));
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
   double s = 0.0;
-  int64_t i = 0;
-  for (; i + 8 <= cnt; i += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; u++) v[u] = p[(i + u) * 3 + k];
-#pragma unroll
-    for (int u = 0; u < 8; u++) s = __dadd_rn(s, v[u]);
+  if (nch > 0) issue(0);
+  for (int64_t c = 0; c < nch; c++) {
+    if (c + 1 < nch) {
+      issue(c + 1);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const double* b = buf[w][c & 1];
+      const int64_t rem = cnt - c * kColChunk;
+      const int len = rem < kColChunk ? (int)rem : kColChunk;
+      for (int j = 0; j < len; j++) s = __dadd_rn(s, b[j]);
+    }
+    __syncwarp();
   }
-  for (; i < cnt; i++) s = __dadd_rn(s, p[i * 3 + k]);
-  out6[t] = __ddiv_rn(s, (double)cnt);
+  if (lane == 0) out6[w] = __ddiv_rn(s, (double)cnt);
 }
 
 // min/max over all centred coordinates of both clouds (scalar l, r).
@@ -339,7 +365,7 @@ int normalize_pair_dev(const double* x, int64_t n, const double* y, int64_t m, d
   double* mean6 = scratch;
   double* part = scratch + 8;
   const int nb = (int)std::min<int64_t>(nblk((n + m) * 3), 592);
-  k_colmean_seq<<<1, 32, 0, s>>>(x, n, y, m, mean6);
+  k_colmean_seq<<<1, 192, 0, s>>>(x, n, y, m, mean6);
   k_centred_minmax<<<nb, kT, 0, s>>>(x, n, y, m, mean6, part);
   k_norm_ctx<<<1, 32, 0, s>>>(part, nb, mean6, a, b, ctx10_dev);
   FGA_CUDA_TRY(cudaMemcpyAsync(ctx10_host, ctx10_dev, sizeof(double) * 10, cudaMemcpyDeviceToHost, s));

@@ -30,13 +30,13 @@ class Session:
     def __init__(self, x, y, params: FgaParams | None = None,
                  options: RegisterOptions | None = None, shard_rank: int = 0,
                  shard_count: int = 1, device: int | None = None, stream: int | None = None,
-                 device_inputs: tuple | None = None):
+                 device_inputs: tuple | None = None, ctx: N.Context | None = None):
         """x, y: PointCloud (host) -- or ``device_inputs=(x_ptr, n, y_ptr, m)``
         for (n,3)/(m,3) fp64 arrays already resident on the device."""
         self.params = params or default_params()
         self.options = options or RegisterOptions()
         validate(self.params)
-        self.ctx = N.context(device if device is not None else self.options.device)
+        self.ctx = ctx or N.context(device if device is not None else self.options.device)
         if stream is not None:
             self.ctx.set_stream(stream)
         self._cp = N.make_params(self.params)
