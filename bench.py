@@ -54,7 +54,23 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--direct-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=65536)
+    ap.add_argument("--default-g", action="store_true",
+                    help="keep G=66.7 (diverges at 1M, SURVEY §0.11) instead of the "
+                         "converging G*sqrt(2000/N)")
     return ap.parse_args()
+
+
+def bench_params(args):
+    """BASELINE configs[2] parameters: theta=0.5; G scaled by sqrt(2000/N) so
+    the 1M registration converges (the reference's field
+    mass grows as sqrt(N) while G stays fixed, which makes the default run
+    fly apart above ~50k points).  The scaling is a user-level parameter
+    applied identically to every arm."""
+    import paper_2009_14005_b200 as fga
+    p = fga.default_params().replace(theta=args.theta)
+    if not args.default_g:
+        p = p.replace(G=66.7 * (2000.0 / args.n) ** 0.5)
+    return p
 
 
 def workload(n, seed):
@@ -137,8 +153,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     x, y = workload(args.n, args.seed)
     K, W = args.steps, args.warmup
-    params = fga.default_params().replace(theta=args.theta, conv_tol=1e-300,
-                                          max_iters=W + K + 1)
+    params = bench_params(args).replace(conv_tol=1e-300, max_iters=W + K + 1)
     opts = fga.RegisterOptions(compute_gpe=False)
     x_t = torch.from_numpy(np.array(x.points)).to(dev)
     y_t = torch.from_numpy(np.array(y.points)).to(dev)
@@ -208,6 +223,7 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": "configs[2]: 1M x 1M FGA pair, Barnes-Hut theta=%g, fixed "
                                "iteration budget" % args.theta,
                    "n_reference": len(x), "n_template": len(y), "theta": args.theta,
+                   "G": params.G,
                    "tree_nodes": sess.n_nodes, "parallelism": f"template-shard x{world}",
                    "l2": "flushed between timed steps (256 MiB write, outside the events)"},
         "gpu_launches": 3 * K,
@@ -293,7 +309,7 @@ def run_e2e(args, x, y, sess):
     from paper_2009_14005_b200 import _native as N
     xn, yn, ctx = fga.normalize_pair(x, y, -5.0, 5.0)
     sy = fga.niv_masses(yn, 16, ctx, 20)
-    p = fga.default_params()
+    p = bench_params(args)
     qm_np = np.maximum(0.1 * sy / sy.max(), max(1e-6, p.dt * p.eta))  # registration.py:87
     m = len(yn)
 
@@ -334,15 +350,17 @@ def run_e2e(args, x, y, sess):
 
 def run_registration(args, x, y):
     import paper_2009_14005_b200 as fga
-    p = fga.default_params().replace(theta=args.theta)
+    p = bench_params(args)
     fga.register(fga.PointCloud(x.points[:5000]), fga.PointCloud(y.points[:5000]), params=p)
     t0 = time.perf_counter()
     r = fga.register(x, y, params=p)
     wall = time.perf_counter() - t0
     return {"wall_s": wall, "iterations": r.iterations, "converged": r.converged,
             "interactions": int(r.interactions.sum()), "timings_ms": r.timings_ms,
-            "api": "register(x, y) from host numpy, default params except theta; includes "
-                   "normalize, NIV masses, tree build, 2x O(NM) energy, iteration budget"}
+            "params": {"theta": p.theta, "G": p.G, "max_iters": p.max_iters,
+                       "conv_tol": p.conv_tol},
+            "api": "register(x, y) from host numpy; includes normalize, NIV masses, tree "
+                   "build, 2x O(NM) energy and the iteration loop"}
 
 
 # --------------------------------------------------------------------------- CPU
@@ -352,7 +370,8 @@ def cpu_baseline(args, x, y, sample):
     template queries at the initial state."""
     from oracle import oracle as orc
     orc.build_lib()
-    p = {"G": 66.7, "eps": 0.2}
+    bp = bench_params(args)
+    p = {"G": bp.G, "eps": 0.2}
     xn, yn, ctx = orc.normalize_pair(x.points, y.points, -5.0, 5.0)
     sx = orc.niv_masses(xn, 16, -5.0, 5.0, 20)
     sy = orc.niv_masses(yn, 16, -5.0, 5.0, 20)
@@ -386,13 +405,14 @@ def run_reference(args, rank):
     mx, my = orc.rescale(sx, sy, 0.1, 0.2)
     tree = orc.tree_build(xn, mx, 20)
     threads = orc.max_threads()
+    G = 66.7 if args.default_g else 66.7 * (2000.0 / args.n) ** 0.5
     sample = min(16384, len(yn))
     rng = np.random.default_rng(1)
 
     def step():
         idx = rng.choice(len(yn), size=sample, replace=False)
         t0 = time.perf_counter()
-        _, _, acc = orc.bh_forces(tree, yn[idx], my[idx], args.theta, 66.7, 0.2, threads)
+        _, _, acc = orc.bh_forces(tree, yn[idx], my[idx], args.theta, G, 0.2, threads)
         return float(acc.sum()), time.perf_counter() - t0
 
     for _ in range(args.warmup):

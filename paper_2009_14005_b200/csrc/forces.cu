@@ -26,6 +26,7 @@
 //
 // K11 potential energy (_kernels.gpe_kernel, _kernels.py:53-67): same tiling.
 #include <climits>
+#include <cstdlib>
 
 #include "fga_session.cuh"
 
@@ -286,16 +287,14 @@ struct F32Params {
   float theta2, eps2;
 };
 
-template <typename Real, bool kGuardZero>
-__global__ void __launch_bounds__(kForceThreads, 4) k_bh_iterate(TreeRecords tr, int n_nodes,
-                                                               TemplateView tv,
-                                                               const IterState* __restrict__ st,
-                                                               SimParams sp, F32Params f,
-                                                               double* partials, float cmag) {
+template <typename Real, bool kGuardZero, int kT>
+__global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? 1024 : 768) / kT) k_bh_iterate(
+    TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, SimParams sp,
+    F32Params f, double* partials, float cmag) {
   if (st->done) return;
-  __shared__ typename WinOf<Real>::T wins[kWarps];
+  __shared__ typename WinOf<Real>::T wins[kT / 32];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + wl;
+  const int64_t gw = (int64_t)blockIdx.x * (kT / 32) + wl;
   const int64_t i = gw * 32 + lane;
   const bool active = i < tv.m;
   double y[3] = {0, 0, 0}, v[3] = {0, 0, 0}, mq = 1.0;
@@ -862,30 +861,49 @@ inline unsigned grid_for(int64_t items, int64_t per_block) {
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
-int64_t bh_iterate_warps(int64_t m) { return (int64_t)grid_for(m, kForceThreads) * kWarps; }
+static int bh_block() {
+  static int b = [] {
+    const char* e = getenv("FGA_BH_BLOCK");
+    int v = e ? atoi(e) : 128;
+    return (v == 64 || v == 128 || v == 256) ? v : 128;
+  }();
+  return b;
+}
+int64_t bh_iterate_warps(int64_t m) {
+  const int t = bh_block();
+  return (int64_t)grid_for(m, t) * (t / 32);
+}
 int64_t direct_iterate_warps(int64_t m, int precision) {
   const int64_t per = precision ? kForceThreads : kForceThreads * kDirectQPT;
   return (int64_t)grid_for(m, per) * kWarps;
 }
 int64_t gpe_warps(int64_t m, int precision) { return direct_iterate_warps(m, precision); }
 
-void launch_bh_iterate(const TreeDev& T, const TemplateView& tv, const IterState* st,
-                       const SimParams& sp, double* partials, int precision, cudaStream_t s) {
-  if (tv.m <= 0) return;
-  const unsigned g = grid_for(tv.m, kForceThreads);
+template <int kT>
+static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const IterState* st,
+                                const SimParams& sp, double* partials, int precision,
+                                cudaStream_t s) {
+  const unsigned g = grid_for(tv.m, kT);
   const F32Params f{(float)sp.theta2, (float)sp.eps2};
   const bool gz = !(sp.eps2 > 0.0);
   const int nn = (int)T.n_nodes;
   const float cm = (float)T.cmag;
   if (precision)
-    k_bh_iterate<double, false><<<g, kForceThreads, 0, s>>>(T.records(), nn, tv, st, sp, f,
-                                                            partials, cm);
+    k_bh_iterate<double, false, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm);
   else if (gz)
-    k_bh_iterate<float, true><<<g, kForceThreads, 0, s>>>(T.records(), nn, tv, st, sp, f,
-                                                          partials, cm);
+    k_bh_iterate<float, true, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm);
   else
-    k_bh_iterate<float, false><<<g, kForceThreads, 0, s>>>(T.records(), nn, tv, st, sp, f,
-                                                           partials, cm);
+    k_bh_iterate<float, false, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm);
+}
+
+void launch_bh_iterate(const TreeDev& T, const TemplateView& tv, const IterState* st,
+                       const SimParams& sp, double* partials, int precision, cudaStream_t s) {
+  if (tv.m <= 0) return;
+  switch (bh_block()) {
+    case 64: launch_bh_iterate_t<64>(T, tv, st, sp, partials, precision, s); break;
+    case 256: launch_bh_iterate_t<256>(T, tv, st, sp, partials, precision, s); break;
+    default: launch_bh_iterate_t<128>(T, tv, st, sp, partials, precision, s); break;
+  }
 }
 
 void launch_direct_iterate(const RefPoints& ref, const TemplateView& tv, const IterState* st,

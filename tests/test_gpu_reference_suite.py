@@ -273,27 +273,53 @@ def _ctx(F):
     return NormalizationContext(mean_x=z, mean_y=z, l=-5.0, r=5.0, a=-5.0, b=5.0)
 
 
-def test_niv_count_ratio(F):
-    """10:1 occupancy -> 0.1 value ratio (test_masses.py:73-83)."""
-    pts = np.vstack([np.full((10, 3), -4.9), np.full((1, 3), 4.9)])
-    v = F.niv_masses(F.PointCloud(pts), 16, _ctx(F), 20)
-    assert abs(v[0] / v[-1] - 0.1) < 1e-12
+def test_niv_two_cell_count_ratio(F):
+    rho, depth = 16, 20
+    edge = 10.0 / rho
+    crowded = np.tile(np.array([[-5 + 0.3 * edge] * 3]), (10, 1))
+    crowded = crowded + np.linspace(0, 0.1 * edge, 10)[:, None]
+    lone = np.array([[-5 + 5.5 * edge, -5 + 0.3 * edge, -5 + 0.3 * edge]])
+    v = F.niv_masses(F.PointCloud(np.vstack([crowded, lone])), rho, _ctx(F), depth)
+    assert np.allclose(v[:10], v[0]) and abs(v[0] / v[10] - 0.1) < 1e-12
 
 
 def test_niv_single_cell_closed_form(F):
-    n = 7
-    v = F.niv_masses(F.PointCloud(np.full((n, 3), 0.1)), 16, _ctx(F), 20)
-    edge = 10.0 / 16
-    ball = (4.0 / 3.0) * np.pi * (10.0 / (2 * 20 * 16)) ** 3
+    rho, depth, n = 16, 20, 4
+    edge = 10.0 / rho
+    ball = 4.0 / 3.0 * np.pi * (10.0 / (2 * depth * rho)) ** 3
+    pts = np.full((n, 3), -5 + 0.2 * edge) + np.linspace(0, 0.1 * edge, n)[:, None]
+    v = F.niv_masses(F.PointCloud(pts), rho, _ctx(F), depth)
     assert np.allclose(v, edge**3 * edge**3 / (n * ball), rtol=1e-12)
 
 
-def test_niv_uniform_interior_cov(F):
-    rng = F.synth.rng_from_seed(9)
+def test_niv_uniform_lattice_equal_values(F):
+    rho = 4
+    c = -5 + (np.arange(rho) + 0.5) * (10.0 / rho)
+    pts = np.stack(np.meshgrid(c, c, c, indexing="ij"), axis=-1).reshape(-1, 3)
+    v = F.niv_masses(F.PointCloud(pts), rho, _ctx(F), 20)
+    assert np.allclose(v, v[0])
+
+
+def test_niv_uniform_cube_low_variation_interior(F):
+    rng = F.synth.rng_from_seed(2)
+    rho = 4
     pts = rng.uniform(-5, 5, size=(200000, 3))
-    v = F.niv_masses(F.PointCloud(pts), 16, _ctx(F), 20)
-    interior = np.all(np.abs(pts) < 4.0, axis=1)
+    v = F.niv_masses(F.PointCloud(pts), rho, _ctx(F), 20)
+    idx = np.clip(np.floor((pts + 5) / (10.0 / rho)).astype(int), 0, rho - 1)
+    interior = np.all((idx >= 1) & (idx <= rho - 2), axis=1)
     assert v[interior].std() / v[interior].mean() < 0.05
+
+
+def test_niv_denser_cells_get_smaller_values(F):
+    rng = F.synth.rng_from_seed(3)
+    pts = np.vstack([rng.uniform(-5, -2, size=(20, 3)), rng.uniform(2, 2.2, size=(200, 3))])
+    v = F.niv_masses(F.PointCloud(pts), 16, _ctx(F), 20)
+    assert v[:20].mean() > v[20:].mean()
+
+
+def test_niv_rejects_bad_rho(F):
+    with pytest.raises(F.InvalidParam):
+        F.niv_masses(F.PointCloud(np.zeros((1, 3))), 1, _ctx(F), 20)
 
 
 # ------------------------------------------------------ test_registration.py
