@@ -101,7 +101,9 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
   int visits = 0, accepted = 0;
   int cursor = active ? 0 : n_nodes;
   int wbase = INT_MIN / 2;
-  constexpr float kRel = 8.0f * 5.97e-8f;  // 8 unit roundoffs: d^2, theta^2 d^2, l^2
+  constexpr float kRel = 12.0f * 5.97e-8f;  // unit roundoffs of d^2, theta^2 d^2 and l^2 (~ t2d2 at a tie)
+  constexpr float kSqrt3 = 1.7320508f;
+  const float theta = sqrtf(theta2), itheta = theta > 0.f ? 1.0f / theta : 0.f;
   while (true) {
     const int n = __reduce_min_sync(0xffffffffu, cursor);
     if (n >= n_nodes) break;
@@ -113,8 +115,11 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
         const float4 a = __ldg(&A[j]);
         const NodeB32 b = B[j];
         win->r[lane].a = a;
-        win->r[lane].b = make_float4(b.l2, __int_as_float(b.skip),
-                                     b.l2 > -INFINITY ? 4.776e-7f * fabsf(b.l2) : 0.f, 0.f);
+        // p = sqrt3*theta/len, q = sqrt3*len/theta: 2|d|delta <= delta*(d2*p + q) with
+        // the AM-GM pivot at |d| = len/theta, where MAC ties happen
+        const float il = b.l2 > 0.f ? rsqrt_approx(b.l2) : 0.f;
+        win->r[lane].b = make_float4(b.l2, __int_as_float(b.skip), kSqrt3 * theta * il,
+                                     kSqrt3 * b.l2 * il * itheta);
       }
       __syncwarp();
     }
@@ -126,9 +131,8 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
     const float t2d2 = theta2 * d2;
     bool acc = b.x < t2d2;
-    const float s1 = fabsf(dx) + fabsf(dy) + fabsf(dz);
-    const float band = fmaf(gA, s1, fmaf(kRel, t2d2, b.z));  // b.z = gB-free kRel*|l2|
-    const bool near = mine && fabsf(t2d2 - b.x) <= band + gB;
+    const float band = fmaf(gA, fmaf(d2, b.z, b.w), fmaf(kRel, t2d2, gB));
+    const bool near = mine && fabsf(t2d2 - b.x) <= band;
     if (__any_sync(0xffffffffu, near)) {  // warp-uniform branch, rarely taken
       if (near) acc = mac_exact(A64, B64, n, qpx[qi], qpy[qi], qpz[qi], theta2_64);
     }
@@ -206,7 +210,7 @@ __device__ __forceinline__ Trav64Out traverse64(const double4* __restrict__ A,
 __device__ __forceinline__ void guard_coeffs(float qmag, float cmag, float theta2, float& gA,
                                              float& gB) {
   const float delta = (qmag + cmag) * 5.97e-8f;
-  gA = 2.5f * delta * theta2;
+  gA = 1.25f * delta * theta2;                    // times (d2*p + q) >= 2*sqrt3*|d|
   gB = 3.75f * delta * delta * theta2 + 1e-37f;
 }
 
@@ -288,7 +292,7 @@ struct F32Params {
 };
 
 template <typename Real, bool kGuardZero, int kT>
-__global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? 1024 : 768) / kT) k_bh_iterate(
+__global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? 1280 : 768) / kT) k_bh_iterate(
     TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, SimParams sp,
     F32Params f, double* partials, float cmag) {
   if (st->done) return;
