@@ -34,6 +34,7 @@ namespace fga {
 namespace {
 
 constexpr int kWin = 32;
+constexpr int kNumSMs = 148;
 constexpr int kWarps = kForceThreads / 32;
 
 struct Win32 {
@@ -46,7 +47,7 @@ struct Win64 {
 };
 
 // exact fp64 MAC of the reference (_kernels.py:26-29, :37)
-__device__ __noinline__ bool mac_exact(const double4* __restrict__ A64,
+__device__ __forceinline__ bool mac_exact(const double4* __restrict__ A64,
                                        const NodeB64* __restrict__ B64, int node, double qx,
                                        double qy, double qz, double theta2) {
   const double4 a = A64[node];
@@ -294,11 +295,16 @@ struct F32Params {
 template <typename Real, bool kGuardZero, int kT>
 __global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? 1280 : 768) / kT) k_bh_iterate(
     TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, SimParams sp,
-    F32Params f, double* partials, float cmag) {
+    F32Params f, double* partials, float cmag, int nblocks, int per_sm) {
   if (st->done) return;
+  // Block -> chunk remap: the blocks a given SM runs concurrently (b, b+148,
+  // b+296, ...) take CONSECUTIVE Morton chunks, so the warps sharing an L1
+  // traverse the same part of the tree.
+  const int chunk = (int)(blockIdx.x % kNumSMs) * per_sm + (int)(blockIdx.x / kNumSMs);
+  if (chunk >= nblocks) return;
   __shared__ typename WinOf<Real>::T wins[kT / 32];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * (kT / 32) + wl;
+  const int64_t gw = (int64_t)chunk * (kT / 32) + wl;
   const int64_t i = gw * 32 + lane;
   const bool active = i < tv.m;
   double y[3] = {0, 0, 0}, v[3] = {0, 0, 0}, mq = 1.0;
@@ -887,17 +893,22 @@ template <int kT>
 static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const IterState* st,
                                 const SimParams& sp, double* partials, int precision,
                                 cudaStream_t s) {
-  const unsigned g = grid_for(tv.m, kT);
+  const int nb = (int)grid_for(tv.m, kT);
+  const int per = (nb + kNumSMs - 1) / kNumSMs;
+  const unsigned g = (unsigned)(per * kNumSMs);
   const F32Params f{(float)sp.theta2, (float)sp.eps2};
   const bool gz = !(sp.eps2 > 0.0);
   const int nn = (int)T.n_nodes;
   const float cm = (float)T.cmag;
   if (precision)
-    k_bh_iterate<double, false, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm);
+    k_bh_iterate<double, false, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm,
+                                                     nb, per);
   else if (gz)
-    k_bh_iterate<float, true, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm);
+    k_bh_iterate<float, true, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm,
+                                                   nb, per);
   else
-    k_bh_iterate<float, false, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm);
+    k_bh_iterate<float, false, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm,
+                                                    nb, per);
 }
 
 void launch_bh_iterate(const TreeDev& T, const TemplateView& tv, const IterState* st,

@@ -168,13 +168,16 @@ def main(n=1_000_000, nq=16384, theta=0.5):
     start = len(order) // 2
     sel = order[start:start + nq]
     q = np.ascontiguousarray(yn[sel])
-    for W in (32, 64):
+    for W in (32, 64, 128, 256):
         t0 = time.time()
         a = sim(com, l2, sk, q, theta * theta, W)
         print(f"W={W}: warp-min steps/warp {a[0]/(nq/32):.0f} refills/warp {a[1]/(nq/32):.0f} | "
               f"windowed outer/warp {a[2]/(nq/32):.0f} inner/warp {a[3]/(nq/32):.0f} | "
               f"visits/q {a[4]/nq:.0f}  ({time.time()-t0:.1f}s)")
-    b = sim_thread(com, l2, sk, q, theta * theta)
+    if os.environ.get("SIM_THREAD"):
+        b = sim_thread(com, l2, sk, q, theta * theta)
+    else:
+        return
     print(f"per-thread: steps/warp {b[0]/(nq/32):.0f}  distinct nodes/step {b[1]/b[0]:.2f} "
           f"128B lines/step {b[2]/b[0]:.2f}")
 
