@@ -47,7 +47,7 @@ struct Win64 {
 };
 
 // exact fp64 MAC of the reference (_kernels.py:26-29, :37)
-__device__ __forceinline__ bool mac_exact(const double4* __restrict__ A64,
+__device__ __noinline__ bool mac_exact(const double4* __restrict__ A64,
                                        const NodeB64* __restrict__ B64, int node, double qx,
                                        double qy, double qz, double theta2) {
   const double4 a = A64[node];
