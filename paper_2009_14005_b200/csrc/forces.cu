@@ -297,10 +297,10 @@ __global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? 1280 : 768) / kT) k_b
     TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, SimParams sp,
     F32Params f, double* partials, float cmag, int nblocks, int per_sm) {
   if (st->done) return;
-  // Block -> chunk remap: the blocks a given SM runs concurrently (b, b+148,
-  // b+296, ...) take CONSECUTIVE Morton chunks, so the warps sharing an L1
-  // traverse the same part of the tree.
-  const int chunk = (int)(blockIdx.x % kNumSMs) * per_sm + (int)(blockIdx.x / kNumSMs);
+  // (An SM-contiguous block->chunk remap for L1 sharing was measured 3%
+  // slower -- per-SM load imbalance -- so blocks map to chunks in order.)
+  (void)per_sm;
+  const int chunk = (int)blockIdx.x;
   if (chunk >= nblocks) return;
   __shared__ typename WinOf<Real>::T wins[kT / 32];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -894,8 +894,8 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
                                 const SimParams& sp, double* partials, int precision,
                                 cudaStream_t s) {
   const int nb = (int)grid_for(tv.m, kT);
-  const int per = (nb + kNumSMs - 1) / kNumSMs;
-  const unsigned g = (unsigned)(per * kNumSMs);
+  const int per = 0;
+  const unsigned g = (unsigned)nb;
   const F32Params f{(float)sp.theta2, (float)sp.eps2};
   const bool gz = !(sp.eps2 > 0.0);
   const int nn = (int)T.n_nodes;
