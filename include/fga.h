@@ -80,6 +80,17 @@ typedef struct {
   double setup_ms, loop_ms, gpe_ms; /* device-timed phases (CUDA events)       */
 } fga_result;
 
+/* One pair of a batched registration (BASELINE configs[4]). */
+typedef struct {
+  double R[9], t[3];        /* transform in the original frame               */
+  int64_t iterations;
+  int32_t converged;
+  int32_t status;           /* FGA_OK or the FGA_ERR_* this pair raised      */
+  double gpe_initial, gpe_final;
+  int64_t interactions;     /* accepted interactions summed over iterations  */
+  int64_t n_nodes;          /* reference tree size                           */
+} fga_pair_result;
+
 /* ------------------------------------------------------------------ misc */
 int fga_version(void);
 const char* fga_last_error(void);
@@ -101,6 +112,27 @@ int fga_synchronize(fga_ctx* ctx);
 int fga_register(fga_ctx* ctx, const double* x, int64_t n, const double* y, int64_t m, int dim,
                  const fga_params* params, const fga_options* options, fga_result* out,
                  double* deltas, double* traj, double* gpe_trace, int64_t* interactions_per_iter);
+
+/* --------------------------------------------- batched driver (config 5)
+ * registration.register applied to n_pairs independent pairs in ONE
+ * persistent kernel (one CTA per pair at a time, whole loop on the device).
+ * x_all/y_all: concatenated (sum n_p, 3) / (sum m_p, 3) fp64 clouds,
+ * x_offsets/y_offsets: n_pairs+1 row offsets.  options->x_weights/y_weights,
+ * if set, are concatenated like x_all/y_all.  Per-pair failures (empty,
+ * degenerate, too large for the batched kernel: > 8192 points) are reported
+ * in fga_pair_result.status instead of aborting the batch, like
+ * registration.register_sequence does (registration.py:192-200).  deltas
+ * (optional) is n_pairs * max_iters.  FP32 force precision only. */
+int fga_register_batch(fga_ctx* ctx, const double* x_all, const int64_t* x_offsets,
+                       const double* y_all, const int64_t* y_offsets, int64_t n_pairs, int dim,
+                       const fga_params* params, const fga_options* options,
+                       fga_pair_result* out, double* deltas);
+/* Same with device-resident clouds/offsets/weights/outputs (stream-ordered). */
+int fga_register_batch_dev(fga_ctx* ctx, const double* x_all, const int64_t* x_offsets,
+                           const double* y_all, const int64_t* y_offsets, int64_t n_pairs,
+                           int nmax, int mmax, int dim, const fga_params* params,
+                           const fga_options* options, fga_pair_result* out_dev,
+                           double* deltas_dev);
 
 /* ---------------------------------------------- session (stepwise) entry
  * The same loop split into stream-ordered pieces so a host can insert a

@@ -72,6 +72,14 @@ class CResult(ctypes.Structure):
                 ("setup_ms", _dbl), ("loop_ms", _dbl), ("gpe_ms", _dbl)]
 
 
+class CPairResult(ctypes.Structure):
+    """fga_pair_result (include/fga.h)."""
+
+    _fields_ = [("R", _dbl * 9), ("t", _dbl * 3), ("iterations", _i64), ("converged", _i32),
+                ("status", _i32), ("gpe_initial", _dbl), ("gpe_final", _dbl),
+                ("interactions", _i64), ("n_nodes", _i64)]
+
+
 # name -> (restype, argtypes); every symbol include/fga.h declares
 SIGNATURES = {
     "fga_version": (_c_int, []),
@@ -84,6 +92,12 @@ SIGNATURES = {
     "fga_register": (_c_int, [_vp, _vp, _i64, _vp, _i64, _c_int, ctypes.POINTER(CParams),
                               ctypes.POINTER(COptions), ctypes.POINTER(CResult), _vp, _vp, _vp,
                               _vp]),
+    "fga_register_batch": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _c_int,
+                                    ctypes.POINTER(CParams), ctypes.POINTER(COptions), _vp,
+                                    _vp]),
+    "fga_register_batch_dev": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _c_int, _c_int, _c_int,
+                                        ctypes.POINTER(CParams), ctypes.POINTER(COptions), _vp,
+                                        _vp]),
     "fga_session_begin": (_c_int, [_vp, _vp, _i64, _vp, _i64, _c_int, ctypes.POINTER(CParams),
                                    ctypes.POINTER(COptions), _c_int, _c_int]),
     "fga_session_begin_dev": (_c_int, [_vp, _vp, _i64, _vp, _i64, _c_int,
@@ -147,6 +161,36 @@ def last_error() -> str:
 
 
 _INVALID_RE = re.compile(r"invalid parameter (\w+)=(.*)$")
+
+
+def error_for(rc: int, msg: str = ""):
+    """Exception instance for a C return code (None for FGA_OK)."""
+    if rc == FGA_OK:
+        return None
+    try:
+        check_msg(rc, msg)
+    except Exception as e:  # noqa: BLE001
+        return e
+    return None
+
+
+def check_msg(rc: int, msg: str) -> None:
+    if rc == FGA_OK:
+        return
+    if rc == FGA_ERR_INVALID:
+        m = _INVALID_RE.search(msg)
+        if m:
+            raise InvalidParam(m.group(1), m.group(2))
+        raise InvalidParam("argument", msg)
+    if rc == FGA_ERR_EMPTY:
+        raise EmptyCloud(msg)
+    if rc == FGA_ERR_DEGENERATE:
+        raise DegenerateExtent(msg)
+    if rc == FGA_ERR_NONFINITE:
+        raise NonFiniteWeight(msg)
+    if rc == FGA_ERR_LENGTH:
+        raise LengthMismatch(msg)
+    raise DeviceError(f"libfga error {rc}: {msg}")
 
 
 def check(rc: int) -> None:

@@ -18,6 +18,7 @@
 
 #include "../../include/fga.h"
 #include "fga_session.cuh"
+#include "fga_batched.cuh"
 
 namespace fga {
 static thread_local std::string g_err;
@@ -65,6 +66,7 @@ struct Session {
 
 struct fga_ctx {
   int device = 0;
+  DevBuf batch_in[6], batch_scratch, batch_out, batch_deltas, batch_counter;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   TreeDev tree;
@@ -443,6 +445,11 @@ int fga_destroy(fga_ctx* c) {
   c->tree_pts.release();
   c->tree_masses.release();
   for (auto& b : c->op) b.release();
+  for (auto& b : c->batch_in) b.release();
+  c->batch_scratch.release();
+  c->batch_out.release();
+  c->batch_deltas.release();
+  c->batch_counter.release();
   Session& S = c->S;
   DevBuf* all[] = {&S.x_raw,   &S.y_raw,  &S.xn,        &S.yn,       &S.ctx_dev,   &S.mx,
                    &S.my,      &S.flat,   &S.counts,    &S.cells,    &S.ref32,     &S.ref64,
@@ -678,6 +685,164 @@ int fga_register(fga_ctx* c, const double* x, int64_t n, const double* y, int64_
   }
   S.gpe_ms = gpe_ms;
   return fga_session_finish(c, out, deltas, traj, gpe_trace, inter, nullptr);
+}
+
+// ------------------------------------------------------------------ batched
+int fga_register_batch_dev(fga_ctx* c, const double* x_all, const int64_t* x_offsets,
+                           const double* y_all, const int64_t* y_offsets, int64_t n_pairs,
+                           int nmax, int mmax, int dim, const fga_params* params,
+                           const fga_options* options, fga_pair_result* out_dev,
+                           double* deltas_dev) {
+  CTX_TRY(c);
+  TRY(validate(params));
+  if (dim != 3) {
+    set_error("the B200 path implements D=3 (D=2 is not built yet)");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  if (n_pairs <= 0) return FGA_OK;
+  fga_options def{};
+  def.normalize = 1;
+  def.compute_gpe = 1;
+  const fga_options O = options ? *options : def;
+  if (O.precision != FGA_PREC_FP32) {
+    set_error("fga_register_batch: FP32 force precision only");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  if (params->max_depth > kMaxLevels) {
+    set_error("max_depth must be <= 21 on the GPU path");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  nmax = std::max(nmax, 1);
+  mmax = std::max(mmax, 1);
+  if (nmax > 8192 || mmax > 8192) {
+    set_error("fga_register_batch: pairs are limited to 8192 points per cloud");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  const int64_t ncell64 = (int64_t)params->rho * params->rho * params->rho;
+  if (ncell64 > 16384) {
+    set_error("fga_register_batch: rho^3 must be <= 16384");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  int P = 2048;
+  while (P < std::max(nmax, mmax)) P <<= 1;
+  const int ncell = (int)ncell64;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int grid = (int)std::min<int64_t>(n_pairs, sms);
+  const size_t cap = (size_t)4 * nmax + 64 * (size_t)params->max_depth;
+  const size_t smem = batch_smem_bytes(P, nmax, ncell);
+  // per-slot scratch
+  const size_t per_slot = sizeof(double) * ((size_t)nmax * 3 + (size_t)mmax * 3 + nmax + mmax) +
+                          sizeof(int) * std::max(nmax, mmax) + sizeof(float4) * nmax +
+                          cap * (1 + 4 * 3 + 4 * 8 + 8 + 24 + 8 + 16 + 8 + 32 + 16) +
+                          sizeof(double) * (size_t)mmax * 7 + 1024;
+  FGA_CUDA_TRY(c->batch_scratch.reserve(per_slot * grid + 4096));
+  BatchArgs a{};
+  char* q = c->batch_scratch.as<char>();
+  auto take = [&](size_t bytes) {
+    char* r = q;
+    q += (bytes + 255) / 256 * 256;
+    return r;
+  };
+  const size_t g = grid;
+  a.scratch.xn = (double*)take(sizeof(double) * nmax * 3 * g);
+  a.scratch.yn = (double*)take(sizeof(double) * mmax * 3 * g);
+  a.scratch.mx = (double*)take(sizeof(double) * nmax * g);
+  a.scratch.my = (double*)take(sizeof(double) * mmax * g);
+  a.scratch.flat = (int*)take(sizeof(int) * std::max(nmax, mmax) * g);
+  a.scratch.ref32 = (float4*)take(sizeof(float4) * nmax * g);
+  a.scratch.nlev = (signed char*)take(cap * g);
+  a.scratch.nstart = (int*)take(sizeof(int) * cap * g);
+  a.scratch.nocc = (int*)take(sizeof(int) * cap * g);
+  a.scratch.nskip = (int*)take(sizeof(int) * cap * g);
+  a.scratch.nchild = (int*)take(sizeof(int) * 8 * cap * g);
+  a.scratch.nmass = (double*)take(sizeof(double) * cap * g);
+  a.scratch.nmc = (double*)take(sizeof(double) * 3 * cap * g);
+  a.scratch.nlen = (double*)take(sizeof(double) * cap * g);
+  a.scratch.ra32 = (float4*)take(sizeof(float4) * cap * g);
+  a.scratch.rb32 = (NodeB32*)take(sizeof(NodeB32) * cap * g);
+  a.scratch.ra64 = (double4*)take(sizeof(double4) * cap * g);
+  a.scratch.rb64 = (NodeB64*)take(sizeof(NodeB64) * cap * g);
+  a.scratch.tpl = (double*)take(sizeof(double) * mmax * 7 * g);
+  if ((size_t)(q - c->batch_scratch.as<char>()) > c->batch_scratch.bytes) {
+    set_error("internal: batched scratch sizing");
+    return FGA_ERR_NOMEM;
+  }
+  FGA_CUDA_TRY(c->batch_counter.reserve(sizeof(int)));
+  FGA_CUDA_TRY(cudaMemsetAsync(c->batch_counter.p, 0, sizeof(int), c->stream));
+  a.x = x_all;
+  a.y = y_all;
+  a.xoff = reinterpret_cast<const long long*>(x_offsets);
+  a.yoff = reinterpret_cast<const long long*>(y_offsets);
+  a.x_weights = O.x_weights;
+  a.y_weights = O.y_weights;
+  a.n_pairs = (int)n_pairs;
+  a.nmax = nmax;
+  a.mmax = mmax;
+  a.P = P;
+  a.ncell = ncell;
+  a.node_cap = cap;
+  const double extent = params->norm_b - params->norm_a;
+  a.cell_edge = extent / params->rho;
+  a.cell_vol = std::pow(a.cell_edge, 3);
+  const double r_ball = extent / (2.0 * params->max_depth * params->rho);
+  a.ball_vol = (4.0 / 3.0) * M_PI * std::pow(r_ball, 3);
+  a.p = *params;
+  a.opt = O;
+  a.counter = c->batch_counter.as<int>();
+  a.out = out_dev;
+  a.deltas = deltas_dev;
+  return launch_register_batch(a, grid, smem, c->stream);
+}
+
+int fga_register_batch(fga_ctx* c, const double* x_all, const int64_t* x_offsets,
+                       const double* y_all, const int64_t* y_offsets, int64_t n_pairs, int dim,
+                       const fga_params* params, const fga_options* options,
+                       fga_pair_result* out, double* deltas) {
+  CTX_TRY(c);
+  if (n_pairs <= 0) return FGA_OK;
+  if (!x_offsets || !y_offsets || !out) return FGA_ERR_INVALID;
+  int nmax = 0, mmax = 0;
+  for (int64_t p = 0; p < n_pairs; p++) {
+    nmax = (int)std::max<int64_t>(nmax, x_offsets[p + 1] - x_offsets[p]);
+    mmax = (int)std::max<int64_t>(mmax, y_offsets[p + 1] - y_offsets[p]);
+  }
+  const int64_t nx = x_offsets[n_pairs], ny = y_offsets[n_pairs];
+  cudaStream_t s = c->stream;
+  TRY(h2d(c->batch_in[0], x_all, 3 * nx, s));
+  TRY(h2d(c->batch_in[1], y_all, 3 * ny, s));
+  TRY(h2d(c->batch_in[2], x_offsets, n_pairs + 1, s));
+  TRY(h2d(c->batch_in[3], y_offsets, n_pairs + 1, s));
+  fga_options O;
+  if (options) {
+    O = *options;
+  } else {
+    O = fga_options{};
+    O.normalize = 1;
+    O.compute_gpe = 1;
+  }
+  if (O.x_weights) {
+    TRY(h2d(c->batch_in[4], O.x_weights, nx, s));
+    O.x_weights = c->batch_in[4].as<double>();
+  }
+  if (O.y_weights) {
+    TRY(h2d(c->batch_in[5], O.y_weights, ny, s));
+    O.y_weights = c->batch_in[5].as<double>();
+  }
+  FGA_CUDA_TRY(c->batch_out.reserve(sizeof(fga_pair_result) * n_pairs));
+  if (deltas) FGA_CUDA_TRY(c->batch_deltas.reserve(sizeof(double) * n_pairs * params->max_iters));
+  TRY(fga_register_batch_dev(c, c->batch_in[0].as<double>(), c->batch_in[2].as<int64_t>(),
+                             c->batch_in[1].as<double>(), c->batch_in[3].as<int64_t>(), n_pairs,
+                             nmax, mmax, dim, params, &O, c->batch_out.as<fga_pair_result>(),
+                             deltas ? c->batch_deltas.as<double>() : nullptr));
+  FGA_CUDA_TRY(cudaMemcpyAsync(out, c->batch_out.p, sizeof(fga_pair_result) * n_pairs,
+                               cudaMemcpyDeviceToHost, s));
+  if (deltas)
+    FGA_CUDA_TRY(cudaMemcpyAsync(deltas, c->batch_deltas.p,
+                                 sizeof(double) * n_pairs * params->max_iters,
+                                 cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  return FGA_OK;
 }
 
 // ------------------------------------------------------------------ tree ops

@@ -28,253 +28,10 @@
 #include <climits>
 #include <cstdlib>
 
-#include "fga_session.cuh"
+#include "fga_device.cuh"
 
 namespace fga {
 namespace {
-
-constexpr int kWin = 32;
-constexpr int kNumSMs = 148;
-constexpr int kWarps = kForceThreads / 32;
-
-struct Win32 {
-  float4 a[kWin];
-  NodeB32 b[kWin];
-};
-struct Win64 {
-  double4 a[kWin];
-  NodeB64 b[kWin];
-};
-
-// exact fp64 MAC of the reference (_kernels.py:26-29, :37)
-__device__ __noinline__ bool mac_exact(const double4* __restrict__ A64,
-                                       const NodeB64* __restrict__ B64, int node, double qx,
-                                       double qy, double qz, double theta2) {
-  const double4 a = A64[node];
-  const double dx = __dsub_rn(qx, a.x), dy = __dsub_rn(qy, a.y), dz = __dsub_rn(qz, a.z);
-  const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-  return B64[node].l2 < __dmul_rn(theta2, d2);
-}
-
-__device__ __forceinline__ float rsqrt_approx(float x) {
-  float r;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-
-struct Trav32Out {
-  float ax, ay, az;
-  int visits, accepted;
-};
-
-// FP32 warp-coherent traversal.  All 32 lanes must call it (inactive lanes
-// pass active=false).  Branch-free step: every lane evaluates the node at the
-// warp-minimum cursor and the results are committed only on the lanes whose
-// cursor is that node (SIMT issues the instructions once per warp either way,
-// so predication is cheaper than divergent branches + reconvergence).
-//
-// Exact-MAC guard: with q and com rounded to fp32 (each coordinate off by at
-// most delta = (|q|max + |com|max) * 2^-24) the fp32 d^2 differs from the
-// fp64 one by at most 2*delta*(|dx|+|dy|+|dz|) + 3*delta^2 + 4u*d^2.  When
-// |theta^2 d^2 - l^2| is inside that bound (plus the rounding of l^2 and of
-// theta^2 d^2) the decision is re-made exactly in fp64 from the fp64 records,
-// so the accepted set always equals the reference's (_kernels.py:37).
-// gA = 2*delta*theta^2*1.25, gB = 3*delta^2*theta^2*1.25 (per lane).
-struct WinRec32 {
-  float4 a;  // com.xyz, mass
-  float4 b;  // l2 | -inf, skip (int bits), unused, unused
-};
-struct WinBuf32 {
-  WinRec32 r[kWin];
-};
-
-template <bool kGuardZero>
-__device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
-                                                const NodeB32* __restrict__ B,
-                                                const double4* __restrict__ A64,
-                                                const NodeB64* __restrict__ B64, int n_nodes,
-                                                float qx, float qy, float qz, bool active,
-                                                float theta2, double theta2_64, float eps2,
-                                                float gA, float gB, const double* qpx,
-                                                const double* qpy, const double* qpz, int64_t qi,
-                                                WinBuf32* win, int lane) {
-  float ax = 0.f, ay = 0.f, az = 0.f;
-  int visits = 0, accepted = 0;
-  int cursor = active ? 0 : n_nodes;
-  int wbase = INT_MIN / 2;
-  constexpr float kRel = 12.0f * 5.97e-8f;  // unit roundoffs of d^2, theta^2 d^2 and l^2 (~ t2d2 at a tie)
-  constexpr float kSqrt3 = 1.7320508f;
-  const float theta = sqrtf(theta2), itheta = theta > 0.f ? 1.0f / theta : 0.f;
-  while (true) {
-    const int n = __reduce_min_sync(0xffffffffu, cursor);
-    if (n >= n_nodes) break;
-    if ((unsigned)(n - wbase) >= (unsigned)kWin) {
-      wbase = n;
-      __syncwarp();
-      const int j = n + lane;
-      if (j < n_nodes) {
-        const float4 a = __ldg(&A[j]);
-        const NodeB32 b = B[j];
-        win->r[lane].a = a;
-        // p = sqrt3*theta/len, q = sqrt3*len/theta: 2|d|delta <= delta*(d2*p + q) with
-        // the AM-GM pivot at |d| = len/theta, where MAC ties happen
-        const float il = b.l2 > 0.f ? rsqrt_approx(b.l2) : 0.f;
-        win->r[lane].b = make_float4(b.l2, __int_as_float(b.skip), kSqrt3 * theta * il,
-                                     kSqrt3 * b.l2 * il * itheta);
-      }
-      __syncwarp();
-    }
-    const WinRec32& rec = win->r[n - wbase];
-    const float4 a = rec.a;
-    const float4 b = rec.b;
-    const bool mine = cursor == n;
-    const float dx = a.x - qx, dy = a.y - qy, dz = a.z - qz;
-    const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-    const float t2d2 = theta2 * d2;
-    bool acc = b.x < t2d2;
-    const float band = fmaf(gA, fmaf(d2, b.z, b.w), fmaf(kRel, t2d2, gB));
-    const bool near = mine && fabsf(t2d2 - b.x) <= band;
-    if (__any_sync(0xffffffffu, near)) {  // warp-uniform branch, rarely taken
-      if (near) acc = mac_exact(A64, B64, n, qpx[qi], qpy[qi], qpz[qi], theta2_64);
-    }
-    const bool take = mine && acc;
-    const float r2 = d2 + eps2;
-    const float inv = rsqrt_approx(r2);
-    float w = a.w * (inv * inv * inv);
-    if (!take) w = 0.f;
-    if (kGuardZero && !(r2 > 0.f)) w = 0.f;  // reference skips d2+eps2 == 0 (:39)
-    ax = fmaf(w, dx, ax);
-    ay = fmaf(w, dy, ay);
-    az = fmaf(w, dz, az);
-    asm("{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %2, 0;\n\tsetp.ne.b32 q, %3, 0;\n\t"
-        "@p add.s32 %0, %0, 1;\n\t@q add.s32 %1, %1, 1;\n\t}"
-        : "+r"(visits), "+r"(accepted) : "r"((int)mine), "r"((int)take));
-    const int next = acc ? __float_as_int(b.y) : n + 1;
-    cursor = mine ? next : cursor;
-  }
-  return Trav32Out{ax, ay, az, visits, accepted};
-}
-
-struct Trav64Out {
-  double fx, fy, fz;
-  int visits, accepted;
-};
-
-// FP64 traversal: the reference's arithmetic and order exactly.  gq = G*m_q.
-__device__ __forceinline__ Trav64Out traverse64(const double4* __restrict__ A,
-                                                const NodeB64* __restrict__ B, int n_nodes,
-                                                double qx, double qy, double qz, double gq,
-                                                bool active, double theta2, double eps2,
-                                                Win64* win, int lane) {
-  Trav64Out o{0.0, 0.0, 0.0, 0, 0};
-  int cursor = active ? 0 : n_nodes;
-  int wbase = INT_MIN / 2;
-  while (true) {
-    const int n = __reduce_min_sync(0xffffffffu, cursor);
-    if (n >= n_nodes) break;
-    if ((unsigned)(n - wbase) >= (unsigned)kWin) {
-      wbase = n;
-      __syncwarp();
-      const int j = n + lane;
-      if (j < n_nodes) {
-        win->a[lane] = A[j];
-        win->b[lane] = B[j];
-      }
-      __syncwarp();
-    }
-    if (cursor == n) {
-      const double4 a = win->a[n - wbase];
-      const NodeB64 b = win->b[n - wbase];
-      const double dx = __dsub_rn(qx, a.x), dy = __dsub_rn(qy, a.y), dz = __dsub_rn(qz, a.z);
-      const double d2 =
-          __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-      o.visits++;
-      if (b.l2 < __dmul_rn(theta2, d2)) {
-        o.accepted++;
-        const double denom = __dadd_rn(d2, eps2);
-        if (denom > 0.0) {
-          const double w = __ddiv_rn(__dmul_rn(gq, a.w), __dmul_rn(denom, __dsqrt_rn(denom)));
-          o.fx = __dsub_rn(o.fx, __dmul_rn(w, dx));
-          o.fy = __dsub_rn(o.fy, __dmul_rn(w, dy));
-          o.fz = __dsub_rn(o.fz, __dmul_rn(w, dz));
-        }
-        cursor = (int)b.skip;
-      } else {
-        cursor = n + 1;
-      }
-    }
-  }
-  return o;
-}
-
-// Per-lane guard coefficients (see traverse32).
-__device__ __forceinline__ void guard_coeffs(float qmag, float cmag, float theta2, float& gA,
-                                             float& gB) {
-  const float delta = (qmag + cmag) * 5.97e-8f;
-  gA = 1.25f * delta * theta2;                    // times (d2*p + q) >= 2*sqrt3*|d|
-  gB = 3.75f * delta * delta * theta2 + 1e-37f;
-}
-
-// ---------------------------------------------------------------- iterate epilogue
-struct Partial {
-  double v[17];
-};
-
-__device__ __forceinline__ void partial_zero(Partial& p) {
-#pragma unroll
-  for (int k = 0; k < 17; k++) p.v[k] = 0.0;
-}
-
-// Applies R,t of the previous step to (y, v') in place (registration.py:135-136).
-__device__ __forceinline__ void apply_pending(const IterState* st, double y[3], double v[3]) {
-  double ny[3], nv[3];
-#pragma unroll
-  for (int r = 0; r < 3; r++) {
-    ny[r] = st->Rp[3 * r] * y[0] + st->Rp[3 * r + 1] * y[1] + st->Rp[3 * r + 2] * y[2] + st->tp[r];
-    nv[r] = st->Rp[3 * r] * v[0] + st->Rp[3 * r + 1] * v[1] + st->Rp[3 * r + 2] * v[2];
-  }
-#pragma unroll
-  for (int r = 0; r < 3; r++) {
-    y[r] = ny[r];
-    v[r] = nv[r];
-  }
-}
-
-// total_force + step (dynamics.py:40, :45-46) in the reference's operation
-// order, then this query's contribution to the Kabsch sums.
-__device__ __forceinline__ void step_and_accumulate(const double F[3], const double y[3],
-                                                    const double v[3], double mq,
-                                                    const SimParams& sp, const double s[3],
-                                                    double vp[3], Partial& p) {
-  double w[3], u[3];
-#pragma unroll
-  for (int k = 0; k < 3; k++) {
-    const double f = __dsub_rn(F[k], __dmul_rn(sp.eta, v[k]));
-    vp[k] = __dadd_rn(v[k], __ddiv_rn(__dmul_rn(sp.dt, f), mq));
-    const double d = __dmul_rn(sp.dt, vp[k]);
-    u[k] = y[k] - s[k];
-    w[k] = (y[k] + d) - s[k];
-  }
-#pragma unroll
-  for (int k = 0; k < 3; k++) {
-    p.v[kSumU + k] += u[k];
-    p.v[kSumW + k] += w[k];
-  }
-#pragma unroll
-  for (int i = 0; i < 3; i++)
-#pragma unroll
-    for (int j = 0; j < 3; j++) p.v[kSumWU + 3 * i + j] = fma(w[i], u[j], p.v[kSumWU + 3 * i + j]);
-}
-
-__device__ __forceinline__ void warp_store_partial(Partial& p, int lane, double* out) {
-#pragma unroll
-  for (int k = 0; k < 17; k++) p.v[k] = warp_sum(p.v[k]);
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < 17; k++) out[k] = p.v[k];
-    out[17] = 0.0;
-  }
-}
 
 // ---------------------------------------------------------------- BH iterate
 template <typename Real>
@@ -427,97 +184,7 @@ __global__ void __launch_bounds__(kForceThreads) k_bh_operator(
 }
 
 // ---------------------------------------------------------------- direct sum
-constexpr int kTile = 1024;
-
-// ---- packed FP32x2 arithmetic (sm_100 FFMA2/FADD2/FMUL2): two queries per
-// instruction, which halves the issue slots of the FP32 inner loops (they are
-// issue-bound with scalar FP32: ncu showed 84% issue-slot utilisation at 56%
-// of FP32 peak).  A scalar operand {s, s} becomes the .F32 broadcast form.
-__device__ __forceinline__ float2 sub2s(float s, float2 q) {  // s - q
-  float2 d;
-  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%2};\n\tmov.b64 rb, {%3,%4};\n\t"
-      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y) : "f"(s), "f"(q.x), "f"(q.y));
-  return d;
-}
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
-  float2 d;
-  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
-      "mov.b64 rc, {%6,%7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return d;
-}
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
-  float2 d;
-  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
-      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 mul2s(float s, float2 b) {
-  float2 d;
-  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%2};\n\tmov.b64 rb, {%3,%4};\n\t"
-      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y) : "f"(s), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 add2s(float2 a, float s) {
-  float2 d;
-  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%4};\n\t"
-      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(s));
-  return d;
-}
-
-// FP32 tile loop: P packs of 2 queries against jmax staged sources
-// {x, y, z, m}.  Per source and pack: 3 FADD2, 3 FFMA2 (r^2 + eps^2),
-// 2 MUFU.RSQ, 3 FMUL2 (m r^-3), 3 FFMA2 (accumulate) = 20 FLOP per pair in
-// 7 issue slots per pair.  kGuard handles eps == 0 (coincident points).
-template <int P, bool kGuard>
-__device__ __forceinline__ void direct_tile32(const float4* __restrict__ sm, int jmax,
-                                              const float2 (&qx)[P], const float2 (&qy)[P],
-                                              const float2 (&qz)[P], float eps2,
-                                              float2 (&ax)[P], float2 (&ay)[P],
-                                              float2 (&az)[P]) {
-  const float2 e2 = make_float2(eps2, eps2);
-#pragma unroll 4
-  for (int j = 0; j < jmax; j++) {
-    const float4 s = sm[j];
-#pragma unroll
-    for (int k = 0; k < P; k++) {
-      const float2 dx = sub2s(s.x, qx[k]), dy = sub2s(s.y, qy[k]), dz = sub2s(s.z, qz[k]);
-      const float2 r2 = fma2(dx, dx, fma2(dy, dy, fma2(dz, dz, e2)));
-      float2 inv;
-      inv.x = rsqrt_approx(r2.x);
-      inv.y = rsqrt_approx(r2.y);
-      float2 w = mul2(mul2s(s.w, inv), mul2(inv, inv));
-      if (kGuard) {
-        if (!(r2.x > 0.f)) w.x = 0.f;
-        if (!(r2.y > 0.f)) w.y = 0.f;
-      }
-      ax[k] = fma2(w, dx, ax[k]);
-      ay[k] = fma2(w, dy, ay[k]);
-      az[k] = fma2(w, dz, az[k]);
-    }
-  }
-}
-
-// fp64 brute force term (bhtree.py:158-164): w = m / d2^1.5, sum w*delta.
-__device__ __forceinline__ void direct_tile64(const double4* __restrict__ sm, int jmax, double qx,
-                                              double qy, double qz, double eps2, double& sx,
-                                              double& sy, double& sz) {
-  for (int j = 0; j < jmax; j++) {
-    const double4 s = sm[j];
-    const double dx = __dsub_rn(qx, s.x), dy = __dsub_rn(qy, s.y), dz = __dsub_rn(qz, s.z);
-    const double d2 = __dadd_rn(
-        __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)), eps2);
-    const double w = d2 > 0.0 ? __ddiv_rn(s.w, __dmul_rn(d2, __dsqrt_rn(d2))) : 0.0;
-    sx = __dadd_rn(sx, __dmul_rn(w, dx));
-    sy = __dadd_rn(sy, __dmul_rn(w, dy));
-    sz = __dadd_rn(sz, __dmul_rn(w, dz));
-  }
-}
+// (kTile: fga_device.cuh)
 
 template <bool kGuard>
 __global__ void __launch_bounds__(kForceThreads, 3) k_direct_iterate32(
@@ -717,38 +384,6 @@ __global__ void __launch_bounds__(kForceThreads) k_direct_operator64(
 }
 
 // ---------------------------------------------------------------- energy
-__device__ __forceinline__ float rcp_approx(float x) {
-  float r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-__device__ __forceinline__ float sqrt_approx(float x) {
-  float r;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-  return r;
-}
-
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-  float2 d;
-  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
-      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ float2 fma2s(float s, float2 b, float2 c) {  // s*b + c
-  float2 d;
-  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2,%2};\n\tmov.b64 rb, {%3,%4};\n\t"
-      "mov.b64 rc, {%5,%6};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y) : "f"(s), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return d;
-}
-
-// K11 energy.  Per pair: |y - x| (MUFU.SQRT) and 1/(|y - x| + eps).  The two
-// MUFU ops per pair make the scalar kernel MUFU-bound (16/clk/SM), so half of
-// the pairs (pack 1) compute the reciprocal on the FMA pipe instead: a
-// bit-trick seed and three Newton steps on w = -1/x (w' = w (2 + x w), error
-// 0.125^8 ~ 6e-8), in packed FP32x2 arithmetic.  FP32 within a tile, fp64
-// across tiles and across queries (<= 1e-6 relative, tested).
 template <bool kNewton>
 __global__ void __launch_bounds__(kForceThreads, 3) k_gpe32(const float4* __restrict__ src,
                                                             int64_t n,
@@ -775,49 +410,13 @@ __global__ void __launch_bounds__(kForceThreads, 3) k_gpe32(const float4* __rest
   double acc[Q];
 #pragma unroll
   for (int k = 0; k < Q; k++) acc[k] = 0.0;
-  const float2 e2 = make_float2(eps, eps);
-  const float2 two = make_float2(2.f, 2.f);
   for (int64_t t0 = 0; t0 < n; t0 += kTile) {
     const int jmax = (int)((n - t0) < (int64_t)kTile ? (n - t0) : (int64_t)kTile);
     __syncthreads();
     for (int j = threadIdx.x; j < jmax; j += kForceThreads) sm[j] = __ldg(&src[t0 + j]);
     __syncthreads();
     float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
-#pragma unroll 4
-    for (int j = 0; j < jmax; j++) {
-      const float4 s = sm[j];
-      {  // pack 0: MUFU reciprocal
-        const float2 dx = sub2s(s.x, qx[0]), dy = sub2s(s.y, qy[0]), dz = sub2s(s.z, qz[0]);
-        const float2 d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
-        float2 den;
-        den.x = sqrt_approx(d2.x);
-        den.y = sqrt_approx(d2.y);
-        den = add2(den, e2);
-        float2 r;
-        r.x = rcp_approx(den.x);
-        r.y = rcp_approx(den.y);
-        a0 = fma2s(s.w, r, a0);
-      }
-      {  // pack 1: Newton reciprocal (accumulates -m/x)
-        const float2 dx = sub2s(s.x, qx[1]), dy = sub2s(s.y, qy[1]), dz = sub2s(s.z, qz[1]);
-        const float2 d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
-        float2 den;
-        den.x = sqrt_approx(d2.x);
-        den.y = sqrt_approx(d2.y);
-        den = add2(den, e2);
-        float2 w;
-        if (kNewton) {
-          w.x = __int_as_float(0xFEF311C3u - __float_as_uint(den.x));
-          w.y = __int_as_float(0xFEF311C3u - __float_as_uint(den.y));
-#pragma unroll
-          for (int it = 0; it < 3; it++) w = mul2(w, fma2(den, w, two));
-        } else {
-          w.x = -rcp_approx(den.x);
-          w.y = -rcp_approx(den.y);
-        }
-        a1 = fma2s(s.w, w, a1);
-      }
-    }
+    gpe_tile32<kNewton>(sm, jmax, qx, qy, qz, eps, a0, a1);
     acc[0] += (double)a0.x;
     acc[1] += (double)a0.y;
     acc[2] -= (double)a1.x;

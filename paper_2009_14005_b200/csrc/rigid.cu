@@ -8,7 +8,7 @@
 // (procrustes.py:23-25) up to rounding.  The 3x3 SVD is a one-sided Jacobi in
 // fp64 (no LAPACK on the device); the reflection guard and the rotation are
 // the reference's (:27-33): R = U diag(1, 1, sign det(U V^T)) V^T.
-#include "fga_session.cuh"
+#include "fga_device.cuh"
 
 namespace fga {
 namespace {
@@ -42,113 +42,6 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce(const double* __restr
     for (int j = 0; j < kReduceThreads / 32; j++) v += sm[j][threadIdx.x];
     if (direct_pairs >= 0.0 && (threadIdx.x == kAccepted || threadIdx.x == kVisits)) v = direct_pairs;
     sums[threadIdx.x] = v;
-  }
-}
-
-// ------------------------------------------------------------------ 3x3 SVD
-// One-sided Jacobi on the columns of A (3x3, row-major): A V = U S.
-__device__ void svd3(const double C[9], double U[9], double S[3], double V[9]) {
-  double A[9];
-  for (int k = 0; k < 9; k++) A[k] = C[k];
-  for (int k = 0; k < 9; k++) V[k] = (k % 4 == 0) ? 1.0 : 0.0;
-  const int P[3] = {0, 0, 1}, Q[3] = {1, 2, 2};
-  for (int sweep = 0; sweep < 30; sweep++) {
-    double off = 0.0;
-    for (int r = 0; r < 3; r++) {
-      const int p = P[r], q = Q[r];
-      double alpha = 0.0, beta = 0.0, gamma = 0.0;
-      for (int k = 0; k < 3; k++) {
-        alpha += A[3 * k + p] * A[3 * k + p];
-        beta += A[3 * k + q] * A[3 * k + q];
-        gamma += A[3 * k + p] * A[3 * k + q];
-      }
-      if (gamma == 0.0) continue;
-      const double rel = fabs(gamma) / sqrt(alpha * beta);
-      off = fmax(off, rel);
-      if (!(rel > 1e-17)) continue;
-      const double zeta = (beta - alpha) / (2.0 * gamma);
-      const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-      const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-      for (int k = 0; k < 3; k++) {
-        const double ap = A[3 * k + p], aq = A[3 * k + q];
-        A[3 * k + p] = c * ap - s * aq;
-        A[3 * k + q] = s * ap + c * aq;
-        const double vp = V[3 * k + p], vq = V[3 * k + q];
-        V[3 * k + p] = c * vp - s * vq;
-        V[3 * k + q] = s * vp + c * vq;
-      }
-    }
-    if (off < 1e-16) break;
-  }
-  // singular values = column norms, sorted descending (LAPACK order)
-  int ord[3] = {0, 1, 2};
-  double nrm[3];
-  for (int j = 0; j < 3; j++)
-    nrm[j] = sqrt(A[j] * A[j] + A[3 + j] * A[3 + j] + A[6 + j] * A[6 + j]);
-  for (int a = 0; a < 2; a++)
-    for (int b = 0; b < 2 - a; b++)
-      if (nrm[ord[b]] < nrm[ord[b + 1]]) {
-        int tmp = ord[b];
-        ord[b] = ord[b + 1];
-        ord[b + 1] = tmp;
-      }
-  double Vs[9];
-  for (int j = 0; j < 3; j++) {
-    S[j] = nrm[ord[j]];
-    for (int k = 0; k < 3; k++) {
-      Vs[3 * k + j] = V[3 * k + ord[j]];
-      U[3 * k + j] = S[j] > 0.0 ? A[3 * k + ord[j]] / S[j] : 0.0;
-    }
-  }
-  for (int k = 0; k < 9; k++) V[k] = Vs[k];
-  // Orthonormal completion: u1 normalized, u2 Gram-Schmidt, u3 = u1 x u2.
-  double u1[3] = {U[0], U[3], U[6]}, u2[3] = {U[1], U[4], U[7]};
-  double n1 = sqrt(u1[0] * u1[0] + u1[1] * u1[1] + u1[2] * u1[2]);
-  if (!(n1 > 0.0)) {
-    u1[0] = 1.0;
-    u1[1] = u1[2] = 0.0;
-    n1 = 1.0;
-  }
-  for (int k = 0; k < 3; k++) u1[k] /= n1;
-  double d12 = u1[0] * u2[0] + u1[1] * u2[1] + u1[2] * u2[2];
-  for (int k = 0; k < 3; k++) u2[k] -= d12 * u1[k];
-  double n2 = sqrt(u2[0] * u2[0] + u2[1] * u2[1] + u2[2] * u2[2]);
-  if (!(n2 > 1e-300)) {  // rank <= 1: any unit vector orthogonal to u1
-    const int a = fabs(u1[0]) < 0.9 ? 0 : 1;
-    double e[3] = {0, 0, 0};
-    e[a] = 1.0;
-    d12 = u1[a];
-    for (int k = 0; k < 3; k++) u2[k] = e[k] - d12 * u1[k];
-    n2 = sqrt(u2[0] * u2[0] + u2[1] * u2[1] + u2[2] * u2[2]);
-  }
-  for (int k = 0; k < 3; k++) u2[k] /= n2;
-  const double u3[3] = {u1[1] * u2[2] - u1[2] * u2[1], u1[2] * u2[0] - u1[0] * u2[2],
-                        u1[0] * u2[1] - u1[1] * u2[0]};
-  for (int k = 0; k < 3; k++) {
-    U[3 * k] = u1[k];
-    U[3 * k + 1] = u2[k];
-    U[3 * k + 2] = u3[k];
-  }
-}
-
-__device__ __forceinline__ double det3(const double M[9]) {
-  return M[0] * (M[4] * M[8] - M[5] * M[7]) - M[1] * (M[3] * M[8] - M[5] * M[6]) +
-         M[2] * (M[3] * M[7] - M[4] * M[6]);
-}
-
-// procrustes.solve_rotation (procrustes.py:12-35) from the cross-covariance.
-__device__ void kabsch_rotation(const double C[9], double R[9], int* degenerate) {
-  double U[9], S[3], V[9];
-  svd3(C, U, S, V);
-  // sign(det(U Vt)) (:28-30); det(U) = +1 by construction
-  double sgn = det3(V) < 0.0 ? -1.0 : 1.0;
-  for (int i = 0; i < 3; i++)
-    for (int j = 0; j < 3; j++)
-      R[3 * i + j] = U[3 * i] * V[3 * j] + U[3 * i + 1] * V[3 * j + 1] + sgn * U[3 * i + 2] * V[3 * j + 2];
-  if (degenerate) {
-    const double tol = 1e-12 * fmax(S[0], 1e-300);  // _DEGENERATE_REL_TOL (:8)
-    int rank = (S[0] > tol) + (S[1] > tol) + (S[2] > tol);
-    *degenerate = rank < 2;
   }
 }
 

@@ -11,7 +11,7 @@
 #include <cub/cub.cuh>
 
 #include "../../include/fga.h"
-#include "fga_session.cuh"
+#include "fga_device.cuh"
 
 namespace fga {
 namespace {
@@ -134,16 +134,6 @@ __global__ void k_norm_apply(const double* __restrict__ x, int64_t n, const doub
 }
 
 // ---------------------------------------------------------------- NIV
-// idx = clip(floor((p - a) / edge), 0, rho-1) with numpy's float->int64 cast
-// (out-of-range values become INT64_MIN, then clip to 0).
-__device__ __forceinline__ long long niv_axis(double p, double a, double edge, int rho) {
-  const double f = floor(__ddiv_rn(__dsub_rn(p, a), edge));
-  long long v;
-  if (!(f >= -9.223372036854775808e18 && f < 9.223372036854775808e18)) v = LLONG_MIN;
-  else v = (long long)f;
-  return v < 0 ? 0 : (v > rho - 1 ? rho - 1 : v);
-}
-
 __global__ void k_niv_hist(const double* __restrict__ pts, int64_t n, int rho, double a,
                            double edge, int* __restrict__ flat,
                            unsigned long long* __restrict__ counts) {

@@ -32,6 +32,7 @@
 
 #include "fga_internal.cuh"
 #include "fga_tree.cuh"
+#include "fga_device.cuh"
 #include "../../include/fga.h"
 
 namespace fga {
@@ -119,13 +120,6 @@ __global__ void k_keys(const double* __restrict__ pts, int64_t n, const double* 
   idx[i] = (int)i;
 }
 
-__device__ __forceinline__ int common_levels(unsigned long long a, unsigned long long b, int L) {
-  unsigned long long x = a ^ b;
-  if (x == 0ull) return L;
-  int lz = __clzll((long long)x) - (64 - 3 * L);
-  return lz / 3;
-}
-
 // c_i for i in [0, N] and the number of nodes each point starts.
 __global__ void k_levels(const unsigned long long* __restrict__ keys, int64_t n, int L,
                          signed char* __restrict__ clev, int* __restrict__ count) {
@@ -164,29 +158,6 @@ __device__ __forceinline__ int64_t lower_bound_key(const unsigned long long* key
     if (keys[mid] >= bound) hi = mid; else lo = mid + 1;
   }
   return lo;
-}
-
-__device__ __forceinline__ unsigned long long low_mask(int bits) {
-  return bits >= 64 ? ~0ull : ((1ull << bits) - 1ull);
-}
-
-// Replays the bbox of the node at level `l` on the path of `key`.
-__device__ __forceinline__ void node_bbox(unsigned long long key, int l, int L,
-                                          const double* __restrict__ box, double lo[3],
-                                          double hi[3]) {
-#pragma unroll
-  for (int k = 0; k < 3; k++) {
-    lo[k] = box[k];
-    hi[k] = box[3 + k];
-  }
-  for (int lev = 1; lev <= l; lev++) {
-    unsigned digit = (unsigned)(key >> (3 * (L - lev))) & 7u;
-#pragma unroll
-    for (int k = 0; k < 3; k++) {
-      double c = __dadd_rn(lo[k], __dmul_rn(__dsub_rn(hi[k], lo[k]), 0.5));
-      if ((digit >> (2 - k)) & 1u) lo[k] = c; else hi[k] = c;
-    }
-  }
 }
 
 __global__ void k_emit(const unsigned long long* __restrict__ keys, int64_t n, int L,

@@ -130,6 +130,80 @@ def _result_from_c(res, deltas, traj, gtrace, inter, options) -> RegistrationRes
 
 
 @dataclass
+class BatchResult:
+    """Outcome of register_batch: one entry per pair; a pair that failed
+    (empty / degenerate / unsupported) has results[i] = None and errors[i]
+    set, the others are unaffected (like register_sequence's per-pair
+    failure handling, registration.py:192-200)."""
+
+    results: list
+    errors: list
+    interactions: np.ndarray | None = None
+
+
+def register_batch(pairs, params: FgaParams | None = None,
+                   options: RegisterOptions | None = None) -> BatchResult:
+    """register(x, y) for many independent (x, y) pairs in ONE persistent
+    device kernel (BASELINE configs[4]; csrc/batched.cu).  Each cloud may hold
+    up to 8192 points.  Landmarks are not supported; external weights in
+    options.x_weights / y_weights must be lists (one array per pair)."""
+    params = params or default_params()
+    options = options or RegisterOptions()
+    validate(params)
+    pairs = list(pairs)
+    P = len(pairs)
+    if P == 0:
+        return BatchResult([], [], np.zeros(0, np.int64))
+    xs, ys = [], []
+    for x, y in pairs:
+        if x.dim != y.dim:
+            raise EmptyCloud(f"dimension mismatch: {x.dim} vs {y.dim}")
+        xs.append(x.points)
+        ys.append(y.points)
+    xoff = np.zeros(P + 1, np.int64)
+    yoff = np.zeros(P + 1, np.int64)
+    xoff[1:] = np.cumsum([len(a) for a in xs])
+    yoff[1:] = np.cumsum([len(a) for a in ys])
+    X = np.ascontiguousarray(np.concatenate(xs) if xoff[-1] else np.zeros((0, 3)))
+    Y = np.ascontiguousarray(np.concatenate(ys) if yoff[-1] else np.zeros((0, 3)))
+    xw = yw = None
+    if options.x_weights is not None:
+        xw = np.ascontiguousarray(np.concatenate(
+            [check_weights(len(a), w) for a, w in zip(xs, options.x_weights)]))
+    if options.y_weights is not None:
+        yw = np.ascontiguousarray(np.concatenate(
+            [check_weights(len(a), w) for a, w in zip(ys, options.y_weights)]))
+    c = N.context(options.device)
+    out = (N.CPairResult * P)()
+    deltas = np.zeros((P, params.max_iters)) if options.record_iterations else None
+    cp = N.make_params(params)
+    co = _c_options(options, xw, yw)
+    N.check(N.lib().fga_register_batch(c.handle, N.ptr(X), N.ptr(xoff), N.ptr(Y), N.ptr(yoff), P,
+                                       pairs[0][0].dim, N.ctypes.byref(cp), N.ctypes.byref(co),
+                                       N.ctypes.addressof(out), N.ptr(deltas)))
+    results, errors = [], []
+    inter = np.zeros(P, np.int64)
+    for i, r in enumerate(out):
+        inter[i] = r.interactions
+        if r.status != 0:
+            results.append(None)
+            errors.append(N.error_for(r.status, f"pair {i}"))
+            continue
+        it = int(r.iterations)
+        recs = []
+        if deltas is not None:
+            recs = [IterationRecord(index=k, transform_delta=float(deltas[i, k])) for k in range(it)]
+        results.append(RegistrationResult(
+            transform=RigidTransform(np.array(r.R).reshape(3, 3), np.array(r.t)),
+            iterations=it, gpe_trace=[], converged=bool(r.converged),
+            gpe_initial=float(r.gpe_initial) if options.compute_gpe else None,
+            gpe_final=float(r.gpe_final) if options.compute_gpe else None,
+            records=recs, interactions=None))
+        errors.append(None)
+    return BatchResult(results, errors, inter)
+
+
+@dataclass
 class SequenceResult:
     """Pairwise frame transforms plus composed absolute poses
     (registration.py:169-175)."""
