@@ -205,6 +205,7 @@ def run_ours(args, rank, world, local_rank):
     visits_total = None
     interactions = float(inter.sum())
     value = interactions / (total_ms / 1e3)
+    batched = None if args.no_batched else run_batched(args, rank, world)  # every rank
     if rank != 0:
         return None
 
@@ -248,10 +249,8 @@ def run_ours(args, rank, world, local_rank):
         line["registration"] = run_registration(args, x, y)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, x, y, args.cpu_sample)
-    if not args.no_batched:
-        b = run_batched(args, rank, world)
-        if b is not None:
-            line["batched"] = b
+    if batched is not None:
+        line["batched"] = batched
     return line
 
 
