@@ -63,6 +63,8 @@ typedef struct {
   int32_t poll_every;        /* iterations enqueued between host polls of the
                                 device convergence flag (0 = default 8)       */
   int32_t compute_gpe;       /* 1 (default semantics): gpe_initial/final      */
+  int32_t mass_field;        /* 0 = NIV lattice (reference default), 1 = kNN  */
+  int32_t knn_k;             /* k for mass_field = 1 (default 16, <= 32)      */
 } fga_options;
 
 /* Mirrors registration.RegistrationResult (core.py:162-172). */
@@ -219,6 +221,14 @@ int fga_direct_forces(fga_ctx* ctx, const double* ref, const double* ref_masses,
 int fga_gpe_kernel(fga_ctx* ctx, const double* pos_y, const double* mass_y, int64_t m,
                    const double* pos_x, const double* mass_x, int64_t n, int dim, double G,
                    double eps, int precision, double* out);
+/* Exact k nearest OTHER points of every point (grid-bucketed, fp64 distances,
+ * ties broken by index): idx (n,k) int64 and squared distances (n,k), either
+ * may be NULL.  1 <= k < n, k <= 32. */
+int fga_knn(fga_ctx* ctx, const double* pts, int64_t n, int dim, int k, int64_t* idx,
+            double* d2);
+/* kNN smooth-particle masses: (4/3) pi r_k^3 / k, floored at 1e-6 (an opt-in
+ * alternative to niv_masses, BASELINE configs[3]). */
+int fga_knn_masses(fga_ctx* ctx, const double* pts, int64_t n, int dim, int k, double* out);
 /* masses.niv_masses (masses.py:85-116). */
 int fga_niv_masses(fga_ctx* ctx, const double* pts, int64_t n, int dim, int rho, double a,
                    double b, int max_depth, double* out);

@@ -59,7 +59,8 @@ class COptions(ctypes.Structure):
 
     _fields_ = [("trace_gpe", _i32), ("normalize", _i32), ("record_iterations", _i32),
                 ("precision", _i32), ("x_weights", _vp), ("y_weights", _vp),
-                ("poll_every", _i32), ("compute_gpe", _i32)]
+                ("poll_every", _i32), ("compute_gpe", _i32), ("mass_field", _i32),
+                ("knn_k", _i32)]
 
 
 class CResult(ctypes.Structure):
@@ -125,6 +126,8 @@ SIGNATURES = {
                                    _c_int, _vp]),
     "fga_gpe_kernel": (_c_int, [_vp, _vp, _vp, _i64, _vp, _vp, _i64, _c_int, _dbl, _dbl, _c_int,
                                 ctypes.POINTER(_dbl)]),
+    "fga_knn": (_c_int, [_vp, _vp, _i64, _c_int, _c_int, _vp, _vp]),
+    "fga_knn_masses": (_c_int, [_vp, _vp, _i64, _c_int, _c_int, _vp]),
     "fga_niv_masses": (_c_int, [_vp, _vp, _i64, _c_int, _c_int, _dbl, _dbl, _c_int, _vp]),
     "fga_normalize_pair": (_c_int, [_vp, _vp, _i64, _vp, _i64, _c_int, _dbl, _dbl, _vp, _vp,
                                     _vp]),

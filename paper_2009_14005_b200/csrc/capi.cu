@@ -195,6 +195,9 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
     TRY(h2d(S.scratch, S.O.x_weights, n, s));
     launch_external_masses(S.scratch.as<double>(), n, S.mx.as<double>(), s);
     FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  } else if (S.O.mass_field == 1) {
+    TRY(knn_dev(S.xn.as<double>(), n, S.O.knn_k, nullptr, nullptr, S.mx.as<double>(), S.scratch,
+                S.cub_tmp, s));
   } else {
     TRY(niv_masses_dev(S.xn.as<double>(), n, S.P.rho, ca, cb, S.P.max_depth, S.mx.as<double>(),
                        S.flat.as<int>(), S.counts.as<long long>(), S.cells.as<double>(), s));
@@ -203,6 +206,9 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
     TRY(h2d(S.scratch, S.O.y_weights, m, s));
     launch_external_masses(S.scratch.as<double>(), m, S.my.as<double>(), s);
     FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  } else if (S.O.mass_field == 1) {
+    TRY(knn_dev(S.yn.as<double>(), m, S.O.knn_k, nullptr, nullptr, S.my.as<double>(), S.scratch,
+                S.cub_tmp, s));
   } else {
     TRY(niv_masses_dev(S.yn.as<double>(), m, S.P.rho, ca, cb, S.P.max_depth, S.my.as<double>(),
                        S.flat.as<int>(), S.counts.as<long long>(), S.cells.as<double>(), s));
@@ -268,6 +274,11 @@ int session_begin_common(fga_ctx* c, int64_t n, int64_t m, int dim, const fga_pa
   def.compute_gpe = 1;
   S.O = options ? *options : def;
   if (S.O.poll_every <= 0) S.O.poll_every = 8;
+  if (S.O.knn_k <= 0) S.O.knn_k = 16;
+  if (S.O.mass_field == 1 && (S.O.knn_k >= n || S.O.knn_k >= m || S.O.knn_k > 32)) {
+    set_error("invalid parameter knn_k=" + std::to_string(S.O.knn_k));
+    return FGA_ERR_INVALID;
+  }
   S.precision = S.O.precision ? 1 : 0;
   S.direct = params->theta == 0.0;
   S.n = n;
@@ -1000,6 +1011,43 @@ int fga_gpe_kernel(fga_ctx* c, const double* pos_y, const double* mass_y, int64_
   FGA_CUDA_TRY(cudaMemcpyAsync(&v, sums.as<double>() + kGpe, sizeof(double), cudaMemcpyDeviceToHost, s));
   FGA_CUDA_TRY(cudaStreamSynchronize(s));
   *value = -G * v;
+  return FGA_OK;
+}
+
+int fga_knn(fga_ctx* c, const double* pts, int64_t n, int dim, int k, int64_t* idx, double* d2) {
+  CTX_TRY(c);
+  if (dim != 3) {
+    set_error("the B200 path implements D=3 (D=2 is not built yet)");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  if (n <= 0) return FGA_OK;
+  cudaStream_t s = c->stream;
+  DevBuf &p = c->op[0], &oi = c->op[1], &od = c->op[2], &sc = c->op[3], &tmp = c->op[4];
+  TRY(h2d(p, pts, 3 * n, s));
+  FGA_CUDA_TRY(oi.reserve(sizeof(long long) * n * std::max(k, 1)));
+  FGA_CUDA_TRY(od.reserve(sizeof(double) * n * std::max(k, 1)));
+  TRY(knn_dev(p.as<double>(), n, k, idx ? oi.as<long long>() : nullptr,
+              d2 ? od.as<double>() : nullptr, nullptr, sc, tmp, s));
+  if (idx) FGA_CUDA_TRY(cudaMemcpyAsync(idx, oi.p, sizeof(long long) * n * k, cudaMemcpyDeviceToHost, s));
+  if (d2) FGA_CUDA_TRY(cudaMemcpyAsync(d2, od.p, sizeof(double) * n * k, cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  return FGA_OK;
+}
+
+int fga_knn_masses(fga_ctx* c, const double* pts, int64_t n, int dim, int k, double* out) {
+  CTX_TRY(c);
+  if (dim != 3) {
+    set_error("the B200 path implements D=3 (D=2 is not built yet)");
+    return FGA_ERR_UNSUPPORTED;
+  }
+  if (n <= 0) return FGA_OK;
+  cudaStream_t s = c->stream;
+  DevBuf &p = c->op[0], &o = c->op[1], &sc = c->op[3], &tmp = c->op[4];
+  TRY(h2d(p, pts, 3 * n, s));
+  FGA_CUDA_TRY(o.reserve(sizeof(double) * n));
+  TRY(knn_dev(p.as<double>(), n, k, nullptr, nullptr, o.as<double>(), sc, tmp, s));
+  FGA_CUDA_TRY(cudaMemcpyAsync(out, o.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
   return FGA_OK;
 }
 

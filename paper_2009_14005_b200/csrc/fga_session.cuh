@@ -82,4 +82,7 @@ void launch_gather_template(const double* pts_aos, const double* mass, const int
 void launch_gather_queries(const double* q_aos, const double* qm, const int* order, int64_t m,
                            double* qx, double* qy, double* qz, double* qms, cudaStream_t s);
 
+int knn_dev(const double* pts, int64_t n, int k, long long* out_idx, double* out_d2,
+            double* out_mass, DevBuf& scratch, DevBuf& cub_tmp, cudaStream_t s);
+
 }  // namespace fga

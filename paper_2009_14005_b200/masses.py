@@ -67,6 +67,29 @@ def niv_masses(cloud: PointCloud, rho: int, ctx: NormalizationContext, max_depth
     return out
 
 
+def knn(cloud: PointCloud, k: int = 16):
+    """Exact k nearest OTHER points of every point on the device (grid
+    bucketing, fp64 distances, ties by index): (idx (n,k) int64, d2 (n,k))."""
+    n = len(cloud)
+    idx = np.empty((n, k), np.int64)
+    d2 = np.empty((n, k))
+    c = N.context()
+    N.check(N.lib().fga_knn(c.handle, N.ptr(cloud.points), n, cloud.dim, int(k), N.ptr(idx),
+                            N.ptr(d2)))
+    return idx, d2
+
+
+def knn_masses(cloud: PointCloud, k: int = 16):
+    """kNN smooth-particle masses (BASELINE configs[3]; not a reference
+    feature): (4/3) pi r_k^3 / k, floored at MASS_FLOOR.  Use through
+    RegisterOptions(mass_field="knn") or as x/y_weights."""
+    out = np.empty(len(cloud))
+    c = N.context()
+    N.check(N.lib().fga_knn_masses(c.handle, N.ptr(cloud.points), len(cloud), cloud.dim, int(k),
+                                   N.ptr(out)))
+    return out
+
+
 def rbf_masses(cloud: PointCloud, anchors, sigma: float):
     """Landmark RBF field (masses.py:55-82): not on the B200 path yet."""
     if sigma <= 0:

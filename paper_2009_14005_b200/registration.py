@@ -52,16 +52,21 @@ class RegisterOptions:
     poll_every: int = 8
     device: int | None = None
     compute_gpe: bool = True
+    mass_field: str = "niv"   # "niv" (reference SPM default) or "knn" (configs[3])
+    knn_k: int = 16
 
 
 def _c_options(options: RegisterOptions, xw, yw) -> N.COptions:
     if options.precision not in ("fp32", "fp64"):
         raise GravregError(f"precision must be 'fp32' or 'fp64', got {options.precision!r}")
+    if options.mass_field not in ("niv", "knn"):
+        raise GravregError(f"mass_field must be 'niv' or 'knn', got {options.mass_field!r}")
     return N.COptions(int(bool(options.trace_gpe)), int(bool(options.normalize)),
                       int(bool(options.record_iterations)),
                       N.PREC_FP64 if options.precision == "fp64" else N.PREC_FP32,
                       N.ptr(xw), N.ptr(yw), int(options.poll_every),
-                      int(bool(options.compute_gpe)))
+                      int(bool(options.compute_gpe)), 1 if options.mass_field == "knn" else 0,
+                      int(options.knn_k))
 
 
 def _check_inputs(x, y, landmarks, params, options):
