@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--direct-steps", type=int, default=3)
     ap.add_argument("--no-batched", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the configs[1]/configs[3] registration legs")
     ap.add_argument("--batch-pairs", type=int, default=4096)
     ap.add_argument("--cpu-sample", type=int, default=65536)
     ap.add_argument("--default-g", action="store_true",
@@ -251,6 +253,8 @@ def run_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = cpu_baseline(args, x, y, args.cpu_sample)
     if batched is not None:
         line["batched"] = batched
+    if world == 1 and not args.no_configs:
+        line["configs"] = run_other_configs(args)
     return line
 
 
@@ -399,6 +403,49 @@ def run_batched(args, rank, world):
             "failed": int(sum(e is not None for e in br.errors)),
             "api": "register_batch (fga_register_batch: one persistent kernel, host buffers)",
             "sharding": f"pairs split over {world} GPU(s), no collective"}
+
+
+def run_other_configs(args):
+    """configs[1] (100k LiDAR-shaped pair) and configs[3] (200k partial
+    overlap, 5% outliers, inhomogeneous density, kNN-16 masses): one full
+    register() each from host numpy, theta 0.5, G*sqrt(2000/N)."""
+    import paper_2009_14005_b200 as fga
+    from paper_2009_14005_b200 import synth
+    out = {}
+    rng = synth.rng_from_seed(2)
+    x = synth.lidar_scan(100_000, rng)
+    gt = synth.random_rigid(rng, np.deg2rad(10), 1.0)
+    y = synth.misalign(x, gt)
+    p = fga.default_params().replace(theta=0.5, G=66.7 * (2000.0 / len(x)) ** 0.5)
+    fga.register(fga.PointCloud(x.points[:5000]), fga.PointCloud(y.points[:5000]), params=p)
+    t0 = time.perf_counter()
+    r = fga.register(x, y, params=p)
+    wall = time.perf_counter() - t0
+    out["c2_lidar_100k"] = {
+        "wall_s": wall, "iterations": r.iterations, "converged": r.converged,
+        "rotation_err_deg": fga.angular_deviation(gt.rotation, r.transform.rotation),
+        "interactions_per_s_loop": float(r.interactions.sum()) / (r.timings_ms["loop"] / 1e3),
+        "timings_ms": r.timings_ms}
+    rng = synth.rng_from_seed(4)
+    x, y0 = synth.partial_overlap(200_000, rng)
+    gt = synth.random_rigid(rng, np.deg2rad(60), 0.1)
+    y = synth.misalign(y0, gt)
+    p = fga.default_params().replace(theta=0.5, G=66.7 * (2000.0 / len(x)) ** 0.5)
+    o = fga.RegisterOptions(mass_field="knn", knn_k=16)
+    from paper_2009_14005_b200 import masses
+    masses.knn_masses(x, 16)
+    t0 = time.perf_counter()
+    masses.knn_masses(x, 16)
+    knn_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    r = fga.register(x, y, params=p, options=o)
+    wall = time.perf_counter() - t0
+    out["c4_overlap_200k_knn16"] = {
+        "wall_s": wall, "iterations": r.iterations, "converged": r.converged,
+        "knn16_masses_s_200k_host_api": knn_s,
+        "interactions_per_s_loop": float(r.interactions.sum()) / (r.timings_ms["loop"] / 1e3),
+        "timings_ms": r.timings_ms}
+    return out
 
 
 def run_registration(args, x, y):
