@@ -102,6 +102,37 @@ int check_ctx(fga_ctx* c) {
     if (r_) return r_;             \
   } while (0)
 
+// D = 2 clouds ride the 3-D machinery as z = 0 (the tree then only ever
+// takes the upper z child, so topology, preorder, lengths and forces are the
+// quadtree's).  Host-side pad / unpad of (n, dim) arrays.
+struct Pad3 {
+  std::vector<double> buf;
+  const double* ptr = nullptr;
+};
+Pad3 pad3(const double* p, int64_t n, int dim) {
+  Pad3 r;
+  if (dim == 3 || !p) {
+    r.ptr = p;
+    return r;
+  }
+  r.buf.assign((size_t)n * 3, 0.0);
+  for (int64_t i = 0; i < n; i++)
+    for (int k = 0; k < dim; k++) r.buf[i * 3 + k] = p[i * dim + k];
+  r.ptr = r.buf.data();
+  return r;
+}
+void unpad3(const double* p3, int64_t n, int dim, double* out) {
+  for (int64_t i = 0; i < n; i++)
+    for (int k = 0; k < dim; k++) out[i * dim + k] = p3[i * 3 + k];
+}
+int check_dim(int dim) {
+  if (dim != 2 && dim != 3) {
+    set_error("invalid parameter points=dimension " + std::to_string(dim));
+    return FGA_ERR_INVALID;
+  }
+  return FGA_OK;
+}
+
 int invalid(const char* name, double v) {
   set_error(std::string("invalid parameter ") + name + "=" + std::to_string(v));
   return FGA_ERR_INVALID;
@@ -186,7 +217,7 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
   // mass fields (registration.py:64-88)
   FGA_CUDA_TRY(S.mx.reserve(sizeof(double) * n));
   FGA_CUDA_TRY(S.my.reserve(sizeof(double) * m));
-  const int64_t ncell = (int64_t)S.P.rho * S.P.rho * S.P.rho;
+  const int64_t ncell = (int64_t)S.P.rho * S.P.rho * (S.sp.dim == 3 ? S.P.rho : 1);
   FGA_CUDA_TRY(S.flat.reserve(sizeof(int) * std::max(n, m)));
   FGA_CUDA_TRY(S.counts.reserve(sizeof(long long) * (ncell + 1)));
   FGA_CUDA_TRY(S.cells.reserve(sizeof(double) * ncell));
@@ -196,10 +227,10 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
     launch_external_masses(S.scratch.as<double>(), n, S.mx.as<double>(), s);
     FGA_CUDA_TRY(cudaStreamSynchronize(s));
   } else if (S.O.mass_field == 1) {
-    TRY(knn_dev(S.xn.as<double>(), n, S.O.knn_k, nullptr, nullptr, S.mx.as<double>(), S.scratch,
-                S.cub_tmp, s));
+    TRY(knn_dev(S.xn.as<double>(), n, S.sp.dim, S.O.knn_k, nullptr, nullptr, S.mx.as<double>(),
+                S.scratch, S.cub_tmp, s));
   } else {
-    TRY(niv_masses_dev(S.xn.as<double>(), n, S.P.rho, ca, cb, S.P.max_depth, S.mx.as<double>(),
+    TRY(niv_masses_dev(S.xn.as<double>(), n, S.sp.dim, S.P.rho, ca, cb, S.P.max_depth, S.mx.as<double>(),
                        S.flat.as<int>(), S.counts.as<long long>(), S.cells.as<double>(), s));
   }
   if (S.O.y_weights) {
@@ -207,17 +238,20 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
     launch_external_masses(S.scratch.as<double>(), m, S.my.as<double>(), s);
     FGA_CUDA_TRY(cudaStreamSynchronize(s));
   } else if (S.O.mass_field == 1) {
-    TRY(knn_dev(S.yn.as<double>(), m, S.O.knn_k, nullptr, nullptr, S.my.as<double>(), S.scratch,
-                S.cub_tmp, s));
+    TRY(knn_dev(S.yn.as<double>(), m, S.sp.dim, S.O.knn_k, nullptr, nullptr, S.my.as<double>(),
+                S.scratch, S.cub_tmp, s));
   } else {
-    TRY(niv_masses_dev(S.yn.as<double>(), m, S.P.rho, ca, cb, S.P.max_depth, S.my.as<double>(),
+    TRY(niv_masses_dev(S.yn.as<double>(), m, S.sp.dim, S.P.rho, ca, cb, S.P.max_depth, S.my.as<double>(),
                        S.flat.as<int>(), S.counts.as<long long>(), S.cells.as<double>(), s));
   }
   FGA_CUDA_TRY(S.scratch.reserve(sizeof(double) * 8192));
   launch_rescale(S.mx.as<double>(), n, S.my.as<double>(), m, S.P.dt, S.P.eta,
                  S.scratch.as<double>(), s);
   // reference side: tree (BH) and packed points (direct sum, energy)
-  if (!S.direct) TRY(tree_build_dev(c->tree, S.xn.as<double>(), S.mx.as<double>(), n, S.P.max_depth, s));
+  if (!S.direct) {
+    TRY(tree_build_dev(c->tree, S.xn.as<double>(), S.mx.as<double>(), n, S.P.max_depth, s));
+    c->tree.dim = S.sp.dim;
+  }
   FGA_CUDA_TRY(S.ref32.reserve(sizeof(float4) * n));
   if (S.precision) FGA_CUDA_TRY(S.ref64.reserve(sizeof(double4) * n));
   launch_pack_ref(S.xn.as<double>(), S.mx.as<double>(), n, S.ref32.as<float4>(),
@@ -258,10 +292,7 @@ int session_begin_common(fga_ctx* c, int64_t n, int64_t m, int dim, const fga_pa
     set_error("registration requires a non-empty cloud");
     return FGA_ERR_EMPTY;
   }
-  if (dim != 3) {
-    set_error("the B200 path implements D=3 (D=2 is not built yet)");
-    return FGA_ERR_UNSUPPORTED;
-  }
+  TRY(check_dim(dim));
   if (shard_count < 1 || shard_rank < 0 || shard_rank >= shard_count) {
     set_error("invalid shard_rank/shard_count");
     return FGA_ERR_INVALID;
@@ -296,6 +327,7 @@ int session_begin_common(fga_ctx* c, int64_t n, int64_t m, int dim, const fga_pa
   S.sp.max_iters = params->max_iters;
   S.sp.m_total = m;
   S.sp.trace_gpe = S.O.trace_gpe;
+  S.sp.dim = dim;
   S.gpe_initial = S.gpe_final = NAN;
   S.have_gpe_initial = S.have_gpe_final = false;
   S.applied = false;
@@ -498,6 +530,10 @@ int fga_session_begin_dev(fga_ctx* c, const double* x_dev, int64_t n, const doub
                           int64_t m, int dim, const fga_params* params,
                           const fga_options* options, int shard_rank, int shard_count) {
   CTX_TRY(c);
+  if (dim != 3) {
+    set_error("fga_session_begin_dev: device inputs must be (n, 3)");
+    return FGA_ERR_UNSUPPORTED;
+  }
   TRY(session_begin_common(c, n, m, dim, params, options, shard_rank, shard_count));
   TRY(session_setup(c, x_dev, y_dev));
   c->S.active = true;
@@ -510,8 +546,10 @@ int fga_session_begin(fga_ctx* c, const double* x, int64_t n, const double* y, i
   CTX_TRY(c);
   TRY(session_begin_common(c, n, m, dim, params, options, shard_rank, shard_count));
   Session& S = c->S;
-  TRY(h2d(S.x_raw, x, 3 * n, c->stream));
-  TRY(h2d(S.y_raw, y, 3 * m, c->stream));
+  const Pad3 px = pad3(x, n, dim), py = pad3(y, m, dim);
+  TRY(h2d(S.x_raw, px.ptr, 3 * n, c->stream));
+  TRY(h2d(S.y_raw, py.ptr, 3 * m, c->stream));
+  FGA_CUDA_TRY(cudaStreamSynchronize(c->stream));  // pad buffers die here
   TRY(session_setup(c, S.x_raw.as<double>(), S.y_raw.as<double>()));
   S.active = true;
   return FGA_OK;
@@ -860,19 +898,18 @@ int fga_register_batch(fga_ctx* c, const double* x_all, const int64_t* x_offsets
 int fga_tree_build(fga_ctx* c, const double* pts, const double* masses, int64_t n, int dim,
                    int max_depth, int64_t* n_nodes) {
   CTX_TRY(c);
+  TRY(check_dim(dim));
   if (n <= 0) {
     set_error("registration requires a non-empty cloud");
     return FGA_ERR_EMPTY;
   }
-  if (dim != 3) {
-    set_error("the B200 path implements D=3 (D=2 is not built yet)");
-    return FGA_ERR_UNSUPPORTED;
-  }
-  TRY(h2d(c->tree_pts, pts, 3 * n, c->stream));
+  const Pad3 pp = pad3(pts, n, dim);
+  TRY(h2d(c->tree_pts, pp.ptr, 3 * n, c->stream));
   TRY(h2d(c->tree_masses, masses, n, c->stream));
   TRY(tree_build_dev(c->tree, c->tree_pts.as<double>(), c->tree_masses.as<double>(), n, max_depth,
                      c->stream));
   FGA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->tree.dim = dim;
   if (n_nodes) *n_nodes = c->tree.n_nodes;
   return FGA_OK;
 }
@@ -880,18 +917,46 @@ int fga_tree_build(fga_ctx* c, const double* pts, const double* masses, int64_t 
 int fga_tree_export(fga_ctx* c, int64_t* children, double* com, double* mass, double* length,
                     int64_t* occupancy, int64_t* depth, double* bbox_min, double* bbox_max) {
   CTX_TRY(c);
-  return tree_export_host(c->tree, c->stream, children, com, mass, length, occupancy, depth,
-                          bbox_min, bbox_max);
+  TreeDev& T = c->tree;
+  if (T.dim == 3)
+    return tree_export_host(T, c->stream, children, com, mass, length, occupancy, depth, bbox_min,
+                            bbox_max);
+  // D = 2: the z bit of every child slot is 1 (z = 0 >= centre 0), so the
+  // quadtree slot is slot3 >> 1; drop the z column of com / bbox.
+  const int64_t nn = T.n_nodes;
+  std::vector<int64_t> ch(children ? nn * 8 : 0);
+  std::vector<double> cm(com ? nn * 3 : 0), bl(bbox_min ? nn * 3 : 0), bh(bbox_max ? nn * 3 : 0);
+  TRY(tree_export_host(T, c->stream, children ? ch.data() : nullptr, com ? cm.data() : nullptr,
+                       mass, length, occupancy, depth, bbox_min ? bl.data() : nullptr,
+                       bbox_max ? bh.data() : nullptr));
+  if (children)
+    for (int64_t x = 0; x < nn; x++)
+      for (int q = 0; q < 4; q++) children[x * 4 + q] = ch[x * 8 + 2 * q + 1];
+  if (com) unpad3(cm.data(), nn, 2, com);
+  if (bbox_min) unpad3(bl.data(), nn, 2, bbox_min);
+  if (bbox_max) unpad3(bh.data(), nn, 2, bbox_max);
+  return FGA_OK;
 }
 
 int fga_tree_upload(fga_ctx* c, const int64_t* children, const double* com, const double* mass,
                     const double* length, int64_t n_nodes, int n_child, int dim) {
   CTX_TRY(c);
-  if (dim != 3) {
-    set_error("the B200 path implements D=3 (D=2 is not built yet)");
-    return FGA_ERR_UNSUPPORTED;
+  TRY(check_dim(dim));
+  if (n_child != (1 << dim)) {
+    set_error("tree upload: children must have 2^dim slots");
+    return FGA_ERR_INVALID;
   }
-  return tree_upload_host(c->tree, children, com, mass, length, n_nodes, n_child, c->stream);
+  if (dim == 3) {
+    c->tree.dim = 3;
+    return tree_upload_host(c->tree, children, com, mass, length, n_nodes, 8, c->stream);
+  }
+  std::vector<int64_t> ch((size_t)std::max<int64_t>(n_nodes, 0) * 8, -1);
+  for (int64_t x = 0; x < n_nodes; x++)
+    for (int q = 0; q < 4; q++) ch[x * 8 + 2 * q + 1] = children[x * 4 + q];
+  const Pad3 pc = pad3(com, n_nodes, 2);
+  TRY(tree_upload_host(c->tree, ch.data(), pc.ptr, mass, length, n_nodes, 8, c->stream));
+  c->tree.dim = 2;
+  return FGA_OK;
 }
 
 int fga_tree_forces(fga_ctx* c, const double* queries, const double* qm, int64_t m, double theta,
@@ -903,10 +968,12 @@ int fga_tree_forces(fga_ctx* c, const double* queries, const double* qm, int64_t
     return FGA_ERR_STATE;
   }
   if (m <= 0) return FGA_OK;
+  const int dim = c->tree.dim;
   cudaStream_t s = c->stream;
   DevBuf &q = c->op[0], &qmd = c->op[1], &soa = c->op[2], &out = c->op[3];
   DevBuf &kin = c->op[4], &kout = c->op[5], &iin = c->op[6], &iout = c->op[7];
-  TRY(h2d(q, queries, 3 * m, s));
+  const Pad3 pq = pad3(queries, m, dim);
+  TRY(h2d(q, pq.ptr, 3 * m, s));
   TRY(h2d(qmd, qm, m, s));
   DevBuf& tmp = c->S.cub_tmp;
   DevBuf& scratch = c->S.scratch;
@@ -922,10 +989,13 @@ int fga_tree_forces(fga_ctx* c, const double* queries, const double* qm, int64_t
   launch_bh_operator(c->tree, b, b + m, b + 2 * m, b + 3 * m, iout.as<int>(), m, theta, G, eps2, f,
                      vis, acc, precision, s);
   FGA_CUDA_TRY(cudaGetLastError());
-  FGA_CUDA_TRY(cudaMemcpyAsync(forces, f, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s));
+  std::vector<double> f3(dim == 3 ? 0 : 3 * m);
+  FGA_CUDA_TRY(cudaMemcpyAsync(dim == 3 ? forces : f3.data(), f, sizeof(double) * 3 * m,
+                               cudaMemcpyDeviceToHost, s));
   if (visits) FGA_CUDA_TRY(cudaMemcpyAsync(visits, vis, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
   if (accepted) FGA_CUDA_TRY(cudaMemcpyAsync(accepted, acc, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
   FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  if (dim != 3) unpad3(f3.data(), m, dim, forces);
   return FGA_OK;
 }
 
@@ -943,10 +1013,7 @@ int fga_direct_forces(fga_ctx* c, const double* ref, const double* rm, int64_t n
                       const double* queries, const double* qm, int64_t m, int dim, double G,
                       double eps, int precision, double* forces) {
   CTX_TRY(c);
-  if (dim != 3) {
-    set_error("the B200 path implements D=3 (D=2 is not built yet)");
-    return FGA_ERR_UNSUPPORTED;
-  }
+  TRY(check_dim(dim));
   if (n <= 0) {
     set_error("registration requires a non-empty cloud");
     return FGA_ERR_EMPTY;
@@ -955,12 +1022,13 @@ int fga_direct_forces(fga_ctx* c, const double* ref, const double* rm, int64_t n
   cudaStream_t s = c->stream;
   DevBuf &r = c->op[0], &rmd = c->op[1], &pk = c->op[2], &q = c->op[3], &qmd = c->op[4],
          &soa = c->op[5], &out = c->op[6];
-  TRY(h2d(r, ref, 3 * n, s));
+  const Pad3 pr = pad3(ref, n, dim), pq = pad3(queries, m, dim);
+  TRY(h2d(r, pr.ptr, 3 * n, s));
   TRY(h2d(rmd, rm, n, s));
   FGA_CUDA_TRY(pk.reserve(precision ? sizeof(double4) * n : sizeof(float4) * n));
   launch_pack_ref(r.as<double>(), rmd.as<double>(), n, precision ? nullptr : pk.as<float4>(),
                   precision ? pk.as<double4>() : nullptr, s);
-  TRY(h2d(q, queries, 3 * m, s));
+  TRY(h2d(q, pq.ptr, 3 * m, s));
   TRY(h2d(qmd, qm, m, s));
   FGA_CUDA_TRY(soa.reserve(sizeof(double) * 4 * m));
   double* b = soa.as<double>();
@@ -969,8 +1037,11 @@ int fga_direct_forces(fga_ctx* c, const double* ref, const double* rm, int64_t n
   RefPoints rp{precision ? nullptr : pk.as<float4>(), precision ? pk.as<double4>() : nullptr, n};
   launch_direct_operator(rp, b, b + m, b + 2 * m, b + 3 * m, m, G, eps, out.as<double>(), precision, s);
   FGA_CUDA_TRY(cudaGetLastError());
-  FGA_CUDA_TRY(cudaMemcpyAsync(forces, out.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s));
+  std::vector<double> f3(dim == 3 ? 0 : 3 * m);
+  FGA_CUDA_TRY(cudaMemcpyAsync(dim == 3 ? forces : f3.data(), out.p, sizeof(double) * 3 * m,
+                               cudaMemcpyDeviceToHost, s));
   FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  if (dim != 3) unpad3(f3.data(), m, dim, forces);
   return FGA_OK;
 }
 
@@ -978,10 +1049,7 @@ int fga_gpe_kernel(fga_ctx* c, const double* pos_y, const double* mass_y, int64_
                    const double* pos_x, const double* mass_x, int64_t n, int dim, double G,
                    double eps, int precision, double* value) {
   CTX_TRY(c);
-  if (dim != 3) {
-    set_error("the B200 path implements D=3 (D=2 is not built yet)");
-    return FGA_ERR_UNSUPPORTED;
-  }
+  TRY(check_dim(dim));
   if (!value) return FGA_ERR_INVALID;
   cudaStream_t s = c->stream;
   if (m <= 0 || n <= 0) {
@@ -990,12 +1058,13 @@ int fga_gpe_kernel(fga_ctx* c, const double* pos_y, const double* mass_y, int64_
   }
   DevBuf &r = c->op[0], &rmd = c->op[1], &pk = c->op[2], &q = c->op[3], &qmd = c->op[4],
          &soa = c->op[5], &part = c->op[6], &sums = c->op[7];
-  TRY(h2d(r, pos_x, 3 * n, s));
+  const Pad3 pr = pad3(pos_x, n, dim), pq = pad3(pos_y, m, dim);
+  TRY(h2d(r, pr.ptr, 3 * n, s));
   TRY(h2d(rmd, mass_x, n, s));
   FGA_CUDA_TRY(pk.reserve(precision ? sizeof(double4) * n : sizeof(float4) * n));
   launch_pack_ref(r.as<double>(), rmd.as<double>(), n, precision ? nullptr : pk.as<float4>(),
                   precision ? pk.as<double4>() : nullptr, s);
-  TRY(h2d(q, pos_y, 3 * m, s));
+  TRY(h2d(q, pq.ptr, 3 * m, s));
   TRY(h2d(qmd, mass_y, m, s));
   FGA_CUDA_TRY(soa.reserve(sizeof(double) * 4 * m));
   double* b = soa.as<double>();
@@ -1016,17 +1085,15 @@ int fga_gpe_kernel(fga_ctx* c, const double* pos_y, const double* mass_y, int64_
 
 int fga_knn(fga_ctx* c, const double* pts, int64_t n, int dim, int k, int64_t* idx, double* d2) {
   CTX_TRY(c);
-  if (dim != 3) {
-    set_error("the B200 path implements D=3 (D=2 is not built yet)");
-    return FGA_ERR_UNSUPPORTED;
-  }
+  TRY(check_dim(dim));
   if (n <= 0) return FGA_OK;
   cudaStream_t s = c->stream;
   DevBuf &p = c->op[0], &oi = c->op[1], &od = c->op[2], &sc = c->op[3], &tmp = c->op[4];
-  TRY(h2d(p, pts, 3 * n, s));
+  const Pad3 pp = pad3(pts, n, dim);
+  TRY(h2d(p, pp.ptr, 3 * n, s));
   FGA_CUDA_TRY(oi.reserve(sizeof(long long) * n * std::max(k, 1)));
   FGA_CUDA_TRY(od.reserve(sizeof(double) * n * std::max(k, 1)));
-  TRY(knn_dev(p.as<double>(), n, k, idx ? oi.as<long long>() : nullptr,
+  TRY(knn_dev(p.as<double>(), n, dim, k, idx ? oi.as<long long>() : nullptr,
               d2 ? od.as<double>() : nullptr, nullptr, sc, tmp, s));
   if (idx) FGA_CUDA_TRY(cudaMemcpyAsync(idx, oi.p, sizeof(long long) * n * k, cudaMemcpyDeviceToHost, s));
   if (d2) FGA_CUDA_TRY(cudaMemcpyAsync(d2, od.p, sizeof(double) * n * k, cudaMemcpyDeviceToHost, s));
@@ -1036,16 +1103,14 @@ int fga_knn(fga_ctx* c, const double* pts, int64_t n, int dim, int k, int64_t* i
 
 int fga_knn_masses(fga_ctx* c, const double* pts, int64_t n, int dim, int k, double* out) {
   CTX_TRY(c);
-  if (dim != 3) {
-    set_error("the B200 path implements D=3 (D=2 is not built yet)");
-    return FGA_ERR_UNSUPPORTED;
-  }
+  TRY(check_dim(dim));
   if (n <= 0) return FGA_OK;
   cudaStream_t s = c->stream;
   DevBuf &p = c->op[0], &o = c->op[1], &sc = c->op[3], &tmp = c->op[4];
-  TRY(h2d(p, pts, 3 * n, s));
+  const Pad3 pp = pad3(pts, n, dim);
+  TRY(h2d(p, pp.ptr, 3 * n, s));
   FGA_CUDA_TRY(o.reserve(sizeof(double) * n));
-  TRY(knn_dev(p.as<double>(), n, k, nullptr, nullptr, o.as<double>(), sc, tmp, s));
+  TRY(knn_dev(p.as<double>(), n, dim, k, nullptr, nullptr, o.as<double>(), sc, tmp, s));
   FGA_CUDA_TRY(cudaMemcpyAsync(out, o.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
   FGA_CUDA_TRY(cudaStreamSynchronize(s));
   return FGA_OK;
@@ -1054,22 +1119,20 @@ int fga_knn_masses(fga_ctx* c, const double* pts, int64_t n, int dim, int k, dou
 int fga_niv_masses(fga_ctx* c, const double* pts, int64_t n, int dim, int rho, double a, double b,
                    int max_depth, double* out) {
   CTX_TRY(c);
-  if (dim != 3) {
-    set_error("the B200 path implements D=3 (D=2 is not built yet)");
-    return FGA_ERR_UNSUPPORTED;
-  }
+  TRY(check_dim(dim));
   if (rho < 2) return invalid("rho", rho);
   if (n <= 0) return FGA_OK;
   cudaStream_t s = c->stream;
   DevBuf &p = c->op[0], &o = c->op[1], &flat = c->op[2], &cnt = c->op[3], &cells = c->op[4];
-  TRY(h2d(p, pts, 3 * n, s));
-  const int64_t ncell = (int64_t)rho * rho * rho;
+  const Pad3 pp = pad3(pts, n, dim);
+  TRY(h2d(p, pp.ptr, 3 * n, s));
+  const int64_t ncell = (int64_t)rho * rho * (dim == 3 ? rho : 1);
   FGA_CUDA_TRY(o.reserve(sizeof(double) * n));
   FGA_CUDA_TRY(flat.reserve(sizeof(int) * n));
   FGA_CUDA_TRY(cnt.reserve(sizeof(long long) * (ncell + 1)));
   FGA_CUDA_TRY(cells.reserve(sizeof(double) * ncell));
-  TRY(niv_masses_dev(p.as<double>(), n, rho, a, b, max_depth, o.as<double>(), flat.as<int>(),
-                     cnt.as<long long>(), cells.as<double>(), s));
+  TRY(niv_masses_dev(p.as<double>(), n, dim, rho, a, b, max_depth, o.as<double>(),
+                     flat.as<int>(), cnt.as<long long>(), cells.as<double>(), s));
   FGA_CUDA_TRY(cudaMemcpyAsync(out, o.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
   FGA_CUDA_TRY(cudaStreamSynchronize(s));
   return FGA_OK;
@@ -1078,10 +1141,7 @@ int fga_niv_masses(fga_ctx* c, const double* pts, int64_t n, int dim, int rho, d
 int fga_normalize_pair(fga_ctx* c, const double* x, int64_t n, const double* y, int64_t m, int dim,
                        double a, double b, double* xn, double* yn, double* ctx10) {
   CTX_TRY(c);
-  if (dim != 3) {
-    set_error("the B200 path implements D=3 (D=2 is not built yet)");
-    return FGA_ERR_UNSUPPORTED;
-  }
+  TRY(check_dim(dim));
   if (n <= 0 || m <= 0) {
     set_error("registration requires a non-empty cloud");
     return FGA_ERR_EMPTY;
@@ -1089,8 +1149,9 @@ int fga_normalize_pair(fga_ctx* c, const double* x, int64_t n, const double* y, 
   cudaStream_t s = c->stream;
   DevBuf &dx = c->op[0], &dy = c->op[1], &ox = c->op[2], &oy = c->op[3], &cd = c->op[4],
          &sc = c->op[5];
-  TRY(h2d(dx, x, 3 * n, s));
-  TRY(h2d(dy, y, 3 * m, s));
+  const Pad3 px = pad3(x, n, dim), py = pad3(y, m, dim);
+  TRY(h2d(dx, px.ptr, 3 * n, s));
+  TRY(h2d(dy, py.ptr, 3 * m, s));
   FGA_CUDA_TRY(ox.reserve(sizeof(double) * 3 * n));
   FGA_CUDA_TRY(oy.reserve(sizeof(double) * 3 * m));
   FGA_CUDA_TRY(cd.reserve(sizeof(double) * 16));
@@ -1098,9 +1159,12 @@ int fga_normalize_pair(fga_ctx* c, const double* x, int64_t n, const double* y, 
   double host_ctx[10];
   TRY(normalize_pair_dev(dx.as<double>(), n, dy.as<double>(), m, a, b, ox.as<double>(),
                          oy.as<double>(), cd.as<double>(), sc.as<double>(), sc.bytes, host_ctx, s));
-  FGA_CUDA_TRY(cudaMemcpyAsync(xn, ox.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
-  FGA_CUDA_TRY(cudaMemcpyAsync(yn, oy.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s));
+  std::vector<double> hx(3 * n), hy(3 * m);
+  FGA_CUDA_TRY(cudaMemcpyAsync(hx.data(), ox.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaMemcpyAsync(hy.data(), oy.p, sizeof(double) * 3 * m, cudaMemcpyDeviceToHost, s));
   FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  unpad3(hx.data(), n, dim, xn);
+  unpad3(hy.data(), m, dim, yn);
   if (ctx10) std::memcpy(ctx10, host_ctx, sizeof(host_ctx));
   return FGA_OK;
 }
@@ -1108,26 +1172,27 @@ int fga_normalize_pair(fga_ctx* c, const double* x, int64_t n, const double* y, 
 int fga_solve_rigid(fga_ctx* c, const double* y, const double* yd, int64_t m, int dim, double* R,
                     double* t, int32_t* degenerate) {
   CTX_TRY(c);
-  if (dim != 3) {
-    set_error("the B200 path implements D=3 (D=2 is not built yet)");
-    return FGA_ERR_UNSUPPORTED;
-  }
+  TRY(check_dim(dim));
   if (m <= 0) {
     set_error("registration requires a non-empty cloud");
     return FGA_ERR_EMPTY;
   }
   cudaStream_t s = c->stream;
   DevBuf &dy = c->op[0], &dd = c->op[1], &o = c->op[2];
-  TRY(h2d(dy, y, 3 * m, s));
-  TRY(h2d(dd, yd, 3 * m, s));
+  const Pad3 py = pad3(y, m, dim), pd = pad3(yd, m, dim);
+  TRY(h2d(dy, py.ptr, 3 * m, s));
+  TRY(h2d(dd, pd.ptr, 3 * m, s));
   FGA_CUDA_TRY(o.reserve(sizeof(double) * 16));
-  launch_solve_rigid(dy.as<double>(), dd.as<double>(), m, nullptr, o.as<double>(), s);
+  launch_solve_rigid(dy.as<double>(), dd.as<double>(), m, dim, o.as<double>(), s);
   FGA_CUDA_TRY(cudaGetLastError());
   double h[13];
   FGA_CUDA_TRY(cudaMemcpyAsync(h, o.p, sizeof(h), cudaMemcpyDeviceToHost, s));
   FGA_CUDA_TRY(cudaStreamSynchronize(s));
-  if (R) std::memcpy(R, h, sizeof(double) * 9);
-  if (t) std::memcpy(t, h + 9, sizeof(double) * 3);
+  if (R)
+    for (int i = 0; i < dim; i++)
+      for (int j = 0; j < dim; j++) R[i * dim + j] = h[i * 3 + j];
+  if (t)
+    for (int i = 0; i < dim; i++) t[i] = h[9 + i];
   if (degenerate) *degenerate = (int32_t)h[12];
   return FGA_OK;
 }

@@ -533,6 +533,37 @@ __device__ void kabsch_rotation(const double C[9], double R[9], int* degenerate)
 }
 
 
+// procrustes.solve_rotation for D = 2 (procrustes.py:12-35): the SVD
+// solution U diag(1, sign det(U V^T)) V^T is the maximiser of tr(R^T C) over
+// SO(2), i.e. the rotation by atan2(C10 - C01, C00 + C11).  C is the 3x3
+// buffer of the z-padded problem; the result is embedded as diag(R2, 1).
+__device__ void kabsch_rotation_2d(const double C[9], double R[9], int* degenerate) {
+  const double c = C[0] + C[4], s = C[3] - C[1];
+  const double h = sqrt(c * c + s * s);
+  double cs = 1.0, sn = 0.0;
+  if (h > 0.0) {
+    cs = c / h;
+    sn = s / h;
+  }
+  R[0] = cs;
+  R[1] = -sn;
+  R[2] = 0.0;
+  R[3] = sn;
+  R[4] = cs;
+  R[5] = 0.0;
+  R[6] = 0.0;
+  R[7] = 0.0;
+  R[8] = 1.0;
+  if (degenerate) {  // singular values of the 2x2 block
+    const double a = C[0], b = C[1], cc = C[3], d = C[4];
+    const double s1 = sqrt((a + d) * (a + d) + (cc - b) * (cc - b));
+    const double s2 = sqrt((a - d) * (a - d) + (cc + b) * (cc + b));
+    const double smax = 0.5 * (s1 + s2), smin = 0.5 * fabs(s1 - s2);
+    const double tol = 1e-12 * fmax(smax, 1e-300);
+    *degenerate = ((smax > tol) + (smin > tol)) < 1;
+  }
+}
+
 // ---------------------------------------------------------------- tree keys
 __device__ __forceinline__ int common_levels(unsigned long long a, unsigned long long b, int L) {
   unsigned long long x = a ^ b;

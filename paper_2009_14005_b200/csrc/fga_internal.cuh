@@ -59,6 +59,7 @@ struct SimParams {
   long long max_iters;
   long long m_total;  // template size across all shards (Kabsch mean divisor)
   int trace_gpe;
+  int dim;            // 2 or 3 (2-D clouds are carried as z = const)
 };
 
 // ---------------------------------------------------------------- errors

@@ -57,14 +57,14 @@ void launch_update(const double* sums, IterState* st, const SimParams& sp, doubl
                    int has_gpe, cudaStream_t s);
 void launch_apply_pending(const TemplateView& tv, const IterState* st, cudaStream_t s);
 void launch_state_init(IterState* st, const double* mean3, cudaStream_t s);
-void launch_solve_rigid(const double* y, const double* yd, int64_t m, double* scratch,
-                        double* out13, cudaStream_t s);
+void launch_solve_rigid(const double* y, const double* yd, int64_t m, int dim, double* out13,
+                        cudaStream_t s);
 
 // Setup (setup.cu)
 int normalize_pair_dev(const double* x, int64_t n, const double* y, int64_t m, double a, double b,
                        double* xn, double* yn, double* ctx10_dev, double* scratch,
                        size_t scratch_bytes, double* ctx10_host, cudaStream_t s);
-int niv_masses_dev(const double* pts, int64_t n, int rho, double a, double b, int max_depth,
+int niv_masses_dev(const double* pts, int64_t n, int dim, int rho, double a, double b, int max_depth,
                    double* out, int* flat_scratch, long long* counts_scratch, double* cells_scratch,
                    cudaStream_t s);
 void launch_external_masses(const double* w, int64_t n, double* out, cudaStream_t s);
@@ -82,7 +82,7 @@ void launch_gather_template(const double* pts_aos, const double* mass, const int
 void launch_gather_queries(const double* q_aos, const double* qm, const int* order, int64_t m,
                            double* qx, double* qy, double* qz, double* qms, cudaStream_t s);
 
-int knn_dev(const double* pts, int64_t n, int k, long long* out_idx, double* out_d2,
+int knn_dev(const double* pts, int64_t n, int dim, int k, long long* out_idx, double* out_d2,
             double* out_mass, DevBuf& scratch, DevBuf& cub_tmp, cudaStream_t s);
 
 }  // namespace fga

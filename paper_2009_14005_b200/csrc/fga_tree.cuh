@@ -35,6 +35,7 @@ struct TreeRecords {
 struct TreeDev {
   int64_t n_points = 0, n_nodes = 0;
   int L = 0;
+  int dim = 3;  // 2: quadtree carried as z = 0 (see capi.cu pad3)
   double cmag = 0.0;  // max |coordinate| over node centres (fp32 MAC guard)
   double box_host[6] = {0, 0, 0, 0, 0, 0};
   bool exportable = false;

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kKT) k_knn(const double* __restrict__ p, int64
                                              const int* __restrict__ cend, int k,
                                              long long* __restrict__ out_idx,
                                              double* __restrict__ out_d2,
-                                             double* __restrict__ out_mass) {
+                                             double* __restrict__ out_mass, int dim) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int i = order[t];
@@ -145,14 +145,17 @@ __global__ void __launch_bounds__(kKT) k_knn(const double* __restrict__ p, int64
     for (int j = 0; j < k; j++) out_d2[(int64_t)i * k + j] = bd[j];
   if (out_mass) {
     const double r = sqrt(bd[k - 1]);
-    const double v = isfinite(r) ? (4.0 / 3.0) * M_PI * r * r * r / k : 0.0;
+    // volume (area for D = 2) per point of the k-NN ball
+    const double v = !isfinite(r) ? 0.0
+                     : dim == 2   ? M_PI * r * r / k
+                                  : (4.0 / 3.0) * M_PI * r * r * r / k;
     out_mass[i] = fmax(v, 1e-6);
   }
 }
 
 }  // namespace
 
-int knn_dev(const double* pts, int64_t n, int k, long long* out_idx, double* out_d2,
+int knn_dev(const double* pts, int64_t n, int dim, int k, long long* out_idx, double* out_d2,
             double* out_mass, DevBuf& scratch, DevBuf& cub_tmp, cudaStream_t s) {
   if (n <= 0) return FGA_OK;
   if (k < 1 || k > kKnnMax || k >= n) {
@@ -174,9 +177,10 @@ int knn_dev(const double* pts, int64_t n, int k, long long* out_idx, double* out
   for (int a = 0; a < 3; a++) {
     g.lo[a] = box[a];
     ext[a] = std::max(box[3 + a] - box[a], 1e-12);
-    vol *= ext[a];
+    if (a < dim) vol *= ext[a];
   }
-  double h = std::cbrt(vol * std::max(k, 2) / (double)n);
+  double h = dim == 2 ? std::sqrt(vol * std::max(k, 2) / (double)n)
+                      : std::cbrt(vol * std::max(k, 2) / (double)n);
   for (int a = 0; a < 3; a++) h = std::max(h, ext[a] / 512.0);  // <= 512 cells per axis
   g.h = h;
   g.inv_h = 1.0 / h;
@@ -215,10 +219,10 @@ int knn_dev(const double* pts, int64_t n, int k, long long* out_idx, double* out
   const unsigned kb = (unsigned)((n + kKT - 1) / kKT);
   if (k <= 16)
     k_knn<16><<<kb, kKT, 0, s>>>(pts, n, order, cell_s, g, cstart, cend, k, out_idx, out_d2,
-                                 out_mass);
+                                 out_mass, dim);
   else
     k_knn<32><<<kb, kKT, 0, s>>>(pts, n, order, cell_s, g, cstart, cend, k, out_idx, out_d2,
-                                 out_mass);
+                                 out_mass, dim);
   FGA_CUDA_TRY(cudaGetLastError());
   return FGA_OK;
 }

@@ -59,7 +59,8 @@ __global__ void k_update(const double* __restrict__ sums, IterState* st, SimPara
   for (int i = 0; i < 3; i++)
     for (int j = 0; j < 3; j++) C[3 * i + j] = sums[kSumWU + 3 * i + j] - M * mu_w[i] * mu_u[j];
   double R[9];
-  kabsch_rotation(C, R, nullptr);
+  if (sp.dim == 2) kabsch_rotation_2d(C, R, nullptr);
+  else kabsch_rotation(C, R, nullptr);
   double mu_y[3], mu_d[3], t[3];
   for (int k = 0; k < 3; k++) {
     mu_y[k] = mu_u[k] + st->shift[k];
@@ -145,7 +146,8 @@ __global__ void k_state_init(IterState* st, const double* __restrict__ mean3) {
 // cross-covariance) in one block, then the Kabsch rotation.
 __global__ void __launch_bounds__(kReduceThreads) k_solve_rigid(const double* __restrict__ y,
                                                                 const double* __restrict__ yd,
-                                                                int64_t m, double* out13) {
+                                                                int64_t m, int dim,
+                                                                double* out13) {
   __shared__ double sm[kReduceThreads / 32][9];
   __shared__ double mean[6];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -191,7 +193,8 @@ __global__ void __launch_bounds__(kReduceThreads) k_solve_rigid(const double* __
       C[k] = v;
     }
     int degenerate = 0;
-    kabsch_rotation(C, R, &degenerate);
+    if (dim == 2) kabsch_rotation_2d(C, R, &degenerate);
+    else kabsch_rotation(C, R, &degenerate);
     for (int k = 0; k < 9; k++) out13[k] = R[k];
     for (int k = 0; k < 3; k++)  // t = mean(y_d) - R mean(y) (:42)
       out13[9 + k] = mean[3 + k] - (R[3 * k] * mean[0] + R[3 * k + 1] * mean[1] + R[3 * k + 2] * mean[2]);
@@ -223,10 +226,9 @@ void launch_state_init(IterState* st, const double* mean3, cudaStream_t s) {
   k_state_init<<<1, 32, 0, s>>>(st, mean3);
 }
 
-void launch_solve_rigid(const double* y, const double* yd, int64_t m, double* scratch,
-                        double* out13, cudaStream_t s) {
-  (void)scratch;
-  k_solve_rigid<<<1, kReduceThreads, 0, s>>>(y, yd, m, out13);
+void launch_solve_rigid(const double* y, const double* yd, int64_t m, int dim, double* out13,
+                        cudaStream_t s) {
+  k_solve_rigid<<<1, kReduceThreads, 0, s>>>(y, yd, m, dim, out13);
 }
 
 }  // namespace fga

@@ -134,15 +134,15 @@ __global__ void k_norm_apply(const double* __restrict__ x, int64_t n, const doub
 }
 
 // ---------------------------------------------------------------- NIV
-__global__ void k_niv_hist(const double* __restrict__ pts, int64_t n, int rho, double a,
+__global__ void k_niv_hist(const double* __restrict__ pts, int64_t n, int dim, int rho, double a,
                            double edge, int* __restrict__ flat,
                            unsigned long long* __restrict__ counts) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const long long ix = niv_axis(pts[i * 3], a, edge, rho);
   const long long iy = niv_axis(pts[i * 3 + 1], a, edge, rho);
-  const long long iz = niv_axis(pts[i * 3 + 2], a, edge, rho);
-  const long long f = (ix * rho + iy) * rho + iz;  // masses.py:106-108
+  long long f = ix * rho + iy;  // masses.py:106-108
+  if (dim == 3) f = f * rho + niv_axis(pts[i * 3 + 2], a, edge, rho);
   flat[i] = (int)f;
   atomicAdd(&counts[f], 1ull);
 }
@@ -369,13 +369,14 @@ int normalize_pair_dev(const double* x, int64_t n, const double* y, int64_t m, d
   return FGA_OK;
 }
 
-int niv_masses_dev(const double* pts, int64_t n, int rho, double a, double b, int max_depth,
-                   double* out, int* flat, long long* counts, double* cell_value, cudaStream_t s) {
+int niv_masses_dev(const double* pts, int64_t n, int dim, int rho, double a, double b,
+                   int max_depth, double* out, int* flat, long long* counts, double* cell_value,
+                   cudaStream_t s) {
   if (rho < 2) {
     set_error("invalid parameter rho");
     return FGA_ERR_INVALID;
   }
-  const int64_t ncell64 = (int64_t)rho * rho * rho;
+  const int64_t ncell64 = (int64_t)rho * rho * (dim == 3 ? rho : 1);
   if (ncell64 > (1ll << 26)) {
     set_error("niv: rho^3 too large for the device lattice");
     return FGA_ERR_UNSUPPORTED;
@@ -384,12 +385,13 @@ int niv_masses_dev(const double* pts, int64_t n, int rho, double a, double b, in
   // Python-float scalars exactly as masses.py:97-102 computes them
   const double extent = b - a;
   const double cell_edge = extent / rho;
-  const double cell_vol = std::pow(cell_edge, 3);
+  const double cell_vol = std::pow(cell_edge, dim);  // masses.py:98
   const double r_ball = extent / (2.0 * max_depth * rho);
-  const double ball_vol = (4.0 / 3.0) * M_PI * std::pow(r_ball, 3);
+  const double ball_vol = dim == 2 ? M_PI * std::pow(r_ball, 2)  // :102
+                                   : (4.0 / 3.0) * M_PI * std::pow(r_ball, 3);
   unsigned long long* cnt = reinterpret_cast<unsigned long long*>(counts);
   FGA_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (ncell + 1), s));
-  k_niv_hist<<<nblk(n), kT, 0, s>>>(pts, n, rho, a, cell_edge, flat, cnt);
+  k_niv_hist<<<nblk(n), kT, 0, s>>>(pts, n, dim, rho, a, cell_edge, flat, cnt);
   k_niv_nnz<<<1, 1024, 0, s>>>(cnt, ncell, cnt + ncell);
   k_niv_cells<<<nblk(ncell), kT, 0, s>>>(cnt, ncell, cnt + ncell, cell_vol, ball_vol, cell_value);
   k_niv_gather<<<nblk(n), kT, 0, s>>>(flat, n, cell_value, out);

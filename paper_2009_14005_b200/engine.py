@@ -63,6 +63,7 @@ class Session:
         self.m_local = int(m_local.value)
         self.n_nodes = int(nn.value)
         self.shard_count = shard_count
+        self.dim = 3 if device_inputs is not None else x.dim
 
     # ---- stream-ordered pieces
     def bind_sums(self, dev_ptr: int):
@@ -113,6 +114,6 @@ class Session:
         N.check(N.lib().fga_session_finish(self.ctx.handle, ctypes.byref(res), N.ptr(deltas),
                                            N.ptr(traj), N.ptr(gtrace), N.ptr(inter),
                                            N.ptr(visits)))
-        out = _result_from_c(res, deltas, traj, gtrace, inter, self.options)
+        out = _result_from_c(res, deltas, traj, gtrace, inter, self.options, self.dim)
         out.visits_per_iter = visits[:out.iterations].copy()
         return out

@@ -18,8 +18,9 @@ from .core import RigidTransform
 def _solve(y, y_d):
     y = N.f64(y)
     y_d = N.f64(y_d)
-    R = np.empty((3, 3))
-    t = np.empty(3)
+    d = y.shape[1]
+    R = np.empty((d, d))
+    t = np.empty(d)
     deg = N._i32(0)
     c = N.context()
     N.check(N.lib().fga_solve_rigid(c.handle, N.ptr(y), N.ptr(y_d), len(y), y.shape[1], N.ptr(R),

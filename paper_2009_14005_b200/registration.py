@@ -105,13 +105,15 @@ def register(x: PointCloud, y: PointCloud, landmarks=None, params: FgaParams | N
                                  x.dim, N.ctypes.byref(cp), N.ctypes.byref(co),
                                  N.ctypes.byref(res), N.ptr(deltas), N.ptr(traj), N.ptr(gtrace),
                                  N.ptr(inter)))
-    return _result_from_c(res, deltas, traj, gtrace, inter, options)
+    return _result_from_c(res, deltas, traj, gtrace, inter, options, x.dim)
 
 
-def _result_from_c(res, deltas, traj, gtrace, inter, options) -> RegistrationResult:
+def _result_from_c(res, deltas, traj, gtrace, inter, options, dim=3) -> RegistrationResult:
     it = int(res.iterations)
-    R = np.array(res.R).reshape(3, 3)
-    t = np.array(res.t)
+    R = np.array(res.R).reshape(3, 3)[:dim, :dim].copy()
+    t = np.array(res.t)[:dim].copy()
+    if dim == 2:  # D = 2 ran as z = const: keep the in-plane block of [R|t]
+        traj = traj[:, :2, [0, 1, 3]]
     gpe_trace = [float(v) for v in gtrace[:it]] if options.trace_gpe else []
     records = []
     if options.record_iterations:

@@ -92,3 +92,26 @@ def test_oracle_register_trajectory(golden, orc, seed):
     assert np.array_equal(r.t_orig, g[k + "t"])
     assert r.gpe_initial == float(g[k + "gpe_initial"])
     assert r.gpe_final == float(g[k + "gpe_final"])
+
+
+def test_oracle_two_d_matches_reference(golden, orc):
+    """D = 2 (quadtree, 2-D NIV, 2-D Kabsch, registration) bit-exact."""
+    g = golden("two_d")
+    t = orc.tree_build(g["x"], g["xm"], 20)
+    for k in ("children", "occupancy", "depth", "bbox_min", "bbox_max", "mass", "com"):
+        assert np.array_equal(getattr(t, k), g[f"tree/{k}"]), k
+    for theta in (0.0, 0.5):
+        f, v, _ = orc.bh_forces(t, g["q"], g["qm"], theta, 66.7, 0.2)
+        assert np.array_equal(v, g[f"bh/theta{theta}/visits"])
+        assert np.array_equal(f, g[f"bh/theta{theta}/forces"])
+    assert orc.gpe(g["q"], g["qm"], g["x"], g["xm"], 66.7, 0.2) == float(g["gpe"])
+    xn, yn, ctx = orc.normalize_pair(g["norm/x"], g["norm/y"], -5.0, 5.0)
+    assert np.array_equal(xn, g["norm/xn"]) and np.array_equal(yn, g["norm/yn"])
+    assert np.array_equal(orc.niv_masses(xn, 16, -5.0, 5.0, 20), g["norm/niv_x"])
+    for i in range(len(g["rigid/y"])):
+        R, tt = orc.solve_rigid(g["rigid/y"][i], g["rigid/yd"][i])
+        assert np.array_equal(R, g["rigid/R"][i]) and np.array_equal(tt, g["rigid/t"][i])
+    r = orc.register(g["reg/x"], g["reg/y"])
+    assert r.iterations == int(g["reg/iterations"])
+    assert np.array_equal(np.array(r.deltas), g["reg/deltas"])
+    assert np.array_equal(r.t_orig, g["reg/t"]) and np.array_equal(r.R_orig, g["reg/R"])
