@@ -35,6 +35,7 @@ extern "C" {
 #define FGA_ERR_NONFINITE (-7)   /* NonFiniteWeight                              */
 #define FGA_ERR_LENGTH (-8)      /* LengthMismatch                               */
 #define FGA_ERR_STATE (-9)       /* call order (e.g. no tree built yet)          */
+#define FGA_ERR_SINGULAR (-10)   /* SingularCollocation (RBF landmark field)     */
 
 #define FGA_PREC_FP32 0 /* FP32 traversal/direct sums, fp64 state (default)   */
 #define FGA_PREC_FP64 1 /* fp64 everywhere: bit-exact reference visit order   */
@@ -65,6 +66,10 @@ typedef struct {
   int32_t compute_gpe;       /* 1 (default semantics): gpe_initial/final      */
   int32_t mass_field;        /* 0 = NIV lattice (reference default), 1 = kNN  */
   int32_t knn_k;             /* k for mass_field = 1 (default 16, <= 32)      */
+  const int64_t* x_landmarks;/* LandmarkSet.reference_indices() or NULL       */
+  const int64_t* y_landmarks;/* LandmarkSet.template_indices() or NULL        */
+  int32_t n_landmarks;       /* > 0: SPM = field * RBF (registration.py:74-83) */
+  int32_t pad2_;
 } fga_options;
 
 /* Mirrors registration.RegistrationResult (core.py:162-172). */
@@ -229,6 +234,10 @@ int fga_knn(fga_ctx* ctx, const double* pts, int64_t n, int dim, int k, int64_t*
 /* kNN smooth-particle masses: (4/3) pi r_k^3 / k, floored at 1e-6 (an opt-in
  * alternative to niv_masses, BASELINE configs[3]). */
 int fga_knn_masses(fga_ctx* ctx, const double* pts, int64_t n, int dim, int k, double* out);
+/* masses.rbf_masses (masses.py:55-82): Gaussian RBF through the anchors
+ * pts[anchors[j]]; FGA_ERR_SINGULAR when cond(K) > 1e12.  m <= 64. */
+int fga_rbf_masses(fga_ctx* ctx, const double* pts, int64_t n, int dim, const int64_t* anchors,
+                   int m, double sigma, double* out);
 /* masses.niv_masses (masses.py:85-116). */
 int fga_niv_masses(fga_ctx* ctx, const double* pts, int64_t n, int dim, int rho, double a,
                    double b, int max_depth, double* out);

@@ -153,6 +153,26 @@ def niv_masses(pts, rho, a, b, max_depth):
     return np.maximum(cell_value[flat], MASS_FLOOR)
 
 
+def rbf_masses(pts, anchors, sigma):
+    """masses.py:55-82 (Gaussian RBF collocation through the anchors)."""
+    pts = _f64(pts)
+    anchors = list(anchors)
+    if sigma <= 0:
+        raise ValueError("InvalidParam sigma")
+    if not anchors:
+        return np.ones(len(pts))
+    centers = pts[anchors]
+    dmat = np.linalg.norm(centers[:, None, :] - centers[None, :, :], axis=-1)
+    K = np.exp(-(dmat * dmat) / (sigma * sigma))
+    cond = np.linalg.cond(K)
+    if not np.isfinite(cond) or cond > 1e12:
+        raise ValueError("SingularCollocation")
+    lam = np.linalg.solve(K, np.ones(len(centers)))
+    deval = np.linalg.norm(pts[:, None, :] - centers[None, :, :], axis=-1)
+    values = np.exp(-(deval * deval) / (sigma * sigma)) @ lam
+    return np.maximum(values, MASS_FLOOR)
+
+
 def external_masses(w, n):
     """masses.py:128-135."""
     w = _f64(w)
@@ -298,7 +318,9 @@ class OracleResult:
 
 def register(x, y, G=66.7, epsilon=0.2, eta=0.2, dt=0.1, theta=0.6, rho=16, max_depth=20,
              norm_range=(-5.0, 5.0), conv_tol=1e-4, max_iters=100, x_weights=None,
-             y_weights=None, normalize=True, nthreads=0, gpe=True, force_fn=None):
+             y_weights=None, normalize=True, nthreads=0, gpe=True, force_fn=None,
+             landmarks=None, sigma=0.03):
+    """registration.py:91-166; landmarks = (reference_indices, template_indices)."""
     a, b = norm_range
     if normalize:
         xn, yn, ctx = normalize_pair(x, y, a, b)
@@ -310,6 +332,11 @@ def register(x, y, G=66.7, epsilon=0.2, eta=0.2, dt=0.1, theta=0.6, rho=16, max_
         xn, rho, a, b, max_depth)
     sy = external_masses(y_weights, len(yn)) if y_weights is not None else niv_masses(
         yn, rho, a, b, max_depth)
+    if landmarks is not None and len(landmarks[0]) > 0:  # registration.py:74-83
+        if x_weights is None:
+            sx = sx * rbf_masses(xn, landmarks[0], sigma)
+        if y_weights is None:
+            sy = sy * rbf_masses(yn, landmarks[1], sigma)
     mx, my = rescale(sx, sy, dt, eta)
     tree = tree_build(xn, mx, max_depth)
     d = xn.shape[1]

@@ -15,6 +15,7 @@ import threading
 import numpy as np
 
 from .errors import (
+    SingularCollocation,
     DegenerateExtent,
     DeviceError,
     EmptyCloud,
@@ -35,6 +36,7 @@ FGA_ERR_DEGENERATE = -6
 FGA_ERR_NONFINITE = -7
 FGA_ERR_LENGTH = -8
 FGA_ERR_STATE = -9
+FGA_ERR_SINGULAR = -10
 
 PREC_FP32 = 0
 PREC_FP64 = 1
@@ -60,7 +62,8 @@ class COptions(ctypes.Structure):
     _fields_ = [("trace_gpe", _i32), ("normalize", _i32), ("record_iterations", _i32),
                 ("precision", _i32), ("x_weights", _vp), ("y_weights", _vp),
                 ("poll_every", _i32), ("compute_gpe", _i32), ("mass_field", _i32),
-                ("knn_k", _i32)]
+                ("knn_k", _i32), ("x_landmarks", _vp), ("y_landmarks", _vp),
+                ("n_landmarks", _i32), ("pad2_", _i32)]
 
 
 class CResult(ctypes.Structure):
@@ -128,6 +131,7 @@ SIGNATURES = {
                                 ctypes.POINTER(_dbl)]),
     "fga_knn": (_c_int, [_vp, _vp, _i64, _c_int, _c_int, _vp, _vp]),
     "fga_knn_masses": (_c_int, [_vp, _vp, _i64, _c_int, _c_int, _vp]),
+    "fga_rbf_masses": (_c_int, [_vp, _vp, _i64, _c_int, _vp, _c_int, _dbl, _vp]),
     "fga_niv_masses": (_c_int, [_vp, _vp, _i64, _c_int, _c_int, _dbl, _dbl, _c_int, _vp]),
     "fga_normalize_pair": (_c_int, [_vp, _vp, _i64, _vp, _i64, _c_int, _dbl, _dbl, _vp, _vp,
                                     _vp]),
@@ -193,6 +197,8 @@ def check_msg(rc: int, msg: str) -> None:
         raise NonFiniteWeight(msg)
     if rc == FGA_ERR_LENGTH:
         raise LengthMismatch(msg)
+    if rc == FGA_ERR_SINGULAR:
+        raise SingularCollocation(msg)
     raise DeviceError(f"libfga error {rc}: {msg}")
 
 
@@ -214,6 +220,8 @@ def check(rc: int) -> None:
         raise NonFiniteWeight(msg)
     if rc == FGA_ERR_LENGTH:
         raise LengthMismatch(msg)
+    if rc == FGA_ERR_SINGULAR:
+        raise SingularCollocation(msg)
     raise DeviceError(f"libfga error {rc}: {msg}")
 
 

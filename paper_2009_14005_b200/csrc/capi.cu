@@ -47,7 +47,7 @@ struct Session {
   bool last_pass_gpe = false;
   DevBuf x_raw, y_raw, xn, yn, ctx_dev, mx, my, flat, counts, cells, ref32, ref64;
   DevBuf tkeys_in, tkeys, tidx_in, tidx, cub_tmp, tpl;
-  DevBuf partials, gpe_part, sums, state, scratch;
+  DevBuf partials, gpe_part, sums, state, scratch, lm_idx, rbf_scratch;
   DevBuf rec_delta, rec_traj, rec_gpe, rec_inter, rec_visits;
   float setup_ms = 0.f, loop_ms = 0.f, gpe_ms = 0.f;
 
@@ -244,6 +244,20 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
     TRY(niv_masses_dev(S.yn.as<double>(), m, S.sp.dim, S.P.rho, ca, cb, S.P.max_depth, S.my.as<double>(),
                        S.flat.as<int>(), S.counts.as<long long>(), S.cells.as<double>(), s));
   }
+  // landmark SPM: field * RBF (registration.py:74-83; only for NIV fields)
+  if (S.O.n_landmarks > 0) {
+    const int L = S.O.n_landmarks;
+    if (!S.O.x_weights) {
+      TRY(h2d(S.lm_idx, reinterpret_cast<const long long*>(S.O.x_landmarks), L, s));
+      TRY(rbf_apply_dev(S.xn.as<double>(), n, S.lm_idx.as<long long>(), L, S.P.sigma, 1,
+                        S.mx.as<double>(), S.rbf_scratch, s));
+    }
+    if (!S.O.y_weights) {
+      TRY(h2d(S.lm_idx, reinterpret_cast<const long long*>(S.O.y_landmarks), L, s));
+      TRY(rbf_apply_dev(S.yn.as<double>(), m, S.lm_idx.as<long long>(), L, S.P.sigma, 1,
+                        S.my.as<double>(), S.rbf_scratch, s));
+    }
+  }
   FGA_CUDA_TRY(S.scratch.reserve(sizeof(double) * 8192));
   launch_rescale(S.mx.as<double>(), n, S.my.as<double>(), m, S.P.dt, S.P.eta,
                  S.scratch.as<double>(), s);
@@ -306,6 +320,18 @@ int session_begin_common(fga_ctx* c, int64_t n, int64_t m, int dim, const fga_pa
   S.O = options ? *options : def;
   if (S.O.poll_every <= 0) S.O.poll_every = 8;
   if (S.O.knn_k <= 0) S.O.knn_k = 16;
+  if (S.O.n_landmarks > 0) {  // LandmarkSet.check_bounds (masses.py:44-48)
+    for (int j = 0; j < S.O.n_landmarks; j++) {
+      if (S.O.y_landmarks[j] < 0 || S.O.y_landmarks[j] >= m) {
+        set_error("invalid parameter pairs=template index out of range");
+        return FGA_ERR_INVALID;
+      }
+      if (S.O.x_landmarks[j] < 0 || S.O.x_landmarks[j] >= n) {
+        set_error("invalid parameter pairs=reference index out of range");
+        return FGA_ERR_INVALID;
+      }
+    }
+  }
   if (S.O.mass_field == 1 && (S.O.knn_k >= n || S.O.knn_k >= m || S.O.knn_k > 32)) {
     set_error("invalid parameter knn_k=" + std::to_string(S.O.knn_k));
     return FGA_ERR_INVALID;
@@ -494,6 +520,8 @@ int fga_destroy(fga_ctx* c) {
   c->batch_deltas.release();
   c->batch_counter.release();
   Session& S = c->S;
+  S.lm_idx.release();
+  S.rbf_scratch.release();
   DevBuf* all[] = {&S.x_raw,   &S.y_raw,  &S.xn,        &S.yn,       &S.ctx_dev,   &S.mx,
                    &S.my,      &S.flat,   &S.counts,    &S.cells,    &S.ref32,     &S.ref64,
                    &S.tkeys_in, &S.tkeys, &S.tidx_in,   &S.tidx,     &S.cub_tmp,   &S.tpl,
@@ -1111,6 +1139,29 @@ int fga_knn_masses(fga_ctx* c, const double* pts, int64_t n, int dim, int k, dou
   TRY(h2d(p, pp.ptr, 3 * n, s));
   FGA_CUDA_TRY(o.reserve(sizeof(double) * n));
   TRY(knn_dev(p.as<double>(), n, dim, k, nullptr, nullptr, o.as<double>(), sc, tmp, s));
+  FGA_CUDA_TRY(cudaMemcpyAsync(out, o.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  return FGA_OK;
+}
+
+int fga_rbf_masses(fga_ctx* c, const double* pts, int64_t n, int dim, const int64_t* anchors,
+                   int m, double sigma, double* out) {
+  CTX_TRY(c);
+  TRY(check_dim(dim));
+  if (!(sigma > 0)) return invalid("sigma", sigma);
+  if (n <= 0) return FGA_OK;
+  for (int j = 0; j < m; j++)
+    if (anchors[j] < 0 || anchors[j] >= n) {
+      set_error("invalid parameter anchors=index out of range");
+      return FGA_ERR_INVALID;
+    }
+  cudaStream_t s = c->stream;
+  DevBuf &p = c->op[0], &o = c->op[1], &ix = c->op[2], &sc = c->op[3];
+  const Pad3 pp = pad3(pts, n, dim);
+  TRY(h2d(p, pp.ptr, 3 * n, s));
+  TRY(h2d(ix, reinterpret_cast<const long long*>(anchors), std::max(m, 1), s));
+  FGA_CUDA_TRY(o.reserve(sizeof(double) * n));
+  TRY(rbf_apply_dev(p.as<double>(), n, ix.as<long long>(), m, sigma, 0, o.as<double>(), sc, s));
   FGA_CUDA_TRY(cudaMemcpyAsync(out, o.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
   FGA_CUDA_TRY(cudaStreamSynchronize(s));
   return FGA_OK;

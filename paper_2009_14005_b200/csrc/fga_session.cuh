@@ -85,4 +85,7 @@ void launch_gather_queries(const double* q_aos, const double* qm, const int* ord
 int knn_dev(const double* pts, int64_t n, int dim, int k, long long* out_idx, double* out_d2,
             double* out_mass, DevBuf& scratch, DevBuf& cub_tmp, cudaStream_t s);
 
+int rbf_apply_dev(const double* pts, int64_t n, const long long* anchor_idx_dev, int m,
+                  double sigma, int mode, double* out, DevBuf& scratch, cudaStream_t s);
+
 }  // namespace fga

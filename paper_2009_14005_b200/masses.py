@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _native as N
 from .core import PointCloud
-from .errors import DeviceError, InvalidParam, LengthMismatch, NonFiniteWeight
+from .errors import InvalidParam, LengthMismatch, NonFiniteWeight
 from .normalize import NormalizationContext
 
 MASS_FLOOR = 1e-6
@@ -91,10 +91,17 @@ def knn_masses(cloud: PointCloud, k: int = 16):
 
 
 def rbf_masses(cloud: PointCloud, anchors, sigma: float):
-    """Landmark RBF field (masses.py:55-82): not on the B200 path yet."""
+    """Gaussian RBF field through the anchors, forced to 1.0 at every anchor
+    (masses.py:55-82), on the device; SingularCollocation when the kernel
+    matrix condition exceeds 1e12.  No anchors -> uniform 1.0."""
     if sigma <= 0:
         raise InvalidParam("sigma", sigma)
-    raise DeviceError("rbf_masses (landmark SPM) is not built on the B200 path yet")
+    a = np.ascontiguousarray(list(anchors), dtype=np.int64)
+    out = np.empty(len(cloud))
+    c = N.context()
+    N.check(N.lib().fga_rbf_masses(c.handle, N.ptr(cloud.points), len(cloud), cloud.dim,
+                                   N.ptr(a) if len(a) else None, len(a), float(sigma), N.ptr(out)))
+    return out
 
 
 def spm(niv, rbf):

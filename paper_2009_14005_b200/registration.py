@@ -28,7 +28,7 @@ from .core import (
     default_params,
     validate,
 )
-from .errors import DeviceError, EmptyCloud, GravregError
+from .errors import DeviceError, EmptyCloud, GravregError, InvalidParam
 from .masses import check_weights
 
 # Mass rescale constants (registration.py:41-54); the device applies them in
@@ -56,7 +56,7 @@ class RegisterOptions:
     knn_k: int = 16
 
 
-def _c_options(options: RegisterOptions, xw, yw) -> N.COptions:
+def _c_options(options: RegisterOptions, xw, yw, lm=None) -> N.COptions:
     if options.precision not in ("fp32", "fp64"):
         raise GravregError(f"precision must be 'fp32' or 'fp64', got {options.precision!r}")
     if options.mass_field not in ("niv", "knn"):
@@ -66,7 +66,8 @@ def _c_options(options: RegisterOptions, xw, yw) -> N.COptions:
                       N.PREC_FP64 if options.precision == "fp64" else N.PREC_FP32,
                       N.ptr(xw), N.ptr(yw), int(options.poll_every),
                       int(bool(options.compute_gpe)), 1 if options.mass_field == "knn" else 0,
-                      int(options.knn_k))
+                      int(options.knn_k), N.ptr(lm[0]) if lm else None,
+                      N.ptr(lm[1]) if lm else None, len(lm[0]) if lm else 0, 0)
 
 
 def _check_inputs(x, y, landmarks, params, options):
@@ -75,14 +76,17 @@ def _check_inputs(x, y, landmarks, params, options):
     y.require_nonempty()
     if x.dim != y.dim:
         raise EmptyCloud(f"dimension mismatch: {x.dim} vs {y.dim}")
+    lm = None
     if landmarks is not None:
         landmarks.check_bounds(len(y), len(x))
-        if len(landmarks) > 0:
-            raise DeviceError("landmark (RBF x NIV) mass fields are not built on the B200 path "
-                              "yet; pass external weights via RegisterOptions.x/y_weights")
+        if len(landmarks) > 0:  # registration.py:74-83: SPM = NIV * RBF(landmarks)
+            if params.sigma <= 0:
+                raise InvalidParam("sigma", params.sigma)
+            lm = (np.ascontiguousarray(landmarks.reference_indices(), dtype=np.int64),
+                  np.ascontiguousarray(landmarks.template_indices(), dtype=np.int64))
     xw = check_weights(len(x), options.x_weights) if options.x_weights is not None else None
     yw = check_weights(len(y), options.y_weights) if options.y_weights is not None else None
-    return xw, yw
+    return xw, yw, lm
 
 
 def register(x: PointCloud, y: PointCloud, landmarks=None, params: FgaParams | None = None,
@@ -91,7 +95,7 @@ def register(x: PointCloud, y: PointCloud, landmarks=None, params: FgaParams | N
     the original (unnormalized) frame (registration.py:91-166)."""
     params = params or default_params()
     options = options or RegisterOptions()
-    xw, yw = _check_inputs(x, y, landmarks, params, options)
+    xw, yw, lm = _check_inputs(x, y, landmarks, params, options)
     c = N.context(options.device)
     mi = int(params.max_iters)
     deltas = np.zeros(mi)
@@ -100,7 +104,7 @@ def register(x: PointCloud, y: PointCloud, landmarks=None, params: FgaParams | N
     inter = np.zeros(mi, np.int64)
     res = N.CResult()
     cp = N.make_params(params)
-    co = _c_options(options, xw, yw)
+    co = _c_options(options, xw, yw, lm)
     N.check(N.lib().fga_register(c.handle, N.ptr(x.points), len(x), N.ptr(y.points), len(y),
                                  x.dim, N.ctypes.byref(cp), N.ctypes.byref(co),
                                  N.ctypes.byref(res), N.ptr(deltas), N.ptr(traj), N.ptr(gtrace),

@@ -115,3 +115,15 @@ def test_oracle_two_d_matches_reference(golden, orc):
     assert r.iterations == int(g["reg/iterations"])
     assert np.array_equal(np.array(r.deltas), g["reg/deltas"])
     assert np.array_equal(r.t_orig, g["reg/t"]) and np.array_equal(r.R_orig, g["reg/R"])
+
+
+def test_oracle_rbf_and_landmark_registration(golden, orc):
+    g = golden("rbf")
+    for j in range(3):
+        v = orc.rbf_masses(g["rbf/pts"], list(g[f"rbf/{j}/anchors"]), float(g[f"rbf/{j}/sigma"]))
+        assert np.array_equal(v, g[f"rbf/{j}/values"])
+    idx = [int(i) for i in g["lm/idx"]]
+    r = orc.register(g["lm/x"], g["lm/y"], landmarks=(idx, idx), sigma=12.0)
+    assert r.iterations == int(g["lm/iterations"])
+    assert np.array_equal(np.array(r.deltas), g["lm/deltas"])
+    assert np.array_equal(r.R_orig, g["lm/R"]) and np.array_equal(r.t_orig, g["lm/t"])
