@@ -1159,7 +1159,8 @@ int fga_rbf_masses(fga_ctx* c, const double* pts, int64_t n, int dim, const int6
   DevBuf &p = c->op[0], &o = c->op[1], &ix = c->op[2], &sc = c->op[3];
   const Pad3 pp = pad3(pts, n, dim);
   TRY(h2d(p, pp.ptr, 3 * n, s));
-  TRY(h2d(ix, reinterpret_cast<const long long*>(anchors), std::max(m, 1), s));
+  if (m > 0) TRY(h2d(ix, reinterpret_cast<const long long*>(anchors), m, s));
+  else FGA_CUDA_TRY(ix.reserve(sizeof(long long)));
   FGA_CUDA_TRY(o.reserve(sizeof(double) * n));
   TRY(rbf_apply_dev(p.as<double>(), n, ix.as<long long>(), m, sigma, 0, o.as<double>(), sc, s));
   FGA_CUDA_TRY(cudaMemcpyAsync(out, o.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
