@@ -61,10 +61,18 @@ def random_rotation(rng, max_angle_rad):
     return axis_angle(axis / np.linalg.norm(axis), angle)
 
 
-def random_rigid(rng, max_angle_rad, max_translation):
-    """Uniform-axis rotation with angle U(0, max), translation of length
-    U(0, max_t) along a uniform direction (synth.py:134-139)."""
-    R = random_rotation(rng, max_angle_rad)
+def euler_rotation(rng, max_angle_rad):
+    """Rz(c) Ry(b) Rx(a) with a, b, c ~ U(0, max) (synth.py:109-118)."""
+    rx, ry, rz = rng.uniform(0.0, max_angle_rad, size=3)
+    return (axis_angle([0.0, 0.0, 1.0], rz) @ axis_angle([0.0, 1.0, 0.0], ry)
+            @ axis_angle([1.0, 0.0, 0.0], rx))
+
+
+def random_rigid(rng, max_angle_rad, max_translation, euler=False):
+    """Uniform-axis rotation with angle U(0, max) (or per-axis Euler angles),
+    translation of length U(0, max_t) along a uniform direction
+    (synth.py:134-139)."""
+    R = euler_rotation(rng, max_angle_rad) if euler else random_rotation(rng, max_angle_rad)
     direction = rng.normal(size=3)
     direction /= np.linalg.norm(direction)
     return RigidTransform(R, direction * rng.uniform(0.0, max_translation))

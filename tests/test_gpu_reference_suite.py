@@ -1,6 +1,6 @@
 """The reference's own hot-path tests (pkg/tests/test_bhtree.py,
 test_dynamics.py, test_masses.py, test_registration.py, test_acceptance.py
-criteria 1-5, 7-9), re-run against the B200 package (D=3; the device path
+criteria 1-9), re-run against the B200 package (D=3; the device path
 implements D=3 only).  Same inputs, seeds and thresholds as the reference.
 GPU only."""
 
@@ -197,6 +197,23 @@ def test_criterion_05_noise_robustness(F):
         y = F.synth.misalign(x, gt)
         ok += F.rmse(y, F.register(x, y).transform, gt) < 0.01
     assert ok / 20 >= 0.6
+
+
+def test_criterion_06_landmark_lift(F):
+    """test_acceptance.py:163-178: 3 landmark correspondences lift success on
+    near-symmetric boxes under large Euler rotations."""
+    p = F.default_params().replace(sigma=12.0)
+    plain_ok = lm_ok = 0
+    for s in range(20):
+        rng = F.synth.rng_from_seed(2000 + s)
+        x = F.synth.bumped_box(2000, rng)
+        gt = F.synth.random_rigid(rng, 3 * np.pi / 4, 0.1, euler=True)
+        y = F.synth.misalign(x, gt)
+        idx = rng.choice(2000, size=3, replace=False)
+        lm = F.LandmarkSet(tuple((int(i), int(i)) for i in idx))
+        plain_ok += F.rmse(y, F.register(x, y).transform, gt) < 0.01
+        lm_ok += F.rmse(y, F.register(x, y, landmarks=lm, params=p).transform, gt) < 0.01
+    assert lm_ok > plain_ok
 
 
 def test_criterion_08_frame_consistency(F):
