@@ -66,7 +66,9 @@ struct WinBuf32 {
   WinRec32 r[kWin];
 };
 
-template <bool kGuardZero>
+// kW: nodes per window refill (<= 32); 0 = no window, every step reads the
+// node with one warp-uniform (broadcast) load through L1.
+template <bool kGuardZero, int kW = kWin>
 __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
                                                 const NodeB32* __restrict__ B,
                                                 const double4* __restrict__ A64,
@@ -86,25 +88,33 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
   while (true) {
     const int n = __reduce_min_sync(0xffffffffu, cursor);
     if (n >= n_nodes) break;
-    if ((unsigned)(n - wbase) >= (unsigned)kWin) {
-      wbase = n;
-      __syncwarp();
-      const int j = n + lane;
-      if (j < n_nodes) {
-        const float4 a = __ldg(&A[j]);
-        const NodeB32 b = B[j];
-        win->r[lane].a = a;
-        // p = sqrt3*theta/len, q = sqrt3*len/theta: 2|d|delta <= delta*(d2*p + q) with
-        // the AM-GM pivot at |d| = len/theta, where MAC ties happen
-        const float il = b.l2 > 0.f ? rsqrt_approx(b.l2) : 0.f;
-        win->r[lane].b = make_float4(b.l2, __int_as_float(b.skip), kSqrt3 * theta * il,
-                                     kSqrt3 * b.l2 * il * itheta);
+    float4 a, b;
+    if constexpr (kW == 0) {
+      a = __ldg(&A[n]);
+      const float2 nb = __ldg(reinterpret_cast<const float2*>(B) + n);
+      const float il = nb.x > 0.f ? rsqrt_approx(nb.x) : 0.f;
+      b = make_float4(nb.x, nb.y, kSqrt3 * theta * il, kSqrt3 * nb.x * il * itheta);
+    } else {
+      if ((unsigned)(n - wbase) >= (unsigned)kW) {
+        wbase = n;
+        __syncwarp();
+        const int j = n + lane;
+        if (lane < kW && j < n_nodes) {
+          const float4 ga = __ldg(&A[j]);
+          const NodeB32 gb = B[j];
+          win->r[lane].a = ga;
+          // p = sqrt3*theta/len, q = sqrt3*len/theta: 2|d|delta <= delta*(d2*p + q) with
+          // the AM-GM pivot at |d| = len/theta, where MAC ties happen
+          const float il = gb.l2 > 0.f ? rsqrt_approx(gb.l2) : 0.f;
+          win->r[lane].b = make_float4(gb.l2, __int_as_float(gb.skip), kSqrt3 * theta * il,
+                                       kSqrt3 * gb.l2 * il * itheta);
+        }
+        __syncwarp();
       }
-      __syncwarp();
+      const WinRec32& rec = win->r[n - wbase];
+      a = rec.a;
+      b = rec.b;
     }
-    const WinRec32& rec = win->r[n - wbase];
-    const float4 a = rec.a;
-    const float4 b = rec.b;
     const bool mine = cursor == n;
     const float dx = a.x - qx, dy = a.y - qy, dz = a.z - qz;
     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));

@@ -49,7 +49,7 @@ struct F32Params {
   float theta2, eps2;
 };
 
-template <typename Real, bool kGuardZero, int kT>
+template <typename Real, bool kGuardZero, int kT, int kW = kWin>
 __global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? 1280 : 768) / kT) k_bh_iterate(
     TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, SimParams sp,
     F32Params f, double* partials, float cmag, int nblocks, int per_sm) {
@@ -87,8 +87,8 @@ __global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? 1280 : 768) / kT) k_b
     const float qx = (float)y[0], qy = (float)y[1], qz = (float)y[2];
     float gA, gB;
     guard_coeffs(fmaxf(fabsf(qx), fmaxf(fabsf(qy), fabsf(qz))), cmag, f.theta2, gA, gB);
-    Trav32Out o = traverse32<kGuardZero>(tr.a32, tr.b32, tr.a64, tr.b64, n_nodes, qx, qy, qz,
-                                         active, f.theta2, sp.theta2, f.eps2, gA, gB, tv.px,
+    Trav32Out o = traverse32<kGuardZero, kW>(tr.a32, tr.b32, tr.a64, tr.b64, n_nodes, qx, qy, qz,
+                                             active, f.theta2, sp.theta2, f.eps2, gA, gB, tv.px,
                                          tv.py, tv.pz, i, &wins[wl], lane);
     const double gq = sp.G * mq;
     F[0] = gq * (double)o.ax;
@@ -478,6 +478,15 @@ static int bh_block() {
   }();
   return b;
 }
+// Experimental: FGA_BH_WIN = 0 / 8 / 16 / 32 nodes per traversal window refill.
+static int bh_win() {
+  static int w = [] {
+    const char* e = getenv("FGA_BH_WIN");
+    int v = e ? atoi(e) : kWin;
+    return (v == 0 || v == 8 || v == 16 || v == 32) ? v : kWin;
+  }();
+  return w;
+}
 int64_t bh_iterate_warps(int64_t m) {
   const int t = bh_block();
   return (int64_t)grid_for(m, t) * (t / 32);
@@ -505,6 +514,15 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
   else if (gz)
     k_bh_iterate<float, true, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm,
                                                    nb, per);
+  else if (kT == 128 && bh_win() == 0)
+    k_bh_iterate<float, false, kT, 0><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials,
+                                                       cm, nb, per);
+  else if (kT == 128 && bh_win() == 8)
+    k_bh_iterate<float, false, kT, 8><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials,
+                                                       cm, nb, per);
+  else if (kT == 128 && bh_win() == 16)
+    k_bh_iterate<float, false, kT, 16><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials,
+                                                        cm, nb, per);
   else
     k_bh_iterate<float, false, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm,
                                                     nb, per);
