@@ -40,6 +40,14 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   return r;
 }
 
+// band of a node (see the guard note below); -inf for a leaf (l2 = -inf),
+// so a leaf is never re-checked.  gA = 1.25*2 sqrt3 delta theta, gB = the
+// delta^2 term.
+__device__ __forceinline__ float node_band(float l2, float gA, float gB) {
+  const float len = l2 > 0.f ? l2 * rsqrt_approx(l2) : 0.f;
+  return fmaf(gA, len, fmaf(13.0f * 5.97e-8f, l2, gB));
+}
+
 struct Trav32Out {
   float ax, ay, az;
   int visits, accepted;
@@ -53,14 +61,19 @@ struct Trav32Out {
 //
 // Exact-MAC guard: with q and com rounded to fp32 (each coordinate off by at
 // most delta = (|q|max + |com|max) * 2^-24) the fp32 d^2 differs from the
-// fp64 one by at most 2*delta*(|dx|+|dy|+|dz|) + 3*delta^2 + 4u*d^2.  When
-// |theta^2 d^2 - l^2| is inside that bound (plus the rounding of l^2 and of
-// theta^2 d^2) the decision is re-made exactly in fp64 from the fp64 records,
+// fp64 one by at most err(d) = 2*delta*(|dx|+|dy|+|dz|) + 3*delta^2 + 4u*d^2.
+// The fp32 decision can only be wrong when |theta^2 d^2 - l^2| <= err(d)
+// (the exact difference has the other sign), which pins D = theta*|d| to
+// within ~2 sqrt3 delta theta of len.  There err(d) <= 2 sqrt3 delta theta len
+// + 21 delta^2 theta^2 + 13u l^2, so one band per node,
+//   band = 1.25*(2 sqrt3 delta theta) len + 13u l^2 + 1.25*27 delta^2 theta^2,
+// computed when the node enters the window, covers every wrong decision:
+// inside it the decision is re-made exactly in fp64 from the fp64 records,
 // so the accepted set always equals the reference's (_kernels.py:37).
-// gA = 2*delta*theta^2*1.25, gB = 3*delta^2*theta^2*1.25 (per lane).
+// delta is the warp maximum, so the band is warp-uniform per node.
 struct WinRec32 {
   float4 a;  // com.xyz, mass
-  float4 b;  // l2 | -inf, skip (int bits), unused, unused
+  float4 b;  // l2 | -inf, skip (int bits), band, unused
 };
 struct WinBuf32 {
   WinRec32 r[kWin];
@@ -82,9 +95,10 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
   int visits = 0, accepted = 0;
   int cursor = active ? 0 : n_nodes;
   int wbase = INT_MIN / 2;
-  constexpr float kRel = 12.0f * 5.97e-8f;  // unit roundoffs of d^2, theta^2 d^2 and l^2 (~ t2d2 at a tie)
-  constexpr float kSqrt3 = 1.7320508f;
-  const float theta = sqrtf(theta2), itheta = theta > 0.f ? 1.0f / theta : 0.f;
+  const int64_t qs = active ? qi : 0;  // inactive lanes join the exact re-check
+  // one band per warp: the largest lane delta (inactive lanes pass 0)
+  gA = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gA)));
+  gB = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gB)));
   while (true) {
     const int n = __reduce_min_sync(0xffffffffu, cursor);
     if (n >= n_nodes) break;
@@ -92,8 +106,7 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
     if constexpr (kW == 0) {
       a = __ldg(&A[n]);
       const float2 nb = __ldg(reinterpret_cast<const float2*>(B) + n);
-      const float il = nb.x > 0.f ? rsqrt_approx(nb.x) : 0.f;
-      b = make_float4(nb.x, nb.y, kSqrt3 * theta * il, kSqrt3 * nb.x * il * itheta);
+      b = make_float4(nb.x, nb.y, node_band(nb.x, gA, gB), 0.f);
     } else {
       if ((unsigned)(n - wbase) >= (unsigned)kW) {
         wbase = n;
@@ -103,11 +116,7 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
           const float4 ga = __ldg(&A[j]);
           const NodeB32 gb = B[j];
           win->r[lane].a = ga;
-          // p = sqrt3*theta/len, q = sqrt3*len/theta: 2|d|delta <= delta*(d2*p + q) with
-          // the AM-GM pivot at |d| = len/theta, where MAC ties happen
-          const float il = gb.l2 > 0.f ? rsqrt_approx(gb.l2) : 0.f;
-          win->r[lane].b = make_float4(gb.l2, __int_as_float(gb.skip), kSqrt3 * theta * il,
-                                       kSqrt3 * gb.l2 * il * itheta);
+          win->r[lane].b = make_float4(gb.l2, __int_as_float(gb.skip), node_band(gb.l2, gA, gB), 0.f);
         }
         __syncwarp();
       }
@@ -120,10 +129,12 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
     const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
     const float t2d2 = theta2 * d2;
     bool acc = b.x < t2d2;
-    const float band = fmaf(gA, fmaf(d2, b.z, b.w), fmaf(kRel, t2d2, gB));
-    const bool near = mine && fabsf(t2d2 - b.x) <= band;
+    const bool near = mine && fabsf(t2d2 - b.x) <= b.z;
     if (__any_sync(0xffffffffu, near)) {  // warp-uniform branch, rarely taken
-      if (near) acc = mac_exact(A64, B64, n, qpx[qi], qpy[qi], qpz[qi], theta2_64);
+      // every lane makes the (cheap, L2-resident) exact check so the call is
+      // not divergent; only the near lanes use it
+      const bool e = mac_exact(A64, B64, n, qpx[qs], qpy[qs], qpz[qs], theta2_64);
+      acc = near ? e : acc;
     }
     const bool take = mine && acc;
     const float r2 = d2 + eps2;
@@ -195,12 +206,12 @@ __device__ __forceinline__ Trav64Out traverse64(const double4* __restrict__ A,
   return o;
 }
 
-// Per-lane guard coefficients (see traverse32).
+// Per-lane guard coefficients (see traverse32): band(node) = gA*len + kRel*l2 + gB.
 __device__ __forceinline__ void guard_coeffs(float qmag, float cmag, float theta2, float& gA,
                                              float& gB) {
   const float delta = (qmag + cmag) * 5.97e-8f;
-  gA = 1.25f * delta * theta2;                    // times (d2*p + q) >= 2*sqrt3*|d|
-  gB = 3.75f * delta * delta * theta2 + 1e-37f;
+  gA = 4.34f * delta * sqrtf(theta2);         // 1.25 * 2 sqrt3 delta theta
+  gB = 34.f * delta * delta * theta2 + 1e-37f;  // 1.25 * 27 delta^2 theta^2
 }
 
 // ---------------------------------------------------------------- iterate epilogue
