@@ -37,6 +37,9 @@ METRIC = "particle-pair interactions/sec and registration wall-time, 1M-pt FGA, 
 UNIT = "interactions/s"
 FLOP_PER_INTERACTION = 20  # GPU Gems 3 ch.31 n-body convention
 FLOP_PER_VISIT = 9         # MAC: 3 sub + 5 (d^2) + 1 (theta^2 d^2)
+BYTES_PER_VISIT = 32       # one 32 B node record per query-node visit
+BYTES_PER_QUERY = 32       # + 16 B query in, 16 B state out per template point
+BUILD_BYTES_PER_POINT = 350  # SURVEY §8(d) K2-K5 algorithmic bytes per reference point
 
 
 def parse():
@@ -54,6 +57,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--direct-steps", type=int, default=3)
     ap.add_argument("--no-batched", action="store_true")
+    ap.add_argument("--no-build", action="store_true")
+    ap.add_argument("--build-sizes", default="1000000,16000000")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the configs[1]/configs[3] registration legs")
     ap.add_argument("--batch-pairs", type=int, default=4096)
@@ -231,18 +236,30 @@ def run_ours(args, rank, world, local_rank):
                    "G": params.G,
                    "tree_nodes": sess.n_nodes, "parallelism": f"template-shard x{world}",
                    "l2": "flushed between timed steps (256 MiB write, outside the events)"},
-        "gpu_launches": 3 * K,
+        "gpu_launches": 4 * K,  # k_bh_iterate, k_reduce_stage, k_reduce_final, k_update
         "interactions_per_step": per_launch_inter,
     }
-    flop = FLOP_PER_INTERACTION * per_launch_inter + FLOP_PER_VISIT * _visits_per_step(res, W, K)
+    visits_step = _visits_per_step(res, W, K)
+    flop = FLOP_PER_INTERACTION * per_launch_inter + FLOP_PER_VISIT * visits_step
     achieved = flop / mean_force_s / 1e12
+    l2_peak, l2_src = l2_peak_gbs()
+    alg_bytes = BYTES_PER_VISIT * visits_step + BYTES_PER_QUERY * len(y)
+    l2_achieved = alg_bytes / mean_force_s / 1e9
     line["roofline"] = {
-        "kernel": "k_bh_iterate<float> (+k_reduce)", "bound": "fp32", "unit": "TFLOP/s",
-        "achieved": achieved, "peak": peak, "frac": achieved / peak,
-        "peak_source": f"2*148*128*sm_max_mhz ({peak_src} MEASURED_PEAKS.json sm_max_mhz={fmax})",
-        "work": f"{FLOP_PER_INTERACTION} FLOP/interaction + {FLOP_PER_VISIT} FLOP/visit",
-        "ms_per_launch": mean_force_s * 1e3, "traffic": _traffic("bh")}
+        "kernel": "k_bh_iterate<float> (+k_reduce)", "bound": "l2", "unit": "GB/s",
+        "achieved": l2_achieved, "peak": l2_peak, "frac": l2_achieved / l2_peak if l2_peak else None,
+        "peak_source": l2_src,
+        "work": f"SURVEY §8(d) K6: {BYTES_PER_VISIT} B/visit x {visits_step:.4g} visits + "
+                f"{BYTES_PER_QUERY} B x {len(y)} queries = {alg_bytes:.4g} B per launch",
+        "ms_per_launch": mean_force_s * 1e3, "traffic": _traffic("bh"),
+        "fp32_view": {"achieved_tflops": achieved, "peak_tflops": peak, "frac": achieved / peak,
+                      "peak_source": f"2*148*128*sm_max_mhz ({peak_src} MEASURED_PEAKS.json "
+                                     f"sm_max_mhz={fmax})",
+                      "work": f"{FLOP_PER_INTERACTION} FLOP/interaction + {FLOP_PER_VISIT} "
+                              "FLOP/visit"}}
     line["clocks"] = clocks
+    if world == 1 and not args.no_build:
+        line["tree_build"] = run_tree_build(args, dev, peaks, peak_src)
     if world == 1 and not args.no_direct:
         line["direct"] = run_direct(args, x, y, dev, stream, peak, peak_src, fmax)
     if world == 1 and not args.no_e2e:
@@ -256,6 +273,85 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_configs:
         line["configs"] = run_other_configs(args)
     return line
+
+
+_L2_CACHE = {}
+
+
+def l2_peak_gbs():
+    """Measured L2 read bandwidth (libfgaprobe.so: all SMs stream a 32 MiB
+    L2-resident buffer), the K6 roofline denominator; MEASURED_PEAKS.json has
+    no L2 figure."""
+    if "v" in _L2_CACHE:
+        return _L2_CACHE["v"]
+    import ctypes
+    v, src = None, "unavailable"
+    try:
+        lib = ctypes.CDLL(os.path.join(ROOT, "paper_2009_14005_b200", "_lib", "libfgaprobe.so"))
+        lib.fga_probe_l2_read.argtypes = [ctypes.c_size_t, ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_double)]
+        best = 0.0
+        for _ in range(3):
+            g = ctypes.c_double(0.0)
+            if lib.fga_probe_l2_read(64 << 20, 200, ctypes.byref(g)) == 0:
+                best = max(best, g.value)
+        if best > 0:
+            v = best
+            src = "measured live: libfgaprobe L2 read probe, 64 MiB x 200 passes, best of 3"
+    except OSError as e:
+        src = f"unavailable ({e})"
+    _L2_CACHE["v"] = (v, src)
+    return v, src
+
+
+def run_tree_build(args, dev, peaks, peak_src):
+    """K2-K5 (fga_tree_build_dev: bbox, exact keys, radix sort, emission,
+    summarize, traversal records) on device-resident points, CUDA events per
+    build (the build's one internal node-count sync included).  Roofline:
+    SURVEY §8(d) 350 algorithmic B/point against HBM."""
+    import ctypes
+
+    import torch
+
+    from paper_2009_14005_b200 import _native as N
+    from paper_2009_14005_b200 import synth
+    L = N.lib()
+    c = N.Context(dev.index)
+    stream = torch.cuda.current_stream()
+    c.set_stream(stream.cuda_stream)
+    hbm = float(peaks.get("hbm_gbs", 6552.3))
+    out = {}
+    for n in [int(v) for v in args.build_sizes.split(",") if v]:
+        rng = synth.rng_from_seed(args.seed)
+        pts = torch.from_numpy(synth.blob(n, rng).points).to(dev)
+        ms = torch.full((n,), 1.0, dtype=torch.float64, device=dev)
+        nn = N._i64(0)
+        for _ in range(3):
+            N.check(L.fga_tree_build_dev(c.handle, pts.data_ptr(), ms.data_ptr(), n, 20,
+                                         ctypes.byref(nn)))
+        reps = 10 if n <= 2_000_000 else 4
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        times = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            N.check(L.fga_tree_build_dev(c.handle, pts.data_ptr(), ms.data_ptr(), n, 20,
+                                         ctypes.byref(nn)))
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        t = float(np.median(times)) / 1e3
+        ach = BUILD_BYTES_PER_POINT * n / t / 1e9
+        out[str(n)] = {"ms": t * 1e3, "nodes": int(nn.value), "points_per_s": n / t,
+                       "roofline": {"bound": "hbm", "unit": "GB/s", "achieved": ach,
+                                    "peak": hbm, "frac": ach / hbm,
+                                    "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs",
+                                    "work": f"SURVEY §8(d): {BUILD_BYTES_PER_POINT} B/point"}}
+        del pts, ms, flush
+    c.close()
+    out["api"] = "fga_tree_build_dev (blob points, unit masses, max_depth 20), median of reps, L2 flushed"
+    return out
 
 
 def _visits_per_step(res, W, K):

@@ -185,12 +185,20 @@ int fga_session_finish(fga_ctx* ctx, fga_result* out, double* deltas, double* tr
 int fga_session_set_gpe(fga_ctx* ctx, int which /*0 initial,1 final*/, double value);
 /* Number of template points owned by this shard and total tree nodes. */
 int fga_session_info(fga_ctx* ctx, int64_t* m_local, int64_t* n_nodes);
+/* The session's rescaled mass fields (registration.py:85-87) in input order:
+ * mx (n) for the reference, my (m) for the template; either may be NULL. */
+int fga_session_masses(fga_ctx* ctx, double* mx, double* my);
 
 /* --------------------------------------------------- tree-level entries
  * bhtree.build (bhtree.py:56-122) on the device; the tree stays in the
  * context.  n_nodes receives the node count. */
 int fga_tree_build(fga_ctx* ctx, const double* pts, const double* masses, int64_t n, int dim,
                    int max_depth, int64_t* n_nodes);
+/* Same build from device-resident (n,3) points and masses, stream-ordered
+ * (one internal sync for the node count); the inputs must stay alive while
+ * the context's tree is used (the tree references them). */
+int fga_tree_build_dev(fga_ctx* ctx, const double* pts_dev, const double* masses_dev, int64_t n,
+                       int max_depth, int64_t* n_nodes);
 /* Copy the context's tree out in the BHTree array layout (bhtree.py:14-45):
  * children (n_nodes,8) int64, com (n_nodes,3), mass, length, occupancy,
  * depth (int64), bbox_min/max (n_nodes,3).  Any pointer may be NULL. */

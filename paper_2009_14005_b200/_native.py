@@ -118,8 +118,10 @@ SIGNATURES = {
     "fga_session_poll": (_c_int, [_vp, ctypes.POINTER(_c_int), ctypes.POINTER(_i64)]),
     "fga_session_finish": (_c_int, [_vp, ctypes.POINTER(CResult), _vp, _vp, _vp, _vp, _vp]),
     "fga_session_set_gpe": (_c_int, [_vp, _c_int, _dbl]),
+    "fga_session_masses": (_c_int, [_vp, _vp, _vp]),
     "fga_session_info": (_c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "fga_tree_build": (_c_int, [_vp, _vp, _vp, _i64, _c_int, _c_int, ctypes.POINTER(_i64)]),
+    "fga_tree_build_dev": (_c_int, [_vp, _vp, _vp, _i64, _c_int, ctypes.POINTER(_i64)]),
     "fga_tree_export": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fga_tree_upload": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _c_int, _c_int]),
     "fga_tree_forces": (_c_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _dbl, _c_int, _vp, _vp, _vp]),

@@ -47,7 +47,7 @@ struct Session {
   bool last_pass_gpe = false;
   DevBuf x_raw, y_raw, xn, yn, ctx_dev, mx, my, flat, counts, cells, ref32, ref64;
   DevBuf tkeys_in, tkeys, tidx_in, tidx, cub_tmp, tpl;
-  DevBuf partials, gpe_part, sums, state, scratch, lm_idx, rbf_scratch;
+  DevBuf partials, gpe_part, sums, state, scratch, lm_idx, rbf_scratch, red_stage;
   DevBuf rec_delta, rec_traj, rec_gpe, rec_inter, rec_visits;
   float setup_ms = 0.f, loop_ms = 0.f, gpe_ms = 0.f;
 
@@ -258,7 +258,7 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
                         S.my.as<double>(), S.rbf_scratch, s));
     }
   }
-  FGA_CUDA_TRY(S.scratch.reserve(sizeof(double) * 8192));
+  FGA_CUDA_TRY(S.scratch.reserve(sizeof(double) * (8 + pairwise_sum_scratch_doubles(n) + 600)));
   launch_rescale(S.mx.as<double>(), n, S.my.as<double>(), m, S.P.dt, S.P.eta,
                  S.scratch.as<double>(), s);
   // reference side: tree (BH) and packed points (direct sum, energy)
@@ -287,6 +287,7 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
                               : bh_iterate_warps(S.m_local);
   FGA_CUDA_TRY(S.partials.reserve(sizeof(double) * kPartialStride * std::max<int64_t>(nw, 1)));
   FGA_CUDA_TRY(S.gpe_part.reserve(sizeof(double) * std::max<int64_t>(gpe_warps(S.m_local, S.precision), 1)));
+  FGA_CUDA_TRY(S.red_stage.reserve(sizeof(double) * reduce_stage_doubles()));
   const int64_t mi = S.P.max_iters;
   FGA_CUDA_TRY(S.rec_delta.reserve(sizeof(double) * mi));
   FGA_CUDA_TRY(S.rec_traj.reserve(sizeof(double) * 12 * mi));
@@ -370,7 +371,7 @@ int session_gpe(fga_ctx* c, const IterState* gate) {
   launch_gpe(S.ref(), tv.px, tv.py, tv.pz, tv.mq, S.m_local, S.sp.eps, gate, S.gpe_part.as<double>(),
              S.precision, c->stream);
   launch_reduce(S.partials.as<double>(), 0, S.gpe_part.as<double>(), S.m_local > 0 ? ngw : 0, -1.0,
-                S.sums_ptr(), c->stream);
+                S.sums_ptr(), S.red_stage.as<double>(), c->stream);
   FGA_CUDA_TRY(cudaGetLastError());
   return FGA_OK;
 }
@@ -397,7 +398,7 @@ int session_forces(fga_ctx* c) {
   }
   const double pairs = S.direct ? (double)S.n * (double)S.m_local : -1.0;
   launch_reduce(S.partials.as<double>(), nw, S.gpe_part.as<double>(), ngw, pairs,
-                S.sums_ptr(), s);
+                S.sums_ptr(), S.red_stage.as<double>(), s);
   S.last_pass_gpe = with_gpe;
   S.passes++;
   FGA_CUDA_TRY(cudaGetLastError());
@@ -655,6 +656,17 @@ int fga_session_info(fga_ctx* c, int64_t* m_local, int64_t* n_nodes) {
   SESSION_TRY(c);
   if (m_local) *m_local = c->S.m_local;
   if (n_nodes) *n_nodes = c->S.direct ? 0 : c->tree.n_nodes;
+  return FGA_OK;
+}
+
+int fga_session_masses(fga_ctx* c, double* mx, double* my) {
+  SESSION_TRY(c);
+  Session& S = c->S;
+  if (mx)
+    FGA_CUDA_TRY(cudaMemcpyAsync(mx, S.mx.p, sizeof(double) * S.n, cudaMemcpyDeviceToHost, c->stream));
+  if (my)
+    FGA_CUDA_TRY(cudaMemcpyAsync(my, S.my.p, sizeof(double) * S.m, cudaMemcpyDeviceToHost, c->stream));
+  FGA_CUDA_TRY(cudaStreamSynchronize(c->stream));
   return FGA_OK;
 }
 
@@ -942,6 +954,19 @@ int fga_tree_build(fga_ctx* c, const double* pts, const double* masses, int64_t 
   return FGA_OK;
 }
 
+int fga_tree_build_dev(fga_ctx* c, const double* pts_dev, const double* masses_dev, int64_t n,
+                       int max_depth, int64_t* n_nodes) {
+  CTX_TRY(c);
+  if (n <= 0) {
+    set_error("registration requires a non-empty cloud");
+    return FGA_ERR_EMPTY;
+  }
+  TRY(tree_build_dev(c->tree, pts_dev, masses_dev, n, max_depth, c->stream));
+  c->tree.dim = 3;
+  if (n_nodes) *n_nodes = c->tree.n_nodes;
+  return FGA_OK;
+}
+
 int fga_tree_export(fga_ctx* c, int64_t* children, double* com, double* mass, double* length,
                     int64_t* occupancy, int64_t* depth, double* bbox_min, double* bbox_max) {
   CTX_TRY(c);
@@ -1099,10 +1124,11 @@ int fga_gpe_kernel(fga_ctx* c, const double* pos_y, const double* mass_y, int64_
   launch_gather_queries(q.as<double>(), qmd.as<double>(), nullptr, m, b, b + m, b + 2 * m, b + 3 * m, s);
   const int64_t ngw = gpe_warps(m, precision);
   FGA_CUDA_TRY(part.reserve(sizeof(double) * ngw));
-  FGA_CUDA_TRY(sums.reserve(sizeof(double) * kPartialStride));
+  FGA_CUDA_TRY(sums.reserve(sizeof(double) * (kPartialStride + reduce_stage_doubles())));
   RefPoints rp{precision ? nullptr : pk.as<float4>(), precision ? pk.as<double4>() : nullptr, n};
   launch_gpe(rp, b, b + m, b + 2 * m, b + 3 * m, m, eps, nullptr, part.as<double>(), precision, s);
-  launch_reduce(nullptr, 0, part.as<double>(), ngw, -1.0, sums.as<double>(), s);
+  launch_reduce(nullptr, 0, part.as<double>(), ngw, -1.0, sums.as<double>(),
+                sums.as<double>() + kPartialStride, s);
   FGA_CUDA_TRY(cudaGetLastError());
   double v = 0.0;
   FGA_CUDA_TRY(cudaMemcpyAsync(&v, sums.as<double>() + kGpe, sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -107,4 +107,24 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Fixed-order block reduction (kOp 0 sum, 1 min, 2 max); the result is valid
+// on every thread.  Deterministic for a given blockDim.
+template <int kOp>
+__device__ __forceinline__ double op3(double a, double b) {
+  return kOp == 0 ? a + b : (kOp == 1 ? fmin(a, b) : fmax(a, b));
+}
+template <int kOp>
+__device__ double block_reduce(double v) {
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op3<kOp>(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();  // sh may still be read by a previous call
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  v = sh[0];
+  for (int j = 1; j < nw; j++) v = op3<kOp>(v, sh[j]);
+  return v;
+}
+
 }  // namespace fga

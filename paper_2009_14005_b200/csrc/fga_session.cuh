@@ -50,8 +50,10 @@ void launch_direct_operator(const RefPoints& ref, const double* qx, const double
                             double* fout, int precision, cudaStream_t s);
 
 // Rigid side (rigid.cu)
+size_t reduce_stage_doubles();
 void launch_reduce(const double* partials, int64_t nwarps, const double* gpe_partials,
-                   int64_t ngwarps, double direct_pairs, double* sums, cudaStream_t s);
+                   int64_t ngwarps, double direct_pairs, double* sums, double* stage,
+                   cudaStream_t s);
 void launch_update(const double* sums, IterState* st, const SimParams& sp, double* rec_delta,
                    double* rec_traj, double* rec_gpe, long long* rec_inter, long long* rec_visits,
                    int has_gpe, cudaStream_t s);
@@ -68,6 +70,8 @@ int niv_masses_dev(const double* pts, int64_t n, int dim, int rho, double a, dou
                    double* out, int* flat_scratch, long long* counts_scratch, double* cells_scratch,
                    cudaStream_t s);
 void launch_external_masses(const double* w, int64_t n, double* out, cudaStream_t s);
+size_t pairwise_sum_scratch_doubles(int64_t n);
+void launch_np_sum(const double* a, int64_t n, double* out, double* scratch, cudaStream_t s);
 void launch_rescale(double* sx, int64_t n, double* sy, int64_t m, double dt, double eta,
                     double* scratch, cudaStream_t s);
 void launch_pack_ref(const double* xn, const double* mx, int64_t n, float4* p32, double4* p64,

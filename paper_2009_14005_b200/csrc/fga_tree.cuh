@@ -8,21 +8,7 @@
 
 namespace fga {
 
-// Ascending-preorder node arrays (the reference's numbering, bhtree.py:77).
-struct TreeNodesView {
-  signed char* level;
-  int* start;
-  int* occ;
-  int* skip;
-  int* parent;
-  unsigned* childmask;
-  int* arrive;
-  int* children;  // (n_nodes, 8), -1 absent
-  double* mass;
-  double* mc;     // sum m*p (n_nodes, 3)
-  double* com;    // (n_nodes, 3)
-  double* length;
-};
+constexpr int kLvlInts = 2 * (kMaxLevels + 1) + 2 * (kMaxLevels + 3);
 
 // Mirrored-preorder traversal records.
 struct TreeRecords {
@@ -42,24 +28,19 @@ struct TreeDev {
   const double* pts = nullptr;     // (n,3) device, not owned
   const double* masses = nullptr;  // (n,) device, not owned
   DevBuf box, scratch, keys_in, keys, idx_in, idx, clev, count, offset, cub_tmp;
-  DevBuf level, start, occ, skip, parent, childmask, arrive, children, mass, mc, com, length;
+  // build intermediates: packed (x,y,z,m) in input order, sorted copy, level
+  // counts/offsets, internal-node lists, BFS-ordered node sums (mass, m*p)
+  DevBuf packed, sp, bcount, lvl, inodes, sums;
   DevBuf a32, b32, a64, b64;
   DevBuf export_buf;
 
-  TreeNodesView view() const {
-    return TreeNodesView{level.as<signed char>(), start.as<int>(),    occ.as<int>(),
-                         skip.as<int>(),          parent.as<int>(),   childmask.as<unsigned>(),
-                         arrive.as<int>(),        children.as<int>(), mass.as<double>(),
-                         mc.as<double>(),         com.as<double>(),   length.as<double>()};
-  }
   TreeRecords records() const {
     return TreeRecords{a32.as<float4>(), b32.as<NodeB32>(), a64.as<double4>(), b64.as<NodeB64>()};
   }
   void release() {
-    DevBuf* all[] = {&box,  &scratch, &keys_in,   &keys,   &idx_in,   &idx,      &clev,
-                     &count, &offset, &cub_tmp,   &level,  &start,    &occ,      &skip,
-                     &parent, &childmask, &arrive, &children, &mass,  &mc,       &com,
-                     &length, &a32,   &b32,       &a64,    &b64,      &export_buf};
+    DevBuf* all[] = {&box,    &scratch, &keys_in, &keys,   &idx_in, &idx, &clev,
+                     &count,  &offset,  &cub_tmp, &packed, &sp,     &bcount, &lvl,
+                     &inodes, &sums,    &a32,     &b32,    &a64,    &b64,  &export_buf};
     for (DevBuf* b : all) b->release();
     n_nodes = 0;
     exportable = false;

@@ -15,34 +15,43 @@ namespace {
 
 constexpr int kReduceThreads = 1024;
 
-// Block-wide sums of the per-warp partial records, fixed order.
-__global__ void __launch_bounds__(kReduceThreads) k_reduce(const double* __restrict__ partials,
-                                                           int64_t nwarps,
-                                                           const double* __restrict__ gpe_part,
-                                                           int64_t ngwarps, double direct_pairs,
-                                                           double* __restrict__ sums) {
+// Sums of the per-warp partial records in a fixed order: kRedBlocks blocks
+// each reduce a contiguous range of warps (thread-strided, then a fixed block
+// tree), one warp adds the block results in block order.
+constexpr int kRedBlocks = 148;
+constexpr int kRedThreads = 256;
+
+__global__ void __launch_bounds__(kRedThreads) k_reduce_stage(const double* __restrict__ partials,
+                                                             int64_t nwarps,
+                                                             const double* __restrict__ gpe_part,
+                                                             int64_t ngwarps,
+                                                             double* __restrict__ stage) {
+  const int64_t b = blockIdx.x, nb = gridDim.x;
+  const int64_t w0 = nwarps * b / nb, w1 = nwarps * (b + 1) / nb;
+  const int64_t g0 = ngwarps * b / nb, g1 = ngwarps * (b + 1) / nb;
   double acc[kPartialStride];
 #pragma unroll
   for (int k = 0; k < kPartialStride; k++) acc[k] = 0.0;
-  for (int64_t w = threadIdx.x; w < nwarps; w += kReduceThreads) {
+  for (int64_t w = w0 + threadIdx.x; w < w1; w += kRedThreads) {
 #pragma unroll
     for (int k = 0; k < 17; k++) acc[k] += partials[w * kPartialStride + k];
   }
-  for (int64_t w = threadIdx.x; w < ngwarps; w += kReduceThreads) acc[kGpe] += gpe_part[w];
-  __shared__ double sm[kReduceThreads / 32][kPartialStride];
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-#pragma unroll
+  for (int64_t w = g0 + threadIdx.x; w < g1; w += kRedThreads) acc[kGpe] += gpe_part[w];
+#pragma unroll 1
   for (int k = 0; k < kPartialStride; k++) {
-    const double v = warp_sum(acc[k]);
-    if (lane == 0) sm[wl][k] = v;
+    const double v = block_reduce<0>(acc[k]);
+    if (threadIdx.x == 0) stage[b * kPartialStride + k] = v;
   }
-  __syncthreads();
-  if (threadIdx.x < kPartialStride) {
-    double v = 0.0;
-    for (int j = 0; j < kReduceThreads / 32; j++) v += sm[j][threadIdx.x];
-    if (direct_pairs >= 0.0 && (threadIdx.x == kAccepted || threadIdx.x == kVisits)) v = direct_pairs;
-    sums[threadIdx.x] = v;
-  }
+}
+
+__global__ void k_reduce_final(const double* __restrict__ stage, int nb, double direct_pairs,
+                               double* __restrict__ sums) {
+  const int k = threadIdx.x;
+  if (k >= kPartialStride) return;
+  double v = 0.0;
+  for (int b = 0; b < nb; b++) v += stage[b * kPartialStride + k];
+  if (direct_pairs >= 0.0 && (k == kAccepted || k == kVisits)) v = direct_pairs;
+  sums[k] = v;
 }
 
 __global__ void k_update(const double* __restrict__ sums, IterState* st, SimParams sp,
@@ -204,10 +213,13 @@ __global__ void __launch_bounds__(kReduceThreads) k_solve_rigid(const double* __
 
 }  // namespace
 
+size_t reduce_stage_doubles() { return (size_t)kRedBlocks * kPartialStride; }
+
 void launch_reduce(const double* partials, int64_t nwarps, const double* gpe_partials,
-                   int64_t ngwarps, double direct_pairs, double* sums, cudaStream_t s) {
-  k_reduce<<<1, kReduceThreads, 0, s>>>(partials, nwarps, gpe_partials, ngwarps, direct_pairs,
-                                        sums);
+                   int64_t ngwarps, double direct_pairs, double* sums, double* stage,
+                   cudaStream_t s) {
+  k_reduce_stage<<<kRedBlocks, kRedThreads, 0, s>>>(partials, nwarps, gpe_partials, ngwarps, stage);
+  k_reduce_final<<<1, 32, 0, s>>>(stage, kRedBlocks, direct_pairs, sums);
 }
 
 void launch_update(const double* sums, IterState* st, const SimParams& sp, double* rec_delta,

@@ -8,6 +8,9 @@
 // bit-identical to numpy's (tests/test_gpu_setup.py).  The cloud means use a
 // sequential column sum because that IS numpy's order for an axis-0
 // reduction of an (n,3) C-contiguous array.
+#include <algorithm>
+#include <vector>
+
 #include <cub/cub.cuh>
 
 #include "../../include/fga.h"
@@ -191,32 +194,86 @@ __global__ void k_external(const double* __restrict__ w, int64_t n, double* __re
 }
 
 // ---------------------------------------------------------------- rescale
-// Deterministic sum(sx) and max(sy); one block.
-__global__ void k_sum_max(const double* __restrict__ sx, int64_t n, const double* __restrict__ sy,
-                          int64_t m, double* out2) {
-  double s = 0.0, mx = -INFINITY;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += sx[i];
-  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) mx = fmax(mx, sy[i]);
-  s = warp_sum(s);
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  __shared__ double a[32], b[32];
-  if ((threadIdx.x & 31) == 0) {
-    a[threadIdx.x >> 5] = s;
-    b[threadIdx.x >> 5] = mx;
+// ---- numpy's float64 sum of a contiguous 1-D array, bit for bit:
+// pairwise_sum_DOUBLE (numpy umath loops_utils.h.src) splits n at
+// n2 = n/2 - (n/2)%8 until n <= 128, sums such a block with 8 interleaved
+// accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus the
+// n%8 tail, and n < 8 sequentially from 0.  The recursion tree depends on n
+// only: one thread per node at a depth d0 where every shallower node is
+// internal (the tree is complete down to d0), then the complete top d0 levels
+// are combined pairwise, left + right, in one block.
+__device__ double np_pairwise_sum(const double* __restrict__ a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; i++) r = __dadd_rn(r, a[i]);
+    return r;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0, u = -INFINITY;
-    for (int j = 0; j < (int)(blockDim.x >> 5); j++) {
-      t += a[j];
-      u = fmax(u, b[j]);
-    }
-    out2[0] = t;
-    out2[1] = u;
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; i++) res = __dadd_rn(res, a[i]);
+    return res;
   }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise_sum(a, n2), np_pairwise_sum(a + n2, n - n2));
 }
 
-// sx <- min(budget * sx / sum(sx), 0.022); sy <- max(0.1 * sy / max(sy), floor)
+__global__ void k_pw_nodes(const double* __restrict__ a, int64_t n, int d0, double* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (1ll << d0)) return;
+  int64_t lo = 0, len = n;
+  for (int l = d0 - 1; l >= 0; l--) {  // path bits, most significant = first split
+    int64_t n2 = len / 2;
+    n2 -= n2 % 8;
+    if ((t >> l) & 1) {
+      lo += n2;
+      len -= n2;
+    } else {
+      len = n2;
+    }
+  }
+  out[t] = np_pairwise_sum(a + lo, len);
+}
+
+// buf holds 2^d0 node sums; ping-pongs with buf + 2^d0; result -> *out
+__global__ void k_pw_combine(double* __restrict__ buf, int d0, double* __restrict__ out) {
+  double* src = buf;
+  double* dst = buf + (1ll << d0);
+  for (int l = d0; l > 0; l--) {
+    const int cnt = 1 << (l - 1);
+    for (int k = threadIdx.x; k < cnt; k += blockDim.x) dst[k] = __dadd_rn(src[2 * k], src[2 * k + 1]);
+    __syncthreads();
+    double* t = src;
+    src = dst;
+    dst = t;
+  }
+  if (threadIdx.x == 0) *out = src[0];
+}
+
+// max(sy): per-block partials, then one block (order-free)
+__global__ void k_max_partial(const double* __restrict__ sy, int64_t m, double* __restrict__ part) {
+  double mx = -INFINITY;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += stride)
+    mx = fmax(mx, sy[i]);
+  mx = block_reduce<2>(mx);
+  if (threadIdx.x == 0) part[blockIdx.x] = mx;
+}
+__global__ void k_max_final(const double* __restrict__ part, int nparts, double* out) {
+  double mx = -INFINITY;
+  for (int j = threadIdx.x; j < nparts; j += blockDim.x) mx = fmax(mx, part[j]);
+  mx = block_reduce<2>(mx);
+  if (threadIdx.x == 0) *out = mx;
+}
+
 __global__ void k_rescale(double* sx, int64_t n, double* sy, int64_t m, const double* sm2,
                           double budget, double floor_) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -252,10 +309,12 @@ __global__ void k_mean_partial(const double* __restrict__ p, int64_t n, double* 
   }
 }
 __global__ void k_mean_final(const double* __restrict__ part, int nparts, int64_t n, double* out3) {
-  if (threadIdx.x >= 3) return;
-  double v = 0.0;
-  for (int j = 0; j < nparts; j++) v += part[j * 3 + threadIdx.x];
-  out3[threadIdx.x] = v / (double)n;
+  for (int k = 0; k < 3; k++) {
+    double v = 0.0;
+    for (int j = threadIdx.x; j < nparts; j += blockDim.x) v += part[j * 3 + k];
+    v = block_reduce<0>(v);
+    if (threadIdx.x == 0) out3[k] = v / (double)n;
+  }
 }
 
 __global__ void k_bbox6_partial(const double* __restrict__ p, int64_t n, double* __restrict__ part) {
@@ -286,11 +345,13 @@ __global__ void k_bbox6_partial(const double* __restrict__ p, int64_t n, double*
   }
 }
 __global__ void k_bbox6_final(const double* __restrict__ part, int nparts, double* out6) {
-  const int k = threadIdx.x;
-  if (k >= 6) return;
-  double v = part[k];
-  for (int j = 1; j < nparts; j++) v = k < 3 ? fmin(v, part[j * 6 + k]) : fmax(v, part[j * 6 + k]);
-  out6[k] = v;
+  for (int k = 0; k < 6; k++) {
+    double v = k < 3 ? INFINITY : -INFINITY;
+    for (int j = threadIdx.x; j < nparts; j += blockDim.x)
+      v = k < 3 ? fmin(v, part[j * 6 + k]) : fmax(v, part[j * 6 + k]);
+    v = k < 3 ? block_reduce<1>(v) : block_reduce<2>(v);
+    if (threadIdx.x == 0) out6[k] = v;
+  }
 }
 
 // 21-bit-per-axis Morton key over the cloud's own bbox (locality only).
@@ -405,11 +466,52 @@ void launch_external_masses(const double* w, int64_t n, double* out, cudaStream_
 
 // registration.py:85-87 (FIELD_MASS=16, FIELD_MASS_POINTS=2000,
 // REFERENCE_POINT_CAP=0.022, TEMPLATE_PEAK_MASS=0.1, floor max(1e-6, dt*eta))
+// depth d0 <= 16 of the pairwise recursion down to which every node is
+// internal (sizes at one depth take only a few distinct values)
+static int pw_depth(int64_t n) {
+  std::vector<int64_t> sizes{n};
+  int d = 0;
+  while (d < 16) {
+    int64_t mn = sizes[0];
+    for (int64_t v : sizes) mn = std::min(mn, v);
+    if (mn <= 128) break;
+    std::vector<int64_t> next;
+    for (int64_t v : sizes) {
+      int64_t n2 = v / 2;
+      n2 -= n2 % 8;
+      for (int64_t c : {n2, v - n2})
+        if (std::find(next.begin(), next.end(), c) == next.end()) next.push_back(c);
+    }
+    sizes.swap(next);
+    d++;
+  }
+  return d;
+}
+
+size_t pairwise_sum_scratch_doubles(int64_t n) { return 2 * ((size_t)1 << pw_depth(n)); }
+
+// numpy float64 sum(a) of a contiguous device array -> *out (device)
+void launch_np_sum(const double* a, int64_t n, double* out, double* scratch, cudaStream_t s) {
+  const int d0 = pw_depth(n);
+  const int64_t nodes = 1ll << d0;
+  k_pw_nodes<<<(unsigned)((nodes + 127) / 128), 128, 0, s>>>(a, n, d0, scratch);
+  k_pw_combine<<<1, 1024, 0, s>>>(scratch, d0, out);
+}
+
+// registration.py:85-87 (FIELD_MASS=16, FIELD_MASS_POINTS=2000,
+// REFERENCE_POINT_CAP=0.022, TEMPLATE_PEAK_MASS=0.1, floor max(1e-6, dt*eta));
+// sx.sum() is numpy's pairwise sum, reproduced exactly.  scratch: 8 +
+// pairwise_sum_scratch_doubles(n) + 600 doubles.
 void launch_rescale(double* sx, int64_t n, double* sy, int64_t m, double dt, double eta,
                     double* scratch, cudaStream_t s) {
   const double budget = 16.0 * std::sqrt((double)n / 2000.0);
   const double floor_ = std::max(1e-6, dt * eta);
-  k_sum_max<<<1, 1024, 0, s>>>(sx, n, sy, m, scratch);
+  double* pw = scratch + 8;
+  double* part = pw + pairwise_sum_scratch_doubles(n);
+  launch_np_sum(sx, n, scratch, pw, s);
+  const int nb = (int)std::min<int64_t>(nblk(m), 592);
+  k_max_partial<<<nb, kT, 0, s>>>(sy, m, part);
+  k_max_final<<<1, 256, 0, s>>>(part, nb, scratch + 1);
   k_rescale<<<nblk(std::max(n, m)), kT, 0, s>>>(sx, n, sy, m, scratch, budget, floor_);
 }
 
@@ -421,13 +523,13 @@ void launch_pack_ref(const double* xn, const double* mx, int64_t n, float4* p32,
 void launch_mean3(const double* pts, int64_t n, double* scratch, double* out3, cudaStream_t s) {
   const int nb = (int)std::min<int64_t>(nblk(n), 592);
   k_mean_partial<<<nb, kT, 0, s>>>(pts, n, scratch);
-  k_mean_final<<<1, 32, 0, s>>>(scratch, nb, n, out3);
+  k_mean_final<<<1, 256, 0, s>>>(scratch, nb, n, out3);
 }
 
 void launch_bbox(const double* pts, int64_t n, double* scratch, double* out6, cudaStream_t s) {
   const int nb = (int)std::min<int64_t>(nblk(n), 592);
   k_bbox6_partial<<<nb, kT, 0, s>>>(pts, n, scratch);
-  k_bbox6_final<<<1, 32, 0, s>>>(scratch, nb, out6);
+  k_bbox6_final<<<1, 256, 0, s>>>(scratch, nb, out6);
 }
 
 void launch_morton_keys(const double* pts, int64_t n, const double* box6,

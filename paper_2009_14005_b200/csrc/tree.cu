@@ -14,20 +14,23 @@
 //   count = s_i > L ? 0 : max(1, e_i - s_i + 1)
 //   preorder(i, l) = excl_scan(count)_i + (l - s_i)
 // which is exactly the reference's preorder: (start, level) lexicographic.
-// Node aggregates are reduced bottom-up (last-arriving child computes the
-// parent, children in slot order: deterministic), then the traversal records
-// are written in *mirrored* preorder (see fga_internal.cuh).
+// Children of a node in ascending preorder are x+1, skip[x+1], ... < skip[x]
+// in slot order, so no child table is kept.  Node aggregates are reduced
+// level by level from the depth cap up (children in slot order:
+// deterministic), and each node's traversal records are written in the same
+// pass, in *mirrored* preorder (see fga_internal.cuh).
 //
 // Kernels (all HBM/L2-bound integer + fp64 work; no tensor cores):
 //   k_bbox_*        root bbox = per-axis min/max (bhtree.py:107-108)
-//   k_keys          exact per-axis fp64 split replay -> 3L-bit key
+//   k_keys          per-axis fp64 split recursion -> 3L-bit key (dyadic fast
+//                   path with an exact-replay fallback near split planes)
 //   (cub radix sort, stable: keeps the reference's within-leaf index order)
-//   k_levels        c_i and per-point node counts
-//   (cub exclusive scan) -> node offsets, node count
-//   k_emit          per node: level, start, occupancy, skip, parent, slot,
-//                   children[parent][slot], bbox replay -> length (:83)
-//   k_summarize     mass, m*com bottom-up (:78-82)
-//   k_records       mirrored traversal records (fp32 and fp64)
+//   k_levels        c_i, per-point node counts, per-block per-level counts
+//   (cub exclusive scan) -> preorder node offsets, node count
+//   k_level_scan    per level: block offsets -> level-major (BFS) positions
+//   k_emit          per node, in BFS order: start, occupancy, first child,
+//                   mirrored index, bbox replay -> length (:83)
+//   k_sum_level x (L+1)  mass, m*com bottom-up (:78-82) + mirrored records
 #include <cub/cub.cuh>
 
 #include "fga_internal.cuh"
@@ -81,248 +84,541 @@ __global__ void k_bbox_partial(const double* __restrict__ pts, int64_t n, double
   }
 }
 
-__global__ void k_bbox_final(const double* __restrict__ part, int nparts, double* __restrict__ out) {
-  int k = threadIdx.x;
-  if (k >= 6) return;
-  double r = part[k];
-  for (int j = 1; j < nparts; j++) r = k < 3 ? fmin(r, part[j * 6 + k]) : fmax(r, part[j * 6 + k]);
-  out[k] = r;
+// box[0..5] = lo, hi; box[6..8] = 2^L / (hi - lo) per axis; box[9] = the
+// fast-key guard (see k_keys)
+__global__ void k_bbox_final(const double* __restrict__ part, int nparts, int L,
+                             double* __restrict__ out) {
+  for (int k = 0; k < 6; k++) {
+    double v = k < 3 ? INFINITY : -INFINITY;
+    for (int j = threadIdx.x; j < nparts; j += blockDim.x)
+      v = k < 3 ? fmin(v, part[j * 6 + k]) : fmax(v, part[j * 6 + k]);
+    v = k < 3 ? block_reduce<1>(v) : block_reduce<2>(v);
+    if (threadIdx.x == 0) out[k] = v;
+  }
+  if (threadIdx.x == 0) {
+    double R = 0.0;
+    for (int k = 0; k < 3; k++) {
+      const double w = out[3 + k] - out[k];
+      out[6 + k] = w > 0.0 ? ldexp(1.0, L) / w : 0.0;
+      R = fmax(R, fmax(fabs(out[k]), fabs(out[3 + k])));
+    }
+    out[9] = 256.0 * 1.1102230246251565e-16 * R;  // 256 u R
+  }
 }
 
 // ---------------------------------------------------------------- keys
-// Exact replay of the per-axis fp64 midpoint recursion.  __dadd_rn/__dmul_rn
-// keep nvcc from contracting anything: (hi - lo) / 2.0 == (hi - lo) * 0.5
-// exactly in binary floating point.
-__global__ void k_keys(const double* __restrict__ pts, int64_t n, const double* __restrict__ box,
-                       int L, unsigned long long* __restrict__ keys, int* __restrict__ idx) {
+// Keys = the per-axis fp64 midpoint recursion of the reference
+// (bhtree.py:89-104): c = lo + (hi - lo)/2, bit = x >= c, 3 bits per level,
+// x most significant.
+//
+// Fast path: every split plane the recursion produces is the exact dyadic
+// plane lo0 + j (hi0 - lo0)/2^(l+1) up to accumulated rounding (<= ~4u R per
+// level, R = max |box|), and the planes a point is tested against include
+// the two finest-grid lines around it, the nearest planes of all.  So when
+// f = (x - lo0) 2^L/(hi0 - lo0) is farther than a guard (256 u R, x units)
+// from an integer, the recursion's bits are exactly floor(f).  Otherwise (a
+// few points in 1e7, the top corner, flat axes) the recursion is replayed
+// with __dadd_rn/__dmul_rn, so the result always equals the reference's.
+__device__ __forceinline__ unsigned long long spread3(unsigned long long v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x1f00000000ffffull;
+  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+
+__device__ __forceinline__ bool fast_axis(double x, double lo0, double scale, double gf, int L,
+                                          unsigned long long& q) {
+  if (!(scale > 0.0)) return false;
+  const double f = (x - lo0) * scale;
+  const double fl = floor(f);
+  const double fr = f - fl;
+  if (!(fmin(fr, 1.0 - fr) > gf) || fl < 0.0 || fl >= ldexp(1.0, L)) return false;
+  q = (unsigned long long)fl;
+  return true;
+}
+
+__global__ void k_keys(const double* __restrict__ pts, const double* __restrict__ masses, int64_t n,
+                       const double* __restrict__ box, int L, unsigned long long* __restrict__ keys,
+                       int* __restrict__ idx, double4* __restrict__ packed) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  double p[3], lo[3], hi[3];
+  double p[3];
 #pragma unroll
-  for (int k = 0; k < 3; k++) {
-    p[k] = pts[i * 3 + k];
-    lo[k] = box[k];
-    hi[k] = box[3 + k];
-  }
+  for (int k = 0; k < 3; k++) p[k] = pts[i * 3 + k];
+  packed[i] = make_double4(p[0], p[1], p[2], masses[i]);  // one 32 B record per point
+  const double guard = box[9];
+  unsigned long long q[3];
+  bool fast = true;
+#pragma unroll
+  for (int k = 0; k < 3; k++)
+    fast = fast_axis(p[k], box[k], box[6 + k], guard * box[6 + k], L, q[k]) && fast;
   unsigned long long key = 0;
-  for (int l = 0; l < L; l++) {
-    unsigned digit = 0;
+  if (fast) {
+    key = (spread3(q[0]) << 2) | (spread3(q[1]) << 1) | spread3(q[2]);
+  } else {
+    double lo[3], hi[3];
 #pragma unroll
     for (int k = 0; k < 3; k++) {
-      double c = __dadd_rn(lo[k], __dmul_rn(__dsub_rn(hi[k], lo[k]), 0.5));
-      bool up = p[k] >= c;
-      digit = (digit << 1) | (up ? 1u : 0u);
-      if (up) lo[k] = c; else hi[k] = c;
+      lo[k] = box[k];
+      hi[k] = box[3 + k];
     }
-    key = (key << 3) | digit;
+    for (int l = 0; l < L; l++) {
+      unsigned digit = 0;
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        double c = __dadd_rn(lo[k], __dmul_rn(__dsub_rn(hi[k], lo[k]), 0.5));
+        bool up = p[k] >= c;
+        digit = (digit << 1) | (up ? 1u : 0u);
+        if (up) lo[k] = c; else hi[k] = c;
+      }
+      key = (key << 3) | digit;
+    }
   }
   keys[i] = key;
   idx[i] = (int)i;
 }
 
-// c_i for i in [0, N] and the number of nodes each point starts.
-__global__ void k_levels(const unsigned long long* __restrict__ keys, int64_t n, int L,
-                         signed char* __restrict__ clev, int* __restrict__ count) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i > n) return;
-  int c = (i == 0 || i == n) ? -1 : common_levels(keys[i - 1], keys[i], L);
-  clev[i] = (signed char)c;
-  if (i == n) {
-    count[i] = 0;
-    return;
+// Point i's chain of nodes: (i, l) for s <= l <= e, where s = c_i + 1 and
+// e = max(s, min(L, c_{i+1} + 1)); none when s > L (a duplicate key).  The
+// nodes below e are internal (they also hold point i+1, which shares c_{i+1}
+// >= l levels) and (i, e) is always a leaf: it holds point i alone, or sits at
+// the depth cap.
+struct Chain {
+  int s, e, cn;
+};
+__device__ __forceinline__ Chain chain_of(const signed char* __restrict__ clev, int64_t i,
+                                          int64_t n, int L) {
+  Chain c{L + 1, -1, -1};
+  if (i < n) {
+    c.cn = clev[i + 1];
+    c.s = clev[i] + 1;
+    if (c.s <= L) c.e = max(c.s, min(L, c.cn + 1));
   }
-  int cn = (i + 1 == n) ? -1 : common_levels(keys[i], keys[i + 1], L);
-  int s = c + 1;
-  int cnt = 0;
-  if (s <= L) {
-    int e = min(L, cn + 1);
-    cnt = max(1, e - s + 1);
-  }
-  count[i] = cnt;
+  return c;
 }
 
-// first j in [lo, hi) with keys[j] > bound (keys sorted)
-__device__ __forceinline__ int64_t upper_bound_key(const unsigned long long* keys, int64_t lo,
-                                                   int64_t hi, unsigned long long bound) {
+// c_i for i in [0, N], the number of nodes each point starts, and per block
+// of kThreads points the number of nodes it starts at each level:
+// bcount[l * nb + block] (all nodes) and bcount[(L + 1 + l) * nb + block]
+// (internal nodes).
+__global__ void __launch_bounds__(kThreads) k_levels(const unsigned long long* __restrict__ keys,
+                                                     int64_t n, int L,
+                                                     signed char* __restrict__ clev,
+                                                     int* __restrict__ count,
+                                                     int* __restrict__ bcount) {
+  __shared__ int hist[2 * (kMaxLevels + 1)];
+  if (threadIdx.x < 2 * (kMaxLevels + 1)) hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i <= n) {
+    const int c = (i == 0 || i == n) ? -1 : common_levels(keys[i - 1], keys[i], L);
+    clev[i] = (signed char)c;
+    int cnt = 0;
+    if (i < n) {
+      const int cn = (i + 1 == n) ? -1 : common_levels(keys[i], keys[i + 1], L);
+      const int s = c + 1;
+      if (s <= L) {
+        const int e = max(s, min(L, cn + 1));
+        cnt = e - s + 1;
+        for (int l = s; l <= e; l++) atomicAdd(&hist[l], 1);
+        for (int l = s; l < e; l++) atomicAdd(&hist[L + 1 + l], 1);
+      }
+    }
+    count[i] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * (L + 1))
+    bcount[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = hist[threadIdx.x];
+}
+
+// Per row (one block each): exclusive scan of the block counts in place, the
+// row total into row_total[row].
+__global__ void __launch_bounds__(1024) k_level_scan(int* __restrict__ bcount, int nb,
+                                                     int* __restrict__ row_total) {
+  const int row = blockIdx.x;
+  int* v = bcount + (int64_t)row * nb;
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int b0 = min(nb, (int)threadIdx.x * per), b1 = min(nb, b0 + per);
+  int sum = 0;
+  for (int b = b0; b < b1; b++) sum += v[b];
+  __shared__ int sh[1024];
+  sh[threadIdx.x] = sum;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {  // inclusive Hillis-Steele
+    const int t = threadIdx.x >= (unsigned)o ? sh[threadIdx.x - o] : 0;
+    __syncthreads();
+    sh[threadIdx.x] += t;
+    __syncthreads();
+  }
+  int acc = sh[threadIdx.x] - sum;
+  for (int b = b0; b < b1; b++) {
+    const int t = v[b];
+    v[b] = acc;
+    acc += t;
+  }
+  if (threadIdx.x == blockDim.x - 1) row_total[row] = sh[threadIdx.x];
+}
+
+// lvl_off[l]: first BFS position of level l (lvl_off[L+1] = lvl_off[L+2] =
+// node count); ilvl_off[l]: first slot of level l in the internal-node list.
+__global__ void k_level_offsets(const int* __restrict__ row_total, int L, int* __restrict__ lvl_off,
+                                int* __restrict__ ilvl_off) {
+  if (threadIdx.x != 0) return;
+  int a = 0, b = 0;
+  for (int l = 0; l <= L; l++) {
+    lvl_off[l] = a;
+    ilvl_off[l] = b;
+    a += row_total[l];
+    b += row_total[L + 1 + l];
+  }
+  lvl_off[L + 1] = lvl_off[L + 2] = a;
+  ilvl_off[L + 1] = b;
+}
+
+// first j in [from, n) with keys[j] > bound (keys sorted): galloping search
+// from `from` (subtree ends are near the start for all but the top levels)
+__device__ __forceinline__ int64_t upper_bound_gallop(const unsigned long long* keys, int64_t from,
+                                                      int64_t n, unsigned long long bound) {
+  int64_t lo = from, hi = n, step = 1;
+  while (true) {
+    const int64_t j = lo + step - 1;
+    if (j >= n) break;
+    if (keys[j] > bound) {
+      hi = j;
+      break;
+    }
+    lo = j + 1;
+    step <<= 1;
+  }
   while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
+    const int64_t mid = (lo + hi) >> 1;
     if (keys[mid] > bound) hi = mid; else lo = mid + 1;
   }
   return lo;
 }
-// first j in [lo, hi) with keys[j] >= bound
-__device__ __forceinline__ int64_t lower_bound_key(const unsigned long long* keys, int64_t lo,
-                                                   int64_t hi, unsigned long long bound) {
+
+// One bbox split step of the reference's recursion (bhtree.py:90-103) along
+// the key digit of level `lev`.
+__device__ __forceinline__ void bbox_step(unsigned long long key, int lev, int L, double lo[3],
+                                          double hi[3]) {
+  const unsigned digit = (unsigned)(key >> (3 * (L - lev))) & 7u;
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    const double c = __dadd_rn(lo[k], __dmul_rn(__dsub_rn(hi[k], lo[k]), 0.5));
+    if ((digit >> (2 - k)) & 1u) lo[k] = c; else hi[k] = c;
+  }
+}
+
+// numpy's pairwise 1-D sum (loops_utils.h.src) of the masses of sorted
+// points [lo, lo + cnt); leaves hold one point except at the depth cap,
+// where this makes the leaf mass bit-exact.
+__device__ double pairwise_mass(const double4* __restrict__ sp, int64_t lo, int64_t cnt) {
+  if (cnt < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < cnt; i++) r = __dadd_rn(r, sp[lo + i].w);
+    return r;
+  } else if (cnt <= 128) {
+    double r[8];
+    int64_t i;
+    for (int j = 0; j < 8; j++) r[j] = sp[lo + j].w;
+    for (i = 8; i < cnt - (cnt % 8); i += 8)
+      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], sp[lo + i + j].w);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < cnt; i++) res = __dadd_rn(res, sp[lo + i].w);
+    return res;
+  }
+  int64_t n2 = cnt / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_mass(sp, lo, n2), pairwise_mass(sp, lo + n2, cnt - n2));
+}
+
+// Leaf aggregate (bhtree.py:78-82): pairwise mass, sequential sum of m*p.
+__device__ __forceinline__ void leaf_sums(const double4* __restrict__ sp, int start, int occ,
+                                          double& ms, double mc[3]) {
+  ms = occ == 1 ? sp[start].w : pairwise_mass(sp, start, occ);
+  mc[0] = mc[1] = mc[2] = 0.0;
+  for (int q = 0; q < occ; q++) {
+    const double4 v = sp[start + q];
+    mc[0] = __dadd_rn(mc[0], __dmul_rn(v.x, v.w));
+    mc[1] = __dadd_rn(mc[1], __dmul_rn(v.y, v.w));
+    mc[2] = __dadd_rn(mc[2], __dmul_rn(v.z, v.w));
+  }
+}
+
+// The node's traversal records at its mirrored-preorder index.
+__device__ __forceinline__ void write_records(const TreeRecords& r, int mir, int rskip, bool leaf,
+                                              double len, double ms, const double mc[3]) {
+  const double cx = __ddiv_rn(mc[0], ms), cy = __ddiv_rn(mc[1], ms), cz = __ddiv_rn(mc[2], ms);
+  const double l2 = __dmul_rn(len, len);
+  r.a64[mir] = make_double4(cx, cy, cz, ms);
+  r.b64[mir] = NodeB64{leaf ? -INFINITY : l2, (long long)rskip};
+  r.a32[mir] = make_float4((float)cx, (float)cy, (float)cz, (float)ms);
+  r.b32[mir] = NodeB32{leaf ? -INFINITY : (float)l2, rskip};
+}
+
+// Sorted copy of the points with their masses: one gather after the sort so
+// that every later pass reads points contiguously.
+__global__ void k_gather_sorted(const double4* __restrict__ packed, const int* __restrict__ idx,
+                                int64_t n, double4* __restrict__ sp) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  sp[i] = packed[idx[i]];
+}
+
+// Within-block ranks of the threads whose chains hold a node at level l
+// (all nodes, and internal nodes only): warp ballots + warp prefix in shared
+// memory.  Must be called by the whole block.
+struct BlockRanks {
+  unsigned bal[2][kMaxLevels + 1][kThreads / 32];
+  int pre[2][kMaxLevels + 1][kThreads / 32];
+};
+__device__ __forceinline__ void block_ranks(BlockRanks& R, const Chain& c, int L) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int l = 0; l <= L; l++) {
+    const unsigned ba = __ballot_sync(0xffffffffu, c.s <= l && l <= c.e);
+    const unsigned bi = __ballot_sync(0xffffffffu, c.s <= l && l < c.e);
+    if (lane == 0) {
+      R.bal[0][l][w] = ba;
+      R.pre[0][l][w] = __popc(ba);
+      R.bal[1][l][w] = bi;
+      R.pre[1][l][w] = __popc(bi);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * (L + 1)) {
+    const int k = threadIdx.x > L, l = threadIdx.x - k * (L + 1);
+    int acc = 0;
+    for (int q = 0; q < kThreads / 32; q++) {
+      const int v = R.pre[k][l][q];
+      R.pre[k][l][q] = acc;
+      acc += v;
+    }
+  }
+  __syncthreads();
+}
+// slot of this thread's node at level l among all (k=0) / internal (k=1)
+// level-l nodes: global offsets + block offset + warp prefix + lane rank
+__device__ __forceinline__ int level_slot(const BlockRanks& R, int k, int l, int L,
+                                          const int* __restrict__ off,
+                                          const int* __restrict__ boff) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  return off[l] + boff[(int64_t)(k * (L + 1) + l) * gridDim.x + blockIdx.x] + R.pre[k][l][w] +
+         __popc(R.bal[k][l][w] & ((1u << lane) - 1u));
+}
+
+// Internal node of the level lists (one 32-byte record).
+struct InNode {
+  int pos;    // BFS position (sums[] index)
+  int fc;     // BFS position of the first child = the chain's next node
+  int mir;    // mirrored-preorder index: level + n - skip
+  int rskip;  // mir + subtree size (the traversal record's skip)
+  double len; // bbox diagonal (bhtree.py:83)
+  double pad;
+};
+
+// Per point i, the nodes (i, s_i..e_i), one level per loop turn for the
+// whole block so that each level's writes are contiguous.  Node (i, l) has
+// BFS position lvl_off[l] + (level-l nodes started before i): each level is
+// contiguous and sorted by start, and the children of consecutive internal
+// nodes are consecutive one level down.  Internal nodes go to the per-level
+// list `in`; leaves are summarized here (bhtree.py:78-82) and write their
+// traversal records.  Preorder numbering from offset[]: x = offset[i] + l -
+// s_i, skip = offset[end].  The bbox (for the length, :83) is replayed
+// incrementally along the chain.  Same point->block mapping as k_levels.
+__global__ void __launch_bounds__(kThreads, 4) k_emit(const unsigned long long* __restrict__ keys,
+                                                   int64_t n, int L,
+                                                   const signed char* __restrict__ clev,
+                                                   const int* __restrict__ offset,
+                                                   const int* __restrict__ boff,
+                                                   const int* __restrict__ lvl_off,
+                                                   const int* __restrict__ ilvl_off,
+                                                   const double* __restrict__ box, int n_nodes,
+                                                   const double4* __restrict__ sp,
+                                                   InNode* __restrict__ in,
+                                                   double4* __restrict__ sums, TreeRecords r) {
+  __shared__ BlockRanks R;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const Chain c = chain_of(clev, i, n, L);
+  block_ranks(R, c, L);
+  if (c.s > c.e) return;
+  const unsigned long long k = keys[i];
+  const int base = offset[i];
+  double lo[3], hi[3];
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    lo[a] = box[a];
+    hi[a] = box[3 + a];
+  }
+  for (int l = 0; l <= c.e; l++) {
+    if (l > 0) bbox_step(k, l, L, lo, hi);
+    if (l < c.s) continue;
+    int64_t end;
+    if (l == 0) end = n;
+    else if (l > c.cn) end = i + 1;
+    else end = upper_bound_gallop(keys, i + 1, n, k | low_mask(3 * (L - l)));
+    const int x = base + (l - c.s);
+    const int skip = offset[end];
+    const int mir = l + n_nodes - skip;
+    const int rskip = mir + (skip - x);
+    double sq = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      const double ex = __dsub_rn(hi[a], lo[a]);
+      sq = __dadd_rn(sq, __dmul_rn(ex, ex));
+    }
+    const double len = __dsqrt_rn(sq);
+    const int pos = level_slot(R, 0, l, L, lvl_off, boff);
+    if (l < c.e) {
+      in[level_slot(R, 1, l, L, ilvl_off, boff)] =
+          InNode{pos, level_slot(R, 0, l + 1, L, lvl_off, boff), mir, rskip, len, 0.0};
+    } else {
+      double ms, mc[3];
+      leaf_sums(sp, (int)i, (int)(end - i), ms, mc);
+      sums[pos] = make_double4(ms, mc[0], mc[1], mc[2]);
+      write_records(r, mir, rskip, true, len, ms, mc);
+    }
+  }
+}
+
+// Level l of the bottom-up summary (bhtree.py:77-83), levels L-1..0 in
+// order, over the level's internal nodes: the children of internal node k are
+// the BFS range [fc_k, fc_{k+1}) one level down (the last one's ends with the
+// level), summed in slot order -- a fixed order, independent of scheduling.
+// The node's traversal records are written here too, at its mirrored index.
+__device__ __forceinline__ void sum_internal(int k, int e, int lend, const InNode* __restrict__ in,
+                                             double4* __restrict__ sums, const TreeRecords& r) {
+  const InNode nd = in[k];
+  const int cend = k + 1 < e ? in[k + 1].fc : lend;
+  double ms = 0.0, mc[3] = {0.0, 0.0, 0.0};
+  for (int ch = nd.fc; ch < cend; ch++) {
+    const double4 v = sums[ch];
+    ms = __dadd_rn(ms, v.x);
+    mc[0] = __dadd_rn(mc[0], v.y);
+    mc[1] = __dadd_rn(mc[1], v.z);
+    mc[2] = __dadd_rn(mc[2], v.w);
+  }
+  sums[nd.pos] = make_double4(ms, mc[0], mc[1], mc[2]);
+  write_records(r, nd.mir, nd.rskip, false, nd.len, ms, mc);
+}
+
+// one large level over the whole grid
+__global__ void __launch_bounds__(256) k_sum_level(int l, const int* __restrict__ lvl_off,
+                                                   const int* __restrict__ ilvl_off,
+                                                   const InNode* __restrict__ in,
+                                                   double4* __restrict__ sums, TreeRecords r) {
+  const int b = ilvl_off[l], e = ilvl_off[l + 1], lend = lvl_off[l + 2];
+  for (int k = b + blockIdx.x * blockDim.x + threadIdx.x; k < e; k += gridDim.x * blockDim.x)
+    sum_internal(k, e, lend, in, sums, r);
+}
+
+// consecutive small levels l_hi..l_lo (descending) in one block
+__global__ void __launch_bounds__(1024) k_sum_levels_small(int l_hi, int l_lo,
+                                                           const int* __restrict__ lvl_off,
+                                                           const int* __restrict__ ilvl_off,
+                                                           const InNode* __restrict__ in,
+                                                           double4* __restrict__ sums,
+                                                           TreeRecords r) {
+  for (int l = l_hi; l >= l_lo; l--) {
+    const int b = ilvl_off[l], e = ilvl_off[l + 1], lend = lvl_off[l + 2];
+    for (int k = b + threadIdx.x; k < e; k += blockDim.x) sum_internal(k, e, lend, in, sums, r);
+    __syncthreads();  // level l complete before its parents
+  }
+}
+
+// first p in [0, to) with keys[p] >= bound, galloping backwards from `to`
+__device__ __forceinline__ int64_t lower_bound_gallop(const unsigned long long* keys, int64_t to,
+                                                      unsigned long long bound) {
+  int64_t lo = 0, hi = to, step = 1;
+  while (true) {
+    const int64_t j = hi - step;
+    if (j < 0) break;
+    if (keys[j] < bound) {
+      lo = j + 1;
+      break;
+    }
+    hi = j;
+    step <<= 1;
+  }
   while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
+    const int64_t mid = (lo + hi) >> 1;
     if (keys[mid] >= bound) hi = mid; else lo = mid + 1;
   }
   return lo;
 }
 
-__global__ void k_emit(const unsigned long long* __restrict__ keys, int64_t n, int L,
-                       const signed char* __restrict__ clev, const int* __restrict__ offset,
-                       const double* __restrict__ box, TreeNodesView t) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int ci = clev[i], cn = clev[i + 1];
-  const int s = ci + 1;
-  if (s > L) return;  // exact duplicate of the previous key: no new node
-  const int e = max(s, min(L, cn + 1));
-  const int base = offset[i];
+// The reference's preorder arrays (bhtree.py:14-45), re-derived per chain
+// node exactly as k_emit does; each node registers itself in its parent's
+// child slot (parent: the chain's previous node, or found by a backwards
+// search for the start of the parent's key prefix).  children must be -1
+// filled.  Export only, not on the registration path.
+__global__ void __launch_bounds__(kThreads) k_export(const unsigned long long* __restrict__ keys,
+                                                     int64_t n, int L,
+                                                     const signed char* __restrict__ clev,
+                                                     const int* __restrict__ offset,
+                                                     const int* __restrict__ boff,
+                                                     const int* __restrict__ lvl_off,
+                                                     const double* __restrict__ box,
+                                                     const double4* __restrict__ sums,
+                                                     long long* children, double* com,
+                                                     double* mass, double* length,
+                                                     long long* occupancy, long long* depth,
+                                                     double* bmin, double* bmax) {
+  __shared__ BlockRanks R;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const Chain c = chain_of(clev, i, n, L);
+  block_ranks(R, c, L);
+  if (c.s > c.e) return;
   const unsigned long long k = keys[i];
-  for (int l = s; l <= e; l++) {
-    const int node = base + (l - s);
+  const int base = offset[i];
+  double lo[3], hi[3];
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    lo[a] = box[a];
+    hi[a] = box[3 + a];
+  }
+  for (int l = 0; l <= c.e; l++) {
+    if (l > 0) bbox_step(k, l, L, lo, hi);
+    if (l < c.s) continue;
     int64_t end;
     if (l == 0) end = n;
-    else if (l > cn) end = i + 1;
-    else end = upper_bound_key(keys, i + 1, n, k | low_mask(3 * (L - l)));
-    const int occ = (int)(end - i);
-    t.level[node] = (signed char)l;
-    t.start[node] = (int)i;
-    t.occ[node] = occ;
-    t.skip[node] = offset[end];
-    int parent = -1;
-    if (l > s) {
-      parent = node - 1;
-    } else if (l > 0) {
-      const unsigned long long pre = k & ~low_mask(3 * (L - l + 1));
-      const int64_t p = lower_bound_key(keys, 0, i, pre);
-      parent = offset[p] + (l - 1 - ((int)clev[p] + 1));
+    else if (l > c.cn) end = i + 1;
+    else end = upper_bound_gallop(keys, i + 1, n, k | low_mask(3 * (L - l)));
+    const int64_t x = base + (l - c.s);
+    const double4 v = sums[level_slot(R, 0, l, L, lvl_off, boff)];
+    if (mass) mass[x] = v.x;
+    if (com) {
+      com[x * 3] = __ddiv_rn(v.y, v.x);
+      com[x * 3 + 1] = __ddiv_rn(v.z, v.x);
+      com[x * 3 + 2] = __ddiv_rn(v.w, v.x);
     }
-    t.parent[node] = parent;
-    if (parent >= 0) {
-      const unsigned slot = (unsigned)(k >> (3 * (L - l))) & 7u;
-      t.children[(int64_t)parent * 8 + slot] = node;
-      atomicOr(&t.childmask[parent], 1u << slot);
+    if (occupancy) occupancy[x] = end - i;
+    if (depth) depth[x] = l;
+    if (length) {
+      double sq = 0.0;
+      for (int a = 0; a < 3; a++) {
+        const double ex = __dsub_rn(hi[a], lo[a]);
+        sq = __dadd_rn(sq, __dmul_rn(ex, ex));
+      }
+      length[x] = __dsqrt_rn(sq);
     }
-    double lo[3], hi[3];
-    node_bbox(k, l, L, box, lo, hi);
-    double sq = 0.0;
-#pragma unroll
     for (int a = 0; a < 3; a++) {
-      double ex = __dsub_rn(hi[a], lo[a]);
-      sq = __dadd_rn(sq, __dmul_rn(ex, ex));
+      if (bmin) bmin[x * 3 + a] = lo[a];
+      if (bmax) bmax[x * 3 + a] = hi[a];
     }
-    t.length[node] = __dsqrt_rn(sq);
-  }
-}
-
-// numpy's pairwise 1-D sum for n <= 128 (loops_utils.h.src); leaves hold one
-// point except at the depth cap, where this makes the leaf mass bit-exact.
-__device__ double pairwise_mass(const int* __restrict__ idx, int64_t lo, int64_t cnt,
-                                const double* __restrict__ m) {
-  if (cnt < 8) {
-    double r = 0.0;
-    for (int64_t i = 0; i < cnt; i++) r = __dadd_rn(r, m[idx[lo + i]]);
-    return r;
-  } else if (cnt <= 128) {
-    double r[8];
-    int64_t i;
-    for (int j = 0; j < 8; j++) r[j] = m[idx[lo + j]];
-    for (i = 8; i < cnt - (cnt % 8); i += 8)
-      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], m[idx[lo + i + j]]);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < cnt; i++) res = __dadd_rn(res, m[idx[lo + i]]);
-    return res;
-  }
-  int64_t n2 = cnt / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(pairwise_mass(idx, lo, n2, m), pairwise_mass(idx, lo + n2, cnt - n2, m));
-}
-
-// Leaves sum their points in the reference's order (bhtree.py:78-82); every
-// internal node is reduced by the last of its children to finish (children in
-// slot order), so the result does not depend on scheduling.
-__global__ void k_summarize(TreeNodesView t, int64_t n_nodes, int L, const int* __restrict__ idx,
-                            const double* __restrict__ pts, const double* __restrict__ masses) {
-  int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x >= n_nodes) return;
-  const int occ = t.occ[x];
-  if (!(occ == 1 || t.level[x] == L)) return;
-  const int start = t.start[x];
-  double ms = pairwise_mass(idx, start, occ, masses);
-  double mc[3] = {0.0, 0.0, 0.0};
-  for (int j = 0; j < occ; j++) {
-    const int p = idx[start + j];
-    const double w = masses[p];
-#pragma unroll
-    for (int k = 0; k < 3; k++) mc[k] = __dadd_rn(mc[k], __dmul_rn(pts[(int64_t)p * 3 + k], w));
-  }
-  t.mass[x] = ms;
-#pragma unroll
-  for (int k = 0; k < 3; k++) {
-    t.mc[x * 3 + k] = mc[k];
-    t.com[x * 3 + k] = __ddiv_rn(mc[k], ms);
-  }
-  int node = (int)x;
-  while (true) {
-    const int par = t.parent[node];
-    if (par < 0) break;
-    __threadfence();
-    const int nk = __popc(t.childmask[par]);
-    if (atomicAdd(&t.arrive[par], 1) != nk - 1) break;
-    __threadfence();
-    double s = 0.0, c[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int slot = 0; slot < 8; slot++) {
-      const int ch = __ldcg(&t.children[(int64_t)par * 8 + slot]);
-      if (ch < 0) continue;
-      s = __dadd_rn(s, __ldcg(&t.mass[ch]));
-#pragma unroll
-      for (int k = 0; k < 3; k++) c[k] = __dadd_rn(c[k], __ldcg(&t.mc[(int64_t)ch * 3 + k]));
-    }
-    t.mass[par] = s;
-#pragma unroll
-    for (int k = 0; k < 3; k++) {
-      t.mc[(int64_t)par * 3 + k] = c[k];
-      t.com[(int64_t)par * 3 + k] = __ddiv_rn(c[k], s);
-    }
-    node = par;
-  }
-}
-
-// Ascending preorder X -> mirrored preorder: mirror(X) = level + n - skip(X)
-// (ancestors, then every larger-slot sibling subtree of X and its ancestors).
-__global__ void k_records(TreeNodesView t, int64_t n_nodes, int L, TreeRecords r) {
-  int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x >= n_nodes) return;
-  const int lev = t.level[x];
-  const int skip = t.skip[x];
-  const int mir = lev + (int)n_nodes - skip;
-  const int size = skip - (int)x;
-  const bool leaf = t.occ[x] == 1 || lev == L;
-  const double cx = t.com[x * 3], cy = t.com[x * 3 + 1], cz = t.com[x * 3 + 2];
-  const double ms = t.mass[x];
-  const double len = t.length[x];
-  const double l2 = __dmul_rn(len, len);
-  r.a64[mir] = make_double4(cx, cy, cz, ms);
-  r.b64[mir] = NodeB64{leaf ? -INFINITY : l2, (long long)(mir + size)};
-  r.a32[mir] = make_float4((float)cx, (float)cy, (float)cz, (float)ms);
-  r.b32[mir] = NodeB32{leaf ? -INFINITY : (float)l2, mir + size};
-}
-
-__global__ void k_export(TreeNodesView t, int64_t n_nodes, int L, const double* __restrict__ box,
-                         const unsigned long long* __restrict__ keys, long long* children,
-                         double* com, double* mass, double* length, long long* occupancy,
-                         long long* depth, double* bmin, double* bmax) {
-  int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x >= n_nodes) return;
-  if (children)
-    for (int s = 0; s < 8; s++) children[x * 8 + s] = t.children[x * 8 + s];
-  if (com)
-    for (int k = 0; k < 3; k++) com[x * 3 + k] = t.com[x * 3 + k];
-  if (mass) mass[x] = t.mass[x];
-  if (length) length[x] = t.length[x];
-  if (occupancy) occupancy[x] = t.occ[x];
-  if (depth) depth[x] = t.level[x];
-  if (bmin || bmax) {
-    double lo[3], hi[3];
-    node_bbox(keys[t.start[x]], t.level[x], L, box, lo, hi);
-    for (int k = 0; k < 3; k++) {
-      if (bmin) bmin[x * 3 + k] = lo[k];
-      if (bmax) bmax[x * 3 + k] = hi[k];
+    if (children && l > 0) {
+      int64_t parent;
+      if (l > c.s) {
+        parent = x - 1;
+      } else {
+        const int64_t p = lower_bound_gallop(keys, i, k & ~low_mask(3 * (L - l + 1)));
+        parent = offset[p] + (l - 1 - ((int)clev[p] + 1));
+      }
+      const unsigned slot = (unsigned)(k >> (3 * (L - l))) & 7u;
+      children[parent * 8 + slot] = x;
     }
   }
 }
@@ -350,16 +646,18 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   T.masses = masses_dev;
   const int nb = (int)std::min<int64_t>(blocks_for(n), 4 * 148);
   FGA_CUDA_TRY(T.scratch.reserve(sizeof(double) * 6 * (nb + 1)));
-  FGA_CUDA_TRY(T.box.reserve(sizeof(double) * 6));
+  FGA_CUDA_TRY(T.box.reserve(sizeof(double) * 10));
   k_bbox_partial<<<nb, kThreads, 0, st>>>(pts_dev, n, T.scratch.as<double>());
-  k_bbox_final<<<1, 32, 0, st>>>(T.scratch.as<double>(), nb, T.box.as<double>());
+  k_bbox_final<<<1, 256, 0, st>>>(T.scratch.as<double>(), nb, L, T.box.as<double>());
 
   FGA_CUDA_TRY(T.keys_in.reserve(sizeof(unsigned long long) * n));
   FGA_CUDA_TRY(T.keys.reserve(sizeof(unsigned long long) * n));
   FGA_CUDA_TRY(T.idx_in.reserve(sizeof(int) * n));
   FGA_CUDA_TRY(T.idx.reserve(sizeof(int) * n));
-  k_keys<<<blocks_for(n), kThreads, 0, st>>>(pts_dev, n, T.box.as<double>(), L,
-                                             T.keys_in.as<unsigned long long>(), T.idx_in.as<int>());
+  FGA_CUDA_TRY(T.packed.reserve(sizeof(double4) * n));
+  k_keys<<<blocks_for(n), kThreads, 0, st>>>(pts_dev, masses_dev, n, T.box.as<double>(), L,
+                                             T.keys_in.as<unsigned long long>(), T.idx_in.as<int>(),
+                                             T.packed.as<double4>());
   size_t tmp_bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, T.keys_in.as<unsigned long long>(),
                                   T.keys.as<unsigned long long>(), T.idx_in.as<int>(),
@@ -371,19 +669,33 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
       T.cub_tmp.p, tmp_bytes, T.keys_in.as<unsigned long long>(), T.keys.as<unsigned long long>(),
       T.idx_in.as<int>(), T.idx.as<int>(), (int)n, 0, 3 * L, st));
 
+  FGA_CUDA_TRY(T.sp.reserve(sizeof(double4) * n));
+  k_gather_sorted<<<blocks_for(n), kThreads, 0, st>>>(T.packed.as<double4>(), T.idx.as<int>(), n,
+                                                      T.sp.as<double4>());
   FGA_CUDA_TRY(T.clev.reserve(n + 1));
   FGA_CUDA_TRY(T.count.reserve(sizeof(int) * (n + 1)));
   FGA_CUDA_TRY(T.offset.reserve(sizeof(int) * (n + 1)));
-  k_levels<<<blocks_for(n + 1), kThreads, 0, st>>>(T.keys.as<unsigned long long>(), n, L,
-                                                   T.clev.as<signed char>(), T.count.as<int>());
+  const int nbl = blocks_for(n + 1);
+  FGA_CUDA_TRY(T.bcount.reserve(sizeof(int) * (int64_t)2 * (L + 1) * nbl));
+  FGA_CUDA_TRY(T.lvl.reserve(sizeof(int) * kLvlInts));
+  int* row_total = T.lvl.as<int>();
+  int* lvl_off = row_total + 2 * (kMaxLevels + 1);
+  int* ilvl_off = lvl_off + (kMaxLevels + 3);
+  k_levels<<<nbl, kThreads, 0, st>>>(T.keys.as<unsigned long long>(), n, L,
+                                     T.clev.as<signed char>(), T.count.as<int>(),
+                                     T.bcount.as<int>());
+  k_level_scan<<<2 * (L + 1), 1024, 0, st>>>(T.bcount.as<int>(), nbl, row_total);
+  k_level_offsets<<<1, 32, 0, st>>>(row_total, L, lvl_off, ilvl_off);
   scan_bytes = T.cub_tmp.bytes;
   FGA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(T.cub_tmp.p, scan_bytes, T.count.as<int>(),
                                              T.offset.as<int>(), (int)(n + 1), st));
-  // node count and root box to the host (one sync per build)
+  // node count, per-level counts and root box to the host (one sync per build)
   int nn = 0;
   double box[6];
+  int lvl_host[kLvlInts];
   FGA_CUDA_TRY(cudaMemcpyAsync(&nn, T.offset.as<int>() + n, sizeof(int), cudaMemcpyDeviceToHost, st));
   FGA_CUDA_TRY(cudaMemcpyAsync(box, T.box.p, sizeof(box), cudaMemcpyDeviceToHost, st));
+  FGA_CUDA_TRY(cudaMemcpyAsync(lvl_host, T.lvl.p, sizeof(lvl_host), cudaMemcpyDeviceToHost, st));
   FGA_CUDA_TRY(cudaStreamSynchronize(st));
   T.n_nodes = nn;
   T.cmag = 0.0;
@@ -391,33 +703,35 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   for (int k = 0; k < 6; k++) T.box_host[k] = box[k];
 
   const int64_t nn64 = nn;
-  FGA_CUDA_TRY(T.level.reserve(nn64));
-  FGA_CUDA_TRY(T.start.reserve(sizeof(int) * nn64));
-  FGA_CUDA_TRY(T.occ.reserve(sizeof(int) * nn64));
-  FGA_CUDA_TRY(T.skip.reserve(sizeof(int) * nn64));
-  FGA_CUDA_TRY(T.parent.reserve(sizeof(int) * nn64));
-  FGA_CUDA_TRY(T.childmask.reserve(sizeof(unsigned) * nn64));
-  FGA_CUDA_TRY(T.arrive.reserve(sizeof(int) * nn64));
-  FGA_CUDA_TRY(T.children.reserve(sizeof(int) * 8 * nn64));
-  FGA_CUDA_TRY(T.mass.reserve(sizeof(double) * nn64));
-  FGA_CUDA_TRY(T.mc.reserve(sizeof(double) * 3 * nn64));
-  FGA_CUDA_TRY(T.com.reserve(sizeof(double) * 3 * nn64));
-  FGA_CUDA_TRY(T.length.reserve(sizeof(double) * nn64));
+  FGA_CUDA_TRY(T.inodes.reserve(sizeof(InNode) * nn64));
+  FGA_CUDA_TRY(T.sums.reserve(sizeof(double4) * nn64));
   FGA_CUDA_TRY(T.a32.reserve(sizeof(float4) * nn64));
   FGA_CUDA_TRY(T.b32.reserve(sizeof(NodeB32) * nn64));
   FGA_CUDA_TRY(T.a64.reserve(sizeof(double4) * nn64));
   FGA_CUDA_TRY(T.b64.reserve(sizeof(NodeB64) * nn64));
-  FGA_CUDA_TRY(cudaMemsetAsync(T.children.p, 0xff, sizeof(int) * 8 * nn64, st));
-  FGA_CUDA_TRY(cudaMemsetAsync(T.childmask.p, 0, sizeof(unsigned) * nn64, st));
-  FGA_CUDA_TRY(cudaMemsetAsync(T.arrive.p, 0, sizeof(int) * nn64, st));
 
-  TreeNodesView v = T.view();
-  k_emit<<<blocks_for(n), kThreads, 0, st>>>(T.keys.as<unsigned long long>(), n, L,
-                                             T.clev.as<signed char>(), T.offset.as<int>(),
-                                             T.box.as<double>(), v);
-  k_summarize<<<blocks_for(nn64), kThreads, 0, st>>>(v, nn64, L, T.idx.as<int>(), pts_dev,
-                                                     masses_dev);
-  k_records<<<blocks_for(nn64), kThreads, 0, st>>>(v, nn64, L, T.records());
+  k_emit<<<nbl, kThreads, 0, st>>>(T.keys.as<unsigned long long>(), n, L, T.clev.as<signed char>(),
+                                   T.offset.as<int>(), T.bcount.as<int>(), lvl_off, ilvl_off,
+                                   T.box.as<double>(), nn, T.sp.as<double4>(),
+                                   T.inodes.as<InNode>(), T.sums.as<double4>(), T.records());
+  // levels L-1..0 bottom-up (level L holds leaves only): a level with many
+  // internal nodes gets its own grid; runs of small levels share one block
+  const int* internal = lvl_host + (L + 1);  // row totals, internal nodes per level
+  constexpr int kSmall = 8192;
+  for (int l = L - 1; l >= 0;) {
+    if (internal[l] > kSmall) {
+      const int grid = (int)std::min<int64_t>(blocks_for(internal[l]), 148 * 8);
+      k_sum_level<<<grid, 256, 0, st>>>(l, lvl_off, ilvl_off, T.inodes.as<InNode>(),
+                                        T.sums.as<double4>(), T.records());
+      l--;
+      continue;
+    }
+    int lo = l;
+    while (lo - 1 >= 0 && internal[lo - 1] <= kSmall) lo--;
+    k_sum_levels_small<<<1, 1024, 0, st>>>(l, lo, lvl_off, ilvl_off, T.inodes.as<InNode>(),
+                                           T.sums.as<double4>(), T.records());
+    l = lo - 1;
+  }
   FGA_CUDA_TRY(cudaGetLastError());
   T.exportable = true;
   return FGA_OK;
@@ -443,9 +757,14 @@ int tree_export_host(TreeDev& T, cudaStream_t st, int64_t* children, double* com
   long long* d_depth = (long long*)p; p += sizeof(long long) * nn;
   double* d_bmin = (double*)p; p += sizeof(double) * 3 * nn;
   double* d_bmax = (double*)p;
-  k_export<<<blocks_for(nn), kThreads, 0, st>>>(T.view(), nn, T.L, T.box.as<double>(),
-                                                T.keys.as<unsigned long long>(), d_children, d_com,
-                                                d_mass, d_len, d_occ, d_depth, d_bmin, d_bmax);
+  if (children) FGA_CUDA_TRY(cudaMemsetAsync(d_children, 0xff, sizeof(long long) * 8 * nn, st));
+  const int* lvl_off = T.lvl.as<int>() + 2 * (kMaxLevels + 1);
+  k_export<<<blocks_for(T.n_points + 1), kThreads, 0, st>>>(
+      T.keys.as<unsigned long long>(), T.n_points, T.L, T.clev.as<signed char>(),
+      T.offset.as<int>(), T.bcount.as<int>(), lvl_off, T.box.as<double>(), T.sums.as<double4>(),
+      children ? d_children : nullptr, com ? d_com : nullptr, mass ? d_mass : nullptr,
+      length ? d_len : nullptr, occupancy ? d_occ : nullptr, depth ? d_depth : nullptr,
+      bmin ? d_bmin : nullptr, bmax ? d_bmax : nullptr);
   FGA_CUDA_TRY(cudaGetLastError());
 #define CP(dst, src, cnt)                                                                 \
   if (dst) FGA_CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(double) * (cnt), cudaMemcpyDeviceToHost, st));

@@ -64,6 +64,14 @@ class Session:
         self.n_nodes = int(nn.value)
         self.shard_count = shard_count
         self.dim = 3 if device_inputs is not None else x.dim
+        self.n, self.m = int(n_x), int(n_y)
+
+    def masses(self):
+        """(mx, my): the rescaled mass fields in input order (fga_session_masses)."""
+        mx = np.empty(self.n)
+        my = np.empty(self.m)
+        N.check(N.lib().fga_session_masses(self.ctx.handle, N.ptr(mx), N.ptr(my)))
+        return mx, my
 
     # ---- stream-ordered pieces
     def bind_sums(self, dev_ptr: int):

@@ -32,8 +32,29 @@ def test_tree_build_matches_reference(golden, fga, case):
     assert np.abs(t.com - g[f"{case}/com"]).max() <= 1e-12 * max(scale, 1.0)
 
 
+def _split_plane_points(rng, n, lo, hi, L=20):
+    """Points exactly on fp64 split planes of the midpoint recursion
+    (bhtree.py:89-104) and one ulp either side, inside a box pinned by two
+    corner points: the cases where the device's fast key path must defer to
+    the exact replay."""
+    pts = np.empty((n, 3))
+    for k in range(3):
+        for i in range(n):
+            a, b = lo, hi
+            c = a
+            for _ in range(int(rng.integers(1, L + 1))):
+                c = a + (b - a) / 2.0
+                if rng.integers(0, 2):
+                    a = c
+                else:
+                    b = c
+            pts[i, k] = [c, np.nextafter(c, -np.inf), np.nextafter(c, np.inf)][rng.integers(0, 3)]
+    return np.vstack([[lo] * 3, [hi] * 3, np.clip(pts, lo, hi)])
+
+
 @pytest.mark.parametrize("kind,n", [("uniform", 50000), ("blob", 200000), ("grid", 27000),
-                                    ("dups", 20000)])
+                                    ("dups", 20000), ("planes_dyadic", 6000),
+                                    ("planes_odd", 6000)])
 def test_tree_build_matches_oracle_large(orc, fga, kind, n):
     from paper_2009_14005_b200 import bhtree
     rng = np.random.default_rng(n)
@@ -46,6 +67,10 @@ def test_tree_build_matches_oracle_large(orc, fga, kind, n):
         g = np.arange(30, dtype=np.float64) * 0.25
         p = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
         p = p[rng.permutation(len(p))]
+    elif kind == "planes_dyadic":
+        p = _split_plane_points(rng, n, -3.0, 5.0)
+    elif kind == "planes_odd":
+        p = _split_plane_points(rng, n, -1.3, 2.9000000000000004)
     else:
         base = rng.uniform(-1, 1, size=(n // 50, 3))
         p = base[rng.integers(0, len(base), size=n)]
