@@ -30,7 +30,7 @@ struct TreeDev {
   DevBuf box, scratch, keys_in, keys, idx_in, idx, clev, count, offset, cub_tmp;
   // build intermediates: packed (x,y,z,m) in input order, sorted copy, level
   // counts/offsets, internal-node lists, BFS-ordered node sums (mass, m*p)
-  DevBuf packed, sp, bcount, lvl, inodes, sums;
+  DevBuf keys32_in, keys32, packed, sp, bcount, lvl, inodes, sums, sizep;
   DevBuf a32, b32, a64, b64;
   DevBuf export_buf;
 
@@ -39,8 +39,8 @@ struct TreeDev {
   }
   void release() {
     DevBuf* all[] = {&box,    &scratch, &keys_in, &keys,   &idx_in, &idx, &clev,
-                     &count,  &offset,  &cub_tmp, &packed, &sp,     &bcount, &lvl,
-                     &inodes, &sums,    &a32,     &b32,    &a64,    &b64,  &export_buf};
+                     &count,  &offset,  &cub_tmp, &keys32_in, &keys32, &packed, &sp,     &bcount, &lvl,
+                     &inodes, &sums,    &sizep,    &a32,    &b32,    &a64,    &b64,  &export_buf};
     for (DevBuf* b : all) b->release();
     n_nodes = 0;
     exportable = false;

@@ -38,6 +38,12 @@
 #include "fga_device.cuh"
 #include "../../include/fga.h"
 
+#define TRY_RC(x)                 \
+  do {                            \
+    const int rc_ = (x);          \
+    if (rc_ != FGA_OK) return rc_; \
+  } while (0)
+
 namespace fga {
 
 namespace {
@@ -140,8 +146,43 @@ __device__ __forceinline__ bool fast_axis(double x, double lo0, double scale, do
   return true;
 }
 
+__device__ __forceinline__ unsigned long long point_key(const double p[3],
+                                                        const double* __restrict__ box, int L) {
+  const double guard = box[9];
+  unsigned long long q[3];
+  bool fast = true;
+#pragma unroll
+  for (int k = 0; k < 3; k++)
+    fast = fast_axis(p[k], box[k], box[6 + k], guard * box[6 + k], L, q[k]) && fast;
+  if (fast) return (spread3(q[0]) << 2) | (spread3(q[1]) << 1) | spread3(q[2]);
+  double lo[3], hi[3];
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    lo[k] = box[k];
+    hi[k] = box[3 + k];
+  }
+  unsigned long long key = 0;
+  for (int l = 0; l < L; l++) {
+    unsigned digit = 0;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      const double c = __dadd_rn(lo[k], __dmul_rn(__dsub_rn(hi[k], lo[k]), 0.5));
+      const bool up = p[k] >= c;
+      digit = (digit << 1) | (up ? 1u : 0u);
+      if (up) lo[k] = c; else hi[k] = c;
+    }
+    key = (key << 3) | digit;
+  }
+  return key;
+}
+
+// Key of every point in input order, the sort's index payload and the packed
+// (x, y, z, m) record.  The sort runs on the top 32 key bits (keys32, 4 radix
+// passes instead of 8); keys64 (the full key) is written only for the
+// fallback full sort.
 __global__ void k_keys(const double* __restrict__ pts, const double* __restrict__ masses, int64_t n,
-                       const double* __restrict__ box, int L, unsigned long long* __restrict__ keys,
+                       const double* __restrict__ box, int L, int shift,
+                       unsigned* __restrict__ keys32, unsigned long long* __restrict__ keys64,
                        int* __restrict__ idx, double4* __restrict__ packed) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -149,36 +190,61 @@ __global__ void k_keys(const double* __restrict__ pts, const double* __restrict_
 #pragma unroll
   for (int k = 0; k < 3; k++) p[k] = pts[i * 3 + k];
   packed[i] = make_double4(p[0], p[1], p[2], masses[i]);  // one 32 B record per point
-  const double guard = box[9];
-  unsigned long long q[3];
-  bool fast = true;
-#pragma unroll
-  for (int k = 0; k < 3; k++)
-    fast = fast_axis(p[k], box[k], box[6 + k], guard * box[6 + k], L, q[k]) && fast;
-  unsigned long long key = 0;
-  if (fast) {
-    key = (spread3(q[0]) << 2) | (spread3(q[1]) << 1) | spread3(q[2]);
-  } else {
-    double lo[3], hi[3];
-#pragma unroll
-    for (int k = 0; k < 3; k++) {
-      lo[k] = box[k];
-      hi[k] = box[3 + k];
-    }
-    for (int l = 0; l < L; l++) {
-      unsigned digit = 0;
-#pragma unroll
-      for (int k = 0; k < 3; k++) {
-        double c = __dadd_rn(lo[k], __dmul_rn(__dsub_rn(hi[k], lo[k]), 0.5));
-        bool up = p[k] >= c;
-        digit = (digit << 1) | (up ? 1u : 0u);
-        if (up) lo[k] = c; else hi[k] = c;
-      }
-      key = (key << 3) | digit;
-    }
-  }
-  keys[i] = key;
+  const unsigned long long key = point_key(p, box, L);
+  if (keys64) keys64[i] = key;
+  else keys32[i] = (unsigned)(key >> shift);
   idx[i] = (int)i;
+}
+
+// Sorted copy of the points (one random gather of the packed records) and,
+// when the sort ran on the top key bits only, the full key recomputed from
+// the point (no second gather).
+__global__ void k_gather_sorted(const double4* __restrict__ packed, const int* __restrict__ idx,
+                                int64_t n, const double* __restrict__ box, int L,
+                                double4* __restrict__ sp, unsigned long long* __restrict__ keys) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 v = packed[idx[i]];
+  sp[i] = v;
+  if (keys) {
+    const double p[3] = {v.x, v.y, v.z};
+    keys[i] = point_key(p, box, L);
+  }
+}
+
+// After the (stable) sort on the top 32 bits: every run of equal top bits is
+// put in full-key order by one thread (stable insertion sort, so equal keys
+// keep index order as the reference's partition does).  Runs longer than
+// kRun set *overflow and the build falls back to the full 64-bit sort.
+constexpr int kRun = 64;
+__global__ void k_fixup_runs(const unsigned* __restrict__ hi, int64_t n,
+                             unsigned long long* __restrict__ key, int* __restrict__ idx,
+                             double4* __restrict__ sp, int* __restrict__ overflow) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned h = hi[i];
+  if ((i > 0 && hi[i - 1] == h) || i + 1 >= n || hi[i + 1] != h) return;  // not a run head
+  int len = 2;
+  while (i + len < n && hi[i + len] == h)
+    if (++len > kRun) {
+      atomicOr(overflow, 1);
+      return;
+    }
+  for (int a = 1; a < len; a++) {
+    const unsigned long long kk = key[i + a];
+    int b = a - 1;
+    if (key[i + b] <= kk) continue;
+    const int id = idx[i + a];
+    const double4 v = sp[i + a];
+    for (; b >= 0 && key[i + b] > kk; b--) {
+      key[i + b + 1] = key[i + b];
+      idx[i + b + 1] = idx[i + b];
+      sp[i + b + 1] = sp[i + b];
+    }
+    key[i + b + 1] = kk;
+    idx[i + b + 1] = id;
+    sp[i + b + 1] = v;
+  }
 }
 
 // Point i's chain of nodes: (i, l) for s <= l <= e, where s = c_i + 1 and
@@ -412,12 +478,12 @@ __device__ __forceinline__ int level_slot(const BlockRanks& R, int k, int l, int
 
 // Internal node of the level lists (one 32-byte record).
 struct InNode {
-  int pos;    // BFS position (sums[] index)
+  int pos;    // BFS position (sums[] / sizep[] index)
   int fc;     // BFS position of the first child = the chain's next node
-  int mir;    // mirrored-preorder index: level + n - skip
-  int rskip;  // mir + subtree size (the traversal record's skip)
+  int x;      // preorder index (bhtree.py:77)
+  int pad;
   double len; // bbox diagonal (bhtree.py:83)
-  double pad;
+  double pad2;
 };
 
 // Per point i, the nodes (i, s_i..e_i), one level per loop turn for the
@@ -425,11 +491,12 @@ struct InNode {
 // BFS position lvl_off[l] + (level-l nodes started before i): each level is
 // contiguous and sorted by start, and the children of consecutive internal
 // nodes are consecutive one level down.  Internal nodes go to the per-level
-// list `in`; leaves are summarized here (bhtree.py:78-82) and write their
+// list `in` (their subtree sizes are found bottom-up);
+// the chain's leaf (i, e) is summarized here (bhtree.py:78-82) and writes its
 // traversal records.  Preorder numbering from offset[]: x = offset[i] + l -
-// s_i, skip = offset[end].  The bbox (for the length, :83) is replayed
+// s_i, skip = x + subtree size.  The bbox (for the length, :83) is replayed
 // incrementally along the chain.  Same point->block mapping as k_levels.
-__global__ void __launch_bounds__(kThreads, 4) k_emit(const unsigned long long* __restrict__ keys,
+__global__ void __launch_bounds__(kThreads) k_emit(const unsigned long long* __restrict__ keys,
                                                    int64_t n, int L,
                                                    const signed char* __restrict__ clev,
                                                    const int* __restrict__ offset,
@@ -439,7 +506,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_emit(const unsigned long long* 
                                                    const double* __restrict__ box, int n_nodes,
                                                    const double4* __restrict__ sp,
                                                    InNode* __restrict__ in,
-                                                   double4* __restrict__ sums, TreeRecords r) {
+                                                   double4* __restrict__ sums,
+                                                   int* __restrict__ sizep, TreeRecords r) {
   __shared__ BlockRanks R;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const Chain c = chain_of(clev, i, n, L);
@@ -453,35 +521,35 @@ __global__ void __launch_bounds__(kThreads, 4) k_emit(const unsigned long long* 
     lo[a] = box[a];
     hi[a] = box[3 + a];
   }
+  double len = 0.0;
+  int pos = 0;
   for (int l = 0; l <= c.e; l++) {
     if (l > 0) bbox_step(k, l, L, lo, hi);
     if (l < c.s) continue;
-    int64_t end;
-    if (l == 0) end = n;
-    else if (l > c.cn) end = i + 1;
-    else end = upper_bound_gallop(keys, i + 1, n, k | low_mask(3 * (L - l)));
-    const int x = base + (l - c.s);
-    const int skip = offset[end];
-    const int mir = l + n_nodes - skip;
-    const int rskip = mir + (skip - x);
     double sq = 0.0;
 #pragma unroll
     for (int a = 0; a < 3; a++) {
       const double ex = __dsub_rn(hi[a], lo[a]);
       sq = __dadd_rn(sq, __dmul_rn(ex, ex));
     }
-    const double len = __dsqrt_rn(sq);
-    const int pos = level_slot(R, 0, l, L, lvl_off, boff);
-    if (l < c.e) {
+    len = __dsqrt_rn(sq);
+    pos = level_slot(R, 0, l, L, lvl_off, boff);
+    if (l < c.e)
       in[level_slot(R, 1, l, L, ilvl_off, boff)] =
-          InNode{pos, level_slot(R, 0, l + 1, L, lvl_off, boff), mir, rskip, len, 0.0};
-    } else {
-      double ms, mc[3];
-      leaf_sums(sp, (int)i, (int)(end - i), ms, mc);
-      sums[pos] = make_double4(ms, mc[0], mc[1], mc[2]);
-      write_records(r, mir, rskip, true, len, ms, mc);
-    }
+          InNode{pos, level_slot(R, 0, l + 1, L, lvl_off, boff), base + (l - c.s), 0, len, 0.0};
   }
+  // the chain's leaf (i, e): point i alone, or a depth-cap cell of duplicates
+  int64_t end;
+  if (c.e > c.cn) end = i + 1;
+  else if (c.e == 0) end = n;
+  else end = upper_bound_gallop(keys, i + 1, n, k | low_mask(3 * (L - c.e)));
+  double ms, mc[3];
+  leaf_sums(sp, (int)i, (int)(end - i), ms, mc);
+  sums[pos] = make_double4(ms, mc[0], mc[1], mc[2]);
+  sizep[pos] = 1;
+  const int x = base + (c.e - c.s);
+  const int mir = c.e + n_nodes - (x + 1);  // skip = x + 1
+  write_records(r, mir, mir + 1, true, len, ms, mc);
 }
 
 // Level l of the bottom-up summary (bhtree.py:77-83), levels L-1..0 in
@@ -489,42 +557,53 @@ __global__ void __launch_bounds__(kThreads, 4) k_emit(const unsigned long long* 
 // the BFS range [fc_k, fc_{k+1}) one level down (the last one's ends with the
 // level), summed in slot order -- a fixed order, independent of scheduling.
 // The node's traversal records are written here too, at its mirrored index.
-__device__ __forceinline__ void sum_internal(int k, int e, int lend, const InNode* __restrict__ in,
-                                             double4* __restrict__ sums, const TreeRecords& r) {
+// subtree size = 1 + the children's (preorder skip = x + size)
+__device__ __forceinline__ void sum_internal(int l, int k, int e, int lend, int n_nodes,
+                                             const InNode* __restrict__ in,
+                                             double4* __restrict__ sums, int* __restrict__ sizep,
+                                             const TreeRecords& r) {
   const InNode nd = in[k];
   const int cend = k + 1 < e ? in[k + 1].fc : lend;
   double ms = 0.0, mc[3] = {0.0, 0.0, 0.0};
+  int size = 1;
   for (int ch = nd.fc; ch < cend; ch++) {
     const double4 v = sums[ch];
     ms = __dadd_rn(ms, v.x);
     mc[0] = __dadd_rn(mc[0], v.y);
     mc[1] = __dadd_rn(mc[1], v.z);
     mc[2] = __dadd_rn(mc[2], v.w);
+    size += sizep[ch];
   }
   sums[nd.pos] = make_double4(ms, mc[0], mc[1], mc[2]);
-  write_records(r, nd.mir, nd.rskip, false, nd.len, ms, mc);
+  sizep[nd.pos] = size;
+  const int mir = l + n_nodes - (nd.x + size);
+  write_records(r, mir, mir + size, false, nd.len, ms, mc);
 }
 
 // one large level over the whole grid
 __global__ void __launch_bounds__(256) k_sum_level(int l, const int* __restrict__ lvl_off,
-                                                   const int* __restrict__ ilvl_off,
+                                                   const int* __restrict__ ilvl_off, int n_nodes,
                                                    const InNode* __restrict__ in,
-                                                   double4* __restrict__ sums, TreeRecords r) {
+                                                   double4* __restrict__ sums,
+                                                   int* __restrict__ sizep, TreeRecords r) {
   const int b = ilvl_off[l], e = ilvl_off[l + 1], lend = lvl_off[l + 2];
   for (int k = b + blockIdx.x * blockDim.x + threadIdx.x; k < e; k += gridDim.x * blockDim.x)
-    sum_internal(k, e, lend, in, sums, r);
+    sum_internal(l, k, e, lend, n_nodes, in, sums, sizep, r);
 }
 
 // consecutive small levels l_hi..l_lo (descending) in one block
 __global__ void __launch_bounds__(1024) k_sum_levels_small(int l_hi, int l_lo,
                                                            const int* __restrict__ lvl_off,
                                                            const int* __restrict__ ilvl_off,
+                                                           int n_nodes,
                                                            const InNode* __restrict__ in,
                                                            double4* __restrict__ sums,
+                                                           int* __restrict__ sizep,
                                                            TreeRecords r) {
   for (int l = l_hi; l >= l_lo; l--) {
     const int b = ilvl_off[l], e = ilvl_off[l + 1], lend = lvl_off[l + 2];
-    for (int k = b + threadIdx.x; k < e; k += blockDim.x) sum_internal(k, e, lend, in, sums, r);
+    for (int k = b + threadIdx.x; k < e; k += blockDim.x)
+      sum_internal(l, k, e, lend, n_nodes, in, sums, sizep, r);
     __syncthreads();  // level l complete before its parents
   }
 }
@@ -650,53 +729,91 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   k_bbox_partial<<<nb, kThreads, 0, st>>>(pts_dev, n, T.scratch.as<double>());
   k_bbox_final<<<1, 256, 0, st>>>(T.scratch.as<double>(), nb, L, T.box.as<double>());
 
-  FGA_CUDA_TRY(T.keys_in.reserve(sizeof(unsigned long long) * n));
+  const int shift = std::max(0, 3 * L - 32);
+  const int sort_bits = std::min(32, 3 * L);
   FGA_CUDA_TRY(T.keys.reserve(sizeof(unsigned long long) * n));
+  FGA_CUDA_TRY(T.keys32_in.reserve(sizeof(unsigned) * n));
+  FGA_CUDA_TRY(T.keys32.reserve(sizeof(unsigned) * n));
   FGA_CUDA_TRY(T.idx_in.reserve(sizeof(int) * n));
   FGA_CUDA_TRY(T.idx.reserve(sizeof(int) * n));
   FGA_CUDA_TRY(T.packed.reserve(sizeof(double4) * n));
-  k_keys<<<blocks_for(n), kThreads, 0, st>>>(pts_dev, masses_dev, n, T.box.as<double>(), L,
-                                             T.keys_in.as<unsigned long long>(), T.idx_in.as<int>(),
-                                             T.packed.as<double4>());
-  size_t tmp_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, T.keys_in.as<unsigned long long>(),
-                                  T.keys.as<unsigned long long>(), T.idx_in.as<int>(),
-                                  T.idx.as<int>(), (int)n, 0, 3 * L, st);
-  size_t scan_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (int*)nullptr, (int*)nullptr, (int)(n + 1), st);
-  FGA_CUDA_TRY(T.cub_tmp.reserve(std::max(tmp_bytes, scan_bytes)));
-  FGA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(
-      T.cub_tmp.p, tmp_bytes, T.keys_in.as<unsigned long long>(), T.keys.as<unsigned long long>(),
-      T.idx_in.as<int>(), T.idx.as<int>(), (int)n, 0, 3 * L, st));
-
   FGA_CUDA_TRY(T.sp.reserve(sizeof(double4) * n));
-  k_gather_sorted<<<blocks_for(n), kThreads, 0, st>>>(T.packed.as<double4>(), T.idx.as<int>(), n,
-                                                      T.sp.as<double4>());
   FGA_CUDA_TRY(T.clev.reserve(n + 1));
   FGA_CUDA_TRY(T.count.reserve(sizeof(int) * (n + 1)));
   FGA_CUDA_TRY(T.offset.reserve(sizeof(int) * (n + 1)));
   const int nbl = blocks_for(n + 1);
   FGA_CUDA_TRY(T.bcount.reserve(sizeof(int) * (int64_t)2 * (L + 1) * nbl));
-  FGA_CUDA_TRY(T.lvl.reserve(sizeof(int) * kLvlInts));
+  FGA_CUDA_TRY(T.lvl.reserve(sizeof(int) * (kLvlInts + 1)));
   int* row_total = T.lvl.as<int>();
   int* lvl_off = row_total + 2 * (kMaxLevels + 1);
   int* ilvl_off = lvl_off + (kMaxLevels + 3);
-  k_levels<<<nbl, kThreads, 0, st>>>(T.keys.as<unsigned long long>(), n, L,
-                                     T.clev.as<signed char>(), T.count.as<int>(),
-                                     T.bcount.as<int>());
-  k_level_scan<<<2 * (L + 1), 1024, 0, st>>>(T.bcount.as<int>(), nbl, row_total);
-  k_level_offsets<<<1, 32, 0, st>>>(row_total, L, lvl_off, ilvl_off);
-  scan_bytes = T.cub_tmp.bytes;
-  FGA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(T.cub_tmp.p, scan_bytes, T.count.as<int>(),
-                                             T.offset.as<int>(), (int)(n + 1), st));
-  // node count, per-level counts and root box to the host (one sync per build)
+  int* overflow = T.lvl.as<int>() + kLvlInts;
+  {
+    size_t b32 = 0, b64 = 0, bscan = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b32, T.keys32_in.as<unsigned>(), T.keys32.as<unsigned>(),
+                                    T.idx_in.as<int>(), T.idx.as<int>(), (int)n, 0, sort_bits, st);
+    cub::DeviceRadixSort::SortPairs(nullptr, b64, (const unsigned long long*)nullptr,
+                                    (unsigned long long*)nullptr, T.idx_in.as<int>(),
+                                    T.idx.as<int>(), (int)n, 0, 3 * L, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, bscan, (int*)nullptr, (int*)nullptr, (int)(n + 1), st);
+    FGA_CUDA_TRY(T.cub_tmp.reserve(std::max(std::max(b32, b64), bscan)));
+  }
+  FGA_CUDA_TRY(cudaMemsetAsync(overflow, 0, sizeof(int), st));
+  k_keys<<<blocks_for(n), kThreads, 0, st>>>(pts_dev, masses_dev, n, T.box.as<double>(), L, shift,
+                                             T.keys32_in.as<unsigned>(), nullptr, T.idx_in.as<int>(),
+                                             T.packed.as<double4>());
+  size_t tmp_bytes = T.cub_tmp.bytes;
+  FGA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(T.cub_tmp.p, tmp_bytes, T.keys32_in.as<unsigned>(),
+                                               T.keys32.as<unsigned>(), T.idx_in.as<int>(),
+                                               T.idx.as<int>(), (int)n, 0, sort_bits, st));
+  k_gather_sorted<<<blocks_for(n), kThreads, 0, st>>>(T.packed.as<double4>(), T.idx.as<int>(), n,
+                                                      T.box.as<double>(), L, T.sp.as<double4>(),
+                                                      T.keys.as<unsigned long long>());
+  if (shift > 0)
+    k_fixup_runs<<<blocks_for(n), kThreads, 0, st>>>(T.keys32.as<unsigned>(), n,
+                                                     T.keys.as<unsigned long long>(),
+                                                     T.idx.as<int>(), T.sp.as<double4>(), overflow);
+  // levels, per-level block counts, preorder offsets (rerun after a fallback)
+  auto levels = [&]() -> int {
+    k_levels<<<nbl, kThreads, 0, st>>>(T.keys.as<unsigned long long>(), n, L,
+                                       T.clev.as<signed char>(), T.count.as<int>(),
+                                       T.bcount.as<int>());
+    k_level_scan<<<2 * (L + 1), 1024, 0, st>>>(T.bcount.as<int>(), nbl, row_total);
+    k_level_offsets<<<1, 32, 0, st>>>(row_total, L, lvl_off, ilvl_off);
+    size_t sb = T.cub_tmp.bytes;
+    FGA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(T.cub_tmp.p, sb, T.count.as<int>(),
+                                               T.offset.as<int>(), (int)(n + 1), st));
+    return FGA_OK;
+  };
+  TRY_RC(levels());
+  // node count, per-level counts, run overflow and root box to the host
+  // (one sync per build)
   int nn = 0;
   double box[6];
-  int lvl_host[kLvlInts];
-  FGA_CUDA_TRY(cudaMemcpyAsync(&nn, T.offset.as<int>() + n, sizeof(int), cudaMemcpyDeviceToHost, st));
-  FGA_CUDA_TRY(cudaMemcpyAsync(box, T.box.p, sizeof(box), cudaMemcpyDeviceToHost, st));
-  FGA_CUDA_TRY(cudaMemcpyAsync(lvl_host, T.lvl.p, sizeof(lvl_host), cudaMemcpyDeviceToHost, st));
-  FGA_CUDA_TRY(cudaStreamSynchronize(st));
+  int lvl_host[kLvlInts + 1];
+  auto fetch = [&]() -> int {
+    FGA_CUDA_TRY(cudaMemcpyAsync(&nn, T.offset.as<int>() + n, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FGA_CUDA_TRY(cudaMemcpyAsync(box, T.box.p, sizeof(box), cudaMemcpyDeviceToHost, st));
+    FGA_CUDA_TRY(cudaMemcpyAsync(lvl_host, T.lvl.p, sizeof(lvl_host), cudaMemcpyDeviceToHost, st));
+    FGA_CUDA_TRY(cudaStreamSynchronize(st));
+    return FGA_OK;
+  };
+  TRY_RC(fetch());
+  if (lvl_host[kLvlInts]) {  // a long run of equal top bits: full 64-bit sort
+    FGA_CUDA_TRY(T.keys_in.reserve(sizeof(unsigned long long) * n));
+    k_keys<<<blocks_for(n), kThreads, 0, st>>>(pts_dev, masses_dev, n, T.box.as<double>(), L, 0,
+                                               nullptr, T.keys_in.as<unsigned long long>(),
+                                               T.idx_in.as<int>(), T.packed.as<double4>());
+    tmp_bytes = T.cub_tmp.bytes;
+    FGA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(
+        T.cub_tmp.p, tmp_bytes, T.keys_in.as<unsigned long long>(), T.keys.as<unsigned long long>(),
+        T.idx_in.as<int>(), T.idx.as<int>(), (int)n, 0, 3 * L, st));
+    k_gather_sorted<<<blocks_for(n), kThreads, 0, st>>>(T.packed.as<double4>(), T.idx.as<int>(), n,
+                                                        T.box.as<double>(), L, T.sp.as<double4>(),
+                                                        nullptr);
+    TRY_RC(levels());
+    TRY_RC(fetch());
+  }
   T.n_nodes = nn;
   T.cmag = 0.0;
   for (int k = 0; k < 6; k++) T.cmag = std::max(T.cmag, std::fabs(box[k]));
@@ -705,6 +822,7 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   const int64_t nn64 = nn;
   FGA_CUDA_TRY(T.inodes.reserve(sizeof(InNode) * nn64));
   FGA_CUDA_TRY(T.sums.reserve(sizeof(double4) * nn64));
+  FGA_CUDA_TRY(T.sizep.reserve(sizeof(int) * nn64));
   FGA_CUDA_TRY(T.a32.reserve(sizeof(float4) * nn64));
   FGA_CUDA_TRY(T.b32.reserve(sizeof(NodeB32) * nn64));
   FGA_CUDA_TRY(T.a64.reserve(sizeof(double4) * nn64));
@@ -713,23 +831,24 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   k_emit<<<nbl, kThreads, 0, st>>>(T.keys.as<unsigned long long>(), n, L, T.clev.as<signed char>(),
                                    T.offset.as<int>(), T.bcount.as<int>(), lvl_off, ilvl_off,
                                    T.box.as<double>(), nn, T.sp.as<double4>(),
-                                   T.inodes.as<InNode>(), T.sums.as<double4>(), T.records());
+                                   T.inodes.as<InNode>(), T.sums.as<double4>(), T.sizep.as<int>(),
+                                   T.records());
   // levels L-1..0 bottom-up (level L holds leaves only): a level with many
   // internal nodes gets its own grid; runs of small levels share one block
   const int* internal = lvl_host + (L + 1);  // row totals, internal nodes per level
-  constexpr int kSmall = 8192;
+  constexpr int kSmall = 2048;
   for (int l = L - 1; l >= 0;) {
     if (internal[l] > kSmall) {
       const int grid = (int)std::min<int64_t>(blocks_for(internal[l]), 148 * 8);
-      k_sum_level<<<grid, 256, 0, st>>>(l, lvl_off, ilvl_off, T.inodes.as<InNode>(),
-                                        T.sums.as<double4>(), T.records());
+      k_sum_level<<<grid, 256, 0, st>>>(l, lvl_off, ilvl_off, nn, T.inodes.as<InNode>(),
+                                        T.sums.as<double4>(), T.sizep.as<int>(), T.records());
       l--;
       continue;
     }
     int lo = l;
     while (lo - 1 >= 0 && internal[lo - 1] <= kSmall) lo--;
-    k_sum_levels_small<<<1, 1024, 0, st>>>(l, lo, lvl_off, ilvl_off, T.inodes.as<InNode>(),
-                                           T.sums.as<double4>(), T.records());
+    k_sum_levels_small<<<1, 1024, 0, st>>>(l, lo, lvl_off, ilvl_off, nn, T.inodes.as<InNode>(),
+                                           T.sums.as<double4>(), T.sizep.as<int>(), T.records());
     l = lo - 1;
   }
   FGA_CUDA_TRY(cudaGetLastError());

@@ -54,7 +54,7 @@ def _split_plane_points(rng, n, lo, hi, L=20):
 
 @pytest.mark.parametrize("kind,n", [("uniform", 50000), ("blob", 200000), ("grid", 27000),
                                     ("dups", 20000), ("planes_dyadic", 6000),
-                                    ("planes_odd", 6000)])
+                                    ("planes_odd", 6000), ("dups200", 20000), ("dense", 30000)])
 def test_tree_build_matches_oracle_large(orc, fga, kind, n):
     from paper_2009_14005_b200 import bhtree
     rng = np.random.default_rng(n)
@@ -71,6 +71,13 @@ def test_tree_build_matches_oracle_large(orc, fga, kind, n):
         p = _split_plane_points(rng, n, -3.0, 5.0)
     elif kind == "planes_odd":
         p = _split_plane_points(rng, n, -1.3, 2.9000000000000004)
+    elif kind == "dups200":  # runs of > 64 equal keys: the full-sort fallback
+        base = rng.uniform(-1, 1, size=(n // 200, 3))
+        p = base[rng.integers(0, len(base), size=n)]
+    elif kind == "dense":  # clusters far below the top-32-bit cell size: run fix-ups
+        c = rng.uniform(-4, 4, size=(40, 3))
+        p = np.vstack([c, c[rng.integers(0, 40, size=n - 40)] +
+                       rng.normal(size=(n - 40, 3)) * 2e-4])
     else:
         base = rng.uniform(-1, 1, size=(n // 50, 3))
         p = base[rng.integers(0, len(base), size=n)]
