@@ -557,7 +557,10 @@ def run_batched(args, rank, world):
 def run_other_configs(args):
     """configs[1] (100k LiDAR-shaped pair) and configs[3] (200k partial
     overlap, 5% outliers, inhomogeneous density, kNN-16 masses): one full
-    register() each from host numpy, theta 0.5, G*sqrt(2000/N)."""
+    register() each from host numpy, theta 0.5.  G per scene from a sweep
+    (tools/sweep_c2.py, tools/sweep_c4.py): the 160 m x 16 m x 4.5 m street
+    scan flies apart for G >= 1 and converges for G = 0.2; the partial-overlap
+    pair diverges at G*sqrt(2000/N) = 6.67 and converges at G = 2."""
     import paper_2009_14005_b200 as fga
     from paper_2009_14005_b200 import synth
     out = {}
@@ -565,13 +568,13 @@ def run_other_configs(args):
     x = synth.lidar_scan(100_000, rng)
     gt = synth.random_rigid(rng, np.deg2rad(10), 1.0)
     y = synth.misalign(x, gt)
-    p = fga.default_params().replace(theta=0.5, G=66.7 * (2000.0 / len(x)) ** 0.5)
+    p = fga.default_params().replace(theta=0.5, G=0.2)
     fga.register(fga.PointCloud(x.points[:5000]), fga.PointCloud(y.points[:5000]), params=p)
     t0 = time.perf_counter()
     r = fga.register(x, y, params=p)
     wall = time.perf_counter() - t0
     out["c2_lidar_100k"] = {
-        "wall_s": wall, "iterations": r.iterations, "converged": r.converged,
+        "wall_s": wall, "iterations": r.iterations, "converged": r.converged, "G": p.G,
         "rotation_err_deg": fga.angular_deviation(gt.rotation, r.transform.rotation),
         "interactions_per_s_loop": float(r.interactions.sum()) / (r.timings_ms["loop"] / 1e3),
         "timings_ms": r.timings_ms}
@@ -579,7 +582,7 @@ def run_other_configs(args):
     x, y0 = synth.partial_overlap(200_000, rng)
     gt = synth.random_rigid(rng, np.deg2rad(60), 0.1)
     y = synth.misalign(y0, gt)
-    p = fga.default_params().replace(theta=0.5, G=66.7 * (2000.0 / len(x)) ** 0.5)
+    p = fga.default_params().replace(theta=0.5, G=2.0)
     o = fga.RegisterOptions(mass_field="knn", knn_k=16)
     from paper_2009_14005_b200 import masses
     masses.knn_masses(x, 16)
@@ -590,7 +593,8 @@ def run_other_configs(args):
     r = fga.register(x, y, params=p, options=o)
     wall = time.perf_counter() - t0
     out["c4_overlap_200k_knn16"] = {
-        "wall_s": wall, "iterations": r.iterations, "converged": r.converged,
+        "wall_s": wall, "iterations": r.iterations, "converged": r.converged, "G": p.G,
+        "rotation_err_deg": fga.angular_deviation(gt.rotation, r.transform.rotation),
         "knn16_masses_s_200k_host_api": knn_s,
         "interactions_per_s_loop": float(r.interactions.sum()) / (r.timings_ms["loop"] / 1e3),
         "timings_ms": r.timings_ms}

@@ -185,6 +185,16 @@ int fga_session_finish(fga_ctx* ctx, fga_result* out, double* deltas, double* tr
 int fga_session_set_gpe(fga_ctx* ctx, int which /*0 initial,1 final*/, double value);
 /* Number of template points owned by this shard and total tree nodes. */
 int fga_session_info(fga_ctx* ctx, int64_t* m_local, int64_t* n_nodes);
+/* Iteration state (checkpoint / resume, teacher-forced parity): template
+ * positions and velocities entering the next iteration, normalized frame,
+ * host (m,3) arrays in input order (a shard reads / writes its own rows
+ * only), the accumulated [R_acc | t_acc] (registration.py:137-138) and the
+ * number of completed iterations.  set_state resumes from such a state
+ * (pending step transform = identity). */
+int fga_session_get_state(fga_ctx* ctx, double* pos, double* vel, double* racc9, double* tacc3,
+                          int64_t* iter);
+int fga_session_set_state(fga_ctx* ctx, const double* pos, const double* vel, const double* racc9,
+                          const double* tacc3, int64_t iter);
 /* The session's rescaled mass fields (registration.py:85-87) in input order:
  * mx (n) for the reference, my (m) for the template; either may be NULL. */
 int fga_session_masses(fga_ctx* ctx, double* mx, double* my);

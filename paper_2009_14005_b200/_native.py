@@ -118,6 +118,8 @@ SIGNATURES = {
     "fga_session_poll": (_c_int, [_vp, ctypes.POINTER(_c_int), ctypes.POINTER(_i64)]),
     "fga_session_finish": (_c_int, [_vp, ctypes.POINTER(CResult), _vp, _vp, _vp, _vp, _vp]),
     "fga_session_set_gpe": (_c_int, [_vp, _c_int, _dbl]),
+    "fga_session_get_state": (_c_int, [_vp, _vp, _vp, _vp, _vp, ctypes.POINTER(_i64)]),
+    "fga_session_set_state": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64]),
     "fga_session_masses": (_c_int, [_vp, _vp, _vp]),
     "fga_session_info": (_c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "fga_tree_build": (_c_int, [_vp, _vp, _vp, _i64, _c_int, _c_int, ctypes.POINTER(_i64)]),

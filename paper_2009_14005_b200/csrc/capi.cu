@@ -659,6 +659,79 @@ int fga_session_info(fga_ctx* c, int64_t* m_local, int64_t* n_nodes) {
   return FGA_OK;
 }
 
+int fga_session_get_state(fga_ctx* c, double* pos, double* vel, double* racc9, double* tacc3,
+                          int64_t* iter) {
+  SESSION_TRY(c);
+  Session& S = c->S;
+  cudaStream_t s = c->stream;
+  if (pos || vel) {
+    FGA_CUDA_TRY(S.scratch.reserve(sizeof(double) * 6 * std::max<int64_t>(S.m, 1)));
+    double* dp = S.scratch.as<double>();
+    double* dv = dp + 3 * S.m;
+    if (pos) FGA_CUDA_TRY(cudaMemcpyAsync(dp, pos, sizeof(double) * 3 * S.m, cudaMemcpyHostToDevice, s));
+    if (vel) FGA_CUDA_TRY(cudaMemcpyAsync(dv, vel, sizeof(double) * 3 * S.m, cudaMemcpyHostToDevice, s));
+    launch_state_get(S.view(), S.st(), S.tidx.as<int>(), S.m_begin, dp, dv, s);
+    FGA_CUDA_TRY(cudaGetLastError());
+    if (pos) FGA_CUDA_TRY(cudaMemcpyAsync(pos, dp, sizeof(double) * 3 * S.m, cudaMemcpyDeviceToHost, s));
+    if (vel) FGA_CUDA_TRY(cudaMemcpyAsync(vel, dv, sizeof(double) * 3 * S.m, cudaMemcpyDeviceToHost, s));
+  }
+  IterState st;
+  FGA_CUDA_TRY(cudaMemcpyAsync(&st, S.st(), sizeof(st), cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  if (racc9)
+    for (int k = 0; k < 9; k++) racc9[k] = st.Racc[k];
+  if (tacc3)
+    for (int k = 0; k < 3; k++) tacc3[k] = st.tacc[k];
+  if (iter) *iter = st.iter;
+  return FGA_OK;
+}
+
+int fga_session_set_state(fga_ctx* c, const double* pos, const double* vel, const double* racc9,
+                          const double* tacc3, int64_t iter) {
+  SESSION_TRY(c);
+  Session& S = c->S;
+  cudaStream_t s = c->stream;
+  if (!pos || !vel || !racc9 || !tacc3) {
+    set_error("set_state: positions, velocities, R_acc and t_acc are required");
+    return FGA_ERR_INVALID;
+  }
+  if (iter < 0 || iter >= S.sp.max_iters) {
+    set_error("set_state: iteration outside [0, max_iters)");
+    return FGA_ERR_INVALID;
+  }
+  FGA_CUDA_TRY(S.scratch.reserve(sizeof(double) * 6 * std::max<int64_t>(S.m, 1)));
+  double* dp = S.scratch.as<double>();
+  double* dv = dp + 3 * S.m;
+  FGA_CUDA_TRY(cudaMemcpyAsync(dp, pos, sizeof(double) * 3 * S.m, cudaMemcpyHostToDevice, s));
+  FGA_CUDA_TRY(cudaMemcpyAsync(dv, vel, sizeof(double) * 3 * S.m, cudaMemcpyHostToDevice, s));
+  launch_state_set(S.view(), S.tidx.as<int>(), S.m_begin, dp, dv, s);
+  FGA_CUDA_TRY(cudaGetLastError());
+  IterState st;
+  FGA_CUDA_TRY(cudaMemcpyAsync(&st, S.st(), sizeof(st), cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  double mean[3] = {0.0, 0.0, 0.0};
+  for (int64_t i = 0; i < S.m; i++)
+    for (int k = 0; k < 3; k++) mean[k] += pos[i * 3 + k];
+  for (int k = 0; k < 9; k++) {
+    st.Rp[k] = (k % 4 == 0) ? 1.0 : 0.0;
+    st.Racc[k] = racc9[k];
+  }
+  for (int k = 0; k < 3; k++) {
+    st.tp[k] = 0.0;
+    st.tacc[k] = tacc3[k];
+    st.shift[k] = S.m > 0 ? mean[k] / (double)S.m : 0.0;
+  }
+  st.iter = iter;
+  st.done = 0;
+  st.converged = 0;
+  st.gpe_pending = 0;
+  FGA_CUDA_TRY(cudaMemcpyAsync(S.st(), &st, sizeof(st), cudaMemcpyHostToDevice, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  S.applied = false;
+  S.have_gpe_final = false;
+  return FGA_OK;
+}
+
 int fga_session_masses(fga_ctx* c, double* mx, double* my) {
   SESSION_TRY(c);
   Session& S = c->S;

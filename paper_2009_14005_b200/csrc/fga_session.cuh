@@ -58,6 +58,10 @@ void launch_update(const double* sums, IterState* st, const SimParams& sp, doubl
                    double* rec_traj, double* rec_gpe, long long* rec_inter, long long* rec_visits,
                    int has_gpe, cudaStream_t s);
 void launch_apply_pending(const TemplateView& tv, const IterState* st, cudaStream_t s);
+void launch_state_get(const TemplateView& tv, const IterState* st, const int* order, int64_t begin,
+                      double* pos, double* vel, cudaStream_t s);
+void launch_state_set(const TemplateView& tv, const int* order, int64_t begin, const double* pos,
+                      const double* vel, cudaStream_t s);
 void launch_state_init(IterState* st, const double* mean3, cudaStream_t s);
 void launch_solve_rigid(const double* y, const double* yd, int64_t m, int dim, double* out13,
                         cudaStream_t s);

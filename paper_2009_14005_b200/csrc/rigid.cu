@@ -133,6 +133,35 @@ __global__ void k_apply_pending(TemplateView tv, const IterState* __restrict__ s
   tv.pz[i] = ny[2];
 }
 
+// Session state in input order (checkpoint / teacher forcing): positions and
+// velocities with the pending step transform applied (the state entering the
+// next iteration), without changing the session.
+__global__ void k_state_get(TemplateView tv, const IterState* __restrict__ st,
+                            const int* __restrict__ order, int64_t begin, double* __restrict__ pos,
+                            double* __restrict__ vel) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= tv.m) return;
+  double y[3] = {tv.px[i], tv.py[i], tv.pz[i]}, v[3] = {tv.vx[i], tv.vy[i], tv.vz[i]};
+  apply_pending(st, y, v);
+  const int64_t src = order[begin + i];
+  for (int k = 0; k < 3; k++) {
+    pos[src * 3 + k] = y[k];
+    vel[src * 3 + k] = v[k];
+  }
+}
+__global__ void k_state_set(TemplateView tv, const int* __restrict__ order, int64_t begin,
+                            const double* __restrict__ pos, const double* __restrict__ vel) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= tv.m) return;
+  const int64_t src = order[begin + i];
+  tv.px[i] = pos[src * 3];
+  tv.py[i] = pos[src * 3 + 1];
+  tv.pz[i] = pos[src * 3 + 2];
+  tv.vx[i] = vel[src * 3];
+  tv.vy[i] = vel[src * 3 + 1];
+  tv.vz[i] = vel[src * 3 + 2];
+}
+
 __global__ void k_state_init(IterState* st, const double* __restrict__ mean3) {
   if (threadIdx.x != 0) return;
   for (int k = 0; k < 9; k++) {
@@ -232,6 +261,17 @@ void launch_update(const double* sums, IterState* st, const SimParams& sp, doubl
 void launch_apply_pending(const TemplateView& tv, const IterState* st, cudaStream_t s) {
   if (tv.m <= 0) return;
   k_apply_pending<<<(unsigned)((tv.m + 255) / 256), 256, 0, s>>>(tv, st);
+}
+
+void launch_state_get(const TemplateView& tv, const IterState* st, const int* order, int64_t begin,
+                      double* pos, double* vel, cudaStream_t s) {
+  if (tv.m <= 0) return;
+  k_state_get<<<(unsigned)((tv.m + 255) / 256), 256, 0, s>>>(tv, st, order, begin, pos, vel);
+}
+void launch_state_set(const TemplateView& tv, const int* order, int64_t begin, const double* pos,
+                      const double* vel, cudaStream_t s) {
+  if (tv.m <= 0) return;
+  k_state_set<<<(unsigned)((tv.m + 255) / 256), 256, 0, s>>>(tv, order, begin, pos, vel);
 }
 
 void launch_state_init(IterState* st, const double* mean3, cudaStream_t s) {

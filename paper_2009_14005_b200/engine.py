@@ -66,6 +66,29 @@ class Session:
         self.dim = 3 if device_inputs is not None else x.dim
         self.n, self.m = int(n_x), int(n_y)
 
+    def get_state(self):
+        """Iteration state entering the next iteration (normalized frame, input
+        order): dict(positions, velocities, R_acc, t_acc, iteration)."""
+        pos = np.zeros((self.m, 3))
+        vel = np.zeros((self.m, 3))
+        R = np.zeros(9)
+        t = np.zeros(3)
+        it = N._i64(0)
+        N.check(N.lib().fga_session_get_state(self.ctx.handle, N.ptr(pos), N.ptr(vel), N.ptr(R),
+                                              N.ptr(t), ctypes.byref(it)))
+        return {"positions": pos, "velocities": vel, "R_acc": R.reshape(3, 3), "t_acc": t,
+                "iteration": int(it.value)}
+
+    def set_state(self, positions, velocities, R_acc, t_acc, iteration: int):
+        """Resume from a state (see get_state); e.g. a checkpoint, or the
+        reference's own state for teacher-forced parity."""
+        pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(self.m, 3)
+        vel = np.ascontiguousarray(velocities, dtype=np.float64).reshape(self.m, 3)
+        R = np.ascontiguousarray(R_acc, dtype=np.float64).reshape(9)
+        t = np.ascontiguousarray(t_acc, dtype=np.float64).reshape(3)
+        N.check(N.lib().fga_session_set_state(self.ctx.handle, N.ptr(pos), N.ptr(vel), N.ptr(R),
+                                              N.ptr(t), int(iteration)))
+
     def masses(self):
         """(mx, my): the rescaled mass fields in input order (fga_session_masses)."""
         mx = np.empty(self.n)

@@ -1,0 +1,98 @@
+"""Teacher-forced iteration parity (SURVEY §8(c) protocol 2): the session is
+put into the reference's exact state entering iteration k (positions,
+velocities, [R_acc | t_acc], from the golden run of register() on config-1
+seed 0, tests/golden/make_golden.py) and runs ONE iteration; its
+[R_acc | t_acc] and the state it hands to iteration k+1 must equal the
+reference's (registration.py:130-154).  The same golden states pin the
+force operator on the session's tree (bhtree.bh_forces, bhtree.py:125-152).
+GPU only."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fga():
+    import paper_2009_14005_b200 as f
+    return f
+
+
+def _session(fga, g, precision):
+    from paper_2009_14005_b200.engine import Session
+    x, y = fga.PointCloud(g["s0/x"]), fga.PointCloud(g["s0/y"])
+    p = fga.default_params().replace(theta=0.5)
+    return Session(x, y, p, fga.RegisterOptions(compute_gpe=False, record_iterations=True,
+                                                precision=precision))
+
+
+def test_session_setup_state_matches_reference(golden, fga):
+    g = golden("register")
+    s = _session(fga, g, "fp64")
+    st = s.get_state()
+    mx, my = s.masses()
+    s.finish()
+    assert st["iteration"] == 0
+    assert np.array_equal(st["positions"], g["tf/yn"])  # normalized template, bit-exact
+    assert not st["velocities"].any()
+    assert np.array_equal(mx, g["tf/mass_x"]) and np.array_equal(my, g["tf/mass_y"])
+    assert np.array_equal(st["R_acc"], np.eye(3)) and not st["t_acc"].any()
+
+
+@pytest.mark.parametrize("it", [0, 1, 3])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_teacher_forced_iteration(golden, fga, it, precision):
+    g = golden("register")
+    s = _session(fga, g, precision)
+    prev = g[f"tf/it{it}/traj_prev"]
+    s.set_state(g[f"tf/it{it}/pos"], g[f"tf/it{it}/vel"], prev[:, :3], prev[:, 3], it)
+    s.iterate(1)
+    st = s.get_state()
+    res = s.finish()
+    assert res.iterations == it + 1
+    tol = 2e-6 if precision == "fp32" else 1e-11
+    assert np.abs(res.trajectory[it] - g[f"tf/it{it}/traj"]).max() < tol
+    if it == 0:  # the state entering iteration 1
+        assert np.abs(st["positions"] - g["tf/it1/pos"]).max() < tol
+        assert np.abs(st["velocities"] - g["tf/it1/vel"]).max() < tol * 10
+
+
+@pytest.mark.parametrize("it", [0, 1, 3])
+def test_teacher_forced_forces_on_session_tree(golden, fga, it):
+    """bh_forces on the GPU-built tree of the normalized reference cloud at
+    the reference's own iteration-k template state: fp64 bit-exact."""
+    from paper_2009_14005_b200 import bhtree
+    g = golden("register")
+    p = fga.default_params().replace(theta=0.5)
+    t = bhtree.build(fga.PointCloud(g["tf/xn"]), g["tf/mass_x"], p.max_depth)
+    f = bhtree.bh_forces(t, g[f"tf/it{it}/pos"], g["tf/mass_y"], p, precision="fp64")
+    assert np.array_equal(f, g[f"tf/it{it}/grav"])
+    f32 = bhtree.bh_forces(t, g[f"tf/it{it}/pos"], g["tf/mass_y"], p, precision="fp32")
+    scale = np.linalg.norm(g[f"tf/it{it}/grav"], axis=1).max()
+    assert np.abs(f32 - g[f"tf/it{it}/grav"]).max() <= 1e-5 * scale
+
+
+def test_checkpoint_resume_is_exact(fga):
+    """get_state after k iterations, set_state into a fresh session, continue:
+    the same trajectory as an uninterrupted run (fp64)."""
+    from paper_2009_14005_b200 import synth
+    from paper_2009_14005_b200.engine import Session
+    rng = synth.rng_from_seed(11)
+    x = synth.blob(3000, rng)
+    y = synth.misalign(x, synth.random_rigid(rng, np.deg2rad(40), 0.1))
+    p = fga.default_params().replace(theta=0.5, conv_tol=1e-300, max_iters=8)
+    o = fga.RegisterOptions(compute_gpe=False, record_iterations=True, precision="fp64")
+    a = Session(x, y, p, o)
+    a.iterate(8)
+    ra = a.finish()
+    b = Session(x, y, p, o)
+    b.iterate(3)
+    ck = b.get_state()
+    b.finish()
+    c = Session(x, y, p, o)
+    c.set_state(ck["positions"], ck["velocities"], ck["R_acc"], ck["t_acc"], ck["iteration"])
+    c.iterate(5)
+    rc = c.finish()
+    assert rc.iterations == 8
+    assert np.abs(rc.trajectory[3:] - ra.trajectory[3:]).max() < 1e-10

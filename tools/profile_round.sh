@@ -11,6 +11,16 @@ echo "launch list rc=$?"
 python tools/prof_kernels.py --mode all --iters 2 > $OUT/prof_all_plain.log 2>&1
 echo "prof plain rc=$?"
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_bh_iterate|k_direct_iterate32|k_gpe32|k_emit|k_summarize|k_keys|k_levels|k_records" \
-    -c 12 -o $OUT/full python tools/prof_kernels.py --mode all --iters 2 > $OUT/ncu_full.log 2>&1
+    -k regex:"k_bh_iterate|k_direct_iterate32|k_gpe32" \
+    -c 4 -o $OUT/full python tools/prof_kernels.py --mode all --iters 2 > $OUT/ncu_full.log 2>&1
 echo "ncu full rc=$?"
+python tools/prof_build.py 16000000 2 > $OUT/prof_build_plain.log 2>&1
+echo "build plain rc=$?"
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --cache-control none \
+    --clock-control none --csv --log-file $OUT/build16m.csv python tools/prof_build.py 16000000 2 \
+    > $OUT/ncu_build.log 2>&1
+echo "build launch list rc=$?"
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --cache-control none \
+    --clock-control none --csv --log-file $OUT/build1m.csv python tools/prof_build.py 1000000 2 \
+    > $OUT/ncu_build1m.log 2>&1
+echo "build 1M launch list rc=$?"
