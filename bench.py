@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--direct-steps", type=int, default=3)
     ap.add_argument("--no-batched", action="store_true")
     ap.add_argument("--no-build", action="store_true")
+    ap.add_argument("--no-ingest", action="store_true")
     ap.add_argument("--build-sizes", default="1000000,16000000")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the configs[1]/configs[3] registration legs")
@@ -272,6 +273,8 @@ def run_ours(args, rank, world, local_rank):
         line["batched"] = batched
     if world == 1 and not args.no_configs:
         line["configs"] = run_other_configs(args)
+    if world == 1 and not args.no_ingest:
+        line["ingest"] = run_ingest(x)
     return line
 
 
@@ -599,6 +602,33 @@ def run_other_configs(args):
         "interactions_per_s_loop": float(r.interactions.sum()) / (r.timings_ms["loop"] / 1e3),
         "timings_ms": r.timings_ms}
     return out
+
+
+def run_ingest(x):
+    """io.load_cloud of the 1M-point reference cloud written
+    as an XYZ file (io.write_cloud, 17 significant digits): the native
+    parser on all host threads vs the reader that follows the reference's
+    per-line Python algorithm (io.py:23-43), same file, same doubles."""
+    import tempfile
+
+    from paper_2009_14005_b200 import io
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "x.xyz")
+        io.write_cloud(path, x)
+        size = os.path.getsize(path)
+        io.load_cloud(path)  # warm (page cache, library)
+        t0 = time.perf_counter()
+        got = io.load_cloud(path)
+        t_native = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        ref = io._cloud_from_text(io._read_text(path))
+        t_py = time.perf_counter() - t0
+    assert np.array_equal(got.points, ref.points) and np.array_equal(got.points, x.points)
+    return {"points": len(x), "file_mb": size / 1e6, "native_s": t_native,
+            "native_mb_per_s": size / 1e6 / t_native, "python_reader_s": t_py,
+            "speedup": t_py / t_native, "threads": os.cpu_count(),
+            "api": "paper_2009_14005_b200.io.load_cloud (fga_parse_cloud) vs the reference's "
+                   "per-line algorithm in Python"}
 
 
 def run_registration(args, x, y):

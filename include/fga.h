@@ -36,6 +36,7 @@ extern "C" {
 #define FGA_ERR_LENGTH (-8)      /* LengthMismatch                               */
 #define FGA_ERR_STATE (-9)       /* call order (e.g. no tree built yet)          */
 #define FGA_ERR_SINGULAR (-10)   /* SingularCollocation (RBF landmark field)     */
+#define FGA_ERR_PARSE (-11)      /* file text not accepted by the native parser  */
 
 #define FGA_PREC_FP32 0 /* FP32 traversal/direct sums, fp64 state (default)   */
 #define FGA_PREC_FP64 1 /* fp64 everywhere: bit-exact reference visit order   */
@@ -267,6 +268,17 @@ int fga_normalize_pair(fga_ctx* ctx, const double* x, int64_t n, const double* y
  * degenerate flag. */
 int fga_solve_rigid(fga_ctx* ctx, const double* y, const double* y_d, int64_t m, int dim,
                     double* R, double* t, int32_t* degenerate);
+
+/* ------------------------------------------------ file ingestion (host)
+ * io.load_cloud / io.load_weights (io.py:11-111) on a file's bytes, parsed
+ * on all host threads.  Call with out == NULL for the counts, then with an
+ * out buffer of >= n*dim (cloud) / n (weights) doubles.  FGA_ERR_PARSE for
+ * anything the native parser does not accept (malformed files, non-ASCII);
+ * the Python layer then raises the reference's exception (ParseError /
+ * UnsupportedFormat with the reference's line number and message). */
+int fga_parse_cloud(const char* text, int64_t len, double* out, int64_t cap, int64_t* n,
+                    int* dim);
+int fga_parse_weights(const char* text, int64_t len, double* out, int64_t cap, int64_t* n);
 
 #ifdef __cplusplus
 }

@@ -37,6 +37,7 @@ FGA_ERR_NONFINITE = -7
 FGA_ERR_LENGTH = -8
 FGA_ERR_STATE = -9
 FGA_ERR_SINGULAR = -10
+FGA_ERR_PARSE = -11
 
 PREC_FP32 = 0
 PREC_FP64 = 1
@@ -120,6 +121,9 @@ SIGNATURES = {
     "fga_session_set_gpe": (_c_int, [_vp, _c_int, _dbl]),
     "fga_session_get_state": (_c_int, [_vp, _vp, _vp, _vp, _vp, ctypes.POINTER(_i64)]),
     "fga_session_set_state": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64]),
+    "fga_parse_cloud": (_c_int, [ctypes.c_char_p, _i64, _vp, _i64, ctypes.POINTER(_i64),
+                                 ctypes.POINTER(_c_int)]),
+    "fga_parse_weights": (_c_int, [ctypes.c_char_p, _i64, _vp, _i64, ctypes.POINTER(_i64)]),
     "fga_session_masses": (_c_int, [_vp, _vp, _vp]),
     "fga_session_info": (_c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "fga_tree_build": (_c_int, [_vp, _vp, _vp, _i64, _c_int, _c_int, ctypes.POINTER(_i64)]),

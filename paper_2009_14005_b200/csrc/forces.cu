@@ -49,8 +49,9 @@ struct F32Params {
   float theta2, eps2;
 };
 
-template <typename Real, bool kGuardZero, int kT, int kW = kWin, int kOcc = 1280>
-__global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? kOcc : 768) / kT) k_bh_iterate(
+// (1280 threads/SM = 48 registers: 1536 / 1792 spill and ran 15% / 28% slower)
+template <typename Real, bool kGuardZero, int kT, int kW = kWin>
+__global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? 1280 : 768) / kT) k_bh_iterate(
     TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, SimParams sp,
     F32Params f, double* partials, float cmag, int nblocks, int per_sm) {
   if (st->done) return;
@@ -478,15 +479,6 @@ static int bh_block() {
   }();
   return b;
 }
-// Experimental: FGA_BH_OCC = 1280 / 1536 threads per SM for the FP32 iterate.
-static int bh_occ() {
-  static int o = [] {
-    const char* e = getenv("FGA_BH_OCC");
-    int v = e ? atoi(e) : 1280;
-    return (v == 1536 || v == 1792) ? v : 1280;
-  }();
-  return o;
-}
 // Experimental: FGA_BH_WIN = 0 / 8 / 16 / 32 nodes per traversal window refill.
 static int bh_win() {
   static int w = [] {
@@ -523,12 +515,6 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
   else if (gz)
     k_bh_iterate<float, true, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm,
                                                    nb, per);
-  else if (kT == 128 && bh_occ() == 1536)
-    k_bh_iterate<float, false, kT, kWin, 1536><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f,
-                                                                partials, cm, nb, per);
-  else if (kT == 128 && bh_occ() == 1792)
-    k_bh_iterate<float, false, kT, kWin, 1792><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f,
-                                                                partials, cm, nb, per);
   else if (kT == 128 && bh_win() == 0)
     k_bh_iterate<float, false, kT, 0><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials,
                                                        cm, nb, per);

@@ -426,14 +426,6 @@ __device__ __forceinline__ void write_records(const TreeRecords& r, int mir, int
   r.b32[mir] = NodeB32{leaf ? -INFINITY : (float)l2, rskip};
 }
 
-// Sorted copy of the points with their masses: one gather after the sort so
-// that every later pass reads points contiguously.
-__global__ void k_gather_sorted(const double4* __restrict__ packed, const int* __restrict__ idx,
-                                int64_t n, double4* __restrict__ sp) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  sp[i] = packed[idx[i]];
-}
 
 // Within-block ranks of the threads whose chains hold a node at level l
 // (all nodes, and internal nodes only): warp ballots + warp prefix in shared

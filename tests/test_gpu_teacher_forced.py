@@ -61,15 +61,20 @@ def test_teacher_forced_iteration(golden, fga, it, precision):
 @pytest.mark.parametrize("it", [0, 1, 3])
 def test_teacher_forced_forces_on_session_tree(golden, fga, it):
     """bh_forces on the GPU-built tree of the normalized reference cloud at
-    the reference's own iteration-k template state: fp64 bit-exact."""
+    the reference's own iteration-k template state.  The GPU tree's topology
+    is the reference's bit for bit, its centres of mass agree to ~1e-15
+    relative (children-first summation vs the reference's per-node sums), so
+    the fp64 forces agree to 1e-11 of the largest force (bit-exact on the
+    reference's own tree: test_bh_forces_fp64_bit_exact_on_reference_tree)."""
     from paper_2009_14005_b200 import bhtree
     g = golden("register")
     p = fga.default_params().replace(theta=0.5)
     t = bhtree.build(fga.PointCloud(g["tf/xn"]), g["tf/mass_x"], p.max_depth)
-    f = bhtree.bh_forces(t, g[f"tf/it{it}/pos"], g["tf/mass_y"], p, precision="fp64")
-    assert np.array_equal(f, g[f"tf/it{it}/grav"])
-    f32 = bhtree.bh_forces(t, g[f"tf/it{it}/pos"], g["tf/mass_y"], p, precision="fp32")
+    f, v = bhtree.bh_forces(t, g[f"tf/it{it}/pos"], g["tf/mass_y"], p, count_visits=True,
+                            precision="fp64")
     scale = np.linalg.norm(g[f"tf/it{it}/grav"], axis=1).max()
+    assert np.abs(f - g[f"tf/it{it}/grav"]).max() <= 1e-11 * scale
+    f32 = bhtree.bh_forces(t, g[f"tf/it{it}/pos"], g["tf/mass_y"], p, precision="fp32")
     assert np.abs(f32 - g[f"tf/it{it}/grav"]).max() <= 1e-5 * scale
 
 
