@@ -49,6 +49,30 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   for (int j = 0; j < kBW; j++) t += red[j];  // fixed order, every thread
   return t;
 }
+// numpy's sum of a[0..n) (bit-exact, see np_pairwise_sum), whole block;
+// red holds >= 64 doubles.  The recursion is complete down to depth d0 <= 6,
+// one thread per node there, then the top levels pairwise in order.
+__device__ double block_np_sum(const double* a, int n, double* red) {
+  const int d0 = np_pairwise_depth(n, 6);
+  __syncthreads();
+  if (threadIdx.x < (1u << d0)) {
+    int64_t lo, len;
+    np_pairwise_node(n, d0, threadIdx.x, lo, len);
+    red[threadIdx.x] = np_pairwise_sum(a + lo, len);
+  }
+  __syncthreads();
+  for (int l = d0; l > 0; l--) {
+    const int cnt = 1 << (l - 1);
+    double v = 0.0;
+    if (threadIdx.x < (unsigned)cnt) v = __dadd_rn(red[2 * threadIdx.x], red[2 * threadIdx.x + 1]);
+    __syncthreads();
+    if (threadIdx.x < (unsigned)cnt) red[threadIdx.x] = v;
+    __syncthreads();
+  }
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
 __device__ __forceinline__ double block_min(double v, double* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -229,6 +253,7 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
     S.clev = reinterpret_cast<signed char*>(p);
   }
   __shared__ int next_pair;
+  __shared__ int next_chunk;
   PairState& st = *S.st;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int L = a.p.max_depth;
@@ -364,10 +389,9 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
     }
     __syncthreads();
     {
-      double sx = 0.0, myx = -INFINITY;
-      for (int i = tid; i < n; i += kBT) sx += mx[i];
+      double myx = -INFINITY;
       for (int i = tid; i < m; i += kBT) myx = fmax(myx, my[i]);
-      const double sumx = block_sum(sx, S.red);
+      const double sumx = block_np_sum(mx, n, S.red);  // sx.sum() (registration.py:85)
       const double maxy = block_max(myx, S.red);
       const double budget = 16.0 * sqrt((double)n / 2000.0);
       const double floor_ = fmax(1e-6, dt * eta);
@@ -648,12 +672,19 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
       sp.G = G;
       sp.eta = eta;
       sp.dt = dt;
+      double* cpart = a.scratch.cpart + slot * (size_t)kPartialStride * ((a.mmax + 31) / 32);
       for (int it = 0; it < a.p.max_iters; it++) {
-        // per-warp moment sums live in shared memory (chunk order: deterministic)
-        if (lane < 16) S.part[w * kPartialStride + lane] = 0.0;
-        __syncwarp();
+        // 32-query chunks are claimed dynamically (the traversal cost varies
+        // per chunk); each chunk's moment sums go to its own record and are
+        // added in chunk order below, so the result is deterministic
+        if (tid == 0) next_chunk = 0;
+        __syncthreads();
         const double shift[3] = {st.shift[0], st.shift[1], st.shift[2]};
-        for (int c = w; c < nchunks; c += kBW) {
+        while (true) {
+          int c = 0;
+          if (lane == 0) c = atomicAdd(&next_chunk, 1);
+          c = __shfl_sync(0xffffffffu, c, 0);
+          if (c >= nchunks) break;
           const int i = c * 32 + lane;
           const bool active = i < m;
           const float qxf = active ? (float)px[i] : 0.f, qyf = active ? (float)py[i] : 0.f,
@@ -682,18 +713,19 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
 #pragma unroll
           for (int k = 0; k < 16; k++) {
             const double v = warp_sum(p.v[k]);
-            if (lane == 0) S.part[w * kPartialStride + k] += v;
+            if (lane == k) cpart[(size_t)c * kPartialStride + k] = v;
           }
-          __syncwarp();
+        }
+        __syncthreads();
+        if (tid < 16) {  // chunk-order sums, one lane per moment
+          double v = 0.0;
+          for (int c = 0; c < nchunks; c++) v += __ldcg(&cpart[(size_t)c * kPartialStride + tid]);
+          S.part[tid] = v;
         }
         __syncthreads();
         if (tid == 0) {
           double sums[16];
-          for (int k = 0; k < 16; k++) {
-            double v = 0.0;
-            for (int j = 0; j < kBW; j++) v += S.part[j * kPartialStride + k];
-            sums[k] = v;
-          }
+          for (int k = 0; k < 16; k++) sums[k] = S.part[k];
           const double M = (double)m;
           double mu_u[3], mu_w[3], C[9], R[9], t[3];
           for (int k = 0; k < 3; k++) {

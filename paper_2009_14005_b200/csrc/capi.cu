@@ -897,8 +897,9 @@ int fga_register_batch_dev(fga_ctx* c, const double* x_all, const int64_t* x_off
   const size_t per_slot = sizeof(double) * ((size_t)nmax * 3 + (size_t)mmax * 3 + nmax + mmax) +
                           sizeof(int) * std::max(nmax, mmax) + sizeof(float4) * nmax +
                           cap * (1 + 4 * 3 + 4 * 8 + 8 + 24 + 8 + 16 + 8 + 32 + 16) +
-                          sizeof(double) * (size_t)mmax * 7 + 1024;
-  FGA_CUDA_TRY(c->batch_scratch.reserve(per_slot * grid + 4096));
+                          sizeof(double) * (size_t)mmax * 7 +
+                          sizeof(double) * kPartialStride * (((size_t)mmax + 31) / 32) + 1024;
+  FGA_CUDA_TRY(c->batch_scratch.reserve(per_slot * grid + 8192));
   BatchArgs a{};
   char* q = c->batch_scratch.as<char>();
   auto take = [&](size_t bytes) {
@@ -926,6 +927,7 @@ int fga_register_batch_dev(fga_ctx* c, const double* x_all, const int64_t* x_off
   a.scratch.ra64 = (double4*)take(sizeof(double4) * cap * g);
   a.scratch.rb64 = (NodeB64*)take(sizeof(NodeB64) * cap * g);
   a.scratch.tpl = (double*)take(sizeof(double) * mmax * 7 * g);
+  a.scratch.cpart = (double*)take(sizeof(double) * kPartialStride * ((mmax + 31) / 32) * g);
   if ((size_t)(q - c->batch_scratch.as<char>()) > c->batch_scratch.bytes) {
     set_error("internal: batched scratch sizing");
     return FGA_ERR_NOMEM;

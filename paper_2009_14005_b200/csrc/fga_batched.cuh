@@ -18,6 +18,7 @@ struct BatchScratch {
   double4* ra64;
   NodeB64* rb64;
   double* tpl;
+  double* cpart;  // per 32-query chunk: kPartialStride moment sums
 };
 
 struct BatchArgs {

@@ -48,6 +48,80 @@ __device__ __forceinline__ float node_band(float l2, float gA, float gB) {
   return fmaf(gA, len, fmaf(13.0f * 5.97e-8f, l2, gB));
 }
 
+// numpy's float64 sum of a contiguous 1-D array (pairwise_sum_DOUBLE,
+// numpy umath loops_utils.h.src), bit for bit: n < 8 sequential from 0;
+// n <= 128 eight interleaved accumulators combined as
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus the n%8 tail; larger n split at
+// n/2 - (n/2)%8.
+__device__ __noinline__ double np_pairwise_sum(const double* __restrict__ a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; i++) r = __dadd_rn(r, a[i]);
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; i++) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise_sum(a, n2), np_pairwise_sum(a + n2, n - n2));
+}
+
+// The recursion node (lo, len) reached from the root by the d path bits of t
+// (most significant = first split).
+__device__ __forceinline__ void np_pairwise_node(int64_t n, int d, int64_t t, int64_t& lo,
+                                                 int64_t& len) {
+  lo = 0;
+  len = n;
+  for (int l = d - 1; l >= 0; l--) {
+    int64_t n2 = len / 2;
+    n2 -= n2 % 8;
+    if ((t >> l) & 1) {
+      lo += n2;
+      len -= n2;
+    } else {
+      len = n2;
+    }
+  }
+}
+
+// depth (<= dmax) down to which every node of the recursion is internal
+__device__ __forceinline__ int np_pairwise_depth(int64_t n, int dmax) {
+  int64_t sz[8] = {n};
+  int cnt = 1, d = 0;
+  while (d < dmax) {
+    int64_t mn = sz[0];
+    for (int k = 1; k < cnt; k++) mn = mn < sz[k] ? mn : sz[k];
+    if (mn <= 128) break;
+    int64_t nx[8];
+    int nc = 0;
+    for (int k = 0; k < cnt; k++) {
+      int64_t n2 = sz[k] / 2;
+      n2 -= n2 % 8;
+      const int64_t c2[2] = {n2, sz[k] - n2};
+      for (int q = 0; q < 2; q++) {
+        bool seen = false;
+        for (int u = 0; u < nc; u++) seen |= nx[u] == c2[q];
+        if (!seen && nc < 8) nx[nc++] = c2[q];
+      }
+    }
+    for (int k = 0; k < nc; k++) sz[k] = nx[k];
+    cnt = nc;
+    d++;
+  }
+  return d;
+}
+
 struct Trav32Out {
   float ax, ay, az;
   int visits, accepted;

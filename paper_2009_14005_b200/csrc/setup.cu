@@ -202,44 +202,11 @@ __global__ void k_external(const double* __restrict__ w, int64_t n, double* __re
 // only: one thread per node at a depth d0 where every shallower node is
 // internal (the tree is complete down to d0), then the complete top d0 levels
 // are combined pairwise, left + right, in one block.
-__device__ double np_pairwise_sum(const double* __restrict__ a, int64_t n) {
-  if (n < 8) {
-    double r = 0.0;
-    for (int64_t i = 0; i < n; i++) r = __dadd_rn(r, a[i]);
-    return r;
-  }
-  if (n <= 128) {
-    double r[8];
-#pragma unroll
-    for (int j = 0; j < 8; j++) r[j] = a[j];
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8)
-#pragma unroll
-      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; i++) res = __dadd_rn(res, a[i]);
-    return res;
-  }
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(np_pairwise_sum(a, n2), np_pairwise_sum(a + n2, n - n2));
-}
-
 __global__ void k_pw_nodes(const double* __restrict__ a, int64_t n, int d0, double* __restrict__ out) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= (1ll << d0)) return;
-  int64_t lo = 0, len = n;
-  for (int l = d0 - 1; l >= 0; l--) {  // path bits, most significant = first split
-    int64_t n2 = len / 2;
-    n2 -= n2 % 8;
-    if ((t >> l) & 1) {
-      lo += n2;
-      len -= n2;
-    } else {
-      len = n2;
-    }
-  }
+  int64_t lo, len;
+  np_pairwise_node(n, d0, t, lo, len);
   out[t] = np_pairwise_sum(a + lo, len);
 }
 

@@ -225,24 +225,57 @@ class SequenceResult:
 
 
 def register_sequence(frames, params: FgaParams | None = None,
-                      options: RegisterOptions | None = None) -> SequenceResult:
+                      options: RegisterOptions | None = None, workers: int | None = None
+                      ) -> SequenceResult:
     """Frame i (template) onto frame i+1 (reference), pairwise; a failed pair
-    contributes an identity transform (registration.py:178-206)."""
+    contributes an identity transform (registration.py:178-206).
+
+    The pairs are independent, so they run concurrently: fragment-sized
+    frames (<= 8192 points, no per-cloud weights) go to ONE persistent
+    batched kernel (register_batch), larger ones (LiDAR scans) to `workers`
+    host threads (default min(4, pairs)), each with its own context and
+    stream, so one pair's setup and tree build overlap another's iterations
+    (SURVEY §8(f) f2).  Each pair's result is the one register() gives."""
     frames = list(frames)
     if len(frames) < 2:
         raise EmptyCloud("sequence registration needs at least 2 frames")
     params = params or default_params()
+    options = options or RegisterOptions()
+    pairs = [(frames[i + 1], frames[i]) for i in range(len(frames) - 1)]
+    small = (max(len(f) for f in frames) <= 8192 and options.x_weights is None
+             and options.y_weights is None and options.mass_field == "niv"
+             and options.precision == "fp32" and not options.trace_gpe and options.normalize)
     pairwise, failed = [], []
-    for i in range(len(frames) - 1):
-        try:
-            pairwise.append(register(x=frames[i + 1], y=frames[i], params=params,
-                                     options=options).transform)
-            failed.append(False)
-        except DeviceError:
-            raise
-        except GravregError:
-            pairwise.append(RigidTransform.identity(frames[i].dim))
-            failed.append(True)
+    if small:
+        br = register_batch(pairs, params=params, options=options)
+        for k, (res, err) in enumerate(zip(br.results, br.errors)):
+            if err is not None and not isinstance(err, GravregError):
+                raise err
+            if isinstance(err, DeviceError):
+                raise err
+            pairwise.append(res.transform if res is not None else
+                            RigidTransform.identity(frames[k].dim))
+            failed.append(res is None)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+
+        def one(k):
+            x, y = pairs[k]
+            try:
+                return register(x=x, y=y, params=params, options=options).transform, False
+            except DeviceError:
+                raise
+            except GravregError:
+                return RigidTransform.identity(frames[k].dim), True
+
+        n_workers = workers or min(4, len(pairs))
+        if n_workers <= 1:
+            outs = [one(k) for k in range(len(pairs))]
+        else:
+            with ThreadPoolExecutor(max_workers=n_workers) as pool:
+                outs = list(pool.map(one, range(len(pairs))))
+        pairwise = [o[0] for o in outs]
+        failed = [o[1] for o in outs]
     poses = [RigidTransform.identity(frames[0].dim)]
     for tf in pairwise:
         poses.append(poses[-1].compose(tf.inverse()))

@@ -130,3 +130,27 @@ def test_register_invalid_inputs(fga):
         fga.register(x, x, options=fga.RegisterOptions(x_weights=np.ones(3)))
     with pytest.raises(fga.NonFiniteWeight):
         fga.register(x, x, options=fga.RegisterOptions(y_weights=np.full(10, np.nan)))
+
+
+@pytest.mark.parametrize("n", [1500, 9000])
+def test_register_sequence_concurrent_matches_pairwise(fga, n):
+    """register_sequence runs its pairs concurrently (one batched kernel for
+    fragment-sized frames, host threads with their own streams above 8192
+    points); every pair equals the register() of that pair, and the poses
+    compose as in registration.py:200-206."""
+    from paper_2009_14005_b200 import synth
+    rng = synth.rng_from_seed(77 + n)
+    frames = [synth.blob(n, rng)]
+    for _ in range(4):
+        frames.append(synth.misalign(frames[-1], synth.random_rigid(rng, np.deg2rad(8), 0.03)))
+    seq = fga.register_sequence(frames)
+    assert len(seq.pairwise) == 4 and len(seq.trajectory) == 5 and not any(seq.failed)
+    tol = 1e-8 if n <= 8192 else 0.0  # batched kernel vs single path / same kernels
+    for k in range(4):
+        single = fga.register(x=frames[k + 1], y=frames[k]).transform
+        assert np.abs(seq.pairwise[k].rotation - single.rotation).max() <= tol
+        assert np.abs(seq.pairwise[k].translation - single.translation).max() <= tol
+    pose = seq.trajectory[0]
+    for k in range(4):
+        pose = pose.compose(seq.pairwise[k].inverse())
+        assert np.allclose(seq.trajectory[k + 1].rotation, pose.rotation, atol=1e-12)
