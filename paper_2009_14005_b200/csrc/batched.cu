@@ -637,12 +637,12 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
             __syncthreads();
             for (int j = tid; j < jmax; j += kBT) tile[j] = ref32[t0 + j];
             __syncthreads();
-            float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
-            gpe_tile32<true>(tile, jmax, qx, qy, qz, (float)eps, a0, a1);
-            acc[0] += (double)a0.x;
-            acc[1] += (double)a0.y;
-            acc[2] -= (double)a1.x;
-            acc[3] -= (double)a1.y;
+            float2 a2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            gpe_tile32<true, 2>(tile, jmax, qx, qy, qz, (float)eps, a2);
+            acc[0] += (double)a2[0].x;
+            acc[1] += (double)a2[0].y;
+            acc[2] -= (double)a2[1].x;
+            acc[3] -= (double)a2[1].y;
           }
           for (int k = 0; k < 4; k++)
             if (qi[k] < m) tot += pm[qi[k]] * acc[k];

@@ -471,50 +471,39 @@ __device__ __forceinline__ void direct_tile64(const double4* __restrict__ sm, in
   }
 }
 
-// K11 energy inner loop: 4 queries (2 packs) against jmax staged sources.
-// Pack 0 uses MUFU sqrt+rcp; pack 1 takes the reciprocal on the FMA pipe
-// (bit-trick seed + 3 Newton steps on w = -1/x, accumulating -m/x), which
-// balances the MUFU and FMA pipes.  a0 += sum m/(d+eps); a1 += -sum m/(d+eps).
-template <bool kNewton>
+// K11 energy inner loop: 2*NP queries (NP packs of 2) against jmax staged
+// sources.  Even packs use MUFU sqrt+rcp; odd packs take the reciprocal on
+// the FMA pipe (bit-trick seed + 3 Newton steps on w = -1/x, accumulating
+// -m/x), which balances the MUFU and FMA pipes.  acc[k] += +-sum m/(d+eps).
+template <bool kNewton, int NP>
 __device__ __forceinline__ void gpe_tile32(const float4* __restrict__ sm, int jmax,
-                                           const float2 (&qx)[2], const float2 (&qy)[2],
-                                           const float2 (&qz)[2], float eps, float2& a0,
-                                           float2& a1) {
+                                           const float2 (&qx)[NP], const float2 (&qy)[NP],
+                                           const float2 (&qz)[NP], float eps,
+                                           float2 (&acc)[NP]) {
   const float2 e2 = make_float2(eps, eps);
   const float2 two = make_float2(2.f, 2.f);
-#pragma unroll 4
+#pragma unroll 2
   for (int j = 0; j < jmax; j++) {
     const float4 s = sm[j];
-    {
-      const float2 dx = sub2s(s.x, qx[0]), dy = sub2s(s.y, qy[0]), dz = sub2s(s.z, qz[0]);
-      const float2 d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
-      float2 den;
-      den.x = sqrt_approx(d2.x);
-      den.y = sqrt_approx(d2.y);
-      den = add2(den, e2);
-      float2 r;
-      r.x = rcp_approx(den.x);
-      r.y = rcp_approx(den.y);
-      a0 = fma2s(s.w, r, a0);
-    }
-    {
-      const float2 dx = sub2s(s.x, qx[1]), dy = sub2s(s.y, qy[1]), dz = sub2s(s.z, qz[1]);
+#pragma unroll
+    for (int k = 0; k < NP; k++) {
+      const float2 dx = sub2s(s.x, qx[k]), dy = sub2s(s.y, qy[k]), dz = sub2s(s.z, qz[k]);
       const float2 d2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
       float2 den;
       den.x = sqrt_approx(d2.x);
       den.y = sqrt_approx(d2.y);
       den = add2(den, e2);
       float2 w;
-      if (kNewton) {
+      if (kNewton && (k & 1)) {
         w.x = __int_as_float(0xFEF311C3u - __float_as_uint(den.x));
         w.y = __int_as_float(0xFEF311C3u - __float_as_uint(den.y));
 #pragma unroll
         for (int it = 0; it < 3; it++) w = mul2(w, fma2(den, w, two));
       } else {
-        w.x = -rcp_approx(den.x);
-        w.y = -rcp_approx(den.y);
+        w.x = rcp_approx(den.x);
+        w.y = rcp_approx(den.y);
       }
-      a1 = fma2s(s.w, w, a1);
+      acc[k] = fma2s(s.w, w, acc[k]);
     }
   }
 }

@@ -137,7 +137,11 @@ __device__ __forceinline__ unsigned long long spread3(unsigned long long v) {
 
 __device__ __forceinline__ bool fast_axis(double x, double lo0, double scale, double gf, int L,
                                           unsigned long long& q) {
-  if (!(scale > 0.0)) return false;
+  if (!(scale > 0.0)) {  // flat axis (hi == lo, e.g. a 2-D cloud's z): every split is lo,
+    if (x != lo0) return false;  // x >= lo at every level -> all ones
+    q = (1ull << L) - 1ull;
+    return true;
+  }
   const double f = (x - lo0) * scale;
   const double fl = floor(f);
   const double fr = f - fl;
