@@ -25,6 +25,8 @@ from .errors import (
 )
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfga.so")
+# A/B experiments only: FGA_LIB_PATH points at an alternative in-tree build
+LIB_PATH = os.environ.get("FGA_LIB_PATH", LIB_PATH)
 
 FGA_OK = 0
 FGA_ERR_INVALID = -1

@@ -483,15 +483,6 @@ static int bh_block() {
   }();
   return b;
 }
-// Experimental: FGA_BH_WIN = 0 / 8 / 16 / 32 nodes per traversal window refill.
-static int bh_win() {
-  static int w = [] {
-    const char* e = getenv("FGA_BH_WIN");
-    int v = e ? atoi(e) : kWin;
-    return (v == 0 || v == 8 || v == 16 || v == 32) ? v : kWin;
-  }();
-  return w;
-}
 int64_t bh_iterate_warps(int64_t m) {
   const int t = bh_block();
   return (int64_t)grid_for(m, t) * (t / 32);
@@ -525,15 +516,6 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
   else if (gz)
     k_bh_iterate<float, true, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm,
                                                    nb, per);
-  else if (kT == 128 && bh_win() == 0)
-    k_bh_iterate<float, false, kT, 0><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials,
-                                                       cm, nb, per);
-  else if (kT == 128 && bh_win() == 8)
-    k_bh_iterate<float, false, kT, 8><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials,
-                                                       cm, nb, per);
-  else if (kT == 128 && bh_win() == 16)
-    k_bh_iterate<float, false, kT, 16><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials,
-                                                        cm, nb, per);
   else
     k_bh_iterate<float, false, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm,
                                                     nb, per);
