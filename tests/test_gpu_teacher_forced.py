@@ -101,3 +101,35 @@ def test_checkpoint_resume_is_exact(fga):
     rc = c.finish()
     assert rc.iterations == 8
     assert np.abs(rc.trajectory[3:] - ra.trajectory[3:]).max() < 1e-10
+
+
+@pytest.mark.parametrize("case", ["c2", "c4"])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_teacher_forced_config_shapes(golden, fga, case, precision):
+    """configs[1]/[3]-shaped pairs (6k-point LiDAR street scan; 40%-overlap
+    pair with outliers and inhomogeneous density): the session's mass fields
+    are the reference's bit for bit, and from the reference's own states one
+    GPU iteration reproduces its [R_acc | t_acc] (tests/golden/tf_configs.npz)."""
+    from paper_2009_14005_b200.engine import Session
+    g = golden("tf_configs")
+    k = case + "/"
+    p = fga.default_params().replace(theta=0.5, G=float(g[k + "G"]), max_iters=3,
+                                     conv_tol=1e-300)
+    o = fga.RegisterOptions(compute_gpe=False, record_iterations=True, precision=precision)
+    tol = 2e-5 if precision == "fp32" else 1e-10
+    s = Session(fga.PointCloud(g[k + "x"]), fga.PointCloud(g[k + "y"]), p, o)
+    mx, my = s.masses()
+    assert np.array_equal(mx, g[k + "mass_x"]) and np.array_equal(my, g[k + "mass_y"])
+    s.iterate(1)  # iteration 0 from the session's own setup
+    st = s.get_state()
+    r0 = s.finish()
+    assert np.abs(r0.trajectory[0] - g[k + "traj"][0]).max() < tol
+    scale = np.abs(g[k + "pos"][0]).max()
+    assert np.abs(st["positions"] - g[k + "pos"][0]).max() < tol * max(scale, 1.0)
+    for it in (1, 2):
+        s = Session(fga.PointCloud(g[k + "x"]), fga.PointCloud(g[k + "y"]), p, o)
+        prev = g[k + "traj"][it - 1]
+        s.set_state(g[k + "pos"][it - 1], g[k + "vel"][it - 1], prev[:, :3], prev[:, 3], it)
+        s.iterate(1)
+        r = s.finish()
+        assert np.abs(r.trajectory[it] - g[k + "traj"][it]).max() < tol
