@@ -49,6 +49,9 @@ namespace fga {
 namespace {
 
 constexpr int kThreads = 256;
+// points per block of k_levels / k_emit / k_export (they share the block
+// mapping of the per-level block offsets; large blocks keep the scan short)
+constexpr int kLT = 256;  // (1024 measured 5-11% slower: emit latency-bound)
 
 inline int blocks_for(int64_t n, int t = kThreads) {
   int64_t b = (n + t - 1) / t;
@@ -271,10 +274,10 @@ __device__ __forceinline__ Chain chain_of(const signed char* __restrict__ clev, 
 }
 
 // c_i for i in [0, N], the number of nodes each point starts, and per block
-// of kThreads points the number of nodes it starts at each level:
+// of kLT points the number of nodes it starts at each level:
 // bcount[l * nb + block] (all nodes) and bcount[(L + 1 + l) * nb + block]
 // (internal nodes).
-__global__ void __launch_bounds__(kThreads) k_levels(const unsigned long long* __restrict__ keys,
+__global__ void __launch_bounds__(kLT) k_levels(const unsigned long long* __restrict__ keys,
                                                      int64_t n, int L,
                                                      signed char* __restrict__ clev,
                                                      int* __restrict__ count,
@@ -435,8 +438,8 @@ __device__ __forceinline__ void write_records(const TreeRecords& r, int mir, int
 // (all nodes, and internal nodes only): warp ballots + warp prefix in shared
 // memory.  Must be called by the whole block.
 struct BlockRanks {
-  unsigned bal[2][kMaxLevels + 1][kThreads / 32];
-  int pre[2][kMaxLevels + 1][kThreads / 32];
+  unsigned bal[2][kMaxLevels + 1][kLT / 32];
+  int pre[2][kMaxLevels + 1][kLT / 32];
 };
 __device__ __forceinline__ void block_ranks(BlockRanks& R, const Chain& c, int L) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -454,7 +457,7 @@ __device__ __forceinline__ void block_ranks(BlockRanks& R, const Chain& c, int L
   if (threadIdx.x < 2 * (L + 1)) {
     const int k = threadIdx.x > L, l = threadIdx.x - k * (L + 1);
     int acc = 0;
-    for (int q = 0; q < kThreads / 32; q++) {
+    for (int q = 0; q < kLT / 32; q++) {
       const int v = R.pre[k][l][q];
       R.pre[k][l][q] = acc;
       acc += v;
@@ -492,7 +495,7 @@ struct InNode {
 // traversal records.  Preorder numbering from offset[]: x = offset[i] + l -
 // s_i, skip = x + subtree size.  The bbox (for the length, :83) is replayed
 // incrementally along the chain.  Same point->block mapping as k_levels.
-__global__ void __launch_bounds__(kThreads) k_emit(const unsigned long long* __restrict__ keys,
+__global__ void __launch_bounds__(kLT) k_emit(const unsigned long long* __restrict__ keys,
                                                    int64_t n, int L,
                                                    const signed char* __restrict__ clev,
                                                    const int* __restrict__ offset,
@@ -630,7 +633,7 @@ __device__ __forceinline__ int64_t lower_bound_gallop(const unsigned long long* 
 // child slot (parent: the chain's previous node, or found by a backwards
 // search for the start of the parent's key prefix).  children must be -1
 // filled.  Export only, not on the registration path.
-__global__ void __launch_bounds__(kThreads) k_export(const unsigned long long* __restrict__ keys,
+__global__ void __launch_bounds__(kLT) k_export(const unsigned long long* __restrict__ keys,
                                                      int64_t n, int L,
                                                      const signed char* __restrict__ clev,
                                                      const int* __restrict__ offset,
@@ -737,7 +740,7 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   FGA_CUDA_TRY(T.clev.reserve(n + 1));
   FGA_CUDA_TRY(T.count.reserve(sizeof(int) * (n + 1)));
   FGA_CUDA_TRY(T.offset.reserve(sizeof(int) * (n + 1)));
-  const int nbl = blocks_for(n + 1);
+  const int nbl = blocks_for(n + 1, kLT);
   FGA_CUDA_TRY(T.bcount.reserve(sizeof(int) * (int64_t)2 * (L + 1) * nbl));
   FGA_CUDA_TRY(T.lvl.reserve(sizeof(int) * (kLvlInts + 1)));
   int* row_total = T.lvl.as<int>();
@@ -771,7 +774,7 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
                                                      T.idx.as<int>(), T.sp.as<double4>(), overflow);
   // levels, per-level block counts, preorder offsets (rerun after a fallback)
   auto levels = [&]() -> int {
-    k_levels<<<nbl, kThreads, 0, st>>>(T.keys.as<unsigned long long>(), n, L,
+    k_levels<<<nbl, kLT, 0, st>>>(T.keys.as<unsigned long long>(), n, L,
                                        T.clev.as<signed char>(), T.count.as<int>(),
                                        T.bcount.as<int>());
     k_level_scan<<<2 * (L + 1), 1024, 0, st>>>(T.bcount.as<int>(), nbl, row_total);
@@ -824,7 +827,7 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   FGA_CUDA_TRY(T.a64.reserve(sizeof(double4) * nn64));
   FGA_CUDA_TRY(T.b64.reserve(sizeof(NodeB64) * nn64));
 
-  k_emit<<<nbl, kThreads, 0, st>>>(T.keys.as<unsigned long long>(), n, L, T.clev.as<signed char>(),
+  k_emit<<<nbl, kLT, 0, st>>>(T.keys.as<unsigned long long>(), n, L, T.clev.as<signed char>(),
                                    T.offset.as<int>(), T.bcount.as<int>(), lvl_off, ilvl_off,
                                    T.box.as<double>(), nn, T.sp.as<double4>(),
                                    T.inodes.as<InNode>(), T.sums.as<double4>(), T.sizep.as<int>(),
@@ -874,7 +877,7 @@ int tree_export_host(TreeDev& T, cudaStream_t st, int64_t* children, double* com
   double* d_bmax = (double*)p;
   if (children) FGA_CUDA_TRY(cudaMemsetAsync(d_children, 0xff, sizeof(long long) * 8 * nn, st));
   const int* lvl_off = T.lvl.as<int>() + 2 * (kMaxLevels + 1);
-  k_export<<<blocks_for(T.n_points + 1), kThreads, 0, st>>>(
+  k_export<<<blocks_for(T.n_points + 1, kLT), kLT, 0, st>>>(
       T.keys.as<unsigned long long>(), T.n_points, T.L, T.clev.as<signed char>(),
       T.offset.as<int>(), T.bcount.as<int>(), lvl_off, T.box.as<double>(), T.sums.as<double4>(),
       children ? d_children : nullptr, com ? d_com : nullptr, mass ? d_mass : nullptr,
