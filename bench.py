@@ -240,6 +240,10 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": 4 * K,  # k_bh_iterate, k_reduce_stage, k_reduce_final, k_update
         "interactions_per_step": per_launch_inter,
     }
+    # also visits/s and "equivalent direct pairs/s" (N*M per
+    # iteration over the same time), labelled as such
+    line["visits_per_s"] = _visits_per_step(res, W, K) * K / (total_ms / 1e3)
+    line["equivalent_direct_pairs_per_s"] = float(len(x)) * float(len(y)) * K / (total_ms / 1e3)
     visits_step = _visits_per_step(res, W, K)
     flop = FLOP_PER_INTERACTION * per_launch_inter + FLOP_PER_VISIT * visits_step
     achieved = flop / mean_force_s / 1e12
@@ -595,6 +599,14 @@ def run_other_configs(args):
     t0 = time.perf_counter()
     r = fga.register(x, y, params=p, options=o)
     wall = time.perf_counter() - t0
+    o_niv = fga.RegisterOptions()
+    t0 = time.perf_counter()
+    r_niv = fga.register(x, y, params=p, options=o_niv)
+    wall_niv = time.perf_counter() - t0
+    out["c4_overlap_200k_niv"] = {
+        "wall_s": wall_niv, "iterations": r_niv.iterations, "converged": r_niv.converged,
+        "G": p.G, "rotation_err_deg": fga.angular_deviation(gt.rotation, r_niv.transform.rotation),
+        "timings_ms": r_niv.timings_ms}
     out["c4_overlap_200k_knn16"] = {
         "wall_s": wall, "iterations": r.iterations, "converged": r.converged, "G": p.G,
         "rotation_err_deg": fga.angular_deviation(gt.rotation, r.transform.rotation),
@@ -667,11 +679,19 @@ def cpu_baseline(args, x, y, sample):
     t0 = time.perf_counter()
     _, visits, acc = orc.bh_forces(tree, yn[idx], my[idx], args.theta, p["G"], p["eps"], threads)
     dt = time.perf_counter() - t0
+    # the reference as shipped is single-threaded -- one core
+    # on a quarter of the sample
+    idx1 = idx[: max(1, len(idx) // 4)]
+    t0 = time.perf_counter()
+    _, _, acc1 = orc.bh_forces(tree, yn[idx1], my[idx1], args.theta, p["G"], p["eps"], 1)
+    dt1 = time.perf_counter() - t0
     return {"value": float(acc.sum()) / dt, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{len(idx)} template queries of the {len(yn)}-point workload at the "
                       f"initial state (oracle bh_forces, theta={args.theta}); tree build "
                       f"{build_s:.2f} s single-threaded",
-            "seconds": dt, "visits_per_query": float(visits.mean())}
+            "seconds": dt, "visits_per_query": float(visits.mean()),
+            "one_core": {"value": float(acc1.sum()) / dt1, "unit": UNIT, "cores": 1,
+                         "sample": f"{len(idx1)} of the same queries", "seconds": dt1}}
 
 
 def run_reference(args, rank):
