@@ -32,7 +32,7 @@ def _check_knn(pts, k):
     return idx, d2
 
 
-@pytest.mark.parametrize("kind", ["blob", "uniform", "overlap_outliers"])
+@pytest.mark.parametrize("kind", ["blob", "uniform", "overlap_outliers", "far_offset"])
 def test_knn_exact_vs_ckdtree(kind):
     from paper_2009_14005_b200 import synth
     rng = synth.rng_from_seed(7)
@@ -40,6 +40,8 @@ def test_knn_exact_vs_ckdtree(kind):
         pts = synth.blob(20000, rng).points
     elif kind == "uniform":
         pts = rng.uniform(-5, 5, size=(20000, 3))
+    elif kind == "far_offset":  # tiny spacing far from the origin: fp32 prefilter at its limit
+        pts = synth.blob(20000, rng).points * 0.01 + np.array([500.0, -300.0, 750.0])
     else:
         x, _ = synth.partial_overlap(20000, rng)
         pts = x.points
