@@ -242,7 +242,8 @@ def register_sequence(frames, params: FgaParams | None = None,
     params = params or default_params()
     options = options or RegisterOptions()
     pairs = [(frames[i + 1], frames[i]) for i in range(len(frames) - 1)]
-    small = (max(len(f) for f in frames) <= 8192 and options.x_weights is None
+    small = (max(len(f) for f in frames) <= 8192 and all(f.dim == 3 for f in frames)
+             and options.x_weights is None
              and options.y_weights is None and options.mass_field == "niv"
              and options.precision == "fp32" and not options.trace_gpe and options.normalize)
     pairwise, failed = [], []

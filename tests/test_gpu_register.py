@@ -154,3 +154,19 @@ def test_register_sequence_concurrent_matches_pairwise(fga, n):
     for k in range(4):
         pose = pose.compose(seq.pairwise[k].inverse())
         assert np.allclose(seq.trajectory[k + 1].rotation, pose.rotation, atol=1e-12)
+
+
+def test_register_sequence_two_d(fga):
+    """2-D frames take the per-pair path (the batched kernel is 3-D only)."""
+    rng = np.random.default_rng(5)
+    base = rng.uniform(-0.5, 0.5, size=(800, 2))
+    frames = [fga.PointCloud(base)]
+    for k in range(3):
+        a = 0.05 * (k + 1)
+        R = np.array([[np.cos(a), -np.sin(a)], [np.sin(a), np.cos(a)]])
+        frames.append(fga.PointCloud(frames[-1].points @ R.T + 0.01))
+    seq = fga.register_sequence(frames)
+    assert len(seq.pairwise) == 3 and not any(seq.failed)
+    for k in range(3):
+        single = fga.register(x=frames[k + 1], y=frames[k]).transform
+        assert np.array_equal(seq.pairwise[k].rotation, single.rotation)
