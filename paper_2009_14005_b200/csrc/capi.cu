@@ -48,6 +48,7 @@ struct Session {
   DevBuf x_raw, y_raw, xn, yn, ctx_dev, mx, my, flat, counts, cells, ref32, ref64;
   DevBuf tkeys_in, tkeys, tidx_in, tidx, cub_tmp, tpl;
   DevBuf partials, gpe_part, sums, state, scratch, lm_idx, rbf_scratch, red_stage;
+  DevBuf gpe_snap, gpe_part2, gpe_sums2;  // initial energy on the aux stream
   DevBuf rec_delta, rec_traj, rec_gpe, rec_inter, rec_visits;
   float setup_ms = 0.f, loop_ms = 0.f, gpe_ms = 0.f;
 
@@ -75,6 +76,9 @@ struct fga_ctx {
   Session S;
   int* pinned = nullptr;  // poll buffer: done, pad, iter(lo,hi)
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  // second stream for the initial energy, which runs alongside the iterations
+  cudaStream_t aux = nullptr;
+  cudaEvent_t aev[3] = {nullptr, nullptr, nullptr};
 };
 
 namespace {
@@ -531,6 +535,12 @@ int fga_destroy(fga_ctx* c) {
   for (DevBuf* b : all) b->release();
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->aev)
+    if (e) cudaEventDestroy(e);
+  if (c->aux) {
+    cudaStreamSynchronize(c->aux);
+    cudaStreamDestroy(c->aux);
+  }
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -813,7 +823,38 @@ int fga_register(fga_ctx* c, const double* x, int64_t n, const double* y, int64_
   Session& S = c->S;
   cudaStream_t s = c->stream;
   float gpe_ms = 0.f;
-  if (S.O.compute_gpe) {
+  // The initial energy (registration.py:124) only reads the initial template
+  // state: it runs on a second stream from a snapshot of that state, next to
+  // the iterations (a MUFU-bound pass beside an issue-bound one).
+  static const bool async_gpe = [] {
+    const char* e = getenv("FGA_ASYNC_GPE");
+    return !(e && atoi(e) == 0);
+  }();
+  const bool gpe_async = S.O.compute_gpe && async_gpe && !S.O.trace_gpe && S.m_local > 0;
+  if (gpe_async) {
+    if (!c->aux) {
+      FGA_CUDA_TRY(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+      for (auto& e : c->aev) FGA_CUDA_TRY(cudaEventCreate(&e));
+    }
+    const int64_t ml = S.m_local;
+    const TemplateView tv = S.view();
+    FGA_CUDA_TRY(S.gpe_snap.reserve(sizeof(double) * 4 * ml));
+    double* snap = S.gpe_snap.as<double>();
+    FGA_CUDA_TRY(cudaMemcpyAsync(snap, tv.px, sizeof(double) * 3 * ml, cudaMemcpyDeviceToDevice, s));
+    FGA_CUDA_TRY(cudaMemcpyAsync(snap + 3 * ml, tv.mq, sizeof(double) * ml, cudaMemcpyDeviceToDevice, s));
+    const int64_t ngw = gpe_warps(ml, S.precision);
+    FGA_CUDA_TRY(S.gpe_part2.reserve(sizeof(double) * std::max<int64_t>(ngw, 1)));
+    FGA_CUDA_TRY(S.gpe_sums2.reserve(sizeof(double) * (kPartialStride + reduce_stage_doubles())));
+    FGA_CUDA_TRY(cudaEventRecord(c->aev[0], s));
+    FGA_CUDA_TRY(cudaStreamWaitEvent(c->aux, c->aev[0], 0));
+    FGA_CUDA_TRY(cudaEventRecord(c->aev[1], c->aux));
+    launch_gpe(S.ref(), snap, snap + ml, snap + 2 * ml, snap + 3 * ml, ml, S.sp.eps, nullptr,
+               S.gpe_part2.as<double>(), S.precision, c->aux);
+    launch_reduce(nullptr, 0, S.gpe_part2.as<double>(), ngw, -1.0, S.gpe_sums2.as<double>(),
+                  S.gpe_sums2.as<double>() + kPartialStride, c->aux);
+    FGA_CUDA_TRY(cudaGetLastError());
+    FGA_CUDA_TRY(cudaEventRecord(c->aev[2], c->aux));
+  } else if (S.O.compute_gpe) {
     FGA_CUDA_TRY(cudaEventRecord(c->ev[4], s));
     TRY(session_gpe(c, nullptr));
     FGA_CUDA_TRY(cudaEventRecord(c->ev[5], s));
@@ -834,6 +875,15 @@ int fga_register(fga_ctx* c, const double* x, int64_t n, const double* y, int64_
   FGA_CUDA_TRY(cudaEventRecord(c->ev[3], s));
   FGA_CUDA_TRY(cudaEventSynchronize(c->ev[3]));
   cudaEventElapsedTime(&S.loop_ms, c->ev[2], c->ev[3]);
+  if (gpe_async) {
+    FGA_CUDA_TRY(cudaEventSynchronize(c->aev[2]));
+    double v = 0.0;
+    FGA_CUDA_TRY(cudaMemcpy(&v, S.gpe_sums2.as<double>() + kGpe, sizeof(double),
+                            cudaMemcpyDeviceToHost));
+    S.gpe_initial = -S.P.G * v;  // _kernels.py:67
+    S.have_gpe_initial = true;
+    cudaEventElapsedTime(&gpe_ms, c->aev[1], c->aev[2]);
+  }
   TRY(session_apply(c));
   if (S.O.compute_gpe) {
     FGA_CUDA_TRY(cudaEventRecord(c->ev[4], s));
