@@ -580,6 +580,21 @@ def run_other_configs(args):
     t0 = time.perf_counter()
     r = fga.register(x, y, params=p)
     wall = time.perf_counter() - t0
+    # the second variant of SURVEY §8(d) C2: the same street rescanned from a
+    # sensor moved by gt (different sampling -- a realistic next frame)
+    rng2 = synth.rng_from_seed(2)
+    scene = synth.lidar_scene(rng2)
+    xa = synth.lidar_scan(100_000, rng2, scene=scene)
+    gt2 = synth.random_rigid(rng2, np.deg2rad(10), 1.0)
+    yb = synth.lidar_scan(100_000, rng2, scene=scene, pose=gt2)
+    t0 = time.perf_counter()
+    r2 = fga.register(xa, yb, params=p)
+    wall2 = time.perf_counter() - t0
+    out["c2_lidar_100k_rescan"] = {
+        "wall_s": wall2, "iterations": r2.iterations, "converged": r2.converged, "G": p.G,
+        "rotation_err_deg": fga.angular_deviation(gt2.rotation, r2.transform.rotation),
+        "translation_err_m": float(np.linalg.norm(r2.transform.translation - gt2.translation)),
+        "timings_ms": r2.timings_ms}
     out["c2_lidar_100k"] = {
         "wall_s": wall, "iterations": r.iterations, "converged": r.converged, "G": p.G,
         "rotation_err_deg": fga.angular_deviation(gt.rotation, r.transform.rotation),

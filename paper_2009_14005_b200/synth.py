@@ -91,28 +91,9 @@ def add_uniform_noise(cloud: PointCloud, fraction, rng, low=-0.5, high=0.5):
     return PointCloud(np.vstack([cloud.points, rng.uniform(low, high, size=(extra, cloud.dim))]))
 
 
-def lidar_scan(n, rng, sensor_height=1.73):
-    """A spinning 64-beam scan (elevation -24.9..+2 deg, 0.18 deg azimuth
-    steps) of a street: ground plane, two facades at +-8 m, 20 box "cars" and
-    poles; range noise N(0, 2 cm); subsampled to exactly n returns, so the
-    density falls off ~1/r^2 like a real sensor (config 2)."""
-    elev = np.deg2rad(np.linspace(-24.9, 2.0, 64))
-    az = np.deg2rad(np.arange(0.0, 360.0, 0.18))
-    E, A = np.meshgrid(elev, az, indexing="ij")
-    d = np.stack([np.cos(E) * np.cos(A), np.cos(E) * np.sin(A), np.sin(E)], -1).reshape(-1, 3)
-    o = np.array([0.0, 0.0, sensor_height])
-    t = np.full(len(d), np.inf)
-    # ground z = 0
-    dz = d[:, 2]
-    with np.errstate(divide="ignore", invalid="ignore"):
-        tg = np.where(dz < 0, -o[2] / dz, np.inf)
-        t = np.minimum(t, tg)
-        # facades y = +-8 (height 0..12 m)
-        for wall in (8.0, -8.0):
-            tw = np.where(d[:, 1] * np.sign(wall) > 0, wall / d[:, 1], np.inf)
-            zw = o[2] + tw * dz
-            t = np.minimum(t, np.where((zw >= 0) & (zw <= 12.0), tw, np.inf))
-    # axis-aligned boxes (cars 4.5 x 1.8 x 1.5) and poles (0.3 x 0.3 x 6)
+def lidar_scene(rng):
+    """The street of lidar_scan: 20 box "cars" (4.5 x 1.8 x 1.5 m) in four
+    lanes and 12 poles (0.3 x 0.3 x 6 m) along the facades, as (lo, hi) boxes."""
     boxes = []
     for _ in range(20):
         cx = rng.uniform(-40, 40)
@@ -122,6 +103,39 @@ def lidar_scan(n, rng, sensor_height=1.73):
         cx = rng.uniform(-40, 40)
         cy = rng.choice([-7.0, 7.0])
         boxes.append(((cx - 0.15, cy - 0.15, 0.0), (cx + 0.15, cy + 0.15, 6.0)))
+    return boxes
+
+
+def lidar_scan(n, rng, sensor_height=1.73, scene=None, pose=None):
+    """A spinning 64-beam scan (elevation -24.9..+2 deg, 0.18 deg azimuth
+    steps) of a street: ground plane, two facades at +-8 m, 20 box "cars" and
+    poles; range noise N(0, 2 cm); subsampled to exactly n returns, so the
+    density falls off ~1/r^2 like a real sensor (config 2).
+
+    `scene` (lidar_scene) fixes the street; `pose` (RigidTransform, sensor
+    frame -> street frame) moves the sensor: the returns are in the SENSOR's
+    frame, so a second scan from `pose` is a realistic next frame whose
+    registration onto the first recovers `pose` (different sampling, not a
+    rigid copy)."""
+    elev = np.deg2rad(np.linspace(-24.9, 2.0, 64))
+    az = np.deg2rad(np.arange(0.0, 360.0, 0.18))
+    E, A = np.meshgrid(elev, az, indexing="ij")
+    d = np.stack([np.cos(E) * np.cos(A), np.cos(E) * np.sin(A), np.sin(E)], -1).reshape(-1, 3)
+    o = np.array([0.0, 0.0, sensor_height])
+    if pose is not None:  # rays of the moved sensor, in street coordinates
+        d = d @ pose.rotation.T
+        o = pose.rotation @ o + pose.translation
+    t = np.full(len(d), np.inf)
+    dz = d[:, 2]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        # ground z = 0
+        t = np.minimum(t, np.where(dz < 0, -o[2] / dz, np.inf))
+        # facades y = +-8 (height 0..12 m)
+        for wall in (8.0, -8.0):
+            tw = np.where(d[:, 1] * np.sign(wall - o[1]) > 0, (wall - o[1]) / d[:, 1], np.inf)
+            zw = o[2] + tw * dz
+            t = np.minimum(t, np.where((zw >= 0) & (zw <= 12.0), tw, np.inf))
+    boxes = scene if scene is not None else lidar_scene(rng)
     with np.errstate(divide="ignore", invalid="ignore"):
         inv = 1.0 / d
         for lo, hi in boxes:
@@ -134,6 +148,8 @@ def lidar_scan(n, rng, sensor_height=1.73):
     ok = np.isfinite(t) & (t < 80.0)
     r = t[ok] + rng.normal(0.0, 0.02, size=ok.sum())
     pts = o + d[ok] * r[:, None]
+    if pose is not None:  # street -> sensor frame
+        pts = (pts - pose.translation) @ pose.rotation
     if len(pts) >= n:
         pts = pts[np.sort(rng.choice(len(pts), size=n, replace=False))]
     else:  # densify by jittered resampling to reach exactly n returns
