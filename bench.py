@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--direct-steps", type=int, default=3)
     ap.add_argument("--no-batched", action="store_true")
     ap.add_argument("--no-build", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true")
     ap.add_argument("--no-ingest", action="store_true")
     ap.add_argument("--build-sizes", default="1000000,16000000")
     ap.add_argument("--no-configs", action="store_true",
@@ -267,6 +268,8 @@ def run_ours(args, rank, world, local_rank):
         line["tree_build"] = run_tree_build(args, dev, peaks, peak_src)
     if world == 1 and not args.no_direct:
         line["direct"] = run_direct(args, x, y, dev, stream, peak, peak_src, fmax)
+    if world == 1 and not args.no_fp64:
+        line["fp64_mode"] = run_fp64(args, x_t, y_t, len(x), len(y), dev, stream, local_rank)
     if world == 1 and not args.no_e2e:
         line["e2e"] = run_e2e(args, x, y, sess)
     if world == 1 and not args.no_registration:
@@ -359,6 +362,37 @@ def run_tree_build(args, dev, peaks, peak_src):
     c.close()
     out["api"] = "fga_tree_build_dev (blob points, unit masses, max_depth 20), median of reps, L2 flushed"
     return out
+
+
+def run_fp64(args, x_t, y_t, n, m, dev, stream, local_rank):
+    """The same 1M iteration with precision="fp64": the reference's
+    arithmetic and node order (forces bit-identical to bh_forces_kernel on
+    the same tree), for the cost of exactness next to the FP32 headline."""
+    import torch
+
+    import paper_2009_14005_b200 as fga
+    from paper_2009_14005_b200.engine import Session
+    K, W = 3, 1
+    params = bench_params(args).replace(conv_tol=1e-300, max_iters=W + K + 1)
+    sess = Session(None, None, params, fga.RegisterOptions(compute_gpe=False, precision="fp64"),
+                   device=local_rank, stream=stream.cuda_stream,
+                   device_inputs=(x_t.data_ptr(), n, y_t.data_ptr(), m))
+    for _ in range(W):
+        sess.forces()
+        sess.update()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(K):
+        sess.forces()
+        sess.update()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    res = sess.finish()
+    inter = float(res.interactions[W:W + K].mean())
+    return {"ms_per_step": ms, "value": inter / (ms / 1e3), "unit": UNIT,
+            "note": "precision=fp64: reference arithmetic, bit-identical forces on the same tree"}
 
 
 def _visits_per_step(res, W, K):
