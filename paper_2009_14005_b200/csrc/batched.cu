@@ -25,6 +25,7 @@ namespace {
 
 constexpr int kBT = 1024;  // threads per CTA
 constexpr int kBW = kBT / 32;
+static_assert(kBT == 1024, "the chunk-sum split assumes 16 moments x 64 ranges");
 
 struct PairState {
   double R[9], t[3], Racc[9], tacc[3], shift[3];
@@ -717,15 +718,26 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
           }
         }
         __syncthreads();
-        if (tid < 16) {  // chunk-order sums, one lane per moment
+        {  // chunk sums in a fixed order, all threads: 16 moments x 64 contiguous chunk ranges,
+           // ranges paired in the warp, then the 32 warp results in warp order
+          const int k = tid & 15, part = tid >> 4;
+          const int c0 = (int)((int64_t)nchunks * part / 64);
+          const int c1 = (int)((int64_t)nchunks * (part + 1) / 64);
           double v = 0.0;
-          for (int c = 0; c < nchunks; c++) v += __ldcg(&cpart[(size_t)c * kPartialStride + tid]);
-          S.part[tid] = v;
+          for (int c = c0; c < c1; c++) v += __ldcg(&cpart[(size_t)c * kPartialStride + k]);
+          v += __shfl_down_sync(0xffffffffu, v, 16);  // part 2w + part 2w+1
+          if (lane < 16) S.part[w * 16 + k] = v;
+          __syncthreads();
+          if (tid < 16) {
+            double t = 0.0;
+            for (int q = 0; q < kBW; q++) t += S.part[q * 16 + tid];
+            S.part[kBW * 16 + tid] = t;
+          }
         }
         __syncthreads();
         if (tid == 0) {
           double sums[16];
-          for (int k = 0; k < 16; k++) sums[k] = S.part[k];
+          for (int k = 0; k < 16; k++) sums[k] = S.part[kBW * 16 + k];
           const double M = (double)m;
           double mu_u[3], mu_w[3], C[9], R[9], t[3];
           for (int k = 0; k < 3; k++) {
