@@ -8,8 +8,6 @@
 
 namespace fga {
 
-constexpr int kLvlInts = 2 * (kMaxLevels + 1) + 2 * (kMaxLevels + 3);
-
 // Mirrored-preorder traversal records.
 struct TreeRecords {
   float4* a32;
@@ -28,9 +26,9 @@ struct TreeDev {
   const double* pts = nullptr;     // (n,3) device, not owned
   const double* masses = nullptr;  // (n,) device, not owned
   DevBuf box, scratch, keys_in, keys, idx_in, idx, clev, count, offset, cub_tmp;
-  // build intermediates: packed (x,y,z,m) in input order, sorted copy, level
-  // counts/offsets, internal-node lists, BFS-ordered node sums (mass, m*p)
-  DevBuf keys32_in, keys32, packed, sp, bcount, lvl, inodes, sums, sizep;
+  // build intermediates: packed (x,y,z,m) in input order, sorted copy, the
+  // run-overflow flag, per-(level, block) boundary partials (tree.cu Cross)
+  DevBuf keys32_in, keys32, packed, sp, lvl, cross;
   DevBuf a32, b32, a64, b64;
   DevBuf export_buf;
 
@@ -39,8 +37,8 @@ struct TreeDev {
   }
   void release() {
     DevBuf* all[] = {&box,    &scratch, &keys_in, &keys,   &idx_in, &idx, &clev,
-                     &count,  &offset,  &cub_tmp, &keys32_in, &keys32, &packed, &sp,     &bcount, &lvl,
-                     &inodes, &sums,    &sizep,    &a32,    &b32,    &a64,    &b64,  &export_buf};
+                     &count,  &offset,  &cub_tmp, &keys32_in, &keys32, &packed, &sp,     &lvl,
+                     &cross,  &a32,    &b32,    &a64,    &b64,  &export_buf};
     for (DevBuf* b : all) b->release();
     n_nodes = 0;
     exportable = false;

@@ -25,12 +25,13 @@
 //   k_keys          per-axis fp64 split recursion -> 3L-bit key (dyadic fast
 //                   path with an exact-replay fallback near split planes)
 //   (cub radix sort, stable: keeps the reference's within-leaf index order)
-//   k_levels        c_i, per-point node counts, per-block per-level counts
-//   (cub exclusive scan) -> preorder node offsets, node count
-//   k_level_scan    per level: block offsets -> level-major (BFS) positions
-//   k_emit          per node, in BFS order: start, occupancy, first child,
-//                   mirrored index, bbox replay -> length (:83)
-//   k_sum_level x (L+1)  mass, m*com bottom-up (:78-82) + mirrored records
+//   k_gather_sorted sorted points + full keys; k_fixup_runs low key bits
+//   k_count         c_i and per-point node counts
+//   (cub exclusive scan) -> preorder offsets, node count
+//   k_subtrees      per block of 512 sorted points: the chains top-down
+//                   (bbox replay -> length, skip = offset[end]) and the
+//                   aggregates bottom-up in shared memory; mirrored records
+//   k_crossing      nodes that cross block boundaries: partials combined
 #include <cub/cub.cuh>
 
 #include "fga_internal.cuh"
@@ -49,10 +50,6 @@ namespace fga {
 namespace {
 
 constexpr int kThreads = 256;
-// points per block of k_levels / k_emit / k_export (they share the block
-// mapping of the per-level block offsets; large blocks keep the scan short)
-constexpr int kLT = 256;  // (1024 measured 5-11% slower: emit latency-bound)
-
 inline int blocks_for(int64_t n, int t = kThreads) {
   int64_t b = (n + t - 1) / t;
   return (int)(b < 1 ? 1 : b);
@@ -259,96 +256,23 @@ __global__ void k_fixup_runs(const unsigned* __restrict__ hi, int64_t n,
 // nodes below e are internal (they also hold point i+1, which shares c_{i+1}
 // >= l levels) and (i, e) is always a leaf: it holds point i alone, or sits at
 // the depth cap.
-struct Chain {
-  int s, e, cn;
-};
-__device__ __forceinline__ Chain chain_of(const signed char* __restrict__ clev, int64_t i,
-                                          int64_t n, int L) {
-  Chain c{L + 1, -1, -1};
-  if (i < n) {
-    c.cn = clev[i + 1];
-    c.s = clev[i] + 1;
-    if (c.s <= L) c.e = max(c.s, min(L, c.cn + 1));
-  }
-  return c;
-}
+__device__ __forceinline__ int chain_end(int s, int cn, int L) { return max(s, min(L, cn + 1)); }
 
-// c_i for i in [0, N], the number of nodes each point starts, and per block
-// of kLT points the number of nodes it starts at each level:
-// bcount[l * nb + block] (all nodes) and bcount[(L + 1 + l) * nb + block]
-// (internal nodes).
-__global__ void __launch_bounds__(kLT) k_levels(const unsigned long long* __restrict__ keys,
-                                                     int64_t n, int L,
-                                                     signed char* __restrict__ clev,
-                                                     int* __restrict__ count,
-                                                     int* __restrict__ bcount) {
-  __shared__ int hist[2 * (kMaxLevels + 1)];
-  if (threadIdx.x < 2 * (kMaxLevels + 1)) hist[threadIdx.x] = 0;
-  __syncthreads();
+// c_i for i in [0, N] (c_0 = c_N = -1) and the number of nodes each point
+// starts (count[N] = 0, so the exclusive scan's last entry is the node count).
+__global__ void k_count(const unsigned long long* __restrict__ keys, int64_t n, int L,
+                        signed char* __restrict__ clev, int* __restrict__ count) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i <= n) {
-    const int c = (i == 0 || i == n) ? -1 : common_levels(keys[i - 1], keys[i], L);
-    clev[i] = (signed char)c;
-    int cnt = 0;
-    if (i < n) {
-      const int cn = (i + 1 == n) ? -1 : common_levels(keys[i], keys[i + 1], L);
-      const int s = c + 1;
-      if (s <= L) {
-        const int e = max(s, min(L, cn + 1));
-        cnt = e - s + 1;
-        for (int l = s; l <= e; l++) atomicAdd(&hist[l], 1);
-        for (int l = s; l < e; l++) atomicAdd(&hist[L + 1 + l], 1);
-      }
-    }
-    count[i] = cnt;
+  if (i > n) return;
+  const int c = (i == 0 || i == n) ? -1 : common_levels(keys[i - 1], keys[i], L);
+  clev[i] = (signed char)c;
+  int cnt = 0;
+  if (i < n) {
+    const int cn = (i + 1 == n) ? -1 : common_levels(keys[i], keys[i + 1], L);
+    const int s = c + 1;
+    if (s <= L) cnt = chain_end(s, cn, L) - s + 1;
   }
-  __syncthreads();
-  if (threadIdx.x < 2 * (L + 1))
-    bcount[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = hist[threadIdx.x];
-}
-
-// Per row (one block each): exclusive scan of the block counts in place, the
-// row total into row_total[row].
-__global__ void __launch_bounds__(1024) k_level_scan(int* __restrict__ bcount, int nb,
-                                                     int* __restrict__ row_total) {
-  const int row = blockIdx.x;
-  int* v = bcount + (int64_t)row * nb;
-  const int per = (nb + blockDim.x - 1) / blockDim.x;
-  const int b0 = min(nb, (int)threadIdx.x * per), b1 = min(nb, b0 + per);
-  int sum = 0;
-  for (int b = b0; b < b1; b++) sum += v[b];
-  __shared__ int sh[1024];
-  sh[threadIdx.x] = sum;
-  __syncthreads();
-  for (int o = 1; o < (int)blockDim.x; o <<= 1) {  // inclusive Hillis-Steele
-    const int t = threadIdx.x >= (unsigned)o ? sh[threadIdx.x - o] : 0;
-    __syncthreads();
-    sh[threadIdx.x] += t;
-    __syncthreads();
-  }
-  int acc = sh[threadIdx.x] - sum;
-  for (int b = b0; b < b1; b++) {
-    const int t = v[b];
-    v[b] = acc;
-    acc += t;
-  }
-  if (threadIdx.x == blockDim.x - 1) row_total[row] = sh[threadIdx.x];
-}
-
-// lvl_off[l]: first BFS position of level l (lvl_off[L+1] = lvl_off[L+2] =
-// node count); ilvl_off[l]: first slot of level l in the internal-node list.
-__global__ void k_level_offsets(const int* __restrict__ row_total, int L, int* __restrict__ lvl_off,
-                                int* __restrict__ ilvl_off) {
-  if (threadIdx.x != 0) return;
-  int a = 0, b = 0;
-  for (int l = 0; l <= L; l++) {
-    lvl_off[l] = a;
-    ilvl_off[l] = b;
-    a += row_total[l];
-    b += row_total[L + 1 + l];
-  }
-  lvl_off[L + 1] = lvl_off[L + 2] = a;
-  ilvl_off[L + 1] = b;
+  count[i] = cnt;
 }
 
 // first j in [from, n) with keys[j] > bound (keys sorted): galloping search
@@ -385,6 +309,16 @@ __device__ __forceinline__ void bbox_step(unsigned long long key, int lev, int L
   }
 }
 
+__device__ __forceinline__ double diag_len(const double lo[3], const double hi[3]) {
+  double sq = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; a++) {
+    const double ex = __dsub_rn(hi[a], lo[a]);
+    sq = __dadd_rn(sq, __dmul_rn(ex, ex));
+  }
+  return __dsqrt_rn(sq);  // np.linalg.norm (bhtree.py:83)
+}
+
 // numpy's pairwise 1-D sum (loops_utils.h.src) of the masses of sorted
 // points [lo, lo + cnt); leaves hold one point except at the depth cap,
 // where this makes the leaf mass bit-exact.
@@ -409,202 +343,364 @@ __device__ double pairwise_mass(const double4* __restrict__ sp, int64_t lo, int6
   return __dadd_rn(pairwise_mass(sp, lo, n2), pairwise_mass(sp, lo + n2, cnt - n2));
 }
 
-// Leaf aggregate (bhtree.py:78-82): pairwise mass, sequential sum of m*p.
-__device__ __forceinline__ void leaf_sums(const double4* __restrict__ sp, int start, int occ,
-                                          double& ms, double mc[3]) {
-  ms = occ == 1 ? sp[start].w : pairwise_mass(sp, start, occ);
-  mc[0] = mc[1] = mc[2] = 0.0;
-  for (int q = 0; q < occ; q++) {
+// Leaf aggregate (bhtree.py:78-82): pairwise mass, sequential sum of m*p, as
+// {m, m x, m y, m z}.
+__device__ __forceinline__ double4 leaf_sums(const double4* __restrict__ sp, int64_t start,
+                                             int64_t occ) {
+  double4 r;
+  r.x = occ == 1 ? sp[start].w : pairwise_mass(sp, start, occ);
+  r.y = r.z = r.w = 0.0;
+  for (int64_t q = 0; q < occ; q++) {
     const double4 v = sp[start + q];
-    mc[0] = __dadd_rn(mc[0], __dmul_rn(v.x, v.w));
-    mc[1] = __dadd_rn(mc[1], __dmul_rn(v.y, v.w));
-    mc[2] = __dadd_rn(mc[2], __dmul_rn(v.z, v.w));
+    r.y = __dadd_rn(r.y, __dmul_rn(v.x, v.w));
+    r.z = __dadd_rn(r.z, __dmul_rn(v.y, v.w));
+    r.w = __dadd_rn(r.w, __dmul_rn(v.z, v.w));
   }
+  return r;
 }
 
-// The node's traversal records at its mirrored-preorder index.
-__device__ __forceinline__ void write_records(const TreeRecords& r, int mir, int rskip, bool leaf,
-                                              double len, double ms, const double mc[3]) {
-  const double cx = __ddiv_rn(mc[0], ms), cy = __ddiv_rn(mc[1], ms), cz = __ddiv_rn(mc[2], ms);
+__device__ __forceinline__ void add4(double4& a, const double4& b) {
+  a.x = __dadd_rn(a.x, b.x);
+  a.y = __dadd_rn(a.y, b.y);
+  a.z = __dadd_rn(a.z, b.z);
+  a.w = __dadd_rn(a.w, b.w);
+}
+
+// The node's traversal records at its mirrored-preorder index, in two halves:
+// the structural one ({l^2, skip}, known top-down) and the aggregate one
+// ({com, mass}, known bottom-up).
+__device__ __forceinline__ void write_records_b(const TreeRecords& r, int mir, int rskip, bool leaf,
+                                                double len) {
   const double l2 = __dmul_rn(len, len);
-  r.a64[mir] = make_double4(cx, cy, cz, ms);
   r.b64[mir] = NodeB64{leaf ? -INFINITY : l2, (long long)rskip};
-  r.a32[mir] = make_float4((float)cx, (float)cy, (float)cz, (float)ms);
   r.b32[mir] = NodeB32{leaf ? -INFINITY : (float)l2, rskip};
 }
-
-
-// Within-block ranks of the threads whose chains hold a node at level l
-// (all nodes, and internal nodes only): warp ballots + warp prefix in shared
-// memory.  Must be called by the whole block.
-struct BlockRanks {
-  unsigned bal[2][kMaxLevels + 1][kLT / 32];
-  int pre[2][kMaxLevels + 1][kLT / 32];
-};
-__device__ __forceinline__ void block_ranks(BlockRanks& R, const Chain& c, int L) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int l = 0; l <= L; l++) {
-    const unsigned ba = __ballot_sync(0xffffffffu, c.s <= l && l <= c.e);
-    const unsigned bi = __ballot_sync(0xffffffffu, c.s <= l && l < c.e);
-    if (lane == 0) {
-      R.bal[0][l][w] = ba;
-      R.pre[0][l][w] = __popc(ba);
-      R.bal[1][l][w] = bi;
-      R.pre[1][l][w] = __popc(bi);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < 2 * (L + 1)) {
-    const int k = threadIdx.x > L, l = threadIdx.x - k * (L + 1);
-    int acc = 0;
-    for (int q = 0; q < kLT / 32; q++) {
-      const int v = R.pre[k][l][q];
-      R.pre[k][l][q] = acc;
-      acc += v;
-    }
-  }
-  __syncthreads();
-}
-// slot of this thread's node at level l among all (k=0) / internal (k=1)
-// level-l nodes: global offsets + block offset + warp prefix + lane rank
-__device__ __forceinline__ int level_slot(const BlockRanks& R, int k, int l, int L,
-                                          const int* __restrict__ off,
-                                          const int* __restrict__ boff) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  return off[l] + boff[(int64_t)(k * (L + 1) + l) * gridDim.x + blockIdx.x] + R.pre[k][l][w] +
-         __popc(R.bal[k][l][w] & ((1u << lane) - 1u));
+__device__ __forceinline__ void write_records_a(const TreeRecords& r, int mir, const double4& v) {
+  const double cx = __ddiv_rn(v.y, v.x), cy = __ddiv_rn(v.z, v.x), cz = __ddiv_rn(v.w, v.x);
+  r.a64[mir] = make_double4(cx, cy, cz, v.x);
+  r.a32[mir] = make_float4((float)cx, (float)cy, (float)cz, (float)v.x);
 }
 
-// Internal node of the level lists (one 32-byte record).
-struct InNode {
-  int pos;    // BFS position (sums[] / sizep[] index)
-  int fc;     // BFS position of the first child = the chain's next node
-  int x;      // preorder index (bhtree.py:77)
-  int pad;
-  double len; // bbox diagonal (bhtree.py:83)
-  double pad2;
+// ---------------------------------------------------------------- hierarchy
+// Node (i, l) holds the sorted points [i, end), end = first j > i with
+// c_j < l, and its preorder subtree is the chain rest of i plus every chain
+// of the points in (i, end); so its preorder skip is offset[end] and its
+// mirrored index is l + n_nodes - offset[end] -- no bottom-up size pass.
+//
+// The aggregates (mass, m*p) are reduced bottom-up inside blocks of kST
+// consecutive sorted points (k_subtrees): a node is summed over its children
+// in slot order, starting from 0.0.  A node that crosses block boundaries gets
+// one partial per block it touches (the same fold over its children inside
+// that block, a crossing child contributing its own partial); k_crossing adds
+// them in a fixed dyadic shape.  Every result is a fixed function of the input
+// (kST is a constant), whatever the scheduling.
+constexpr int kST = 512;
+constexpr int kSW = kST / 32;
+
+// Per (level, block) boundary partials, SoA by level (index l * nb + b):
+//   pr/prx/prlen: the node owned by block b (starting in it) that runs past
+//                 its end, if any (prx = preorder index, -1 = none)
+//   pl/plend:     the node that starts before block b and covers its first
+//                 point, and where it ends inside b (-1 = past the block)
+//   mn[b]:        min c_j over the block's points 1..kST (the next block's
+//                 first point included): a level-l node covering the block's
+//                 first point ends inside it iff mn[b] < l
+// plus the dyadic sums / minima over aligned runs of 2^k blocks (k >= 1):
+//   hs[l * hn + ho[k] + j] = hs_{k-1}[2j] + hs_{k-1}[2j+1] (hs_0 = pl),
+//   hm[ho[k] + j] = min of the same runs of mn.
+constexpr int kMaxHier = 32;
+struct Cross {
+  double4* pr;
+  double4* pl;
+  double* prlen;
+  int* prx;
+  int* plend;
+  int* mn;
+  double4* hs;
+  int* hm;
+  int hn;  // entries per level in hs (sum of the dyadic level sizes)
+  int K;   // dyadic levels: 2^K >= nb
+  int ho[kMaxHier + 1];
 };
 
-// Per point i, the nodes (i, s_i..e_i), one level per loop turn for the
-// whole block so that each level's writes are contiguous.  Node (i, l) has
-// BFS position lvl_off[l] + (level-l nodes started before i): each level is
-// contiguous and sorted by start, and the children of consecutive internal
-// nodes are consecutive one level down.  Internal nodes go to the per-level
-// list `in` (their subtree sizes are found bottom-up);
-// the chain's leaf (i, e) is summarized here (bhtree.py:78-82) and writes its
-// traversal records.  Preorder numbering from offset[]: x = offset[i] + l -
-// s_i, skip = x + subtree size.  The bbox (for the length, :83) is replayed
-// incrementally along the chain.  Same point->block mapping as k_levels.
-__global__ void __launch_bounds__(kLT) k_emit(const unsigned long long* __restrict__ keys,
-                                                   int64_t n, int L,
-                                                   const signed char* __restrict__ clev,
-                                                   const int* __restrict__ offset,
-                                                   const int* __restrict__ boff,
-                                                   const int* __restrict__ lvl_off,
-                                                   const int* __restrict__ ilvl_off,
-                                                   const double* __restrict__ box, int n_nodes,
-                                                   const double4* __restrict__ sp,
-                                                   InNode* __restrict__ in,
-                                                   double4* __restrict__ sums,
-                                                   int* __restrict__ sizep, TreeRecords r) {
-  __shared__ BlockRanks R;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const Chain c = chain_of(clev, i, n, L);
-  block_ranks(R, c, L);
-  if (c.s > c.e) return;
-  const unsigned long long k = keys[i];
-  const int base = offset[i];
-  double lo[3], hi[3];
-#pragma unroll
-  for (int a = 0; a < 3; a++) {
-    lo[a] = box[a];
-    hi[a] = box[3 + a];
+// first set bit at a position > j of a kST-bit mask (nz: its non-zero words);
+// kST when none
+__device__ __forceinline__ int next_bit(const unsigned* __restrict__ m, unsigned nz, int j) {
+  const int wd = (j + 1) >> 5;
+  if (wd >= kSW) return kST;
+  const unsigned v = m[wd] & (~0u << ((j + 1) & 31));
+  if (v) return (wd << 5) + __ffs(v) - 1;
+  const unsigned z = nz & (~0u << (wd + 1));
+  if (!z) return kST;
+  const int w2 = __ffs(z) - 1;
+  return (w2 << 5) + __ffs(m[w2]) - 1;
+}
+
+// One block = kST sorted points, one thread each.  Per level l, bit masks
+// over the block's points: B_l (c_j < l: a node at level <= l starts at j, so
+// it ends every level-l range), H_l (a level-l node starts at j, or j = 0 and
+// the level-l node covering it started earlier -- the "pseudo head") and I_l
+// (the internal ones among H_l).  All the block's points share the levels <=
+// lca (the common levels of its first and last key): below lca only position
+// 0 has nodes, each with one child, so thread 0 walks them alone.
+//   top-down, every thread: its chain (bhtree.py:90-103 bbox replay from the
+//     shared level-lca box -> length; skip = offset[end]) -> structural
+//     records; its leaf's sums (:78-82) -> the leaf's aggregate record;
+//   bottom-up, per level lhi..lca: the level's internal heads, compacted to
+//     the first threads, fold their children (the H_{l+1} bits inside their
+//     range, in slot order) from shared memory.  Level-l ranges are
+//     disjoint, so the in-place update needs no more than the level barrier.
+__global__ void __launch_bounds__(kST, 2) k_subtrees(const unsigned long long* __restrict__ keys,
+                                                     int64_t n, int L,
+                                                     const signed char* __restrict__ clev,
+                                                     const int* __restrict__ offset,
+                                                     const double* __restrict__ box,
+                                                     const double4* __restrict__ sp,
+                                                     TreeRecords r, Cross cr, int nb) {
+  __shared__ unsigned mB[kMaxLevels + 2][kSW], mH[kMaxLevels + 2][kSW], mI[kMaxLevels + 2][kSW];
+  __shared__ unsigned nzB[kMaxLevels + 2], nzH[kMaxLevels + 2];
+  __shared__ unsigned short preI[kMaxLevels + 2][kSW + 1];
+  __shared__ short list[kST];
+  __shared__ int offs[kST + 1];
+  __shared__ signed char cs[kST + 1];
+  __shared__ double4 V[kST];
+  __shared__ double pbox[6];
+  __shared__ int s_maxe, s_mn;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5, b = blockIdx.x;
+  const int64_t B0 = (int64_t)b * kST, i = B0 + t;
+  const int64_t last = min(B0 + kST, n) - 1;
+  const int nn = offset[n];
+  cs[t] = i <= n ? clev[i] : (signed char)-1;
+  offs[t] = i <= n ? offset[i] : nn;
+  if (t == 0) {
+    const int64_t j = B0 + kST;
+    cs[kST] = j <= n ? clev[j] : (signed char)-1;
+    offs[kST] = j <= n ? offset[j] : nn;
+    s_maxe = -1;
+    s_mn = kMaxLevels + 1;
   }
-  double len = 0.0;
-  int pos = 0;
-  for (int l = 0; l <= c.e; l++) {
-    if (l > 0) bbox_step(k, l, L, lo, hi);
-    if (l < c.s) continue;
-    double sq = 0.0;
+  if (t <= L) cr.prx[t * nb + b] = -1;
+  const unsigned long long k0 = keys[B0];
+  const int lca = last > B0 ? common_levels(k0, keys[last], L) : L;
+  __syncthreads();
+  const int c = cs[t], c0 = cs[0], cend = cs[kST];
+  const bool has = i < n && c + 1 <= L;
+  const int s = c + 1, e = has ? chain_end(s, cs[t + 1], L) : -1;
+  if (has) atomicMax(&s_maxe, e);
+  if (t > 0) atomicMin(&s_mn, c);
+  if (t == kST - 1) {
+    atomicMin(&s_mn, cend);
+    // the box of the level-lca node holding every point of the block
+    double lo[3], hi[3];
 #pragma unroll
     for (int a = 0; a < 3; a++) {
-      const double ex = __dsub_rn(hi[a], lo[a]);
-      sq = __dadd_rn(sq, __dmul_rn(ex, ex));
+      lo[a] = box[a];
+      hi[a] = box[3 + a];
     }
-    len = __dsqrt_rn(sq);
-    pos = level_slot(R, 0, l, L, lvl_off, boff);
-    if (l < c.e)
-      in[level_slot(R, 1, l, L, ilvl_off, boff)] =
-          InNode{pos, level_slot(R, 0, l + 1, L, lvl_off, boff), base + (l - c.s), 0, len, 0.0};
+    for (int l = 1; l <= lca; l++) bbox_step(k0, l, L, lo, hi);
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      pbox[a] = lo[a];
+      pbox[3 + a] = hi[a];
+    }
   }
-  // the chain's leaf (i, e): point i alone, or a depth-cap cell of duplicates
-  int64_t end;
-  if (c.e > c.cn) end = i + 1;
-  else if (c.e == 0) end = n;
-  else end = upper_bound_gallop(keys, i + 1, n, k | low_mask(3 * (L - c.e)));
-  double ms, mc[3];
-  leaf_sums(sp, (int)i, (int)(end - i), ms, mc);
-  sums[pos] = make_double4(ms, mc[0], mc[1], mc[2]);
-  sizep[pos] = 1;
-  const int x = base + (c.e - c.s);
-  const int mir = c.e + n_nodes - (x + 1);  // skip = x + 1
-  write_records(r, mir, mir + 1, true, len, ms, mc);
+  for (int l = lca; l <= L + 1; l++) {
+    const bool ph = t == 0 && l <= c0;
+    const unsigned bb = __ballot_sync(0xffffffffu, c < l);
+    const unsigned bh = __ballot_sync(0xffffffffu, (has && s <= l && l <= e) || ph);
+    const unsigned bi = __ballot_sync(0xffffffffu, (has && s <= l && l < e) || (ph && l < L));
+    if (lane == 0) {
+      mB[l][w] = bb;
+      mH[l][w] = bh;
+      mI[l][w] = bi;
+    }
+  }
+  __syncthreads();
+  if (t >= lca && t <= L + 1) {  // per level: non-zero word summaries, internal-head word prefix
+    unsigned zb = 0, zh = 0, acc = 0;
+    for (int q = 0; q < kSW; q++) {
+      zb |= (mB[t][q] != 0u ? 1u : 0u) << q;
+      zh |= (mH[t][q] != 0u ? 1u : 0u) << q;
+      preI[t][q] = (unsigned short)acc;
+      acc += __popc(mI[t][q]);
+    }
+    nzB[t] = zb;
+    nzH[t] = zh;
+    preI[t][kSW] = (unsigned short)acc;
+  }
+  __syncthreads();
+  if (t == 0) cr.mn[b] = s_mn;
+
+  // top-down: structural records (and the length / preorder index of a node
+  // that runs past the block; k_crossing writes its records), leaf sums
+  double4 leafv = make_double4(0.0, 0.0, 0.0, 0.0);
+  if (has) {
+    const unsigned long long key = keys[i];
+    const int x0 = offs[t] - s;  // preorder index of (i, l) = x0 + l
+    double lo[3], hi[3];
+    int lv;
+    if (s <= lca) {  // (thread 0 only: the other points start below lca)
+      lv = 0;
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        lo[a] = box[a];
+        hi[a] = box[3 + a];
+      }
+    } else {
+      lv = lca;
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        lo[a] = pbox[a];
+        hi[a] = pbox[3 + a];
+      }
+    }
+    // the chain's leaf (i, e): point i alone, or a depth-cap cell of duplicates
+    int64_t end;
+    if (e > cs[t + 1]) end = i + 1;
+    else if (e == 0) end = n;
+    else end = upper_bound_gallop(keys, i + 1, n, key | low_mask(3 * (L - e)));
+    leafv = leaf_sums(sp, i, end - i);
+    for (int l = s; l <= e; l++) {
+      while (lv < l) bbox_step(key, ++lv, L, lo, hi);
+      const double len = diag_len(lo, hi);
+      const int x = x0 + l;
+      if (l == e) {
+        const int mir = l + nn - (x + 1);
+        write_records_b(r, mir, mir + 1, true, len);
+        write_records_a(r, mir, leafv);
+      } else {
+        const int p = l <= lca ? kST : next_bit(mB[l], nzB[l], t);
+        if (p < kST || cend < l) {
+          const int skipp = offs[p];
+          const int mir = l + nn - skipp;
+          write_records_b(r, mir, mir + (skipp - x), false, len);
+        } else {
+          cr.prx[l * nb + b] = x;
+          cr.prlen[l * nb + b] = len;
+        }
+      }
+    }
+  }
+  V[t] = leafv;
+  const int top = s_maxe;
+  const int lhi = max(top - 1, min(c0, L - 1));
+  __syncthreads();
+
+  // bottom-up over the internal heads, level by level
+  for (int l = lhi; l >= lca; l--) {
+    if ((mI[l][w] >> lane) & 1u)
+      list[preI[l][w] + __popc(mI[l][w] & ((1u << lane) - 1u))] = (short)t;
+    __syncthreads();
+    if (t < preI[l][kSW]) {
+      const int j = list[t];
+      const int p = next_bit(mB[l], nzB[l], j);
+      double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
+      for (int q = j; q < p; q = next_bit(mH[l + 1], nzH[l + 1], q)) add4(v, V[q]);
+      V[j] = v;  // ranges are disjoint: nobody else reads V[j] at this level
+      const bool local = p < kST || cend < l;
+      if (j == 0 && l <= c0) {
+        cr.pl[l * nb + b] = v;
+        cr.plend[l * nb + b] = local ? p : -1;
+      } else if (local) {
+        write_records_a(r, l + nn - offs[p], v);
+      } else {
+        cr.pr[l * nb + b] = v;
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) {  // levels above lca: position 0's nodes, one child each
+    double4 v = V[0];
+    for (int l = lhi >= lca ? lca - 1 : L; l >= 0; l--) {
+      const bool reg = has && s <= l && l <= e;
+      const bool pse = l <= c0;
+      if (!reg && !pse) continue;
+      if (reg && l == e) {
+        v = leafv;  // (its records are written)
+        continue;
+      }
+      if (pse && l == L) v = make_double4(0.0, 0.0, 0.0, 0.0);  // a duplicate run owned earlier
+      else v = make_double4(__dadd_rn(0.0, v.x), __dadd_rn(0.0, v.y), __dadd_rn(0.0, v.z),
+                            __dadd_rn(0.0, v.w));  // the one-child fold
+      const bool local = cend < l;
+      if (pse) {
+        cr.pl[l * nb + b] = v;
+        cr.plend[l * nb + b] = local ? (int)(n - B0 < kST ? n - B0 : (int64_t)kST) : -1;  // (the last block ends at n)
+      } else if (local) {
+        write_records_a(r, l + nn - offs[kST], v);
+      } else {
+        cr.pr[l * nb + b] = v;
+      }
+    }
+  }
 }
 
-// Level l of the bottom-up summary (bhtree.py:77-83), levels L-1..0 in
-// order, over the level's internal nodes: the children of internal node k are
-// the BFS range [fc_k, fc_{k+1}) one level down (the last one's ends with the
-// level), summed in slot order -- a fixed order, independent of scheduling.
-// The node's traversal records are written here too, at its mirrored index.
-// subtree size = 1 + the children's (preorder skip = x + size)
-__device__ __forceinline__ void sum_internal(int l, int k, int e, int lend, int n_nodes,
-                                             const InNode* __restrict__ in,
-                                             double4* __restrict__ sums, int* __restrict__ sizep,
-                                             const TreeRecords& r) {
-  const InNode nd = in[k];
-  const int cend = k + 1 < e ? in[k + 1].fc : lend;
-  double ms = 0.0, mc[3] = {0.0, 0.0, 0.0};
-  int size = 1;
-  for (int ch = nd.fc; ch < cend; ch++) {
-    const double4 v = sums[ch];
-    ms = __dadd_rn(ms, v.x);
-    mc[0] = __dadd_rn(mc[0], v.y);
-    mc[1] = __dadd_rn(mc[1], v.z);
-    mc[2] = __dadd_rn(mc[2], v.w);
-    size += sizep[ch];
+// Dyadic sums (per level) and minima over aligned runs of 2^k blocks, one
+// block per level (blockIdx.x == L + 1: the minima); fixed shape.
+__global__ void __launch_bounds__(1024) k_hier(int L, int nb, Cross cr) {
+  const int l = blockIdx.x;
+  for (int k = 1; k <= cr.K; k++) {
+    const int sz = (nb + (1 << k) - 1) >> k, psz = (nb + (1 << (k - 1)) - 1) >> (k - 1);
+    for (int j = threadIdx.x; j < sz; j += blockDim.x) {
+      const int a = 2 * j, b2 = 2 * j + 1;
+      if (l <= L) {
+        const double4* src = k == 1 ? cr.pl + (int64_t)l * nb : cr.hs + (int64_t)l * cr.hn + cr.ho[k - 1];
+        double4 v = src[a];
+        if (b2 < psz) add4(v, src[b2]);
+        cr.hs[(int64_t)l * cr.hn + cr.ho[k] + j] = v;
+      } else {
+        const int* src = k == 1 ? cr.mn : cr.hm + cr.ho[k - 1];
+        cr.hm[cr.ho[k] + j] = b2 < psz ? min(src[a], src[b2]) : src[a];
+      }
+    }
+    __syncthreads();
   }
-  sums[nd.pos] = make_double4(ms, mc[0], mc[1], mc[2]);
-  sizep[nd.pos] = size;
-  const int mir = l + n_nodes - (nd.x + size);
-  write_records(r, mir, mir + size, false, nd.len, ms, mc);
 }
 
-// one large level over the whole grid
-__global__ void __launch_bounds__(256) k_sum_level(int l, const int* __restrict__ lvl_off,
-                                                   const int* __restrict__ ilvl_off, int n_nodes,
-                                                   const InNode* __restrict__ in,
-                                                   double4* __restrict__ sums,
-                                                   int* __restrict__ sizep, TreeRecords r) {
-  const int b = ilvl_off[l], e = ilvl_off[l + 1], lend = lvl_off[l + 2];
-  for (int k = b + blockIdx.x * blockDim.x + threadIdx.x; k < e; k += gridDim.x * blockDim.x)
-    sum_internal(l, k, e, lend, n_nodes, in, sums, sizep, r);
+__device__ __forceinline__ int hier_min(const Cross& cr, int k, int j) {
+  return k == 0 ? cr.mn[j] : cr.hm[cr.ho[k] + j];
 }
 
-// consecutive small levels l_hi..l_lo (descending) in one block
-__global__ void __launch_bounds__(1024) k_sum_levels_small(int l_hi, int l_lo,
-                                                           const int* __restrict__ lvl_off,
-                                                           const int* __restrict__ ilvl_off,
-                                                           int n_nodes,
-                                                           const InNode* __restrict__ in,
-                                                           double4* __restrict__ sums,
-                                                           int* __restrict__ sizep,
-                                                           TreeRecords r) {
-  for (int l = l_hi; l >= l_lo; l--) {
-    const int b = ilvl_off[l], e = ilvl_off[l + 1], lend = lvl_off[l + 2];
-    for (int k = b + threadIdx.x; k < e; k += blockDim.x)
-      sum_internal(l, k, e, lend, n_nodes, in, sums, sizep, r);
-    __syncthreads();  // level l complete before its parents
+// One thread per (level, block) with an owned crossing node: the block where
+// it ends (first later block with mn < l, by the dyadic minima), its partials
+// over the blocks after its own (the canonical dyadic cover, left to right),
+// and its records.
+__global__ void __launch_bounds__(256) k_crossing(int L, int nb, int64_t n,
+                                                  const int* __restrict__ offset, Cross cr,
+                                                  TreeRecords r) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= (int64_t)(L + 1) * nb) return;
+  const int l = (int)(g / nb), b = (int)(g % nb);
+  const int x = cr.prx[l * nb + b];
+  if (x < 0) return;
+  // end block: first bb > b with mn[bb] < l
+  int p = b + 1, k = 0;
+  while (true) {
+    while (k < cr.K && (p & ((2 << k) - 1)) == 0 && hier_min(cr, k + 1, p >> (k + 1)) >= l) k++;
+    if (hier_min(cr, k, p >> k) >= l) {
+      p += 1 << k;
+      continue;
+    }
+    break;
   }
+  while (k > 0) {
+    k--;
+    if (hier_min(cr, k, p >> k) >= l) p += 1 << k;
+  }
+  const int bend = p;
+  double4 v = cr.pr[l * nb + b];
+  for (int q = b + 1; q <= bend;) {
+    int kk = min(__ffs(q) - 1, cr.K);
+    while (q + (1 << kk) - 1 > bend) kk--;
+    add4(v, kk == 0 ? cr.pl[l * nb + q] : cr.hs[(int64_t)l * cr.hn + cr.ho[kk] + (q >> kk)]);
+    q += 1 << kk;
+  }
+  const int64_t end = (int64_t)bend * kST + cr.plend[l * nb + bend];
+  const int nn = offset[n];
+  const int skipp = offset[end];
+  const int mir = l + nn - skipp;
+  write_records_b(r, mir, mir + (skipp - x), false, cr.prlen[l * nb + b]);
+  write_records_a(r, mir, v);
 }
 
 // first p in [0, to) with keys[p] >= bound, galloping backwards from `to`
@@ -629,27 +725,27 @@ __device__ __forceinline__ int64_t lower_bound_gallop(const unsigned long long* 
 }
 
 // The reference's preorder arrays (bhtree.py:14-45), re-derived per chain
-// node exactly as k_emit does; each node registers itself in its parent's
-// child slot (parent: the chain's previous node, or found by a backwards
-// search for the start of the parent's key prefix).  children must be -1
-// filled.  Export only, not on the registration path.
-__global__ void __launch_bounds__(kLT) k_export(const unsigned long long* __restrict__ keys,
-                                                     int64_t n, int L,
-                                                     const signed char* __restrict__ clev,
-                                                     const int* __restrict__ offset,
-                                                     const int* __restrict__ boff,
-                                                     const int* __restrict__ lvl_off,
-                                                     const double* __restrict__ box,
-                                                     const double4* __restrict__ sums,
-                                                     long long* children, double* com,
-                                                     double* mass, double* length,
-                                                     long long* occupancy, long long* depth,
-                                                     double* bmin, double* bmax) {
-  __shared__ BlockRanks R;
+// node as k_subtrees does; mass and com are read back from the node's fp64
+// record (mirrored index l + n_nodes - offset[end]).  Each node registers
+// itself in its parent's child slot (parent: the chain's previous node, or
+// found by a backwards search for the start of the parent's key prefix).
+// children must be -1 filled.  Export only, not on the registration path.
+__global__ void __launch_bounds__(256) k_export(const unsigned long long* __restrict__ keys,
+                                                int64_t n, int L,
+                                                const signed char* __restrict__ clev,
+                                                const int* __restrict__ offset,
+                                                const double* __restrict__ box,
+                                                const double4* __restrict__ a64,
+                                                long long* children, double* com,
+                                                double* mass, double* length,
+                                                long long* occupancy, long long* depth,
+                                                double* bmin, double* bmax) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const Chain c = chain_of(clev, i, n, L);
-  block_ranks(R, c, L);
-  if (c.s > c.e) return;
+  if (i >= n) return;
+  const int s = clev[i] + 1, cn = clev[i + 1];
+  if (s > L) return;
+  const int e = chain_end(s, cn, L);
+  const int nn = offset[n];
   const unsigned long long k = keys[i];
   const int base = offset[i];
   double lo[3], hi[3];
@@ -658,38 +754,31 @@ __global__ void __launch_bounds__(kLT) k_export(const unsigned long long* __rest
     lo[a] = box[a];
     hi[a] = box[3 + a];
   }
-  for (int l = 0; l <= c.e; l++) {
+  for (int l = 0; l <= e; l++) {
     if (l > 0) bbox_step(k, l, L, lo, hi);
-    if (l < c.s) continue;
+    if (l < s) continue;
     int64_t end;
     if (l == 0) end = n;
-    else if (l > c.cn) end = i + 1;
+    else if (l > cn) end = i + 1;
     else end = upper_bound_gallop(keys, i + 1, n, k | low_mask(3 * (L - l)));
-    const int64_t x = base + (l - c.s);
-    const double4 v = sums[level_slot(R, 0, l, L, lvl_off, boff)];
-    if (mass) mass[x] = v.x;
+    const int64_t x = base + (l - s);
+    const double4 v = a64[l + nn - offset[end]];
+    if (mass) mass[x] = v.w;
     if (com) {
-      com[x * 3] = __ddiv_rn(v.y, v.x);
-      com[x * 3 + 1] = __ddiv_rn(v.z, v.x);
-      com[x * 3 + 2] = __ddiv_rn(v.w, v.x);
+      com[x * 3] = v.x;
+      com[x * 3 + 1] = v.y;
+      com[x * 3 + 2] = v.z;
     }
     if (occupancy) occupancy[x] = end - i;
     if (depth) depth[x] = l;
-    if (length) {
-      double sq = 0.0;
-      for (int a = 0; a < 3; a++) {
-        const double ex = __dsub_rn(hi[a], lo[a]);
-        sq = __dadd_rn(sq, __dmul_rn(ex, ex));
-      }
-      length[x] = __dsqrt_rn(sq);
-    }
+    if (length) length[x] = diag_len(lo, hi);
     for (int a = 0; a < 3; a++) {
       if (bmin) bmin[x * 3 + a] = lo[a];
       if (bmax) bmax[x * 3 + a] = hi[a];
     }
     if (children && l > 0) {
       int64_t parent;
-      if (l > c.s) {
+      if (l > s) {
         parent = x - 1;
       } else {
         const int64_t p = lower_bound_gallop(keys, i, k & ~low_mask(3 * (L - l + 1)));
@@ -740,13 +829,8 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   FGA_CUDA_TRY(T.clev.reserve(n + 1));
   FGA_CUDA_TRY(T.count.reserve(sizeof(int) * (n + 1)));
   FGA_CUDA_TRY(T.offset.reserve(sizeof(int) * (n + 1)));
-  const int nbl = blocks_for(n + 1, kLT);
-  FGA_CUDA_TRY(T.bcount.reserve(sizeof(int) * (int64_t)2 * (L + 1) * nbl));
-  FGA_CUDA_TRY(T.lvl.reserve(sizeof(int) * (kLvlInts + 1)));
-  int* row_total = T.lvl.as<int>();
-  int* lvl_off = row_total + 2 * (kMaxLevels + 1);
-  int* ilvl_off = lvl_off + (kMaxLevels + 3);
-  int* overflow = T.lvl.as<int>() + kLvlInts;
+  FGA_CUDA_TRY(T.lvl.reserve(sizeof(int) * 2));
+  int* overflow = T.lvl.as<int>();
   {
     size_t b32 = 0, b64 = 0, bscan = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b32, T.keys32_in.as<unsigned>(), T.keys32.as<unsigned>(),
@@ -772,33 +856,28 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
     k_fixup_runs<<<blocks_for(n), kThreads, 0, st>>>(T.keys32.as<unsigned>(), n,
                                                      T.keys.as<unsigned long long>(),
                                                      T.idx.as<int>(), T.sp.as<double4>(), overflow);
-  // levels, per-level block counts, preorder offsets (rerun after a fallback)
+  // c_i, node counts, preorder offsets (rerun after a fallback)
   auto levels = [&]() -> int {
-    k_levels<<<nbl, kLT, 0, st>>>(T.keys.as<unsigned long long>(), n, L,
-                                       T.clev.as<signed char>(), T.count.as<int>(),
-                                       T.bcount.as<int>());
-    k_level_scan<<<2 * (L + 1), 1024, 0, st>>>(T.bcount.as<int>(), nbl, row_total);
-    k_level_offsets<<<1, 32, 0, st>>>(row_total, L, lvl_off, ilvl_off);
+    k_count<<<blocks_for(n + 1), kThreads, 0, st>>>(T.keys.as<unsigned long long>(), n, L,
+                                                    T.clev.as<signed char>(), T.count.as<int>());
     size_t sb = T.cub_tmp.bytes;
     FGA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(T.cub_tmp.p, sb, T.count.as<int>(),
                                                T.offset.as<int>(), (int)(n + 1), st));
     return FGA_OK;
   };
   TRY_RC(levels());
-  // node count, per-level counts, run overflow and root box to the host
-  // (one sync per build)
-  int nn = 0;
+  // node count, run overflow and root box to the host (one sync per build)
+  int nn = 0, ovf = 0;
   double box[6];
-  int lvl_host[kLvlInts + 1];
   auto fetch = [&]() -> int {
     FGA_CUDA_TRY(cudaMemcpyAsync(&nn, T.offset.as<int>() + n, sizeof(int), cudaMemcpyDeviceToHost, st));
     FGA_CUDA_TRY(cudaMemcpyAsync(box, T.box.p, sizeof(box), cudaMemcpyDeviceToHost, st));
-    FGA_CUDA_TRY(cudaMemcpyAsync(lvl_host, T.lvl.p, sizeof(lvl_host), cudaMemcpyDeviceToHost, st));
+    FGA_CUDA_TRY(cudaMemcpyAsync(&ovf, overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
     FGA_CUDA_TRY(cudaStreamSynchronize(st));
     return FGA_OK;
   };
   TRY_RC(fetch());
-  if (lvl_host[kLvlInts]) {  // a long run of equal top bits: full 64-bit sort
+  if (ovf) {  // a long run of equal top bits: full 64-bit sort
     FGA_CUDA_TRY(T.keys_in.reserve(sizeof(unsigned long long) * n));
     k_keys<<<blocks_for(n), kThreads, 0, st>>>(pts_dev, masses_dev, n, T.box.as<double>(), L, 0,
                                                nullptr, T.keys_in.as<unsigned long long>(),
@@ -819,36 +898,41 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   for (int k = 0; k < 6; k++) T.box_host[k] = box[k];
 
   const int64_t nn64 = nn;
-  FGA_CUDA_TRY(T.inodes.reserve(sizeof(InNode) * nn64));
-  FGA_CUDA_TRY(T.sums.reserve(sizeof(double4) * nn64));
-  FGA_CUDA_TRY(T.sizep.reserve(sizeof(int) * nn64));
   FGA_CUDA_TRY(T.a32.reserve(sizeof(float4) * nn64));
   FGA_CUDA_TRY(T.b32.reserve(sizeof(NodeB32) * nn64));
   FGA_CUDA_TRY(T.a64.reserve(sizeof(double4) * nn64));
   FGA_CUDA_TRY(T.b64.reserve(sizeof(NodeB64) * nn64));
-
-  k_emit<<<nbl, kLT, 0, st>>>(T.keys.as<unsigned long long>(), n, L, T.clev.as<signed char>(),
-                                   T.offset.as<int>(), T.bcount.as<int>(), lvl_off, ilvl_off,
-                                   T.box.as<double>(), nn, T.sp.as<double4>(),
-                                   T.inodes.as<InNode>(), T.sums.as<double4>(), T.sizep.as<int>(),
-                                   T.records());
-  // levels L-1..0 bottom-up (level L holds leaves only): a level with many
-  // internal nodes gets its own grid; runs of small levels share one block
-  const int* internal = lvl_host + (L + 1);  // row totals, internal nodes per level
-  constexpr int kSmall = 2048;
-  for (int l = L - 1; l >= 0;) {
-    if (internal[l] > kSmall) {
-      const int grid = (int)std::min<int64_t>(blocks_for(internal[l]), 148 * 8);
-      k_sum_level<<<grid, 256, 0, st>>>(l, lvl_off, ilvl_off, nn, T.inodes.as<InNode>(),
-                                        T.sums.as<double4>(), T.sizep.as<int>(), T.records());
-      l--;
-      continue;
-    }
-    int lo = l;
-    while (lo - 1 >= 0 && internal[lo - 1] <= kSmall) lo--;
-    k_sum_levels_small<<<1, 1024, 0, st>>>(l, lo, lvl_off, ilvl_off, nn, T.inodes.as<InNode>(),
-                                           T.sums.as<double4>(), T.sizep.as<int>(), T.records());
-    l = lo - 1;
+  const int nbs = (int)((n + kST - 1) / kST);
+  const int64_t ncr = (int64_t)(L + 1) * nbs;
+  Cross cr{};
+  cr.K = 0;
+  while ((1ll << cr.K) < nbs) cr.K++;
+  cr.hn = 0;
+  for (int k = 1; k <= cr.K; k++) {
+    cr.ho[k] = cr.hn;
+    cr.hn += (nbs + (1 << k) - 1) >> k;
+  }
+  FGA_CUDA_TRY(T.cross.reserve(ncr * (2 * sizeof(double4) + sizeof(double) + 2 * sizeof(int)) +
+                               sizeof(int) * nbs + sizeof(double4) * (L + 1) * (int64_t)cr.hn +
+                               sizeof(int) * cr.hn + 64));
+  {
+    char* q = T.cross.as<char>();
+    cr.pr = (double4*)q; q += sizeof(double4) * ncr;
+    cr.pl = (double4*)q; q += sizeof(double4) * ncr;
+    cr.hs = (double4*)q; q += sizeof(double4) * (L + 1) * (int64_t)cr.hn;
+    cr.prlen = (double*)q; q += sizeof(double) * ncr;
+    cr.prx = (int*)q; q += sizeof(int) * ncr;
+    cr.plend = (int*)q; q += sizeof(int) * ncr;
+    cr.mn = (int*)q; q += sizeof(int) * nbs;
+    cr.hm = (int*)q;
+  }
+  k_subtrees<<<nbs, kST, 0, st>>>(T.keys.as<unsigned long long>(), n, L, T.clev.as<signed char>(),
+                                  T.offset.as<int>(), T.box.as<double>(), T.sp.as<double4>(),
+                                  T.records(), cr, nbs);
+  if (nbs > 1) {
+    k_hier<<<L + 2, 1024, 0, st>>>(L, nbs, cr);
+    k_crossing<<<(int)((ncr + 255) / 256), 256, 0, st>>>(L, nbs, n, T.offset.as<int>(), cr,
+                                                         T.records());
   }
   FGA_CUDA_TRY(cudaGetLastError());
   T.exportable = true;
@@ -876,10 +960,9 @@ int tree_export_host(TreeDev& T, cudaStream_t st, int64_t* children, double* com
   double* d_bmin = (double*)p; p += sizeof(double) * 3 * nn;
   double* d_bmax = (double*)p;
   if (children) FGA_CUDA_TRY(cudaMemsetAsync(d_children, 0xff, sizeof(long long) * 8 * nn, st));
-  const int* lvl_off = T.lvl.as<int>() + 2 * (kMaxLevels + 1);
-  k_export<<<blocks_for(T.n_points + 1, kLT), kLT, 0, st>>>(
+  k_export<<<blocks_for(T.n_points), 256, 0, st>>>(
       T.keys.as<unsigned long long>(), T.n_points, T.L, T.clev.as<signed char>(),
-      T.offset.as<int>(), T.bcount.as<int>(), lvl_off, T.box.as<double>(), T.sums.as<double4>(),
+      T.offset.as<int>(), T.box.as<double>(), T.a64.as<double4>(),
       children ? d_children : nullptr, com ? d_com : nullptr, mass ? d_mass : nullptr,
       length ? d_len : nullptr, occupancy ? d_occ : nullptr, depth ? d_depth : nullptr,
       bmin ? d_bmin : nullptr, bmax ? d_bmax : nullptr);
