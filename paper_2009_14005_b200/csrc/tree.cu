@@ -394,8 +394,12 @@ __device__ __forceinline__ void write_records_a(const TreeRecords& r, int mir, c
 // that block, a crossing child contributing its own partial); k_crossing adds
 // them in a fixed dyadic shape.  Every result is a fixed function of the input
 // (kST is a constant), whatever the scheduling.
-constexpr int kST = 512;
+#ifndef FGA_KST
+#define FGA_KST 128
+#endif
+constexpr int kST = FGA_KST;
 constexpr int kSW = kST / 32;
+constexpr int kSTBlocks = 1024 / kST;  // resident blocks per SM at 64 registers
 
 // Per (level, block) boundary partials, SoA by level (index l * nb + b):
 //   pr/prx/prlen: the node owned by block b (starting in it) that runs past
@@ -436,53 +440,78 @@ __device__ __forceinline__ int next_bit(const unsigned* __restrict__ m, unsigned
   return (w2 << 5) + __ffs(m[w2]) - 1;
 }
 
+// last set bit at a position <= j of a kST-bit mask (nz: its non-zero words);
+// the caller guarantees one exists
+__device__ __forceinline__ int prev_bit_incl(const unsigned* __restrict__ m, unsigned nz, int j) {
+  const int wd = j >> 5;
+  const unsigned v = m[wd] & (0xffffffffu >> (31 - (j & 31)));
+  if (v) return (wd << 5) + 31 - __clz(v);
+  const int w2 = 31 - __clz(nz & ((1u << wd) - 1u));
+  return (w2 << 5) + 31 - __clz(m[w2]);
+}
+
+// number of set bits at positions [a, b) of a kST-bit mask
+__device__ __forceinline__ int count_bits(const unsigned* __restrict__ m, int a, int b) {
+  if (a >= b) return 0;
+  const int wa = a >> 5, wb = (b - 1) >> 5;
+  const unsigned lo = ~0u << (a & 31), hi = 0xffffffffu >> (31 - ((b - 1) & 31));
+  if (wa == wb) return __popc(m[wa] & lo & hi);
+  int c = __popc(m[wa] & lo) + __popc(m[wb] & hi);
+  for (int q = wa + 1; q < wb; q++) c += __popc(m[q]);
+  return c;
+}
+
 // One block = kST sorted points, one thread each.  Per level l, bit masks
 // over the block's points: B_l (c_j < l: a node at level <= l starts at j, so
-// it ends every level-l range), H_l (a level-l node starts at j, or j = 0 and
-// the level-l node covering it started earlier -- the "pseudo head") and I_l
-// (the internal ones among H_l).  All the block's points share the levels <=
-// lca (the common levels of its first and last key): below lca only position
-// 0 has nodes, each with one child, so thread 0 walks them alone.
-//   top-down, every thread: its chain (bhtree.py:90-103 bbox replay from the
-//     shared level-lca box -> length; skip = offset[end]) -> structural
-//     records; its leaf's sums (:78-82) -> the leaf's aggregate record;
-//   bottom-up, per level lhi..lca: the level's internal heads, compacted to
-//     the first threads, fold their children (the H_{l+1} bits inside their
-//     range, in slot order) from shared memory.  Level-l ranges are
-//     disjoint, so the in-place update needs no more than the level barrier.
-__global__ void __launch_bounds__(kST, 2) k_subtrees(const unsigned long long* __restrict__ keys,
+// it ends every level-l range) and H_l (a level-l node starts at j, or j = 0
+// and the level-l node covering it started earlier -- the "pseudo head").
+// All the block's points share the levels <= lca (the common levels of its
+// first and last key), so above lca only position 0 has nodes, one child each.
+//   leaves: every thread sums its chain's leaf (bhtree.py:78-82);
+//   top-down, one node per thread: bbox replay from the shared level-lca box
+//     (bhtree.py:90-103) -> length, skip = offset[end] -> structural record;
+//   bottom-up, no barriers: each thread climbs from its leaf; a node's
+//     children report to a per-(level, head) counter and the last one to
+//     arrive folds them in slot order (starting from 0.0) and climbs on.
+__global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long long* __restrict__ keys,
                                                      int64_t n, int L,
                                                      const signed char* __restrict__ clev,
                                                      const int* __restrict__ offset,
                                                      const double* __restrict__ box,
                                                      const double4* __restrict__ sp,
                                                      TreeRecords r, Cross cr, int nb) {
-  __shared__ unsigned mB[kMaxLevels + 2][kSW], mH[kMaxLevels + 2][kSW], mI[kMaxLevels + 2][kSW];
+  __shared__ unsigned mB[kMaxLevels + 2][kSW], mH[kMaxLevels + 2][kSW];
   __shared__ unsigned nzB[kMaxLevels + 2], nzH[kMaxLevels + 2];
-  __shared__ unsigned short preI[kMaxLevels + 2][kSW + 1];
-  __shared__ short list[kST];
+  __shared__ int arrived[kMaxLevels + 1][kST];
   __shared__ int offs[kST + 1];
   __shared__ signed char cs[kST + 1];
+  __shared__ unsigned long long skey[kST];
   __shared__ double4 V[kST];
   __shared__ double pbox[6];
-  __shared__ int s_maxe, s_mn;
+  __shared__ int s_maxe, s_mn, s_q;
+  constexpr int kMap = 4 * kST;  // node -> point map of the top-down pass
+  __shared__ short nmap[kMap];
+  __shared__ double4 qv[kST];  // queued aggregate records of the climb
+  __shared__ int qmir[kST];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5, b = blockIdx.x;
   const int64_t B0 = (int64_t)b * kST, i = B0 + t;
   const int64_t last = min(B0 + kST, n) - 1;
   const int nn = offset[n];
   cs[t] = i <= n ? clev[i] : (signed char)-1;
   offs[t] = i <= n ? offset[i] : nn;
+  skey[t] = i < n ? keys[i] : 0ull;
   if (t == 0) {
     const int64_t j = B0 + kST;
     cs[kST] = j <= n ? clev[j] : (signed char)-1;
     offs[kST] = j <= n ? offset[j] : nn;
     s_maxe = -1;
     s_mn = kMaxLevels + 1;
+    s_q = 0;
   }
   if (t <= L) cr.prx[t * nb + b] = -1;
-  const unsigned long long k0 = keys[B0];
-  const int lca = last > B0 ? common_levels(k0, keys[last], L) : L;
   __syncthreads();
+  const unsigned long long k0 = skey[0];
+  const int lca = last > B0 ? common_levels(k0, skey[last - B0], L) : L;
   const int c = cs[t], c0 = cs[0], cend = cs[kST];
   const bool has = i < n && c + 1 <= L;
   const int s = c + 1, e = has ? chain_end(s, cs[t + 1], L) : -1;
@@ -504,72 +533,91 @@ __global__ void __launch_bounds__(kST, 2) k_subtrees(const unsigned long long* _
       pbox[3 + a] = hi[a];
     }
   }
-  for (int l = lca; l <= L + 1; l++) {
+  // leaf sums (bhtree.py:78-82) and the leaf's aggregate record
+  double4 leafv = make_double4(0.0, 0.0, 0.0, 0.0);
+  if (has) {
+    int64_t end;  // point i alone, or a depth-cap cell of duplicates
+    if (e > cs[t + 1]) end = i + 1;
+    else if (e == 0) end = n;
+    else end = upper_bound_gallop(keys, i + 1, n, skey[t] | low_mask(3 * (L - e)));
+    leafv = leaf_sums(sp, i, end - i);
+    write_records_a(r, e + nn - (offs[t] + (e - s) + 1), leafv);
+    const int x0 = offs[t] - offs[0];
+    if (x0 + (e - s) < kMap)
+      for (int q = 0; q <= e - s; q++) nmap[x0 + q] = (short)t;
+  }
+  V[t] = leafv;
+  __syncthreads();
+  const int top = s_maxe;
+  const int mtop = max(top, min(c0, L));  // deepest level with a head
+  for (int l = lca; l <= mtop; l++) {
     const bool ph = t == 0 && l <= c0;
     const unsigned bb = __ballot_sync(0xffffffffu, c < l);
     const unsigned bh = __ballot_sync(0xffffffffu, (has && s <= l && l <= e) || ph);
-    const unsigned bi = __ballot_sync(0xffffffffu, (has && s <= l && l < e) || (ph && l < L));
     if (lane == 0) {
       mB[l][w] = bb;
       mH[l][w] = bh;
-      mI[l][w] = bi;
     }
   }
+  for (int l = lca; l < mtop; l++) arrived[l][t] = 0;
   __syncthreads();
-  if (t >= lca && t <= L + 1) {  // per level: non-zero word summaries, internal-head word prefix
-    unsigned zb = 0, zh = 0, acc = 0;
+  if (t >= lca && t <= mtop) {  // per level: non-zero word summaries
+    unsigned zb = 0, zh = 0;
     for (int q = 0; q < kSW; q++) {
       zb |= (mB[t][q] != 0u ? 1u : 0u) << q;
       zh |= (mH[t][q] != 0u ? 1u : 0u) << q;
-      preI[t][q] = (unsigned short)acc;
-      acc += __popc(mI[t][q]);
     }
     nzB[t] = zb;
     nzH[t] = zh;
-    preI[t][kSW] = (unsigned short)acc;
   }
   __syncthreads();
   if (t == 0) cr.mn[b] = s_mn;
 
-  // top-down: structural records (and the length / preorder index of a node
-  // that runs past the block; k_crossing writes its records), leaf sums
-  double4 leafv = make_double4(0.0, 0.0, 0.0, 0.0);
-  if (has) {
-    const unsigned long long key = keys[i];
-    const int x0 = offs[t] - s;  // preorder index of (i, l) = x0 + l
-    double lo[3], hi[3];
-    int lv;
-    if (s <= lca) {  // (thread 0 only: the other points start below lca)
-      lv = 0;
-#pragma unroll
-      for (int a = 0; a < 3; a++) {
-        lo[a] = box[a];
-        hi[a] = box[3 + a];
+  // top-down, one node per thread (the block's nodes are the preorder range
+  // [offs[0], offs[kST])); a node that runs past the block leaves its length
+  // and preorder index to k_crossing
+  {
+    const int offs0 = offs[0], nbn = offs[kST] - offs0;
+    for (int kk = t; kk < nbn; kk += kST) {
+      const int x = offs0 + kk;
+      int j;  // the point whose chain holds node x
+      if (nbn <= kMap) {
+        j = nmap[kk];
+      } else {
+        int lo_ = 0, hi_ = kST;
+        while (hi_ - lo_ > 1) {
+          const int mid = (lo_ + hi_) >> 1;
+          if (offs[mid] <= x) lo_ = mid; else hi_ = mid;
+        }
+        j = lo_;
       }
-    } else {
-      lv = lca;
+      const int sj = cs[j] + 1, ej = chain_end(sj, cs[j + 1], L);
+      const int l = sj + (x - offs[j]);
+      const unsigned long long key = skey[j];
+      double bl[3], bh[3];
+      int lv;
+      if (l <= lca) {  // (position 0 only: the other points start below lca)
+        lv = 0;
 #pragma unroll
-      for (int a = 0; a < 3; a++) {
-        lo[a] = pbox[a];
-        hi[a] = pbox[3 + a];
+        for (int a = 0; a < 3; a++) {
+          bl[a] = box[a];
+          bh[a] = box[3 + a];
+        }
+      } else {
+        lv = lca;
+#pragma unroll
+        for (int a = 0; a < 3; a++) {
+          bl[a] = pbox[a];
+          bh[a] = pbox[3 + a];
+        }
       }
-    }
-    // the chain's leaf (i, e): point i alone, or a depth-cap cell of duplicates
-    int64_t end;
-    if (e > cs[t + 1]) end = i + 1;
-    else if (e == 0) end = n;
-    else end = upper_bound_gallop(keys, i + 1, n, key | low_mask(3 * (L - e)));
-    leafv = leaf_sums(sp, i, end - i);
-    for (int l = s; l <= e; l++) {
-      while (lv < l) bbox_step(key, ++lv, L, lo, hi);
-      const double len = diag_len(lo, hi);
-      const int x = x0 + l;
-      if (l == e) {
+      while (lv < l) bbox_step(key, ++lv, L, bl, bh);
+      const double len = diag_len(bl, bh);
+      if (l == ej) {
         const int mir = l + nn - (x + 1);
         write_records_b(r, mir, mir + 1, true, len);
-        write_records_a(r, mir, leafv);
       } else {
-        const int p = l <= lca ? kST : next_bit(mB[l], nzB[l], t);
+        const int p = l <= lca ? kST : next_bit(mB[l], nzB[l], j);
         if (p < kST || cend < l) {
           const int skipp = offs[p];
           const int mir = l + nn - skipp;
@@ -581,49 +629,67 @@ __global__ void __launch_bounds__(kST, 2) k_subtrees(const unsigned long long* _
       }
     }
   }
-  V[t] = leafv;
-  const int top = s_maxe;
-  const int lhi = max(top - 1, min(c0, L - 1));
-  __syncthreads();
 
-  // bottom-up over the internal heads, level by level
-  for (int l = lhi; l >= lca; l--) {
-    if ((mI[l][w] >> lane) & 1u)
-      list[preI[l][w] + __popc(mI[l][w] & ((1u << lane) - 1u))] = (short)t;
-    __syncthreads();
-    if (t < preI[l][kSW]) {
-      const int j = list[t];
-      const int p = next_bit(mB[l], nzB[l], j);
-      double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
-      for (int q = j; q < p; q = next_bit(mH[l + 1], nzH[l + 1], q)) add4(v, V[q]);
-      V[j] = v;  // ranges are disjoint: nobody else reads V[j] at this level
-      const bool local = p < kST || cend < l;
-      if (j == 0 && l <= c0) {
-        cr.pl[l * nb + b] = v;
-        cr.plend[l * nb + b] = local ? p : -1;
-      } else if (local) {
-        write_records_a(r, l + nn - offs[p], v);
-      } else {
-        cr.pr[l * nb + b] = v;
+  // bottom-up.  A climb starts at every leaf: the thread's own, and at
+  // position 0 the depth-cap duplicate run owned by an earlier block (its
+  // value here is 0).
+  int pos = t, lev = has ? e : (t == 0 && c0 == L ? L : -1);
+  double4 v = leafv;
+  bool up = lev >= 0;
+  while (up && lev > lca) {
+    const int pl = lev - 1;
+    const int hp = prev_bit_incl(mH[pl], nzH[pl], pos);  // the parent's head
+    const int pend = next_bit(mB[pl], nzB[pl], hp);       // ... and range end
+    const int nch = count_bits(mH[lev], hp, pend);
+    __threadfence_block();  // this child's V before the arrival
+    if (atomicAdd(&arrived[pl][hp], 1) != nch - 1) {
+      up = false;
+      break;
+    }
+    __threadfence_block();  // every child's V after it
+    v = make_double4(0.0, 0.0, 0.0, 0.0);
+    {  // children: the H_lev bits in [hp, pend), in slot order
+      const unsigned* mh = mH[lev];
+      int wd = hp >> 5;
+      unsigned m = mh[wd] & (~0u << (hp & 31));
+      while (true) {
+        while (m) {
+          const int q = (wd << 5) + __ffs(m) - 1;
+          if (q >= pend) break;
+          add4(v, V[q]);
+          m &= m - 1u;
+        }
+        if (++wd >= kSW || (wd << 5) >= pend) break;
+        m = mh[wd];
       }
     }
-    __syncthreads();
-  }
-  if (t == 0) {  // levels above lca: position 0's nodes, one child each
-    double4 v = V[0];
-    for (int l = lhi >= lca ? lca - 1 : L; l >= 0; l--) {
-      const bool reg = has && s <= l && l <= e;
-      const bool pse = l <= c0;
-      if (!reg && !pse) continue;
-      if (reg && l == e) {
-        v = leafv;  // (its records are written)
-        continue;
+    V[hp] = v;
+    const bool local = pend < kST || cend < pl;
+    if (hp == 0 && pl <= c0) {
+      cr.pl[pl * nb + b] = v;
+      cr.plend[pl * nb + b] = local ? pend : -1;
+    } else if (local) {  // queued: the divisions run compacted after the climb
+      const int slot = atomicAdd(&s_q, 1);
+      if (slot < kST) {
+        qv[slot] = v;
+        qmir[slot] = pl + nn - offs[pend];
+      } else {
+        write_records_a(r, pl + nn - offs[pend], v);
       }
-      if (pse && l == L) v = make_double4(0.0, 0.0, 0.0, 0.0);  // a duplicate run owned earlier
-      else v = make_double4(__dadd_rn(0.0, v.x), __dadd_rn(0.0, v.y), __dadd_rn(0.0, v.z),
-                            __dadd_rn(0.0, v.w));  // the one-child fold
+    } else {
+      cr.pr[pl * nb + b] = v;
+    }
+    pos = hp;
+    lev = pl;
+  }
+  if (up) {  // this thread holds position 0's node at level lev <= lca; each
+             // level above has one node there (pseudo up to c0, then the
+             // chain of point 0), with one child
+    for (int l = lev - 1; l >= 0; l--) {
+      v = make_double4(__dadd_rn(0.0, v.x), __dadd_rn(0.0, v.y), __dadd_rn(0.0, v.z),
+                       __dadd_rn(0.0, v.w));  // the one-child fold
       const bool local = cend < l;
-      if (pse) {
+      if (l <= c0) {
         cr.pl[l * nb + b] = v;
         cr.plend[l * nb + b] = local ? (int)(n - B0 < kST ? n - B0 : (int64_t)kST) : -1;  // (the last block ends at n)
       } else if (local) {
@@ -633,27 +699,50 @@ __global__ void __launch_bounds__(kST, 2) k_subtrees(const unsigned long long* _
       }
     }
   }
+  __syncthreads();
+  const int nq = min(s_q, kST);
+  for (int k = t; k < nq; k += kST) write_records_a(r, qmir[k], qv[k]);
 }
 
-// Dyadic sums (per level) and minima over aligned runs of 2^k blocks, one
-// block per level (blockIdx.x == L + 1: the minima); fixed shape.
-__global__ void __launch_bounds__(1024) k_hier(int L, int nb, Cross cr) {
-  const int l = blockIdx.x;
-  for (int k = 1; k <= cr.K; k++) {
-    const int sz = (nb + (1 << k) - 1) >> k, psz = (nb + (1 << (k - 1)) - 1) >> (k - 1);
-    for (int j = threadIdx.x; j < sz; j += blockDim.x) {
-      const int a = 2 * j, b2 = 2 * j + 1;
-      if (l <= L) {
-        const double4* src = k == 1 ? cr.pl + (int64_t)l * nb : cr.hs + (int64_t)l * cr.hn + cr.ho[k - 1];
-        double4 v = src[a];
-        if (b2 < psz) add4(v, src[b2]);
-        cr.hs[(int64_t)l * cr.hn + cr.ho[k] + j] = v;
-      } else {
-        const int* src = k == 1 ? cr.mn : cr.hm + cr.ho[k - 1];
-        cr.hm[cr.ho[k] + j] = b2 < psz ? min(src[a], src[b2]) : src[a];
+// Dyadic sums (per level) and minima over aligned runs of 2^k blocks, fixed
+// shape: hs_k[j] = hs_{k-1}[2j] + hs_{k-1}[2j+1].  One launch builds levels
+// k0+1..k0+5 from level k0: each warp takes 32 consecutive level-k0 entries
+// and pairs them up through shuffles (blockIdx.y = tree level, L + 1 = the
+// minima).
+__global__ void __launch_bounds__(256) k_hier(int L, int nb, int k0, Cross cr) {
+  const int l = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int sz0 = (nb + (1 << k0) - 1) >> k0;
+  if (j - lane >= sz0) return;  // (whole warps only)
+  if (l <= L) {
+    const double4* src = k0 == 0 ? cr.pl + (int64_t)l * nb : cr.hs + (int64_t)l * cr.hn + cr.ho[k0];
+    double4 v = j < sz0 ? src[j] : make_double4(0.0, 0.0, 0.0, 0.0);
+    for (int d = 1; d <= 5 && k0 + d <= cr.K; d++) {
+      double4 y;
+      y.x = __shfl_down_sync(0xffffffffu, v.x, 1 << (d - 1));
+      y.y = __shfl_down_sync(0xffffffffu, v.y, 1 << (d - 1));
+      y.z = __shfl_down_sync(0xffffffffu, v.z, 1 << (d - 1));
+      y.w = __shfl_down_sync(0xffffffffu, v.w, 1 << (d - 1));
+      const int szd = (nb + (1 << (k0 + d)) - 1) >> (k0 + d);
+      const int jd = j >> d;
+      if ((lane & ((1 << d) - 1)) == 0) {
+        if (((j >> (d - 1)) + 1) < ((nb + (1 << (k0 + d - 1)) - 1) >> (k0 + d - 1))) add4(v, y);
+        if (jd < szd) cr.hs[(int64_t)l * cr.hn + cr.ho[k0 + d] + jd] = v;
       }
     }
-    __syncthreads();
+  } else {
+    const int* src = k0 == 0 ? cr.mn : cr.hm + cr.ho[k0];
+    int v = j < sz0 ? src[j] : -1;
+    for (int d = 1; d <= 5 && k0 + d <= cr.K; d++) {
+      const int y = __shfl_down_sync(0xffffffffu, v, 1 << (d - 1));
+      const int szd = (nb + (1 << (k0 + d)) - 1) >> (k0 + d);
+      const int jd = j >> d;
+      if ((lane & ((1 << d) - 1)) == 0) {
+        if (((j >> (d - 1)) + 1) < ((nb + (1 << (k0 + d - 1)) - 1) >> (k0 + d - 1))) v = min(v, y);
+        if (jd < szd) cr.hm[cr.ho[k0 + d] + jd] = v;
+      }
+    }
   }
 }
 
@@ -930,7 +1019,10 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
                                   T.offset.as<int>(), T.box.as<double>(), T.sp.as<double4>(),
                                   T.records(), cr, nbs);
   if (nbs > 1) {
-    k_hier<<<L + 2, 1024, 0, st>>>(L, nbs, cr);
+    for (int k0 = 0; k0 < cr.K; k0 += 5) {
+      const int sz0 = (nbs + (1 << k0) - 1) >> k0;
+      k_hier<<<dim3((sz0 + 255) / 256, L + 2), 256, 0, st>>>(L, nbs, k0, cr);
+    }
     k_crossing<<<(int)((ncr + 255) / 256), 256, 0, st>>>(L, nbs, n, T.offset.as<int>(), cr,
                                                          T.records());
   }
