@@ -91,6 +91,49 @@ def test_tree_build_matches_oracle_large(orc, fga, kind, n):
     assert np.abs(t.com - o.com).max() <= 1e-12 * max(np.abs(o.com).max(), 1.0)
 
 
+def _boundary_case(kind, rng):
+    """Inputs around the device build's 128-point blocks (csrc/tree.cu
+    k_subtrees / k_crossing): sizes next to block multiples, duplicate runs
+    and depth-cap leaves spanning several blocks, shallow depth caps, a flat
+    axis."""
+    L = 20
+    if kind.startswith("n"):
+        p = rng.uniform(-2, 3, size=(int(kind[1:]), 3))
+    elif kind == "dup_runs":  # 5 distinct points x 300: depth-cap leaves over 3 blocks
+        p = np.repeat(rng.uniform(-1, 1, size=(5, 3)), 300, axis=0)[rng.permutation(1500)]
+    elif kind == "dup_plus_uniform":
+        p = np.vstack([np.repeat(rng.uniform(-1, 1, size=(1, 3)), 600, axis=0),
+                       rng.uniform(-1, 1, size=(900, 3))])
+    elif kind.startswith("cap"):
+        L = int(kind[3:])
+        p = rng.uniform(-1, 1, size=(3000, 3))
+    elif kind == "flat_z":
+        p = np.column_stack([rng.uniform(-1, 1, size=(3000, 2)), np.full(3000, 0.25)])
+    else:  # one tight cluster inside a sparse cloud: deep chains across blocks
+        p = np.vstack([rng.uniform(-1, 1, size=(700, 3)),
+                       0.3 + rng.normal(size=(700, 3)) * 1e-9])
+    return p, L
+
+
+@pytest.mark.parametrize("kind", ["n1", "n2", "n127", "n128", "n129", "n255", "n257", "n1000",
+                                  "n4097", "dup_runs", "dup_plus_uniform", "cap1", "cap2",
+                                  "cap3", "flat_z", "tight_cluster"])
+def test_tree_build_block_boundaries(orc, fga, kind):
+    from paper_2009_14005_b200 import bhtree
+    import zlib
+    rng = np.random.default_rng(zlib.crc32(kind.encode()))
+    p, L = _boundary_case(kind, rng)
+    m = rng.uniform(0.001, 0.02, size=len(p))
+    t = bhtree.build(fga.PointCloud(p), m, L)
+    o = orc.tree_build(p, m, L)
+    assert t.node_count == o.node_count
+    for k in ("children", "occupancy", "depth", "bbox_min", "bbox_max"):
+        assert np.array_equal(getattr(t, k), getattr(o, k)), k
+    assert np.allclose(t.length, o.length, rtol=2.5e-16, atol=0)
+    assert np.allclose(t.mass, o.mass, rtol=1e-12, atol=0)
+    assert np.abs(t.com - o.com).max() <= 1e-12 * max(np.abs(o.com).max(), 1.0)
+
+
 @pytest.mark.parametrize("theta", [0.0, 0.3, 0.5, 0.6, 0.9])
 def test_bh_forces_fp64_bit_exact_on_reference_tree(golden, orc, fga, theta):
     """fga_tree_forces(fp64) on the reference's own tree: same visits, same
