@@ -290,7 +290,7 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
   const int64_t nw = S.direct ? direct_iterate_warps(S.m_local, S.precision)
                               : bh_iterate_warps(S.m_local);
   FGA_CUDA_TRY(S.partials.reserve(sizeof(double) * kPartialStride * std::max<int64_t>(nw, 1)));
-  FGA_CUDA_TRY(S.gpe_part.reserve(sizeof(double) * std::max<int64_t>(gpe_warps(S.m_local, S.precision), 1)));
+  FGA_CUDA_TRY(S.gpe_part.reserve(sizeof(double) * std::max<int64_t>(gpe_warps(S.m_local, n, S.precision), 1)));
   FGA_CUDA_TRY(S.red_stage.reserve(sizeof(double) * reduce_stage_doubles()));
   const int64_t mi = S.P.max_iters;
   FGA_CUDA_TRY(S.rec_delta.reserve(sizeof(double) * mi));
@@ -371,7 +371,7 @@ int session_begin_common(fga_ctx* c, int64_t n, int64_t m, int dim, const fga_pa
 int session_gpe(fga_ctx* c, const IterState* gate) {
   Session& S = c->S;
   TemplateView tv = S.view();
-  const int64_t ngw = gpe_warps(S.m_local, S.precision);
+  const int64_t ngw = gpe_warps(S.m_local, S.ref().n, S.precision);
   launch_gpe(S.ref(), tv.px, tv.py, tv.pz, tv.mq, S.m_local, S.sp.eps, gate, S.gpe_part.as<double>(),
              S.precision, c->stream);
   launch_reduce(S.partials.as<double>(), 0, S.gpe_part.as<double>(), S.m_local > 0 ? ngw : 0, -1.0,
@@ -398,7 +398,7 @@ int session_forces(fga_ctx* c) {
   if (with_gpe && S.m_local > 0) {
     launch_gpe(S.ref(), tv.px, tv.py, tv.pz, tv.mq, S.m_local, S.sp.eps, S.st(),
                S.gpe_part.as<double>(), S.precision, s);
-    ngw = gpe_warps(S.m_local, S.precision);
+    ngw = gpe_warps(S.m_local, S.ref().n, S.precision);
   }
   const double pairs = S.direct ? (double)S.n * (double)S.m_local : -1.0;
   launch_reduce(S.partials.as<double>(), nw, S.gpe_part.as<double>(), ngw, pairs,
@@ -842,7 +842,7 @@ int fga_register(fga_ctx* c, const double* x, int64_t n, const double* y, int64_
     double* snap = S.gpe_snap.as<double>();
     FGA_CUDA_TRY(cudaMemcpyAsync(snap, tv.px, sizeof(double) * 3 * ml, cudaMemcpyDeviceToDevice, s));
     FGA_CUDA_TRY(cudaMemcpyAsync(snap + 3 * ml, tv.mq, sizeof(double) * ml, cudaMemcpyDeviceToDevice, s));
-    const int64_t ngw = gpe_warps(ml, S.precision);
+    const int64_t ngw = gpe_warps(ml, S.ref().n, S.precision);
     FGA_CUDA_TRY(S.gpe_part2.reserve(sizeof(double) * std::max<int64_t>(ngw, 1)));
     FGA_CUDA_TRY(S.gpe_sums2.reserve(sizeof(double) * (kPartialStride + reduce_stage_doubles())));
     FGA_CUDA_TRY(cudaEventRecord(c->aev[0], s));
@@ -1247,7 +1247,7 @@ int fga_gpe_kernel(fga_ctx* c, const double* pos_y, const double* mass_y, int64_
   FGA_CUDA_TRY(soa.reserve(sizeof(double) * 4 * m));
   double* b = soa.as<double>();
   launch_gather_queries(q.as<double>(), qmd.as<double>(), nullptr, m, b, b + m, b + 2 * m, b + 3 * m, s);
-  const int64_t ngw = gpe_warps(m, precision);
+  const int64_t ngw = gpe_warps(m, n, precision);
   FGA_CUDA_TRY(part.reserve(sizeof(double) * ngw));
   FGA_CUDA_TRY(sums.reserve(sizeof(double) * (kPartialStride + reduce_stage_doubles())));
   RefPoints rp{precision ? nullptr : pk.as<float4>(), precision ? pk.as<double4>() : nullptr, n};

@@ -25,7 +25,7 @@ constexpr int kDirectQPT = 4;  // queries per thread in the FP32 direct sum (2 F
 
 int64_t bh_iterate_warps(int64_t m);
 int64_t direct_iterate_warps(int64_t m, int precision);
-int64_t gpe_warps(int64_t m, int precision);
+int64_t gpe_warps(int64_t m, int64_t n, int precision);
 
 // One force pass of the iteration: applies the pending transform, evaluates
 // forces, fused Euler-Cromer step, per-warp Kabsch partials.

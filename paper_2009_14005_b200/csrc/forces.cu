@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(kForceThreads, 3) k_gpe32(const float4* __rest
                                                             const double* __restrict__ mq,
                                                             int64_t m, float eps,
                                                             const IterState* st,
-                                                            double* partials) {
+                                                            double* partials, int64_t seg) {
   if (st && st->done) return;
   __shared__ float4 sm[kTile];
   constexpr int NP = Q / 2;  // packs of 2 queries; odd packs on Newton
@@ -411,8 +411,9 @@ __global__ void __launch_bounds__(kForceThreads, 3) k_gpe32(const float4* __rest
   double acc[Q];
 #pragma unroll
   for (int k = 0; k < Q; k++) acc[k] = 0.0;
-  for (int64_t t0 = 0; t0 < n; t0 += kTile) {
-    const int jmax = (int)((n - t0) < (int64_t)kTile ? (n - t0) : (int64_t)kTile);
+  const int64_t r0 = (int64_t)blockIdx.y * seg, r1 = min(n, r0 + seg);  // this block's reference segment
+  for (int64_t t0 = r0; t0 < r1; t0 += kTile) {
+    const int jmax = (int)((r1 - t0) < (int64_t)kTile ? (r1 - t0) : (int64_t)kTile);
     __syncthreads();
     for (int j = threadIdx.x; j < jmax; j += kForceThreads) sm[j] = __ldg(&src[t0 + j]);
     __syncthreads();
@@ -434,7 +435,7 @@ __global__ void __launch_bounds__(kForceThreads, 3) k_gpe32(const float4* __rest
     if (i < m) tot += mq[i] * acc[k];
   }
   tot = warp_sum(tot);
-  if (lane == 0) partials[(int64_t)blockIdx.x * kWarps + wl] = tot;
+  if (lane == 0) partials[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * kWarps + wl] = tot;
 }
 
 __global__ void __launch_bounds__(kForceThreads) k_gpe64(const double4* __restrict__ src, int64_t n,
@@ -443,15 +444,16 @@ __global__ void __launch_bounds__(kForceThreads) k_gpe64(const double4* __restri
                                                          const double* __restrict__ pz,
                                                          const double* __restrict__ mq, int64_t m,
                                                          double eps, const IterState* st,
-                                                         double* partials) {
+                                                         double* partials, int64_t seg) {
   if (st && st->done) return;
   __shared__ double4 sm[kTile / 2];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * kForceThreads + threadIdx.x;
   const double qx = i < m ? px[i] : 0.0, qy = i < m ? py[i] : 0.0, qz = i < m ? pz[i] : 0.0;
   double acc = 0.0;
-  for (int64_t t0 = 0; t0 < n; t0 += kTile / 2) {
-    const int jmax = (int)((n - t0) < (int64_t)(kTile / 2) ? (n - t0) : (int64_t)(kTile / 2));
+  const int64_t r0 = (int64_t)blockIdx.y * seg, r1 = min(n, r0 + seg);  // this block's reference segment
+  for (int64_t t0 = r0; t0 < r1; t0 += kTile / 2) {
+    const int jmax = (int)((r1 - t0) < (int64_t)(kTile / 2) ? (r1 - t0) : (int64_t)(kTile / 2));
     __syncthreads();
     for (int j = threadIdx.x; j < jmax; j += kForceThreads) sm[j] = src[t0 + j];
     __syncthreads();
@@ -465,7 +467,7 @@ __global__ void __launch_bounds__(kForceThreads) k_gpe64(const double4* __restri
   }
   double tot = i < m ? __dmul_rn(mq[i], acc) : 0.0;
   tot = warp_sum(tot);
-  if (lane == 0) partials[(int64_t)blockIdx.x * kWarps + wl] = tot;
+  if (lane == 0) partials[((int64_t)blockIdx.y * gridDim.x + blockIdx.x) * kWarps + wl] = tot;
 }
 
 inline unsigned grid_for(int64_t items, int64_t per_block) {
@@ -493,10 +495,28 @@ int64_t direct_iterate_warps(int64_t m, int precision) {
 }
 // queries per thread of the FP32 energy kernel (8 was measured 24% slower)
 constexpr int kGpeQ = 4;
-static int gpe_q() { return kGpeQ; }
-int64_t gpe_warps(int64_t m, int precision) {
-  const int64_t per = precision ? kForceThreads : kForceThreads * gpe_q();
-  return (int64_t)grid_for(m, per) * kWarps;
+// The energy kernels also split the reference points into segments
+// (blockIdx.y) when the queries alone give too few blocks (configs[1]/[3]:
+// 100k-200k points -> 98-196 query blocks on 148 SMs).  The split depends
+// only on (m, n), so the fixed-order partial sums stay deterministic.
+struct GpeShape {
+  int64_t qblocks, splits, seg;
+};
+static GpeShape gpe_shape(int64_t m, int64_t n, int precision) {
+  const int64_t per = precision ? kForceThreads : kForceThreads * kGpeQ;
+  const int64_t tile = precision ? kTile / 2 : kTile;
+  GpeShape g;
+  g.qblocks = grid_for(m, per);
+  int64_t sp = (2 * 3 * 148 + g.qblocks - 1) / g.qblocks;  // two waves of 3 blocks per SM
+  sp = std::max<int64_t>(1, std::min<int64_t>(sp, n / (4 * tile)));  // >= 4 tiles per segment
+  const int64_t tiles = (n + tile - 1) / tile;
+  g.seg = ((tiles + sp - 1) / sp) * tile;
+  g.splits = std::max<int64_t>(1, (n + g.seg - 1) / g.seg);
+  return g;
+}
+int64_t gpe_warps(int64_t m, int64_t n, int precision) {
+  const GpeShape g = gpe_shape(m, n, precision);
+  return g.qblocks * g.splits * kWarps;
 }
 
 template <int kT>
@@ -550,15 +570,17 @@ void launch_gpe(const RefPoints& ref, const double* px, const double* py, const 
                 const double* mq, int64_t m, double eps, const IterState* st, double* partials,
                 int precision, cudaStream_t s) {
   if (m <= 0) return;
+  const GpeShape g = gpe_shape(m, ref.n, precision);
+  const dim3 grid((unsigned)g.qblocks, (unsigned)g.splits);
   if (precision)
-    k_gpe64<<<grid_for(m, kForceThreads), kForceThreads, 0, s>>>(ref.p64, ref.n, px, py, pz, mq, m,
-                                                                 eps, st, partials);
+    k_gpe64<<<grid, kForceThreads, 0, s>>>(ref.p64, ref.n, px, py, pz, mq, m, eps, st, partials,
+                                           g.seg);
   else if (eps > 0.0)
-    k_gpe32<true, kGpeQ><<<grid_for(m, kForceThreads * kGpeQ), kForceThreads, 0, s>>>(
-        ref.p32, ref.n, px, py, pz, mq, m, (float)eps, st, partials);
+    k_gpe32<true, kGpeQ><<<grid, kForceThreads, 0, s>>>(ref.p32, ref.n, px, py, pz, mq, m,
+                                                        (float)eps, st, partials, g.seg);
   else  // eps == 0: keep IEEE rcp semantics (1/0 = inf) on every pair
-    k_gpe32<false, kGpeQ><<<grid_for(m, kForceThreads * kGpeQ), kForceThreads, 0, s>>>(
-        ref.p32, ref.n, px, py, pz, mq, m, (float)eps, st, partials);
+    k_gpe32<false, kGpeQ><<<grid, kForceThreads, 0, s>>>(ref.p32, ref.n, px, py, pz, mq, m,
+                                                         (float)eps, st, partials, g.seg);
 }
 
 void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, const double* qz,
