@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
   NodeB64* rb64 = a.scratch.rb64 + slot * cap;
   double* tp = a.scratch.tpl + slot * a.mmax * 7;
   const double dt = a.p.dt, eta = a.p.eta, G = a.p.G, eps = a.p.epsilon;
-  const double theta2 = a.p.theta * a.p.theta, eps2 = eps * eps;
+  const double theta2 = a.theta2, eps2 = a.eps2;
 
   while (true) {
     if (tid == 0) next_pair = atomicAdd(a.counter, 1);
@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
       __syncthreads();
 
       // ---------------------------------------------------- iterations
-      const float theta2f = (float)theta2, eps2f = (float)eps2;
+      const float theta2f = a.theta2f, eps2f = a.eps2f;
       const int nchunks = (m + 31) / 32;
       double* px = tp;
       double* py = tp + a.mmax;

@@ -999,6 +999,10 @@ int fga_register_batch_dev(fga_ctx* c, const double* x_all, const int64_t* x_off
   const double extent = params->norm_b - params->norm_a;
   a.cell_edge = extent / params->rho;
   a.cell_vol = std::pow(a.cell_edge, 3);
+  a.theta2 = params->theta * params->theta;
+  a.eps2 = params->epsilon * params->epsilon;
+  a.theta2f = (float)a.theta2;
+  a.eps2f = (float)a.eps2;
   const double r_ball = extent / (2.0 * params->max_depth * params->rho);
   a.ball_vol = (4.0 / 3.0) * M_PI * std::pow(r_ball, 3);
   a.p = *params;

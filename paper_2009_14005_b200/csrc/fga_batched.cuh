@@ -34,6 +34,10 @@ struct BatchArgs {
   int ncell;                  // rho^3
   size_t node_cap;            // node capacity per slot
   double cell_edge, cell_vol, ball_vol;
+  // theta^2 and eps^2, precomputed: the traversal loop re-reads them from the
+  // constant bank every step (register-bound at 1024 threads)
+  double theta2, eps2;
+  float theta2f, eps2f;
   fga_params p;
   fga_options opt;
   BatchScratch scratch;
