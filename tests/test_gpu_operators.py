@@ -240,6 +240,26 @@ def test_gpe_vs_reference(golden, fga, prec, tol):
     assert abs(one - float(g["gpe/hand1"])) < 1e-6
 
 
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-6), ("fp64", 1e-13)])
+def test_gpe_split_reference_segments(orc, fga, prec, tol):
+    """40k x 50k: few query blocks, so the energy kernels split the reference
+    points over blockIdx.y (forces.cu gpe_shape).  Same value as the oracle
+    and bitwise the same on a rerun."""
+    from paper_2009_14005_b200 import dynamics
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-5, 5, size=(50000, 3))
+    xm = rng.uniform(0.001, 0.02, size=50000)
+    y = rng.normal(size=(40000, 3)) * 2.0
+    ym = rng.uniform(0.02, 0.1, size=40000)
+    prm = fga.default_params()
+    st = dynamics.SwarmState.at_rest(y, ym)
+    e1 = dynamics.gpe(st, fga.PointCloud(x), xm, prm, precision=prec)
+    e2 = dynamics.gpe(st, fga.PointCloud(x), xm, prm, precision=prec)
+    assert e1 == e2
+    ref = orc.gpe(y, ym, x, xm, prm.G, prm.epsilon)
+    assert abs(e1 - ref) <= tol * abs(ref)
+
+
 @pytest.mark.parametrize("seed", [1, 2])
 def test_normalize_and_niv_bit_exact(golden, fga, seed):
     g = golden("masses")
