@@ -23,9 +23,12 @@
 namespace fga {
 namespace {
 
-constexpr int kBT = 1024;  // threads per CTA
+#ifndef FGA_KBT
+#define FGA_KBT 1024
+#endif
+constexpr int kBT = FGA_KBT;  // threads per CTA
 constexpr int kBW = kBT / 32;
-static_assert(kBT == 1024, "the chunk-sum split assumes 16 moments x 64 ranges");
+static_assert(kBT % 32 == 0 && kBT >= 64, "whole warps, at least two");
 
 struct PairState {
   double R[9], t[3], Racc[9], tacc[3], shift[3];
@@ -718,11 +721,12 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
           }
         }
         __syncthreads();
-        {  // chunk sums in a fixed order, all threads: 16 moments x 64 contiguous chunk ranges,
+        {  // chunk sums in a fixed order, all threads: 16 moments x kBT/16 contiguous chunk ranges,
            // ranges paired in the warp, then the 32 warp results in warp order
+          constexpr int kRanges = kBT / 16;
           const int k = tid & 15, part = tid >> 4;
-          const int c0 = (int)((int64_t)nchunks * part / 64);
-          const int c1 = (int)((int64_t)nchunks * (part + 1) / 64);
+          const int c0 = (int)((int64_t)nchunks * part / kRanges);
+          const int c1 = (int)((int64_t)nchunks * (part + 1) / kRanges);
           double v = 0.0;
           for (int c = c0; c < c1; c++) v += __ldcg(&cpart[(size_t)c * kPartialStride + k]);
           v += __shfl_down_sync(0xffffffffu, v, 16);  // part 2w + part 2w+1
