@@ -28,7 +28,7 @@ struct TreeDev {
   DevBuf box, scratch, keys_in, keys, idx_in, idx, clev, count, offset, cub_tmp;
   // build intermediates: packed (x,y,z,m) in input order, sorted copy, the
   // run-overflow flag, per-(level, block) boundary partials (tree.cu Cross)
-  DevBuf keys32_in, keys32, packed, sp, lvl, cross;
+  DevBuf keys32_in, keys32, packed, sp, flags, cross;
   DevBuf a32, b32, a64, b64;
   DevBuf export_buf;
 
@@ -37,7 +37,7 @@ struct TreeDev {
   }
   void release() {
     DevBuf* all[] = {&box,    &scratch, &keys_in, &keys,   &idx_in, &idx, &clev,
-                     &count,  &offset,  &cub_tmp, &keys32_in, &keys32, &packed, &sp,     &lvl,
+                     &count,  &offset,  &cub_tmp, &keys32_in, &keys32, &packed, &sp,     &flags,
                      &cross,  &a32,    &b32,    &a64,    &b64,  &export_buf};
     for (DevBuf* b : all) b->release();
     n_nodes = 0;

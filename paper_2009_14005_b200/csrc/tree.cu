@@ -924,8 +924,8 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   FGA_CUDA_TRY(T.clev.reserve(n + 1));
   FGA_CUDA_TRY(T.count.reserve(sizeof(int) * (n + 1)));
   FGA_CUDA_TRY(T.offset.reserve(sizeof(int) * (n + 1)));
-  FGA_CUDA_TRY(T.lvl.reserve(sizeof(int) * 2));
-  int* overflow = T.lvl.as<int>();
+  FGA_CUDA_TRY(T.flags.reserve(sizeof(int) * 2));
+  int* overflow = T.flags.as<int>();  // a run of > kRun equal top key bits
   {
     size_t b32 = 0, b64 = 0, bscan = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b32, T.keys32_in.as<unsigned>(), T.keys32.as<unsigned>(),
