@@ -912,8 +912,12 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   k_bbox_partial<<<nb, kThreads, 0, st>>>(pts_dev, n, T.scratch.as<double>());
   k_bbox_final<<<1, 256, 0, st>>>(T.scratch.as<double>(), nb, L, T.box.as<double>());
 
-  const int shift = std::max(0, 3 * L - 32);
-  const int sort_bits = std::min(32, 3 * L);
+  // The sort runs on the top key bits only (3 radix passes for 24 bits, 4 for
+  // 32) and k_fixup_runs orders each run of equal top bits by the full key;
+  // a run longer than kRun retries with 32 bits, then with the full key.
+  // 24 bits first only for small clouds (dense clusters of a large cloud
+  // overflow the runs).
+  int top_bits = n <= (1 << 22) ? 24 : 32;
   FGA_CUDA_TRY(T.keys.reserve(sizeof(unsigned long long) * n));
   FGA_CUDA_TRY(T.keys32_in.reserve(sizeof(unsigned) * n));
   FGA_CUDA_TRY(T.keys32.reserve(sizeof(unsigned) * n));
@@ -929,28 +933,35 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   {
     size_t b32 = 0, b64 = 0, bscan = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b32, T.keys32_in.as<unsigned>(), T.keys32.as<unsigned>(),
-                                    T.idx_in.as<int>(), T.idx.as<int>(), (int)n, 0, sort_bits, st);
+                                    T.idx_in.as<int>(), T.idx.as<int>(), (int)n, 0, 32, st);
     cub::DeviceRadixSort::SortPairs(nullptr, b64, (const unsigned long long*)nullptr,
                                     (unsigned long long*)nullptr, T.idx_in.as<int>(),
                                     T.idx.as<int>(), (int)n, 0, 3 * L, st);
     cub::DeviceScan::ExclusiveSum(nullptr, bscan, (int*)nullptr, (int*)nullptr, (int)(n + 1), st);
     FGA_CUDA_TRY(T.cub_tmp.reserve(std::max(std::max(b32, b64), bscan)));
   }
-  FGA_CUDA_TRY(cudaMemsetAsync(overflow, 0, sizeof(int), st));
-  k_keys<<<blocks_for(n), kThreads, 0, st>>>(pts_dev, masses_dev, n, T.box.as<double>(), L, shift,
-                                             T.keys32_in.as<unsigned>(), nullptr, T.idx_in.as<int>(),
-                                             T.packed.as<double4>());
   size_t tmp_bytes = T.cub_tmp.bytes;
-  FGA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(T.cub_tmp.p, tmp_bytes, T.keys32_in.as<unsigned>(),
-                                               T.keys32.as<unsigned>(), T.idx_in.as<int>(),
-                                               T.idx.as<int>(), (int)n, 0, sort_bits, st));
-  k_gather_sorted<<<blocks_for(n), kThreads, 0, st>>>(T.packed.as<double4>(), T.idx.as<int>(), n,
-                                                      T.box.as<double>(), L, T.sp.as<double4>(),
-                                                      T.keys.as<unsigned long long>());
-  if (shift > 0)
-    k_fixup_runs<<<blocks_for(n), kThreads, 0, st>>>(T.keys32.as<unsigned>(), n,
-                                                     T.keys.as<unsigned long long>(),
-                                                     T.idx.as<int>(), T.sp.as<double4>(), overflow);
+  auto sort_top = [&](int bits) -> int {
+    const int shift = std::max(0, 3 * L - bits);
+    FGA_CUDA_TRY(cudaMemsetAsync(overflow, 0, sizeof(int), st));
+    k_keys<<<blocks_for(n), kThreads, 0, st>>>(pts_dev, masses_dev, n, T.box.as<double>(), L, shift,
+                                               T.keys32_in.as<unsigned>(), nullptr,
+                                               T.idx_in.as<int>(), T.packed.as<double4>());
+    tmp_bytes = T.cub_tmp.bytes;
+    FGA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(T.cub_tmp.p, tmp_bytes, T.keys32_in.as<unsigned>(),
+                                                 T.keys32.as<unsigned>(), T.idx_in.as<int>(),
+                                                 T.idx.as<int>(), (int)n, 0, std::min(bits, 3 * L),
+                                                 st));
+    k_gather_sorted<<<blocks_for(n), kThreads, 0, st>>>(T.packed.as<double4>(), T.idx.as<int>(), n,
+                                                        T.box.as<double>(), L, T.sp.as<double4>(),
+                                                        T.keys.as<unsigned long long>());
+    if (shift > 0)
+      k_fixup_runs<<<blocks_for(n), kThreads, 0, st>>>(T.keys32.as<unsigned>(), n,
+                                                       T.keys.as<unsigned long long>(),
+                                                       T.idx.as<int>(), T.sp.as<double4>(), overflow);
+    return FGA_OK;
+  };
+  TRY_RC(sort_top(top_bits));
   // c_i, node counts, preorder offsets (rerun after a fallback)
   auto levels = [&]() -> int {
     k_count<<<blocks_for(n + 1), kThreads, 0, st>>>(T.keys.as<unsigned long long>(), n, L,
@@ -972,6 +983,12 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
     return FGA_OK;
   };
   TRY_RC(fetch());
+  if (ovf && top_bits < 32) {  // a long run of equal top 24 bits: 32 bits
+    top_bits = 32;
+    TRY_RC(sort_top(top_bits));
+    TRY_RC(levels());
+    TRY_RC(fetch());
+  }
   if (ovf) {  // a long run of equal top bits: full 64-bit sort
     FGA_CUDA_TRY(T.keys_in.reserve(sizeof(unsigned long long) * n));
     k_keys<<<blocks_for(n), kThreads, 0, st>>>(pts_dev, masses_dev, n, T.box.as<double>(), L, 0,
