@@ -140,6 +140,38 @@ def sim_thread(com, l2, sk, q, theta2):
     return steps, distinct, lines
 
 
+def hilbert3(X, bits):
+    """3-D Hilbert index of integer coordinates (Skilling's transpose)."""
+    X = X.copy()
+    M = 1 << (bits - 1)
+    Q = M
+    while Q > 1:
+        P = Q - 1
+        for i in range(3):
+            m = (X[:, i] & Q) != 0
+            X[m, 0] ^= P
+            nm = ~m
+            t = (X[nm, 0] ^ X[nm, i]) & P
+            X[nm, 0] ^= t
+            X[nm, i] ^= t
+        Q >>= 1
+    for i in range(1, 3):
+        X[:, i] ^= X[:, i - 1]
+    t = np.zeros(len(X), dtype=X.dtype)
+    Q = M
+    while Q > 1:
+        m = (X[:, 2] & Q) != 0
+        t[m] ^= Q - 1
+        Q >>= 1
+    for i in range(3):
+        X[:, i] ^= t
+    idx = np.zeros(len(X), dtype=np.int64)
+    for b in range(bits - 1, -1, -1):
+        for i in range(3):
+            idx = (idx << 1) | ((X[:, i] >> b) & 1)
+    return idx
+
+
 def main(n=1_000_000, nq=16384, theta=0.5):
     rng = synth.rng_from_seed(3)
     x = synth.blob(n, rng)
@@ -165,6 +197,17 @@ def main(n=1_000_000, nq=16384, theta=0.5):
         return v
     key = (spread(qi[:, 0]) << np.uint64(2)) | (spread(qi[:, 1]) << np.uint64(1)) | spread(qi[:, 2])
     order = np.argsort(key, kind="stable")
+    if os.environ.get("SIM_ORDER"):  # Morton vs Hilbert 32-query warps, union overhead
+        hord = np.argsort(hilbert3(np.clip((qq * 1023).astype(np.int64), 0, 1023), 10),
+                          kind="stable")
+        for name, o in (("morton", order), ("hilbert", hord)):
+            for frac in (0.25, 0.5, 0.75):
+                st0 = int(len(o) * frac)
+                qs = np.ascontiguousarray(yn[o[st0:st0 + nq]])
+                a = sim(com, l2, sk, qs, theta * theta, 32)
+                print(f"{name} @{frac}: steps/warp {a[0]/(nq/32):.0f} visits/q {a[4]/nq:.0f} "
+                      f"union {a[0]/(nq/32)/(a[4]/nq):.3f}")
+        return
     start = len(order) // 2
     sel = order[start:start + nq]
     q = np.ascontiguousarray(yn[sel])
