@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
       __syncthreads();
     }
 
-    // ---------------------------------------------------- template (Morton order)
+    // ---------------------------------------------------- template (Hilbert order)
     {
       double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
       for (int i = tid; i < m; i += kBT)
@@ -582,9 +582,30 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
             f = fmin(fmax(f, 0.0), 1.0);
             q[k] = (unsigned long long)(f * 1023.0);
           }
+          // 10-bit 3-D Hilbert index (Skilling's transpose; see setup.cu
+          // hilbert3): more compact 32-query warps than Morton order
+          unsigned X[3] = {(unsigned)q[0], (unsigned)q[1], (unsigned)q[2]};
+          for (unsigned Q = 1u << 9; Q > 1; Q >>= 1) {
+            const unsigned P = Q - 1;
+            for (int d = 0; d < 3; d++) {
+              if (X[d] & Q) {
+                X[0] ^= P;
+              } else {
+                const unsigned t = (X[0] ^ X[d]) & P;
+                X[0] ^= t;
+                X[d] ^= t;
+              }
+            }
+          }
+          X[1] ^= X[0];
+          X[2] ^= X[1];
+          unsigned tg = 0;
+          for (unsigned Q = 1u << 9; Q > 1; Q >>= 1)
+            if (X[2] & Q) tg ^= Q - 1;
           key = 0;
           for (int b = 9; b >= 0; b--)
-            key = (key << 3) | (((q[0] >> b) & 1) << 2) | (((q[1] >> b) & 1) << 1) | ((q[2] >> b) & 1);
+            key = (key << 3) | ((((X[0] ^ tg) >> b) & 1) << 2) | ((((X[1] ^ tg) >> b) & 1) << 1) |
+                  (((X[2] ^ tg) >> b) & 1);
         }
         S.keys[i] = key;
         S.idx[i] = i;
