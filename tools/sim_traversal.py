@@ -200,7 +200,16 @@ def main(n=1_000_000, nq=16384, theta=0.5):
     if os.environ.get("SIM_ORDER"):  # Morton vs Hilbert 32-query warps, union overhead
         hord = np.argsort(hilbert3(np.clip((qq * 1023).astype(np.int64), 0, 1023), 10),
                           kind="stable")
-        for name, o in (("morton", order), ("hilbert", hord)):
+        h16 = np.argsort(hilbert3(np.clip((qq * 65535).astype(np.int64), 0, 65535), 16),
+                         kind="stable")
+        xl, xh = xn.min(0), xn.max(0)  # the reference cloud's box (the tree's cells)
+        qr = np.clip((yn - xl) / (xh - xl), 0, 1)
+        hx = np.argsort(hilbert3(np.clip((qr * 1023).astype(np.int64), 0, 1023), 10),
+                        kind="stable")
+        orders = (("morton", order), ("hilbert", hord), ("hilbert16", h16), ("hilbert_refbox", hx))
+        if os.environ.get("SIM_ORDER") == "2":
+            orders = orders[1:]
+        for name, o in orders:
             for frac in (0.25, 0.5, 0.75):
                 st0 = int(len(o) * frac)
                 qs = np.ascontiguousarray(yn[o[st0:st0 + nq]])
