@@ -107,6 +107,11 @@ def _boundary_case(kind, rng):
     elif kind.startswith("cap"):
         L = int(kind[3:])
         p = rng.uniform(-1, 1, size=(3000, 3))
+    elif kind == "close_pairs":  # ~10-node single-child chains: > 4 nodes per point in a block
+        c = rng.uniform(-1, 1, size=(1000, 3))
+        d = rng.normal(size=(1000, 3))
+        p = np.vstack([c, c + 2e-5 * d / np.linalg.norm(d, axis=1, keepdims=True)])
+        p = p[np.argsort(p[:, 0])]
     elif kind == "flat_z":
         p = np.column_stack([rng.uniform(-1, 1, size=(3000, 2)), np.full(3000, 0.25)])
     else:  # one tight cluster inside a sparse cloud: deep chains across blocks
@@ -117,7 +122,7 @@ def _boundary_case(kind, rng):
 
 @pytest.mark.parametrize("kind", ["n1", "n2", "n127", "n128", "n129", "n255", "n257", "n1000",
                                   "n4097", "dup_runs", "dup_plus_uniform", "cap1", "cap2",
-                                  "cap3", "flat_z", "tight_cluster"])
+                                  "cap3", "flat_z", "tight_cluster", "close_pairs"])
 def test_tree_build_block_boundaries(orc, fga, kind):
     from paper_2009_14005_b200 import bhtree
     import zlib
