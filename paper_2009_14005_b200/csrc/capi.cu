@@ -170,19 +170,20 @@ int h2d(DevBuf& b, const T* src, int64_t count, cudaStream_t s) {
 }
 
 int sort_keys(DevBuf& tmp, DevBuf& kin, DevBuf& kout, DevBuf& iin, DevBuf& iout, int64_t n,
-              int end_bit, cudaStream_t s) {
+              int begin_bit, int end_bit, cudaStream_t s) {
   size_t bytes = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin.as<unsigned long long>(),
                                   kout.as<unsigned long long>(), iin.as<int>(), iout.as<int>(),
-                                  (int)n, 0, end_bit, s);
+                                  (int)n, begin_bit, end_bit, s);
   FGA_CUDA_TRY(tmp.reserve(bytes));
   FGA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, kin.as<unsigned long long>(),
                                                kout.as<unsigned long long>(), iin.as<int>(),
-                                               iout.as<int>(), (int)n, 0, end_bit, s));
+                                               iout.as<int>(), (int)n, begin_bit, end_bit, s));
   return FGA_OK;
 }
 
-// Morton order of an AoS (n,3) device cloud -> iout (int, n)
+// Space-filling-curve (Hilbert, setup.cu k_morton) order of an AoS (n,3)
+// device cloud -> iout (int, n)
 int morton_order(const double* pts, int64_t n, DevBuf& kin, DevBuf& kout, DevBuf& iin,
                  DevBuf& iout, DevBuf& tmp, DevBuf& scratch, cudaStream_t s) {
   FGA_CUDA_TRY(kin.reserve(sizeof(unsigned long long) * n));
@@ -193,7 +194,9 @@ int morton_order(const double* pts, int64_t n, DevBuf& kin, DevBuf& kout, DevBuf
   double* box = scratch.as<double>() + 6 * 600;
   launch_bbox(pts, n, scratch.as<double>(), box, s);
   launch_morton_keys(pts, n, box, kin.as<unsigned long long>(), iin.as<int>(), s);
-  return sort_keys(tmp, kin, kout, iin, iout, n, 63, s);
+  // locality only: the top 30 bits (10 per axis, 4 radix passes instead of 8)
+  // order the cloud; equal prefixes keep their input order (stable sort)
+  return sort_keys(tmp, kin, kout, iin, iout, n, 33, 63, s);
 }
 
 // -------------------------------------------------------------------- session
