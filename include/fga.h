@@ -146,7 +146,7 @@ int fga_register_batch_dev(fga_ctx* ctx, const double* x_all, const int64_t* x_o
  * The same loop split into stream-ordered pieces so a host can insert a
  * collective between the force pass and the rigid update (template sharding
  * across GPUs).  shard_rank/shard_count select a contiguous
- * chunk of the Morton-sorted template; every rank passes the FULL clouds (the
+ * chunk of the Hilbert-sorted template; every rank passes the FULL clouds (the
  * normalization and the template mass field are global).  x/y are host
  * pointers for fga_session_begin and device pointers for _dev. */
 int fga_session_begin(fga_ctx* ctx, const double* x, int64_t n, const double* y, int64_t m,

@@ -3,7 +3,7 @@
 One process per GPU (torchrun).  Every rank receives the FULL clouds, runs the
 identical device setup (normalization, masses, tree -- deterministic, so the
 replicated tree is bit-identical everywhere) and owns a contiguous chunk of
-the Morton-ordered template.  Per iteration the only exchange is ONE
+the Hilbert-ordered template.  Per iteration the only exchange is ONE
 all-reduce (sum) of the 18-double sums buffer: the shifted Kabsch moments
 (sum u, sum w, sum w u^T = 15 doubles, the covariance and centroid partials
 of procrustes.py:20-25), the interaction/visit counters and, when tracing,
