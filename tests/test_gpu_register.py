@@ -76,6 +76,24 @@ def test_register_direct_mode_matches_oracle(orc, fga):
     assert np.all(res.interactions == 1500 * 1500)
 
 
+@pytest.mark.parametrize("n,m", [(2, 3), (2, 5), (3, 7), (9, 4), (130, 3)])
+def test_register_tiny_clouds_match_oracle(orc, fga, n, m):
+    """Clouds of a few points (single-block trees, single-warp templates,
+    partial warps): the fp64 path follows the oracle's loop.  (A 2-point
+    template is excluded: its cross-covariance has rank 1, so the rotation
+    about the pair's axis is not unique -- the reference's own `degenerate`
+    case, procrustes.py:34 -- and LAPACK's gesdd and the device Jacobi SVD
+    pick different members of the solution set.)"""
+    rng = np.random.default_rng(n * 100 + m)
+    x = rng.normal(size=(n, 3))
+    y = rng.normal(size=(m, 3)) * 0.5
+    res = fga.register(fga.PointCloud(x), fga.PointCloud(y), params=fga.default_params(),
+                       options=fga.RegisterOptions(record_iterations=True, precision="fp64"))
+    ref = orc.register(x, y)
+    assert res.iterations == ref.iterations and res.converged == ref.converged
+    assert np.abs(res.trajectory - np.array(ref.trajectory)).max() < 1e-9
+
+
 def test_register_identity_and_determinism(fga):
     from paper_2009_14005_b200 import synth
     x = synth.blob(1000, synth.rng_from_seed(3))
