@@ -102,6 +102,42 @@ def sim(com, l2, sk, q, theta2, W):
 
 
 @njit(cache=True)
+def sim_groups(com, l2, sk, q, theta2, G):
+    """warp-min traversal with the 32 lanes split into 32/G independent groups
+    of G lanes (each with its own minimum cursor): warp iterations = max over
+    the groups of their union steps."""
+    n_nodes = len(l2)
+    nw = len(q) // 32
+    total = 0
+    cur = np.zeros(32, np.int64)
+    for w in range(nw):
+        worst = 0
+        for g0 in range(0, 32, G):
+            for l in range(G):
+                cur[l] = 0
+            steps = 0
+            while True:
+                n = cur[:G].min()
+                if n >= n_nodes:
+                    break
+                steps += 1
+                for l in range(G):
+                    if cur[l] == n:
+                        qi = w * 32 + g0 + l
+                        d2 = 0.0
+                        for k in range(3):
+                            dk = q[qi, k] - com[n, k]
+                            d2 += dk * dk
+                        if l2[n] < theta2 * d2:
+                            cur[l] = sk[n]
+                        else:
+                            cur[l] = n + 1
+            worst = max(worst, steps)
+        total += worst
+    return total
+
+
+@njit(cache=True)
 def sim_thread(com, l2, sk, q, theta2):
     """independent per-lane traversal: warp steps = max lane visits; also the
     number of distinct nodes (and 128-B lines of 24-B records) per step."""
@@ -207,6 +243,13 @@ def main(n=1_000_000, nq=16384, theta=0.5):
         hx = np.argsort(hilbert3(np.clip((qr * 1023).astype(np.int64), 0, 1023), 10),
                         kind="stable")
         orders = (("morton", order), ("hilbert", hord), ("hilbert16", h16), ("hilbert_refbox", hx))
+        if os.environ.get("SIM_ORDER") == "groups":
+            for frac in (0.25, 0.5, 0.75):
+                st0 = int(len(hord) * frac)
+                qs = np.ascontiguousarray(yn[hord[st0:st0 + nq]])
+                r = [sim_groups(com, l2, sk, qs, theta * theta, G) / (nq / 32) for G in (32, 16, 8)]
+                print(f"hilbert @{frac}: warp iterations per warp  G=32 {r[0]:.0f}  G=16 {r[1]:.0f}  G=8 {r[2]:.0f}")
+            return
         if os.environ.get("SIM_ORDER") == "2":
             orders = orders[1:]
         for name, o in orders:
