@@ -50,8 +50,11 @@ struct F32Params {
 };
 
 // (1280 threads/SM = 48 registers: 1536 / 1792 spill and ran 15% / 28% slower)
+#ifndef FGA_BH64_TPS
+#define FGA_BH64_TPS 1280  // fp64 traversal: 768 -> 35.8 ms, 1024 -> 31.5, 1280 -> 30.3, 1536 -> 38 (spills)
+#endif
 template <typename Real, bool kGuardZero, int kT, int kW = kWin>
-__global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? 1280 : 768) / kT) k_bh_iterate(
+__global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? 1280 : FGA_BH64_TPS) / kT) k_bh_iterate(
     TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, SimParams sp,
     F32Params f, double* partials, float cmag, int nblocks, int per_sm) {
   if (st->done) return;

@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--mode", default="bh", choices=["bh", "direct", "gpe", "all"])
 ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--iters", type=int, default=3)
+ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
 a = ap.parse_args()
 if a.mode == "all":
     for m in ("bh", "direct", "gpe"):
@@ -27,7 +28,7 @@ x = synth.blob(a.n, rng)
 y = synth.misalign(x, synth.random_rigid(rng, np.deg2rad(60), 0.1))
 theta = 0.0 if a.mode == "direct" else 0.5
 p = fga.default_params().replace(theta=theta, conv_tol=1e-300, max_iters=a.iters + 2)
-s = Session(x, y, p, fga.RegisterOptions(compute_gpe=False), stream=0)
+s = Session(x, y, p, fga.RegisterOptions(compute_gpe=False, precision=a.precision), stream=0)
 if a.mode == "gpe":
     for _ in range(a.iters):
         s.gpe()
