@@ -191,7 +191,13 @@ __global__ void __launch_bounds__(kForceThreads) k_bh_operator(
 // (kTile: fga_device.cuh)
 
 template <bool kGuard>
-__global__ void __launch_bounds__(kForceThreads, 3) k_direct_iterate32(
+#ifndef FGA_DIRECT_MINB
+#define FGA_DIRECT_MINB 3  // 4 spills (240 B) and is 2.5% slower
+#endif
+#ifndef FGA_GPE_MINB
+#define FGA_GPE_MINB 4  // energy: 3 blocks 0.405 s, 4 -> 0.386 s, 5 -> 0.398 s (1M x 1M)
+#endif
+__global__ void __launch_bounds__(kForceThreads, FGA_DIRECT_MINB) k_direct_iterate32(
     const float4* __restrict__ src, int64_t n, TemplateView tv, const IterState* __restrict__ st,
     SimParams sp, float eps2, double* partials) {
   if (st->done) return;
@@ -389,7 +395,7 @@ __global__ void __launch_bounds__(kForceThreads) k_direct_operator64(
 
 // ---------------------------------------------------------------- energy
 template <bool kNewton, int Q>
-__global__ void __launch_bounds__(kForceThreads, 3) k_gpe32(const float4* __restrict__ src,
+__global__ void __launch_bounds__(kForceThreads, FGA_GPE_MINB) k_gpe32(const float4* __restrict__ src,
                                                             int64_t n,
                                                             const double* __restrict__ px,
                                                             const double* __restrict__ py,
