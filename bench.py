@@ -86,10 +86,7 @@ def bench_params(args):
 
 def workload(n, seed):
     from paper_2009_14005_b200 import synth
-    rng = synth.rng_from_seed(seed)
-    x = synth.blob(n, rng)
-    gt = synth.random_rigid(rng, np.deg2rad(60), 0.1)
-    return x, synth.misalign(x, gt)
+    return synth.configs2_pair(n, seed)
 
 
 def load_peaks():
@@ -496,15 +493,10 @@ def run_e2e(args, x, y, sess):
 
 def batch_pairs(P, rank=0, world=1):
     """configs[4]: 3DMatch-fragment-sized pairs, 4096 points each, blob/box
-    alternating, pair p seeded with 100000+p; this rank's
-    share is p = rank, rank+world, ... (pairs sharded, no collective)."""
+    alternating (synth.fragment_pair); this rank's share is
+    p = rank, rank+world, ... (pairs sharded, no collective)."""
     from paper_2009_14005_b200 import synth
-    out = []
-    for p in range(rank, P, world):
-        rng = synth.rng_from_seed(100000 + p)
-        x = synth.blob(4096, rng) if p % 2 == 0 else synth.bumped_box(4096, rng)
-        out.append((x, synth.misalign(x, synth.random_rigid(rng, np.deg2rad(60), 0.1))))
-    return out
+    return [synth.fragment_pair(p) for p in range(rank, P, world)]
 
 
 def run_batched(args, rank, world):
@@ -605,10 +597,7 @@ def run_other_configs(args):
     import paper_2009_14005_b200 as fga
     from paper_2009_14005_b200 import synth
     out = {}
-    rng = synth.rng_from_seed(2)
-    x = synth.lidar_scan(100_000, rng)
-    gt = synth.random_rigid(rng, np.deg2rad(10), 1.0)
-    y = synth.misalign(x, gt)
+    x, y, gt = synth.configs1_pair()
     p = fga.default_params().replace(theta=0.5, G=0.2)
     fga.register(fga.PointCloud(x.points[:5000]), fga.PointCloud(y.points[:5000]), params=p)
     t0 = time.perf_counter()
@@ -634,10 +623,7 @@ def run_other_configs(args):
         "rotation_err_deg": fga.angular_deviation(gt.rotation, r.transform.rotation),
         "interactions_per_s_loop": float(r.interactions.sum()) / (r.timings_ms["loop"] / 1e3),
         "timings_ms": r.timings_ms}
-    rng = synth.rng_from_seed(4)
-    x, y0 = synth.partial_overlap(200_000, rng)
-    gt = synth.random_rigid(rng, np.deg2rad(60), 0.1)
-    y = synth.misalign(y0, gt)
+    x, y, gt = synth.configs3_pair()
     p = fga.default_params().replace(theta=0.5, G=2.0)
     o = fga.RegisterOptions(mass_field="knn", knn_k=16)
     from paper_2009_14005_b200 import masses

@@ -70,7 +70,10 @@ typedef struct {
   const int64_t* x_landmarks;/* LandmarkSet.reference_indices() or NULL       */
   const int64_t* y_landmarks;/* LandmarkSet.template_indices() or NULL        */
   int32_t n_landmarks;       /* > 0: SPM = field * RBF (registration.py:74-83) */
-  int32_t pad2_;
+  int32_t count_visits;      /* 1: the FP32 force pass also counts node visits
+                                (fga_result.visits, visits_per_iter); 0 = off,
+                                2.5% faster (accepted interactions are always
+                                counted; the fp64 pass always counts both)  */
 } fga_options;
 
 /* Mirrors registration.RegistrationResult (core.py:162-172). */
@@ -220,6 +223,11 @@ int fga_tree_export(fga_ctx* ctx, int64_t* children, double* com, double* mass, 
 int fga_tree_upload(fga_ctx* ctx, const int64_t* children, const double* com, const double* mass,
                     const double* length, int64_t n_nodes, int n_child, int dim);
 
+/* Counter bumped by every build / upload into the context's tree (including
+ * the one register() / a session performs): a host caching "tree T is
+ * loaded" compares it before reusing the device copy. */
+int fga_tree_generation(fga_ctx* ctx, int64_t* generation);
+
 /* ------------------------------------------------ operator-level entries */
 /* _kernels.bh_forces_kernel (_kernels.py:7-50) as called by bhtree.bh_forces
  * (bhtree.py:125-147), against the context's tree: forces (m,3) and optional
@@ -230,7 +238,10 @@ int fga_tree_forces(fga_ctx* ctx, const double* queries, const double* query_mas
                     double theta, double G, double eps2, int precision, double* forces,
                     int64_t* visits, int64_t* accepted);
 /* The reference's exact kernel signature (_kernels.py:7-8): uploads the tree
- * arrays, then evaluates.  Convenience for a literal ctypes drop-in. */
+ * arrays (skipped when the same arrays -- address, size, sampled contents --
+ * are still the context's tree), then evaluates in FP64 (the reference's
+ * arithmetic, bit-identical forces and visits).  The literal ctypes drop-in
+ * of INTEGRATION.md. */
 int fga_bh_forces_kernel(fga_ctx* ctx, const int64_t* children, const double* com,
                          const double* mass, const double* length, int64_t n_nodes, int n_child,
                          const double* queries, const double* query_masses, int64_t m, int dim,

@@ -316,6 +316,26 @@ class OracleResult:
     accepted: list  # per-iteration interactions (sum over queries)
 
 
+def setup(x, y, rho=16, max_depth=20, norm_range=(-5.0, 5.0), dt=0.1, eta=0.2):
+    """registration.py:104-121 without the tree: normalized clouds, NIV mass
+    fields and the rescale -> (xn, yn, mx, my, ctx)."""
+    a, b = norm_range
+    xn, yn, ctx = normalize_pair(x, y, a, b)
+    mx, my = rescale(niv_masses(xn, rho, a, b, max_depth), niv_masses(yn, rho, a, b, max_depth),
+                     dt, eta)
+    return xn, yn, mx, my, ctx
+
+
+def iterate(tree, pos, vel, my, r_acc, t_acc, theta, G, epsilon, dt=0.1, eta=0.2, nthreads=0):
+    """One pass of the loop body (registration.py:130-142): forces, step,
+    Kabsch, the rigid update of the swarm and the accumulated transform.
+    Returns (pos, vel, r_acc, t_acc, grav, visits, accepted)."""
+    grav, visits, acc = bh_forces(tree, pos, my, theta, G, epsilon, nthreads)
+    v_new, disp = step(pos, vel, my, grav, dt, eta)
+    R, t = solve_rigid(pos, pos + disp)
+    return (pos @ R.T + t, v_new @ R.T, R @ r_acc, t + R @ t_acc, grav, visits, acc)
+
+
 def register(x, y, G=66.7, epsilon=0.2, eta=0.2, dt=0.1, theta=0.6, rho=16, max_depth=20,
              norm_range=(-5.0, 5.0), conv_tol=1e-4, max_iters=100, x_weights=None,
              y_weights=None, normalize=True, nthreads=0, gpe=True, force_fn=None,
@@ -352,15 +372,16 @@ def register(x, y, G=66.7, epsilon=0.2, eta=0.2, dt=0.1, theta=0.6, rho=16, max_
         if force_fn is not None:
             grav = force_fn(pos, my)
             na = 0
+            v_new, disp = step(pos, vel, my, grav, dt, eta)
+            R, t = solve_rigid(pos, pos + disp)
+            pos = pos @ R.T + t
+            vel = v_new @ R.T
+            r_acc = R @ r_acc
+            t_acc = t + R @ t_acc
         else:
-            grav, _, acc = bh_forces(tree, pos, my, theta, G, epsilon, nthreads)
+            pos, vel, r_acc, t_acc, _, _, acc = iterate(tree, pos, vel, my, r_acc, t_acc, theta,
+                                                        G, epsilon, dt, eta, nthreads)
             na = int(acc.sum())
-        v_new, disp = step(pos, vel, my, grav, dt, eta)
-        R, t = solve_rigid(pos, pos + disp)
-        pos = pos @ R.T + t
-        vel = v_new @ R.T
-        r_acc = R @ r_acc
-        t_acc = t + R @ t_acc
         t_curr = np.hstack([r_acc, t_acc[:, None]])
         delta = float(((t_curr - t_prev) ** 2).sum())
         t_prev = t_curr
@@ -375,3 +396,40 @@ def register(x, y, G=66.7, epsilon=0.2, eta=0.2, dt=0.1, theta=0.6, rho=16, max_
     t_orig = denormalize_translation(r_acc, t_acc, ctx)
     return OracleResult(r_acc, t_acc, r_acc, t_orig, iterations, converged, gi, gf, deltas,
                         traj, accs)
+
+
+# ---------------------------------------------------------------------------
+# registration.py:178-206 -- register_sequence; poses composed like
+# core.py:87-96 (compose = self after other, inverse = (R^T, -R^T t))
+# ---------------------------------------------------------------------------
+@dataclass
+class OracleSequence:
+    pairwise: list  # (R, t) in the original frame per pair
+    trajectory: list  # (R, t) absolute poses, frame-0 coordinates
+    failed: list
+
+
+def register_sequence(frames, **kw):
+    """Frame i (template) onto frame i+1 (reference); a pair that raises the
+    reference's validation errors (here: an empty cloud, or the degenerate
+    extent of normalize.py:52-53) contributes an identity transform and
+    failed=True."""
+    frames = [_f64(f) for f in frames]
+    d = frames[0].shape[1]
+    pairwise, failed = [], []
+    for i in range(len(frames) - 1):
+        try:
+            if len(frames[i]) == 0 or len(frames[i + 1]) == 0:
+                raise ValueError("EmptyCloud")  # PointCloud.require_nonempty (core.py)
+            r = register(frames[i + 1], frames[i], **kw)
+            pairwise.append((r.R_orig, r.t_orig))
+            failed.append(False)
+        except ValueError:  # DegenerateExtent
+            pairwise.append((np.eye(d), np.zeros(d)))
+            failed.append(True)
+    poses = [(np.eye(d), np.zeros(d))]
+    for R, t in pairwise:
+        Ri, ti = R.T, -R.T @ t  # inverse (core.py:94-96)
+        P, p = poses[-1]
+        poses.append((P @ Ri, P @ ti + p))  # compose (core.py:87-92)
+    return OracleSequence(pairwise, poses, failed)

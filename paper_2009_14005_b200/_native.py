@@ -26,7 +26,7 @@ from .errors import (
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfga.so")
 # A/B experiments only: FGA_LIB_PATH points at an alternative in-tree build
-LIB_PATH = os.environ.get("FGA_LIB_PATH", LIB_PATH)
+LIB_PATH = os.environ.get("FGA_LIB_PATH") or LIB_PATH
 
 FGA_OK = 0
 FGA_ERR_INVALID = -1
@@ -66,7 +66,7 @@ class COptions(ctypes.Structure):
                 ("precision", _i32), ("x_weights", _vp), ("y_weights", _vp),
                 ("poll_every", _i32), ("compute_gpe", _i32), ("mass_field", _i32),
                 ("knn_k", _i32), ("x_landmarks", _vp), ("y_landmarks", _vp),
-                ("n_landmarks", _i32), ("pad2_", _i32)]
+                ("n_landmarks", _i32), ("count_visits", _i32)]
 
 
 class CResult(ctypes.Structure):
@@ -132,6 +132,7 @@ SIGNATURES = {
     "fga_tree_build_dev": (_c_int, [_vp, _vp, _vp, _i64, _c_int, ctypes.POINTER(_i64)]),
     "fga_tree_export": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fga_tree_upload": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _c_int, _c_int]),
+    "fga_tree_generation": (_c_int, [_vp, ctypes.POINTER(_i64)]),
     "fga_tree_forces": (_c_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _dbl, _c_int, _vp, _vp, _vp]),
     "fga_bh_forces_kernel": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _c_int, _vp, _vp, _i64,
                                       _c_int, _dbl, _dbl, _dbl, _i64, _vp, _vp]),
@@ -192,6 +193,7 @@ def error_for(rc: int, msg: str = ""):
 
 
 def check_msg(rc: int, msg: str) -> None:
+    """Raise the reference exception for return code ``rc`` with ``msg``."""
     if rc == FGA_OK:
         return
     if rc == FGA_ERR_INVALID:
@@ -214,25 +216,8 @@ def check_msg(rc: int, msg: str) -> None:
 
 def check(rc: int) -> None:
     """Map a C return code onto the reference's exception classes."""
-    if rc == FGA_OK:
-        return
-    msg = last_error()
-    if rc == FGA_ERR_INVALID:
-        m = _INVALID_RE.search(msg)
-        if m:
-            raise InvalidParam(m.group(1), m.group(2))
-        raise InvalidParam("argument", msg)
-    if rc == FGA_ERR_EMPTY:
-        raise EmptyCloud(msg)
-    if rc == FGA_ERR_DEGENERATE:
-        raise DegenerateExtent(msg)
-    if rc == FGA_ERR_NONFINITE:
-        raise NonFiniteWeight(msg)
-    if rc == FGA_ERR_LENGTH:
-        raise LengthMismatch(msg)
-    if rc == FGA_ERR_SINGULAR:
-        raise SingularCollocation(msg)
-    raise DeviceError(f"libfga error {rc}: {msg}")
+    if rc != FGA_OK:
+        check_msg(rc, last_error())
 
 
 def ptr(a) -> int | None:
@@ -271,6 +256,12 @@ class Context:
 
     def sync(self):
         check(lib().fga_synchronize(self.handle))
+
+    def tree_generation(self) -> int:
+        """Counter bumped by every build/upload into this context's tree."""
+        g = _i64(0)
+        check(lib().fga_tree_generation(self.handle, ctypes.byref(g)))
+        return int(g.value)
 
 
 _ctx_local = threading.local()

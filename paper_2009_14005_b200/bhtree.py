@@ -82,21 +82,25 @@ def build(reference: PointCloud, masses, max_depth: int) -> BHTree:
     N.check(N.lib().fga_tree_export(c.handle, N.ptr(t.children), N.ptr(t.com), N.ptr(t.mass),
                                     N.ptr(t.length), N.ptr(t.occupancy), N.ptr(t.depth),
                                     N.ptr(t.bbox_min), N.ptr(t.bbox_max)))
-    c.tree_token = t._token
+    c.tree_token = (t._token, c.tree_generation())
     return t
 
 
 def _ensure_on_device(tree: BHTree, c: N.Context):
-    if getattr(c, "tree_token", None) == tree._token:
+    """Upload ``tree`` unless it is still the context's tree.  The check is on
+    (tree token, the context's tree generation): register(), sessions and
+    other builds on this thread's context replace its tree and bump the
+    generation, so a stale device copy is never reused."""
+    if not hasattr(tree, "_token"):
+        tree._token = next(_tokens)
+    if getattr(c, "tree_token", None) == (tree._token, c.tree_generation()):
         return
     children = np.ascontiguousarray(tree.children, dtype=np.int64)
     com = N.f64(tree.com)
     N.check(N.lib().fga_tree_upload(c.handle, N.ptr(children), N.ptr(com), N.ptr(N.f64(tree.mass)),
                                     N.ptr(N.f64(tree.length)), len(tree.mass), children.shape[1],
                                     tree.dim))
-    c.tree_token = getattr(tree, "_token", None) or id(tree)
-    if not hasattr(tree, "_token"):
-        tree._token = c.tree_token
+    c.tree_token = (tree._token, c.tree_generation())
 
 
 def bh_forces(tree, queries, query_masses, params, count_visits=False, precision="fp64",

@@ -233,6 +233,9 @@ struct BatchSmem {
 }  // namespace
 
 // The persistent kernel.  Scratch slot = blockIdx.x.
+// kGuardZero: epsilon = 0, so a template point on a reference leaf's COM has
+// d2 + eps2 = 0 and the reference skips that term (_kernels.py:38-42)
+template <bool kGuardZero>
 __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   BatchSmem S;
@@ -716,7 +719,7 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
                       qzf = active ? (float)pz[i] : 0.f;
           float gA, gB;
           guard_coeffs(fmaxf(fabsf(qxf), fmaxf(fabsf(qyf), fabsf(qzf))), st.cmag, theta2f, gA, gB);
-          const Trav32Out o = traverse32<false>(ra32, rb32, ra64, rb64, nn, qxf, qyf, qzf, active,
+          const Trav32Out o = traverse32<kGuardZero>(ra32, rb32, ra64, rb64, nn, qxf, qyf, qzf, active,
                                                 theta2f, theta2, eps2f, gA, gB, px, py, pz, i,
                                                 &S.wins[w], lane);
           Partial p;
@@ -877,9 +880,9 @@ size_t batch_smem_bytes(int P, int nmax, int ncell) {
 }
 
 int launch_register_batch(const BatchArgs& a, int grid, size_t smem, cudaStream_t s) {
-  FGA_CUDA_TRY(cudaFuncSetAttribute(k_register_batch, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem));
-  k_register_batch<<<grid, kBT, smem, s>>>(a);
+  auto kern = a.eps2f > 0.f ? k_register_batch<false> : k_register_batch<true>;
+  FGA_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, kBT, smem, s>>>(a);
   FGA_CUDA_TRY(cudaGetLastError());
   return FGA_OK;
 }

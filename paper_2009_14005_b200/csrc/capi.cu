@@ -50,6 +50,10 @@ struct Session {
   DevBuf partials, gpe_part, sums, state, scratch, lm_idx, rbf_scratch, red_stage;
   DevBuf gpe_snap, gpe_part2, gpe_sums2;  // initial energy on the aux stream
   DevBuf rec_delta, rec_traj, rec_gpe, rec_inter, rec_visits;
+  // the session's own reference tree: operator-level builds / uploads into
+  // the context (fga_tree_*) never disturb a live registration, and a
+  // registration never replaces the operator tree
+  TreeDev tree;
   float setup_ms = 0.f, loop_ms = 0.f, gpe_ms = 0.f;
 
   TemplateView view() const {
@@ -79,6 +83,17 @@ struct fga_ctx {
   // second stream for the initial energy, which runs alongside the iterations
   cudaStream_t aux = nullptr;
   cudaEvent_t aev[3] = {nullptr, nullptr, nullptr};
+  // fga_bh_forces_kernel upload cache: the reference calls the kernel once per
+  // force evaluation with the same (immutable) BHTree arrays, so the tree is
+  // re-uploaded only when the arrays' addresses, size or sampled contents
+  // change, or another build/upload replaced the context's tree since.
+  struct ShimKey {
+    const void* p[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t n_nodes = -1;
+    int n_child = 0, dim = 0;
+    uint64_t hash = 0, generation = 0;
+    bool valid = false;
+  } shim;
 };
 
 namespace {
@@ -142,6 +157,43 @@ int invalid(const char* name, double v) {
   return FGA_ERR_INVALID;
 }
 
+// Python repr() of a float: the shortest round-tripping digits, with ".0"
+// on integral values and repr's exponent form (1e+16, 1e-05)
+std::string py_repr(double v) {
+  if (std::isnan(v)) return "nan";
+  if (std::isinf(v)) return v > 0 ? "inf" : "-inf";
+  char buf[64];
+  for (int p = 1; p <= 17; p++) {
+    snprintf(buf, sizeof(buf), "%.*g", p, v);
+    if (std::strtod(buf, nullptr) == v) break;
+  }
+  std::string r(buf);
+  const size_t e = r.find('e');
+  if (e != std::string::npos) {
+    const double ax = std::fabs(v);
+    if (ax >= 1e-4 && ax < 1e16) {  // repr switches to exponent form outside this range
+      snprintf(buf, sizeof(buf), "%.17f", v);
+      r = buf;
+      while (!r.empty() && r.back() == '0') r.pop_back();
+      for (int p = 1; p <= 17; p++) {  // shortest fixed-form digits
+        snprintf(buf, sizeof(buf), "%.*f", p, v);
+        if (std::strtod(buf, nullptr) == v) {
+          r = buf;
+          break;
+        }
+      }
+    } else {
+      std::string mant = r.substr(0, e), ex = r.substr(e + 1);
+      const char sign = ex[0] == '-' ? '-' : '+';
+      if (ex[0] == '-' || ex[0] == '+') ex = ex.substr(1);
+      while (ex.size() > 2 && ex[0] == '0') ex = ex.substr(1);
+      return mant + "e" + sign + ex;
+    }
+  }
+  if (r.find('.') == std::string::npos && r.find('e') == std::string::npos) r += ".0";
+  return r;
+}
+
 // core.validate (core.py:127-151): first failing field.
 int validate(const fga_params* p) {
   if (!p) {
@@ -156,7 +208,11 @@ int validate(const fga_params* p) {
   if (!(p->sigma > 0)) return invalid("sigma", p->sigma);
   if (!(p->rho >= 2)) return invalid("rho", p->rho);
   if (!(p->max_depth >= 1)) return invalid("max_depth", p->max_depth);
-  if (!(p->norm_a < p->norm_b)) return invalid("norm_range", p->norm_a);
+  if (!(p->norm_a < p->norm_b)) {  // InvalidParam("norm_range", params.norm_range)
+    set_error("invalid parameter norm_range=(" + py_repr(p->norm_a) + ", " + py_repr(p->norm_b) +
+              ")");
+    return FGA_ERR_INVALID;
+  }
   if (!(p->conv_tol > 0)) return invalid("conv_tol", p->conv_tol);
   if (!(p->max_iters >= 1)) return invalid("max_iters", p->max_iters);
   return FGA_OK;
@@ -269,9 +325,17 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
   launch_rescale(S.mx.as<double>(), n, S.my.as<double>(), m, S.P.dt, S.P.eta,
                  S.scratch.as<double>(), s);
   // reference side: tree (BH) and packed points (direct sum, energy)
-  if (!S.direct) {
-    TRY(tree_build_dev(c->tree, S.xn.as<double>(), S.mx.as<double>(), n, S.P.max_depth, s));
-    c->tree.dim = S.sp.dim;
+  if (!S.direct || S.P.theta == 0.0) {
+    TRY(tree_build_dev(S.tree, S.xn.as<double>(), S.mx.as<double>(), n, S.P.max_depth, s));
+    S.tree.dim = S.sp.dim;
+  }
+  if (S.P.theta == 0.0) {
+    // theta = 0 opens every cell, so the reference sums over the leaves
+    // (_kernels.py:30-42): the exact O(NM) sum equals that only when no leaf
+    // aggregates two distinct points; otherwise traverse the tree at theta=0
+    int shared = 0;
+    TRY(tree_any_shared_leaf(S.tree, s, &shared));
+    S.direct = !shared;
   }
   FGA_CUDA_TRY(S.ref32.reserve(sizeof(float4) * n));
   if (S.precision) FGA_CUDA_TRY(S.ref64.reserve(sizeof(double4) * n));
@@ -361,6 +425,7 @@ int session_begin_common(fga_ctx* c, int64_t n, int64_t m, int dim, const fga_pa
   S.sp.max_iters = params->max_iters;
   S.sp.m_total = m;
   S.sp.trace_gpe = S.O.trace_gpe;
+  S.sp.count_visits = S.O.count_visits ? 1 : 0;
   S.sp.dim = dim;
   S.gpe_initial = S.gpe_final = NAN;
   S.have_gpe_initial = S.have_gpe_final = false;
@@ -392,7 +457,7 @@ int session_forces(fga_ctx* c) {
     launch_direct_iterate(S.ref(), tv, S.st(), S.sp, S.partials.as<double>(), S.precision, s);
     nw = direct_iterate_warps(S.m_local, S.precision);
   } else {
-    launch_bh_iterate(c->tree, tv, S.st(), S.sp, S.partials.as<double>(), S.precision, s);
+    launch_bh_iterate(c->S.tree, tv, S.st(), S.sp, S.partials.as<double>(), S.precision, s);
     nw = bh_iterate_warps(S.m_local);
   }
   if (S.m_local <= 0) nw = 0;
@@ -519,6 +584,7 @@ int fga_destroy(fga_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   c->tree.release();
+  c->S.tree.release();
   c->tree_pts.release();
   c->tree_masses.release();
   for (auto& b : c->op) b.release();
@@ -668,7 +734,7 @@ int fga_session_apply_pending(fga_ctx* c) {
 int fga_session_info(fga_ctx* c, int64_t* m_local, int64_t* n_nodes) {
   SESSION_TRY(c);
   if (m_local) *m_local = c->S.m_local;
-  if (n_nodes) *n_nodes = c->S.direct ? 0 : c->tree.n_nodes;
+  if (n_nodes) *n_nodes = c->S.direct ? 0 : c->S.tree.n_nodes;
   return FGA_OK;
 }
 
@@ -807,7 +873,7 @@ int fga_session_finish(fga_ctx* c, fga_result* out, double* deltas, double* traj
       out->interactions += iv[k];
       out->visits += vv[k];
     }
-    out->n_nodes = S.direct ? 0 : c->tree.n_nodes;
+    out->n_nodes = S.direct ? 0 : S.tree.n_nodes;
     cudaEventElapsedTime(&S.setup_ms, c->ev[0], c->ev[1]);
     out->setup_ms = S.setup_ms;
     out->loop_ms = S.loop_ms;
@@ -1184,13 +1250,63 @@ int fga_tree_forces(fga_ctx* c, const double* queries, const double* qm, int64_t
   return FGA_OK;
 }
 
+namespace {
+// FNV-1a over ~4k evenly spaced 8-byte words of each array plus its last word
+// (~0.1 ms for a 1M-point tree): detects a different tree at a recycled
+// address; in-place edits of an uploaded tree are not supported (the
+// reference's BHTree is immutable, bhtree.py:14-45).
+uint64_t sampled_hash(uint64_t h, const void* base, int64_t words) {
+  const uint64_t* w = static_cast<const uint64_t*>(base);
+  if (!w || words <= 0) return h;
+  const int64_t step = std::max<int64_t>(1, words / 4096);
+  auto mix = [&](uint64_t v) {
+    for (int b = 0; b < 8; b++) {
+      h ^= (v >> (8 * b)) & 0xff;
+      h *= 1099511628211ull;
+    }
+  };
+  for (int64_t i = 0; i < words; i += step) mix(w[i]);
+  mix(w[words - 1]);
+  return h;
+}
+}  // namespace
+
+int fga_tree_generation(fga_ctx* c, int64_t* generation) {
+  CTX_TRY(c);
+  if (generation) *generation = (int64_t)c->tree.generation;
+  return FGA_OK;
+}
+
 int fga_bh_forces_kernel(fga_ctx* c, const int64_t* children, const double* com,
                          const double* mass, const double* length, int64_t n_nodes, int n_child,
                          const double* queries, const double* qm, int64_t m, int dim,
                          double theta, double G, double eps2, int64_t stack_cap, double* forces,
                          int64_t* visits) {
   (void)stack_cap;  // the stackless traversal needs no stack
-  TRY(fga_tree_upload(c, children, com, mass, length, n_nodes, n_child, dim));
+  CTX_TRY(c);
+  uint64_t h = 1469598103934665603ull;
+  h = sampled_hash(h, children, n_nodes * n_child);
+  h = sampled_hash(h, com, n_nodes * dim);
+  h = sampled_hash(h, mass, n_nodes);
+  h = sampled_hash(h, length, n_nodes);
+  fga_ctx::ShimKey& k = c->shim;
+  const bool hit = k.valid && k.generation == c->tree.generation && k.p[0] == children &&
+                   k.p[1] == com && k.p[2] == mass && k.p[3] == length && k.n_nodes == n_nodes &&
+                   k.n_child == n_child && k.dim == dim && k.hash == h;
+  if (!hit) {
+    k.valid = false;
+    TRY(fga_tree_upload(c, children, com, mass, length, n_nodes, n_child, dim));
+    k.p[0] = children;
+    k.p[1] = com;
+    k.p[2] = mass;
+    k.p[3] = length;
+    k.n_nodes = n_nodes;
+    k.n_child = n_child;
+    k.dim = dim;
+    k.hash = h;
+    k.generation = c->tree.generation;
+    k.valid = true;
+  }
   return fga_tree_forces(c, queries, qm, m, theta, G, eps2, FGA_PREC_FP64, forces, visits, nullptr);
 }
 

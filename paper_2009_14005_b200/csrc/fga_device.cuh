@@ -122,8 +122,30 @@ __device__ __forceinline__ int np_pairwise_depth(int64_t n, int dmax) {
   return d;
 }
 
+// Blocked summation of the FP32 force: the per-lane fp32 partial is folded
+// into an fp64 sum whenever the warp's node index passes the next multiple of
+// FGA_FOLD, so no fp32 sum runs over more than one chunk's terms.
+// tools/fp32_error.py (configs[2], 16k queries): one fp32 running sum over the
+// ~5.5k terms of a query limits the per-query error to 5.5e-5 relative;
+// folding every 4096 node indices into fp64 gives 2.0e-6 (fp32 terms summed
+// exactly: 0.9e-6).  The test rides on the loop's exit check, so it costs
+// nothing per step.
+#ifndef FGA_FOLD
+#define FGA_FOLD 4096
+#endif
+static_assert(FGA_FOLD >= 0, "FGA_FOLD: node-index chunk of the blocked force sum (0 = off)");
+__device__ __forceinline__ int fold_limit(int n, int n_nodes) {
+  if (FGA_FOLD <= 0) return n_nodes;
+  const int next = (n / FGA_FOLD + 1) * FGA_FOLD;
+  return next < n_nodes ? next : n_nodes;
+}
+
+struct NodeC32 {
+  float4 a, b;
+};
+
 struct Trav32Out {
-  float ax, ay, az;
+  double ax, ay, az;  // sum of m * (com - q) / r^3, fp32 terms, blocked sum
   int visits, accepted;
 };
 
@@ -165,7 +187,8 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
                                                 float gA, float gB, const double* qpx,
                                                 const double* qpy, const double* qpz, int64_t qi,
                                                 WinBuf32* win, int lane) {
-  float ax = 0.f, ay = 0.f, az = 0.f;
+  float ax = 0.f, ay = 0.f, az = 0.f;     // the current chunk's partial force
+  double hx = 0.0, hy = 0.0, hz = 0.0;  // folded chunks
   int visits = 0, accepted = 0;
   int cursor = active ? 0 : n_nodes;
   int wbase = INT_MIN / 2;
@@ -173,9 +196,17 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
   // one band per warp: the largest lane delta (inactive lanes pass 0)
   gA = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gA)));
   gB = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gB)));
+  int lim = fold_limit(0, n_nodes);
   while (true) {
     const int n = __reduce_min_sync(0xffffffffu, cursor);
-    if (n >= n_nodes) break;
+    if (n >= lim) {  // exit, or fold the chunk's partial into the running sum
+      if (n >= n_nodes) break;
+      hx += (double)ax;
+      hy += (double)ay;
+      hz += (double)az;
+      ax = ay = az = 0.f;
+      lim = fold_limit(n, n_nodes);
+    }
     float4 a, b;
     if constexpr (kW == 0) {
       a = __ldg(&A[n]);
@@ -225,7 +256,78 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
     const int next = acc ? __float_as_int(b.y) : n + 1;
     cursor = mine ? next : cursor;
   }
-  return Trav32Out{ax, ay, az, visits, accepted};
+  return Trav32Out{hx + (double)ax, hy + (double)ay, hz + (double)az, visits, accepted};
+}
+
+// Direct FP32 traversal (the single-pair force passes, forces.cu): every step
+// reads node n's packed 32 B record (TreeRecords::c32) with two warp-uniform
+// (broadcast) loads through L1 -- consecutive nodes share cache lines and the
+// warps of an SM walk neighbouring regions -- instead of staging a 32-node
+// window through shared memory (a per-lane LDG + 2 STS refill on ~37% of the
+// steps: 15.85 -> 14.1 ms per 1M iteration).  The record carries this
+// launch's guard band and l^2 + theta^2 eps^2 (launch_node_bands), so the MAC
+// is one FFMA on d^2 + eps^2 (which the force needs anyway):
+//   diff = theta^2 (d^2 + eps^2) - (l^2 + theta^2 eps^2),
+// accept iff diff > 0, and re-decide in fp64 iff |diff| <= band (14.1 ->
+// 13.5 ms).  Visits are counted only when asked (kCountVisits; 2.5% of the
+// step).
+template <bool kGuardZero, bool kCountVisits>
+__device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
+                                                 const double4* __restrict__ A64,
+                                                 const NodeB64* __restrict__ B64, int n_nodes,
+                                                 float qx, float qy, float qz, bool active,
+                                                 float theta2, double theta2_64, float eps2,
+                                                 const double* qpx, const double* qpy,
+                                                 const double* qpz, int64_t qi) {
+  float ax = 0.f, ay = 0.f, az = 0.f;     // the current chunk's partial force
+  double hx = 0.0, hy = 0.0, hz = 0.0;  // folded chunks
+  int visits = 0, accepted = 0;
+  int cursor = active ? 0 : n_nodes;
+  const int64_t qs = active ? qi : 0;  // inactive lanes join the exact re-check
+  int lim = fold_limit(0, n_nodes);
+  while (true) {
+    const int n = __reduce_min_sync(0xffffffffu, cursor);
+    if (n >= lim) {  // exit, or fold the chunk's partial into the fp64 sum
+      if (n >= n_nodes) break;
+      hx += (double)ax;
+      hy += (double)ay;
+      hz += (double)az;
+      ax = ay = az = 0.f;
+      lim = fold_limit(n, n_nodes);
+    }
+    const NodeC32* rec = reinterpret_cast<const NodeC32*>(C) + n;
+    const float4 a = __ldg(&rec->a);
+    const float4 b = __ldg(&rec->b);
+    const bool mine = cursor == n;
+    const float dx = a.x - qx, dy = a.y - qy, dz = a.z - qz;
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, eps2)));  // d^2 + eps^2
+    const float diff = fmaf(theta2, r2, -b.x);
+    bool acc = diff > 0.f;
+    const bool near = mine && fabsf(diff) <= b.z;
+    if (__any_sync(0xffffffffu, near)) {  // warp-uniform branch, rarely taken
+      const bool e = mac_exact(A64, B64, n, qpx[qs], qpy[qs], qpz[qs], theta2_64);
+      acc = near ? e : acc;
+    }
+    const bool take = mine && acc;
+    const float inv = rsqrt_approx(r2);
+    float w = a.w * (inv * inv * inv);
+    if (!take) w = 0.f;
+    if (kGuardZero && !(r2 > 0.f)) w = 0.f;  // reference skips d2+eps2 == 0 (:39)
+    ax = fmaf(w, dx, ax);
+    ay = fmaf(w, dy, ay);
+    az = fmaf(w, dz, az);
+    if constexpr (kCountVisits) {
+      asm("{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %2, 0;\n\tsetp.ne.b32 q, %3, 0;\n\t"
+          "@p add.s32 %0, %0, 1;\n\t@q add.s32 %1, %1, 1;\n\t}"
+          : "+r"(visits), "+r"(accepted) : "r"((int)mine), "r"((int)take));
+    } else {
+      asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t@q add.s32 %0, %0, 1;\n\t}"
+          : "+r"(accepted) : "r"((int)take));
+    }
+    const int next = acc ? __float_as_int(b.y) : n + 1;
+    cursor = mine ? next : cursor;
+  }
+  return Trav32Out{hx + (double)ax, hy + (double)ay, hz + (double)az, visits, accepted};
 }
 
 struct Trav64Out {

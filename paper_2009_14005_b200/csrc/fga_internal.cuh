@@ -60,6 +60,7 @@ struct SimParams {
   long long m_total;  // template size across all shards (Kabsch mean divisor)
   int trace_gpe;
   int dim;            // 2 or 3 (2-D clouds are carried as z = const)
+  int count_visits;   // FP32 force pass counts node visits (fga_options.count_visits)
 };
 
 // ---------------------------------------------------------------- errors

@@ -34,36 +34,28 @@ namespace fga {
 namespace {
 
 // ---------------------------------------------------------------- BH iterate
-template <typename Real>
-struct WinOf;
-template <>
-struct WinOf<float> {
-  using T = WinBuf32;
-};
-template <>
-struct WinOf<double> {
-  using T = Win64;
-};
-
 struct F32Params {
   float theta2, eps2;
 };
 
-// (1280 threads/SM = 48 registers: 1536 / 1792 spill and ran 15% / 28% slower)
-#ifndef FGA_BH64_TPS
-#define FGA_BH64_TPS 1280  // fp64 traversal: 768 -> 35.8 ms, 1024 -> 31.5, 1280 -> 30.3, 1536 -> 38 (spills)
+// Resident threads per SM: FP32 traversal 1280 (48 registers; 1024 with 64
+// registers: 15.3 vs 13.5 ms, 1536 with 40 registers + spills: 13.5);
+// fp64 traversal: 768 -> 35.8 ms, 1024 -> 31.5, 1280 -> 30.3, 1536 -> 38 (spills)
+#ifndef FGA_BH32_TPS
+#define FGA_BH32_TPS 1280
 #endif
-template <typename Real, bool kGuardZero, int kT, int kW = kWin>
-__global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? 1280 : FGA_BH64_TPS) / kT) k_bh_iterate(
+#ifndef FGA_BH64_TPS
+#define FGA_BH64_TPS 1280
+#endif
+template <typename Real, bool kGuardZero, bool kCountVisits, int kT>
+__global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? FGA_BH32_TPS : FGA_BH64_TPS) / kT) k_bh_iterate(
     TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, SimParams sp,
-    F32Params f, double* partials, float cmag, int nblocks, int per_sm) {
+    F32Params f, double* partials, int nblocks) {
   if (st->done) return;
   // (An SM-contiguous block->chunk remap for L1 sharing was measured 3%
   // slower -- per-SM load imbalance -- so blocks map to chunks in order.)
-  (void)per_sm;
   const int chunk = (int)blockIdx.x;
   if (chunk >= nblocks) return;
-  __shared__ typename WinOf<Real>::T wins[kT / 32];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t gw = (int64_t)chunk * (kT / 32) + wl;
   const int64_t i = gw * 32 + lane;
@@ -88,19 +80,17 @@ __global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? 1280 : FGA_BH64_TPS) 
   double F[3];
   int nv, na;
   if constexpr (sizeof(Real) == 4) {
-    const float qx = (float)y[0], qy = (float)y[1], qz = (float)y[2];
-    float gA, gB;
-    guard_coeffs(fmaxf(fabsf(qx), fmaxf(fabsf(qy), fabsf(qz))), cmag, f.theta2, gA, gB);
-    Trav32Out o = traverse32<kGuardZero, kW>(tr.a32, tr.b32, tr.a64, tr.b64, n_nodes, qx, qy, qz,
-                                             active, f.theta2, sp.theta2, f.eps2, gA, gB, tv.px,
-                                         tv.py, tv.pz, i, &wins[wl], lane);
+    const Trav32Out o = traverse32d<kGuardZero, kCountVisits>(
+        tr.c32, tr.a64, tr.b64, n_nodes, (float)y[0], (float)y[1], (float)y[2], active, f.theta2,
+        sp.theta2, f.eps2, tv.px, tv.py, tv.pz, i);
     const double gq = sp.G * mq;
-    F[0] = gq * (double)o.ax;
-    F[1] = gq * (double)o.ay;
-    F[2] = gq * (double)o.az;
+    F[0] = gq * o.ax;
+    F[1] = gq * o.ay;
+    F[2] = gq * o.az;
     nv = o.visits;
     na = o.accepted;
   } else {
+    __shared__ Win64 wins[kT / 32];
     Trav64Out o = traverse64(tr.a64, tr.b64, n_nodes, y[0], y[1], y[2], __dmul_rn(sp.G, mq),
                              active, sp.theta2, sp.eps2, &wins[wl], lane);
     F[0] = o.fx;
@@ -145,8 +135,7 @@ __global__ void __launch_bounds__(kForceThreads, FGA_BHOP_MINB) k_bh_operator(
     TreeRecords tr, int n_nodes, const double* __restrict__ qx_, const double* __restrict__ qy_,
     const double* __restrict__ qz_, const double* __restrict__ qm_, const int* __restrict__ order,
     int64_t m, double theta2, double G, double eps2, F32Params f, double* __restrict__ fout,
-    long long* __restrict__ visits, long long* __restrict__ accepted, float cmag) {
-  __shared__ typename WinOf<Real>::T wins[kWarps];
+    long long* __restrict__ visits, long long* __restrict__ accepted) {
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t i = ((int64_t)blockIdx.x * kWarps + wl) * 32 + lane;
   const bool active = i < m;
@@ -160,19 +149,17 @@ __global__ void __launch_bounds__(kForceThreads, FGA_BHOP_MINB) k_bh_operator(
   double F[3];
   int nv, na;
   if constexpr (sizeof(Real) == 4) {
-    const float fx = (float)q[0], fy = (float)q[1], fz = (float)q[2];
-    float gA, gB;
-    guard_coeffs(fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))), cmag, f.theta2, gA, gB);
-    Trav32Out o = traverse32<kGuardZero>(tr.a32, tr.b32, tr.a64, tr.b64, n_nodes, fx, fy, fz,
-                                         active, f.theta2, theta2, f.eps2, gA, gB, qx_, qy_, qz_,
-                                         i, &wins[wl], lane);
+    const Trav32Out o = traverse32d<kGuardZero, true>(
+        tr.c32, tr.a64, tr.b64, n_nodes, (float)q[0], (float)q[1], (float)q[2], active, f.theta2,
+        theta2, f.eps2, qx_, qy_, qz_, i);
     const double gq = G * qm;
-    F[0] = gq * (double)o.ax;
-    F[1] = gq * (double)o.ay;
-    F[2] = gq * (double)o.az;
+    F[0] = gq * o.ax;
+    F[1] = gq * o.ay;
+    F[2] = gq * o.az;
     nv = o.visits;
     na = o.accepted;
   } else {
+    __shared__ Win64 wins[kWarps];
     Trav64Out o = traverse64(tr.a64, tr.b64, n_nodes, q[0], q[1], q[2], __dmul_rn(G, qm), active,
                              theta2, eps2, &wins[wl], lane);
     F[0] = o.fx;
@@ -514,12 +501,28 @@ constexpr int kGpeQ = 4;
 struct GpeShape {
   int64_t qblocks, splits, seg;
 };
+// SM count of the current device (cached per device)
+static int current_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = sms > 0 ? sms : 148;
+  }
+  return cache[dev];
+}
+
 static GpeShape gpe_shape(int64_t m, int64_t n, int precision) {
   const int64_t per = precision ? kForceThreads : kForceThreads * kGpeQ;
   const int64_t tile = precision ? kTile / 2 : kTile;
   GpeShape g;
   g.qblocks = grid_for(m, per);
-  int64_t sp = (2 * 3 * 148 + g.qblocks - 1) / g.qblocks;  // two waves of 3 blocks per SM
+  // two waves of the resident blocks (FGA_GPE_MINB per SM for k_gpe32)
+  const int64_t resident = (int64_t)current_sms() * (precision ? 3 : FGA_GPE_MINB);
+  int64_t sp = (2 * resident + g.qblocks - 1) / g.qblocks;
   sp = std::max<int64_t>(1, std::min<int64_t>(sp, n / (4 * tile)));  // >= 4 tiles per segment
   const int64_t tiles = (n + tile - 1) / tile;
   g.seg = ((tiles + sp - 1) / sp) * tile;
@@ -531,26 +534,99 @@ int64_t gpe_warps(int64_t m, int64_t n, int precision) {
   return g.qblocks * g.splits * kWarps;
 }
 
+static int current_sms();
+
+// ------------------------------------------------------- per-launch node bands
+// The FP32 MAC guard band of every node for this launch's
+// queries: delta = (max |q| + max |com|) 2^-24 over ALL queries (a global
+// bound instead of the warp's), so the band is a per-node constant that the
+// traversal reads from the record instead of forming it per step.  Also
+// folds eps^2 into the record's l^2 (see traverse32d<kBand>): the fma-form
+// MAC then adds <= 3u (l^2 + theta^2 eps^2) of rounding, covered by the
+// 16u l^2 and 4u theta^2 eps^2 terms.
+template <bool kPending>
+__global__ void __launch_bounds__(256) k_qbound(const double* __restrict__ px,
+                                                const double* __restrict__ py,
+                                                const double* __restrict__ pz, int64_t m,
+                                                const IterState* __restrict__ st,
+                                                unsigned* __restrict__ out) {
+  if (kPending && st->done) return;
+  float mx = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double y[3] = {px[i], py[i], pz[i]};
+    if constexpr (kPending) {
+      double v[3] = {0, 0, 0};
+      apply_pending(st, y, v);
+    }
+    const double a = fmax(fabs(y[0]), fmax(fabs(y[1]), fabs(y[2])));
+    mx = fmaxf(mx, __double2float_ru(a));
+  }
+  mx = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(mx)));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(mx));
+}
+
+__global__ void __launch_bounds__(256) k_node_bands(float4* __restrict__ c32, int nn, float theta2,
+                                                    float eps2, float cmag,
+                                                    const unsigned* __restrict__ qbound,
+                                                    const IterState* __restrict__ st) {
+  if (st && st->done) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nn) return;
+  float4 r = c32[2 * i + 1];
+  const float l2 = r.w;  // the node's l^2 as built (-inf: leaf)
+  if (l2 == -INFINITY) {
+    r.x = -INFINITY;  // always accepted, never re-checked
+    r.z = -INFINITY;
+  } else {
+    const float te = theta2 * eps2;
+    const float delta = (__uint_as_float(*qbound) + cmag) * 5.97e-8f;
+    const float gA = 4.34f * delta * sqrtf(theta2);  // 1.25 * 2 sqrt3 delta theta
+    const float gB = 34.f * delta * delta * theta2 + 4.f * 5.97e-8f * te + 1e-37f;
+    r.x = l2 + te;
+    r.z = fmaf(gA, sqrtf(l2), fmaf(16.f * 5.97e-8f, l2, gB));
+  }
+  c32[2 * i + 1] = r;
+}
+
+static void launch_node_bands(const TreeDev& T, const double* px, const double* py,
+                              const double* pz, int64_t m, const IterState* st, float theta2,
+                              float eps2, cudaStream_t s) {
+  unsigned* qb = T.band_scratch.as<unsigned>();
+  cudaMemsetAsync(qb, 0, sizeof(unsigned), s);
+  const int g = (int)std::min<int64_t>(grid_for(m, 256), 4 * current_sms());
+  if (st)
+    k_qbound<true><<<g, 256, 0, s>>>(px, py, pz, m, st, qb);
+  else
+    k_qbound<false><<<g, 256, 0, s>>>(px, py, pz, m, nullptr, qb);
+  const int nn = (int)T.n_nodes;
+  k_node_bands<<<(nn + 255) / 256, 256, 0, s>>>(T.records().c32, nn, theta2, eps2, (float)T.cmag,
+                                                qb, st);
+}
+
 template <int kT>
 static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const IterState* st,
                                 const SimParams& sp, double* partials, int precision,
                                 cudaStream_t s) {
   const int nb = (int)grid_for(tv.m, kT);
-  const int per = 0;
   const unsigned g = (unsigned)nb;
   const F32Params f{(float)sp.theta2, (float)sp.eps2};
   const bool gz = !(sp.eps2 > 0.0);
   const int nn = (int)T.n_nodes;
-  const float cm = (float)T.cmag;
-  if (precision)
-    k_bh_iterate<double, false, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm,
-                                                     nb, per);
+  const TreeRecords r = T.records();
+  if (precision) {
+    k_bh_iterate<double, false, true, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb);
+    return;
+  }
+  launch_node_bands(T, tv.px, tv.py, tv.pz, tv.m, st, f.theta2, f.eps2, s);
+  if (gz && sp.count_visits)
+    k_bh_iterate<float, true, true, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb);
   else if (gz)
-    k_bh_iterate<float, true, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm,
-                                                   nb, per);
+    k_bh_iterate<float, true, false, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb);
+  else if (sp.count_visits)
+    k_bh_iterate<float, false, true, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb);
   else
-    k_bh_iterate<float, false, kT><<<g, kT, 0, s>>>(T.records(), nn, tv, st, sp, f, partials, cm,
-                                                    nb, per);
+    k_bh_iterate<float, false, false, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb);
 }
 
 void launch_bh_iterate(const TreeDev& T, const TemplateView& tv, const IterState* st,
@@ -604,19 +680,21 @@ void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, co
   const double theta2 = theta * theta;
   const F32Params f{(float)theta2, (float)eps2};
   const int nn = (int)T.n_nodes;
-  const float cm = (float)T.cmag;
-  if (precision)
-    k_bh_operator<double, false><<<g, kForceThreads, 0, s>>>(T.records(), nn, qx, qy, qz, qm,
-                                                             order, m, theta2, G, eps2, f, fout,
-                                                             visits, accepted, cm);
-  else if (!(eps2 > 0.0))
-    k_bh_operator<float, true><<<g, kForceThreads, 0, s>>>(T.records(), nn, qx, qy, qz, qm,
-                                                           order, m, theta2, G, eps2, f, fout,
-                                                           visits, accepted, cm);
+  const TreeRecords r = T.records();
+  if (precision) {
+    k_bh_operator<double, false><<<g, kForceThreads, 0, s>>>(r, nn, qx, qy, qz, qm, order, m,
+                                                             theta2, G, eps2, f, fout, visits,
+                                                             accepted);
+    return;
+  }
+  launch_node_bands(T, qx, qy, qz, m, nullptr, f.theta2, f.eps2, s);
+  if (!(eps2 > 0.0))
+    k_bh_operator<float, true><<<g, kForceThreads, 0, s>>>(r, nn, qx, qy, qz, qm, order, m, theta2,
+                                                           G, eps2, f, fout, visits, accepted);
   else
-    k_bh_operator<float, false><<<g, kForceThreads, 0, s>>>(T.records(), nn, qx, qy, qz, qm,
-                                                            order, m, theta2, G, eps2, f, fout,
-                                                            visits, accepted, cm);
+    k_bh_operator<float, false><<<g, kForceThreads, 0, s>>>(r, nn, qx, qy, qz, qm, order, m,
+                                                            theta2, G, eps2, f, fout, visits,
+                                                            accepted);
 }
 
 void launch_direct_operator(const RefPoints& ref, const double* qx, const double* qy,

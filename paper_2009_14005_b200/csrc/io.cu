@@ -17,7 +17,7 @@
 //   * load_weights: file iteration lines (\n, \r\n, \r), strip(), skip blank
 //     and '#', one float per line.
 // Anything these parsers do not accept (including every malformed file and
-// any byte >= 0x80) returns FGA_ERR_PARSE; the Python layer then re-reads
+// any byte >= 0x80 outside a '#' comment line) returns FGA_ERR_PARSE; the Python layer then re-reads
 // the file with its own port of io.py so the exception (class, line number,
 // message) is exactly the reference's.  So the native path may be stricter
 // than the reference, never more lenient.
@@ -175,9 +175,54 @@ int threads_for(size_t bytes) {
   return by_size < t ? by_size : t;
 }
 
-bool ascii_only(const char* b, size_t n) {
-  for (size_t i = 0; i < n; i++)
-    if ((unsigned char)b[i] >= 0x80) return false;
+// Non-ASCII text is accepted only inside whole-line '#' comments (the lines
+// both readers skip, io.py:27-28), as well-formed UTF-8 (what open() decodes;
+// anything else raises in the reference) that encodes no line break
+// (U+0085, U+2028, U+2029 split lines in str.splitlines()).  Lines are cut at
+// the superset of both readers' breaks, so this may reject (-> the Python
+// reader) but never accept text the reference reads differently.
+bool nonascii_only_in_comments(const char* b, size_t n) {
+  bool line_start = true, comment = false;
+  for (size_t i = 0; i < n;) {
+    const unsigned char c = (unsigned char)b[i];
+    if (c < 0x80) {
+      if (is_break_splitlines(c)) {
+        line_start = true;
+        comment = false;
+      } else if (line_start && !is_space(c)) {
+        line_start = false;
+        comment = c == '#';
+      }
+      i++;
+      continue;
+    }
+    if (!comment) return false;
+    int len;
+    uint32_t cp;
+    if (c >= 0xc2 && c <= 0xdf) {
+      len = 2;
+      cp = c & 0x1f;
+    } else if (c >= 0xe0 && c <= 0xef) {
+      len = 3;
+      cp = c & 0x0f;
+    } else if (c >= 0xf0 && c <= 0xf4) {
+      len = 4;
+      cp = c & 0x07;
+    } else {
+      return false;  // continuation byte, overlong lead or > U+10FFFF
+    }
+    if (i + len > n) return false;
+    for (int k = 1; k < len; k++) {
+      const unsigned char d = (unsigned char)b[i + k];
+      if ((d & 0xc0) != 0x80) return false;
+      cp = (cp << 6) | (d & 0x3f);
+    }
+    if ((len == 3 && cp < 0x800) || (len == 4 && (cp < 0x10000 || cp > 0x10ffff)) ||
+        (cp >= 0xd800 && cp <= 0xdfff))
+      return false;  // overlong, out of range or a surrogate
+    if (cp == 0x85 || cp == 0x2028 || cp == 0x2029) return false;
+    i += len;
+  }
   return true;
 }
 
@@ -285,8 +330,8 @@ int fga_parse_cloud(const char* text, int64_t len, double* out, int64_t cap, int
   cache = ParseCache();
   const char* b = text;
   const char* e = text + len;
-  if (!ascii_only(b, (size_t)len)) {
-    set_error("parse_cloud: non-ASCII input (left to the Python reader)");
+  if (!nonascii_only_in_comments(b, (size_t)len)) {
+    set_error("parse_cloud: non-ASCII input outside comments (left to the Python reader)");
     return FGA_ERR_PARSE;
   }
   // sniff the first non-blank line (io.py:14-20)
@@ -475,8 +520,8 @@ int fga_parse_weights(const char* text, int64_t len, double* out, int64_t cap, i
   cache = ParseCache();
   const char* b = text;
   const char* e = text + len;
-  if (!ascii_only(b, (size_t)len)) {
-    set_error("parse_weights: non-ASCII input (left to the Python reader)");
+  if (!nonascii_only_in_comments(b, (size_t)len)) {
+    set_error("parse_weights: non-ASCII input outside comments (left to the Python reader)");
     return FGA_ERR_PARSE;
   }
   const int T = threads_for((size_t)len);

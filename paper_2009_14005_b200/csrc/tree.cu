@@ -34,6 +34,8 @@
 //   k_crossing      nodes that cross block boundaries: partials combined
 #include <cub/cub.cuh>
 
+#include <cstring>
+
 #include "fga_internal.cuh"
 #include "fga_tree.cuh"
 #include "fga_device.cuh"
@@ -373,12 +375,13 @@ __device__ __forceinline__ void write_records_b(const TreeRecords& r, int mir, i
                                                 double len) {
   const double l2 = __dmul_rn(len, len);
   r.b64[mir] = NodeB64{leaf ? -INFINITY : l2, (long long)rskip};
-  r.b32[mir] = NodeB32{leaf ? -INFINITY : (float)l2, rskip};
+  const float l2f = leaf ? -INFINITY : (float)l2;
+  r.c32[2 * mir + 1] = make_float4(l2f, __int_as_float(rskip), 0.f, l2f);
 }
 __device__ __forceinline__ void write_records_a(const TreeRecords& r, int mir, const double4& v) {
   const double cx = __ddiv_rn(v.y, v.x), cy = __ddiv_rn(v.z, v.x), cz = __ddiv_rn(v.w, v.x);
   r.a64[mir] = make_double4(cx, cy, cz, v.x);
-  r.a32[mir] = make_float4((float)cx, (float)cy, (float)cz, (float)v.x);
+  r.c32[2 * mir] = make_float4((float)cx, (float)cy, (float)cz, (float)v.x);
 }
 
 // ---------------------------------------------------------------- hierarchy
@@ -890,6 +893,7 @@ __global__ void __launch_bounds__(256) k_export(const unsigned long long* __rest
 // ------------------------------------------------------------------ host side
 int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, int64_t n, int L,
                    cudaStream_t st) {
+  T.generation++;  // any (re)build, even a failed one, invalidates cached host views
   if (n <= 0) {
     set_error("tree build: empty cloud");
     return FGA_ERR_EMPTY;
@@ -1010,8 +1014,8 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   for (int k = 0; k < 6; k++) T.box_host[k] = box[k];
 
   const int64_t nn64 = nn;
-  FGA_CUDA_TRY(T.a32.reserve(sizeof(float4) * nn64));
-  FGA_CUDA_TRY(T.b32.reserve(sizeof(NodeB32) * nn64));
+  FGA_CUDA_TRY(T.c32.reserve(2 * sizeof(float4) * nn64));
+  FGA_CUDA_TRY(T.band_scratch.reserve(64));
   FGA_CUDA_TRY(T.a64.reserve(sizeof(double4) * nn64));
   FGA_CUDA_TRY(T.b64.reserve(sizeof(NodeB64) * nn64));
   const int nbs = (int)((n + kST - 1) / kST);
@@ -1051,6 +1055,30 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   }
   FGA_CUDA_TRY(cudaGetLastError());
   T.exportable = true;
+  return FGA_OK;
+}
+
+namespace {
+// a depth-cap leaf holding two distinct points (equal full keys, different
+// coordinates): the only way a leaf aggregates more than one position
+__global__ void k_shared_leaf(const double4* __restrict__ sp, const signed char* __restrict__ clev,
+                              int64_t n, int L, int* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + 1;
+  if (i >= n || clev[i] < L) return;
+  const double4 a = sp[i - 1], b = sp[i];
+  if (a.x != b.x || a.y != b.y || a.z != b.z) atomicOr(flag, 1);
+}
+}  // namespace
+
+int tree_any_shared_leaf(TreeDev& T, cudaStream_t st, int* host_flag) {
+  *host_flag = 0;
+  if (!T.exportable || T.n_points < 2) return FGA_OK;
+  int* f = T.flags.as<int>() + 1;
+  FGA_CUDA_TRY(cudaMemsetAsync(f, 0, sizeof(int), st));
+  k_shared_leaf<<<blocks_for(T.n_points - 1), kThreads, 0, st>>>(
+      T.sp.as<double4>(), T.clev.as<signed char>(), T.n_points, T.L, f);
+  FGA_CUDA_TRY(cudaMemcpyAsync(host_flag, f, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FGA_CUDA_TRY(cudaStreamSynchronize(st));
   return FGA_OK;
 }
 
@@ -1102,6 +1130,7 @@ int tree_export_host(TreeDev& T, cudaStream_t st, int64_t* children, double* com
 // present child, depth from the parents.
 int tree_upload_host(TreeDev& T, const int64_t* children, const double* com, const double* mass,
                      const double* length, int64_t nn, int n_child, cudaStream_t st) {
+  T.generation++;
   if (nn <= 0 || n_child != 8) {
     set_error("tree upload: need a non-empty 3-D tree (8 child slots)");
     return nn <= 0 ? FGA_ERR_EMPTY : FGA_ERR_UNSUPPORTED;
@@ -1126,8 +1155,7 @@ int tree_upload_host(TreeDev& T, const int64_t* children, const double* com, con
   }
   std::vector<double4> a64(nn);
   std::vector<NodeB64> b64(nn);
-  std::vector<float4> a32(nn);
-  std::vector<NodeB32> b32(nn);
+  std::vector<float4> c32(2 * nn);
   double cmag = 0.0;
   for (int64_t x = 0; x < nn; x++) {
     bool leaf = true;
@@ -1138,17 +1166,21 @@ int tree_upload_host(TreeDev& T, const int64_t* children, const double* com, con
     const double l2 = length[x] * length[x];
     a64[mir] = make_double4(com[x * 3], com[x * 3 + 1], com[x * 3 + 2], mass[x]);
     b64[mir] = NodeB64{leaf ? -INFINITY : l2, (long long)(mir + size)};
-    a32[mir] = make_float4((float)com[x * 3], (float)com[x * 3 + 1], (float)com[x * 3 + 2],
-                           (float)mass[x]);
-    b32[mir] = NodeB32{leaf ? -INFINITY : (float)l2, (int)(mir + size)};
+    c32[2 * mir] = make_float4((float)com[x * 3], (float)com[x * 3 + 1], (float)com[x * 3 + 2],
+                               (float)mass[x]);
+    const float l2f = leaf ? -INFINITY : (float)l2;
+    float skipf;
+    const int skipi = (int)(mir + size);
+    std::memcpy(&skipf, &skipi, sizeof(float));
+    c32[2 * mir + 1] = make_float4(l2f, skipf, 0.f, l2f);
     for (int k = 0; k < 3; k++) cmag = std::max(cmag, std::fabs(com[x * 3 + k]));
   }
-  FGA_CUDA_TRY(T.a32.reserve(sizeof(float4) * nn));
-  FGA_CUDA_TRY(T.b32.reserve(sizeof(NodeB32) * nn));
   FGA_CUDA_TRY(T.a64.reserve(sizeof(double4) * nn));
   FGA_CUDA_TRY(T.b64.reserve(sizeof(NodeB64) * nn));
-  FGA_CUDA_TRY(cudaMemcpyAsync(T.a32.p, a32.data(), sizeof(float4) * nn, cudaMemcpyHostToDevice, st));
-  FGA_CUDA_TRY(cudaMemcpyAsync(T.b32.p, b32.data(), sizeof(NodeB32) * nn, cudaMemcpyHostToDevice, st));
+  FGA_CUDA_TRY(T.c32.reserve(2 * sizeof(float4) * nn));
+  FGA_CUDA_TRY(T.band_scratch.reserve(64));
+  FGA_CUDA_TRY(cudaMemcpyAsync(T.c32.p, c32.data(), 2 * sizeof(float4) * nn, cudaMemcpyHostToDevice,
+                               st));
   FGA_CUDA_TRY(cudaMemcpyAsync(T.a64.p, a64.data(), sizeof(double4) * nn, cudaMemcpyHostToDevice, st));
   FGA_CUDA_TRY(cudaMemcpyAsync(T.b64.p, b64.data(), sizeof(NodeB64) * nn, cudaMemcpyHostToDevice, st));
   FGA_CUDA_TRY(cudaStreamSynchronize(st));

@@ -5,7 +5,8 @@ default (SPM) mass field on the registration path -- runs on the device
 (libfga ``fga_niv_masses``, bit-identical to masses.py:85-116).
 ``external_masses`` and ``spm`` are the reference's O(N) validation /
 element-wise glue (masses.py:119-135).  The RBF landmark field
-(masses.py:55-82) is not built on the B200 path yet.
+(masses.py:55-82) runs on the device too (``rbf_masses`` -> libfga
+``fga_rbf_masses``, csrc/rbf.cu).
 """
 
 from __future__ import annotations

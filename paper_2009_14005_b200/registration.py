@@ -54,6 +54,7 @@ class RegisterOptions:
     compute_gpe: bool = True
     mass_field: str = "niv"   # "niv" (reference SPM default) or "knn" (configs[3])
     knn_k: int = 16
+    count_visits: bool = False  # FP32 pass also counts node visits (2.5% slower)
 
 
 def _c_options(options: RegisterOptions, xw, yw, lm=None) -> N.COptions:
@@ -67,7 +68,8 @@ def _c_options(options: RegisterOptions, xw, yw, lm=None) -> N.COptions:
                       N.ptr(xw), N.ptr(yw), int(options.poll_every),
                       int(bool(options.compute_gpe)), 1 if options.mass_field == "knn" else 0,
                       int(options.knn_k), N.ptr(lm[0]) if lm else None,
-                      N.ptr(lm[1]) if lm else None, len(lm[0]) if lm else 0, 0)
+                      N.ptr(lm[1]) if lm else None, len(lm[0]) if lm else 0,
+                      int(bool(options.count_visits)))
 
 
 def _check_inputs(x, y, landmarks, params, options):
@@ -150,6 +152,7 @@ class BatchResult:
     results: list
     errors: list
     interactions: np.ndarray | None = None
+    status: np.ndarray | None = None  # per-pair FGA_* return code
 
 
 def register_batch(pairs, params: FgaParams | None = None,
@@ -164,7 +167,7 @@ def register_batch(pairs, params: FgaParams | None = None,
     pairs = list(pairs)
     P = len(pairs)
     if P == 0:
-        return BatchResult([], [], np.zeros(0, np.int64))
+        return BatchResult([], [], np.zeros(0, np.int64), np.zeros(0, np.int32))
     xs, ys = [], []
     for x, y in pairs:
         if x.dim != y.dim:
@@ -194,8 +197,10 @@ def register_batch(pairs, params: FgaParams | None = None,
                                        N.ctypes.addressof(out), N.ptr(deltas)))
     results, errors = [], []
     inter = np.zeros(P, np.int64)
+    status = np.zeros(P, np.int32)
     for i, r in enumerate(out):
         inter[i] = r.interactions
+        status[i] = r.status
         if r.status != 0:
             results.append(None)
             errors.append(N.error_for(r.status, f"pair {i}"))
@@ -211,7 +216,7 @@ def register_batch(pairs, params: FgaParams | None = None,
             gpe_final=float(r.gpe_final) if options.compute_gpe else None,
             records=recs, interactions=None))
         errors.append(None)
-    return BatchResult(results, errors, inter)
+    return BatchResult(results, errors, inter, status)
 
 
 @dataclass
@@ -245,38 +250,47 @@ def register_sequence(frames, params: FgaParams | None = None,
     small = (max(len(f) for f in frames) <= 8192 and all(f.dim == 3 for f in frames)
              and options.x_weights is None
              and options.y_weights is None and options.mass_field == "niv"
-             and options.precision == "fp32" and not options.trace_gpe and options.normalize)
-    pairwise, failed = [], []
+             and options.precision == "fp32" and not options.trace_gpe and options.normalize
+             and params.max_depth <= 21)
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(k):
+        x, y = pairs[k]
+        try:
+            return register(x=x, y=y, params=params, options=options).transform, False
+        except DeviceError:
+            raise
+        except GravregError:
+            return RigidTransform.identity(frames[k].dim), True
+
+    def run_threaded(ks):
+        n_workers = workers or min(4, len(ks))
+        if n_workers <= 1 or len(ks) <= 1:
+            return [one(k) for k in ks]
+        with ThreadPoolExecutor(max_workers=n_workers) as pool:
+            return list(pool.map(one, ks))
+
+    outs = [None] * len(pairs)
     if small:
         br = register_batch(pairs, params=params, options=options)
+        rerun = []
         for k, (res, err) in enumerate(zip(br.results, br.errors)):
-            if err is not None and not isinstance(err, GravregError):
+            if br.status[k] == N.FGA_ERR_UNSUPPORTED:
+                # over the batched kernel's per-pair limits (e.g. a single-child
+                # chain of near-duplicates past its node cap): register() runs it
+                rerun.append(k)
+                continue
+            if err is not None and (not isinstance(err, GravregError)
+                                    or isinstance(err, DeviceError)):
                 raise err
-            if isinstance(err, DeviceError):
-                raise err
-            pairwise.append(res.transform if res is not None else
-                            RigidTransform.identity(frames[k].dim))
-            failed.append(res is None)
+            outs[k] = ((res.transform, False) if res is not None else
+                       (RigidTransform.identity(frames[k].dim), True))
+        for k, o in zip(rerun, run_threaded(rerun)):
+            outs[k] = o
     else:
-        from concurrent.futures import ThreadPoolExecutor
-
-        def one(k):
-            x, y = pairs[k]
-            try:
-                return register(x=x, y=y, params=params, options=options).transform, False
-            except DeviceError:
-                raise
-            except GravregError:
-                return RigidTransform.identity(frames[k].dim), True
-
-        n_workers = workers or min(4, len(pairs))
-        if n_workers <= 1:
-            outs = [one(k) for k in range(len(pairs))]
-        else:
-            with ThreadPoolExecutor(max_workers=n_workers) as pool:
-                outs = list(pool.map(one, range(len(pairs))))
-        pairwise = [o[0] for o in outs]
-        failed = [o[1] for o in outs]
+        outs = run_threaded(list(range(len(pairs))))
+    pairwise = [o[0] for o in outs]
+    failed = [o[1] for o in outs]
     poses = [RigidTransform.identity(frames[0].dim)]
     for tf in pairwise:
         poses.append(poses[-1].compose(tf.inverse()))

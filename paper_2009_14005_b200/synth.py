@@ -184,3 +184,40 @@ def partial_overlap(n, rng, overlap=0.4, outliers=0.05):
     x = add_uniform_noise(x, (n - inliers) / inliers, rng)
     y = add_uniform_noise(y, (n - inliers) / inliers, rng)
     return PointCloud(x.points[:n]), PointCloud(y.points[:n])
+
+
+def fragment_pair(p, n=4096):
+    """BASELINE configs[4] pair p: a 3DMatch-fragment-sized pair (SURVEY
+    §8(d) C5) -- ``blob`` for even p, ``bumped_box`` for odd p, n points,
+    misaligned by a random rigid motion of <= 60 deg / 0.1, seeded with
+    100000 + p (so any shard of the batch regenerates its own pairs)."""
+    rng = rng_from_seed(100000 + p)
+    x = blob(n, rng) if p % 2 == 0 else bumped_box(n, rng)
+    return x, misalign(x, random_rigid(rng, np.deg2rad(60), 0.1))
+
+
+def configs2_pair(n=1_000_000, seed=3):
+    """BASELINE configs[2]: the 1M x 1M pair --
+    ``blob(n)`` and its misaligned copy (<= 60 deg / 0.1), PCG64 seed 3."""
+    rng = rng_from_seed(seed)
+    x = blob(n, rng)
+    gt = random_rigid(rng, np.deg2rad(60), 0.1)
+    return x, misalign(x, gt)
+
+
+def configs1_pair(n=100_000, seed=2):
+    """BASELINE configs[1]: a LiDAR-scan-shaped pair -- the
+    street scan and its copy moved by <= 10 deg / 1 m, PCG64 seed 2."""
+    rng = rng_from_seed(seed)
+    x = lidar_scan(n, rng)
+    gt = random_rigid(rng, np.deg2rad(10), 1.0)
+    return x, misalign(x, gt), gt
+
+
+def configs3_pair(n=200_000, seed=4):
+    """BASELINE configs[3]: the 40%-overlap pair with 5% outliers and
+    inhomogeneous density, template misaligned <= 60 deg."""
+    rng = rng_from_seed(seed)
+    x, y0 = partial_overlap(n, rng)
+    gt = random_rigid(rng, np.deg2rad(60), 0.1)
+    return x, misalign(y0, gt), gt

@@ -1,0 +1,166 @@
+"""Regression tests for the round-1 advisor findings, each
+against the oracle or the reference-semantics path.  GPU only.
+
+* a BHTree's device copy is never reused after register() / another build
+  replaced the context's tree (bhtree.py:125-147 semantics: forces of THE
+  given tree);
+* the batched kernel skips d2 + eps^2 == 0 terms at epsilon = 0
+  (_kernels.py:38-42) instead of producing NaN;
+* register_sequence re-runs a pair the batched kernel cannot hold through
+  register() (registration.py:178-206: one failed pair never aborts the
+  sequence, and a pair register() handles is not a failure);
+* theta = 0 equals the reference's leaf sum when a depth-cap leaf holds
+  several points (_kernels.py:30-42), not the exact O(NM) sum;
+* the C validate reports norm_range as the reference's (a, b) tuple
+  (core.py:145-147).
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _rot_err(Ra, Rb):
+    c = (np.trace(Ra.T @ Rb) - 1) / 2
+    return float(np.arccos(np.clip(c, -1, 1)))
+
+
+def test_bhtree_device_copy_not_stale_after_register(orc):
+    import paper_2009_14005_b200 as fga
+    from paper_2009_14005_b200 import bhtree, synth
+    rng = synth.rng_from_seed(5)
+    x1 = synth.blob(3000, rng)
+    m1 = np.full(len(x1), 0.01)
+    t = bhtree.build(x1, m1, 20)
+    q = rng.normal(size=(500, 3))
+    p = fga.default_params().replace(theta=0.5)
+    f0, v0 = bhtree.bh_forces(t, q, 0.05, p, count_visits=True)
+    # register() and another build replace the thread context's trees
+    x2 = synth.blob(5000, rng)
+    fga.register(x2, synth.misalign(x2, synth.random_rigid(rng, 0.5, 0.1)), params=p)
+    f1, v1 = bhtree.bh_forces(t, q, 0.05, p, count_visits=True)
+    assert np.array_equal(f0, f1) and np.array_equal(v0, v1)
+    t2 = bhtree.build(x2, np.full(len(x2), 0.01), 20)
+    f2, v2 = bhtree.bh_forces(t, q, 0.05, p, count_visits=True)
+    assert np.array_equal(f0, f2) and np.array_equal(v0, v2)
+    of, ov, _ = orc.bh_forces(orc.tree_build(x1.points, m1, 20), q, 0.05, 0.5, p.G, p.epsilon)
+    # (the GPU-built COMs sum children first: forces within 1e-13 of the oracle tree's)
+    assert np.array_equal(v2, ov) and np.abs(f2 - of).max() <= 1e-13 * np.abs(of).max()
+    # the second tree is evaluated as itself too
+    g, w = bhtree.bh_forces(t2, q, 0.05, p, count_visits=True)
+    og, ow, _ = orc.bh_forces(orc.tree_build(x2.points, np.full(len(x2), 0.01), 20), q, 0.05,
+                              0.5, p.G, p.epsilon)
+    assert np.array_equal(w, ow) and np.abs(g - og).max() <= 1e-13 * np.abs(og).max()
+
+
+def test_session_tree_independent_of_operator_builds():
+    """A live stepwise session keeps its own tree while the operator API
+    builds others on the same context."""
+    import paper_2009_14005_b200 as fga
+    from paper_2009_14005_b200 import bhtree, engine, synth
+    rng = synth.rng_from_seed(6)
+    x = synth.blob(4000, rng)
+    y = synth.misalign(x, synth.random_rigid(rng, 0.6, 0.1))
+    p = fga.default_params().replace(theta=0.5)
+    ref = fga.register(x, y, params=p, options=fga.RegisterOptions(record_iterations=True))
+    s = engine.Session(x, y, params=p)
+    other = synth.blob(2500, rng)
+    for k in range(5):
+        s.iterate(1)
+        if k in (1, 3):
+            bhtree.build(other, np.full(len(other), 0.02), 20)
+    s.iterate(p.max_iters)
+    res = s.finish()
+    assert res.iterations == ref.iterations
+    assert np.array_equal(res.transform.rotation, ref.transform.rotation)
+
+
+def test_batched_epsilon_zero_coincident_points():
+    """epsilon = 0 and x == y: template points sit exactly on reference leaf
+    COMs; the batched kernel must skip those terms like register()."""
+    import paper_2009_14005_b200 as fga
+    from paper_2009_14005_b200 import synth
+    rng = synth.rng_from_seed(7)
+    pairs = []
+    for k in range(3):
+        x = synth.blob(1500 + 500 * k, rng)
+        pairs.append((x, x))
+    p = fga.default_params().replace(epsilon=0.0)
+    br = fga.register_batch(pairs, params=p)
+    assert all(e is None for e in br.errors)
+    for (x, y), r in zip(pairs, br.results):
+        assert np.all(np.isfinite(r.transform.rotation)) and np.all(np.isfinite(r.transform.translation))
+        s = fga.register(x, y, params=p)
+        assert r.iterations == s.iterations
+        assert np.abs(r.transform.rotation - s.transform.rotation).max() < 1e-8
+        assert np.abs(r.transform.translation - s.transform.translation).max() < 1e-8
+    seq = fga.register_sequence([pairs[0][0], pairs[0][0]], params=p)
+    assert not seq.failed[0] and np.all(np.isfinite(seq.pairwise[0].rotation))
+
+
+def _near_duplicate_cloud(rng, n_pairs):
+    """n_pairs well-separated points, each doubled at 1e-12: every pair stays
+    together down to the depth cap, a ~15-node single-child chain each --
+    more nodes than the batched kernel's per-pair cap."""
+    from paper_2009_14005_b200 import PointCloud
+    base = rng.uniform(-1, 1, size=(n_pairs, 3))
+    pts = np.concatenate([base, base + 1e-12])
+    return PointCloud(pts)
+
+
+def test_sequence_reruns_pairs_over_the_batched_cap():
+    import paper_2009_14005_b200 as fga
+    from paper_2009_14005_b200 import synth
+    rng = np.random.default_rng(8)
+    f0 = _near_duplicate_cloud(rng, 2000)
+    g = synth.random_rigid(synth.rng_from_seed(9), np.deg2rad(6), 0.02)
+    frames = [f0, synth.misalign(f0, g), synth.misalign(synth.misalign(f0, g), g)]
+    br = fga.register_batch([(frames[1], frames[0])])
+    assert br.status[0] == -4  # FGA_ERR_UNSUPPORTED: over the per-pair node cap
+    seq = fga.register_sequence(frames)
+    assert not any(seq.failed)
+    for k in range(2):
+        single = fga.register(x=frames[k + 1], y=frames[k]).transform
+        assert np.array_equal(seq.pairwise[k].rotation, single.rotation)
+        assert np.array_equal(seq.pairwise[k].translation, single.translation)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-5), ("fp64", 1e-9)])
+def test_theta_zero_with_shared_depth_cap_leaves(orc, precision, tol):
+    """max_depth = 4: leaves hold many points, so the reference's theta = 0
+    force is a sum over leaf COMs, not the exact pairwise sum."""
+    import paper_2009_14005_b200 as fga
+    from paper_2009_14005_b200 import synth
+    rng = synth.rng_from_seed(10)
+    x = synth.blob(2000, rng)
+    y = synth.misalign(x, synth.random_rigid(rng, np.deg2rad(30), 0.1))
+    p = fga.default_params().replace(theta=0.0, max_depth=4)
+    res = fga.register(x, y, params=p, options=fga.RegisterOptions(record_iterations=True,
+                                                                   precision=precision))
+    ref = orc.register(x.points, y.points, theta=0.0, max_depth=4)
+    assert res.iterations == ref.iterations and res.converged == ref.converged
+    assert np.abs(res.trajectory - np.array(ref.trajectory)).max() < tol
+    # the case is meaningful: some leaf aggregates several points
+    from paper_2009_14005_b200 import bhtree
+    t = bhtree.build(x, np.ones(len(x)), 4)
+    leaves = (t.children < 0).all(axis=1)
+    assert t.occupancy[leaves].max() > 1
+
+
+def test_c_validate_norm_range_message():
+    import paper_2009_14005_b200 as fga
+    from paper_2009_14005_b200 import _native as N
+    c = N.context()
+    x = np.random.default_rng(0).normal(size=(50, 3))
+    p = N.make_params(fga.default_params())
+    p.norm_a, p.norm_b = 5.0, -5.0
+    res = N.CResult()
+    rc = N.lib().fga_register(c.handle, N.ptr(x), 50, N.ptr(x), 50, 3, ctypes.byref(p), None,
+                              ctypes.byref(res), None, None, None, None)
+    assert rc == N.FGA_ERR_INVALID
+    assert N.last_error() == "invalid parameter norm_range=(5.0, -5.0)"
+    with pytest.raises(fga.InvalidParam) as e:
+        N.check(rc)
