@@ -278,20 +278,34 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
                                                  float qx, float qy, float qz, bool active,
                                                  float theta2, double theta2_64, float eps2,
                                                  const double* qpx, const double* qpy,
-                                                 const double* qpz, int64_t qi) {
+                                                 const double* qpz, int64_t m_queries,
+                                                 double* hs = nullptr) {
+  // hs (optional): the block's fp64 fold sums in shared memory, 3 per thread
+  // (hs[3 threadIdx.x ..]), so they hold no registers across the loop (folds
+  // are rare; the address is re-derived at each fold)
   float ax = 0.f, ay = 0.f, az = 0.f;     // the current chunk's partial force
   double hx = 0.0, hy = 0.0, hz = 0.0;  // folded chunks
+  if (hs) {
+    double* h = hs + 3 * threadIdx.x;
+    h[0] = h[1] = h[2] = 0.0;
+  }
   int visits = 0, accepted = 0;
   int cursor = active ? 0 : n_nodes;
-  const int64_t qs = active ? qi : 0;  // inactive lanes join the exact re-check
   int lim = fold_limit(0, n_nodes);
   while (true) {
     const int n = __reduce_min_sync(0xffffffffu, cursor);
     if (n >= lim) {  // exit, or fold the chunk's partial into the fp64 sum
       if (n >= n_nodes) break;
-      hx += (double)ax;
-      hy += (double)ay;
-      hz += (double)az;
+      if (hs) {
+        double* h = hs + 3 * threadIdx.x;
+        h[0] += (double)ax;
+        h[1] += (double)ay;
+        h[2] += (double)az;
+      } else {
+        hx += (double)ax;
+        hy += (double)ay;
+        hz += (double)az;
+      }
       ax = ay = az = 0.f;
       lim = fold_limit(n, n_nodes);
     }
@@ -305,6 +319,11 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     bool acc = diff > 0.f;
     const bool near = mine && fabsf(diff) <= b.z;
     if (__any_sync(0xffffffffu, near)) {  // warp-uniform branch, rarely taken
+      // this lane's query, re-derived here (query i = global thread index;
+      // inactive lanes read the last query and ignore the result) so no
+      // register holds it across the loop
+      int64_t qs = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+      qs = qs < m_queries ? qs : m_queries - 1;
       const bool e = mac_exact(A64, B64, n, qpx[qs], qpy[qs], qpz[qs], theta2_64);
       acc = near ? e : acc;
     }
@@ -326,6 +345,12 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     }
     const int next = acc ? __float_as_int(b.y) : n + 1;
     cursor = mine ? next : cursor;
+  }
+  if (hs) {
+    const double* h = hs + 3 * threadIdx.x;
+    hx = h[0];
+    hy = h[1];
+    hz = h[2];
   }
   return Trav32Out{hx + (double)ax, hy + (double)ay, hz + (double)az, visits, accepted};
 }

@@ -38,11 +38,18 @@ struct F32Params {
   float theta2, eps2;
 };
 
-// Resident threads per SM: FP32 traversal 1280 (48 registers; 1024 with 64
-// registers: 15.3 vs 13.5 ms, 1536 with 40 registers + spills: 13.5);
+// Resident threads per SM.  The FP32 traversal is latency-bound on its
+// record loads (ncu: 47% of stall samples at the first use of the loaded
+// record, issue 66% active at 1280 threads), so more warps win even at 32
+// registers with a spilled query coordinate (1M iteration, A/B on one box):
+// 1024 threads 15.3 ms, 1280 13.2, 1536 12.4, 1792 11.6, 2048 11.6.  What
+// gets it there: the fold sums live in shared memory and the exact re-check
+// re-derives its query from the thread index (no register across the loop).
+// Measured and not kept: the query in shared memory (15.3 ms at 1792),
+// L1 prefetch of node n+1 (+1%) or of skip(n) (+7%).
 // fp64 traversal: 768 -> 35.8 ms, 1024 -> 31.5, 1280 -> 30.3, 1536 -> 38 (spills)
 #ifndef FGA_BH32_TPS
-#define FGA_BH32_TPS 1280
+#define FGA_BH32_TPS 1792
 #endif
 #ifndef FGA_BH64_TPS
 #define FGA_BH64_TPS 1280
@@ -80,9 +87,10 @@ __global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? FGA_BH32_TPS : FGA_BH
   double F[3];
   int nv, na;
   if constexpr (sizeof(Real) == 4) {
+    __shared__ double hs[3 * kT];  // the lanes' fp64 fold sums
     const Trav32Out o = traverse32d<kGuardZero, kCountVisits>(
         tr.c32, tr.a64, tr.b64, n_nodes, (float)y[0], (float)y[1], (float)y[2], active, f.theta2,
-        sp.theta2, f.eps2, tv.px, tv.py, tv.pz, i);
+        sp.theta2, f.eps2, tv.px, tv.py, tv.pz, tv.m, hs);
     const double gq = sp.G * mq;
     F[0] = gq * o.ax;
     F[1] = gq * o.ay;
@@ -129,9 +137,10 @@ __global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? FGA_BH32_TPS : FGA_BH
 // ---------------------------------------------------------------- BH operator
 template <typename Real, bool kGuardZero>
 #ifndef FGA_BHOP_MINB
-#define FGA_BHOP_MINB 5  // 1280 threads/SM: fp64 operator 39.5 -> 38.7 ms (1M x 1M, host in/out), fp32 unchanged
+#define FGA_BHOP_MINB 5  // 1280 threads/SM: fp64 operator 39.5 -> 38.7 ms (1M x 1M, host in/out)
 #endif
-__global__ void __launch_bounds__(kForceThreads, FGA_BHOP_MINB) k_bh_operator(
+__global__ void __launch_bounds__(kForceThreads, sizeof(Real) == 4 ? FGA_BH32_TPS / kForceThreads
+                                                                   : FGA_BHOP_MINB) k_bh_operator(
     TreeRecords tr, int n_nodes, const double* __restrict__ qx_, const double* __restrict__ qy_,
     const double* __restrict__ qz_, const double* __restrict__ qm_, const int* __restrict__ order,
     int64_t m, double theta2, double G, double eps2, F32Params f, double* __restrict__ fout,
@@ -149,9 +158,10 @@ __global__ void __launch_bounds__(kForceThreads, FGA_BHOP_MINB) k_bh_operator(
   double F[3];
   int nv, na;
   if constexpr (sizeof(Real) == 4) {
+    __shared__ double hs[3 * kForceThreads];
     const Trav32Out o = traverse32d<kGuardZero, true>(
         tr.c32, tr.a64, tr.b64, n_nodes, (float)q[0], (float)q[1], (float)q[2], active, f.theta2,
-        theta2, f.eps2, qx_, qy_, qz_, i);
+        theta2, f.eps2, qx_, qy_, qz_, m, hs);
     const double gq = G * qm;
     F[0] = gq * o.ax;
     F[1] = gq * o.ay;

@@ -103,3 +103,67 @@ def register_sharded(x, y, params: FgaParams | None = None,
         device = torch.cuda.current_device()
     backend = _LibBackend(x, y, params, options, rank, world, device)
     return run_sharded(backend, params, options, group)
+
+
+def shard_of(n_pairs: int, rank: int, world: int) -> list[int]:
+    """The pairs rank `rank` of `world` registers: p = rank, rank + world, ...
+    (round robin, so fragment pairs of mixed difficulty spread evenly)."""
+    return list(range(rank, n_pairs, world))
+
+
+def register_batch_sharded(pairs, params: FgaParams | None = None,
+                           options: RegisterOptions | None = None, group=None,
+                           gather: bool = True, n_pairs: int | None = None,
+                           _register_batch=None):
+    """Many independent pairs (BASELINE configs[4]) sharded across the ranks
+    of ``group`` with NO collective on the data path: each rank runs
+    register_batch (one persistent kernel) on its own share
+    (``shard_of``) and the results are only gathered at the end.
+
+    ``pairs`` is either a sequence of (x, y) PointCloud pairs (every rank may
+    pass the full list; only its share is touched) or a callable p -> (x, y)
+    with ``n_pairs`` given, so a rank materializes only its own pairs.
+    Returns a registration.BatchResult in pair order: with ``gather`` the full
+    batch on every rank (dist.all_gather_object of the per-rank results),
+    otherwise this rank's entries only (the other slots None) and
+    ``.indices`` = the pairs it ran.  Reference unit of work:
+    registration.register per pair (registration.py:91-166)."""
+    from .registration import BatchResult, register_batch
+
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if callable(pairs):
+        if n_pairs is None:
+            raise ValueError("n_pairs is required when pairs is a callable")
+        total = int(n_pairs)
+        mine = shard_of(total, rank, world)
+        local = [pairs(p) for p in mine]
+    else:
+        pairs = list(pairs)
+        total = len(pairs)
+        mine = shard_of(total, rank, world)
+        local = [pairs[p] for p in mine]
+    run = _register_batch or register_batch
+    br = run(local, params=params, options=options)
+    out = BatchResult([None] * total, [None] * total, None, None)
+    out.indices = mine
+    parts = [(mine, br.results, br.errors, None if br.interactions is None else
+              list(br.interactions), None if br.status is None else list(br.status))]
+    if gather and world > 1:
+        allparts = [None] * world
+        dist.all_gather_object(allparts, parts[0], group=group)
+        parts = allparts
+    inter = [0] * total
+    status = [0] * total
+    for idx, res, err, it, st in parts:
+        for k, p in enumerate(idx):
+            out.results[p] = res[k]
+            out.errors[p] = err[k]
+            if it is not None:
+                inter[p] = int(it[k])
+            if st is not None:
+                status[p] = int(st[k])
+    import numpy as np
+    out.interactions = np.array(inter, np.int64)
+    out.status = np.array(status, np.int32)
+    return out

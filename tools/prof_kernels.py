@@ -23,11 +23,10 @@ if a.mode == "all":
     for m in ("bh", "direct", "gpe"):
         os.system(f"{sys.executable} {__file__} --mode {m} --n {a.n} --iters {a.iters}")
     sys.exit(0)
-rng = synth.rng_from_seed(3)
-x = synth.blob(a.n, rng)
-y = synth.misalign(x, synth.random_rigid(rng, np.deg2rad(60), 0.1))
+x, y = synth.configs2_pair(a.n)  # bench.py's configs[2] workload
 theta = 0.0 if a.mode == "direct" else 0.5
-p = fga.default_params().replace(theta=theta, conv_tol=1e-300, max_iters=a.iters + 2)
+p = fga.default_params().replace(theta=theta, G=66.7 * (2000.0 / a.n) ** 0.5, conv_tol=1e-300,
+                                 max_iters=a.iters + 2)
 s = Session(x, y, p, fga.RegisterOptions(compute_gpe=False, precision=a.precision), stream=0)
 if a.mode == "gpe":
     for _ in range(a.iters):
