@@ -2,21 +2,34 @@
 """FGA hot-path benchmark on B200 (contract: see DESIGN.md "Measurement").
 
 Workload (BASELINE.json configs[2], the 1M-point FGA the metric is quoted
-on): a 1,000,000 x 1,000,000 synthetic blob pair (synth.blob, PCG64 seed 3,
-random rotation <= 60 deg, translation <= 0.1), Barnes-Hut theta = 0.5.  A
-"step" is one FGA iteration: the force pass over the whole template
-(traversal + fused Euler-Cromer step + Kabsch partials), the partial
-reduction and the fp64 rigid update.  `value` = accepted particle-node
-interactions per second (each accepted node is one softened pair
-interaction, the reference's own unit: _kernels.py:37-42), whole job.
+on): a 1,000,000 x 1,000,000 synthetic blob pair (synth.configs2_pair, PCG64
+seed 3, random rotation <= 60 deg, translation <= 0.1), Barnes-Hut theta =
+0.5.  A "step" is one FGA iteration at the INITIAL template state (SURVEY
+§8(d): the headline interactions/s is quoted at iteration 0): the force pass
+over the whole template (traversal + fused Euler-Cromer step + Kabsch
+partials), the partial reduction (+ the all-reduce for N > 1) and the fp64
+rigid update; the state is restored on the device (fga_session_checkpoint)
+before every step, outside the timed region.  `value` = accepted
+particle-node interactions per second (each accepted node is one softened
+pair interaction, the reference's own unit: _kernels.py:37-42), whole job.
 
-Extra legs in the same JSON line (N=1 only): `direct` (theta = 0, exact O(NM)
-direct sum, pairs/s and its FP32 roofline), `e2e` (the reference-facing
-bh_forces drop-in with pinned host buffers: H2D + traversal + D2H per step),
-`registration` (full register() wall time from host arrays), `cpu_baseline`
-(the C oracle on all host cores, bounded sample).
+The reference arm (--impl reference) times the oracle port of the reference's
+CPU path on the same config and the same state (sampled queries), on all
+host cores.
+
+Extra legs on the same JSON line (N=1 unless noted): `e2e` (the reference-
+facing bh_forces drop-in with pinned host buffers, every rank its query
+share), `fp64_mode`, `direct` (theta = 0, exact O(NM)), `gpe` (the O(NM)
+energy), `small_m` (shard 0 of 8 on one GPU), `tree_build`, `registration`
+(full register() wall time, with the CPU reference extrapolated beside it),
+`configs0` (configs[0] register() on GPU vs the oracle on 1 and all host
+cores, measured), `batched` (configs[4], pairs sharded over ranks),
+`configs` (configs[1]/[3]), `ingest`, `cpu_baseline`.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py --gpus 2 --dry-run      # CPU/gloo plumbing check
+Without WORLD_SIZE in the environment, --gpus N > 1 re-launches itself under
+torch.distributed.run with N ranks (127.0.0.1).
 """
 
 from __future__ import annotations
@@ -24,6 +37,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -40,6 +54,7 @@ FLOP_PER_VISIT = 9         # MAC: 3 sub + 5 (d^2) + 1 (theta^2 d^2)
 BYTES_PER_VISIT = 32       # one 32 B node record per query-node visit
 BYTES_PER_QUERY = 32       # + 16 B query in, 16 B state out per template point
 BUILD_BYTES_PER_POINT = 350  # SURVEY §8(d) K2-K5 algorithmic bytes per reference point
+KERNELS_PER_STEP = 6       # k_qbound, k_node_bands, k_bh_iterate, k_reduce_stage/_final, k_update
 
 
 def parse():
@@ -51,18 +66,14 @@ def parse():
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--theta", type=float, default=0.5)
     ap.add_argument("--seed", type=int, default=3)
-    ap.add_argument("--no-direct", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-registration", action="store_true")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only: exercise the launch / rank / barrier / max-over-ranks "
+                         "plumbing with gloo and print the JSON line")
+    for leg in ("direct", "e2e", "registration", "cpu-baseline", "batched", "build", "fp64",
+                "ingest", "configs", "gpe", "small-m", "configs0"):
+        ap.add_argument(f"--no-{leg}", action="store_true")
     ap.add_argument("--direct-steps", type=int, default=3)
-    ap.add_argument("--no-batched", action="store_true")
-    ap.add_argument("--no-build", action="store_true")
-    ap.add_argument("--no-fp64", action="store_true")
-    ap.add_argument("--no-ingest", action="store_true")
     ap.add_argument("--build-sizes", default="1000000,16000000")
-    ap.add_argument("--no-configs", action="store_true",
-                    help="skip the configs[1]/configs[3] registration legs")
     ap.add_argument("--batch-pairs", type=int, default=4096)
     ap.add_argument("--cpu-sample", type=int, default=65536)
     ap.add_argument("--default-g", action="store_true",
@@ -89,6 +100,18 @@ def workload(n, seed):
     return synth.configs2_pair(n, seed)
 
 
+def config_dict(args, n_ref, n_tpl, tree_nodes, world):
+    """The workload description, identical in both arms."""
+    p = bench_params(args)
+    return {"workload": "configs[2]: 1M x 1M FGA pair, Barnes-Hut theta=%g, one iteration "
+                        "at the initial template state" % args.theta,
+            "n_reference": int(n_ref), "n_template": int(n_tpl), "theta": args.theta,
+            "G": p.G, "epsilon": p.epsilon, "seed": args.seed, "tree_nodes": int(tree_nodes),
+            "state": "initial template state (iteration 0), restored before every step",
+            "parallelism": f"template-shard x{world}",
+            "l2": "flushed between timed steps (256 MiB write, outside the events)"}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -100,6 +123,74 @@ def load_peaks():
 
 def fp32_peak_tflops(sm_mhz, sms=148):
     return 2.0 * sms * 128 * sm_mhz * 1e6 / 1e12
+
+
+def _profile(which):
+    """Per-launch counters of the hot kernels from the committed ncu capture
+    (profiles/traffic.json, tools/profile_kernels.sh + tools/ncu_metrics.py)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(which) or {}
+    except OSError:
+        return {}
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(args):
+    """--gpus N without WORLD_SIZE: run this script under torch.distributed.run
+    with N ranks on this node (rank 0 prints the JSON line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args, rank, world):
+    """The multi-rank plumbing without a GPU: gloo process group, W untimed and
+    K timed steps bracketed by barriers, max over ranks of the step time, one
+    JSON line from rank 0 (tests/test_bench_plumbing.py)."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    work = np.random.default_rng(rank).normal(size=(200_000,))
+
+    def step():
+        return float(np.sort(work)[0])
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    if world > 1:
+        dist.barrier()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64)
+    n = torch.tensor([float(len(work) * args.steps)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(n)
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return None
+    return {"metric": METRIC, "value": float(n.item()) / float(t.item()), "unit": "elements/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(t.item()) / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "dry_run": True, "ranks_reporting": world,
+            "config": {"workload": "dry run: CPU sort per rank (plumbing check only)"}}
 
 
 class ClockSampler:
@@ -155,63 +246,80 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_2009_14005_b200 as fga
-    from paper_2009_14005_b200.engine import SUM_ACCEPTED, SUMS_LEN, Session
+    from paper_2009_14005_b200.engine import SUM_VISITS, SUMS_LEN, Session
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     x, y = workload(args.n, args.seed)
     K, W = args.steps, args.warmup
-    params = bench_params(args).replace(conv_tol=1e-300, max_iters=W + K + 1)
-    opts = fga.RegisterOptions(compute_gpe=False)
+    params = bench_params(args).replace(conv_tol=1e-300, max_iters=4)
     x_t = torch.from_numpy(np.array(x.points)).to(dev)
     y_t = torch.from_numpy(np.array(y.points)).to(dev)
     stream = torch.cuda.current_stream()
-    sess = Session(None, None, params, opts, shard_rank=rank, shard_count=world,
-                   device=local_rank, stream=stream.cuda_stream,
-                   device_inputs=(x_t.data_ptr(), len(x), y_t.data_ptr(), len(y)))
-    sums = torch.zeros(SUMS_LEN, dtype=torch.float64, device=dev)
-    sess.bind_sums(sums.data_ptr())
 
-    def one_iteration():
+    def session(count_visits=False, precision="fp32", shard=(rank, world)):
+        s = Session(None, None, params,
+                    fga.RegisterOptions(compute_gpe=False, count_visits=count_visits,
+                                        precision=precision),
+                    shard_rank=shard[0], shard_count=shard[1], device=local_rank,
+                    stream=stream.cuda_stream,
+                    device_inputs=(x_t.data_ptr(), len(x), y_t.data_ptr(), len(y)))
+        sums = torch.zeros(SUMS_LEN, dtype=torch.float64, device=dev)
+        s.bind_sums(sums.data_ptr())
+        s.checkpoint()  # the initial state: every step starts from it
+        return s, sums
+
+    sess, sums = session()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def one_step(ev=None):
+        sess.restore()
+        flush.zero_()
+        if ev:
+            ev[0].record(stream)
         sess.forces()
+        if ev:
+            ev[1].record(stream)
         if world > 1:
             dist.all_reduce(sums)
         sess.update()
+        if ev:
+            ev[2].record(stream)
 
     for _ in range(W):
-        one_iteration()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        one_step()
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(K)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
         for k in range(K):
-            flush.zero_()
-            ev[k][0].record(stream)
-            sess.forces()
-            ev[k][1].record(stream)
-            if world > 1:
-                dist.all_reduce(sums)
-            sess.update()
-            ev[k][2].record(stream)
+            one_step(ev[k])
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(c) for a, _, c in ev]
     force_ms = [a.elapsed_time(b) for a, b, _ in ev]
-    total_ms = float(sum(step_ms))
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([float(sum(step_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     res = sess.finish()
-    inter = res.interactions[W:W + K].astype(np.float64)
-    visits_total = None
-    interactions = float(inter.sum())
-    value = interactions / (total_ms / 1e3)
-    batched = None if args.no_batched else run_batched(args, rank, world)  # every rank
+    inter = float(res.interactions[0])  # all-reduced: the whole job's count per step
+    value = inter * K / (total_ms / 1e3)
+    # node visits of the same state (an untimed counting pass; identical
+    # traversal, visits are not counted in the timed kernel)
+    vsess, vsums = session(count_visits=True)
+    vsess.forces()
+    if world > 1:
+        dist.all_reduce(vsums)
+    torch.cuda.synchronize()
+    visits = float(vsums[SUM_VISITS].item())
+    vsess.finish()
+    del vsess
+    tree_nodes = sess.n_nodes
+    e2e = None if args.no_e2e else run_e2e(args, x, y, rank, world, local_rank)
+    batched = None if args.no_batched else run_batched(args, rank, world)
     if rank != 0:
         return None
 
@@ -219,60 +327,49 @@ def run_ours(args, rank, world, local_rank):
     clocks = clk.summary()
     fmax = float(peaks.get("sm_max_mhz", 1965.0))
     peak = fp32_peak_tflops(fmax)
-    # dominant kernel: the traversal force pass (incl. its tiny partial reduction)
     mean_force_s = float(np.mean(force_ms)) / 1e3
-    per_launch_inter = float(inter.mean()) / 1.0
-    # visits per launch are not in the result rows; use the oracle-equal ratio
-    # recorded by the kernel counters (visits are summed with interactions)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32 forces / f64 state",
-        "data": "synthetic (synth.blob, PCG64 seed %d), random-init inputs" % args.seed,
-        "config": {"workload": "configs[2]: 1M x 1M FGA pair, Barnes-Hut theta=%g, fixed "
-                               "iteration budget" % args.theta,
-                   "n_reference": len(x), "n_template": len(y), "theta": args.theta,
-                   "G": params.G,
-                   "tree_nodes": sess.n_nodes, "parallelism": f"template-shard x{world}",
-                   "l2": "flushed between timed steps (256 MiB write, outside the events)"},
-        "gpu_launches": 4 * K,  # k_bh_iterate, k_reduce_stage, k_reduce_final, k_update
-        "interactions_per_step": per_launch_inter,
+        "data": "synthetic (synth.configs2_pair, PCG64 seed %d), random-init inputs" % args.seed,
+        "config": config_dict(args, len(x), len(y), tree_nodes, world),
+        "gpu_launches": KERNELS_PER_STEP * K,
+        "interactions_per_step": inter, "visits_per_step": visits,
+        "visits_per_s": visits * K / (total_ms / 1e3),
+        "equivalent_direct_pairs_per_s": float(len(x)) * float(len(y)) * K / (total_ms / 1e3),
     }
-    # also visits/s and "equivalent direct pairs/s" (N*M per
-    # iteration over the same time), labelled as such
-    line["visits_per_s"] = _visits_per_step(res, W, K) * K / (total_ms / 1e3)
-    line["equivalent_direct_pairs_per_s"] = float(len(x)) * float(len(y)) * K / (total_ms / 1e3)
-    visits_step = _visits_per_step(res, W, K)
-    flop = FLOP_PER_INTERACTION * per_launch_inter + FLOP_PER_VISIT * visits_step
-    achieved = flop / mean_force_s / 1e12
-    l2_peak, l2_src = l2_peak_gbs()
-    alg_bytes = BYTES_PER_VISIT * visits_step + BYTES_PER_QUERY * len(y)
-    l2_achieved = alg_bytes / mean_force_s / 1e9
-    line["roofline"] = {
-        "kernel": "k_bh_iterate<float> (+k_reduce)", "bound": "l2", "unit": "GB/s",
-        "achieved": l2_achieved, "peak": l2_peak, "frac": l2_achieved / l2_peak if l2_peak else None,
-        "peak_source": l2_src,
-        "work": f"SURVEY §8(d) K6: {BYTES_PER_VISIT} B/visit x {visits_step:.4g} visits + "
-                f"{BYTES_PER_QUERY} B x {len(y)} queries = {alg_bytes:.4g} B per launch",
-        "ms_per_launch": mean_force_s * 1e3, "traffic": _traffic("bh"),
-        "fp32_view": {"achieved_tflops": achieved, "peak_tflops": peak, "frac": achieved / peak,
-                      "peak_source": f"2*148*128*sm_max_mhz ({peak_src} MEASURED_PEAKS.json "
-                                     f"sm_max_mhz={fmax})",
-                      "work": f"{FLOP_PER_INTERACTION} FLOP/interaction + {FLOP_PER_VISIT} "
-                              "FLOP/visit"}}
+    if e2e is not None:
+        line["e2e"] = e2e
+    line["roofline"] = traversal_roofline(mean_force_s, visits, inter, len(y), peak, peak_src,
+                                          fmax)
     line["clocks"] = clocks
+    if world == 1 and not args.no_small_m:
+        line["small_m"] = run_small_m(args, session, inter, mean_force_s, len(y))
+    if world == 1 and not args.no_fp64:
+        line["fp64_mode"] = run_fp64(session, stream, inter)
+    if world == 1 and not args.no_gpe:
+        line["gpe"] = run_gpe(sess, stream, len(x), len(y), peak, peak_src, fmax)
+    del sess
+    torch.cuda.empty_cache()
     if world == 1 and not args.no_build:
         line["tree_build"] = run_tree_build(args, dev, peaks, peak_src)
     if world == 1 and not args.no_direct:
         line["direct"] = run_direct(args, x, y, dev, stream, peak, peak_src, fmax)
-    if world == 1 and not args.no_fp64:
-        line["fp64_mode"] = run_fp64(args, x_t, y_t, len(x), len(y), dev, stream, local_rank)
-    if world == 1 and not args.no_e2e:
-        line["e2e"] = run_e2e(args, x, y, sess)
-    if world == 1 and not args.no_registration:
-        line["registration"] = run_registration(args, x, y)
+    cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(args, x, y, args.cpu_sample)
+        cpu = cpu_baseline(args, x, y, args.cpu_sample)
+        line["cpu_baseline"] = cpu
+        if "fp64_mode" in line:
+            line["fp64_mode"]["vs_cpu_baseline"] = line["fp64_mode"]["value"] / cpu["value"]
+        line["vs_cpu_baseline"] = {"value": value / cpu["value"],
+                                   "e2e": (e2e["value"] / cpu["value"]) if e2e else None,
+                                   "note": "GPU arm / oracle port on all host cores, same "
+                                           "state; the driver computes its own ratio"}
+    if world == 1 and not args.no_registration:
+        line["registration"] = run_registration(args, x, y, cpu)
+    if world == 1 and not args.no_configs0:
+        line["configs0"] = run_configs0()
     if batched is not None:
         line["batched"] = batched
     if world == 1 and not args.no_configs:
@@ -280,6 +377,209 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_ingest:
         line["ingest"] = run_ingest(x)
     return line
+
+
+def traversal_roofline(force_s, visits, inter, m, peak_tflops, peak_src, fmax):
+    """k_bh_iterate: issue/latency-bound inside the SM (ncu), not a DRAM or
+    tensor kernel.  `achieved` = SURVEY §8(d) algorithmic bytes (32 B per
+    query-node visit + 32 B per query) per launch / live launch time, against
+    the live-measured L2 read bandwidth; `traffic` = the L2->SM bytes ncu
+    measured per launch (the node loads mostly hit L1), with DRAM bytes and
+    the issue-slot utilisation beside it."""
+    prof = _profile("bh")
+    l2_peak, l2_src = l2_peak_gbs()
+    alg = BYTES_PER_VISIT * visits + BYTES_PER_QUERY * m
+    ach = alg / force_s / 1e9
+    flop = FLOP_PER_INTERACTION * inter + FLOP_PER_VISIT * visits
+    out = {"kernel": "k_bh_iterate<float> (+k_qbound, k_node_bands, k_reduce)",
+           "bound": "issue/L1TEX (latency of the per-step record loads)", "unit": "GB/s",
+           "achieved": ach, "peak": l2_peak, "frac": ach / l2_peak if l2_peak else None,
+           "peak_source": l2_src,
+           "work": f"SURVEY §8(d) K6: {BYTES_PER_VISIT} B/visit x {visits:.4g} visits + "
+                   f"{BYTES_PER_QUERY} B x {m} queries = {alg:.4g} B per launch (model bytes: "
+                   "most node loads are L1 hits)",
+           "ms_per_launch": force_s * 1e3,
+           "traffic": prof.get("lts_bytes"),
+           "traffic_source": "ncu lts__t_sectors_srcunit_tex x 32 B per launch (L2->SM), "
+                             "profiles/traffic.json",
+           "dram_bytes": prof.get("dram_bytes"),
+           "l1_hit_pct": prof.get("l1_hit_pct"),
+           "fp32_view": {"achieved_tflops": flop / force_s / 1e12, "peak_tflops": peak_tflops,
+                         "frac": flop / force_s / 1e12 / peak_tflops,
+                         "peak_source": f"2*148*128*sm_max_mhz ({peak_src} {fmax} MHz)",
+                         "work": f"{FLOP_PER_INTERACTION} FLOP/interaction + {FLOP_PER_VISIT} "
+                                 "FLOP/visit"}}
+    if prof.get("inst_executed"):
+        issue_peak = 148 * 4 * fmax * 1e6  # warp-instructions per second
+        out["issue_view"] = {
+            "achieved_winst_per_s": prof["inst_executed"] / force_s,
+            "peak_winst_per_s": issue_peak,
+            "frac": prof["inst_executed"] / force_s / issue_peak,
+            "ncu_issue_active_pct": prof.get("issue_active_pct"),
+            "note": "warp instructions per launch (ncu) / live launch time vs 148 SMs x 4 "
+                    "schedulers x f_max"}
+    return out
+
+
+def run_small_m(args, session, inter_full, force_s_full, m_full):
+    """Shard 0 of 8 (M/8 = 125k queries, the per-GPU share of the 8-GPU
+    strong-scaling run) on one GPU: its per-query interaction rate against
+    the full 1M pass's."""
+    import torch
+
+    from paper_2009_14005_b200.engine import SUM_ACCEPTED
+    s, sums = session(shard=(0, 8))
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=sums.device)
+    times, inter = [], 0.0
+    for k in range(8):
+        s.restore()
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        s.forces()
+        b.record(stream)
+        torch.cuda.synchronize()
+        inter = float(sums[SUM_ACCEPTED].item())
+        s.update()
+        if k >= 2:
+            times.append(a.elapsed_time(b) / 1e3)
+    m_local = s.m_local
+    s.finish()
+    t = float(np.mean(times))
+    rate_q = inter / t / m_local
+    full_q = inter_full / force_s_full / m_full
+    return {"queries": m_local, "ms_per_pass": t * 1e3, "interactions_per_s": inter / t,
+            "per_query_rate_vs_1m": rate_q / full_q,
+            "note": "shard 0 of 8 of the configs[2] template (fga_session shard_rank=0, "
+                    "shard_count=8), force pass at the initial state, CUDA events"}
+
+
+def run_fp64(session, stream, inter32):
+    """The same step with precision="fp64": the reference's arithmetic and
+    node order (forces bit-identical to bh_forces_kernel on the same tree)."""
+    import torch
+    s, sums = session(precision="fp64")
+    times = []
+    for k in range(4):
+        s.restore()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        s.forces()
+        s.update()
+        b.record(stream)
+        torch.cuda.synchronize()
+        if k:
+            times.append(a.elapsed_time(b))
+    res = s.finish()
+    ms = float(np.mean(times))
+    inter = float(res.interactions[0])
+    return {"ms_per_step": ms, "value": inter / (ms / 1e3), "unit": UNIT,
+            "same_accepted_set_as_fp32": inter == inter32,
+            "note": "precision=fp64: reference arithmetic, bit-identical forces on the same "
+                    "tree; same initial state"}
+
+
+def run_gpe(sess, stream, n, m, peak, peak_src, fmax):
+    """The O(NM) energy (_kernels.py:53-67, k_gpe32: FP32 pairs, fp64 across
+    tiles) of the initial template vs the 1M reference -- twice per
+    register(), its largest cost."""
+    import torch
+    prof = _profile("gpe")
+    times = []
+    for k in range(3):
+        sess.restore()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        sess.gpe()
+        b.record(stream)
+        torch.cuda.synchronize()
+        sess.take_gpe()
+        if k:
+            times.append(a.elapsed_time(b) / 1e3)
+    t = float(np.mean(times))
+    pairs = float(n) * float(m)
+    ach = FLOP_PER_INTERACTION * pairs / t / 1e12
+    out = {"ms": t * 1e3, "pairs_per_s": pairs / t,
+           "roofline": {"kernel": "k_gpe32", "bound": "FP32 FMA + MUFU", "unit": "TFLOP/s",
+                        "achieved": ach, "peak": peak, "frac": ach / peak,
+                        "peak_source": f"2*148*128*sm_max_mhz ({peak_src}, {fmax} MHz)",
+                        "work": "20 FLOP-equivalent per pair (SURVEY §8(d) K11)",
+                        "traffic": prof.get("dram_bytes"),
+                        "ncu_fma_pipe_pct": prof.get("fma_pipe_pct"),
+                        "ncu_issue_active_pct": prof.get("issue_active_pct")}}
+    return out
+
+
+def run_e2e(args, x, y, rank, world, local_rank):
+    """The reference's per-iteration native crossing (bhtree.bh_forces ->
+    _kernels.bh_forces_kernel, bhtree.py:139) replaced by fga_tree_forces on
+    pinned host buffers: H2D queries+masses, traversal, D2H forces+counters,
+    inside the timed region.  Same state (initial template) and tree as the
+    headline; with N ranks each evaluates its 1/N of the queries (max over
+    ranks of the wall time, accepted interactions summed)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2009_14005_b200 as fga
+    from paper_2009_14005_b200 import _native as N
+    from paper_2009_14005_b200 import bhtree
+    xn, yn, ctx = fga.normalize_pair(x, y, -5.0, 5.0)
+    p = bench_params(args)
+    sx = fga.niv_masses(xn, 16, ctx, 20)
+    sy = fga.niv_masses(yn, 16, ctx, 20)
+    # registration.py:85-87 (the same mass fields the session builds)
+    mx = np.minimum(16.0 * np.sqrt(len(sx) / 2000) * sx / sx.sum(), 0.022)
+    my = np.maximum(0.1 * sy / sy.max(), max(1e-6, p.dt * p.eta))
+    c = N.context(local_rank)
+    bhtree.build(xn, mx, 20)  # the operator tree of this context (outside the timing)
+    m = len(yn)
+    lo, hi = m * rank // world, m * (rank + 1) // world
+    mm = hi - lo
+
+    def pinned(shape, dtype):
+        return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
+
+    q = pinned((mm, 3), torch.float64)
+    q[:] = yn.points[lo:hi]
+    qm = pinned((mm,), torch.float64)
+    qm[:] = my[lo:hi]
+    f = pinned((mm, 3), torch.float64)
+    vis = pinned((mm,), torch.int64)
+    acc = pinned((mm,), torch.int64)
+    L = N.lib()
+
+    def call():
+        N.check(L.fga_tree_forces(c.handle, N.ptr(q), N.ptr(qm), mm, float(args.theta),
+                                  float(p.G), float(p.epsilon) ** 2, N.PREC_FP32, N.ptr(f),
+                                  N.ptr(vis), N.ptr(acc)))
+
+    for _ in range(2):
+        call()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        call()
+    wall = time.perf_counter() - t0
+    t = torch.tensor([wall, float(acc.sum())], dtype=torch.float64,
+                     device=torch.device("cuda", local_rank))
+    if world > 1:
+        tmax = t[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t[1:].clone()
+        dist.all_reduce(tsum)
+        wall, inter = float(tmax.item()), float(tsum.item())
+    else:
+        inter = float(t[1].item())
+    return {"value": inter * args.steps / wall, "unit": UNIT,
+            "h2d_bytes_per_step": int(q.nbytes + qm.nbytes) * world,
+            "d2h_bytes_per_step": int(f.nbytes + vis.nbytes + acc.nbytes) * world,
+            "ms_per_step": 1e3 * wall / args.steps,
+            "api": "fga_tree_forces (drop-in for _kernels.bh_forces_kernel), pinned host "
+                   "buffers, initial template state, FP32 traversal, wall clock per rank, max "
+                   "over ranks",
+            "visits_per_query": float(vis.mean())}
 
 
 _L2_CACHE = {}
@@ -361,53 +661,6 @@ def run_tree_build(args, dev, peaks, peak_src):
     return out
 
 
-def run_fp64(args, x_t, y_t, n, m, dev, stream, local_rank):
-    """The same 1M iteration with precision="fp64": the reference's
-    arithmetic and node order (forces bit-identical to bh_forces_kernel on
-    the same tree), for the cost of exactness next to the FP32 headline."""
-    import torch
-
-    import paper_2009_14005_b200 as fga
-    from paper_2009_14005_b200.engine import Session
-    K, W = 3, 1
-    params = bench_params(args).replace(conv_tol=1e-300, max_iters=W + K + 1)
-    sess = Session(None, None, params, fga.RegisterOptions(compute_gpe=False, precision="fp64"),
-                   device=local_rank, stream=stream.cuda_stream,
-                   device_inputs=(x_t.data_ptr(), n, y_t.data_ptr(), m))
-    for _ in range(W):
-        sess.forces()
-        sess.update()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(K):
-        sess.forces()
-        sess.update()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / K
-    res = sess.finish()
-    inter = float(res.interactions[W:W + K].mean())
-    return {"ms_per_step": ms, "value": inter / (ms / 1e3), "unit": UNIT,
-            "note": "precision=fp64: reference arithmetic, bit-identical forces on the same tree"}
-
-
-def _visits_per_step(res, W, K):
-    v = getattr(res, "visits_per_iter", None)
-    if v is None:
-        return 0.0
-    return float(np.mean(v[W:W + K]))
-
-
-def _traffic(which):
-    p = os.path.join(ROOT, "profiles", "traffic.json")
-    try:
-        with open(p) as f:
-            return json.load(f).get(which)
-    except OSError:
-        return None
-
-
 def run_direct(args, x, y, dev, stream, peak, peak_src, fmax):
     import torch
 
@@ -439,133 +692,71 @@ def run_direct(args, x, y, dev, stream, peak, peak_src, fmax):
             "roofline": {"kernel": "k_direct_iterate32", "bound": "fp32", "unit": "TFLOP/s",
                          "achieved": achieved, "peak": peak, "frac": achieved / peak,
                          "peak_source": f"2*148*128*sm_max_mhz ({peak_src}, {fmax} MHz)",
-                         "work": "20 FLOP/pair", "traffic": _traffic("direct")}}
-
-
-def run_e2e(args, x, y, sess):
-    """The reference's per-iteration native crossing (bhtree.bh_forces ->
-    _kernels.bh_forces_kernel, bhtree.py:139) replaced by fga_tree_forces on
-    pinned host buffers: H2D queries+masses, traversal, D2H forces+counters."""
-    import torch
-
-    import paper_2009_14005_b200 as fga
-    from paper_2009_14005_b200 import _native as N
-    xn, yn, ctx = fga.normalize_pair(x, y, -5.0, 5.0)
-    sy = fga.niv_masses(yn, 16, ctx, 20)
-    p = bench_params(args)
-    qm_np = np.maximum(0.1 * sy / sy.max(), max(1e-6, p.dt * p.eta))  # registration.py:87
-    m = len(yn)
-
-    def pinned(shape, dtype):
-        return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
-
-    q = pinned((m, 3), torch.float64)
-    q[:] = yn.points
-    qm = pinned((m,), torch.float64)
-    qm[:] = qm_np
-    f = pinned((m, 3), torch.float64)
-    vis = pinned((m,), torch.int64)
-    acc = pinned((m,), torch.int64)
-    c = sess.ctx
-    L = N.lib()
-
-    def call():
-        N.check(L.fga_tree_forces(c.handle, N.ptr(q), N.ptr(qm), m, float(args.theta),
-                                  float(p.G), float(p.epsilon) ** 2, N.PREC_FP32, N.ptr(f),
-                                  N.ptr(vis), N.ptr(acc)))
-
-    for _ in range(2):
-        call()
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        call()
-        times.append(time.perf_counter() - t0)
-    inter = float(acc.sum())
-    return {"value": inter * len(times) / sum(times), "unit": UNIT,
-            "h2d_bytes_per_step": int(q.nbytes + qm.nbytes),
-            "d2h_bytes_per_step": int(f.nbytes + vis.nbytes + acc.nbytes),
-            "ms_per_step": 1e3 * sum(times) / len(times),
-            "api": "fga_tree_forces (drop-in for _kernels.bh_forces_kernel), pinned host "
-                   "buffers, initial template state, FP32 traversal",
-            "visits_per_query": float(vis.mean())}
-
-
-def batch_pairs(P, rank=0, world=1):
-    """configs[4]: 3DMatch-fragment-sized pairs, 4096 points each, blob/box
-    alternating (synth.fragment_pair); this rank's share is
-    p = rank, rank+world, ... (pairs sharded, no collective)."""
-    from paper_2009_14005_b200 import synth
-    return [synth.fragment_pair(p) for p in range(rank, P, world)]
+                         "work": "20 FLOP/pair", "traffic": _profile("direct").get("dram_bytes")}}
 
 
 def run_batched(args, rank, world):
-    """configs[4]: all pairs in one persistent kernel (fga_register_batch),
-    default params (theta 0.6).  `kernel_s`: CUDA events around the kernel on
-    device-resident clouds; `wall_s`: the C-ABI call on pinned host buffers
-    (H2D of all clouds + kernel + D2H of the results)."""
+    """configs[4]: the pairs sharded over the ranks with no collective on the
+    data path (distributed.register_batch_sharded, every rank one persistent
+    kernel over its share), default params (theta 0.6).  `wall_s`: the public
+    API from host PointClouds (H2D of the rank's clouds, kernel, D2H of its
+    results; gather=False), max over ranks; `kernel_s`: CUDA events around
+    fga_register_batch_dev on the same device-resident clouds, max over
+    ranks."""
     import ctypes
 
     import torch
 
     import paper_2009_14005_b200 as fga
     from paper_2009_14005_b200 import _native as N
-    pairs = batch_pairs(args.batch_pairs, rank, world)
-    P = len(pairs)
-    xoff = np.zeros(P + 1, np.int64)
-    yoff = np.zeros(P + 1, np.int64)
-    xoff[1:] = np.cumsum([len(x) for x, _ in pairs])
-    yoff[1:] = np.cumsum([len(y) for _, y in pairs])
-
-    def pinned(a):
-        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True).numpy()
-        t[:] = a
-        return t
-
-    X = pinned(np.concatenate([x.points for x, _ in pairs]))
-    Y = pinned(np.concatenate([y.points for _, y in pairs]))
-    params = fga.default_params()
-    cp = N.make_params(params)
-    co = fga.registration._c_options(fga.RegisterOptions(), None, None)
-    out = (N.CPairResult * P)()
-    c = N.context(torch.cuda.current_device())
-    c.set_stream(torch.cuda.current_stream().cuda_stream)
-    L = N.lib()
-
-    def host_call():
-        N.check(L.fga_register_batch(c.handle, N.ptr(X), N.ptr(xoff), N.ptr(Y), N.ptr(yoff), P, 3,
-                                     ctypes.byref(cp), ctypes.byref(co), ctypes.addressof(out),
-                                     None))
-
-    host_call()  # warm-up: full-size scratch, all code paths
-    dev = torch.device("cuda", torch.cuda.current_device())
-    Xd = torch.from_numpy(X).to(dev)
-    Yd = torch.from_numpy(Y).to(dev)
-    xo = torch.from_numpy(xoff).to(dev)
-    yo = torch.from_numpy(yoff).to(dev)
-    res_d = torch.empty(P * ctypes.sizeof(N.CPairResult), dtype=torch.uint8, device=dev)
-    nmax = int(np.diff(xoff).max())
-    mmax = int(np.diff(yoff).max())
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    from paper_2009_14005_b200 import synth
+    from paper_2009_14005_b200.distributed import register_batch_sharded, shard_of
+    dist = None
     if world > 1:
         import torch.distributed as dist
+    P = args.batch_pairs
+    mine = shard_of(P, rank, world)
+    pairs = {p: synth.fragment_pair(p) for p in mine}
+    params = fga.default_params()
+    register_batch_sharded(lambda p: pairs[p], params=params, n_pairs=P, gather=False)  # warm
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    br = register_batch_sharded(lambda p: pairs[p], params=params, n_pairs=P, gather=False)
+    wall = time.perf_counter() - t0
+    its = np.array([br.results[p].iterations for p in mine if br.results[p] is not None])
+    inter = float(sum(int(br.interactions[p]) for p in mine))
+    failed = int(sum(br.status[p] != 0 for p in mine))
+    # the kernel alone on device-resident clouds
+    local = [pairs[p] for p in mine]
+    xoff = np.zeros(len(local) + 1, np.int64)
+    yoff = np.zeros(len(local) + 1, np.int64)
+    xoff[1:] = np.cumsum([len(x) for x, _ in local])
+    yoff[1:] = np.cumsum([len(y) for _, y in local])
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Xd = torch.from_numpy(np.concatenate([x.points for x, _ in local])).to(dev)
+    Yd = torch.from_numpy(np.concatenate([y.points for _, y in local])).to(dev)
+    xo = torch.from_numpy(xoff).to(dev)
+    yo = torch.from_numpy(yoff).to(dev)
+    res_d = torch.empty(len(local) * ctypes.sizeof(N.CPairResult), dtype=torch.uint8, device=dev)
+    cp = N.make_params(params)
+    co = fga.registration._c_options(fga.RegisterOptions(), None, None)
+    c = N.context(dev.index)
+    c.set_stream(torch.cuda.current_stream().cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
         dist.barrier()
     torch.cuda.synchronize()
     e0.record()
-    N.check(L.fga_register_batch_dev(c.handle, Xd.data_ptr(), xo.data_ptr(), Yd.data_ptr(),
-                                     yo.data_ptr(), P, nmax, mmax, 3, ctypes.byref(cp),
-                                     ctypes.byref(co), res_d.data_ptr(), None))
+    N.check(N.lib().fga_register_batch_dev(c.handle, Xd.data_ptr(), xo.data_ptr(), Yd.data_ptr(),
+                                           yo.data_ptr(), len(local), int(np.diff(xoff).max()),
+                                           int(np.diff(yoff).max()), 3, ctypes.byref(cp),
+                                           ctypes.byref(co), res_d.data_ptr(), None))
     e1.record()
     torch.cuda.synchronize()
     kernel_s = e0.elapsed_time(e1) / 1e3
-    t0 = time.perf_counter()
-    host_call()
-    wall = time.perf_counter() - t0
-    its = np.array([r.iterations for r in out])
-    inter = float(sum(r.interactions for r in out))
-    failed = int(sum(r.status != 0 for r in out))
-    if world > 1:
-        import torch.distributed as dist
+    c.set_stream(None)
+    if dist:
         t = torch.tensor([wall, kernel_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         wall, kernel_s = float(t[0]), float(t[1])
@@ -574,17 +765,17 @@ def run_batched(args, rank, world):
         inter, failed = float(s2[0]), int(s2[1])
         if rank != 0:
             return None
-    return {"workload": f"configs[4]: {args.batch_pairs} pairs x 4096 pts (blob/box, seeds "
-                        "100000+p, <=60 deg), default params (theta 0.6)",
-            "pairs_per_s": args.batch_pairs / kernel_s, "kernel_s": kernel_s,
-            "e2e_pairs_per_s": args.batch_pairs / wall, "wall_s": wall,
+    return {"workload": f"configs[4]: {P} pairs x 4096 pts (synth.fragment_pair: blob/box, "
+                        "seeds 100000+p, <=60 deg), default params (theta 0.6)",
+            "pairs_per_s": P / kernel_s, "kernel_s": kernel_s,
+            "e2e_pairs_per_s": P / wall, "wall_s": wall,
             "interactions_per_s": inter / kernel_s,
-            "iterations_min_median_max": [int(its.min()), float(np.median(its)), int(its.max())],
+            "iterations_min_median_max_rank0": [int(its.min()), float(np.median(its)),
+                                                 int(its.max())],
             "failed": failed,
-            "api": "fga_register_batch_dev (device clouds, CUDA events) / fga_register_batch "
-                   "(pinned host buffers, wall clock)",
-            "h2d_bytes": int(X.nbytes + Y.nbytes + xoff.nbytes + yoff.nbytes),
-            "sharding": f"pairs split over {world} GPU(s), no collective"}
+            "api": "distributed.register_batch_sharded (host clouds, wall clock, max over "
+                   "ranks) / fga_register_batch_dev (device clouds, CUDA events)",
+            "sharding": f"pairs p = rank, rank+{world}, ... over {world} GPU(s), no collective"}
 
 
 def run_other_configs(args):
@@ -679,83 +870,146 @@ def run_ingest(x):
                    "per-line algorithm in Python"}
 
 
-def run_registration(args, x, y):
+def run_registration(args, x, y, cpu):
+    """Full register() on configs[2] from host numpy (normalize, NIV masses,
+    tree, 2x O(NM) energy, the iteration loop, denormalize), median of 3
+    after a full-size warm-up; beside it the CPU reference's wall time for
+    the same registration, EXTRAPOLATED from the oracle's measured pieces on
+    this host (build timed in full; one iteration and one energy from timed
+    samples, scaled linearly in M; x the GPU's iteration count)."""
     import paper_2009_14005_b200 as fga
     p = bench_params(args)
-    fga.register(x, y, params=p)  # warm-up at full size (allocations, module loads)
+    fga.register(x, y, params=p)
     walls = []
     for _ in range(3):
         t0 = time.perf_counter()
         r = fga.register(x, y, params=p)
         walls.append(time.perf_counter() - t0)
     wall = float(np.median(walls))
-    return {"wall_s": wall, "walls_s": walls, "iterations": r.iterations, "converged": r.converged,
-            "interactions": int(r.interactions.sum()), "timings_ms": r.timings_ms,
-            "params": {"theta": p.theta, "G": p.G, "max_iters": p.max_iters,
-                       "conv_tol": p.conv_tol},
-            "api": "register(x, y) from host numpy, median of 3 calls after a full-size "
-                   "warm-up; includes normalize, NIV masses, tree build, 2x O(NM) energy "
-                   "and the iteration loop"}
+    out = {"wall_s": wall, "walls_s": walls, "iterations": r.iterations,
+           "converged": r.converged, "interactions": int(r.interactions.sum()),
+           "timings_ms": r.timings_ms,
+           "params": {"theta": p.theta, "G": p.G, "max_iters": p.max_iters,
+                      "conv_tol": p.conv_tol},
+           "api": "register(x, y) from host numpy, median of 3 calls after a full-size warm-up"}
+    if cpu:
+        it_s = cpu["iteration_s_extrapolated"]
+        gpe_s = cpu["gpe_s_extrapolated"]
+        est = cpu["tree_build_s"] + r.iterations * it_s + 2 * gpe_s
+        out["cpu_reference_extrapolated"] = {
+            "wall_s": est, "cores": cpu["cores"], "kind": "port",
+            "parts": {"tree_build_s (measured, 1 core)": cpu["tree_build_s"],
+                      "iteration_s (sampled x M/sample)": it_s,
+                      "gpe_s (sampled x M/sample)": gpe_s, "iterations": r.iterations},
+            "speedup": est / wall, "label": "extrapolated"}
+    return out
+
+
+def run_configs0():
+    """configs[0] (the reference's CPU-runnable case): 2,000 x 2,000 blob
+    pairs, seeds 0..19 (synth.blob, <= 60 deg / 0.1), theta 0.5, NIV masses.
+    GPU register() median wall over the 20 seeds vs the oracle's register()
+    (the reference's algorithm) on 1 host core and on all host cores,
+    MEASURED; same iteration counts required."""
+    import paper_2009_14005_b200 as fga
+    from oracle import oracle as orc
+    from paper_2009_14005_b200 import synth
+    orc.build_lib()
+    pairs = []
+    for s in range(20):
+        rng = synth.rng_from_seed(s)
+        x = synth.blob(2000, rng)
+        pairs.append((x, synth.misalign(x, synth.random_rigid(rng, np.deg2rad(60), 0.1))))
+    p = fga.default_params().replace(theta=0.5)
+    fga.register(*pairs[0], params=p)
+    gw, its = [], []
+    for x, y in pairs:
+        t0 = time.perf_counter()
+        r = fga.register(x, y, params=p)
+        gw.append(time.perf_counter() - t0)
+        its.append(r.iterations)
+    threads = orc.max_threads()
+    cw1, cwn, oits = [], [], []
+    for x, y in pairs:
+        t0 = time.perf_counter()
+        o = orc.register(x.points, y.points, theta=0.5, nthreads=1)
+        cw1.append(time.perf_counter() - t0)
+        oits.append(o.iterations)
+        t0 = time.perf_counter()
+        orc.register(x.points, y.points, theta=0.5, nthreads=threads)
+        cwn.append(time.perf_counter() - t0)
+    return {"workload": "configs[0]: 20 blob pairs 2,000 x 2,000 (seeds 0-19), theta 0.5",
+            "gpu_wall_median_s": float(np.median(gw)),
+            "cpu_1core_wall_median_s": float(np.median(cw1)),
+            "cpu_all_cores_wall_median_s": float(np.median(cwn)), "cpu_cores": threads,
+            "speedup_vs_1core": float(np.median(cw1) / np.median(gw)),
+            "speedup_vs_all_cores": float(np.median(cwn) / np.median(gw)),
+            "iterations_equal": its == oits, "iterations_median": float(np.median(its)),
+            "cpu_kind": "port (oracle.register: C tree/forces/energy + numpy Kabsch, "
+                        "restating registration.py:91-166)"}
 
 
 # --------------------------------------------------------------------------- CPU
 def cpu_baseline(args, x, y, sample):
     """The C oracle (OpenMP, all host threads) on a bounded sample of the same
-    workload: tree over the normalized reference, bh_forces for `sample`
-    template queries at the initial state."""
+    workload and state: tree over the normalized reference (timed, 1 core),
+    bh_forces for `sample` template queries at the initial state, and the
+    O(NM) energy for 4,096 template points (for the registration
+    extrapolation)."""
     from oracle import oracle as orc
     orc.build_lib()
     bp = bench_params(args)
-    p = {"G": bp.G, "eps": 0.2}
-    xn, yn, ctx = orc.normalize_pair(x.points, y.points, -5.0, 5.0)
-    sx = orc.niv_masses(xn, 16, -5.0, 5.0, 20)
-    sy = orc.niv_masses(yn, 16, -5.0, 5.0, 20)
-    mx, my = orc.rescale(sx, sy, 0.1, 0.2)
+    xn, yn, mx, my, _ = orc.setup(x.points, y.points)
     t0 = time.perf_counter()
     tree = orc.tree_build(xn, mx, 20)
     build_s = time.perf_counter() - t0
     idx = np.random.default_rng(0).choice(len(yn), size=min(sample, len(yn)), replace=False)
     threads = orc.max_threads()
     t0 = time.perf_counter()
-    _, visits, acc = orc.bh_forces(tree, yn[idx], my[idx], args.theta, p["G"], p["eps"], threads)
+    _, visits, acc = orc.bh_forces(tree, yn[idx], my[idx], args.theta, bp.G, bp.epsilon, threads)
     dt = time.perf_counter() - t0
     # SURVEY §8(d): the reference as shipped is single-threaded -- one core
     # on a quarter of the sample
     idx1 = idx[: max(1, len(idx) // 4)]
     t0 = time.perf_counter()
-    _, _, acc1 = orc.bh_forces(tree, yn[idx1], my[idx1], args.theta, p["G"], p["eps"], 1)
+    _, _, acc1 = orc.bh_forces(tree, yn[idx1], my[idx1], args.theta, bp.G, bp.epsilon, 1)
     dt1 = time.perf_counter() - t0
+    gidx = idx[:4096]
+    t0 = time.perf_counter()
+    orc.gpe(yn[gidx], my[gidx], xn, mx, bp.G, bp.epsilon, threads)
+    gpe_dt = time.perf_counter() - t0
     return {"value": float(acc.sum()) / dt, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{len(idx)} template queries of the {len(yn)}-point workload at the "
                       f"initial state (oracle bh_forces, theta={args.theta}); tree build "
                       f"{build_s:.2f} s single-threaded",
             "seconds": dt, "visits_per_query": float(visits.mean()),
+            "tree_build_s": build_s,
+            "iteration_s_extrapolated": dt * len(yn) / len(idx),
+            "gpe_s_extrapolated": gpe_dt * len(yn) / len(gidx),
             "one_core": {"value": float(acc1.sum()) / dt1, "unit": UNIT, "cores": 1,
                          "sample": f"{len(idx1)} of the same queries", "seconds": dt1}}
 
 
 def run_reference(args, rank):
     """--impl reference: the reference's CPU algorithm (C oracle port, all host
-    threads) on the same config / metric; each step = one bounded sample."""
+    threads) on the same config and state; each step = bh_forces on 16,384
+    template queries sampled from the initial state."""
     if rank != 0:
         return None
     from oracle import oracle as orc
     orc.build_lib()
     x, y = workload(args.n, args.seed)
-    xn, yn, _ = orc.normalize_pair(x.points, y.points, -5.0, 5.0)
-    sx = orc.niv_masses(xn, 16, -5.0, 5.0, 20)
-    sy = orc.niv_masses(yn, 16, -5.0, 5.0, 20)
-    mx, my = orc.rescale(sx, sy, 0.1, 0.2)
+    bp = bench_params(args)
+    xn, yn, mx, my, _ = orc.setup(x.points, y.points)
     tree = orc.tree_build(xn, mx, 20)
     threads = orc.max_threads()
-    G = 66.7 if args.default_g else 66.7 * (2000.0 / args.n) ** 0.5
     sample = min(16384, len(yn))
     rng = np.random.default_rng(1)
 
     def step():
         idx = rng.choice(len(yn), size=sample, replace=False)
         t0 = time.perf_counter()
-        _, _, acc = orc.bh_forces(tree, yn[idx], my[idx], args.theta, G, 0.2, threads)
+        _, _, acc = orc.bh_forces(tree, yn[idx], my[idx], args.theta, bp.G, bp.epsilon, threads)
         return float(acc.sum()), time.perf_counter() - t0
 
     for _ in range(args.warmup):
@@ -772,8 +1026,7 @@ def run_reference(args, rank):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[2]: 1M x 1M FGA pair, Barnes-Hut theta=%g"
-                       % args.theta, "n_reference": len(x), "n_template": len(y)},
+            "config": config_dict(args, len(x), len(y), tree.node_count, args.gpus),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                              "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -782,9 +1035,16 @@ def run_reference(args, rank):
 
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dry_run:
+        line = run_dry(args, rank, world)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
     if args.impl == "reference":
         line = run_reference(args, rank)
         if line is not None:
@@ -793,6 +1053,10 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # NCCL init logging: the communicator's rank count and transport are
+        # in the log (stderr), so an N-rank run is verifiable
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     line = run_ours(args, rank, world, local_rank)

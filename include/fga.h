@@ -199,6 +199,10 @@ int fga_session_get_state(fga_ctx* ctx, double* pos, double* vel, double* racc9,
                           int64_t* iter);
 int fga_session_set_state(fga_ctx* ctx, const double* pos, const double* vel, const double* racc9,
                           const double* tacc3, int64_t iter);
+/* Device-side checkpoint of this shard's iteration state (template
+ * positions/velocities, pending and accumulated transforms, iteration
+ * counter): restore = 0 saves, 1 restores (stream-ordered, no host copy). */
+int fga_session_checkpoint(fga_ctx* ctx, int restore);
 /* The session's rescaled mass fields (registration.py:85-87) in input order:
  * mx (n) for the reference, my (m) for the template; either may be NULL. */
 int fga_session_masses(fga_ctx* ctx, double* mx, double* my);

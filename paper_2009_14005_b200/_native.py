@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 import re
+import sys
 import threading
 
 import numpy as np
@@ -127,6 +128,7 @@ SIGNATURES = {
                                  ctypes.POINTER(_c_int)]),
     "fga_parse_weights": (_c_int, [ctypes.c_char_p, _i64, _vp, _i64, ctypes.POINTER(_i64)]),
     "fga_session_masses": (_c_int, [_vp, _vp, _vp]),
+    "fga_session_checkpoint": (_c_int, [_vp, _c_int]),
     "fga_session_info": (_c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "fga_tree_build": (_c_int, [_vp, _vp, _vp, _i64, _c_int, _c_int, ctypes.POINTER(_i64)]),
     "fga_tree_build_dev": (_c_int, [_vp, _vp, _vp, _i64, _c_int, ctypes.POINTER(_i64)]),
@@ -272,6 +274,9 @@ def context(device: int | None = None) -> Context:
     device if torch is imported and CUDA is available, else 0)."""
     if device is None:
         device = 0
+        torch = sys.modules.get("torch")
+        if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():
+            device = torch.cuda.current_device()
     cache = getattr(_ctx_local, "cache", None)
     if cache is None:
         cache = _ctx_local.cache = {}

@@ -49,6 +49,8 @@ struct Session {
   DevBuf tkeys_in, tkeys, tidx_in, tidx, cub_tmp, tpl;
   DevBuf partials, gpe_part, sums, state, scratch, lm_idx, rbf_scratch, red_stage;
   DevBuf gpe_snap, gpe_part2, gpe_sums2;  // initial energy on the aux stream
+  DevBuf ckpt;                            // device-side checkpoint (fga_session_checkpoint)
+  bool have_ckpt = false;
   DevBuf rec_delta, rec_traj, rec_gpe, rec_inter, rec_visits;
   // the session's own reference tree: operator-level builds / uploads into
   // the context (fga_tree_*) never disturb a live registration, and a
@@ -596,6 +598,7 @@ int fga_destroy(fga_ctx* c) {
   Session& S = c->S;
   S.lm_idx.release();
   S.rbf_scratch.release();
+  S.ckpt.release();
   DevBuf* all[] = {&S.x_raw,   &S.y_raw,  &S.xn,        &S.yn,       &S.ctx_dev,   &S.mx,
                    &S.my,      &S.flat,   &S.counts,    &S.cells,    &S.ref32,     &S.ref64,
                    &S.tkeys_in, &S.tkeys, &S.tidx_in,   &S.tidx,     &S.cub_tmp,   &S.tpl,
@@ -806,6 +809,31 @@ int fga_session_set_state(fga_ctx* c, const double* pos, const double* vel, cons
   st.gpe_pending = 0;
   FGA_CUDA_TRY(cudaMemcpyAsync(S.st(), &st, sizeof(st), cudaMemcpyHostToDevice, s));
   FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  S.applied = false;
+  S.have_gpe_final = false;
+  return FGA_OK;
+}
+
+int fga_session_checkpoint(fga_ctx* c, int restore) {
+  SESSION_TRY(c);
+  Session& S = c->S;
+  cudaStream_t s = c->stream;
+  const size_t tpl = sizeof(double) * 7 * std::max<int64_t>(S.m_local, 1);
+  if (!restore) {
+    FGA_CUDA_TRY(S.ckpt.reserve(tpl + sizeof(IterState)));
+    FGA_CUDA_TRY(cudaMemcpyAsync(S.ckpt.p, S.tpl.p, tpl, cudaMemcpyDeviceToDevice, s));
+    FGA_CUDA_TRY(cudaMemcpyAsync(S.ckpt.as<char>() + tpl, S.state.p, sizeof(IterState),
+                                 cudaMemcpyDeviceToDevice, s));
+    S.have_ckpt = true;
+    return FGA_OK;
+  }
+  if (!S.have_ckpt) {
+    set_error("checkpoint: nothing saved in this session");
+    return FGA_ERR_STATE;
+  }
+  FGA_CUDA_TRY(cudaMemcpyAsync(S.tpl.p, S.ckpt.p, tpl, cudaMemcpyDeviceToDevice, s));
+  FGA_CUDA_TRY(cudaMemcpyAsync(S.state.p, S.ckpt.as<char>() + tpl, sizeof(IterState),
+                               cudaMemcpyDeviceToDevice, s));
   S.applied = false;
   S.have_gpe_final = false;
   return FGA_OK;

@@ -89,6 +89,14 @@ class Session:
         N.check(N.lib().fga_session_set_state(self.ctx.handle, N.ptr(pos), N.ptr(vel), N.ptr(R),
                                               N.ptr(t), int(iteration)))
 
+    def checkpoint(self):
+        """Save this shard's iteration state on the device (fga_session_checkpoint)."""
+        N.check(N.lib().fga_session_checkpoint(self.ctx.handle, 0))
+
+    def restore(self):
+        """Return to the last checkpoint (stream-ordered device copy)."""
+        N.check(N.lib().fga_session_checkpoint(self.ctx.handle, 1))
+
     def masses(self):
         """(mx, my): the rescaled mass fields in input order (fga_session_masses)."""
         mx = np.empty(self.n)

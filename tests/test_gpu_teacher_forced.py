@@ -133,3 +133,28 @@ def test_teacher_forced_config_shapes(golden, fga, case, precision):
         s.iterate(1)
         r = s.finish()
         assert np.abs(r.trajectory[it] - g[k + "traj"][it]).max() < tol
+
+
+def test_device_checkpoint_restore_is_exact(fga):
+    """fga_session_checkpoint: save on the device after k iterations, run on,
+    restore, run the same iterations again -- bitwise the same transforms
+    (bench.py re-times the initial state this way)."""
+    from paper_2009_14005_b200 import synth
+    from paper_2009_14005_b200.engine import Session
+    rng = synth.rng_from_seed(12)
+    x = synth.blob(5000, rng)
+    y = synth.misalign(x, synth.random_rigid(rng, np.deg2rad(40), 0.1))
+    p = fga.default_params().replace(theta=0.5, conv_tol=1e-300, max_iters=20)
+    s = Session(x, y, p, fga.RegisterOptions(compute_gpe=False, record_iterations=True))
+    s.iterate(3)
+    s.checkpoint()
+    s.iterate(2)
+    a = s.get_state()
+    s.restore()
+    s.iterate(2)
+    b = s.get_state()
+    s.finish()
+    assert a["iteration"] == b["iteration"] == 5
+    assert np.array_equal(a["positions"], b["positions"])
+    assert np.array_equal(a["velocities"], b["velocities"])
+    assert np.array_equal(a["R_acc"], b["R_acc"]) and np.array_equal(a["t_acc"], b["t_acc"])
