@@ -38,7 +38,10 @@ def test_batch_matches_single_pair_path(orc):
         assert np.abs(r.transform.translation - s.transform.translation).max() < 1e-8
         d1 = np.array([q.transform_delta for q in r.records])
         d2 = np.array([q.transform_delta for q in s.records])
-        assert np.allclose(d1, d2, rtol=1e-6, atol=1e-14)
+        # per-iteration deltas (squared transform steps): the single-pair path
+        # sums the FP32 force in fp64 chunks (split into node-range parts for
+        # small templates), the batched kernel in its own order
+        assert np.allclose(d1, d2, rtol=1e-5, atol=1e-14)
         assert abs(r.gpe_initial - s.gpe_initial) <= 1e-6 * abs(s.gpe_initial)
         assert abs(r.gpe_final - s.gpe_final) <= 1e-6 * abs(s.gpe_final)
     for (x, y), r in list(zip(pairs, br.results))[:2]:
