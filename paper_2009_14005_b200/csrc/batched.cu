@@ -448,6 +448,18 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
         S.keys[i] = key;
         S.idx[i] = i;
       }
+#if FGA_CHECKS
+      {  // (status-based: trap-based checks perturbed this kernel, profiles/r02/README.md)
+        __syncthreads();
+        bitonic_sort(S.keys, S.idx, a.P);
+        int bad = 0;
+        for (int i = tid + 1; i < a.P; i += kBT) bad |= S.keys[i - 1] > S.keys[i];
+        bad = __syncthreads_or(bad);
+        if (bad && tid == 0) st.status = FGA_ERR_STATE;
+        __syncthreads();
+        if (st.status) goto finish;
+      }
+#endif
       __syncthreads();
       bitonic_sort(S.keys, S.idx, a.P);
       for (int i = tid; i <= n; i += kBT) {

@@ -309,6 +309,7 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
       ax = ay = az = 0.f;
       lim = fold_limit(n, n_nodes);
     }
+    FGA_CHECK(n >= 0 && n < n_nodes);
     const NodeC32* rec = reinterpret_cast<const NodeC32*>(C) + n;
     const float4 a = __ldg(&rec->a);
     const float4 b = __ldg(&rec->b);

@@ -14,6 +14,7 @@
 //     skip = index just past the node's subtree, so a stackless traversal
 //     that only ever moves forward reproduces the reference visit set.
 #pragma once
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -62,6 +63,26 @@ struct SimParams {
   int dim;            // 2 or 3 (2-D clouds are carried as z = const)
   int count_visits;   // FP32 force pass counts node visits (fga_options.count_visits)
 };
+
+// ---------------------------------------------------------------- checks
+// Device-side invariant checks (bounds of shared/global indices, the tree
+// build's arrival counters), compiled in only for the FGA_CHECKS=1 test
+// build (tools/build_variant.sh checks "-DFGA_CHECKS=1"): a failure traps, so
+// the launch fails loudly (FGA_CHECKS=2 also prints the site).  compute-sanitizer is not
+// available on this GPU pool; this build + tests/test_gpu_determinism.py are
+// the race / out-of-bounds evidence (profiles/r02/README.md).
+#ifndef FGA_CHECKS
+#define FGA_CHECKS 0
+#endif
+#define FGA_CHECK(cond)                                                              \
+  do {                                                                               \
+    if (FGA_CHECKS && !(cond)) {                                                     \
+      if (FGA_CHECKS > 1)                                                            \
+        printf("FGA_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__,  \
+               __LINE__, (int)blockIdx.x, (int)threadIdx.x);                         \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
 
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);

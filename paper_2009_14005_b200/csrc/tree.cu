@@ -620,8 +620,10 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
       }
       while (lv < l) bbox_step(key, ++lv, L, bl, bh);
       const double len = diag_len(bl, bh);
+      FGA_CHECK(j >= 0 && j < kST && l >= sj && l <= ej && x >= offs[j] && x < offs[j + 1]);
       if (l == ej) {
         const int mir = l + nn - (x + 1);
+        FGA_CHECK(mir >= 0 && mir < nn);
         write_records_b(r, mir, mir + 1, true, len);
       } else {
         const int p = l <= lca ? kST : next_bit(mB[l], nzB[l], j);
@@ -650,7 +652,9 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
     const int nch = count_bits(mH[lev], hp, pend);
     __threadfence_block();  // this child's V before the arrival
     const unsigned sh = 8u * (hp & 3);  // byte counters, four per word
+    FGA_CHECK(hp >= 0 && hp < kST && pend > hp && pend <= kST && nch >= 1 && nch <= 8);
     const unsigned old_ = atomicAdd(&arrived[pl][hp >> 2], 1u << sh);
+    FGA_CHECK((int)((old_ >> sh) & 0xffu) < nch);  // never more arrivals than children
     if ((int)((old_ >> sh) & 0xffu) != nch - 1) {
       up = false;
       break;
@@ -679,6 +683,7 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
       cr.plend[pl * nb + b] = local ? pend : -1;
     } else if (local) {  // queued: the divisions run compacted after the climb
       const int slot = atomicAdd(&s_q, 1);
+      FGA_CHECK(pl + nn - offs[pend] >= 0 && pl + nn - offs[pend] < nn);
       if (slot < kST) {
         qv[slot] = v;
         qmir[slot] = pl + nn - offs[pend];
