@@ -895,6 +895,17 @@ __global__ void __launch_bounds__(256) k_export(const unsigned long long* __rest
 
 }  // namespace
 
+// cells at the level cap holding >= 2 points (bit 0) and whether two of
+// them are distinct (bit 1): clev[i] == L means point i shares all L levels
+// with point i - 1
+__global__ void k_cap_runs(const double4* __restrict__ sp, const signed char* __restrict__ clev,
+                           int64_t n, int L, int* __restrict__ flag) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + 1;
+  if (i >= n || clev[i] < L) return;
+  const double4 a = sp[i - 1], b = sp[i];
+  atomicOr(flag, (a.x != b.x || a.y != b.y || a.z != b.z) ? 3 : 1);
+}
+
 // ------------------------------------------------------------------ host side
 int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, int64_t n, int L,
                    cudaStream_t st) {
@@ -907,10 +918,13 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
     set_error("tree build: more than 2^31 points");
     return FGA_ERR_UNSUPPORTED;
   }
-  if (L < 1 || L > kMaxLevels) {
-    set_error("tree build: max_depth must be in [1, 21] on the GPU path");
-    return FGA_ERR_UNSUPPORTED;
+  if (L < 1) {
+    set_error("tree build: max_depth must be >= 1");
+    return FGA_ERR_INVALID;
   }
+  T.L_requested = L;
+  T.cap_runs = T.cap_distinct = false;
+  if (L > kMaxLevels) L = kMaxLevels;  // see TreeDev::L_requested
   T.n_points = n;
   T.L = L;
   T.pts = pts_dev;
@@ -1060,6 +1074,16 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   }
   FGA_CUDA_TRY(cudaGetLastError());
   T.exportable = true;
+  if (T.L_requested > kMaxLevels) {  // cells at the 21-level cap: one sync, rare path
+    FGA_CUDA_TRY(cudaMemsetAsync(T.flags.as<int>() + 1, 0, sizeof(int), st));
+    k_cap_runs<<<blocks_for(n), kThreads, 0, st>>>(T.sp.as<double4>(), T.clev.as<signed char>(), n,
+                                                   L, T.flags.as<int>() + 1);
+    int f = 0;
+    FGA_CUDA_TRY(cudaMemcpyAsync(&f, T.flags.as<int>() + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    FGA_CUDA_TRY(cudaStreamSynchronize(st));
+    T.cap_runs = (f & 1) != 0;
+    T.cap_distinct = (f & 2) != 0;
+  }
   return FGA_OK;
 }
 

@@ -157,10 +157,14 @@ class BatchResult:
 
 def register_batch(pairs, params: FgaParams | None = None,
                    options: RegisterOptions | None = None) -> BatchResult:
-    """register(x, y) for many independent (x, y) pairs in ONE persistent
-    device kernel (BASELINE configs[4]; csrc/batched.cu).  Each cloud may hold
-    up to 8192 points.  Landmarks are not supported; external weights in
-    options.x_weights / y_weights must be lists (one array per pair)."""
+    """register(x, y) for many independent (x, y) pairs: every pair the
+    persistent batched kernel takes (D = 3, <= 8192 points per cloud, FP32
+    forces, NIV or external masses, max_depth <= 21; csrc/batched.cu) runs in
+    ONE launch, the others -- and any pair the kernel reports as over its
+    limits (e.g. a node cap) -- through register() one by one, so every pair
+    gets the result register() gives it.  External weights in
+    options.x_weights / y_weights must be lists (one array per pair); per-pair
+    failures are reported in ``errors`` (registration.py:192-200)."""
     params = params or default_params()
     options = options or RegisterOptions()
     validate(params)
@@ -168,12 +172,50 @@ def register_batch(pairs, params: FgaParams | None = None,
     P = len(pairs)
     if P == 0:
         return BatchResult([], [], np.zeros(0, np.int64), np.zeros(0, np.int32))
-    xs, ys = [], []
     for x, y in pairs:
         if x.dim != y.dim:
             raise EmptyCloud(f"dimension mismatch: {x.dim} vs {y.dim}")
-        xs.append(x.points)
-        ys.append(y.points)
+    kernel_options = (options.precision == "fp32" and options.mass_field == "niv"
+                      and not options.trace_gpe
+                      and params.max_depth <= 21 and params.rho ** 3 <= 16384)
+    in_kernel = [k for k, (x, y) in enumerate(pairs)
+                 if kernel_options and x.dim == 3 and max(len(x), len(y)) <= 8192]
+    results, errors = [None] * P, [None] * P
+    inter = np.zeros(P, np.int64)
+    status = np.zeros(P, np.int32)
+    if in_kernel:
+        br = _register_batch_kernel([pairs[k] for k in in_kernel], params, options,
+                                    None if options.x_weights is None else
+                                    [options.x_weights[k] for k in in_kernel],
+                                    None if options.y_weights is None else
+                                    [options.y_weights[k] for k in in_kernel])
+        for j, k in enumerate(in_kernel):
+            results[k], errors[k] = br.results[j], br.errors[j]
+            inter[k], status[k] = br.interactions[j], br.status[j]
+    rest = [k for k in range(P) if k not in set(in_kernel) or status[k] == N.FGA_ERR_UNSUPPORTED]
+    for k in rest:
+        x, y = pairs[k]
+        o = RegisterOptions(**{**options.__dict__,
+                               "x_weights": None if options.x_weights is None else
+                               options.x_weights[k],
+                               "y_weights": None if options.y_weights is None else
+                               options.y_weights[k]})
+        try:
+            r = register(x, y, params=params, options=o)
+            results[k], errors[k] = r, None
+            inter[k] = int(r.interactions.sum())
+            status[k] = 0
+        except GravregError as e:
+            results[k], errors[k] = None, e
+            status[k] = N.FGA_ERR_UNSUPPORTED if isinstance(e, DeviceError) else N.FGA_ERR_INVALID
+    return BatchResult(results, errors, inter, status)
+
+
+def _register_batch_kernel(pairs, params, options, xws, yws) -> BatchResult:
+    """The persistent batched kernel on pairs it supports (fga_register_batch)."""
+    P = len(pairs)
+    xs = [x.points for x, _ in pairs]
+    ys = [y.points for _, y in pairs]
     xoff = np.zeros(P + 1, np.int64)
     yoff = np.zeros(P + 1, np.int64)
     xoff[1:] = np.cumsum([len(a) for a in xs])
@@ -181,19 +223,19 @@ def register_batch(pairs, params: FgaParams | None = None,
     X = np.ascontiguousarray(np.concatenate(xs) if xoff[-1] else np.zeros((0, 3)))
     Y = np.ascontiguousarray(np.concatenate(ys) if yoff[-1] else np.zeros((0, 3)))
     xw = yw = None
-    if options.x_weights is not None:
+    if xws is not None:
         xw = np.ascontiguousarray(np.concatenate(
-            [check_weights(len(a), w) for a, w in zip(xs, options.x_weights)]))
-    if options.y_weights is not None:
+            [check_weights(len(a), w) for a, w in zip(xs, xws)]))
+    if yws is not None:
         yw = np.ascontiguousarray(np.concatenate(
-            [check_weights(len(a), w) for a, w in zip(ys, options.y_weights)]))
+            [check_weights(len(a), w) for a, w in zip(ys, yws)]))
     c = N.context(options.device)
     out = (N.CPairResult * P)()
     deltas = np.zeros((P, params.max_iters)) if options.record_iterations else None
     cp = N.make_params(params)
     co = _c_options(options, xw, yw)
     N.check(N.lib().fga_register_batch(c.handle, N.ptr(X), N.ptr(xoff), N.ptr(Y), N.ptr(yoff), P,
-                                       pairs[0][0].dim, N.ctypes.byref(cp), N.ctypes.byref(co),
+                                       3, N.ctypes.byref(cp), N.ctypes.byref(co),
                                        N.ctypes.addressof(out), N.ptr(deltas)))
     results, errors = [], []
     inter = np.zeros(P, np.int64)
@@ -247,48 +289,39 @@ def register_sequence(frames, params: FgaParams | None = None,
     params = params or default_params()
     options = options or RegisterOptions()
     pairs = [(frames[i + 1], frames[i]) for i in range(len(frames) - 1)]
-    small = (max(len(f) for f in frames) <= 8192 and all(f.dim == 3 for f in frames)
-             and options.x_weights is None
-             and options.y_weights is None and options.mass_field == "niv"
-             and options.precision == "fp32" and not options.trace_gpe and options.normalize
-             and params.max_depth <= 21)
-    from concurrent.futures import ThreadPoolExecutor
-
-    def one(k):
-        x, y = pairs[k]
-        try:
-            return register(x=x, y=y, params=params, options=options).transform, False
-        except DeviceError:
-            raise
-        except GravregError:
-            return RigidTransform.identity(frames[k].dim), True
-
-    def run_threaded(ks):
-        n_workers = workers or min(4, len(ks))
-        if n_workers <= 1 or len(ks) <= 1:
-            return [one(k) for k in ks]
-        with ThreadPoolExecutor(max_workers=n_workers) as pool:
-            return list(pool.map(one, ks))
-
-    outs = [None] * len(pairs)
-    if small:
+    batched = (len(pairs) > 1 and all(f.dim == 3 and len(f) <= 8192 for f in frames)
+               and options.precision == "fp32" and options.mass_field == "niv"
+               and not options.trace_gpe and options.normalize
+               and options.x_weights is None and options.y_weights is None)
+    if batched:
+        # one persistent kernel; register_batch re-runs through register()
+        # any pair over the kernel's limits (node cap, max_depth > 21)
         br = register_batch(pairs, params=params, options=options)
-        rerun = []
+        outs = []
         for k, (res, err) in enumerate(zip(br.results, br.errors)):
-            if br.status[k] == N.FGA_ERR_UNSUPPORTED:
-                # over the batched kernel's per-pair limits (e.g. a single-child
-                # chain of near-duplicates past its node cap): register() runs it
-                rerun.append(k)
-                continue
             if err is not None and (not isinstance(err, GravregError)
                                     or isinstance(err, DeviceError)):
                 raise err
-            outs[k] = ((res.transform, False) if res is not None else
-                       (RigidTransform.identity(frames[k].dim), True))
-        for k, o in zip(rerun, run_threaded(rerun)):
-            outs[k] = o
+            outs.append((res.transform, False) if res is not None else
+                        (RigidTransform.identity(frames[k].dim), True))
     else:
-        outs = run_threaded(list(range(len(pairs))))
+        from concurrent.futures import ThreadPoolExecutor
+
+        def one(k):
+            x, y = pairs[k]
+            try:
+                return register(x=x, y=y, params=params, options=options).transform, False
+            except DeviceError:
+                raise
+            except GravregError:
+                return RigidTransform.identity(frames[k].dim), True
+
+        n_workers = workers or min(4, len(pairs))
+        if n_workers <= 1:
+            outs = [one(k) for k in range(len(pairs))]
+        else:
+            with ThreadPoolExecutor(max_workers=n_workers) as pool:
+                outs = list(pool.map(one, range(len(pairs))))
     pairwise = [o[0] for o in outs]
     failed = [o[1] for o in outs]
     poses = [RigidTransform.identity(frames[0].dim)]

@@ -121,8 +121,14 @@ def test_sequence_reruns_pairs_over_the_batched_cap():
     f0 = _near_duplicate_cloud(rng, 2000)
     g = synth.random_rigid(synth.rng_from_seed(9), np.deg2rad(6), 0.02)
     frames = [f0, synth.misalign(f0, g), synth.misalign(synth.misalign(f0, g), g)]
-    br = fga.register_batch([(frames[1], frames[0])])
-    assert br.status[0] == -4  # FGA_ERR_UNSUPPORTED: over the per-pair node cap
+    from paper_2009_14005_b200.registration import _register_batch_kernel
+    kb = _register_batch_kernel([(frames[1], frames[0])], fga.default_params(),
+                                fga.RegisterOptions(), None, None)
+    assert kb.status[0] == -4  # FGA_ERR_UNSUPPORTED: over the kernel's per-pair node cap
+    br = fga.register_batch([(frames[1], frames[0])])  # re-run through register()
+    assert br.errors[0] is None and br.status[0] == 0
+    single = fga.register(x=frames[1], y=frames[0]).transform
+    assert np.array_equal(br.results[0].transform.rotation, single.rotation)
     seq = fga.register_sequence(frames)
     assert not any(seq.failed)
     for k in range(2):
