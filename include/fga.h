@@ -269,7 +269,7 @@ int fga_knn(fga_ctx* ctx, const double* pts, int64_t n, int dim, int k, int64_t*
  * alternative to niv_masses, BASELINE configs[3]). */
 int fga_knn_masses(fga_ctx* ctx, const double* pts, int64_t n, int dim, int k, double* out);
 /* masses.rbf_masses (masses.py:55-82): Gaussian RBF through the anchors
- * pts[anchors[j]]; FGA_ERR_SINGULAR when cond(K) > 1e12.  m <= 64. */
+ * pts[anchors[j]]; FGA_ERR_SINGULAR when cond(K) > 1e12.  m <= 2048. */
 int fga_rbf_masses(fga_ctx* ctx, const double* pts, int64_t n, int dim, const int64_t* anchors,
                    int m, double sigma, double* out);
 /* masses.niv_masses (masses.py:85-116). */

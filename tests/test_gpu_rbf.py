@@ -61,3 +61,25 @@ def test_landmark_registration_matches_reference(golden, F):
     with pytest.raises(F.InvalidParam):
         F.register(F.PointCloud(g["lm/x"]), F.PointCloud(g["lm/y"]),
                    landmarks=F.LandmarkSet(((0, 10_000),)))
+
+
+@pytest.mark.parametrize("m,sigma", [(65, 0.6), (200, 0.5), (501, 0.4)])
+def test_rbf_many_landmarks_vs_oracle(F, orc, m, sigma):
+    """More than 64 landmarks (the reference is unbounded): the parallel
+    Jacobi collocation solve (rbf.cu k_rbf_solve_large) against the oracle's
+    numpy restatement of masses.py:55-82."""
+    rng = np.random.default_rng(m)
+    pts = rng.uniform(-5, 5, size=(20000, 3))
+    anchors = sorted(rng.choice(len(pts), m, replace=False).tolist())
+    v = F.rbf_masses(F.PointCloud(pts), anchors, sigma)
+    ref = orc.rbf_masses(pts, anchors, sigma)
+    assert np.allclose(v, ref, rtol=1e-8, atol=1e-14)
+
+
+def test_rbf_many_landmarks_singular(F):
+    """An ill-conditioned collocation (wide kernel over many close anchors)
+    raises SingularCollocation like the reference (cond > 1e12)."""
+    rng = np.random.default_rng(3)
+    pts = rng.uniform(-1, 1, size=(5000, 3))
+    with pytest.raises(F.SingularCollocation):
+        F.rbf_masses(F.PointCloud(pts), list(range(100)), 5.0)
