@@ -30,18 +30,6 @@ constexpr int kBT = FGA_KBT;  // threads per CTA
 constexpr int kBW = kBT / 32;
 static_assert(kBT % 32 == 0 && kBT >= 64, "whole warps, at least two");
 
-struct PairState {
-  double R[9], t[3], Racc[9], tacc[3], shift[3];
-  double ctx[10];
-  double gpe_initial, gpe_final;
-  long long iter, interactions, n_nodes;
-  int done, converged, status;
-  int n, m, pad;
-  double box[6];
-  double sum_mx, max_my;
-  float cmag;
-};
-
 // ---------------------------------------------------------------- block helpers
 __device__ __forceinline__ double block_sum(double v, double* red) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -271,7 +259,7 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
   double* mx = a.scratch.mx + slot * a.nmax;
   double* my = a.scratch.my + slot * a.mmax;
   int* flat = a.scratch.flat + slot * (size_t)max(a.nmax, a.mmax);
-  float4* ref32 = a.scratch.ref32 + slot * a.nmax;
+  float4* const ref32_slot = a.scratch.ref32 + slot * a.nmax;
   const size_t cap = a.node_cap;
   signed char* nlev = a.scratch.nlev + slot * cap;
   int* nstart = a.scratch.nstart + slot * cap;
@@ -281,11 +269,11 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
   double* nmass = a.scratch.nmass + slot * cap;
   double* nmc = a.scratch.nmc + slot * cap * 3;
   double* nlen = a.scratch.nlen + slot * cap;
-  float4* ra32 = a.scratch.ra32 + slot * cap;
+  float4* const ra32 = a.scratch.ra32 + slot * cap;
   NodeB32* rb32 = a.scratch.rb32 + slot * cap;
-  double4* ra64 = a.scratch.ra64 + slot * cap;
-  NodeB64* rb64 = a.scratch.rb64 + slot * cap;
-  double* tp = a.scratch.tpl + slot * a.mmax * 7;
+  double4* const ra64_slot = a.scratch.ra64 + slot * cap;
+  NodeB64* const rb64_slot = a.scratch.rb64 + slot * cap;
+  double* const tp_slot = a.scratch.tpl + slot * a.mmax * 7;
   const double dt = a.p.dt, eta = a.p.eta, G = a.p.G, eps = a.p.epsilon;
   const double theta2 = a.theta2, eps2 = a.eps2;
 
@@ -299,7 +287,17 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
     const int n = (int)(a.xoff[pi + 1] - x0), m = (int)(a.yoff[pi + 1] - y0);
     const double* X = a.x + x0 * 3;
     const double* Y = a.y + y0 * 3;
-    if (tid == 0) {
+    // wide modes keep the pair's records / template / reference copy in
+    // per-pair storage (they outlive this CTA's turn on the pair)
+    const bool wide = a.mode != 0;
+    float4* const ref32 = wide ? a.wide.ref32 + (size_t)pi * a.nmax : ref32_slot;
+    double* const tp = wide ? a.wide.tpl + (size_t)pi * a.mmax * 7 : tp_slot;
+    double4* const ra64 = wide ? a.wide.a64 + (size_t)pi * cap : ra64_slot;
+    NodeB64* const rb64 = wide ? a.wide.b64 + (size_t)pi * cap : rb64_slot;
+    float4* const c32 = wide ? a.wide.c32 + (size_t)pi * cap * 2 : nullptr;
+    if (a.mode == 2) {  // wide finish: the state the iterations left
+      if (tid == 0) st = a.wide.st[pi];
+    } else if (tid == 0) {
       st.status = 0;
       st.n = n;
       st.m = m;
@@ -314,6 +312,7 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
     }
     __syncthreads();
     if (st.status) goto finish;
+    if (a.mode != 2) {  // setup (modes 0, 1); the wide finish starts from the saved state
 
     // ---------------------------------------------------- normalize
     if (a.opt.normalize) {
@@ -562,6 +561,11 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
         rb64[mir] = NodeB64{leaf ? -INFINITY : l2, (long long)(mir + size)};
         ra32[mir] = make_float4((float)cx, (float)cy, (float)cz, (float)ms);
         rb32[mir] = NodeB32{leaf ? -INFINITY : (float)l2, mir + size};
+        if (wide) {
+          c32[2 * mir] = ra32[mir];
+          c32[2 * mir + 1] = make_float4(leaf ? -INFINITY : (float)l2, __int_as_float(mir + size),
+                                         leaf ? 0.f : (float)nlen[x], 0.f);
+        }
       }
       for (int i = tid; i < n; i += kBT)
         ref32[i] = make_float4((float)xn[i * 3], (float)xn[i * 3 + 1], (float)xn[i * 3 + 2],
@@ -651,6 +655,8 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
       __syncthreads();
     }
 
+    }  // setup
+
     {
       // energy of the current positions (_kernels.py:53-67), reused below
       auto energy = [&]() -> double {
@@ -691,13 +697,31 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
         return -G * block_sum(tot, S.red);
       };
 
-      if (a.opt.compute_gpe) {
+      if (a.mode != 2 && a.opt.compute_gpe) {
         const double e = energy();
         if (tid == 0) st.gpe_initial = e;
       }
       __syncthreads();
+      if (a.mode == 2) {  // wide finish: apply the last step transform (pending)
+        for (int i = tid; i < m; i += kBT) {
+          double* px = tp;
+          double* py = tp + a.mmax;
+          double* pz = tp + 2 * a.mmax;
+          const double y[3] = {px[i], py[i], pz[i]};
+          for (int r = 0; r < 3; r++) {
+            const double ny = st.R[3 * r] * y[0] + st.R[3 * r + 1] * y[1] + st.R[3 * r + 2] * y[2] + st.t[r];
+            (r == 0 ? px : r == 1 ? py : pz)[i] = ny;
+          }
+        }
+        __syncthreads();
+      }
+      if (a.mode == 1 && tid == 0) {  // the iterations run as wide launches: pending = identity
+        for (int k = 0; k < 9; k++) st.R[k] = (k % 4 == 0) ? 1.0 : 0.0;
+        for (int k = 0; k < 3; k++) st.t[k] = 0.0;
+      }
 
       // ---------------------------------------------------- iterations
+      if (a.mode == 0) {
       const float theta2f = a.theta2f, eps2f = a.eps2f;
       const int nchunks = (m + 31) / 32;
       double* px = tp;
@@ -844,7 +868,8 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
         __syncthreads();
         if (st.done) break;
       }
-      if (a.opt.compute_gpe) {
+      }
+      if (a.mode != 1 && a.opt.compute_gpe) {
         const double e = energy();
         if (tid == 0) st.gpe_final = e;
       }
@@ -853,6 +878,10 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
 
   finish:
     __syncthreads();
+    if (tid == 0 && a.mode == 1) {  // wide setup: the state the iterations start from
+      a.wide.st[pi] = st;
+      if (st.status == 0) a.wide.list[0][atomicAdd(&a.wide.counts[0], 1)] = pi;
+    }
     if (tid == 0) {
       fga_pair_result r{};
       r.status = st.status;
@@ -877,10 +906,186 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
           r.t[i] = ((v1 + inv * ((v2 + st.tacc[i]) - aa)) + c[i]) + l;
         }
       }
-      a.out[pi] = r;
+      a.out[pi] = r;  // (wide setup: provisional, the finish rewrites it)
     }
     __syncthreads();
   }
+}
+
+// ------------------------------------------------------------ wide iterations
+// One iteration of every active pair: a persistent grid of warps claims
+// (pair, 32-query chunk) items; each applies the pair's pending step
+// transform to its queries (registration.py:135-136), traverses the pair's
+// tree (traverse32d<kStatic>: static records, per-warp guard band), takes
+// the fused step and writes its chunk's moment sums.  k_wide_update then adds
+// each pair's chunk sums in chunk order (deterministic) and runs the rigid
+// update.  Pairs are independent, so results do not depend on the schedule.
+constexpr int kWT = 128;
+#ifndef FGA_WIDE_TPS
+#define FGA_WIDE_TPS 1792  // 1280: 505 ms, 1792: 470 ms for the iterations of the 4,096-pair batch
+#endif
+
+template <bool kGuardZero>
+__global__ void __launch_bounds__(kWT, FGA_WIDE_TPS / kWT) k_wide_forces(BatchArgs a, int cur) {
+  __shared__ double hs[3 * kWT];  // the lanes' fp64 fold sums
+  const int lane = threadIdx.x & 31;
+  const int n_active = a.wide.counts[cur];
+  const int chunks = a.wide.chunks;
+  const int items = n_active * chunks;
+  const int* list = a.wide.list[cur];
+  SimParams sp{};
+  sp.G = a.p.G;
+  sp.eta = a.p.eta;
+  sp.dt = a.p.dt;
+  while (true) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(&a.wide.counts[2], 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= items) break;
+    const int pi = list[item / chunks];
+    const int c = item % chunks;
+    const PairState* st = a.wide.st + pi;
+    const int m = st->m;
+    if (c * 32 >= m) continue;
+    const int i = c * 32 + lane;
+    const bool active = i < m;
+    double* px = a.wide.tpl + (size_t)pi * a.mmax * 7;
+    double* py = px + a.mmax;
+    double* pz = px + 2 * a.mmax;
+    double* vx = px + 3 * a.mmax;
+    double* vy = px + 4 * a.mmax;
+    double* vz = px + 5 * a.mmax;
+    const double* pm = px + 6 * a.mmax;
+    double y[3] = {0.0, 0.0, 0.0}, v[3] = {0.0, 0.0, 0.0};
+    if (active) {
+      const double y0[3] = {px[i], py[i], pz[i]}, v0[3] = {vx[i], vy[i], vz[i]};
+      for (int r = 0; r < 3; r++) {  // the pending step transform
+        y[r] = st->R[3 * r] * y0[0] + st->R[3 * r + 1] * y0[1] + st->R[3 * r + 2] * y0[2] + st->t[r];
+        v[r] = st->R[3 * r] * v0[0] + st->R[3 * r + 1] * v0[1] + st->R[3 * r + 2] * v0[2];
+      }
+      px[i] = y[0];
+      py[i] = y[1];
+      pz[i] = y[2];
+    }
+    const float qxf = (float)y[0], qyf = (float)y[1], qzf = (float)y[2];
+    float gA, gB;
+    guard_coeffs(fmaxf(fabsf(qxf), fmaxf(fabsf(qyf), fabsf(qzf))), st->cmag, a.theta2f, gA, gB);
+    const size_t cap = a.node_cap;
+    const Trav32Out o = traverse32d<kGuardZero, false, true>(
+        a.wide.c32 + (size_t)pi * cap * 2, a.wide.a64 + (size_t)pi * cap,
+        a.wide.b64 + (size_t)pi * cap, (int)st->n_nodes, qxf, qyf, qzf, active, a.theta2f,
+        a.theta2, a.eps2f, px, py, pz, m, hs, gA, gB, i);
+    Partial p;
+    partial_zero(p);
+    if (active) {
+      const double mq = pm[i];
+      const double gq = sp.G * mq;
+      const double F[3] = {gq * o.ax, gq * o.ay, gq * o.az};
+      double vp[3];
+      const double shift[3] = {st->shift[0], st->shift[1], st->shift[2]};
+      step_and_accumulate(F, y, v, mq, sp, shift, vp, p);
+      vx[i] = vp[0];
+      vy[i] = vp[1];
+      vz[i] = vp[2];
+    }
+    const unsigned acc_w = __reduce_add_sync(0xffffffffu, (unsigned)o.accepted);
+    p.v[kAccepted] = lane == 0 ? (double)acc_w : 0.0;
+    double* cp = a.wide.cpart + ((size_t)pi * chunks + c) * kPartialStride;
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      const double sv = warp_sum(p.v[k]);
+      if (lane == k) cp[k] = sv;
+    }
+  }
+}
+
+// The rigid update of every active pair (one warp per pair): chunk sums in
+// chunk order, then the update of registration.py:131-154 by lane 0.
+__global__ void __launch_bounds__(kWT) k_wide_update(BatchArgs a, int cur, int it) {
+  const int lane = threadIdx.x & 31;
+  const int wa = (int)((blockIdx.x * (int64_t)kWT + threadIdx.x) >> 5);
+  if (wa >= a.wide.counts[cur]) return;
+  const int pi = a.wide.list[cur][wa];
+  PairState& st = a.wide.st[pi];
+  const int m = st.m, nchunks = (m + 31) / 32;
+  const double* cp = a.wide.cpart + (size_t)pi * a.wide.chunks * kPartialStride;
+  double v = 0.0;
+  if (lane < 16)
+    for (int c = 0; c < nchunks; c++) v += cp[(size_t)c * kPartialStride + lane];
+  double sums[16];
+#pragma unroll
+  for (int k = 0; k < 16; k++) sums[k] = __shfl_sync(0xffffffffu, v, k);
+  if (lane != 0) return;
+  const double M = (double)m;
+  double mu_u[3], mu_w[3], C[9], R[9], t[3];
+  for (int k = 0; k < 3; k++) {
+    mu_u[k] = sums[kSumU + k] / M;
+    mu_w[k] = sums[kSumW + k] / M;
+  }
+  for (int r = 0; r < 3; r++)
+    for (int cc = 0; cc < 3; cc++) C[3 * r + cc] = sums[kSumWU + 3 * r + cc] - M * mu_w[r] * mu_u[cc];
+  kabsch_rotation(C, R, nullptr);
+  double mu_y[3], mu_d[3];
+  for (int k = 0; k < 3; k++) {
+    mu_y[k] = mu_u[k] + st.shift[k];
+    mu_d[k] = mu_w[k] + st.shift[k];
+  }
+  for (int k = 0; k < 3; k++)
+    t[k] = mu_d[k] - (R[3 * k] * mu_y[0] + R[3 * k + 1] * mu_y[1] + R[3 * k + 2] * mu_y[2]);
+  double Ra[9], ta[3], delta = 0.0;
+  for (int r = 0; r < 3; r++) {
+    for (int cc = 0; cc < 3; cc++)
+      Ra[3 * r + cc] = R[3 * r] * st.Racc[cc] + R[3 * r + 1] * st.Racc[3 + cc] +
+                       R[3 * r + 2] * st.Racc[6 + cc];
+    ta[r] = t[r] + (R[3 * r] * st.tacc[0] + R[3 * r + 1] * st.tacc[1] + R[3 * r + 2] * st.tacc[2]);
+  }
+  for (int r = 0; r < 3; r++) {
+    for (int cc = 0; cc < 3; cc++) {
+      const double e = Ra[3 * r + cc] - st.Racc[3 * r + cc];
+      delta += e * e;
+    }
+    const double e = ta[r] - st.tacc[r];
+    delta += e * e;
+  }
+  for (int k = 0; k < 9; k++) {
+    st.R[k] = R[k];
+    st.Racc[k] = Ra[k];
+  }
+  for (int k = 0; k < 3; k++) {
+    st.t[k] = t[k];
+    st.tacc[k] = ta[k];
+    st.shift[k] = mu_d[k];
+  }
+  st.interactions += (long long)sums[kAccepted];
+  if (a.deltas) a.deltas[(size_t)pi * a.p.max_iters + it] = delta;
+  st.iter = it + 1;
+  if (delta < a.p.conv_tol) {
+    st.converged = 1;
+    st.done = 1;
+  } else if (it + 1 >= a.p.max_iters) {
+    st.done = 1;
+  }
+  if (!st.done) a.wide.list[1 - cur][atomicAdd(&a.wide.counts[1 - cur], 1)] = pi;
+}
+
+int launch_wide_iteration(const BatchArgs& a, int cur, int it, cudaStream_t s) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // next list empty, chunk counter zero
+  FGA_CUDA_TRY(cudaMemsetAsync(a.wide.counts + (1 - cur), 0, sizeof(int), s));
+  FGA_CUDA_TRY(cudaMemsetAsync(a.wide.counts + 2, 0, sizeof(int), s));
+  const int grid = sms * (FGA_WIDE_TPS / kWT);
+  if (a.eps2f > 0.f)
+    k_wide_forces<false><<<grid, kWT, 0, s>>>(a, cur);
+  else
+    k_wide_forces<true><<<grid, kWT, 0, s>>>(a, cur);
+  k_wide_update<<<(a.n_pairs + kWT / 32 - 1) / (kWT / 32), kWT, 0, s>>>(a, cur, it);
+  FGA_CUDA_TRY(cudaGetLastError());
+  return FGA_OK;
 }
 
 size_t batch_smem_bytes(int P, int nmax, int ncell) {

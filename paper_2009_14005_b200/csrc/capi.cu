@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -73,7 +74,7 @@ struct Session {
 
 struct fga_ctx {
   int device = 0;
-  DevBuf batch_in[6], batch_scratch, batch_out, batch_deltas, batch_counter;
+  DevBuf batch_in[6], batch_scratch, batch_out, batch_deltas, batch_counter, batch_wide;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   TreeDev tree;
@@ -600,6 +601,7 @@ int fga_destroy(fga_ctx* c) {
   c->batch_out.release();
   c->batch_deltas.release();
   c->batch_counter.release();
+  c->batch_wide.release();
   Session& S = c->S;
   S.lm_idx.release();
   S.rbf_scratch.release();
@@ -1112,7 +1114,79 @@ int fga_register_batch_dev(fga_ctx* c, const double* x_all, const int64_t* x_off
   a.counter = c->batch_counter.as<int>();
   a.out = out_dev;
   a.deltas = deltas_dev;
-  return launch_register_batch(a, grid, smem, c->stream);
+  a.mode = 0;
+  cudaStream_t s = c->stream;
+  // Wide mode (enough pairs to fill the GPU): setup per pair in the
+  // persistent kernel, then one wide launch per iteration over all active
+  // pairs' query chunks, then the finish (fga_batched.cuh BatchWide).
+  static const int wide_env = [] {
+    const char* e = getenv("FGA_BATCH_WIDE");
+    return e ? atoi(e) : -1;
+  }();
+  const bool use_wide = wide_env >= 0 ? wide_env != 0 : n_pairs >= sms;
+  if (!use_wide) return launch_register_batch(a, grid, smem, s);
+  (void)0;
+  const int chunks = (mmax + 31) / 32;
+  const size_t P64 = (size_t)n_pairs;
+  const size_t wide_bytes =
+      P64 * (cap * (2 * sizeof(float4) + sizeof(double4) + sizeof(NodeB64)) +
+             sizeof(double) * (size_t)mmax * 7 + sizeof(float4) * (size_t)nmax +
+             sizeof(PairState) + sizeof(double) * kPartialStride * chunks + 2 * sizeof(int)) +
+      16 * 256 + 64;
+  FGA_CUDA_TRY(c->batch_wide.reserve(wide_bytes));
+  q = c->batch_wide.as<char>();
+  a.wide.c32 = (float4*)take(2 * sizeof(float4) * cap * P64);
+  a.wide.a64 = (double4*)take(sizeof(double4) * cap * P64);
+  a.wide.b64 = (NodeB64*)take(sizeof(NodeB64) * cap * P64);
+  a.wide.tpl = (double*)take(sizeof(double) * (size_t)mmax * 7 * P64);
+  a.wide.ref32 = (float4*)take(sizeof(float4) * (size_t)nmax * P64);
+  a.wide.st = (PairState*)take(sizeof(PairState) * P64);
+  a.wide.cpart = (double*)take(sizeof(double) * kPartialStride * chunks * P64);
+  a.wide.list[0] = (int*)take(sizeof(int) * P64);
+  a.wide.list[1] = (int*)take(sizeof(int) * P64);
+  a.wide.counts = (int*)take(sizeof(int) * 4);
+  a.wide.chunks = chunks;
+  if ((size_t)(q - c->batch_wide.as<char>()) > c->batch_wide.bytes) {
+    set_error("internal: batched wide sizing");
+    return FGA_ERR_NOMEM;
+  }
+  FGA_CUDA_TRY(cudaMemsetAsync(a.wide.counts, 0, sizeof(int) * 4, s));
+  static const bool phase_times = getenv("FGA_BATCH_PHASES") != nullptr;
+  cudaEvent_t pe[4];
+  if (phase_times)
+    for (auto& e : pe) cudaEventCreate(&e);
+  if (phase_times) cudaEventRecord(pe[0], s);
+  a.mode = 1;
+  TRY(launch_register_batch(a, grid, smem, s));
+  if (phase_times) cudaEventRecord(pe[1], s);
+  int cur = 0;
+  for (int it = 0; it < params->max_iters; it++) {
+    TRY(launch_wide_iteration(a, cur, it, s));
+    cur = 1 - cur;
+    if ((it & 3) == 3 || it + 1 == params->max_iters) {  // stop once every pair is done
+      int active = 0;
+      FGA_CUDA_TRY(cudaMemcpyAsync(&active, a.wide.counts + cur, sizeof(int),
+                                   cudaMemcpyDeviceToHost, s));
+      FGA_CUDA_TRY(cudaStreamSynchronize(s));
+      if (active == 0) break;
+    }
+  }
+  FGA_CUDA_TRY(cudaMemsetAsync(c->batch_counter.p, 0, sizeof(int), s));
+  if (phase_times) cudaEventRecord(pe[2], s);
+  a.mode = 2;
+  TRY(launch_register_batch(a, grid, smem, s));
+  if (phase_times) {  // (design tool: FGA_BATCH_PHASES=1)
+    cudaEventRecord(pe[3], s);
+    cudaEventSynchronize(pe[3]);
+    float t1 = 0, t2 = 0, t3 = 0;
+    cudaEventElapsedTime(&t1, pe[0], pe[1]);
+    cudaEventElapsedTime(&t2, pe[1], pe[2]);
+    cudaEventElapsedTime(&t3, pe[2], pe[3]);
+    fprintf(stderr, "batch wide phases: setup %.2f ms, iterations %.2f ms, finish %.2f ms\n", t1,
+            t2, t3);
+    for (auto& e : pe) cudaEventDestroy(e);
+  }
+  return FGA_OK;
 }
 
 int fga_register_batch(fga_ctx* c, const double* x_all, const int64_t* x_offsets,

@@ -271,7 +271,11 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
 // accept iff diff > 0, and re-decide in fp64 iff |diff| <= band (14.1 ->
 // 13.5 ms).  Visits are counted only when asked (kCountVisits; 2.5% of the
 // step).
-template <bool kGuardZero, bool kCountVisits>
+// kStatic (the wide batched kernels, batched.cu): the records are static,
+// {l^2 | -inf, skip, length, 0}, and the band is formed per step from the
+// warp's coefficients gA / gB (guard_coeffs) -- no per-launch band pass;
+// qidx >= 0 gives the re-check's query index explicitly.
+template <bool kGuardZero, bool kCountVisits, bool kStatic = false>
 __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
                                                  const double4* __restrict__ A64,
                                                  const NodeB64* __restrict__ B64, int n_nodes,
@@ -279,7 +283,8 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
                                                  float theta2, double theta2_64, float eps2,
                                                  const double* qpx, const double* qpy,
                                                  const double* qpz, int64_t m_queries,
-                                                 double* hs = nullptr) {
+                                                 double* hs = nullptr, float gA = 0.f,
+                                                 float gB = 0.f, int64_t qidx = -1) {
   // hs (optional): the block's fp64 fold sums in shared memory, 3 per thread
   // (hs[3 threadIdx.x ..]), so they hold no registers across the loop (folds
   // are rare; the address is re-derived at each fold)
@@ -291,6 +296,10 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
   }
   int visits = 0, accepted = 0;
   int cursor = active ? 0 : n_nodes;
+  if constexpr (kStatic) {  // one band per warp: the largest lane delta
+    gA = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gA)));
+    gB = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gB)));
+  }
   int lim = fold_limit(0, n_nodes);
   while (true) {
     const int n = __reduce_min_sync(0xffffffffu, cursor);
@@ -315,15 +324,24 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     const float4 b = __ldg(&rec->b);
     const bool mine = cursor == n;
     const float dx = a.x - qx, dy = a.y - qy, dz = a.z - qz;
-    const float r2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, eps2)));  // d^2 + eps^2
-    const float diff = fmaf(theta2, r2, -b.x);
+    float r2, diff, band;
+    if constexpr (kStatic) {
+      const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      diff = fmaf(theta2, d2, -b.x);
+      band = fmaf(gA, b.z, fmaf(13.0f * 5.97e-8f, b.x, gB));
+      r2 = d2 + eps2;
+    } else {
+      r2 = fmaf(dx, dx, fmaf(dy, dy, fmaf(dz, dz, eps2)));  // d^2 + eps^2
+      diff = fmaf(theta2, r2, -b.x);
+      band = b.z;
+    }
     bool acc = diff > 0.f;
-    const bool near = mine && fabsf(diff) <= b.z;
+    const bool near = mine && fabsf(diff) <= band;
     if (__any_sync(0xffffffffu, near)) {  // warp-uniform branch, rarely taken
       // this lane's query, re-derived here (query i = global thread index;
       // inactive lanes read the last query and ignore the result) so no
       // register holds it across the loop
-      int64_t qs = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+      int64_t qs = qidx >= 0 ? qidx : blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
       qs = qs < m_queries ? qs : m_queries - 1;
       const bool e = mac_exact(A64, B64, n, qpx[qs], qpy[qs], qpz[qs], theta2_64);
       acc = near ? e : acc;

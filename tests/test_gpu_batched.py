@@ -59,3 +59,33 @@ def test_batch_reports_per_pair_failures():
     assert br.results[0] is not None and br.results[2] is not None
     single = fga.register(*pairs[1])
     assert br.results[2].iterations == single.iterations
+
+
+def test_wide_batch_matches_single_pair_path(orc):
+    """>= one pair per SM selects the wide mode (per-pair setup / finish in
+    the persistent kernel, one wide launch per iteration over all active
+    pairs' chunks).  Every pair equals register() of that pair, a sample
+    equals the oracle, and a rerun is bitwise identical."""
+    import paper_2009_14005_b200 as fga
+    from paper_2009_14005_b200 import synth
+    P = 160  # > 148 SMs
+    pairs = [synth.fragment_pair(p, n=1000 + 37 * (p % 7)) for p in range(P)]
+    pairs[5] = (fga.PointCloud(np.ones((10, 3))), fga.PointCloud(np.ones((10, 3))))
+    p = fga.default_params()
+    br = fga.register_batch(pairs, params=p)
+    assert isinstance(br.errors[5], fga.DegenerateExtent) and br.results[5] is None
+    again = fga.register_batch(pairs, params=p)
+    for k in range(0, P, 9):
+        if k == 5:
+            continue
+        r = br.results[k]
+        s = fga.register(*pairs[k], params=p)
+        assert r.iterations == s.iterations and r.converged == s.converged
+        if s.converged:  # (a non-converging run amplifies summation-order differences)
+            assert np.abs(r.transform.rotation - s.transform.rotation).max() < 1e-7
+        assert np.array_equal(again.results[k].transform.rotation, r.transform.rotation)
+    for k in (0, 17, 33):
+        x, y = pairs[k]
+        o = orc.register(x.points, y.points, theta=p.theta)
+        assert br.results[k].iterations == o.iterations
+        assert np.abs(br.results[k].transform.rotation - o.R_orig).max() < 1e-4
