@@ -956,9 +956,10 @@ __global__ void __launch_bounds__(kWT, FGA_WIDE_TPS / kWT) k_wide_forces(BatchAr
     double* vy = px + 4 * a.mmax;
     double* vz = px + 5 * a.mmax;
     const double* pm = px + 6 * a.mmax;
-    double y[3] = {0.0, 0.0, 0.0}, v[3] = {0.0, 0.0, 0.0};
+    float qxf = 0.f, qyf = 0.f, qzf = 0.f;
     if (active) {
       const double y0[3] = {px[i], py[i], pz[i]}, v0[3] = {vx[i], vy[i], vz[i]};
+      double y[3], v[3];
       for (int r = 0; r < 3; r++) {  // the pending step transform
         y[r] = st->R[3 * r] * y0[0] + st->R[3 * r + 1] * y0[1] + st->R[3 * r + 2] * y0[2] + st->t[r];
         v[r] = st->R[3 * r] * v0[0] + st->R[3 * r + 1] * v0[1] + st->R[3 * r + 2] * v0[2];
@@ -966,8 +967,17 @@ __global__ void __launch_bounds__(kWT, FGA_WIDE_TPS / kWT) k_wide_forces(BatchAr
       px[i] = y[0];
       py[i] = y[1];
       pz[i] = y[2];
+      vx[i] = v[0];
+      vy[i] = v[1];
+      vz[i] = v[2];
+      qxf = (float)y[0];
+      qyf = (float)y[1];
+      qzf = (float)y[2];
     }
-    const float qxf = (float)y[0], qyf = (float)y[1], qzf = (float)y[2];
+    // the fp32 query lives in registers across the traversal (the fp64 state
+    // is re-read afterwards, L1/L2-resident): otherwise the compiler keeps
+    // the doubles and re-converts them (F2F) inside the loop
+    asm volatile("" : "+f"(qxf), "+f"(qyf), "+f"(qzf));
     float gA, gB;
     guard_coeffs(fmaxf(fabsf(qxf), fmaxf(fabsf(qyf), fabsf(qzf))), st->cmag, a.theta2f, gA, gB);
     const size_t cap = a.node_cap;
@@ -978,6 +988,7 @@ __global__ void __launch_bounds__(kWT, FGA_WIDE_TPS / kWT) k_wide_forces(BatchAr
     Partial p;
     partial_zero(p);
     if (active) {
+      const double y[3] = {px[i], py[i], pz[i]}, v[3] = {vx[i], vy[i], vz[i]};
       const double mq = pm[i];
       const double gq = sp.G * mq;
       const double F[3] = {gq * o.ax, gq * o.ay, gq * o.az};
