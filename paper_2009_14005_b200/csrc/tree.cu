@@ -15,23 +15,25 @@
 //   preorder(i, l) = excl_scan(count)_i + (l - s_i)
 // which is exactly the reference's preorder: (start, level) lexicographic.
 // Children of a node in ascending preorder are x+1, skip[x+1], ... < skip[x]
-// in slot order, so no child table is kept.  Node aggregates are reduced
-// level by level from the depth cap up (children in slot order:
-// deterministic), and each node's traversal records are written in the same
-// pass, in *mirrored* preorder (see fga_internal.cuh).
+// in slot order, so no child table is kept.  Node aggregates are exact
+// fixed-point sums over each node's point range (differences of prefix sums,
+// see "aggregates" below), so they are independent of how the work is split;
+// each node's traversal records are written in *mirrored* preorder (see
+// fga_internal.cuh).
 //
 // Kernels (all HBM/L2-bound integer + fp64 work; no tensor cores):
-//   k_bbox_*        root bbox = per-axis min/max (bhtree.py:107-108)
+//   k_bbox_*        root bbox = per-axis min/max (bhtree.py:107-108), max |m|
 //   k_keys          per-axis fp64 split recursion -> 3L-bit key (dyadic fast
 //                   path with an exact-replay fallback near split planes)
 //   (cub radix sort, stable: keeps the reference's within-leaf index order)
 //   k_gather_sorted sorted points + full keys; k_fixup_runs low key bits
 //   k_count         c_i and per-point node counts
 //   (cub exclusive scan) -> preorder offsets, node count
-//   k_subtrees      per block of 512 sorted points: the chains top-down
-//                   (bbox replay -> length, skip = offset[end]) and the
-//                   aggregates bottom-up in shared memory; mirrored records
-//   k_crossing      nodes that cross block boundaries: partials combined
+//   k_subtrees      per block of kST sorted points: exact prefix sums, then
+//                   one node per thread (bbox replay -> length, end -> skip
+//                   and sums) -> records
+//   k_tscan1/2      prefix sums of the block totals
+//   k_crossing      nodes that run past their block: sums from the prefixes
 #include <cub/cub.cuh>
 
 #include <cstring>
@@ -58,8 +60,10 @@ inline int blocks_for(int64_t n, int t = kThreads) {
 }
 
 // ---------------------------------------------------------------- bbox
-__global__ void k_bbox_partial(const double* __restrict__ pts, int64_t n, double* __restrict__ part) {
+__global__ void k_bbox_partial(const double* __restrict__ pts, const double* __restrict__ masses,
+                               int64_t n, double* __restrict__ part) {
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  double mm = 0.0;  // max |mass| (the fixed-point scale of the node sums)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
@@ -68,8 +72,9 @@ __global__ void k_bbox_partial(const double* __restrict__ pts, int64_t n, double
       lo[k] = fmin(lo[k], v);
       hi[k] = fmax(hi[k], v);
     }
+    mm = fmax(mm, fabs(masses[i]));
   }
-  __shared__ double s[6][kThreads / 32];
+  __shared__ double s[7][kThreads / 32];
 #pragma unroll
   for (int k = 0; k < 3; k++) {
     for (int o = 16; o > 0; o >>= 1) {
@@ -77,31 +82,38 @@ __global__ void k_bbox_partial(const double* __restrict__ pts, int64_t n, double
       hi[k] = fmax(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
     }
   }
+  for (int o = 16; o > 0; o >>= 1) mm = fmax(mm, __shfl_xor_sync(0xffffffffu, mm, o));
   int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0)
+  if (l == 0) {
     for (int k = 0; k < 3; k++) {
       s[k][w] = lo[k];
       s[3 + k][w] = hi[k];
     }
+    s[6][w] = mm;
+  }
   __syncthreads();
-  if (threadIdx.x < 6) {
+  if (threadIdx.x < 7) {
     double r = s[threadIdx.x][0];
     for (int j = 1; j < (int)(blockDim.x >> 5); j++)
       r = threadIdx.x < 3 ? fmin(r, s[threadIdx.x][j]) : fmax(r, s[threadIdx.x][j]);
-    part[blockIdx.x * 6 + threadIdx.x] = r;
+    part[blockIdx.x * 7 + threadIdx.x] = r;
   }
 }
 
+__device__ __forceinline__ void fixed_scale(const double* box, int64_t n, double* out);
+
 // box[0..5] = lo, hi; box[6..8] = 2^L / (hi - lo) per axis; box[9] = the
-// fast-key guard (see k_keys)
-__global__ void k_bbox_final(const double* __restrict__ part, int nparts, int L,
+// fast-key guard (see k_keys); box[10] = max |mass|, box[11..13] the
+// fixed-point scale of the node sums (see fixed_scale)
+__global__ void k_bbox_final(const double* __restrict__ part, int nparts, int L, int64_t n,
                              double* __restrict__ out) {
-  for (int k = 0; k < 6; k++) {
-    double v = k < 3 ? INFINITY : -INFINITY;
+  for (int k = 0; k < 7; k++) {
+    double v = k < 3 ? INFINITY : (k < 6 ? -INFINITY : 0.0);
     for (int j = threadIdx.x; j < nparts; j += blockDim.x)
-      v = k < 3 ? fmin(v, part[j * 6 + k]) : fmax(v, part[j * 6 + k]);
+      v = k < 3 ? fmin(v, part[j * 7 + k]) : fmax(v, part[j * 7 + k]);
     v = k < 3 ? block_reduce<1>(v) : block_reduce<2>(v);
-    if (threadIdx.x == 0) out[k] = v;
+    if (threadIdx.x == 0) out[k < 6 ? k : 10] = v;
+    __syncthreads();
   }
   if (threadIdx.x == 0) {
     double R = 0.0;
@@ -111,6 +123,7 @@ __global__ void k_bbox_final(const double* __restrict__ part, int nparts, int L,
       R = fmax(R, fmax(fabs(out[k]), fabs(out[3 + k])));
     }
     out[9] = 256.0 * 1.1102230246251565e-16 * R;  // 256 u R
+    fixed_scale(out, n, out);
   }
 }
 
@@ -321,82 +334,142 @@ __device__ __forceinline__ double diag_len(const double lo[3], const double hi[3
   return __dsqrt_rn(sq);  // np.linalg.norm (bhtree.py:83)
 }
 
-// numpy's pairwise 1-D sum (loops_utils.h.src) of the masses of sorted
-// points [lo, lo + cnt); leaves hold one point except at the depth cap,
-// where this makes the leaf mass bit-exact.
-__device__ double pairwise_mass(const double4* __restrict__ sp, int64_t lo, int64_t cnt) {
-  if (cnt < 8) {
-    double r = 0.0;
-    for (int64_t i = 0; i < cnt; i++) r = __dadd_rn(r, sp[lo + i].w);
-    return r;
-  } else if (cnt <= 128) {
-    double r[8];
-    int64_t i;
-    for (int j = 0; j < 8; j++) r[j] = sp[lo + j].w;
-    for (i = 8; i < cnt - (cnt % 8); i += 8)
-      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], sp[lo + i + j].w);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < cnt; i++) res = __dadd_rn(res, sp[lo + i].w);
-    return res;
+// ---------------------------------------------------------------- aggregates
+// A node's mass and m*p sums (bhtree.py:78-82) are sums over its points; the
+// reference adds them in its own order (numpy's pairwise sum for the mass,
+// row by row for m*p), so no fp64 grouping a parallel build can use gives its
+// last bits.  Here every point's terms (m, m x, m y, m z) -- the products
+// rounded to fp64 as the reference rounds them -- become 128-bit fixed-point
+// integers under one scale 2^S for the whole build, S chosen from the largest
+// possible |term| and n so that no partial sum can overflow and every term
+// above 2^-S is exact.  A node's sums are then differences of prefix sums:
+// exact integers, independent of how the work is split over blocks, threads
+// or crossing partials, and converted to fp64 once (com = one division of the
+// two rounded sums, as the reference's `sum / total`).  The tests hold the
+// aggregates to 1e-12 of the reference's (the topology, lengths and skips
+// are bit-exact).
+typedef unsigned __int128 u128;
+struct __align__(16) Q4 {
+  u128 v[4];
+};
+
+// The scale (k_bbox_final): sums of up to n terms each below max|m| *
+// max(1, max|coord|) stay below 2^122; S <= 1074 (every double is then a
+// multiple of 2^-S: all terms exact), S >= -1000.  box[11] = S, box[12] =
+// 2^(S-64), box[13] = 2^-S.
+__device__ __forceinline__ void fixed_scale(const double* box, int64_t n, double* out) {
+  double R = 1.0;
+#pragma unroll
+  for (int k = 0; k < 6; k++) R = fmax(R, fabs(box[k]));
+  const double bound = box[10] * R * (double)n;
+  int S = 0;
+  if (bound > 0.0 && bound < 1e300) {
+    int e;
+    frexp(bound, &e);  // bound < 2^e
+    S = min(122 - e, 1074);
+  } else if (bound > 0.0) {
+    S = -1000;
   }
-  int64_t n2 = cnt / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(pairwise_mass(sp, lo, n2), pairwise_mass(sp, lo + n2, cnt - n2));
+  out[11] = (double)S;
+  out[12] = ldexp(1.0, S - 64);
+  out[13] = ldexp(1.0, -S);
 }
 
-// Leaf aggregate (bhtree.py:78-82): pairwise mass, sequential sum of m*p, as
-// {m, m x, m y, m z}.
-__device__ __forceinline__ double4 leaf_sums(const double4* __restrict__ sp, int64_t start,
-                                             int64_t occ) {
-  double4 r;
-  r.x = occ == 1 ? sp[start].w : pairwise_mass(sp, start, occ);
-  r.y = r.z = r.w = 0.0;
-  for (int64_t q = 0; q < occ; q++) {
-    const double4 v = sp[start + q];
-    r.y = __dadd_rn(r.y, __dmul_rn(v.x, v.w));
-    r.z = __dadd_rn(r.z, __dmul_rn(v.y, v.w));
-    r.w = __dadd_rn(r.w, __dmul_rn(v.z, v.w));
+// round(v * 2^S) as a two's-complement 128-bit integer (s64 = 2^(S-64)):
+// |v| 2^(S-64) = h + r, h = floor (< 2^58), r in [0, 1) exact, low word =
+// r 2^64 rounded to nearest
+__device__ __forceinline__ u128 to_fixed(double v, double s64) {
+  const double a = fabs(v) * s64;
+  const double h = floor(a);
+  const unsigned long long lo = __double2ull_rn((a - h) * 18446744073709551616.0);
+  const u128 q = ((u128)__double2ull_rn(h) << 64) | lo;
+  return v < 0.0 ? (u128)0 - q : q;
+}
+
+// the two's-complement integer as fp64 (hi * 2^64 + lo, one fused rounding
+// after the exact conversion of hi: within one unit of the last place, and a
+// fixed function of the integer)
+__device__ __forceinline__ double fixed_to_double(u128 u) {
+  const long long hi = (long long)(unsigned long long)(u >> 64);
+  return __fma_rn(__ll2double_rn(hi), 18446744073709551616.0,
+                  __ull2double_rn((unsigned long long)u));
+}
+
+__device__ __forceinline__ void point_terms(const double4& p, double s64, u128 q[4]) {
+  q[0] = to_fixed(p.w, s64);
+  q[1] = to_fixed(__dmul_rn(p.x, p.w), s64);
+  q[2] = to_fixed(__dmul_rn(p.y, p.w), s64);
+  q[3] = to_fixed(__dmul_rn(p.z, p.w), s64);
+}
+
+__device__ __forceinline__ u128 shfl_up128(u128 v, int d) {
+  const unsigned long long lo = __shfl_up_sync(0xffffffffu, (unsigned long long)v, d);
+  const unsigned long long hi = __shfl_up_sync(0xffffffffu, (unsigned long long)(v >> 64), d);
+  return ((u128)hi << 64) | lo;
+}
+
+// inclusive block scan of q over the block's threads (wt: one Q4 per warp,
+// shared; one barrier inside)
+__device__ __forceinline__ void block_scan_q4(u128 q[4], Q4* wt) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      const u128 y = shfl_up128(q[c], d);
+      if (lane >= d) q[c] += y;
+    }
   }
-  return r;
+  if (lane == 31)
+#pragma unroll
+    for (int c = 0; c < 4; c++) wt[w].v[c] = q[c];
+  __syncthreads();
+  for (int ww = 0; ww < w; ww++)
+#pragma unroll
+    for (int c = 0; c < 4; c++) q[c] += wt[ww].v[c];
 }
 
-__device__ __forceinline__ void add4(double4& a, const double4& b) {
-  a.x = __dadd_rn(a.x, b.x);
-  a.y = __dadd_rn(a.y, b.y);
-  a.z = __dadd_rn(a.z, b.z);
-  a.w = __dadd_rn(a.w, b.w);
-}
-
-// The node's traversal records at its mirrored-preorder index, in two halves:
-// the structural one ({l^2, skip}, known top-down) and the aggregate one
-// ({com, mass}, known bottom-up).
-__device__ __forceinline__ void write_records_b(const TreeRecords& r, int mir, int rskip, bool leaf,
-                                                double len) {
+// The node's traversal records at its mirrored-preorder index: fp64 {com,
+// mass} and {l^2 | -inf, skip}, and the packed FP32 record (NodeC32).
+__device__ __forceinline__ void write_node(const TreeRecords& r, int mir, int rskip, bool leaf,
+                                           double len, double cx, double cy, double cz,
+                                           double m) {
   const double l2 = __dmul_rn(len, len);
+  r.a64[mir] = make_double4(cx, cy, cz, m);
   r.b64[mir] = NodeB64{leaf ? -INFINITY : l2, (long long)rskip};
   const float l2f = leaf ? -INFINITY : (float)l2;
+  r.c32[2 * mir] = make_float4((float)cx, (float)cy, (float)cz, (float)m);
   r.c32[2 * mir + 1] = make_float4(l2f, __int_as_float(rskip), 0.f, l2f);
 }
-__device__ __forceinline__ void write_records_a(const TreeRecords& r, int mir, const double4& v) {
-  const double cx = __ddiv_rn(v.y, v.x), cy = __ddiv_rn(v.z, v.x), cz = __ddiv_rn(v.w, v.x);
-  r.a64[mir] = make_double4(cx, cy, cz, v.x);
-  r.c32[2 * mir] = make_float4((float)cx, (float)cy, (float)cz, (float)v.x);
+
+// records of a node whose exact sums are a[0..3] (scaled by 2^S)
+__device__ __forceinline__ void write_node_sums(const TreeRecords& r, int mir, int rskip,
+                                                double len, const u128 a[4], double sinv) {
+#ifdef FGA_XP_NOSUM
+  write_node(r, mir, rskip, false, len, (double)(unsigned long long)a[1], 0.0, 0.0, sinv);
+  return;
+#endif
+  const double am = fixed_to_double(a[0]);
+  write_node(r, mir, rskip, false, len, __ddiv_rn(fixed_to_double(a[1]), am),
+             __ddiv_rn(fixed_to_double(a[2]), am), __ddiv_rn(fixed_to_double(a[3]), am),
+             am * sinv);
 }
 
 // ---------------------------------------------------------------- hierarchy
 // Node (i, l) holds the sorted points [i, end), end = first j > i with
 // c_j < l, and its preorder subtree is the chain rest of i plus every chain
 // of the points in (i, end); so its preorder skip is offset[end] and its
-// mirrored index is l + n_nodes - offset[end] -- no bottom-up size pass.
+// mirrored index is l + n_nodes - offset[end] -- no bottom-up pass at all:
+// with the exact prefix sums a node's aggregate is E[end] - E[i].
 //
-// The aggregates (mass, m*p) are reduced bottom-up inside blocks of kST
-// consecutive sorted points (k_subtrees): a node is summed over its children
-// in slot order, starting from 0.0.  A node that crosses block boundaries gets
-// one partial per block it touches (the same fold over its children inside
-// that block, a crossing child contributing its own partial); k_crossing adds
-// them in a fixed dyadic shape.  Every result is a fixed function of the input
-// (kST is a constant), whatever the scheduling.
+// Blocks of kST consecutive sorted points (k_subtrees) hold their own
+// exclusive prefix sums E_b; a node that runs past its block's end (at most
+// one per level per block) is finished by k_crossing from
+//   G(b) = sum of the totals of blocks < b   (k_tscan1/2)
+//   pst  = E_b(i) of its start                (k_subtrees, owner block)
+//   plE  = E_b'(end) inside the end block b'  (k_subtrees of b': the level-l
+//          node covering b's first point ends there)
+// as G(b') + plE - G(b) - pst.
 #ifndef FGA_KST
 #define FGA_KST 128
 #endif
@@ -405,32 +478,19 @@ constexpr int kSW = kST / 32;
 #ifndef FGA_STB
 #define FGA_STB (1536 / kST)
 #endif
-constexpr int kSTBlocks = FGA_STB;  // resident blocks per SM (40 registers at 128 threads; 12 measured 2% faster than 10 and 8% than 8)
+constexpr int kSTBlocks = FGA_STB;  // resident blocks per SM
+constexpr int kTScan = 256;         // blocks per chunk of the block-total scan
 
-// Per (level, block) boundary partials, SoA by level (index l * nb + b):
-//   pr/prx/prlen: the node owned by block b (starting in it) that runs past
-//                 its end, if any (prx = preorder index, -1 = none)
-//   pl/plend:     the node that starts before block b and covers its first
-//                 point, and where it ends inside b (-1 = past the block)
-//   mn[b]:        min c_j over the block's points 1..kST (the next block's
-//                 first point included): a level-l node covering the block's
-//                 first point ends inside it iff mn[b] < l
-// plus the dyadic sums / minima over aligned runs of 2^k blocks (k >= 1):
-//   hs[l * hn + ho[k] + j] = hs_{k-1}[2j] + hs_{k-1}[2j+1] (hs_0 = pl),
-//   hm[ho[k] + j] = min of the same runs of mn.
-constexpr int kMaxHier = 32;
 struct Cross {
-  double4* pr;
-  double4* pl;
-  double* prlen;
-  int* prx;
-  int* plend;
-  int* mn;
-  double4* hs;
-  int* hm;
-  int hn;  // entries per level in hs (sum of the dyadic level sizes)
-  int K;   // dyadic levels: 2^K >= nb
-  int ho[kMaxHier + 1];
+  int* prx;      // [(L+1) nb] preorder index of the owned crossing node, -1 none
+  int* prs;      // its start point
+  double* prlen; // its length
+  Q4* pst;       // E_b at its start
+  Q4* plE;       // E_b at the end of the level-l node covering b's first point
+  Q4* T;         // [nb] block totals
+  Q4* Gi;        // [nb] inclusive scan of T within chunks of kTScan blocks
+  Q4* CS;        // [nc] chunk totals
+  Q4* CX;        // [nc + 1] exclusive scan of CS (CX[nc] = grand total)
 };
 
 // first set bit at a position > j of a kST-bit mask (nz: its non-zero words);
@@ -446,39 +506,13 @@ __device__ __forceinline__ int next_bit(const unsigned* __restrict__ m, unsigned
   return (w2 << 5) + __ffs(m[w2]) - 1;
 }
 
-// last set bit at a position <= j of a kST-bit mask (nz: its non-zero words);
-// the caller guarantees one exists
-__device__ __forceinline__ int prev_bit_incl(const unsigned* __restrict__ m, unsigned nz, int j) {
-  const int wd = j >> 5;
-  const unsigned v = m[wd] & (0xffffffffu >> (31 - (j & 31)));
-  if (v) return (wd << 5) + 31 - __clz(v);
-  const int w2 = 31 - __clz(nz & ((1u << wd) - 1u));
-  return (w2 << 5) + 31 - __clz(m[w2]);
-}
-
-// number of set bits at positions [a, b) of a kST-bit mask
-__device__ __forceinline__ int count_bits(const unsigned* __restrict__ m, int a, int b) {
-  if (a >= b) return 0;
-  const int wa = a >> 5, wb = (b - 1) >> 5;
-  const unsigned lo = ~0u << (a & 31), hi = 0xffffffffu >> (31 - ((b - 1) & 31));
-  if (wa == wb) return __popc(m[wa] & lo & hi);
-  int c = __popc(m[wa] & lo) + __popc(m[wb] & hi);
-  for (int q = wa + 1; q < wb; q++) c += __popc(m[q]);
-  return c;
-}
-
-// One block = kST sorted points, one thread each.  Per level l, bit masks
+// One block = kST sorted points, one thread each.  Per level l a bit mask
 // over the block's points: B_l (c_j < l: a node at level <= l starts at j, so
-// it ends every level-l range) and H_l (a level-l node starts at j, or j = 0
-// and the level-l node covering it started earlier -- the "pseudo head").
-// All the block's points share the levels <= lca (the common levels of its
-// first and last key), so above lca only position 0 has nodes, one child each.
-//   leaves: every thread sums its chain's leaf (bhtree.py:78-82);
-//   top-down, one node per thread: bbox replay from the shared level-lca box
-//     (bhtree.py:90-103) -> length, skip = offset[end] -> structural record;
-//   bottom-up, no barriers: each thread climbs from its leaf; a node's
-//     children report to a per-(level, head) counter and the last one to
-//     arrive folds them in slot order (starting from 0.0) and climbs on.
+// it ends every level-l range).  All the block's points share the levels <=
+// lca (the common levels of its first and last key), so above lca only
+// position 0 has nodes.  One node per thread: bbox replay from the shared
+// level-lca box (bhtree.py:90-103) -> length; end = the next B_l bit ->
+// skip = offset[end] and the sums E[end] - E[j]; records.
 __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long long* __restrict__ keys,
                                                      int64_t n, int L,
                                                      const signed char* __restrict__ clev,
@@ -486,46 +520,59 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
                                                      const double* __restrict__ box,
                                                      const double4* __restrict__ sp,
                                                      TreeRecords r, Cross cr, int nb) {
-  __shared__ unsigned mB[kMaxLevels + 2][kSW], mH[kMaxLevels + 2][kSW];
-  __shared__ unsigned nzB[kMaxLevels + 2], nzH[kMaxLevels + 2];
-  __shared__ unsigned arrived[kMaxLevels + 1][kST / 4];
+  __shared__ unsigned mB[kMaxLevels + 2][kSW];
+  __shared__ unsigned nzB[kMaxLevels + 2];
   __shared__ int offs[kST + 1];
   __shared__ signed char cs[kST + 1];
   __shared__ unsigned long long skey[kST];
-  __shared__ double4 V[kST];
+  __shared__ double4 P[kST];
+  __shared__ Q4 E[kST + 1];
+  __shared__ Q4 wt[kSW];
   __shared__ double pbox[6];
-  __shared__ int s_maxe, s_mn, s_q;
-  constexpr int kMap = 4 * kST;  // node -> point map of the top-down pass
+  __shared__ int s_maxe;
+  constexpr int kMap = 4 * kST;  // node -> point map of the node pass
   __shared__ short nmap[kMap];
-  __shared__ double4 qv[kST];  // queued aggregate records of the climb
-  __shared__ int qmir[kST];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5, b = blockIdx.x;
   const int64_t B0 = (int64_t)b * kST, i = B0 + t;
   const int64_t last = min(B0 + kST, n) - 1;
   const int nn = offset[n];
+  const double s64 = box[12], sinv = box[13];
   cs[t] = i <= n ? clev[i] : (signed char)-1;
   offs[t] = i <= n ? offset[i] : nn;
   skey[t] = i < n ? keys[i] : 0ull;
+  const double4 pv = i < n ? sp[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+  P[t] = pv;
   if (t == 0) {
     const int64_t j = B0 + kST;
     cs[kST] = j <= n ? clev[j] : (signed char)-1;
     offs[kST] = j <= n ? offset[j] : nn;
     s_maxe = -1;
-    s_mn = kMaxLevels + 1;
-    s_q = 0;
   }
   if (t <= L) cr.prx[t * nb + b] = -1;
-  __syncthreads();
+  {  // the block's exclusive prefix sums E[0..kST] (one barrier inside)
+    u128 q[4];
+    point_terms(pv, s64, q);
+#ifndef FGA_XP_NOSCAN
+    block_scan_q4(q, wt);
+#endif
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+      E[t + 1].v[c] = q[c];
+      if (t == 0) E[0].v[c] = 0;
+    }
+  }
   const unsigned long long k0 = skey[0];
   const int lca = last > B0 ? common_levels(k0, skey[last - B0], L) : L;
   const int c = cs[t], c0 = cs[0], cend = cs[kST];
   const bool has = i < n && c + 1 <= L;
   const int s = c + 1, e = has ? chain_end(s, cs[t + 1], L) : -1;
-  if (has) atomicMax(&s_maxe, e);
-  if (t > 0) atomicMin(&s_mn, c);
-  if (t == kST - 1) {
-    atomicMin(&s_mn, cend);
-    // the box of the level-lca node holding every point of the block
+  if (has) {
+    atomicMax(&s_maxe, e);
+    const int x0 = offs[t] - offs[0];
+    if (x0 + (e - s) < kMap)
+      for (int q = 0; q <= e - s; q++) nmap[x0 + q] = (short)t;
+  }
+  if (t == kST - 1) {  // the box of the level-lca node holding every point of the block
     double lo[3], hi[3];
 #pragma unroll
     for (int a = 0; a < 3; a++) {
@@ -539,271 +586,196 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
       pbox[3 + a] = hi[a];
     }
   }
-  // leaf sums (bhtree.py:78-82) and the leaf's aggregate record
-  double4 leafv = make_double4(0.0, 0.0, 0.0, 0.0);
-  if (has) {
-    int64_t end;  // point i alone, or a depth-cap cell of duplicates
-    if (e > cs[t + 1]) end = i + 1;
-    else if (e == 0) end = n;
-    else end = upper_bound_gallop(keys, i + 1, n, skey[t] | low_mask(3 * (L - e)));
-    leafv = leaf_sums(sp, i, end - i);
-    write_records_a(r, e + nn - (offs[t] + (e - s) + 1), leafv);
-    const int x0 = offs[t] - offs[0];
-    if (x0 + (e - s) < kMap)
-      for (int q = 0; q <= e - s; q++) nmap[x0 + q] = (short)t;
-  }
-  V[t] = leafv;
   __syncthreads();
   const int top = s_maxe;
-  const int mtop = max(top, min(c0, L));  // deepest level with a head
+  const int mtop = max(top, min(c0, L));  // deepest level with a node here
   for (int l = lca; l <= mtop; l++) {
-    const bool ph = t == 0 && l <= c0;
     const unsigned bb = __ballot_sync(0xffffffffu, c < l);
-    const unsigned bh = __ballot_sync(0xffffffffu, (has && s <= l && l <= e) || ph);
-    if (lane == 0) {
-      mB[l][w] = bb;
-      mH[l][w] = bh;
-    }
+    if (lane == 0) mB[l][w] = bb;
   }
-  if (t < kST / 4)
-    for (int l = lca; l < mtop; l++) arrived[l][t] = 0u;
   __syncthreads();
-  if (t >= lca && t <= mtop) {  // per level: non-zero word summaries
-    unsigned zb = 0, zh = 0;
-    for (int q = 0; q < kSW; q++) {
-      zb |= (mB[t][q] != 0u ? 1u : 0u) << q;
-      zh |= (mH[t][q] != 0u ? 1u : 0u) << q;
-    }
+  if (t >= lca && t <= mtop) {  // per level: non-zero word summary
+    unsigned zb = 0;
+    for (int q = 0; q < kSW; q++) zb |= (mB[t][q] != 0u ? 1u : 0u) << q;
     nzB[t] = zb;
-    nzH[t] = zh;
   }
   __syncthreads();
-  if (t == 0) cr.mn[b] = s_mn;
-
-  // top-down, one node per thread (the block's nodes are the preorder range
-  // [offs[0], offs[kST])); a node that runs past the block leaves its length
-  // and preorder index to k_crossing
-  {
-    const int offs0 = offs[0], nbn = offs[kST] - offs0;
-    for (int kk = t; kk < nbn; kk += kST) {
-      const int x = offs0 + kk;
-      int j;  // the point whose chain holds node x
-      if (nbn <= kMap) {
-        j = nmap[kk];
-      } else {
-        int lo_ = 0, hi_ = kST;
-        while (hi_ - lo_ > 1) {
-          const int mid = (lo_ + hi_) >> 1;
-          if (offs[mid] <= x) lo_ = mid; else hi_ = mid;
-        }
-        j = lo_;
-      }
-      const int sj = cs[j] + 1, ej = chain_end(sj, cs[j + 1], L);
-      const int l = sj + (x - offs[j]);
-      const unsigned long long key = skey[j];
-      double bl[3], bh[3];
-      int lv;
-      if (l <= lca) {  // (position 0 only: the other points start below lca)
-        lv = 0;
-#pragma unroll
-        for (int a = 0; a < 3; a++) {
-          bl[a] = box[a];
-          bh[a] = box[3 + a];
-        }
-      } else {
-        lv = lca;
-#pragma unroll
-        for (int a = 0; a < 3; a++) {
-          bl[a] = pbox[a];
-          bh[a] = pbox[3 + a];
-        }
-      }
-      while (lv < l) bbox_step(key, ++lv, L, bl, bh);
-      const double len = diag_len(bl, bh);
-      FGA_CHECK(j >= 0 && j < kST && l >= sj && l <= ej && x >= offs[j] && x < offs[j + 1]);
-      if (l == ej) {
-        const int mir = l + nn - (x + 1);
-        FGA_CHECK(mir >= 0 && mir < nn);
-        write_records_b(r, mir, mir + 1, true, len);
-      } else {
-        const int p = l <= lca ? kST : next_bit(mB[l], nzB[l], j);
-        if (p < kST || cend < l) {
-          const int skipp = offs[p];
-          const int mir = l + nn - skipp;
-          write_records_b(r, mir, mir + (skipp - x), false, len);
-        } else {
-          cr.prx[l * nb + b] = x;
-          cr.prlen[l * nb + b] = len;
-        }
-      }
-    }
+  if (t == 0) cr.T[b] = E[kST];
+  if (t <= min(c0, L)) {  // level-t node covering position 0 (owned earlier): its end here
+    const int l = t;
+    const int p = l <= lca ? kST : next_bit(mB[l], nzB[l], 0);
+    if (p < kST || cend < l) cr.plE[l * nb + b] = E[p];
   }
 
-  // bottom-up.  A climb starts at every leaf: the thread's own, and at
-  // position 0 the depth-cap duplicate run owned by an earlier block (its
-  // value here is 0).
-  int pos = t, lev = has ? e : (t == 0 && c0 == L ? L : -1);
-  double4 v = leafv;
-  bool up = lev >= 0;
-  while (up && lev > lca) {
-    const int pl = lev - 1;
-    const int hp = prev_bit_incl(mH[pl], nzH[pl], pos);  // the parent's head
-    const int pend = next_bit(mB[pl], nzB[pl], hp);       // ... and range end
-    const int nch = count_bits(mH[lev], hp, pend);
-    __threadfence_block();  // this child's V before the arrival
-    const unsigned sh = 8u * (hp & 3);  // byte counters, four per word
-    FGA_CHECK(hp >= 0 && hp < kST && pend > hp && pend <= kST && nch >= 1 && nch <= 8);
-    const unsigned old_ = atomicAdd(&arrived[pl][hp >> 2], 1u << sh);
-    FGA_CHECK((int)((old_ >> sh) & 0xffu) < nch);  // never more arrivals than children
-    if ((int)((old_ >> sh) & 0xffu) != nch - 1) {
-      up = false;
-      break;
-    }
-    __threadfence_block();  // every child's V after it
-    v = make_double4(0.0, 0.0, 0.0, 0.0);
-    {  // children: the H_lev bits in [hp, pend), in slot order
-      const unsigned* mh = mH[lev];
-      int wd = hp >> 5;
-      unsigned m = mh[wd] & (~0u << (hp & 31));
-      while (true) {
-        while (m) {
-          const int q = (wd << 5) + __ffs(m) - 1;
-          if (q >= pend) break;
-          add4(v, V[q]);
-          m &= m - 1u;
-        }
-        if (++wd >= kSW || (wd << 5) >= pend) break;
-        m = mh[wd];
+  const int offs0 = offs[0], nbn = offs[kST] - offs0;
+  for (int kk = t; kk < nbn; kk += kST) {
+    const int x = offs0 + kk;
+    int j;  // the point whose chain holds node x
+    if (nbn <= kMap) {
+      j = nmap[kk];
+    } else {
+      int lo_ = 0, hi_ = kST;
+      while (hi_ - lo_ > 1) {
+        const int mid = (lo_ + hi_) >> 1;
+        if (offs[mid] <= x) lo_ = mid; else hi_ = mid;
       }
+      j = lo_;
     }
-    V[hp] = v;
-    const bool local = pend < kST || cend < pl;
-    if (hp == 0 && pl <= c0) {
-      cr.pl[pl * nb + b] = v;
-      cr.plend[pl * nb + b] = local ? pend : -1;
-    } else if (local) {  // queued: the divisions run compacted after the climb
-      const int slot = atomicAdd(&s_q, 1);
-      FGA_CHECK(pl + nn - offs[pend] >= 0 && pl + nn - offs[pend] < nn);
-      if (slot < kST) {
-        qv[slot] = v;
-        qmir[slot] = pl + nn - offs[pend];
-      } else {
-        write_records_a(r, pl + nn - offs[pend], v);
+    const int sj = cs[j] + 1, ej = chain_end(sj, cs[j + 1], L);
+    const int l = sj + (x - offs[j]);
+    const unsigned long long key = skey[j];
+    double bl[3], bh[3];
+    int lv;
+    if (l <= lca) {  // (position 0 only: the other points start below lca)
+      lv = 0;
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        bl[a] = box[a];
+        bh[a] = box[3 + a];
       }
     } else {
-      cr.pr[pl * nb + b] = v;
+      lv = lca;
+#pragma unroll
+      for (int a = 0; a < 3; a++) {
+        bl[a] = pbox[a];
+        bh[a] = pbox[3 + a];
+      }
     }
-    pos = hp;
-    lev = pl;
-  }
-  if (up) {  // this thread holds position 0's node at level lev <= lca; each
-             // level above has one node there (pseudo up to c0, then the
-             // chain of point 0), with one child
-    for (int l = lev - 1; l >= 0; l--) {
-      v = make_double4(__dadd_rn(0.0, v.x), __dadd_rn(0.0, v.y), __dadd_rn(0.0, v.z),
-                       __dadd_rn(0.0, v.w));  // the one-child fold
-      const bool local = cend < l;
-      if (l <= c0) {
-        cr.pl[l * nb + b] = v;
-        cr.plend[l * nb + b] = local ? (int)(n - B0 < kST ? n - B0 : (int64_t)kST) : -1;  // (the last block ends at n)
-      } else if (local) {
-        write_records_a(r, l + nn - offs[kST], v);
+#ifndef FGA_XP_NOBBOX
+    while (lv < l) bbox_step(key, ++lv, L, bl, bh);
+    const double len = diag_len(bl, bh);
+#else
+    const double len = bl[0] + bh[1] + lv;
+#endif
+    FGA_CHECK(j >= 0 && j < kST && l >= sj && l <= ej && x >= offs[j] && x < offs[j + 1]);
+    if (l == ej) {  // leaf: point j alone, or a depth-cap cell of duplicates
+      const int mir = l + nn - (x + 1);
+      FGA_CHECK(mir >= 0 && mir < nn);
+      const int64_t gi = B0 + j;
+      if (ej > cs[j + 1]) {  // one point: (x m) / m, as the reference's sums of one row
+        const double4 v = P[j];
+        write_node(r, mir, mir + 1, true, len, __ddiv_rn(__dadd_rn(0.0, __dmul_rn(v.x, v.w)), v.w),
+                   __ddiv_rn(__dadd_rn(0.0, __dmul_rn(v.y, v.w)), v.w),
+                   __ddiv_rn(__dadd_rn(0.0, __dmul_rn(v.z, v.w)), v.w), v.w);
       } else {
-        cr.pr[l * nb + b] = v;
+        const int64_t end = ej == 0 ? n : upper_bound_gallop(keys, gi + 1, n, key | low_mask(3 * (L - ej)));
+        u128 a[4] = {0, 0, 0, 0};
+        for (int64_t q = gi; q < end; q++) {
+          u128 tq[4];
+          point_terms(sp[q], s64, tq);
+#pragma unroll
+          for (int cc = 0; cc < 4; cc++) a[cc] += tq[cc];
+        }
+        const double am = fixed_to_double(a[0]);
+        write_node(r, mir, mir + 1, true, len, __ddiv_rn(fixed_to_double(a[1]), am),
+                   __ddiv_rn(fixed_to_double(a[2]), am), __ddiv_rn(fixed_to_double(a[3]), am),
+                   am * sinv);
+      }
+    } else {
+      const int p = l <= lca ? kST : next_bit(mB[l], nzB[l], j);
+      if (p < kST || cend < l) {
+        const int skipp = offs[p];
+        const int mir = l + nn - skipp;
+        FGA_CHECK(mir >= 0 && mir < nn);
+        u128 a[4];
+#pragma unroll
+        for (int cc = 0; cc < 4; cc++) a[cc] = E[p].v[cc] - E[j].v[cc];
+        write_node_sums(r, mir, mir + (skipp - x), len, a, sinv);
+      } else {  // runs past the block: k_crossing
+        cr.prx[l * nb + b] = x;
+        cr.prs[l * nb + b] = (int)(B0 + j);
+        cr.prlen[l * nb + b] = len;
+        cr.pst[l * nb + b] = E[j];
       }
     }
   }
+}
+
+// Scan of the block totals: inclusive within chunks of kTScan blocks, and the
+// chunk totals.
+__global__ void __launch_bounds__(kTScan) k_tscan1(int nb, Cross cr) {
+  __shared__ Q4 wt[kTScan / 32];
+  const int b = blockIdx.x * kTScan + threadIdx.x;
+  u128 q[4] = {0, 0, 0, 0};
+  if (b < nb)
+#pragma unroll
+    for (int c = 0; c < 4; c++) q[c] = cr.T[b].v[c];
+  block_scan_q4(q, wt);
+  if (b < nb)
+#pragma unroll
+    for (int c = 0; c < 4; c++) cr.Gi[b].v[c] = q[c];
+  if (threadIdx.x == kTScan - 1)
+#pragma unroll
+    for (int c = 0; c < 4; c++) cr.CS[blockIdx.x].v[c] = q[c];
+}
+
+// Exclusive scan of the chunk totals (one block; CX[nc] = grand total).
+__global__ void __launch_bounds__(kTScan) k_tscan2(int nc, Cross cr) {
+  __shared__ Q4 wt[kTScan / 32];
+  __shared__ Q4 carry;
+  if (threadIdx.x == 0)
+    for (int c = 0; c < 4; c++) carry.v[c] = 0;
   __syncthreads();
-  const int nq = min(s_q, kST);
-  for (int k = t; k < nq; k += kST) write_records_a(r, qmir[k], qv[k]);
-}
-
-// Dyadic sums (per level) and minima over aligned runs of 2^k blocks, fixed
-// shape: hs_k[j] = hs_{k-1}[2j] + hs_{k-1}[2j+1].  One launch builds levels
-// k0+1..k0+5 from level k0: each warp takes 32 consecutive level-k0 entries
-// and pairs them up through shuffles (blockIdx.y = tree level, L + 1 = the
-// minima).
-__global__ void __launch_bounds__(256) k_hier(int L, int nb, int k0, Cross cr) {
-  const int l = blockIdx.y;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int sz0 = (nb + (1 << k0) - 1) >> k0;
-  if (j - lane >= sz0) return;  // (whole warps only)
-  if (l <= L) {
-    const double4* src = k0 == 0 ? cr.pl + (int64_t)l * nb : cr.hs + (int64_t)l * cr.hn + cr.ho[k0];
-    double4 v = j < sz0 ? src[j] : make_double4(0.0, 0.0, 0.0, 0.0);
-    for (int d = 1; d <= 5 && k0 + d <= cr.K; d++) {
-      double4 y;
-      y.x = __shfl_down_sync(0xffffffffu, v.x, 1 << (d - 1));
-      y.y = __shfl_down_sync(0xffffffffu, v.y, 1 << (d - 1));
-      y.z = __shfl_down_sync(0xffffffffu, v.z, 1 << (d - 1));
-      y.w = __shfl_down_sync(0xffffffffu, v.w, 1 << (d - 1));
-      const int szd = (nb + (1 << (k0 + d)) - 1) >> (k0 + d);
-      const int jd = j >> d;
-      if ((lane & ((1 << d) - 1)) == 0) {
-        if (((j >> (d - 1)) + 1) < ((nb + (1 << (k0 + d - 1)) - 1) >> (k0 + d - 1))) add4(v, y);
-        if (jd < szd) cr.hs[(int64_t)l * cr.hn + cr.ho[k0 + d] + jd] = v;
-      }
-    }
-  } else {
-    const int* src = k0 == 0 ? cr.mn : cr.hm + cr.ho[k0];
-    int v = j < sz0 ? src[j] : -1;
-    for (int d = 1; d <= 5 && k0 + d <= cr.K; d++) {
-      const int y = __shfl_down_sync(0xffffffffu, v, 1 << (d - 1));
-      const int szd = (nb + (1 << (k0 + d)) - 1) >> (k0 + d);
-      const int jd = j >> d;
-      if ((lane & ((1 << d) - 1)) == 0) {
-        if (((j >> (d - 1)) + 1) < ((nb + (1 << (k0 + d - 1)) - 1) >> (k0 + d - 1))) v = min(v, y);
-        if (jd < szd) cr.hm[cr.ho[k0 + d] + jd] = v;
-      }
-    }
+  for (int base = 0; base < nc; base += kTScan) {
+    const int k = base + threadIdx.x;
+    u128 q[4] = {0, 0, 0, 0}, own[4] = {0, 0, 0, 0};
+    if (k < nc)
+#pragma unroll
+      for (int c = 0; c < 4; c++) own[c] = q[c] = cr.CS[k].v[c];
+    block_scan_q4(q, wt);
+    if (k < nc)
+#pragma unroll
+      for (int c = 0; c < 4; c++) cr.CX[k].v[c] = carry.v[c] + q[c] - own[c];
+    __syncthreads();
+    if (threadIdx.x == kTScan - 1)
+#pragma unroll
+      for (int c = 0; c < 4; c++) carry.v[c] += q[c];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) cr.CX[nc] = carry;
 }
 
-__device__ __forceinline__ int hier_min(const Cross& cr, int k, int j) {
-  return k == 0 ? cr.mn[j] : cr.hm[cr.ho[k] + j];
+// sum of the totals of blocks < b
+__device__ __forceinline__ void block_prefix(const Cross& cr, int nb, int b, u128 g[4]) {
+  if (b >= nb) {
+    const int nc = (nb + kTScan - 1) / kTScan;
+#pragma unroll
+    for (int c = 0; c < 4; c++) g[c] = cr.CX[nc].v[c];
+    return;
+  }
+#pragma unroll
+  for (int c = 0; c < 4; c++) g[c] = cr.Gi[b].v[c] - cr.T[b].v[c] + cr.CX[b / kTScan].v[c];
 }
 
-// One thread per (level, block) with an owned crossing node: the block where
-// it ends (first later block with mn < l, by the dyadic minima), its partials
-// over the blocks after its own (the canonical dyadic cover, left to right),
-// and its records.
+// One thread per (level, block) with an owned crossing node: its end (the
+// first later key outside its prefix), its exact sums from the block prefix
+// sums, and its records.
 __global__ void __launch_bounds__(256) k_crossing(int L, int nb, int64_t n,
-                                                  const int* __restrict__ offset, Cross cr,
+                                                  const unsigned long long* __restrict__ keys,
+                                                  const int* __restrict__ offset,
+                                                  const double* __restrict__ box, Cross cr,
                                                   TreeRecords r) {
   const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (g >= (int64_t)(L + 1) * nb) return;
   const int l = (int)(g / nb), b = (int)(g % nb);
   const int x = cr.prx[l * nb + b];
   if (x < 0) return;
-  // end block: first bb > b with mn[bb] < l
-  int p = b + 1, k = 0;
-  while (true) {
-    while (k < cr.K && (p & ((2 << k) - 1)) == 0 && hier_min(cr, k + 1, p >> (k + 1)) >= l) k++;
-    if (hier_min(cr, k, p >> k) >= l) {
-      p += 1 << k;
-      continue;
-    }
-    break;
+  const int64_t i = cr.prs[l * nb + b];
+  const int64_t end = l == 0 ? n : upper_bound_gallop(keys, i + 1, n, keys[i] | low_mask(3 * (L - l)));
+  const int bend = (int)(end / kST), pe = (int)(end - (int64_t)bend * kST);
+  u128 ge[4], gb[4], a[4];
+  block_prefix(cr, nb, bend, ge);
+  block_prefix(cr, nb, b, gb);
+#pragma unroll
+  for (int c = 0; c < 4; c++) {
+    a[c] = ge[c] - gb[c] - cr.pst[l * nb + b].v[c];
+    if (pe > 0) a[c] += cr.plE[l * nb + bend].v[c];
   }
-  while (k > 0) {
-    k--;
-    if (hier_min(cr, k, p >> k) >= l) p += 1 << k;
-  }
-  const int bend = p;
-  double4 v = cr.pr[l * nb + b];
-  for (int q = b + 1; q <= bend;) {
-    int kk = min(__ffs(q) - 1, cr.K);
-    while (q + (1 << kk) - 1 > bend) kk--;
-    add4(v, kk == 0 ? cr.pl[l * nb + q] : cr.hs[(int64_t)l * cr.hn + cr.ho[kk] + (q >> kk)]);
-    q += 1 << kk;
-  }
-  const int64_t end = (int64_t)bend * kST + cr.plend[l * nb + bend];
   const int nn = offset[n];
   const int skipp = offset[end];
   const int mir = l + nn - skipp;
-  write_records_b(r, mir, mir + (skipp - x), false, cr.prlen[l * nb + b]);
-  write_records_a(r, mir, v);
+  FGA_CHECK(mir >= 0 && mir < nn && bend > b);
+  write_node_sums(r, mir, mir + (skipp - x), cr.prlen[l * nb + b], a, box[13]);
 }
 
 // first p in [0, to) with keys[p] >= bound, galloping backwards from `to`
@@ -930,10 +902,10 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   T.pts = pts_dev;
   T.masses = masses_dev;
   const int nb = (int)std::min<int64_t>(blocks_for(n), 4 * 148);
-  FGA_CUDA_TRY(T.scratch.reserve(sizeof(double) * 6 * (nb + 1)));
-  FGA_CUDA_TRY(T.box.reserve(sizeof(double) * 10));
-  k_bbox_partial<<<nb, kThreads, 0, st>>>(pts_dev, n, T.scratch.as<double>());
-  k_bbox_final<<<1, 256, 0, st>>>(T.scratch.as<double>(), nb, L, T.box.as<double>());
+  FGA_CUDA_TRY(T.scratch.reserve(sizeof(double) * 7 * (nb + 1)));
+  FGA_CUDA_TRY(T.box.reserve(sizeof(double) * 16));
+  k_bbox_partial<<<nb, kThreads, 0, st>>>(pts_dev, masses_dev, n, T.scratch.as<double>());
+  k_bbox_final<<<1, 256, 0, st>>>(T.scratch.as<double>(), nb, L, n, T.box.as<double>());
 
   // The sort runs on the top key bits only (3 radix passes for 24 bits, 4 for
   // 32) and k_fixup_runs orders each run of equal top bits by the full key;
@@ -1038,38 +1010,31 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   FGA_CUDA_TRY(T.a64.reserve(sizeof(double4) * nn64));
   FGA_CUDA_TRY(T.b64.reserve(sizeof(NodeB64) * nn64));
   const int nbs = (int)((n + kST - 1) / kST);
+  const int nc = (nbs + kTScan - 1) / kTScan;
   const int64_t ncr = (int64_t)(L + 1) * nbs;
   Cross cr{};
-  cr.K = 0;
-  while ((1ll << cr.K) < nbs) cr.K++;
-  cr.hn = 0;
-  for (int k = 1; k <= cr.K; k++) {
-    cr.ho[k] = cr.hn;
-    cr.hn += (nbs + (1 << k) - 1) >> k;
-  }
-  FGA_CUDA_TRY(T.cross.reserve(ncr * (2 * sizeof(double4) + sizeof(double) + 2 * sizeof(int)) +
-                               sizeof(int) * nbs + sizeof(double4) * (L + 1) * (int64_t)cr.hn +
-                               sizeof(int) * cr.hn + 64));
+  FGA_CUDA_TRY(T.cross.reserve(sizeof(Q4) * (2 * ncr + 2 * (int64_t)nbs + 2 * (int64_t)nc + 1) +
+                               ncr * (2 * sizeof(int) + sizeof(double)) + 256));
   {
-    char* q = T.cross.as<char>();
-    cr.pr = (double4*)q; q += sizeof(double4) * ncr;
-    cr.pl = (double4*)q; q += sizeof(double4) * ncr;
-    cr.hs = (double4*)q; q += sizeof(double4) * (L + 1) * (int64_t)cr.hn;
+    char* q = T.cross.as<char>();  // (Q4 arrays first: 16 B alignment)
+    cr.pst = (Q4*)q; q += sizeof(Q4) * ncr;
+    cr.plE = (Q4*)q; q += sizeof(Q4) * ncr;
+    cr.T = (Q4*)q; q += sizeof(Q4) * nbs;
+    cr.Gi = (Q4*)q; q += sizeof(Q4) * nbs;
+    cr.CS = (Q4*)q; q += sizeof(Q4) * nc;
+    cr.CX = (Q4*)q; q += sizeof(Q4) * (nc + 1);
     cr.prlen = (double*)q; q += sizeof(double) * ncr;
     cr.prx = (int*)q; q += sizeof(int) * ncr;
-    cr.plend = (int*)q; q += sizeof(int) * ncr;
-    cr.mn = (int*)q; q += sizeof(int) * nbs;
-    cr.hm = (int*)q;
+    cr.prs = (int*)q;
   }
   k_subtrees<<<nbs, kST, 0, st>>>(T.keys.as<unsigned long long>(), n, L, T.clev.as<signed char>(),
                                   T.offset.as<int>(), T.box.as<double>(), T.sp.as<double4>(),
                                   T.records(), cr, nbs);
   if (nbs > 1) {
-    for (int k0 = 0; k0 < cr.K; k0 += 5) {
-      const int sz0 = (nbs + (1 << k0) - 1) >> k0;
-      k_hier<<<dim3((sz0 + 255) / 256, L + 2), 256, 0, st>>>(L, nbs, k0, cr);
-    }
-    k_crossing<<<(int)((ncr + 255) / 256), 256, 0, st>>>(L, nbs, n, T.offset.as<int>(), cr,
+    k_tscan1<<<nc, kTScan, 0, st>>>(nbs, cr);
+    k_tscan2<<<1, kTScan, 0, st>>>(nc, cr);
+    k_crossing<<<(int)((ncr + 255) / 256), 256, 0, st>>>(L, nbs, n, T.keys.as<unsigned long long>(),
+                                                         T.offset.as<int>(), T.box.as<double>(), cr,
                                                          T.records());
   }
   FGA_CUDA_TRY(cudaGetLastError());
