@@ -36,6 +36,7 @@
 //   k_crossing      nodes that run past their block: sums from the prefixes
 #include <cub/cub.cuh>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "fga_internal.cuh"
@@ -506,6 +507,16 @@ __device__ __forceinline__ int next_bit(const unsigned* __restrict__ m, unsigned
   return (w2 << 5) + __ffs(m[w2]) - 1;
 }
 
+__device__ __forceinline__ u128 e_limb(const unsigned long long (*E)[kST + 1], int c, int p) {
+  return ((u128)E[2 * c + 1][p] << 64) | E[2 * c][p];
+}
+__device__ __forceinline__ Q4 e_at(const unsigned long long (*E)[kST + 1], int p) {
+  Q4 r;
+#pragma unroll
+  for (int c = 0; c < 4; c++) r.v[c] = e_limb(E, c, p);
+  return r;
+}
+
 // One block = kST sorted points, one thread each.  Per level l a bit mask
 // over the block's points: B_l (c_j < l: a node at level <= l starts at j, so
 // it ends every level-l range).  All the block's points share the levels <=
@@ -525,8 +536,9 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
   __shared__ int offs[kST + 1];
   __shared__ signed char cs[kST + 1];
   __shared__ unsigned long long skey[kST];
-  __shared__ double4 P[kST];
-  __shared__ Q4 E[kST + 1];
+  // SoA in shared memory (64-bit words per thread: no bank conflicts)
+  __shared__ double P[4][kST];                     // the block's points x, y, z, m
+  __shared__ unsigned long long E[8][kST + 1];     // prefix sums: limb 2c = low, 2c+1 = high
   __shared__ Q4 wt[kSW];
   __shared__ double pbox[6];
   __shared__ int s_maxe;
@@ -541,7 +553,10 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
   offs[t] = i <= n ? offset[i] : nn;
   skey[t] = i < n ? keys[i] : 0ull;
   const double4 pv = i < n ? sp[i] : make_double4(0.0, 0.0, 0.0, 0.0);
-  P[t] = pv;
+  P[0][t] = pv.x;
+  P[1][t] = pv.y;
+  P[2][t] = pv.z;
+  P[3][t] = pv.w;
   if (t == 0) {
     const int64_t j = B0 + kST;
     cs[kST] = j <= n ? clev[j] : (signed char)-1;
@@ -549,18 +564,25 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
     s_maxe = -1;
   }
   if (t <= L) cr.prx[t * nb + b] = -1;
-  {  // the block's exclusive prefix sums E[0..kST] (one barrier inside)
-    u128 q[4];
-    point_terms(pv, s64, q);
-#ifndef FGA_XP_NOSCAN
-    block_scan_q4(q, wt);
-#endif
-#pragma unroll
+  {  // the block's exclusive prefix sums E[0..kST]: per component a warp
+     // scan into E, then (after the next barrier) the earlier warps' totals
+#pragma unroll 1
     for (int c = 0; c < 4; c++) {
-      E[t + 1].v[c] = q[c];
-      if (t == 0) E[0].v[c] = 0;
+      const double tv = c == 0 ? pv.w : __dmul_rn(c == 1 ? pv.x : (c == 2 ? pv.y : pv.z), pv.w);
+      u128 q = to_fixed(tv, s64);
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u128 y = shfl_up128(q, d);
+        if (lane >= d) q += y;
+      }
+      E[2 * c][t + 1] = (unsigned long long)q;
+      E[2 * c + 1][t + 1] = (unsigned long long)(q >> 64);
+      if (lane == 31) wt[w].v[c] = q;
     }
+    if (t == 0)
+      for (int c = 0; c < 8; c++) E[c][0] = 0ull;
   }
+  __syncthreads();  // cs, offs, skey, s_maxe
   const unsigned long long k0 = skey[0];
   const int lca = last > B0 ? common_levels(k0, skey[last - B0], L) : L;
   const int c = cs[t], c0 = cs[0], cend = cs[kST];
@@ -587,6 +609,15 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
     }
   }
   __syncthreads();
+  if (w > 0)  // the earlier warps' totals into this thread's prefix sums
+#pragma unroll 1
+    for (int cc = 0; cc < 4; cc++) {
+      u128 add = wt[0].v[cc];
+      for (int ww = 1; ww < w; ww++) add += wt[ww].v[cc];
+      const u128 v = e_limb(E, cc, t + 1) + add;
+      E[2 * cc][t + 1] = (unsigned long long)v;
+      E[2 * cc + 1][t + 1] = (unsigned long long)(v >> 64);
+    }
   const int top = s_maxe;
   const int mtop = max(top, min(c0, L));  // deepest level with a node here
   for (int l = lca; l <= mtop; l++) {
@@ -600,11 +631,11 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
     nzB[t] = zb;
   }
   __syncthreads();
-  if (t == 0) cr.T[b] = E[kST];
+  if (t == 0) cr.T[b] = e_at(E, kST);
   if (t <= min(c0, L)) {  // level-t node covering position 0 (owned earlier): its end here
     const int l = t;
     const int p = l <= lca ? kST : next_bit(mB[l], nzB[l], 0);
-    if (p < kST || cend < l) cr.plE[l * nb + b] = E[p];
+    if (p < kST || cend < l) cr.plE[l * nb + b] = e_at(E, p);
   }
 
   const int offs0 = offs[0], nbn = offs[kST] - offs0;
@@ -653,7 +684,7 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
       FGA_CHECK(mir >= 0 && mir < nn);
       const int64_t gi = B0 + j;
       if (ej > cs[j + 1]) {  // one point: (x m) / m, as the reference's sums of one row
-        const double4 v = P[j];
+        const double4 v = make_double4(P[0][j], P[1][j], P[2][j], P[3][j]);
         write_node(r, mir, mir + 1, true, len, __ddiv_rn(__dadd_rn(0.0, __dmul_rn(v.x, v.w)), v.w),
                    __ddiv_rn(__dadd_rn(0.0, __dmul_rn(v.y, v.w)), v.w),
                    __ddiv_rn(__dadd_rn(0.0, __dmul_rn(v.z, v.w)), v.w), v.w);
@@ -679,13 +710,13 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
         FGA_CHECK(mir >= 0 && mir < nn);
         u128 a[4];
 #pragma unroll
-        for (int cc = 0; cc < 4; cc++) a[cc] = E[p].v[cc] - E[j].v[cc];
+        for (int cc = 0; cc < 4; cc++) a[cc] = e_limb(E, cc, p) - e_limb(E, cc, j);
         write_node_sums(r, mir, mir + (skipp - x), len, a, sinv);
       } else {  // runs past the block: k_crossing
         cr.prx[l * nb + b] = x;
         cr.prs[l * nb + b] = (int)(B0 + j);
         cr.prlen[l * nb + b] = len;
-        cr.pst[l * nb + b] = E[j];
+        cr.pst[l * nb + b] = e_at(E, j);
       }
     }
   }
@@ -947,9 +978,16 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
                                                  T.keys32.as<unsigned>(), T.idx_in.as<int>(),
                                                  T.idx.as<int>(), (int)n, 0, std::min(bits, 3 * L),
                                                  st));
+    size_t fg0 = 0;
+    static const int fg = getenv("FGA_XP_L2FG") ? atoi(getenv("FGA_XP_L2FG")) : 0;
+    if (fg) {
+      cudaDeviceGetLimit(&fg0, cudaLimitMaxL2FetchGranularity);
+      cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, fg);
+    }
     k_gather_sorted<<<blocks_for(n), kThreads, 0, st>>>(T.packed.as<double4>(), T.idx.as<int>(), n,
                                                         T.box.as<double>(), L, T.sp.as<double4>(),
                                                         T.keys.as<unsigned long long>());
+    if (fg) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, fg0);
     if (shift > 0)
       k_fixup_runs<<<blocks_for(n), kThreads, 0, st>>>(T.keys32.as<unsigned>(), n,
                                                        T.keys.as<unsigned long long>(),
