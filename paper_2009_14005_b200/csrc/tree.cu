@@ -446,10 +446,6 @@ __device__ __forceinline__ void write_node(const TreeRecords& r, int mir, int rs
 // records of a node whose exact sums are a[0..3] (scaled by 2^S)
 __device__ __forceinline__ void write_node_sums(const TreeRecords& r, int mir, int rskip,
                                                 double len, const u128 a[4], double sinv) {
-#ifdef FGA_XP_NOSUM
-  write_node(r, mir, rskip, false, len, (double)(unsigned long long)a[1], 0.0, 0.0, sinv);
-  return;
-#endif
   const double am = fixed_to_double(a[0]);
   write_node(r, mir, rskip, false, len, __ddiv_rn(fixed_to_double(a[1]), am),
              __ddiv_rn(fixed_to_double(a[2]), am), __ddiv_rn(fixed_to_double(a[3]), am),
@@ -672,12 +668,8 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
         bh[a] = pbox[3 + a];
       }
     }
-#ifndef FGA_XP_NOBBOX
     while (lv < l) bbox_step(key, ++lv, L, bl, bh);
     const double len = diag_len(bl, bh);
-#else
-    const double len = bl[0] + bh[1] + lv;
-#endif
     FGA_CHECK(j >= 0 && j < kST && l >= sj && l <= ej && x >= offs[j] && x < offs[j + 1]);
     if (l == ej) {  // leaf: point j alone, or a depth-cap cell of duplicates
       const int mir = l + nn - (x + 1);
@@ -978,16 +970,9 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
                                                  T.keys32.as<unsigned>(), T.idx_in.as<int>(),
                                                  T.idx.as<int>(), (int)n, 0, std::min(bits, 3 * L),
                                                  st));
-    size_t fg0 = 0;
-    static const int fg = getenv("FGA_XP_L2FG") ? atoi(getenv("FGA_XP_L2FG")) : 0;
-    if (fg) {
-      cudaDeviceGetLimit(&fg0, cudaLimitMaxL2FetchGranularity);
-      cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, fg);
-    }
     k_gather_sorted<<<blocks_for(n), kThreads, 0, st>>>(T.packed.as<double4>(), T.idx.as<int>(), n,
                                                         T.box.as<double>(), L, T.sp.as<double4>(),
                                                         T.keys.as<unsigned long long>());
-    if (fg) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, fg0);
     if (shift > 0)
       k_fixup_runs<<<blocks_for(n), kThreads, 0, st>>>(T.keys32.as<unsigned>(), n,
                                                        T.keys.as<unsigned long long>(),
