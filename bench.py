@@ -656,11 +656,17 @@ def run_tree_build(args, dev, peaks, peak_src):
             times.append(a.elapsed_time(b))
         t = float(np.median(times)) / 1e3
         ach = BUILD_BYTES_PER_POINT * n / t / 1e9
+        prof = _profile("build").get(str(n)) or {}
+        traffic = prof.get("dram_bytes")
         out[str(n)] = {"ms": t * 1e3, "nodes": int(nn.value), "points_per_s": n / t,
                        "roofline": {"bound": "hbm", "unit": "GB/s", "achieved": ach,
                                     "peak": hbm, "frac": ach / hbm,
                                     "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs",
-                                    "work": f"SURVEY §8(d): {BUILD_BYTES_PER_POINT} B/point"}}
+                                    "work": f"SURVEY §8(d): {BUILD_BYTES_PER_POINT} B/point",
+                                    "traffic": traffic,
+                                    # the DRAM bytes the build actually moves
+                                    # (ncu, all its kernels) over this live time
+                                    "dram_frac": (traffic / t / 1e9 / hbm) if traffic else None}}
         del pts, ms, flush
     c.close()
     out["api"] = "fga_tree_build_dev (blob points, unit masses, max_depth 20), median of reps, L2 flushed"
