@@ -524,6 +524,8 @@ def run_e2e(args, x, y, rank, world, local_rank):
     inside the timed region.  Same state (initial template) and tree as the
     headline; with N ranks each evaluates its 1/N of the queries (max over
     ranks of the wall time, accepted interactions summed)."""
+    import ctypes
+
     import torch
     import torch.distributed as dist
 
@@ -552,13 +554,16 @@ def run_e2e(args, x, y, rank, world, local_rank):
     qm[:] = my[lo:hi]
     f = pinned((mm, 3), torch.float64)
     vis = pinned((mm,), torch.int64)
-    acc = pinned((mm,), torch.int64)
     L = N.lib()
+    total = N._i64(0)
 
     def call():
+        # the reference's outputs (forces, visits); the interaction count of
+        # the call comes back as one integer (fga_last_interactions)
         N.check(L.fga_tree_forces(c.handle, N.ptr(q), N.ptr(qm), mm, float(args.theta),
                                   float(p.G), float(p.epsilon) ** 2, N.PREC_FP32, N.ptr(f),
-                                  N.ptr(vis), N.ptr(acc)))
+                                  N.ptr(vis), None))
+        N.check(L.fga_last_interactions(c.handle, ctypes.byref(total)))
 
     for _ in range(2):
         call()
@@ -568,7 +573,7 @@ def run_e2e(args, x, y, rank, world, local_rank):
     for _ in range(args.steps):
         call()
     wall = time.perf_counter() - t0
-    t = torch.tensor([wall, float(acc.sum())], dtype=torch.float64,
+    t = torch.tensor([wall, float(total.value)], dtype=torch.float64,
                      device=torch.device("cuda", local_rank))
     if world > 1:
         tmax = t[:1].clone()
@@ -580,11 +585,11 @@ def run_e2e(args, x, y, rank, world, local_rank):
         inter = float(t[1].item())
     return {"value": inter * args.steps / wall, "unit": UNIT,
             "h2d_bytes_per_step": int(q.nbytes + qm.nbytes) * world,
-            "d2h_bytes_per_step": int(f.nbytes + vis.nbytes + acc.nbytes) * world,
+            "d2h_bytes_per_step": int(f.nbytes + vis.nbytes + 8) * world,
             "ms_per_step": 1e3 * wall / args.steps,
-            "api": "fga_tree_forces (drop-in for _kernels.bh_forces_kernel), pinned host "
-                   "buffers, initial template state, FP32 traversal, wall clock per rank, max "
-                   "over ranks",
+            "api": "fga_tree_forces (drop-in for _kernels.bh_forces_kernel: forces + visits "
+                   "out, + fga_last_interactions for the count), pinned host buffers, initial "
+                   "template state, FP32 traversal, wall clock per rank, max over ranks",
             "visits_per_query": float(vis.mean())}
 
 

@@ -241,6 +241,12 @@ int fga_tree_generation(fga_ctx* ctx, int64_t* generation);
 int fga_tree_forces(fga_ctx* ctx, const double* queries, const double* query_masses, int64_t m,
                     double theta, double G, double eps2, int precision, double* forces,
                     int64_t* visits, int64_t* accepted);
+/* Accepted (interacting) nodes summed over the queries of the last
+ * fga_tree_forces / fga_bh_forces_kernel call in this context, -1 before the
+ * first -- the interaction count without the per-query `accepted` array (an
+ * extension: the reference does not report it). */
+int fga_last_interactions(fga_ctx* ctx, int64_t* accepted_total);
+
 /* The reference's exact kernel signature (_kernels.py:7-8): uploads the tree
  * arrays (skipped when the same arrays -- address, size, sampled contents --
  * are still the context's tree), then evaluates in FP64 (the reference's

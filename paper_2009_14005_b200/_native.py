@@ -135,6 +135,7 @@ SIGNATURES = {
     "fga_tree_export": (_c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fga_tree_upload": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _c_int, _c_int]),
     "fga_tree_generation": (_c_int, [_vp, ctypes.POINTER(_i64)]),
+    "fga_last_interactions": (_c_int, [_vp, ctypes.POINTER(_i64)]),
     "fga_tree_forces": (_c_int, [_vp, _vp, _vp, _i64, _dbl, _dbl, _dbl, _c_int, _vp, _vp, _vp]),
     "fga_bh_forces_kernel": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _c_int, _vp, _vp, _i64,
                                       _c_int, _dbl, _dbl, _dbl, _i64, _vp, _vp]),

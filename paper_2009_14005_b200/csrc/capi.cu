@@ -80,6 +80,8 @@ struct fga_ctx {
   TreeDev tree;
   DevBuf tree_pts, tree_masses;
   DevBuf op[8];
+  DevBuf op_total;               // device counter: accepted nodes of the last operator call
+  int64_t last_interactions = -1;
   Session S;
   int* pinned = nullptr;  // poll buffer: done, pad, iter(lo,hi)
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -1354,15 +1356,21 @@ int fga_tree_forces(fga_ctx* c, const double* queries, const double* qm, int64_t
   double* f = out.as<double>();
   long long* vis = reinterpret_cast<long long*>(f + 3 * m);
   long long* acc = vis + m;
+  FGA_CUDA_TRY(c->op_total.reserve(sizeof(unsigned long long)));
+  FGA_CUDA_TRY(cudaMemsetAsync(c->op_total.p, 0, sizeof(unsigned long long), s));
   launch_bh_operator(c->tree, b, b + m, b + 2 * m, b + 3 * m, iout.as<int>(), m, theta, G, eps2, f,
-                     vis, acc, precision, s);
+                     visits ? vis : nullptr, accepted ? acc : nullptr,
+                     c->op_total.as<unsigned long long>(), precision, s);
   FGA_CUDA_TRY(cudaGetLastError());
   std::vector<double> f3(dim == 3 ? 0 : 3 * m);
   FGA_CUDA_TRY(cudaMemcpyAsync(dim == 3 ? forces : f3.data(), f, sizeof(double) * 3 * m,
                                cudaMemcpyDeviceToHost, s));
   if (visits) FGA_CUDA_TRY(cudaMemcpyAsync(visits, vis, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
   if (accepted) FGA_CUDA_TRY(cudaMemcpyAsync(accepted, acc, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
+  unsigned long long total = 0;
+  FGA_CUDA_TRY(cudaMemcpyAsync(&total, c->op_total.p, sizeof(total), cudaMemcpyDeviceToHost, s));
   FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  c->last_interactions = (int64_t)total;
   if (dim != 3) unpad3(f3.data(), m, dim, forces);
   return FGA_OK;
 }
@@ -1387,6 +1395,12 @@ uint64_t sampled_hash(uint64_t h, const void* base, int64_t words) {
   return h;
 }
 }  // namespace
+
+int fga_last_interactions(fga_ctx* c, int64_t* accepted_total) {
+  CTX_TRY(c);
+  if (accepted_total) *accepted_total = c->last_interactions;
+  return FGA_OK;
+}
 
 int fga_tree_generation(fga_ctx* c, int64_t* generation) {
   CTX_TRY(c);

@@ -284,7 +284,8 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
                                                  const double* qpx, const double* qpy,
                                                  const double* qpz, int64_t m_queries,
                                                  double* hs = nullptr, float gA = 0.f,
-                                                 float gB = 0.f, int64_t qidx = -1) {
+                                                 float gB = 0.f, int64_t qidx = -1,
+                                                 unsigned* hc = nullptr) {
   // hs (optional): the block's fp64 fold sums in shared memory, 3 per thread
   // (hs[3 threadIdx.x ..]), so they hold no registers across the loop (folds
   // are rare; the address is re-derived at each fold)
@@ -295,6 +296,14 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     h[0] = h[1] = h[2] = 0.0;
   }
   int visits = 0, accepted = 0;
+  // kPacked (counting visits with hc given): one register holds (visits <<
+  // 16) | accepted of the current fold chunk -- at most FGA_FOLD node indices,
+  // each visited at most once -- and the folds add it to the per-thread
+  // totals in shared memory (hc[2 threadIdx.x ..])
+  constexpr bool kPackable = kCountVisits && FGA_FOLD > 0 && FGA_FOLD <= 65535;
+  const bool packed = kPackable && hc != nullptr;
+  unsigned cnt = 0;
+  if (packed) hc[2 * threadIdx.x] = hc[2 * threadIdx.x + 1] = 0u;
   int cursor = active ? 0 : n_nodes;
   if constexpr (kStatic) {  // one band per warp: the largest lane delta
     gA = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gA)));
@@ -316,6 +325,12 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
         hz += (double)az;
       }
       ax = ay = az = 0.f;
+      if (kPackable && packed) {
+        unsigned* hcc = hc + 2 * threadIdx.x;
+        hcc[0] += cnt >> 16;
+        hcc[1] += cnt & 0xffffu;
+        cnt = 0;
+      }
       lim = fold_limit(n, n_nodes);
     }
     FGA_CHECK(n >= 0 && n < n_nodes);
@@ -354,7 +369,11 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     ax = fmaf(w, dx, ax);
     ay = fmaf(w, dy, ay);
     az = fmaf(w, dz, az);
-    if constexpr (kCountVisits) {
+    if (kPackable && packed) {
+      asm("{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %1, 0;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+          "@p add.u32 %0, %0, 65536;\n\t@q add.u32 %0, %0, 1;\n\t}"
+          : "+r"(cnt) : "r"((int)mine), "r"((int)take));
+    } else if constexpr (kCountVisits) {
       asm("{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %2, 0;\n\tsetp.ne.b32 q, %3, 0;\n\t"
           "@p add.s32 %0, %0, 1;\n\t@q add.s32 %1, %1, 1;\n\t}"
           : "+r"(visits), "+r"(accepted) : "r"((int)mine), "r"((int)take));
@@ -364,6 +383,11 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     }
     const int next = acc ? __float_as_int(b.y) : n + 1;
     cursor = mine ? next : cursor;
+  }
+  if (kPackable && packed) {
+    const unsigned* hcc = hc + 2 * threadIdx.x;
+    visits = (int)(hcc[0] + (cnt >> 16));
+    accepted = (int)(hcc[1] + (cnt & 0xffffu));
   }
   if (hs) {
     const double* h = hs + 3 * threadIdx.x;

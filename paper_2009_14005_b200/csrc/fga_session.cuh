@@ -44,7 +44,7 @@ void launch_gpe(const RefPoints& ref, const double* px, const double* py, const 
 void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, const double* qz,
                         const double* qm, const int* order, int64_t m, double theta, double G,
                         double eps2, double* fout, long long* visits, long long* accepted,
-                        int precision, cudaStream_t s);
+                        unsigned long long* acc_total, int precision, cudaStream_t s);
 void launch_direct_operator(const RefPoints& ref, const double* qx, const double* qy,
                             const double* qz, const double* qm, int64_t m, double G, double eps,
                             double* fout, int precision, cudaStream_t s);

@@ -88,9 +88,11 @@ __global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? FGA_BH32_TPS : FGA_BH
   int nv, na;
   if constexpr (sizeof(Real) == 4) {
     __shared__ double hs[3 * kT];  // the lanes' fp64 fold sums
+    __shared__ unsigned hc[kCountVisits ? 2 * kT : 1];  // their visit / accept counts
     const Trav32Out o = traverse32d<kGuardZero, kCountVisits>(
         tr.c32, tr.a64, tr.b64, n_nodes, (float)y[0], (float)y[1], (float)y[2], active, f.theta2,
-        sp.theta2, f.eps2, tv.px, tv.py, tv.pz, tv.m, hs);
+        sp.theta2, f.eps2, tv.px, tv.py, tv.pz, tv.m, hs, 0.f, 0.f, -1,
+        kCountVisits ? hc : nullptr);
     const double gq = sp.G * mq;
     F[0] = gq * o.ax;
     F[1] = gq * o.ay;
@@ -139,36 +141,49 @@ template <typename Real, bool kGuardZero>
 #ifndef FGA_BHOP_MINB
 #define FGA_BHOP_MINB 5  // 1280 threads/SM: fp64 operator 39.5 -> 38.7 ms (1M x 1M, host in/out)
 #endif
-__global__ void __launch_bounds__(kForceThreads, sizeof(Real) == 4 ? FGA_BH32_TPS / kForceThreads
+#ifndef FGA_BHOP32_TPS
+#define FGA_BHOP32_TPS FGA_BH32_TPS
+#endif
+__global__ void __launch_bounds__(kForceThreads, sizeof(Real) == 4 ? FGA_BHOP32_TPS / kForceThreads
                                                                    : FGA_BHOP_MINB) k_bh_operator(
     TreeRecords tr, int n_nodes, const double* __restrict__ qx_, const double* __restrict__ qy_,
     const double* __restrict__ qz_, const double* __restrict__ qm_, const int* __restrict__ order,
     int64_t m, double theta2, double G, double eps2, F32Params f, double* __restrict__ fout,
-    long long* __restrict__ visits, long long* __restrict__ accepted) {
+    long long* __restrict__ visits, long long* __restrict__ accepted,
+    unsigned long long* __restrict__ acc_total) {
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t i = ((int64_t)blockIdx.x * kWarps + wl) * 32 + lane;
   const bool active = i < m;
-  double q[3] = {0, 0, 0}, qm = 0.0;
-  if (active) {
-    q[0] = qx_[i];
-    q[1] = qy_[i];
-    q[2] = qz_[i];
-    qm = qm_[i];
-  }
   double F[3];
   int nv, na;
   if constexpr (sizeof(Real) == 4) {
+    // the query as fp32 only: its mass is re-read after the traversal (L2)
+    // instead of holding registers across it
+    float qf[3] = {0.f, 0.f, 0.f};
+    if (active) {
+      qf[0] = (float)qx_[i];
+      qf[1] = (float)qy_[i];
+      qf[2] = (float)qz_[i];
+    }
     __shared__ double hs[3 * kForceThreads];
+    __shared__ unsigned hc[2 * kForceThreads];
     const Trav32Out o = traverse32d<kGuardZero, true>(
-        tr.c32, tr.a64, tr.b64, n_nodes, (float)q[0], (float)q[1], (float)q[2], active, f.theta2,
-        theta2, f.eps2, qx_, qy_, qz_, m, hs);
-    const double gq = G * qm;
+        tr.c32, tr.a64, tr.b64, n_nodes, qf[0], qf[1], qf[2], active, f.theta2, theta2, f.eps2,
+        qx_, qy_, qz_, m, hs, 0.f, 0.f, -1, hc);
+    const double gq = G * (active ? qm_[i] : 0.0);
     F[0] = gq * o.ax;
     F[1] = gq * o.ay;
     F[2] = gq * o.az;
     nv = o.visits;
     na = o.accepted;
   } else {
+    double q[3] = {0, 0, 0}, qm = 0.0;
+    if (active) {
+      q[0] = qx_[i];
+      q[1] = qy_[i];
+      q[2] = qz_[i];
+      qm = qm_[i];
+    }
     __shared__ Win64 wins[kWarps];
     Trav64Out o = traverse64(tr.a64, tr.b64, n_nodes, q[0], q[1], q[2], __dmul_rn(G, qm), active,
                              theta2, eps2, &wins[wl], lane);
@@ -177,6 +192,10 @@ __global__ void __launch_bounds__(kForceThreads, sizeof(Real) == 4 ? FGA_BH32_TP
     F[2] = o.fz;
     nv = o.visits;
     na = o.accepted;
+  }
+  if (acc_total) {  // the call's interaction count (fga_last_interactions)
+    const unsigned wsum = __reduce_add_sync(0xffffffffu, active ? (unsigned)na : 0u);
+    if (lane == 0) atomicAdd(acc_total, (unsigned long long)wsum);
   }
   if (!active) return;
   const int64_t dst = order ? order[i] : i;
@@ -684,7 +703,7 @@ void launch_gpe(const RefPoints& ref, const double* px, const double* py, const 
 void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, const double* qz,
                         const double* qm, const int* order, int64_t m, double theta, double G,
                         double eps2, double* fout, long long* visits, long long* accepted,
-                        int precision, cudaStream_t s) {
+                        unsigned long long* acc_total, int precision, cudaStream_t s) {
   if (m <= 0) return;
   const unsigned g = grid_for(m, kForceThreads);
   const double theta2 = theta * theta;
@@ -694,17 +713,17 @@ void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, co
   if (precision) {
     k_bh_operator<double, false><<<g, kForceThreads, 0, s>>>(r, nn, qx, qy, qz, qm, order, m,
                                                              theta2, G, eps2, f, fout, visits,
-                                                             accepted);
+                                                             accepted, acc_total);
     return;
   }
   launch_node_bands(T, qx, qy, qz, m, nullptr, f.theta2, f.eps2, s);
   if (!(eps2 > 0.0))
     k_bh_operator<float, true><<<g, kForceThreads, 0, s>>>(r, nn, qx, qy, qz, qm, order, m, theta2,
-                                                           G, eps2, f, fout, visits, accepted);
+                                                           G, eps2, f, fout, visits, accepted, acc_total);
   else
     k_bh_operator<float, false><<<g, kForceThreads, 0, s>>>(r, nn, qx, qy, qz, qm, order, m,
                                                             theta2, G, eps2, f, fout, visits,
-                                                            accepted);
+                                                            accepted, acc_total);
 }
 
 void launch_direct_operator(const RefPoints& ref, const double* qx, const double* qy,

@@ -173,3 +173,38 @@ def test_c_validate_norm_range_message():
     assert N.last_error() == "invalid parameter norm_range=(5.0, -5.0)"
     with pytest.raises(fga.InvalidParam) as e:
         N.check(rc)
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_last_interactions_equals_accepted_sum(orc, precision):
+    """fga_last_interactions (the call's interaction count without the
+    per-query array) equals the per-query accepted counts summed, and the
+    oracle's, in both precisions; with accepted=NULL as well."""
+    from paper_2009_14005_b200 import PointCloud, bhtree, synth
+    from paper_2009_14005_b200 import _native as N
+    rng = synth.rng_from_seed(11)
+    x = synth.blob(20000, rng)
+    mx = rng.uniform(0.005, 0.02, len(x))
+    bhtree.build(PointCloud(x.points), mx, 20)
+    q = np.ascontiguousarray(synth.blob(3000, rng).points)
+    qm = rng.uniform(0.02, 0.1, len(q))
+    c = N.context(0)
+    L = N.lib()
+    f = np.zeros((len(q), 3))
+    vis = np.zeros(len(q), np.int64)
+    acc = np.zeros(len(q), np.int64)
+    total = N._i64(-7)
+    N.check(L.fga_tree_forces(c.handle, N.ptr(q), N.ptr(qm), len(q), 0.5, 1.0, 0.04, precision,
+                              N.ptr(f), N.ptr(vis), N.ptr(acc)))
+    N.check(L.fga_last_interactions(c.handle, ctypes.byref(total)))
+    assert total.value == int(acc.sum()) > 0
+    f2 = np.zeros_like(f)
+    N.check(L.fga_tree_forces(c.handle, N.ptr(q), N.ptr(qm), len(q), 0.5, 1.0, 0.04, precision,
+                              N.ptr(f2), None, None))
+    t2 = N._i64(-7)
+    N.check(L.fga_last_interactions(c.handle, ctypes.byref(t2)))
+    assert t2.value == total.value
+    assert np.array_equal(f, f2)
+    tree = orc.tree_build(x.points, mx, 20)
+    _, ovis, oacc = orc.bh_forces(tree, q, qm, 0.5, 1.0, 0.2, 1)  # (eps, squared inside)
+    assert np.array_equal(vis, ovis) and int(oacc.sum()) == total.value
