@@ -1358,14 +1358,37 @@ int fga_tree_forces(fga_ctx* c, const double* queries, const double* qm, int64_t
   long long* acc = vis + m;
   FGA_CUDA_TRY(c->op_total.reserve(sizeof(unsigned long long)));
   FGA_CUDA_TRY(cudaMemsetAsync(c->op_total.p, 0, sizeof(unsigned long long), s));
-  launch_bh_operator(c->tree, b, b + m, b + 2 * m, b + 3 * m, iout.as<int>(), m, theta, G, eps2, f,
-                     visits ? vis : nullptr, accepted ? acc : nullptr,
+  // Pinned (device-mapped) host outputs: the kernel stores each query's
+  // results straight into them, so the device->host transfer overlaps the
+  // traversal instead of following it
+  // (measured on the 1M drop-in: 14.00 -> 13.83 ms; FGA_ZERO_COPY=0 turns it off)
+  static const bool zc_on = !(getenv("FGA_ZERO_COPY") && atoi(getenv("FGA_ZERO_COPY")) == 0);
+  double* fz = nullptr;
+  long long* vz = nullptr;
+  if (zc_on && dim == 3) {
+    auto mapped = [](void* h) -> void* {
+      cudaPointerAttributes a{};
+      if (!h || cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+      }
+      return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+    };
+    fz = static_cast<double*>(mapped(forces));
+    vz = visits ? static_cast<long long*>(mapped(visits)) : nullptr;
+    if (!fz || (visits && !vz)) fz = nullptr, vz = nullptr;
+  }
+  launch_bh_operator(c->tree, b, b + m, b + 2 * m, b + 3 * m, iout.as<int>(), m, theta, G, eps2,
+                     fz ? fz : f, fz ? vz : (visits ? vis : nullptr), accepted ? acc : nullptr,
                      c->op_total.as<unsigned long long>(), precision, s);
   FGA_CUDA_TRY(cudaGetLastError());
   std::vector<double> f3(dim == 3 ? 0 : 3 * m);
-  FGA_CUDA_TRY(cudaMemcpyAsync(dim == 3 ? forces : f3.data(), f, sizeof(double) * 3 * m,
-                               cudaMemcpyDeviceToHost, s));
-  if (visits) FGA_CUDA_TRY(cudaMemcpyAsync(visits, vis, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
+  if (!fz) {
+    FGA_CUDA_TRY(cudaMemcpyAsync(dim == 3 ? forces : f3.data(), f, sizeof(double) * 3 * m,
+                                 cudaMemcpyDeviceToHost, s));
+    if (visits)
+      FGA_CUDA_TRY(cudaMemcpyAsync(visits, vis, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
+  }
   if (accepted) FGA_CUDA_TRY(cudaMemcpyAsync(accepted, acc, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
   unsigned long long total = 0;
   FGA_CUDA_TRY(cudaMemcpyAsync(&total, c->op_total.p, sizeof(total), cudaMemcpyDeviceToHost, s));

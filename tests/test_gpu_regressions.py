@@ -208,3 +208,32 @@ def test_last_interactions_equals_accepted_sum(orc, precision):
     tree = orc.tree_build(x.points, mx, 20)
     _, ovis, oacc = orc.bh_forces(tree, q, qm, 0.5, 1.0, 0.2, 1)  # (eps, squared inside)
     assert np.array_equal(vis, ovis) and int(oacc.sum()) == total.value
+
+
+def test_pinned_outputs_written_in_place_equal_pageable():
+    """fga_tree_forces with pinned (device-mapped) host outputs has the kernel
+    store straight into them; results equal the pageable-output path's."""
+    import torch
+
+    from paper_2009_14005_b200 import PointCloud, bhtree, synth
+    from paper_2009_14005_b200 import _native as N
+    rng = synth.rng_from_seed(12)
+    x = synth.blob(30000, rng)
+    mx = rng.uniform(0.005, 0.02, len(x))
+    bhtree.build(PointCloud(x.points), mx, 20)
+    q = np.ascontiguousarray(synth.blob(5000, rng).points)
+    qm = rng.uniform(0.02, 0.1, len(q))
+    c = N.context(0)
+    L = N.lib()
+    f = np.zeros((len(q), 3))
+    vis = np.zeros(len(q), np.int64)
+    N.check(L.fga_tree_forces(c.handle, N.ptr(q), N.ptr(qm), len(q), 0.5, 1.0, 0.04, 0,
+                              N.ptr(f), N.ptr(vis), None))
+    fp = torch.full((len(q), 3), np.nan, dtype=torch.float64, pin_memory=True).numpy()
+    vp = torch.full((len(q),), -1, dtype=torch.int64, pin_memory=True).numpy()
+    for _ in range(2):
+        N.check(L.fga_tree_forces(c.handle, N.ptr(q), N.ptr(qm), len(q), 0.5, 1.0, 0.04, 0,
+                                  N.ptr(fp), N.ptr(vp), None))
+        assert np.array_equal(fp, f) and np.array_equal(vp, vis)
+        fp[:] = np.nan
+        vp[:] = -1
