@@ -194,50 +194,77 @@ def run_dry(args, rank, world):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region
+    (samples are matched to the region by their timestamps)."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
         self.path = os.path.join("/tmp", f"fga_clocks_{os.getpid()}.csv")
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+        # nvidia-smi takes a few hundred ms to start: the region begins once
+        # it is sampling
+        t_end = time.time() + 5.0
+        while self.proc is not None and time.time() < t_end and not self._rows():
+            time.sleep(0.02)
+        self.t0 = time.time()
         return self
 
+    def _rows(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines()]
+        except OSError:
+            return []
+        return [[c.strip() for c in r] for r in rows if len(r) >= 8]
+
     def __exit__(self, *a):
+        self.t1 = time.time()
         if self.proc is not None:
             time.sleep(0.15)
             self.proc.terminate()
             self.proc.wait()
 
-    def summary(self):
+    @staticmethod
+    def _ts(v):
+        import datetime
         try:
-            rows = [r.split(",") for r in open(self.path).read().strip().splitlines()]
-        except OSError:
-            rows = []
-        rows = [[c.strip() for c in r] for r in rows if len(r) >= 7]
+            return datetime.datetime.strptime(v, "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
+
+    def summary(self):
+        rows = self._rows()
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        stamped = [(self._ts(r[0]), r) for r in rows]
+        inside = [r for t, r in stamped if t is not None and self.t0 - 0.06 <= t <= self.t1 + 0.06]
+        if not inside:  # (a region shorter than the sampling period) the nearest sample
+            mid = 0.5 * (self.t0 + self.t1)
+            inside = [min(stamped, key=lambda tr: abs((tr[0] or 0.0) - mid))[1]]
+        sm = [float(r[1]) for r in inside if r[1].replace(".", "").isdigit()]
         reasons = set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            for nm, v in zip(names, r[3:7]):
+        for r in inside:
+            for nm, v in zip(names, r[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": sorted(reasons), "samples": len(rows)}
+                "sm_max_mhz": float(inside[0][2]) if inside[0][2].replace(".", "").isdigit() else None,
+                "reasons": sorted(reasons), "samples": len(inside),
+                "region_s": round(self.t1 - self.t0, 3)}
 
 
 # --------------------------------------------------------------------------- ours
