@@ -138,6 +138,14 @@ int fga_register_batch(fga_ctx* ctx, const double* x_all, const int64_t* x_offse
                        const double* y_all, const int64_t* y_offsets, int64_t n_pairs, int dim,
                        const fga_params* params, const fga_options* options,
                        fga_pair_result* out, double* deltas);
+/* Same with one host array per cloud (xs[p]: (xn[p],3), ys[p]: (yn[p],3)):
+ * the clouds go to the device through a pinned staging ring filled on all
+ * host threads while the copy engine drains it (no host-side concatenation).
+ * options->x_weights / y_weights must be NULL (use fga_register_batch). */
+int fga_register_batch_list(fga_ctx* ctx, const double* const* xs, const int64_t* xn,
+                            const double* const* ys, const int64_t* yn, int64_t n_pairs,
+                            int dim, const fga_params* params, const fga_options* options,
+                            fga_pair_result* out, double* deltas);
 /* Same with device-resident clouds/offsets/weights/outputs (stream-ordered). */
 int fga_register_batch_dev(fga_ctx* ctx, const double* x_all, const int64_t* x_offsets,
                            const double* y_all, const int64_t* y_offsets, int64_t n_pairs,

@@ -103,6 +103,9 @@ SIGNATURES = {
     "fga_register_batch": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _c_int,
                                     ctypes.POINTER(CParams), ctypes.POINTER(COptions), _vp,
                                     _vp]),
+    "fga_register_batch_list": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _c_int,
+                                         ctypes.POINTER(CParams), ctypes.POINTER(COptions), _vp,
+                                         _vp]),
     "fga_register_batch_dev": (_c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _c_int, _c_int, _c_int,
                                         ctypes.POINTER(CParams), ctypes.POINTER(COptions), _vp,
                                         _vp]),

@@ -81,6 +81,9 @@ struct fga_ctx {
   DevBuf tree_pts, tree_masses;
   DevBuf op[8];
   DevBuf op_total;               // device counter: accepted nodes of the last operator call
+  // pinned staging ring of fga_register_batch_list (kStageSlots chunks)
+  char* stage[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t last_interactions = -1;
   Session S;
   int* pinned = nullptr;  // poll buffer: done, pad, iter(lo,hi)
@@ -604,6 +607,13 @@ int fga_destroy(fga_ctx* c) {
   c->batch_deltas.release();
   c->batch_counter.release();
   c->batch_wide.release();
+  c->op_total.release();
+  for (int k = 0; k < 4; k++) {
+    if (c->stage[k]) cudaFreeHost(c->stage[k]);
+    if (c->stage_ev[k]) cudaEventDestroy(c->stage_ev[k]);
+    c->stage[k] = nullptr;
+    c->stage_ev[k] = nullptr;
+  }
   Session& S = c->S;
   S.lm_idx.release();
   S.rbf_scratch.release();
@@ -1230,6 +1240,103 @@ int fga_register_batch(fga_ctx* c, const double* x_all, const int64_t* x_offsets
   TRY(fga_register_batch_dev(c, c->batch_in[0].as<double>(), c->batch_in[2].as<int64_t>(),
                              c->batch_in[1].as<double>(), c->batch_in[3].as<int64_t>(), n_pairs,
                              nmax, mmax, dim, params, &O, c->batch_out.as<fga_pair_result>(),
+                             deltas ? c->batch_deltas.as<double>() : nullptr));
+  FGA_CUDA_TRY(cudaMemcpyAsync(out, c->batch_out.p, sizeof(fga_pair_result) * n_pairs,
+                               cudaMemcpyDeviceToHost, s));
+  if (deltas)
+    FGA_CUDA_TRY(cudaMemcpyAsync(deltas, c->batch_deltas.p,
+                                 sizeof(double) * n_pairs * params->max_iters,
+                                 cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  return FGA_OK;
+}
+
+}  // extern "C" (C++ helpers of fga_register_batch_list)
+namespace fga {
+void host_gather_segments(const char* const* src, const int64_t* prefix, int64_t nseg,
+                          int64_t lo, int64_t hi, char* dst);
+}
+
+namespace {
+constexpr int kStageSlots = 4;
+constexpr int64_t kStageBytes = 32ll << 20;
+
+// host segments -> one contiguous device buffer through the pinned ring: the
+// host threads fill chunk k+1 while the copy engine moves chunk k
+int stage_segments_h2d(fga_ctx* c, const char* const* src, const int64_t* prefix, int64_t nseg,
+                       char* dst_dev, cudaStream_t s) {
+  for (int k = 0; k < kStageSlots; k++) {
+    if (!c->stage[k]) {
+      FGA_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&c->stage[k]), kStageBytes,
+                                 cudaHostAllocDefault));
+      FGA_CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev[k], cudaEventDisableTiming));
+      FGA_CUDA_TRY(cudaEventRecord(c->stage_ev[k], s));
+    }
+  }
+  const int64_t total = prefix[nseg];
+  int slot = 0;
+  for (int64_t lo = 0; lo < total; lo += kStageBytes, slot = (slot + 1) % kStageSlots) {
+    const int64_t hi = std::min(total, lo + kStageBytes);
+    FGA_CUDA_TRY(cudaEventSynchronize(c->stage_ev[slot]));  // its previous copy is done
+    fga::host_gather_segments(src, prefix, nseg, lo, hi, c->stage[slot]);
+    FGA_CUDA_TRY(cudaMemcpyAsync(dst_dev + lo, c->stage[slot], (size_t)(hi - lo),
+                                 cudaMemcpyHostToDevice, s));
+    FGA_CUDA_TRY(cudaEventRecord(c->stage_ev[slot], s));
+  }
+  return FGA_OK;
+}
+}  // namespace
+extern "C" {
+
+int fga_register_batch_list(fga_ctx* c, const double* const* xs, const int64_t* xn,
+                            const double* const* ys, const int64_t* yn, int64_t n_pairs, int dim,
+                            const fga_params* params, const fga_options* options,
+                            fga_pair_result* out, double* deltas) {
+  CTX_TRY(c);
+  if (n_pairs <= 0) return FGA_OK;
+  if (!xs || !xn || !ys || !yn || !out) return FGA_ERR_INVALID;
+  if (options && (options->x_weights || options->y_weights)) {
+    set_error("fga_register_batch_list: external weights need fga_register_batch");
+    return FGA_ERR_INVALID;
+  }
+  std::vector<int64_t> xo(n_pairs + 1, 0), yo(n_pairs + 1, 0);
+  int nmax = 0, mmax = 0;
+  for (int64_t p = 0; p < n_pairs; p++) {
+    if (xn[p] < 0 || yn[p] < 0) return FGA_ERR_INVALID;
+    xo[p + 1] = xo[p] + xn[p];
+    yo[p + 1] = yo[p] + yn[p];
+    nmax = (int)std::max<int64_t>(nmax, xn[p]);
+    mmax = (int)std::max<int64_t>(mmax, yn[p]);
+  }
+  // one virtual concatenation: the x clouds, then the y clouds (bytes)
+  std::vector<const char*> src(2 * n_pairs);
+  std::vector<int64_t> pre(2 * n_pairs + 1, 0);
+  for (int64_t p = 0; p < n_pairs; p++) {
+    src[p] = reinterpret_cast<const char*>(xs[p]);
+    src[n_pairs + p] = reinterpret_cast<const char*>(ys[p]);
+  }
+  for (int64_t k = 0; k < 2 * n_pairs; k++)
+    pre[k + 1] = pre[k] + 3 * (int64_t)sizeof(double) * (k < n_pairs ? xn[k] : yn[k - n_pairs]);
+  const int64_t nx = xo[n_pairs], ny = yo[n_pairs];
+  cudaStream_t s = c->stream;
+  FGA_CUDA_TRY(c->batch_in[0].reserve(sizeof(double) * 3 * (nx + ny)));
+  TRY(stage_segments_h2d(c, src.data(), pre.data(), 2 * n_pairs, c->batch_in[0].as<char>(), s));
+  TRY(h2d(c->batch_in[2], xo.data(), n_pairs + 1, s));
+  TRY(h2d(c->batch_in[3], yo.data(), n_pairs + 1, s));
+  fga_options O;
+  if (options) {
+    O = *options;
+  } else {
+    O = fga_options{};
+    O.normalize = 1;
+    O.compute_gpe = 1;
+  }
+  FGA_CUDA_TRY(c->batch_out.reserve(sizeof(fga_pair_result) * n_pairs));
+  if (deltas) FGA_CUDA_TRY(c->batch_deltas.reserve(sizeof(double) * n_pairs * params->max_iters));
+  const double* X = c->batch_in[0].as<double>();
+  TRY(fga_register_batch_dev(c, X, c->batch_in[2].as<int64_t>(), X + 3 * nx,
+                             c->batch_in[3].as<int64_t>(), n_pairs, nmax, mmax, dim, params, &O,
+                             c->batch_out.as<fga_pair_result>(),
                              deltas ? c->batch_deltas.as<double>() : nullptr));
   FGA_CUDA_TRY(cudaMemcpyAsync(out, c->batch_out.p, sizeof(fga_pair_result) * n_pairs,
                                cudaMemcpyDeviceToHost, s));

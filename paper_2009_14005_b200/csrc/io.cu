@@ -30,6 +30,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -566,3 +567,29 @@ int fga_parse_weights(const char* text, int64_t len, double* out, int64_t cap, i
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ staging
+// Copies the byte range [lo, hi) of the virtual concatenation of `nseg`
+// host segments (src[k], prefix[k+1] - prefix[k] bytes) into dst, on all host
+// threads (fga_register_batch_list: many small clouds -> one pinned staging
+// chunk, no numpy concatenation).
+namespace fga {
+void host_gather_segments(const char* const* src, const int64_t* prefix, int64_t nseg,
+                          int64_t lo, int64_t hi, char* dst) {
+  if (hi <= lo) return;
+  // first segment holding byte lo
+  int64_t a = 0, b = nseg;
+  while (b - a > 1) {
+    const int64_t mid = (a + b) / 2;
+    if (prefix[mid] <= lo) a = mid; else b = mid;
+  }
+  int64_t last = a;
+  while (last + 1 < nseg && prefix[last + 1] < hi) last++;
+  const int64_t first = a;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t k = first; k <= last; k++) {
+    const int64_t s0 = std::max(prefix[k], lo), s1 = std::min(prefix[k + 1], hi);
+    if (s1 > s0) std::memcpy(dst + (s0 - lo), src[k] + (s0 - prefix[k]), (size_t)(s1 - s0));
+  }
+}
+}  // namespace fga

@@ -192,7 +192,8 @@ def register_batch(pairs, params: FgaParams | None = None,
         for j, k in enumerate(in_kernel):
             results[k], errors[k] = br.results[j], br.errors[j]
             inter[k], status[k] = br.interactions[j], br.status[j]
-    rest = [k for k in range(P) if k not in set(in_kernel) or status[k] == N.FGA_ERR_UNSUPPORTED]
+    kset = set(in_kernel)
+    rest = [k for k in range(P) if k not in kset or status[k] == N.FGA_ERR_UNSUPPORTED]
     for k in rest:
         x, y = pairs[k]
         o = RegisterOptions(**{**options.__dict__,
@@ -214,29 +215,42 @@ def register_batch(pairs, params: FgaParams | None = None,
 def _register_batch_kernel(pairs, params, options, xws, yws) -> BatchResult:
     """The persistent batched kernel on pairs it supports (fga_register_batch)."""
     P = len(pairs)
-    xs = [x.points for x, _ in pairs]
-    ys = [y.points for _, y in pairs]
-    xoff = np.zeros(P + 1, np.int64)
-    yoff = np.zeros(P + 1, np.int64)
-    xoff[1:] = np.cumsum([len(a) for a in xs])
-    yoff[1:] = np.cumsum([len(a) for a in ys])
-    X = np.ascontiguousarray(np.concatenate(xs) if xoff[-1] else np.zeros((0, 3)))
-    Y = np.ascontiguousarray(np.concatenate(ys) if yoff[-1] else np.zeros((0, 3)))
-    xw = yw = None
-    if xws is not None:
-        xw = np.ascontiguousarray(np.concatenate(
-            [check_weights(len(a), w) for a, w in zip(xs, xws)]))
-    if yws is not None:
-        yw = np.ascontiguousarray(np.concatenate(
-            [check_weights(len(a), w) for a, w in zip(ys, yws)]))
+    xs = [np.ascontiguousarray(x.points, dtype=np.float64) for x, _ in pairs]
+    ys = [np.ascontiguousarray(y.points, dtype=np.float64) for _, y in pairs]
     c = N.context(options.device)
     out = (N.CPairResult * P)()
     deltas = np.zeros((P, params.max_iters)) if options.record_iterations else None
     cp = N.make_params(params)
-    co = _c_options(options, xw, yw)
-    N.check(N.lib().fga_register_batch(c.handle, N.ptr(X), N.ptr(xoff), N.ptr(Y), N.ptr(yoff), P,
-                                       3, N.ctypes.byref(cp), N.ctypes.byref(co),
-                                       N.ctypes.addressof(out), N.ptr(deltas)))
+    if xws is None and yws is None:
+        # one host array per cloud: staged to the device in the library (no
+        # host-side concatenation of the clouds)
+        co = _c_options(options, None, None)
+        xp = np.array([a.ctypes.data for a in xs], dtype=np.uintp)
+        yp = np.array([a.ctypes.data for a in ys], dtype=np.uintp)
+        xn = np.array([len(a) for a in xs], dtype=np.int64)
+        yn = np.array([len(a) for a in ys], dtype=np.int64)
+        N.check(N.lib().fga_register_batch_list(c.handle, N.ptr(xp), N.ptr(xn), N.ptr(yp),
+                                                N.ptr(yn), P, 3, N.ctypes.byref(cp),
+                                                N.ctypes.byref(co), N.ctypes.addressof(out),
+                                                N.ptr(deltas)))
+    else:
+        xoff = np.zeros(P + 1, np.int64)
+        yoff = np.zeros(P + 1, np.int64)
+        xoff[1:] = np.cumsum([len(a) for a in xs])
+        yoff[1:] = np.cumsum([len(a) for a in ys])
+        X = np.ascontiguousarray(np.concatenate(xs) if xoff[-1] else np.zeros((0, 3)))
+        Y = np.ascontiguousarray(np.concatenate(ys) if yoff[-1] else np.zeros((0, 3)))
+        xw = yw = None
+        if xws is not None:
+            xw = np.ascontiguousarray(np.concatenate(
+                [check_weights(len(a), w) for a, w in zip(xs, xws)]))
+        if yws is not None:
+            yw = np.ascontiguousarray(np.concatenate(
+                [check_weights(len(a), w) for a, w in zip(ys, yws)]))
+        co = _c_options(options, xw, yw)
+        N.check(N.lib().fga_register_batch(c.handle, N.ptr(X), N.ptr(xoff), N.ptr(Y), N.ptr(yoff),
+                                           P, 3, N.ctypes.byref(cp), N.ctypes.byref(co),
+                                           N.ctypes.addressof(out), N.ptr(deltas)))
     results, errors = [], []
     inter = np.zeros(P, np.int64)
     status = np.zeros(P, np.int32)
