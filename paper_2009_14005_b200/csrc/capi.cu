@@ -46,6 +46,7 @@ struct Session {
   bool applied = false;
   int64_t passes = 0;      // force passes enqueued
   bool last_pass_gpe = false;
+  bool fused_update = false;  // the last session_forces also ran the update
   DevBuf x_raw, y_raw, xn, yn, ctx_dev, mx, my, flat, counts, cells, ref32, ref64;
   DevBuf tkeys_in, tkeys, tidx_in, tidx, cub_tmp, tpl;
   DevBuf partials, gpe_part, sums, state, scratch, lm_idx, rbf_scratch, red_stage;
@@ -461,7 +462,9 @@ int session_gpe(fga_ctx* c, const IterState* gate) {
   return FGA_OK;
 }
 
-int session_forces(fga_ctx* c) {
+// fuse: the caller runs the update right after (fga_session_iterate): small
+// passes then reduce and update in one kernel (launch_reduce_update)
+int session_forces(fga_ctx* c, bool fuse = false) {
   Session& S = c->S;
   cudaStream_t s = c->stream;
   TemplateView tv = S.view();
@@ -482,10 +485,20 @@ int session_forces(fga_ctx* c) {
     ngw = gpe_warps(S.m_local, S.ref().n, S.precision);
   }
   const double pairs = S.direct ? (double)S.n * (double)S.m_local : -1.0;
-  launch_reduce(S.partials.as<double>(), nw, S.gpe_part.as<double>(), ngw, pairs,
-                S.sums_ptr(), S.red_stage.as<double>(), s);
   S.last_pass_gpe = with_gpe;
   S.passes++;
+  if (fuse && reduce_update_fusable(nw, ngw)) {
+    launch_reduce_update(S.partials.as<double>(), nw, S.gpe_part.as<double>(), ngw, pairs,
+                         S.sums_ptr(), S.st(), S.sp, S.rec_delta.as<double>(),
+                         S.rec_traj.as<double>(), S.rec_gpe.as<double>(),
+                         S.rec_inter.as<long long>(), S.rec_visits.as<long long>(),
+                         with_gpe ? 1 : 0, s);
+    S.fused_update = true;
+  } else {
+    launch_reduce(S.partials.as<double>(), nw, S.gpe_part.as<double>(), ngw, pairs,
+                  S.sums_ptr(), S.red_stage.as<double>(), s);
+    S.fused_update = false;
+  }
   FGA_CUDA_TRY(cudaGetLastError());
   return FGA_OK;
 }
@@ -720,8 +733,8 @@ int fga_session_iterate(fga_ctx* c, int k) {
     return FGA_ERR_STATE;
   }
   for (int i = 0; i < k; i++) {
-    TRY(session_forces(c));
-    TRY(session_update(c));
+    TRY(session_forces(c, true));
+    if (!c->S.fused_update) TRY(session_update(c));
   }
   return FGA_OK;
 }

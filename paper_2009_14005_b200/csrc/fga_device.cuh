@@ -275,7 +275,9 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
 // {l^2 | -inf, skip, length, 0}, and the band is formed per step from the
 // warp's coefficients gA / gB (guard_coeffs) -- no per-launch band pass;
 // qidx >= 0 gives the re-check's query index explicitly.
-template <bool kGuardZero, bool kCountVisits, bool kStatic = false>
+// kSmem: C points to the records copied into shared memory (small trees,
+// k_bh_iterate_small); plain loads instead of the read-only global path
+template <bool kGuardZero, bool kCountVisits, bool kStatic = false, bool kSmem = false>
 __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
                                                  const double4* __restrict__ A64,
                                                  const NodeB64* __restrict__ B64, int n_nodes,
@@ -335,8 +337,8 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     }
     FGA_CHECK(n >= 0 && n < n_nodes);
     const NodeC32* rec = reinterpret_cast<const NodeC32*>(C) + n;
-    const float4 a = __ldg(&rec->a);
-    const float4 b = __ldg(&rec->b);
+    const float4 a = kSmem ? rec->a : __ldg(&rec->a);
+    const float4 b = kSmem ? rec->b : __ldg(&rec->b);
     const bool mine = cursor == n;
     const float dx = a.x - qx, dy = a.y - qy, dz = a.z - qz;
     float r2, diff, band;

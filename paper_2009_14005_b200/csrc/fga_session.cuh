@@ -54,6 +54,12 @@ size_t reduce_stage_doubles();
 void launch_reduce(const double* partials, int64_t nwarps, const double* gpe_partials,
                    int64_t ngwarps, double direct_pairs, double* sums, double* stage,
                    cudaStream_t s);
+bool reduce_update_fusable(int64_t nwarps, int64_t ngwarps);
+void launch_reduce_update(const double* partials, int64_t nwarps, const double* gpe_partials,
+                          int64_t ngwarps, double direct_pairs, double* sums, IterState* st,
+                          const SimParams& sp, double* rec_delta, double* rec_traj,
+                          double* rec_gpe, long long* rec_inter, long long* rec_visits,
+                          int has_gpe, cudaStream_t s);
 void launch_update(const double* sums, IterState* st, const SimParams& sp, double* rec_delta,
                    double* rec_traj, double* rec_gpe, long long* rec_inter, long long* rec_visits,
                    int has_gpe, cudaStream_t s);

@@ -54,11 +54,23 @@ struct F32Params {
 #ifndef FGA_BH64_TPS
 #define FGA_BH64_TPS 1280
 #endif
-template <typename Real, bool kGuardZero, bool kCountVisits, int kT>
-__global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? FGA_BH32_TPS : FGA_BH64_TPS) / kT) k_bh_iterate(
+// kSmall: the whole FP32 record array is first copied into shared memory
+// (trees up to kSmallTreeBytes; launched when the template is small enough
+// that the pass is a few latency-bound warps per SM, e.g. configs[0]'s 2k
+// points: every step's record load is then a shared-memory load instead of an
+// L1/L2 round trip on a cold SM)
+constexpr int kSmallTreeBytes = 200 * 1024;
+template <typename Real, bool kGuardZero, bool kCountVisits, int kT, bool kSmall = false>
+__global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32_TPS : FGA_BH64_TPS) / kT) k_bh_iterate(
     TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, SimParams sp,
     F32Params f, double* partials, int nblocks) {
   if (st->done) return;
+  extern __shared__ float4 s_rec[];
+  if constexpr (kSmall) {
+    const int nv = 2 * n_nodes;
+    for (int k = threadIdx.x; k < nv; k += kT) s_rec[k] = __ldg(tr.c32 + k);
+    __syncthreads();
+  }
   // (An SM-contiguous block->chunk remap for L1 sharing was measured 3%
   // slower -- per-SM load imbalance -- so blocks map to chunks in order.)
   const int chunk = (int)blockIdx.x;
@@ -89,8 +101,8 @@ __global__ void __launch_bounds__(kT, (sizeof(Real) == 4 ? FGA_BH32_TPS : FGA_BH
   if constexpr (sizeof(Real) == 4) {
     __shared__ double hs[3 * kT];  // the lanes' fp64 fold sums
     __shared__ unsigned hc[kCountVisits ? 2 * kT : 1];  // their visit / accept counts
-    const Trav32Out o = traverse32d<kGuardZero, kCountVisits>(
-        tr.c32, tr.a64, tr.b64, n_nodes, (float)y[0], (float)y[1], (float)y[2], active, f.theta2,
+    const Trav32Out o = traverse32d<kGuardZero, kCountVisits, false, kSmall>(
+        kSmall ? s_rec : tr.c32, tr.a64, tr.b64, n_nodes, (float)y[0], (float)y[1], (float)y[2], active, f.theta2,
         sp.theta2, f.eps2, tv.px, tv.py, tv.pz, tv.m, hs, 0.f, 0.f, -1,
         kCountVisits ? hc : nullptr);
     const double gq = sp.G * mq;
@@ -648,6 +660,35 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
     return;
   }
   launch_node_bands(T, tv.px, tv.py, tv.pz, tv.m, st, f.theta2, f.eps2, s);
+  const size_t tree_bytes = sizeof(float4) * 2 * (size_t)nn;
+  if constexpr (kT == 128) {
+  if (tree_bytes <= (size_t)kSmallTreeBytes &&
+      (int64_t)nb <= (int64_t)current_sms() * std::max<int64_t>(1, (220 * 1024) / (int64_t)tree_bytes)) {
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
+      cudaFuncSetAttribute(k_bh_iterate<float, true, true, kT, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallTreeBytes);
+      cudaFuncSetAttribute(k_bh_iterate<float, true, false, kT, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallTreeBytes);
+      cudaFuncSetAttribute(k_bh_iterate<float, false, true, kT, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallTreeBytes);
+      cudaFuncSetAttribute(k_bh_iterate<float, false, false, kT, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallTreeBytes);
+      if (dev >= 0 && dev < 64) attr[dev] = true;
+    }
+    if (gz && sp.count_visits)
+      k_bh_iterate<float, true, true, kT, true><<<g, kT, tree_bytes, s>>>(r, nn, tv, st, sp, f, partials, nb);
+    else if (gz)
+      k_bh_iterate<float, true, false, kT, true><<<g, kT, tree_bytes, s>>>(r, nn, tv, st, sp, f, partials, nb);
+    else if (sp.count_visits)
+      k_bh_iterate<float, false, true, kT, true><<<g, kT, tree_bytes, s>>>(r, nn, tv, st, sp, f, partials, nb);
+    else
+      k_bh_iterate<float, false, false, kT, true><<<g, kT, tree_bytes, s>>>(r, nn, tv, st, sp, f, partials, nb);
+    return;
+  }
+  }
   if (gz && sp.count_visits)
     k_bh_iterate<float, true, true, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb);
   else if (gz)

@@ -20,6 +20,31 @@ constexpr int kReduceThreads = 1024;
 // tree), one warp adds the block results in block order.
 constexpr int kRedBlocks = 148;
 constexpr int kRedThreads = 256;
+constexpr int64_t kFuseWarps = 2048;
+
+// Fixed-order block sum of the kPartialStride accumulators of every thread:
+// a shuffle tree per warp, then thread k adds the warps' results in warp
+// order (two barriers in all, where one block_reduce per slot took 2 x 18).
+// out: shared, kPartialStride doubles, valid after the call.
+template <int kThreads>
+__device__ __forceinline__ void block_sum_slots(double (&acc)[kPartialStride], double* out) {
+  __shared__ double ws[kThreads / 32][kPartialStride];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kPartialStride; k++) {
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) ws[w][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kPartialStride) {
+    double v = 0.0;
+    for (int q = 0; q < kThreads / 32; q++) v += ws[q][threadIdx.x];
+    out[threadIdx.x] = v;
+  }
+  __syncthreads();
+}
 
 __global__ void __launch_bounds__(kRedThreads) k_reduce_stage(const double* __restrict__ partials,
                                                              int64_t nwarps,
@@ -37,11 +62,9 @@ __global__ void __launch_bounds__(kRedThreads) k_reduce_stage(const double* __re
     for (int k = 0; k < 17; k++) acc[k] += partials[w * kPartialStride + k];
   }
   for (int64_t w = g0 + threadIdx.x; w < g1; w += kRedThreads) acc[kGpe] += gpe_part[w];
-#pragma unroll 1
-  for (int k = 0; k < kPartialStride; k++) {
-    const double v = block_reduce<0>(acc[k]);
-    if (threadIdx.x == 0) stage[b * kPartialStride + k] = v;
-  }
+  __shared__ double out[kPartialStride];
+  block_sum_slots<kRedThreads>(acc, out);
+  if (threadIdx.x < kPartialStride) stage[b * kPartialStride + threadIdx.x] = out[threadIdx.x];
 }
 
 __global__ void k_reduce_final(const double* __restrict__ stage, int nb, double direct_pairs,
@@ -54,10 +77,9 @@ __global__ void k_reduce_final(const double* __restrict__ stage, int nb, double 
   sums[k] = v;
 }
 
-__global__ void k_update(const double* __restrict__ sums, IterState* st, SimParams sp,
-                         double* rec_delta, double* rec_traj, double* rec_gpe,
-                         long long* rec_inter, long long* rec_visits, int has_gpe) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void update_body(const double* sums, IterState* st, const SimParams& sp,
+                            double* rec_delta, double* rec_traj, double* rec_gpe,
+                            long long* rec_inter, long long* rec_visits, int has_gpe) {
   if (st->done) return;
   const double M = (double)sp.m_total;
   double mu_u[3], mu_w[3], C[9];
@@ -119,6 +141,45 @@ __global__ void k_update(const double* __restrict__ sums, IterState* st, SimPara
   } else if (it + 1 >= sp.max_iters) {
     st->done = 1;
   }
+}
+
+__global__ void k_update(const double* __restrict__ sums, IterState* st, SimParams sp,
+                         double* rec_delta, double* rec_traj, double* rec_gpe,
+                         long long* rec_inter, long long* rec_visits, int has_gpe) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  update_body(sums, st, sp, rec_delta, rec_traj, rec_gpe, rec_inter, rec_visits, has_gpe);
+}
+
+// Small passes (<= kFuseWarps warp partials): the fixed-order reduction in
+// ONE block and the rigid update in the same kernel (one launch per
+// iteration instead of three; configs[0]-sized registrations are bound by
+// these per-iteration latencies).
+constexpr int kFuseThreads = 256;
+__global__ void __launch_bounds__(kFuseThreads) k_reduce_update(
+    const double* __restrict__ partials, int64_t nwarps, const double* __restrict__ gpe_part,
+    int64_t ngwarps, double direct_pairs, double* __restrict__ sums, IterState* st, SimParams sp,
+    double* rec_delta, double* rec_traj, double* rec_gpe, long long* rec_inter,
+    long long* rec_visits, int has_gpe) {
+  double acc[kPartialStride];
+#pragma unroll
+  for (int k = 0; k < kPartialStride; k++) acc[k] = 0.0;
+  for (int64_t w = threadIdx.x; w < nwarps; w += kFuseThreads) {
+#pragma unroll
+    for (int k = 0; k < 17; k++) acc[k] += partials[w * kPartialStride + k];
+  }
+  for (int64_t w = threadIdx.x; w < ngwarps; w += kFuseThreads) acc[kGpe] += gpe_part[w];
+  __shared__ double out[kPartialStride];
+  block_sum_slots<kFuseThreads>(acc, out);
+  if (threadIdx.x < kPartialStride) {
+    const int k = threadIdx.x;
+    double v = out[k];
+    if (direct_pairs >= 0.0 && (k == kAccepted || k == kVisits)) v = direct_pairs;
+    out[k] = v;
+    sums[k] = v;
+  }
+  __syncthreads();
+  if (st && threadIdx.x == 0)  // (st == nullptr: the reduction alone, launch_reduce)
+    update_body(out, st, sp, rec_delta, rec_traj, rec_gpe, rec_inter, rec_visits, has_gpe);
 }
 
 __global__ void k_apply_pending(TemplateView tv, const IterState* __restrict__ st) {
@@ -247,8 +308,28 @@ size_t reduce_stage_doubles() { return (size_t)kRedBlocks * kPartialStride; }
 void launch_reduce(const double* partials, int64_t nwarps, const double* gpe_partials,
                    int64_t ngwarps, double direct_pairs, double* sums, double* stage,
                    cudaStream_t s) {
+  if (nwarps <= kFuseWarps && ngwarps <= kFuseWarps) {  // the fused kernel's order, no update
+    k_reduce_update<<<1, kFuseThreads, 0, s>>>(partials, nwarps, gpe_partials, ngwarps,
+                                               direct_pairs, sums, nullptr, SimParams{}, nullptr,
+                                               nullptr, nullptr, nullptr, nullptr, 0);
+    return;
+  }
   k_reduce_stage<<<kRedBlocks, kRedThreads, 0, s>>>(partials, nwarps, gpe_partials, ngwarps, stage);
   k_reduce_final<<<1, 32, 0, s>>>(stage, kRedBlocks, direct_pairs, sums);
+}
+
+bool reduce_update_fusable(int64_t nwarps, int64_t ngwarps) {
+  return nwarps <= kFuseWarps && ngwarps <= kFuseWarps;
+}
+
+void launch_reduce_update(const double* partials, int64_t nwarps, const double* gpe_partials,
+                          int64_t ngwarps, double direct_pairs, double* sums, IterState* st,
+                          const SimParams& sp, double* rec_delta, double* rec_traj,
+                          double* rec_gpe, long long* rec_inter, long long* rec_visits,
+                          int has_gpe, cudaStream_t s) {
+  k_reduce_update<<<1, kFuseThreads, 0, s>>>(partials, nwarps, gpe_partials, ngwarps,
+                                             direct_pairs, sums, st, sp, rec_delta, rec_traj,
+                                             rec_gpe, rec_inter, rec_visits, has_gpe);
 }
 
 void launch_update(const double* sums, IterState* st, const SimParams& sp, double* rec_delta,
