@@ -112,9 +112,8 @@ __global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32
     nv = o.visits;
     na = o.accepted;
   } else {
-    __shared__ Win64 wins[kT / 32];
-    Trav64Out o = traverse64(tr.a64, tr.b64, n_nodes, y[0], y[1], y[2], __dmul_rn(sp.G, mq),
-                             active, sp.theta2, sp.eps2, &wins[wl], lane);
+    Trav64Out o = traverse64d(tr.a64, tr.b64, n_nodes, y[0], y[1], y[2], __dmul_rn(sp.G, mq),
+                              active, sp.theta2, sp.eps2);
     F[0] = o.fx;
     F[1] = o.fy;
     F[2] = o.fz;
@@ -196,9 +195,8 @@ __global__ void __launch_bounds__(kForceThreads, sizeof(Real) == 4 ? FGA_BHOP32_
       q[2] = qz_[i];
       qm = qm_[i];
     }
-    __shared__ Win64 wins[kWarps];
-    Trav64Out o = traverse64(tr.a64, tr.b64, n_nodes, q[0], q[1], q[2], __dmul_rn(G, qm), active,
-                             theta2, eps2, &wins[wl], lane);
+    Trav64Out o = traverse64d(tr.a64, tr.b64, n_nodes, q[0], q[1], q[2], __dmul_rn(G, qm), active,
+                              theta2, eps2);
     F[0] = o.fx;
     F[1] = o.fy;
     F[2] = o.fz;

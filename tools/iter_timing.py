@@ -21,7 +21,8 @@ dev = torch.device("cuda", 0)
 xt = torch.from_numpy(np.array(x.points)).to(dev)
 yt = torch.from_numpy(np.array(y.points)).to(dev)
 st = torch.cuda.current_stream()
-s = Session(None, None, p, fga.RegisterOptions(compute_gpe=False), stream=st.cuda_stream,
+prec = os.environ.get("FGA_PREC", "fp32")
+s = Session(None, None, p, fga.RegisterOptions(compute_gpe=False, precision=prec), stream=st.cuda_stream,
             device_inputs=(xt.data_ptr(), n, yt.data_ptr(), n))
 for _ in range(3):
     s.forces()
@@ -40,7 +41,7 @@ ms = np.array([a.elapsed_time(b) for a, b in ev])
 res = s.finish()
 inter = res.interactions[3:3 + K].mean()
 line = f"force pass {ms.mean():.3f} ms (min {ms.min():.3f})  {inter / ms.mean() * 1e3:.4g} inter/s"
-if os.environ.get("FGA_ACC", "1") == "1":
+if os.environ.get("FGA_ACC", "1") == "1" and prec == "fp32":
     from oracle import oracle as orc
     xn, yn, mx, my, _ = orc.setup(x.points, y.points)
     ot = orc.tree_build(xn, mx, 20)
@@ -51,4 +52,4 @@ if os.environ.get("FGA_ACC", "1") == "1":
     rel = np.linalg.norm(f - of, axis=1) / np.linalg.norm(of, axis=1)
     line += (f"  | visits equal {np.array_equal(v, ov) and np.array_equal(a, oa)}  rel max "
              f"{rel.max():.2e} p99 {np.quantile(rel, 0.99):.2e}")
-print(os.path.basename(os.environ.get("FGA_LIB_PATH", "libfga.so")), line, flush=True)
+print(os.path.basename(os.environ.get("FGA_LIB_PATH", "libfga.so")), prec, line, flush=True)
