@@ -308,8 +308,14 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     gB = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gB)));
   }
   int lim = fold_limit(0, n_nodes);
+  // kSmem (one latency-bound wave, records in shared memory): the next n is
+  // one vote after the MAC, the other lanes' minimum computed off the chain
+  // (1M, issue-bound: 11.6 -> 13.0 ms, so the REDUX-at-top form stays there;
+  // configs[0]: loop 1.61 -> 1.50 ms)
+  constexpr bool kVote = kSmem;
+  int n = __reduce_min_sync(0xffffffffu, cursor);
   while (true) {
-    const int n = __reduce_min_sync(0xffffffffu, cursor);
+    if (!kVote) n = __reduce_min_sync(0xffffffffu, cursor);
     if (n >= lim) {  // exit, or fold the chunk's partial into the fp64 sum
       if (n >= n_nodes) break;
       if (hs) {
@@ -336,6 +342,8 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     const float4 a = kSmem ? rec->a : __ldg(&rec->a);
     const float4 b = kSmem ? rec->b : __ldg(&rec->b);
     const bool mine = cursor == n;
+    // (kVote) the other lanes' cursors do not move this step
+    const int m_other = kVote ? __reduce_min_sync(0xffffffffu, mine ? INT_MAX : cursor) : 0;
     const float dx = a.x - qx, dy = a.y - qy, dz = a.z - qz;
     float r2, diff, band;
     if constexpr (kStatic) {
@@ -381,6 +389,8 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     }
     const int next = acc ? __float_as_int(b.y) : n + 1;
     cursor = mine ? next : cursor;
+    if (kVote)
+      n = __any_sync(0xffffffffu, mine && !acc) ? n + 1 : min(__float_as_int(b.y), m_other);
   }
   if (kPackable && packed) {
     const unsigned* hcc = hc + 2 * threadIdx.x;
