@@ -338,8 +338,8 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
     TRY(tree_build_dev(S.tree, S.xn.as<double>(), S.mx.as<double>(), n, S.P.max_depth, s));
     S.tree.dim = S.sp.dim;
     if (S.tree.cap_distinct) {
-      set_error("max_depth > 21 with distinct reference points closer than 2^-21 of the box "
-                "(the GPU tree has 21 levels; not built yet)");
+      set_error("max_depth > 42 with distinct reference points closer than 2^-42 of the box "
+                "(the GPU tree has at most 42 levels)");
       return FGA_ERR_UNSUPPORTED;
     }
   }
@@ -1377,8 +1377,8 @@ int fga_tree_build(fga_ctx* c, const double* pts, const double* masses, int64_t 
                      c->stream));
   FGA_CUDA_TRY(cudaStreamSynchronize(c->stream));
   if (c->tree.cap_runs) {  // the exported arrays would lack the chains below level 21
-    set_error("max_depth > 21 with two reference points in one cell of level 21 (the GPU "
-              "tree has 21 levels; not built yet)");
+    set_error("max_depth > 42 with two reference points in one cell of level 42 (the GPU "
+              "tree has at most 42 levels)");
     return FGA_ERR_UNSUPPORTED;
   }
   c->tree.dim = dim;
@@ -1396,8 +1396,8 @@ int fga_tree_build_dev(fga_ctx* c, const double* pts_dev, const double* masses_d
   TRY(tree_build_dev(c->tree, pts_dev, masses_dev, n, max_depth, c->stream));
   c->tree.dim = 3;
   if (c->tree.cap_runs) {
-    set_error("max_depth > 21 with two reference points in one cell of level 21 (the GPU "
-              "tree has 21 levels; not built yet)");
+    set_error("max_depth > 42 with two reference points in one cell of level 42 (the GPU "
+              "tree has at most 42 levels)");
     return FGA_ERR_UNSUPPORTED;
   }
   if (n_nodes) *n_nodes = c->tree.n_nodes;

@@ -23,6 +23,7 @@
 namespace fga {
 
 constexpr int kMaxLevels = 21;  // 3 bits per level in a 64-bit key
+constexpr int kMaxLevelsDeep = 42;  // ... in a 128-bit key (max_depth > 21 builds)
 constexpr int kPartialStride = 18;  // doubles per warp partial (see PartialSlot)
 
 // Slots of a per-warp (and, after reduction, per-iteration) partial record.

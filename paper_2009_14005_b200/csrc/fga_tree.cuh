@@ -31,13 +31,16 @@ struct TreeDev {
   // "which tree is loaded" (the Python BHTree token, the bh_forces_kernel
   // shim's upload key) compare against it (fga_tree_generation)
   uint64_t generation = 0;
-  // max_depth > 21 (kMaxLevels): the tree is built with 21 levels; valid
-  // when no level-21 cell holds two points (the trees are then equal), and
-  // for a registration also when such cells hold only exact duplicates (the
-  // reference's extra single-child chain below them changes visit counts,
-  // never an accepted term: same com, same mass).  Set by tree_build_dev.
+  // max_depth 22..42 builds with 128-bit keys (wide_keys), exactly the
+  // reference's tree.  max_depth > 42 (kMaxLevelsDeep): built with 42
+  // levels; valid when no level-42 cell holds two points (the trees are then
+  // equal), and for a registration also when such cells hold only exact
+  // duplicates (the reference's extra single-child chain below them changes
+  // visit counts, never an accepted term: same com, same mass).  Set by
+  // tree_build_dev.
   int L_requested = 0;
-  bool cap_runs = false;      // some level-21 cell holds >= 2 points
+  bool wide_keys = false;     // L > 21: 128-bit keys (tree.cu K128)
+  bool cap_runs = false;      // some cell at the level cap holds >= 2 points
   bool cap_distinct = false;  // ... of which two are distinct
   const double* pts = nullptr;     // (n,3) device, not owned
   const double* masses = nullptr;  // (n,) device, not owned

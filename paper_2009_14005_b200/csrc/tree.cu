@@ -151,6 +151,27 @@ __device__ __forceinline__ unsigned long long spread3(unsigned long long v) {
   return v;
 }
 
+// Keys: 3 bits per level, level 1 most significant, in a 64-bit word for
+// L <= 21 (kMaxLevels) or a 128-bit one for L <= 42 (kMaxLevelsDeep: the
+// reference's max_depth beyond 21, bhtree.py:89).
+typedef unsigned long long K64;
+typedef unsigned __int128 K128;
+__device__ __forceinline__ int kclz(K64 x) { return __clzll((long long)x); }
+__device__ __forceinline__ int kclz(K128 x) {
+  const K64 hi = (K64)(x >> 64);
+  return hi ? __clzll((long long)hi) : 64 + __clzll((long long)(K64)x);
+}
+template <class K>
+__device__ __forceinline__ int klevels(K a, K b, int L) {  // common levels of two keys
+  const K x = a ^ b;
+  if (x == (K)0) return L;
+  return (kclz(x) - (8 * (int)sizeof(K) - 3 * L)) / 3;
+}
+template <class K>
+__device__ __forceinline__ K klow(int bits) {
+  return bits >= 8 * (int)sizeof(K) ? ~(K)0 : (((K)1 << bits) - (K)1);
+}
+
 __device__ __forceinline__ bool fast_axis(double x, double lo0, double scale, double gf, int L,
                                           unsigned long long& q) {
   if (!(scale > 0.0)) {  // flat axis (hi == lo, e.g. a 2-D cloud's z): every split is lo,
@@ -166,22 +187,28 @@ __device__ __forceinline__ bool fast_axis(double x, double lo0, double scale, do
   return true;
 }
 
-__device__ __forceinline__ unsigned long long point_key(const double p[3],
-                                                        const double* __restrict__ box, int L) {
+template <class K>
+__device__ __forceinline__ K point_key(const double p[3], const double* __restrict__ box, int L) {
   const double guard = box[9];
   unsigned long long q[3];
   bool fast = true;
 #pragma unroll
   for (int k = 0; k < 3; k++)
     fast = fast_axis(p[k], box[k], box[6 + k], guard * box[6 + k], L, q[k]) && fast;
-  if (fast) return (spread3(q[0]) << 2) | (spread3(q[1]) << 1) | spread3(q[2]);
+  if (fast) {
+    if constexpr (sizeof(K) == 8) return (spread3(q[0]) << 2) | (spread3(q[1]) << 1) | spread3(q[2]);
+    // 42 bits per axis: the top 21 levels' interleave above the low 63 bits
+    const K hi = (spread3(q[0] >> 21) << 2) | (spread3(q[1] >> 21) << 1) | spread3(q[2] >> 21);
+    const K lo = (spread3(q[0]) << 2) | (spread3(q[1]) << 1) | spread3(q[2]);
+    return (hi << 63) | lo;
+  }
   double lo[3], hi[3];
 #pragma unroll
   for (int k = 0; k < 3; k++) {
     lo[k] = box[k];
     hi[k] = box[3 + k];
   }
-  unsigned long long key = 0;
+  K key = 0;
   for (int l = 0; l < L; l++) {
     unsigned digit = 0;
 #pragma unroll
@@ -191,7 +218,7 @@ __device__ __forceinline__ unsigned long long point_key(const double p[3],
       digit = (digit << 1) | (up ? 1u : 0u);
       if (up) lo[k] = c; else hi[k] = c;
     }
-    key = (key << 3) | digit;
+    key = (key << 3) | (K)digit;
   }
   return key;
 }
@@ -200,9 +227,10 @@ __device__ __forceinline__ unsigned long long point_key(const double p[3],
 // (x, y, z, m) record.  The sort runs on the top 32 key bits (keys32, 4 radix
 // passes instead of 8); keys64 (the full key) is written only for the
 // fallback full sort.
+template <class K>
 __global__ void k_keys(const double* __restrict__ pts, const double* __restrict__ masses, int64_t n,
                        const double* __restrict__ box, int L, int shift,
-                       unsigned* __restrict__ keys32, unsigned long long* __restrict__ keys64,
+                       unsigned* __restrict__ keys32, K* __restrict__ keys64,
                        int* __restrict__ idx, double4* __restrict__ packed) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -210,7 +238,7 @@ __global__ void k_keys(const double* __restrict__ pts, const double* __restrict_
 #pragma unroll
   for (int k = 0; k < 3; k++) p[k] = pts[i * 3 + k];
   packed[i] = make_double4(p[0], p[1], p[2], masses[i]);  // one 32 B record per point
-  const unsigned long long key = point_key(p, box, L);
+  const K key = point_key<K>(p, box, L);
   if (keys64) keys64[i] = key;
   else keys32[i] = (unsigned)(key >> shift);
   idx[i] = (int)i;
@@ -219,16 +247,17 @@ __global__ void k_keys(const double* __restrict__ pts, const double* __restrict_
 // Sorted copy of the points (one random gather of the packed records) and,
 // when the sort ran on the top key bits only, the full key recomputed from
 // the point (no second gather).
+template <class K>
 __global__ void k_gather_sorted(const double4* __restrict__ packed, const int* __restrict__ idx,
                                 int64_t n, const double* __restrict__ box, int L,
-                                double4* __restrict__ sp, unsigned long long* __restrict__ keys) {
+                                double4* __restrict__ sp, K* __restrict__ keys) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double4 v = packed[idx[i]];
   sp[i] = v;
   if (keys) {
     const double p[3] = {v.x, v.y, v.z};
-    keys[i] = point_key(p, box, L);
+    keys[i] = point_key<K>(p, box, L);
   }
 }
 
@@ -237,8 +266,9 @@ __global__ void k_gather_sorted(const double4* __restrict__ packed, const int* _
 // keep index order as the reference's partition does).  Runs longer than
 // kRun set *overflow and the build falls back to the full 64-bit sort.
 constexpr int kRun = 64;
+template <class K>
 __global__ void k_fixup_runs(const unsigned* __restrict__ hi, int64_t n,
-                             unsigned long long* __restrict__ key, int* __restrict__ idx,
+                             K* __restrict__ key, int* __restrict__ idx,
                              double4* __restrict__ sp, int* __restrict__ overflow) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -251,7 +281,7 @@ __global__ void k_fixup_runs(const unsigned* __restrict__ hi, int64_t n,
       return;
     }
   for (int a = 1; a < len; a++) {
-    const unsigned long long kk = key[i + a];
+    const K kk = key[i + a];
     int b = a - 1;
     if (key[i + b] <= kk) continue;
     const int id = idx[i + a];
@@ -276,15 +306,16 @@ __device__ __forceinline__ int chain_end(int s, int cn, int L) { return max(s, m
 
 // c_i for i in [0, N] (c_0 = c_N = -1) and the number of nodes each point
 // starts (count[N] = 0, so the exclusive scan's last entry is the node count).
-__global__ void k_count(const unsigned long long* __restrict__ keys, int64_t n, int L,
+template <class K>
+__global__ void k_count(const K* __restrict__ keys, int64_t n, int L,
                         signed char* __restrict__ clev, int* __restrict__ count) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i > n) return;
-  const int c = (i == 0 || i == n) ? -1 : common_levels(keys[i - 1], keys[i], L);
+  const int c = (i == 0 || i == n) ? -1 : klevels(keys[i - 1], keys[i], L);
   clev[i] = (signed char)c;
   int cnt = 0;
   if (i < n) {
-    const int cn = (i + 1 == n) ? -1 : common_levels(keys[i], keys[i + 1], L);
+    const int cn = (i + 1 == n) ? -1 : klevels(keys[i], keys[i + 1], L);
     const int s = c + 1;
     if (s <= L) cnt = chain_end(s, cn, L) - s + 1;
   }
@@ -293,8 +324,9 @@ __global__ void k_count(const unsigned long long* __restrict__ keys, int64_t n, 
 
 // first j in [from, n) with keys[j] > bound (keys sorted): galloping search
 // from `from` (subtree ends are near the start for all but the top levels)
-__device__ __forceinline__ int64_t upper_bound_gallop(const unsigned long long* keys, int64_t from,
-                                                      int64_t n, unsigned long long bound) {
+template <class K>
+__device__ __forceinline__ int64_t upper_bound_gallop(const K* keys, int64_t from, int64_t n,
+                                                      K bound) {
   int64_t lo = from, hi = n, step = 1;
   while (true) {
     const int64_t j = lo + step - 1;
@@ -315,7 +347,8 @@ __device__ __forceinline__ int64_t upper_bound_gallop(const unsigned long long* 
 
 // One bbox split step of the reference's recursion (bhtree.py:90-103) along
 // the key digit of level `lev`.
-__device__ __forceinline__ void bbox_step(unsigned long long key, int lev, int L, double lo[3],
+template <class K>
+__device__ __forceinline__ void bbox_step(K key, int lev, int L, double lo[3],
                                           double hi[3]) {
   const unsigned digit = (unsigned)(key >> (3 * (L - lev))) & 7u;
 #pragma unroll
@@ -520,18 +553,20 @@ __device__ __forceinline__ Q4 e_at(const unsigned long long (*E)[kST + 1], int p
 // position 0 has nodes.  One node per thread: bbox replay from the shared
 // level-lca box (bhtree.py:90-103) -> length; end = the next B_l bit ->
 // skip = offset[end] and the sums E[end] - E[j]; records.
-__global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long long* __restrict__ keys,
+template <class K>
+__global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const K* __restrict__ keys,
                                                      int64_t n, int L,
                                                      const signed char* __restrict__ clev,
                                                      const int* __restrict__ offset,
                                                      const double* __restrict__ box,
                                                      const double4* __restrict__ sp,
                                                      TreeRecords r, Cross cr, int nb) {
-  __shared__ unsigned mB[kMaxLevels + 2][kSW];
-  __shared__ unsigned nzB[kMaxLevels + 2];
+  constexpr int kLv = sizeof(K) == 8 ? kMaxLevels : kMaxLevelsDeep;
+  __shared__ unsigned mB[kLv + 2][kSW];
+  __shared__ unsigned nzB[kLv + 2];
   __shared__ int offs[kST + 1];
   __shared__ signed char cs[kST + 1];
-  __shared__ unsigned long long skey[kST];
+  __shared__ K skey[kST];
   // SoA in shared memory (64-bit words per thread: no bank conflicts)
   __shared__ double P[4][kST];                     // the block's points x, y, z, m
   __shared__ unsigned long long E[8][kST + 1];     // prefix sums: limb 2c = low, 2c+1 = high
@@ -547,7 +582,7 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
   const double s64 = box[12], sinv = box[13];
   cs[t] = i <= n ? clev[i] : (signed char)-1;
   offs[t] = i <= n ? offset[i] : nn;
-  skey[t] = i < n ? keys[i] : 0ull;
+  skey[t] = i < n ? keys[i] : (K)0;
   const double4 pv = i < n ? sp[i] : make_double4(0.0, 0.0, 0.0, 0.0);
   P[0][t] = pv.x;
   P[1][t] = pv.y;
@@ -579,8 +614,8 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
       for (int c = 0; c < 8; c++) E[c][0] = 0ull;
   }
   __syncthreads();  // cs, offs, skey, s_maxe
-  const unsigned long long k0 = skey[0];
-  const int lca = last > B0 ? common_levels(k0, skey[last - B0], L) : L;
+  const K k0 = skey[0];
+  const int lca = last > B0 ? klevels(k0, skey[last - B0], L) : L;
   const int c = cs[t], c0 = cs[0], cend = cs[kST];
   const bool has = i < n && c + 1 <= L;
   const int s = c + 1, e = has ? chain_end(s, cs[t + 1], L) : -1;
@@ -650,7 +685,7 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
     }
     const int sj = cs[j] + 1, ej = chain_end(sj, cs[j + 1], L);
     const int l = sj + (x - offs[j]);
-    const unsigned long long key = skey[j];
+    const K key = skey[j];
     double bl[3], bh[3];
     int lv;
     if (l <= lca) {  // (position 0 only: the other points start below lca)
@@ -681,7 +716,7 @@ __global__ void __launch_bounds__(kST, kSTBlocks) k_subtrees(const unsigned long
                    __ddiv_rn(__dadd_rn(0.0, __dmul_rn(v.y, v.w)), v.w),
                    __ddiv_rn(__dadd_rn(0.0, __dmul_rn(v.z, v.w)), v.w), v.w);
       } else {
-        const int64_t end = ej == 0 ? n : upper_bound_gallop(keys, gi + 1, n, key | low_mask(3 * (L - ej)));
+        const int64_t end = ej == 0 ? n : upper_bound_gallop(keys, gi + 1, n, key | klow<K>(3 * (L - ej)));
         u128 a[4] = {0, 0, 0, 0};
         for (int64_t q = gi; q < end; q++) {
           u128 tq[4];
@@ -773,8 +808,9 @@ __device__ __forceinline__ void block_prefix(const Cross& cr, int nb, int b, u12
 // One thread per (level, block) with an owned crossing node: its end (the
 // first later key outside its prefix), its exact sums from the block prefix
 // sums, and its records.
+template <class K>
 __global__ void __launch_bounds__(256) k_crossing(int L, int nb, int64_t n,
-                                                  const unsigned long long* __restrict__ keys,
+                                                  const K* __restrict__ keys,
                                                   const int* __restrict__ offset,
                                                   const double* __restrict__ box, Cross cr,
                                                   TreeRecords r) {
@@ -784,7 +820,7 @@ __global__ void __launch_bounds__(256) k_crossing(int L, int nb, int64_t n,
   const int x = cr.prx[l * nb + b];
   if (x < 0) return;
   const int64_t i = cr.prs[l * nb + b];
-  const int64_t end = l == 0 ? n : upper_bound_gallop(keys, i + 1, n, keys[i] | low_mask(3 * (L - l)));
+  const int64_t end = l == 0 ? n : upper_bound_gallop(keys, i + 1, n, keys[i] | klow<K>(3 * (L - l)));
   const int bend = (int)(end / kST), pe = (int)(end - (int64_t)bend * kST);
   u128 ge[4], gb[4], a[4];
   block_prefix(cr, nb, bend, ge);
@@ -802,8 +838,8 @@ __global__ void __launch_bounds__(256) k_crossing(int L, int nb, int64_t n,
 }
 
 // first p in [0, to) with keys[p] >= bound, galloping backwards from `to`
-__device__ __forceinline__ int64_t lower_bound_gallop(const unsigned long long* keys, int64_t to,
-                                                      unsigned long long bound) {
+template <class K>
+__device__ __forceinline__ int64_t lower_bound_gallop(const K* keys, int64_t to, K bound) {
   int64_t lo = 0, hi = to, step = 1;
   while (true) {
     const int64_t j = hi - step;
@@ -828,7 +864,8 @@ __device__ __forceinline__ int64_t lower_bound_gallop(const unsigned long long* 
 // itself in its parent's child slot (parent: the chain's previous node, or
 // found by a backwards search for the start of the parent's key prefix).
 // children must be -1 filled.  Export only, not on the registration path.
-__global__ void __launch_bounds__(256) k_export(const unsigned long long* __restrict__ keys,
+template <class K>
+__global__ void __launch_bounds__(256) k_export(const K* __restrict__ keys,
                                                 int64_t n, int L,
                                                 const signed char* __restrict__ clev,
                                                 const int* __restrict__ offset,
@@ -844,7 +881,7 @@ __global__ void __launch_bounds__(256) k_export(const unsigned long long* __rest
   if (s > L) return;
   const int e = chain_end(s, cn, L);
   const int nn = offset[n];
-  const unsigned long long k = keys[i];
+  const K k = keys[i];
   const int base = offset[i];
   double lo[3], hi[3];
 #pragma unroll
@@ -858,7 +895,7 @@ __global__ void __launch_bounds__(256) k_export(const unsigned long long* __rest
     int64_t end;
     if (l == 0) end = n;
     else if (l > cn) end = i + 1;
-    else end = upper_bound_gallop(keys, i + 1, n, k | low_mask(3 * (L - l)));
+    else end = upper_bound_gallop(keys, i + 1, n, k | klow<K>(3 * (L - l)));
     const int64_t x = base + (l - s);
     const double4 v = a64[l + nn - offset[end]];
     if (mass) mass[x] = v.w;
@@ -879,7 +916,7 @@ __global__ void __launch_bounds__(256) k_export(const unsigned long long* __rest
       if (l > s) {
         parent = x - 1;
       } else {
-        const int64_t p = lower_bound_gallop(keys, i, k & ~low_mask(3 * (L - l + 1)));
+        const int64_t p = lower_bound_gallop(keys, i, k & ~klow<K>(3 * (L - l + 1)));
         parent = offset[p] + (l - 1 - ((int)clev[p] + 1));
       }
       const unsigned slot = (unsigned)(k >> (3 * (L - l))) & 7u;
@@ -902,6 +939,10 @@ __global__ void k_cap_runs(const double4* __restrict__ sp, const signed char* __
 }
 
 // ------------------------------------------------------------------ host side
+template <class K>
+static int tree_build_k(TreeDev& T, const double* pts_dev, const double* masses_dev, int64_t n,
+                        int L, cudaStream_t st);
+
 int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, int64_t n, int L,
                    cudaStream_t st) {
   T.generation++;  // any (re)build, even a failed one, invalidates cached host views
@@ -919,7 +960,15 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   }
   T.L_requested = L;
   T.cap_runs = T.cap_distinct = false;
-  if (L > kMaxLevels) L = kMaxLevels;  // see TreeDev::L_requested
+  if (L > kMaxLevelsDeep) L = kMaxLevelsDeep;  // see TreeDev::L_requested
+  T.wide_keys = L > kMaxLevels;  // 128-bit keys beyond 21 levels
+  return T.wide_keys ? tree_build_k<K128>(T, pts_dev, masses_dev, n, L, st)
+                     : tree_build_k<K64>(T, pts_dev, masses_dev, n, L, st);
+}
+
+template <class K>
+static int tree_build_k(TreeDev& T, const double* pts_dev, const double* masses_dev, int64_t n,
+                        int L, cudaStream_t st) {
   T.n_points = n;
   T.L = L;
   T.pts = pts_dev;
@@ -936,7 +985,7 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   // 24 bits first only for small clouds (dense clusters of a large cloud
   // overflow the runs).
   int top_bits = n <= (1 << 22) ? 24 : 32;
-  FGA_CUDA_TRY(T.keys.reserve(sizeof(unsigned long long) * n));
+  FGA_CUDA_TRY(T.keys.reserve(sizeof(K) * n));
   FGA_CUDA_TRY(T.keys32_in.reserve(sizeof(unsigned) * n));
   FGA_CUDA_TRY(T.keys32.reserve(sizeof(unsigned) * n));
   FGA_CUDA_TRY(T.idx_in.reserve(sizeof(int) * n));
@@ -952,8 +1001,8 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
     size_t b32 = 0, b64 = 0, bscan = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b32, T.keys32_in.as<unsigned>(), T.keys32.as<unsigned>(),
                                     T.idx_in.as<int>(), T.idx.as<int>(), (int)n, 0, 32, st);
-    cub::DeviceRadixSort::SortPairs(nullptr, b64, (const unsigned long long*)nullptr,
-                                    (unsigned long long*)nullptr, T.idx_in.as<int>(),
+    cub::DeviceRadixSort::SortPairs(nullptr, b64, (const K*)nullptr, (K*)nullptr,
+                                    T.idx_in.as<int>(),
                                     T.idx.as<int>(), (int)n, 0, 3 * L, st);
     cub::DeviceScan::ExclusiveSum(nullptr, bscan, (int*)nullptr, (int*)nullptr, (int)(n + 1), st);
     FGA_CUDA_TRY(T.cub_tmp.reserve(std::max(std::max(b32, b64), bscan)));
@@ -962,7 +1011,7 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
   auto sort_top = [&](int bits) -> int {
     const int shift = std::max(0, 3 * L - bits);
     FGA_CUDA_TRY(cudaMemsetAsync(overflow, 0, sizeof(int), st));
-    k_keys<<<blocks_for(n), kThreads, 0, st>>>(pts_dev, masses_dev, n, T.box.as<double>(), L, shift,
+    k_keys<K><<<blocks_for(n), kThreads, 0, st>>>(pts_dev, masses_dev, n, T.box.as<double>(), L, shift,
                                                T.keys32_in.as<unsigned>(), nullptr,
                                                T.idx_in.as<int>(), T.packed.as<double4>());
     tmp_bytes = T.cub_tmp.bytes;
@@ -970,19 +1019,19 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
                                                  T.keys32.as<unsigned>(), T.idx_in.as<int>(),
                                                  T.idx.as<int>(), (int)n, 0, std::min(bits, 3 * L),
                                                  st));
-    k_gather_sorted<<<blocks_for(n), kThreads, 0, st>>>(T.packed.as<double4>(), T.idx.as<int>(), n,
+    k_gather_sorted<K><<<blocks_for(n), kThreads, 0, st>>>(T.packed.as<double4>(), T.idx.as<int>(), n,
                                                         T.box.as<double>(), L, T.sp.as<double4>(),
-                                                        T.keys.as<unsigned long long>());
+                                                        T.keys.as<K>());
     if (shift > 0)
       k_fixup_runs<<<blocks_for(n), kThreads, 0, st>>>(T.keys32.as<unsigned>(), n,
-                                                       T.keys.as<unsigned long long>(),
+                                                       T.keys.as<K>(),
                                                        T.idx.as<int>(), T.sp.as<double4>(), overflow);
     return FGA_OK;
   };
   TRY_RC(sort_top(top_bits));
   // c_i, node counts, preorder offsets (rerun after a fallback)
   auto levels = [&]() -> int {
-    k_count<<<blocks_for(n + 1), kThreads, 0, st>>>(T.keys.as<unsigned long long>(), n, L,
+    k_count<<<blocks_for(n + 1), kThreads, 0, st>>>(T.keys.as<K>(), n, L,
                                                     T.clev.as<signed char>(), T.count.as<int>());
     size_t sb = T.cub_tmp.bytes;
     FGA_CUDA_TRY(cub::DeviceScan::ExclusiveSum(T.cub_tmp.p, sb, T.count.as<int>(),
@@ -1008,15 +1057,15 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
     TRY_RC(fetch());
   }
   if (ovf) {  // a long run of equal top bits: full 64-bit sort
-    FGA_CUDA_TRY(T.keys_in.reserve(sizeof(unsigned long long) * n));
-    k_keys<<<blocks_for(n), kThreads, 0, st>>>(pts_dev, masses_dev, n, T.box.as<double>(), L, 0,
-                                               nullptr, T.keys_in.as<unsigned long long>(),
+    FGA_CUDA_TRY(T.keys_in.reserve(sizeof(K) * n));
+    k_keys<K><<<blocks_for(n), kThreads, 0, st>>>(pts_dev, masses_dev, n, T.box.as<double>(), L, 0,
+                                               nullptr, T.keys_in.as<K>(),
                                                T.idx_in.as<int>(), T.packed.as<double4>());
     tmp_bytes = T.cub_tmp.bytes;
     FGA_CUDA_TRY(cub::DeviceRadixSort::SortPairs(
-        T.cub_tmp.p, tmp_bytes, T.keys_in.as<unsigned long long>(), T.keys.as<unsigned long long>(),
+        T.cub_tmp.p, tmp_bytes, T.keys_in.as<K>(), T.keys.as<K>(),
         T.idx_in.as<int>(), T.idx.as<int>(), (int)n, 0, 3 * L, st));
-    k_gather_sorted<<<blocks_for(n), kThreads, 0, st>>>(T.packed.as<double4>(), T.idx.as<int>(), n,
+    k_gather_sorted<K><<<blocks_for(n), kThreads, 0, st>>>(T.packed.as<double4>(), T.idx.as<int>(), n,
                                                         T.box.as<double>(), L, T.sp.as<double4>(),
                                                         nullptr);
     TRY_RC(levels());
@@ -1050,19 +1099,19 @@ int tree_build_dev(TreeDev& T, const double* pts_dev, const double* masses_dev, 
     cr.prx = (int*)q; q += sizeof(int) * ncr;
     cr.prs = (int*)q;
   }
-  k_subtrees<<<nbs, kST, 0, st>>>(T.keys.as<unsigned long long>(), n, L, T.clev.as<signed char>(),
+  k_subtrees<<<nbs, kST, 0, st>>>(T.keys.as<K>(), n, L, T.clev.as<signed char>(),
                                   T.offset.as<int>(), T.box.as<double>(), T.sp.as<double4>(),
                                   T.records(), cr, nbs);
   if (nbs > 1) {
     k_tscan1<<<nc, kTScan, 0, st>>>(nbs, cr);
     k_tscan2<<<1, kTScan, 0, st>>>(nc, cr);
-    k_crossing<<<(int)((ncr + 255) / 256), 256, 0, st>>>(L, nbs, n, T.keys.as<unsigned long long>(),
+    k_crossing<<<(int)((ncr + 255) / 256), 256, 0, st>>>(L, nbs, n, T.keys.as<K>(),
                                                          T.offset.as<int>(), T.box.as<double>(), cr,
                                                          T.records());
   }
   FGA_CUDA_TRY(cudaGetLastError());
   T.exportable = true;
-  if (T.L_requested > kMaxLevels) {  // cells at the 21-level cap: one sync, rare path
+  if (T.L_requested > L) {  // cells at the 42-level cap: one sync, rare path
     FGA_CUDA_TRY(cudaMemsetAsync(T.flags.as<int>() + 1, 0, sizeof(int), st));
     k_cap_runs<<<blocks_for(n), kThreads, 0, st>>>(T.sp.as<double4>(), T.clev.as<signed char>(), n,
                                                    L, T.flags.as<int>() + 1);
@@ -1120,12 +1169,15 @@ int tree_export_host(TreeDev& T, cudaStream_t st, int64_t* children, double* com
   double* d_bmin = (double*)p; p += sizeof(double) * 3 * nn;
   double* d_bmax = (double*)p;
   if (children) FGA_CUDA_TRY(cudaMemsetAsync(d_children, 0xff, sizeof(long long) * 8 * nn, st));
-  k_export<<<blocks_for(T.n_points), 256, 0, st>>>(
-      T.keys.as<unsigned long long>(), T.n_points, T.L, T.clev.as<signed char>(),
-      T.offset.as<int>(), T.box.as<double>(), T.a64.as<double4>(),
-      children ? d_children : nullptr, com ? d_com : nullptr, mass ? d_mass : nullptr,
-      length ? d_len : nullptr, occupancy ? d_occ : nullptr, depth ? d_depth : nullptr,
-      bmin ? d_bmin : nullptr, bmax ? d_bmax : nullptr);
+  auto exp = [&](auto* keys) {
+    k_export<<<blocks_for(T.n_points), 256, 0, st>>>(
+        keys, T.n_points, T.L, T.clev.as<signed char>(), T.offset.as<int>(), T.box.as<double>(),
+        T.a64.as<double4>(), children ? d_children : nullptr, com ? d_com : nullptr,
+        mass ? d_mass : nullptr, length ? d_len : nullptr, occupancy ? d_occ : nullptr,
+        depth ? d_depth : nullptr, bmin ? d_bmin : nullptr, bmax ? d_bmax : nullptr);
+  };
+  if (T.wide_keys) exp(T.keys.as<K128>());
+  else exp(T.keys.as<K64>());
   FGA_CUDA_TRY(cudaGetLastError());
 #define CP(dst, src, cnt)                                                                 \
   if (dst) FGA_CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(double) * (cnt), cudaMemcpyDeviceToHost, st));
