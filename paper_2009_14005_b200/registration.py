@@ -156,13 +156,14 @@ class BatchResult:
 
 
 def register_batch(pairs, params: FgaParams | None = None,
-                   options: RegisterOptions | None = None) -> BatchResult:
+                   options: RegisterOptions | None = None,
+                   workers: int | None = None) -> BatchResult:
     """register(x, y) for many independent (x, y) pairs: every pair the
     persistent batched kernel takes (D = 3, <= 8192 points per cloud, FP32
     forces, NIV or external masses, max_depth <= 21; csrc/batched.cu) runs in
     ONE launch, the others -- and any pair the kernel reports as over its
-    limits (e.g. a node cap) -- through register() one by one, so every pair
-    gets the result register() gives it.  External weights in
+    limits (e.g. a node cap) -- through register() on up to `workers` host
+    threads (default 4), so every pair gets the result register() gives it.  External weights in
     options.x_weights / y_weights must be lists (one array per pair); per-pair
     failures are reported in ``errors`` (registration.py:192-200)."""
     params = params or default_params()
@@ -194,7 +195,8 @@ def register_batch(pairs, params: FgaParams | None = None,
             inter[k], status[k] = br.interactions[j], br.status[j]
     kset = set(in_kernel)
     rest = [k for k in range(P) if k not in kset or status[k] == N.FGA_ERR_UNSUPPORTED]
-    for k in rest:
+
+    def one(k):
         x, y = pairs[k]
         o = RegisterOptions(**{**options.__dict__,
                                "x_weights": None if options.x_weights is None else
@@ -203,12 +205,24 @@ def register_batch(pairs, params: FgaParams | None = None,
                                options.y_weights[k]})
         try:
             r = register(x, y, params=params, options=o)
-            results[k], errors[k] = r, None
-            inter[k] = int(r.interactions.sum())
-            status[k] = 0
+            return r, None, int(r.interactions.sum()), 0
         except GravregError as e:
-            results[k], errors[k] = None, e
-            status[k] = N.FGA_ERR_UNSUPPORTED if isinstance(e, DeviceError) else N.FGA_ERR_INVALID
+            return (None, e, 0,
+                    N.FGA_ERR_UNSUPPORTED if isinstance(e, DeviceError) else N.FGA_ERR_INVALID)
+
+    # the pairs the kernel does not take run through register() on up to
+    # `workers` host threads, each with its own context and stream (one
+    # pair's setup and tree build overlap another's iterations; results are
+    # register()'s, whatever the thread)
+    n_workers = min(workers or 4, len(rest))
+    if n_workers > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=n_workers) as pool:
+            outs = list(pool.map(one, rest))
+    else:
+        outs = [one(k) for k in rest]
+    for k, (r, e, it, st) in zip(rest, outs):
+        results[k], errors[k], inter[k], status[k] = r, e, it, st
     return BatchResult(results, errors, inter, status)
 
 
