@@ -928,6 +928,7 @@ constexpr int kWT = 128;
 template <bool kGuardZero>
 __global__ void __launch_bounds__(kWT, FGA_WIDE_TPS / kWT) k_wide_forces(BatchArgs a, int cur) {
   __shared__ double hs[3 * kWT];  // the lanes' fp64 fold sums
+  __shared__ double qsh[3 * kWT];  // ... and fp64 queries (the exact re-check)
   const int lane = threadIdx.x & 31;
   const int n_active = a.wide.counts[cur];
   const int chunks = a.wide.chunks;
@@ -978,13 +979,24 @@ __global__ void __launch_bounds__(kWT, FGA_WIDE_TPS / kWT) k_wide_forces(BatchAr
     // is re-read afterwards, L1/L2-resident): otherwise the compiler keeps
     // the doubles and re-converts them (F2F) inside the loop
     asm volatile("" : "+f"(qxf), "+f"(qyf), "+f"(qzf));
+    {
+      double* q = qsh + 3 * threadIdx.x;
+      q[0] = active ? px[i] : 0.0;
+      q[1] = active ? py[i] : 0.0;
+      q[2] = active ? pz[i] : 0.0;
+    }
     float gA, gB;
     guard_coeffs(fmaxf(fabsf(qxf), fmaxf(fabsf(qyf), fabsf(qzf))), st->cmag, a.theta2f, gA, gB);
     const size_t cap = a.node_cap;
+    // the pair's record base, formed once: left to itself the compiler
+    // re-derives pi * cap * 32 + base on the uniform datapath at every
+    // traversal step (8 issue slots per step)
+    const float4* c32 = a.wide.c32 + (size_t)pi * cap * 2;
+    asm volatile("" : "+l"(c32));
     const Trav32Out o = traverse32d<kGuardZero, false, true>(
-        a.wide.c32 + (size_t)pi * cap * 2, a.wide.a64 + (size_t)pi * cap,
-        a.wide.b64 + (size_t)pi * cap, (int)st->n_nodes, qxf, qyf, qzf, active, a.theta2f,
-        a.theta2, a.eps2f, px, py, pz, m, hs, gA, gB, i);
+        c32, a.wide.a64 + (size_t)pi * cap, a.wide.b64 + (size_t)pi * cap, (int)st->n_nodes, qxf,
+        qyf, qzf, active, a.theta2f, a.theta2, a.eps2f, nullptr, nullptr, nullptr, m, hs, gA, gB,
+        -1, nullptr, qsh);
     Partial p;
     partial_zero(p);
     if (active) {

@@ -283,7 +283,10 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
                                                  const double* qpz, int64_t m_queries,
                                                  double* hs = nullptr, float gA = 0.f,
                                                  float gB = 0.f, int64_t qidx = -1,
-                                                 unsigned* hc = nullptr) {
+                                                 unsigned* hc = nullptr,
+                                                 const double* qsh = nullptr) {
+  // qsh (optional): the lanes' fp64 queries in shared memory (3 per thread)
+  // for the exact re-check, instead of pointers + index held across the loop
   // hs (optional): the block's fp64 fold sums in shared memory, 3 per thread
   // (hs[3 threadIdx.x ..]), so they hold no registers across the loop (folds
   // are rare; the address is re-derived at each fold)
@@ -362,9 +365,15 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
       // this lane's query, re-derived here (query i = global thread index;
       // inactive lanes read the last query and ignore the result) so no
       // register holds it across the loop
-      int64_t qs = qidx >= 0 ? qidx : blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-      qs = qs < m_queries ? qs : m_queries - 1;
-      const bool e = mac_exact(A64, B64, n, qpx[qs], qpy[qs], qpz[qs], theta2_64);
+      bool e;
+      if (qsh) {
+        const double* q = qsh + 3 * threadIdx.x;
+        e = mac_exact(A64, B64, n, q[0], q[1], q[2], theta2_64);
+      } else {
+        int64_t qs = qidx >= 0 ? qidx : blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        qs = qs < m_queries ? qs : m_queries - 1;
+        e = mac_exact(A64, B64, n, qpx[qs], qpy[qs], qpz[qs], theta2_64);
+      }
       acc = near ? e : acc;
     }
     const bool take = mine && acc;
