@@ -112,6 +112,17 @@ def config_dict(args, n_ref, n_tpl, tree_nodes, world):
             "l2": "flushed between timed steps (256 MiB write, outside the events)"}
 
 
+def host_threads():
+    """Host threads for the CPU legs: every core this process may run on,
+    passed explicitly to the oracle's OpenMP regions (torch.distributed.run
+    sets OMP_NUM_THREADS=1 in every rank, which would otherwise leave the
+    reference arm on one core at N > 1)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return os.cpu_count() or 1
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -972,7 +983,7 @@ def run_configs0():
         r = fga.register(x, y, params=p)
         gw.append(time.perf_counter() - t0)
         its.append(r.iterations)
-    threads = orc.max_threads()
+    threads = host_threads()
     cw1, cwn, oits = [], [], []
     for x, y in pairs:
         t0 = time.perf_counter()
@@ -1008,7 +1019,7 @@ def cpu_baseline(args, x, y, sample):
     tree = orc.tree_build(xn, mx, 20)
     build_s = time.perf_counter() - t0
     idx = np.random.default_rng(0).choice(len(yn), size=min(sample, len(yn)), replace=False)
-    threads = orc.max_threads()
+    threads = host_threads()
     t0 = time.perf_counter()
     _, visits, acc = orc.bh_forces(tree, yn[idx], my[idx], args.theta, bp.G, bp.epsilon, threads)
     dt = time.perf_counter() - t0
@@ -1046,7 +1057,7 @@ def run_reference(args, rank):
     bp = bench_params(args)
     xn, yn, mx, my, _ = orc.setup(x.points, y.points)
     tree = orc.tree_build(xn, mx, 20)
-    threads = orc.max_threads()
+    threads = host_threads()
     sample = min(16384, len(yn))
     rng = np.random.default_rng(1)
 
@@ -1094,16 +1105,27 @@ def main():
         if line is not None:
             print(json.dumps(line), flush=True)
         return
+    # FGA_BENCH_FUNCTIONAL=1: a functional check of the N-rank code path on a
+    # one-GPU box -- every rank on cuda:0, gloo collectives; its numbers are
+    # not measurements (the ranks share one GPU)
+    functional = os.environ.get("FGA_BENCH_FUNCTIONAL") == "1"
+    if functional:
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
-        # NCCL init logging: the communicator's rank count and transport are
-        # in the log (stderr), so an N-rank run is verifiable
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            # NCCL init logging: the communicator's rank count and transport
+            # are in the log (stderr), so an N-rank run is verifiable
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     line = run_ours(args, rank, world, local_rank)
+    if line is not None and functional:
+        line["functional_check_only"] = "all ranks on one GPU (FGA_BENCH_FUNCTIONAL=1)"
     if line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:
