@@ -18,6 +18,7 @@ ap.add_argument("--mode", default="bh", choices=["bh", "direct", "gpe", "all"])
 ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+ap.add_argument("--shard", default="0/1", help="r/N: template shard r of N (per-GPU work of N GPUs)")
 a = ap.parse_args()
 if a.mode == "all":
     for m in ("bh", "direct", "gpe"):
@@ -27,11 +28,17 @@ x, y = synth.configs2_pair(a.n)  # bench.py's configs[2] workload
 theta = 0.0 if a.mode == "direct" else 0.5
 p = fga.default_params().replace(theta=theta, G=66.7 * (2000.0 / a.n) ** 0.5, conv_tol=1e-300,
                                  max_iters=a.iters + 2)
-s = Session(x, y, p, fga.RegisterOptions(compute_gpe=False, precision=a.precision), stream=0)
+sr, sn = (int(v) for v in a.shard.split("/"))
+s = Session(x, y, p, fga.RegisterOptions(compute_gpe=False, precision=a.precision), stream=0,
+            shard_rank=sr, shard_count=sn)
 if a.mode == "gpe":
     for _ in range(a.iters):
         s.gpe()
         print("gpe", s.take_gpe())
+elif sn > 1:
+    for _ in range(a.iters):  # (a shard alone: no collective, the update uses its partial sums)
+        s.forces()
+        s.update()
 else:
     s.iterate(a.iters)
 r = s.finish()
