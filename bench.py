@@ -494,7 +494,9 @@ def run_small_m(args, session, inter_full, force_s_full, m_full):
             "interactions_per_s_vs_1m": inter / t / full,
             "ideal_ms": force_s_full * 1e3 * inter / inter_full,
             "note": "shard 0 of 8 of the configs[2] template (fga_session shard_rank=0, "
-                    "shard_count=8), force pass at the initial state, CUDA events"}
+                    "shard_count=8), force pass at the initial state, CUDA events; the "
+                    "passes after the first (which records the warps' node traces) run as "
+                    "split passes (forces.cu k_bh_split)"}
 
 
 def run_fp64(session, stream, inter32):

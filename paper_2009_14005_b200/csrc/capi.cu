@@ -47,6 +47,8 @@ struct Session {
   int64_t passes = 0;      // force passes enqueued
   bool last_pass_gpe = false;
   bool fused_update = false;  // the last session_forces also ran the update
+  bool split_traced = false;  // small shards: the warps' split trace is recorded
+  DevBuf split_trace, split_f, split_a;
   DevBuf x_raw, y_raw, xn, yn, ctx_dev, mx, my, flat, counts, cells, ref32, ref64;
   DevBuf tkeys_in, tkeys, tidx_in, tidx, cub_tmp, tpl;
   DevBuf partials, gpe_part, sums, state, scratch, lm_idx, rbf_scratch, red_stage;
@@ -446,6 +448,7 @@ int session_begin_common(fga_ctx* c, int64_t n, int64_t m, int dim, const fga_pa
   S.applied = false;
   S.passes = 0;
   S.last_pass_gpe = false;
+  S.split_traced = false;
   S.sums_ext = nullptr;
   return FGA_OK;
 }
@@ -464,6 +467,7 @@ int session_gpe(fga_ctx* c, const IterState* gate) {
 
 // fuse: the caller runs the update right after (fga_session_iterate): small
 // passes then reduce and update in one kernel (launch_reduce_update)
+constexpr int64_t kSplitPartsMax = 8;  // >= forces.cu FGA_SPLIT_PARTS
 int session_forces(fga_ctx* c, bool fuse = false) {
   Session& S = c->S;
   cudaStream_t s = c->stream;
@@ -473,7 +477,18 @@ int session_forces(fga_ctx* c, bool fuse = false) {
     launch_direct_iterate(S.ref(), tv, S.st(), S.sp, S.partials.as<double>(), S.precision, s);
     nw = direct_iterate_warps(S.m_local, S.precision);
   } else {
-    launch_bh_iterate(c->S.tree, tv, S.st(), S.sp, S.partials.as<double>(), S.precision, s);
+    SplitBufs sb{nullptr, nullptr, nullptr, &S.split_traced};
+    if (!S.precision && S.m_local > 0) {
+      const int64_t nwq = (S.m_local + 31) / 32;
+      FGA_CUDA_TRY(S.split_trace.reserve(sizeof(int) * 65 * (nwq + 8)));
+      FGA_CUDA_TRY(S.split_f.reserve(sizeof(double) * 3 * kSplitPartsMax * S.m_local));
+      FGA_CUDA_TRY(S.split_a.reserve(sizeof(int) * kSplitPartsMax * S.m_local));
+      sb.trace = S.split_trace.as<int>();
+      sb.fpart = S.split_f.as<double>();
+      sb.apart = S.split_a.as<int>();
+    }
+    launch_bh_iterate(c->S.tree, tv, S.st(), S.sp, S.partials.as<double>(), S.precision, s,
+                      sb.trace ? &sb : nullptr);
     nw = bh_iterate_warps(S.m_local);
   }
   if (S.m_local <= 0) nw = 0;
@@ -631,6 +646,9 @@ int fga_destroy(fga_ctx* c) {
   S.lm_idx.release();
   S.rbf_scratch.release();
   S.ckpt.release();
+  S.split_trace.release();
+  S.split_f.release();
+  S.split_a.release();
   DevBuf* all[] = {&S.x_raw,   &S.y_raw,  &S.xn,        &S.yn,       &S.ctx_dev,   &S.mx,
                    &S.my,      &S.flat,   &S.counts,    &S.cells,    &S.ref32,     &S.ref64,
                    &S.tkeys_in, &S.tkeys, &S.tidx_in,   &S.tidx,     &S.cub_tmp,   &S.tpl,

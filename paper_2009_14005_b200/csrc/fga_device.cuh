@@ -273,7 +273,13 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
 // qidx >= 0 gives the re-check's query index explicitly.
 // kSmem: C points to the records copied into shared memory (small trees,
 // k_bh_iterate_small); plain loads instead of the read-only global path
-template <bool kGuardZero, bool kCountVisits, bool kStatic = false, bool kSmem = false>
+// kRange: only the nodes in [lo, hi) contribute (a part of a split warp,
+// k_bh_split): the walk to lo jumps every subtree that ends at or before lo
+// and re-decides the chain spanning lo by the same MAC without counting it.
+// kTrace: records the warp's node index every 256 steps (trace[0..63]) and
+// its step count (trace[64]) -- the split points of later passes.
+template <bool kGuardZero, bool kCountVisits, bool kStatic = false, bool kSmem = false,
+          bool kRange = false, bool kTrace = false>
 __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
                                                  const double4* __restrict__ A64,
                                                  const NodeB64* __restrict__ B64, int n_nodes,
@@ -284,7 +290,8 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
                                                  double* hs = nullptr, float gA = 0.f,
                                                  float gB = 0.f, int64_t qidx = -1,
                                                  unsigned* hc = nullptr,
-                                                 const double* qsh = nullptr) {
+                                                 const double* qsh = nullptr, int lo = 0,
+                                                 int hi = -1, int* trace = nullptr) {
   // qsh (optional): the lanes' fp64 queries in shared memory (3 per thread)
   // for the exact re-check, instead of pointers + index held across the loop
   // hs (optional): the block's fp64 fold sums in shared memory, 3 per thread
@@ -301,6 +308,7 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
   // 16) | accepted of the current fold chunk -- at most FGA_FOLD node indices,
   // each visited at most once -- and the folds add it to the per-thread
   // totals in shared memory (hc[2 threadIdx.x ..])
+  static_assert(!(kRange && kCountVisits), "a split part counts accepted nodes only");
   constexpr bool kPackable = kCountVisits && FGA_FOLD > 0 && FGA_FOLD <= 65535;
   const bool packed = kPackable && hc != nullptr;
   unsigned cnt = 0;
@@ -310,7 +318,9 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     gA = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gA)));
     gB = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(gB)));
   }
-  int lim = fold_limit(0, n_nodes);
+  const int end = (kRange && hi >= 0) ? hi : n_nodes;
+  int lim = fold_limit(0, end);
+  int steps = 0;  // (kTrace)
   // kSmem (one latency-bound wave, records in shared memory): the next n is
   // one vote after the MAC, the other lanes' minimum computed off the chain
   // (1M, issue-bound: 11.6 -> 13.0 ms, so the REDUX-at-top form stays there;
@@ -319,8 +329,12 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
   int n = __reduce_min_sync(0xffffffffu, cursor);
   while (true) {
     if (!kVote) n = __reduce_min_sync(0xffffffffu, cursor);
+    if constexpr (kTrace) {
+      if ((steps & 255) == 0 && (threadIdx.x & 31) == 0 && (steps >> 8) < 64) trace[steps >> 8] = n;
+      steps++;
+    }
     if (n >= lim) {  // exit, or fold the chunk's partial into the fp64 sum
-      if (n >= n_nodes) break;
+      if (n >= end) break;
       if (hs) {
         double* h = hs + 3 * threadIdx.x;
         h[0] += (double)ax;
@@ -338,13 +352,24 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
         hcc[1] += cnt & 0xffffu;
         cnt = 0;
       }
-      lim = fold_limit(n, n_nodes);
+      lim = fold_limit(n, end);
     }
     FGA_CHECK(n >= 0 && n < n_nodes);
     const NodeC32* rec = reinterpret_cast<const NodeC32*>(C) + n;
     const float4 a = kSmem ? rec->a : __ldg(&rec->a);
     const float4 b = kSmem ? rec->b : __ldg(&rec->b);
     const bool mine = cursor == n;
+    bool pre = false;  // (kRange) a node before lo: decides the walk, adds nothing
+    if constexpr (kRange) {
+      if (n < lo) {
+        const int skp = __float_as_int(b.y);
+        if (skp <= lo) {  // its whole subtree lies before lo (warp-uniform)
+          if (mine) cursor = skp;
+          continue;
+        }
+        pre = true;
+      }
+    }
     // (kVote) the other lanes' cursors do not move this step
     const int m_other = kVote ? __reduce_min_sync(0xffffffffu, mine ? INT_MAX : cursor) : 0;
     const float dx = a.x - qx, dy = a.y - qy, dz = a.z - qz;
@@ -376,7 +401,7 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
       }
       acc = near ? e : acc;
     }
-    const bool take = mine && acc;
+    const bool take = mine && acc && !pre;
     const float inv = rsqrt_approx(r2);
     float w = a.w * (inv * inv * inv);
     if (!take) w = 0.f;
@@ -400,6 +425,9 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     cursor = mine ? next : cursor;
     if (kVote)
       n = __any_sync(0xffffffffu, mine && !acc) ? n + 1 : min(__float_as_int(b.y), m_other);
+  }
+  if constexpr (kTrace) {
+    if ((threadIdx.x & 31) == 0) trace[64] = steps;
   }
   if (kPackable && packed) {
     const unsigned* hcc = hc + 2 * threadIdx.x;

@@ -29,8 +29,18 @@ int64_t gpe_warps(int64_t m, int64_t n, int precision);
 
 // One force pass of the iteration: applies the pending transform, evaluates
 // forces, fused Euler-Cromer step, per-warp Kabsch partials.
+// split passes of small template shards (forces.cu k_bh_split): the warps'
+// recorded traces (65 ints per warp), the two parts' fp64 force sums (2 m x 3)
+// and accepted counts (2 m), and whether the trace has been recorded
+struct SplitBufs {
+  int* trace;
+  double* fpart;
+  int* apart;
+  bool* have_trace;
+};
 void launch_bh_iterate(const TreeDev& T, const TemplateView& tv, const IterState* st,
-                       const SimParams& sp, double* partials, int precision, cudaStream_t s);
+                       const SimParams& sp, double* partials, int precision, cudaStream_t s,
+                       const SplitBufs* sb = nullptr);
 void launch_direct_iterate(const RefPoints& ref, const TemplateView& tv, const IterState* st,
                            const SimParams& sp, double* partials, int precision, cudaStream_t s);
 // Energy of the current (already transformed) positions: per-warp partials of

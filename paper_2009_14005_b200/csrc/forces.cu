@@ -60,10 +60,12 @@ struct F32Params {
 // points: every step's record load is then a shared-memory load instead of an
 // L1/L2 round trip on a cold SM)
 constexpr int kSmallTreeBytes = 200 * 1024;
-template <typename Real, bool kGuardZero, bool kCountVisits, int kT, bool kSmall = false>
+constexpr int kTraceLen = 65;  // per-warp split trace: 64 node indices + the step count
+template <typename Real, bool kGuardZero, bool kCountVisits, int kT, bool kSmall = false,
+          bool kTrace = false>
 __global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32_TPS : FGA_BH64_TPS) / kT) k_bh_iterate(
     TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, SimParams sp,
-    F32Params f, double* partials, int nblocks) {
+    F32Params f, double* partials, int nblocks, int* trace = nullptr) {
   if (st->done) return;
   extern __shared__ float4 s_rec[];
   if constexpr (kSmall) {
@@ -101,10 +103,10 @@ __global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32
   if constexpr (sizeof(Real) == 4) {
     __shared__ double hs[3 * kT];  // the lanes' fp64 fold sums
     __shared__ unsigned hc[kCountVisits ? 2 * kT : 1];  // their visit / accept counts
-    const Trav32Out o = traverse32d<kGuardZero, kCountVisits, false, kSmall>(
+    const Trav32Out o = traverse32d<kGuardZero, kCountVisits, false, kSmall, false, kTrace>(
         kSmall ? s_rec : tr.c32, tr.a64, tr.b64, n_nodes, (float)y[0], (float)y[1], (float)y[2], active, f.theta2,
         sp.theta2, f.eps2, tv.px, tv.py, tv.pz, tv.m, hs, 0.f, 0.f, -1,
-        kCountVisits ? hc : nullptr);
+        kCountVisits ? hc : nullptr, nullptr, 0, -1, kTrace ? trace + gw * kTraceLen : nullptr);
     const double gq = sp.G * mq;
     F[0] = gq * o.ax;
     F[1] = gq * o.ay;
@@ -144,6 +146,128 @@ __global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32
   // counts are already warp totals: divide the upcoming warp_sum by 32
   p.v[kAccepted] = lane == 0 ? p.v[kAccepted] : 0.0;
   p.v[kVisits] = lane == 0 ? p.v[kVisits] : 0.0;
+  warp_store_partial(p, lane, partials + gw * kPartialStride);
+}
+
+// ---------------------------------------------------------------- split passes
+// Small template shards (one wave with at most half the resident warp slots
+// used: an 8-way shard of the 1M template) end with their heaviest warps'
+// step chains (per-warp union steps up to 1.6x the mean).  The first pass
+// records each warp's node index every 256 steps (k_bh_iterate<kTrace>);
+// later passes run every warp as TWO warps over the node ranges [0, s) and
+// [s, n_nodes), s = the node at half its recorded steps rounded to a fold
+// chunk (FGA_FOLD) boundary -- so every fp32 chunk sum is the unsplit one and
+// only the fp64 fold of the chunks is regrouped -- and a second kernel adds
+// the two parts and runs the epilogue.  Visits and accepted sets unchanged.
+constexpr int kSplitT = 128;
+#ifndef FGA_SPLIT_PARTS
+#define FGA_SPLIT_PARTS 8
+#endif
+constexpr int kParts = FGA_SPLIT_PARTS;
+static_assert(kParts >= 2 && kParts <= 8, "capi.cu reserves 8 parts (kSplitPartsMax)");
+// the node index where part p of warp w starts (p = 0 .. kParts): the node at
+// p/kParts of its recorded steps, rounded to a fold chunk boundary
+__device__ __forceinline__ int split_point(const int* __restrict__ trace, int64_t w, int p,
+                                           int n_nodes) {
+  if (p <= 0) return 0;
+  if (p >= kParts) return n_nodes;
+  const int* tw = trace + w * kTraceLen;
+  const int steps = tw[64];
+  const int k = min(63, (int)(((int64_t)steps * p / kParts) >> 8));
+  int sp = steps > 0 ? tw[k] : 0;
+  if (FGA_FOLD > 0) sp = ((sp + FGA_FOLD / 2) / FGA_FOLD) * FGA_FOLD;
+  return min(max(sp, 0), n_nodes);
+}
+
+template <bool kGuardZero>
+__global__ void __launch_bounds__(kSplitT, FGA_BH32_TPS / kSplitT) k_bh_split(
+    TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, F32Params f,
+    double theta2_64, const int* __restrict__ trace, int64_t nwarps, double* __restrict__ fpart,
+    int* __restrict__ apart) {
+  if (st->done) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (kSplitT / 32) + (threadIdx.x >> 5);
+  if (g >= kParts * nwarps) return;  // (whole warps)
+  // part-major: neighbouring warps of the grid walk the same node range
+  // (L1 reuse across a block's and an SM's warps, as in the unsplit pass)
+  const int64_t w = g % nwarps;
+  const int part = (int)(g / nwarps);
+  const int64_t i = w * 32 + lane;
+  const bool active = i < tv.m;
+  double y[3] = {0, 0, 0};
+  if (active) {  // the position with the pending step applied (written back by k_bh_split_epi)
+    double v[3] = {0, 0, 0};
+    y[0] = tv.px[i];
+    y[1] = tv.py[i];
+    y[2] = tv.pz[i];
+    apply_pending(st, y, v);
+  }
+  int lo = 0, hi = 0;
+  for (int q = 1; q <= part + 1; q++) {  // monotone part boundaries
+    lo = hi;
+    hi = max(lo, split_point(trace, w, q, n_nodes));
+  }
+  __shared__ double hs[3 * kSplitT];
+  __shared__ double qsh[3 * kSplitT];
+  {
+    double* q = qsh + 3 * threadIdx.x;
+    q[0] = y[0];
+    q[1] = y[1];
+    q[2] = y[2];
+  }
+  const Trav32Out o = traverse32d<kGuardZero, false, false, false, true>(
+      tr.c32, tr.a64, tr.b64, n_nodes, (float)y[0], (float)y[1], (float)y[2], active, f.theta2,
+      theta2_64, f.eps2, nullptr, nullptr, nullptr, tv.m, hs, 0.f, 0.f, -1, nullptr, qsh, lo, hi);
+  if (!active) return;
+  double* fp = fpart + (part * tv.m + i) * 3;
+  fp[0] = o.ax;
+  fp[1] = o.ay;
+  fp[2] = o.az;
+  apart[part * tv.m + i] = o.accepted;
+}
+
+template <int kT>
+__global__ void __launch_bounds__(kT) k_bh_split_epi(TemplateView tv, const IterState* __restrict__ st,
+                                                     SimParams sp, const double* __restrict__ fpart,
+                                                     const int* __restrict__ apart,
+                                                     double* partials, int nblocks) {
+  if (st->done) return;
+  const int chunk = (int)blockIdx.x;
+  if (chunk >= nblocks) return;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)chunk * (kT / 32) + wl;
+  const int64_t i = gw * 32 + lane;
+  const bool active = i < tv.m;
+  Partial p;
+  partial_zero(p);
+  int na = 0;
+  if (active) {
+    double y[3] = {tv.px[i], tv.py[i], tv.pz[i]}, v[3] = {tv.vx[i], tv.vy[i], tv.vz[i]};
+    const double mq = tv.mq[i];
+    apply_pending(st, y, v);
+    tv.px[i] = y[0];
+    tv.py[i] = y[1];
+    tv.pz[i] = y[2];
+    double h[3] = {0.0, 0.0, 0.0};
+    for (int q = 0; q < kParts; q++) {  // the parts in node order
+      const double* fq = fpart + (q * tv.m + i) * 3;
+      h[0] += fq[0];
+      h[1] += fq[1];
+      h[2] += fq[2];
+      na += apart[q * tv.m + i];
+    }
+    const double gq = sp.G * mq;
+    const double F[3] = {gq * h[0], gq * h[1], gq * h[2]};
+    double vp[3];
+    const double s[3] = {st->shift[0], st->shift[1], st->shift[2]};
+    step_and_accumulate(F, y, v, mq, sp, s, vp, p);
+    tv.vx[i] = vp[0];
+    tv.vy[i] = vp[1];
+    tv.vz[i] = vp[2];
+  }
+  p.v[kAccepted] = (double)__reduce_add_sync(0xffffffffu, (unsigned)na);
+  p.v[kVisits] = 0.0;
+  p.v[kAccepted] = lane == 0 ? p.v[kAccepted] : 0.0;
   warp_store_partial(p, lane, partials + gw * kPartialStride);
 }
 
@@ -646,7 +770,7 @@ static void launch_node_bands(const TreeDev& T, const double* px, const double* 
 template <int kT>
 static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const IterState* st,
                                 const SimParams& sp, double* partials, int precision,
-                                cudaStream_t s) {
+                                cudaStream_t s, const SplitBufs* sb) {
   const int nb = (int)grid_for(tv.m, kT);
   const unsigned g = (unsigned)nb;
   const F32Params f{(float)sp.theta2, (float)sp.eps2};
@@ -686,6 +810,33 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
       k_bh_iterate<float, false, false, kT, true><<<g, kT, tree_bytes, s>>>(r, nn, tv, st, sp, f, partials, nb);
     return;
   }
+  // small shards: record the warps' traces once, then split passes
+  static const bool split_on = !(getenv("FGA_SPLIT") && atoi(getenv("FGA_SPLIT")) == 0);
+  const int64_t nw = (int64_t)nb * (kT / 32);
+  if (split_on && sb && !sp.count_visits && nw >= 8 &&
+      2 * nw <= (int64_t)current_sms() * (FGA_BH32_TPS / 32)) {
+    if (!*sb->have_trace) {
+      if (gz)
+        k_bh_iterate<float, true, false, kT, false, true><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f,
+                                                                         partials, nb, sb->trace);
+      else
+        k_bh_iterate<float, false, false, kT, false, true><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f,
+                                                                          partials, nb, sb->trace);
+      *sb->have_trace = true;
+      return;
+    }
+    static const bool split_log = getenv("FGA_SPLIT_LOG") != nullptr;  // (tests)
+    if (split_log) fprintf(stderr, "[fga] split pass: %lld warps x %d parts\n", (long long)nw, kParts);
+    const unsigned gs = (unsigned)((kParts * nw + kSplitT / 32 - 1) / (kSplitT / 32));
+    if (gz)
+      k_bh_split<true><<<gs, kSplitT, 0, s>>>(r, nn, tv, st, f, sp.theta2, sb->trace, nw,
+                                              sb->fpart, sb->apart);
+    else
+      k_bh_split<false><<<gs, kSplitT, 0, s>>>(r, nn, tv, st, f, sp.theta2, sb->trace, nw,
+                                               sb->fpart, sb->apart);
+    k_bh_split_epi<kT><<<g, kT, 0, s>>>(tv, st, sp, sb->fpart, sb->apart, partials, nb);
+    return;
+  }
   }
   if (gz && sp.count_visits)
     k_bh_iterate<float, true, true, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb);
@@ -698,12 +849,13 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
 }
 
 void launch_bh_iterate(const TreeDev& T, const TemplateView& tv, const IterState* st,
-                       const SimParams& sp, double* partials, int precision, cudaStream_t s) {
+                       const SimParams& sp, double* partials, int precision, cudaStream_t s,
+                       const SplitBufs* sb) {
   if (tv.m <= 0) return;
   switch (bh_block()) {
-    case 64: launch_bh_iterate_t<64>(T, tv, st, sp, partials, precision, s); break;
-    case 256: launch_bh_iterate_t<256>(T, tv, st, sp, partials, precision, s); break;
-    default: launch_bh_iterate_t<128>(T, tv, st, sp, partials, precision, s); break;
+    case 64: launch_bh_iterate_t<64>(T, tv, st, sp, partials, precision, s, sb); break;
+    case 256: launch_bh_iterate_t<256>(T, tv, st, sp, partials, precision, s, sb); break;
+    default: launch_bh_iterate_t<128>(T, tv, st, sp, partials, precision, s, sb); break;
   }
 }
 
