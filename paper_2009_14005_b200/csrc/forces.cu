@@ -160,6 +160,9 @@ __global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32
 // only the fp64 fold of the chunks is regrouped -- and a second kernel adds
 // the two parts and runs the epilogue.  Visits and accepted sets unchanged.
 constexpr int kSplitT = 128;
+#ifndef FGA_SPLIT_TPS
+#define FGA_SPLIT_TPS FGA_BH32_TPS
+#endif
 #ifndef FGA_SPLIT_PARTS
 #define FGA_SPLIT_PARTS 8
 #endif
@@ -180,7 +183,7 @@ __device__ __forceinline__ int split_point(const int* __restrict__ trace, int64_
 }
 
 template <bool kGuardZero>
-__global__ void __launch_bounds__(kSplitT, FGA_BH32_TPS / kSplitT) k_bh_split(
+__global__ void __launch_bounds__(kSplitT, FGA_SPLIT_TPS / kSplitT) k_bh_split(
     TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, F32Params f,
     double theta2_64, const int* __restrict__ trace, int64_t nwarps, double* __restrict__ fpart,
     int* __restrict__ apart) {
