@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kBT, 1) k_register_batch(BatchArgs a) {
   NodeB64* const rb64_slot = a.scratch.rb64 + slot * cap;
   double* const tp_slot = a.scratch.tpl + slot * a.mmax * 7;
   const double dt = a.p.dt, eta = a.p.eta, G = a.p.G, eps = a.p.epsilon;
-  const double theta2 = a.theta2, eps2 = a.eps2;
+  const double theta2 = a.theta2;
 
   while (true) {
     if (tid == 0) next_pair = atomicAdd(a.counter, 1);

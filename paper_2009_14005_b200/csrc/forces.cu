@@ -160,6 +160,9 @@ __global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32
 // only the fp64 fold of the chunks is regrouped -- and a second kernel adds
 // the two parts and runs the epilogue.  Visits and accepted sets unchanged.
 constexpr int kSplitT = 128;
+#ifndef FGA_SPLIT_WAVE
+#define FGA_SPLIT_WAVE 2  // split passes when the warps fill <= 1/FGA_SPLIT_WAVE of the slots
+#endif
 #ifndef FGA_SPLIT_TPS
 #define FGA_SPLIT_TPS FGA_BH32_TPS
 #endif
@@ -817,7 +820,7 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
   static const bool split_on = !(getenv("FGA_SPLIT") && atoi(getenv("FGA_SPLIT")) == 0);
   const int64_t nw = (int64_t)nb * (kT / 32);
   if (split_on && sb && !sp.count_visits && nw >= 8 &&
-      2 * nw <= (int64_t)current_sms() * (FGA_BH32_TPS / 32)) {
+      FGA_SPLIT_WAVE * nw <= (int64_t)current_sms() * (FGA_BH32_TPS / 32)) {
     if (!*sb->have_trace) {
       if (gz)
         k_bh_iterate<float, true, false, kT, false, true><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f,
