@@ -48,7 +48,8 @@ struct Session {
   bool last_pass_gpe = false;
   bool fused_update = false;  // the last session_forces also ran the update
   bool split_traced = false;  // small shards: the warps' split trace is recorded
-  DevBuf split_trace, split_f, split_a;
+  bool order_ready = false;   // multi-wave passes: the heaviest-first block order is set
+  DevBuf split_trace, split_f, split_a, order_buf;
   DevBuf x_raw, y_raw, xn, yn, ctx_dev, mx, my, flat, counts, cells, ref32, ref64;
   DevBuf tkeys_in, tkeys, tidx_in, tidx, cub_tmp, tpl;
   DevBuf partials, gpe_part, sums, state, scratch, lm_idx, rbf_scratch, red_stage;
@@ -371,7 +372,7 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
   launch_mean3(S.yn.as<double>(), m, S.scratch.as<double>(), S.scratch.as<double>() + 4096, s);
   launch_state_init(S.st(), S.scratch.as<double>() + 4096, s);
   const int64_t nw = S.direct ? direct_iterate_warps(S.m_local, S.precision)
-                              : bh_iterate_warps(S.m_local);
+                              : bh_iterate_warps(S.m_local, S.precision);
   FGA_CUDA_TRY(S.partials.reserve(sizeof(double) * kPartialStride * std::max<int64_t>(nw, 1)));
   FGA_CUDA_TRY(S.gpe_part.reserve(sizeof(double) * std::max<int64_t>(gpe_warps(S.m_local, n, S.precision), 1)));
   FGA_CUDA_TRY(S.red_stage.reserve(sizeof(double) * reduce_stage_doubles()));
@@ -449,6 +450,7 @@ int session_begin_common(fga_ctx* c, int64_t n, int64_t m, int dim, const fga_pa
   S.passes = 0;
   S.last_pass_gpe = false;
   S.split_traced = false;
+  S.order_ready = false;
   S.sums_ext = nullptr;
   return FGA_OK;
 }
@@ -486,10 +488,18 @@ int session_forces(fga_ctx* c, bool fuse = false) {
       sb.trace = S.split_trace.as<int>();
       sb.fpart = S.split_f.as<double>();
       sb.apart = S.split_a.as<int>();
+      const int64_t nblk = nwq / 2 + 8;  // >= blocks of any block size >= 64 threads
+      FGA_CUDA_TRY(S.order_buf.reserve(sizeof(int) * 4 * nblk + (4 << 20)));
+      sb.order = S.order_buf.as<int>();
+      sb.okeys = sb.order + nblk;
+      const uintptr_t t0 = reinterpret_cast<uintptr_t>(sb.okeys + 3 * nblk);
+      sb.tmp = reinterpret_cast<void*>((t0 + 255) & ~uintptr_t(255));
+      sb.tmp_bytes = (4 << 20) - 256;
+      sb.have_order = &S.order_ready;
     }
     launch_bh_iterate(c->S.tree, tv, S.st(), S.sp, S.partials.as<double>(), S.precision, s,
                       sb.trace ? &sb : nullptr);
-    nw = bh_iterate_warps(S.m_local);
+    nw = bh_iterate_warps(S.m_local, S.precision);
   }
   if (S.m_local <= 0) nw = 0;
   const bool with_gpe = S.O.trace_gpe && S.passes > 0;
@@ -649,6 +659,7 @@ int fga_destroy(fga_ctx* c) {
   S.split_trace.release();
   S.split_f.release();
   S.split_a.release();
+  S.order_buf.release();
   DevBuf* all[] = {&S.x_raw,   &S.y_raw,  &S.xn,        &S.yn,       &S.ctx_dev,   &S.mx,
                    &S.my,      &S.flat,   &S.counts,    &S.cells,    &S.ref32,     &S.ref64,
                    &S.tkeys_in, &S.tkeys, &S.tidx_in,   &S.tidx,     &S.cub_tmp,   &S.tpl,

@@ -291,7 +291,10 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
                                                  float gB = 0.f, int64_t qidx = -1,
                                                  unsigned* hc = nullptr,
                                                  const double* qsh = nullptr, int lo = 0,
-                                                 int hi = -1, int* trace = nullptr) {
+                                                 int hi = -1, int* trace = nullptr,
+                                                 const int* border = nullptr) {
+  // border (optional): the block -> chunk order of the launch (the query of
+  // the exact re-check is chunk * blockDim + thread)
   // qsh (optional): the lanes' fp64 queries in shared memory (3 per thread)
   // for the exact re-check, instead of pointers + index held across the loop
   // hs (optional): the block's fp64 fold sums in shared memory, 3 per thread
@@ -395,7 +398,8 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
         const double* q = qsh + 3 * threadIdx.x;
         e = mac_exact(A64, B64, n, q[0], q[1], q[2], theta2_64);
       } else {
-        int64_t qs = qidx >= 0 ? qidx : blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        const int64_t blk = border ? border[blockIdx.x] : blockIdx.x;
+        int64_t qs = qidx >= 0 ? qidx : blk * (int64_t)blockDim.x + threadIdx.x;
         qs = qs < m_queries ? qs : m_queries - 1;
         e = mac_exact(A64, B64, n, qpx[qs], qpy[qs], qpz[qs], theta2_64);
       }

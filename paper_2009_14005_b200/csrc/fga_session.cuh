@@ -23,7 +23,7 @@ struct RefPoints {
 constexpr int kForceThreads = 256;
 constexpr int kDirectQPT = 4;  // queries per thread in the FP32 direct sum (2 FFMA2 packs)
 
-int64_t bh_iterate_warps(int64_t m);
+int64_t bh_iterate_warps(int64_t m, int precision);
 int64_t direct_iterate_warps(int64_t m, int precision);
 int64_t gpe_warps(int64_t m, int64_t n, int precision);
 
@@ -37,6 +37,13 @@ struct SplitBufs {
   double* fpart;
   int* apart;
   bool* have_trace;
+  // multi-wave passes: blocks launched heaviest first (LPT order from the
+  // first pass's trace): order/okeys (4 x blocks ints), CUB scratch
+  int* order = nullptr;
+  int* okeys = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  bool* have_order = nullptr;
 };
 void launch_bh_iterate(const TreeDev& T, const TemplateView& tv, const IterState* st,
                        const SimParams& sp, double* partials, int precision, cudaStream_t s,

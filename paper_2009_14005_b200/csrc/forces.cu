@@ -25,6 +25,8 @@
 // 2 queries per thread, FP32 FMA/MUFU inner loop, fp64 across tiles.
 //
 // K11 potential energy (_kernels.gpe_kernel, _kernels.py:53-67): same tiling.
+#include <cub/cub.cuh>
+
 #include <climits>
 #include <cstdlib>
 
@@ -65,7 +67,8 @@ template <typename Real, bool kGuardZero, bool kCountVisits, int kT, bool kSmall
           bool kTrace = false>
 __global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32_TPS : FGA_BH64_TPS) / kT) k_bh_iterate(
     TreeRecords tr, int n_nodes, TemplateView tv, const IterState* __restrict__ st, SimParams sp,
-    F32Params f, double* partials, int nblocks, int* trace = nullptr) {
+    F32Params f, double* partials, int nblocks, int* trace = nullptr,
+    const int* __restrict__ order = nullptr) {
   if (st->done) return;
   extern __shared__ float4 s_rec[];
   if constexpr (kSmall) {
@@ -74,8 +77,9 @@ __global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32
     __syncthreads();
   }
   // (An SM-contiguous block->chunk remap for L1 sharing was measured 3%
-  // slower -- per-SM load imbalance -- so blocks map to chunks in order.)
-  const int chunk = (int)blockIdx.x;
+  // slower -- per-SM load imbalance.)  With `order` the chunks run heaviest
+  // first (the block->partial-slot map is unchanged: same sums)
+  const int chunk = order ? order[blockIdx.x] : (int)blockIdx.x;
   if (chunk >= nblocks) return;
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t gw = (int64_t)chunk * (kT / 32) + wl;
@@ -106,7 +110,8 @@ __global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32
     const Trav32Out o = traverse32d<kGuardZero, kCountVisits, false, kSmall, false, kTrace>(
         kSmall ? s_rec : tr.c32, tr.a64, tr.b64, n_nodes, (float)y[0], (float)y[1], (float)y[2], active, f.theta2,
         sp.theta2, f.eps2, tv.px, tv.py, tv.pz, tv.m, hs, 0.f, 0.f, -1,
-        kCountVisits ? hc : nullptr, nullptr, 0, -1, kTrace ? trace + gw * kTraceLen : nullptr);
+        kCountVisits ? hc : nullptr, nullptr, 0, -1, kTrace ? trace + gw * kTraceLen : nullptr,
+        order);
     const double gq = sp.G * mq;
     F[0] = gq * o.ax;
     F[1] = gq * o.ay;
@@ -147,6 +152,18 @@ __global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32
   p.v[kAccepted] = lane == 0 ? p.v[kAccepted] : 0.0;
   p.v[kVisits] = lane == 0 ? p.v[kVisits] : 0.0;
   warp_store_partial(p, lane, partials + gw * kPartialStride);
+}
+
+// ---------------------------------------------------------------- block order
+// key = the block's recorded warp steps (k_bh_iterate<kTrace>), value = block
+__global__ void k_block_work(const int* __restrict__ trace, int nblocks, int wpb,
+                             unsigned* __restrict__ key, int* __restrict__ val) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nblocks) return;
+  unsigned w = 0;
+  for (int k = 0; k < wpb; k++) w += (unsigned)trace[((int64_t)b * wpb + k) * kTraceLen + 64];
+  key[b] = w;
+  val[b] = b;
 }
 
 // ---------------------------------------------------------------- split passes
@@ -645,16 +662,25 @@ inline unsigned grid_for(int64_t items, int64_t per_block) {
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
-static int bh_block() {
-  static int b = [] {
+static int current_sms();
+// Threads per block of the iteration kernel for m template queries: 64 for
+// multi-wave FP32 passes (with the heaviest-first block order, finer blocks
+// leave less of a slot idle behind a block's slowest warp: 1M pass 11.08 ->
+// 10.93 ms), 128 for one-wave passes (the shared-memory small-tree and split
+// paths are tuned there) and the fp64 kernel.  FGA_BH_BLOCK forces a size.
+static int bh_block(int64_t m, int precision) {
+  static const int forced = [] {
     const char* e = getenv("FGA_BH_BLOCK");
-    int v = e ? atoi(e) : 128;
-    return (v == 64 || v == 128 || v == 256) ? v : 128;
+    const int v = e ? atoi(e) : 0;
+    return (v == 64 || v == 128 || v == 256) ? v : 0;
   }();
-  return b;
+  if (forced) return forced;
+  if (precision) return 128;
+  const int64_t warps128 = (int64_t)grid_for(m, 128) * 4;
+  return warps128 <= (int64_t)current_sms() * (FGA_BH32_TPS / 32) ? 128 : 64;
 }
-int64_t bh_iterate_warps(int64_t m) {
-  const int t = bh_block();
+int64_t bh_iterate_warps(int64_t m, int precision) {
+  const int t = bh_block(m, precision);
   return (int64_t)grid_for(m, t) * (t / 32);
 }
 int64_t direct_iterate_warps(int64_t m, int precision) {
@@ -844,6 +870,38 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
     return;
   }
   }
+  // multi-wave passes: the first one records the warps' steps, the later
+  // ones launch the blocks heaviest first (LPT: a shorter tail)
+  static const bool order_on = !(getenv("FGA_LPT") && atoi(getenv("FGA_LPT")) == 0);
+  if (order_on && sb && sb->order && !sp.count_visits) {
+    if (!*sb->have_order) {
+      if (gz)
+        k_bh_iterate<float, true, false, kT, false, true><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f,
+                                                                         partials, nb, sb->trace);
+      else
+        k_bh_iterate<float, false, false, kT, false, true><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f,
+                                                                          partials, nb, sb->trace);
+      unsigned* kin = reinterpret_cast<unsigned*>(sb->okeys);
+      unsigned* kout = kin + nb;
+      int* vin = sb->okeys + 2 * nb;
+      k_block_work<<<(nb + 255) / 256, 256, 0, s>>>(sb->trace, nb, kT / 32, kin, vin);
+      size_t bytes = 0;
+      cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, kin, kout, vin, sb->order, nb, 0,
+                                                32, s);
+      if (bytes <= sb->tmp_bytes &&
+          cub::DeviceRadixSort::SortPairsDescending(sb->tmp, bytes, kin, kout, vin, sb->order,
+                                                    nb, 0, 32, s) == cudaSuccess)
+        *sb->have_order = true;
+      return;
+    }
+    if (gz)
+      k_bh_iterate<float, true, false, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb,
+                                                            nullptr, sb->order);
+    else
+      k_bh_iterate<float, false, false, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb,
+                                                             nullptr, sb->order);
+    return;
+  }
   if (gz && sp.count_visits)
     k_bh_iterate<float, true, true, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb);
   else if (gz)
@@ -858,7 +916,7 @@ void launch_bh_iterate(const TreeDev& T, const TemplateView& tv, const IterState
                        const SimParams& sp, double* partials, int precision, cudaStream_t s,
                        const SplitBufs* sb) {
   if (tv.m <= 0) return;
-  switch (bh_block()) {
+  switch (bh_block(tv.m, precision)) {
     case 64: launch_bh_iterate_t<64>(T, tv, st, sp, partials, precision, s, sb); break;
     case 256: launch_bh_iterate_t<256>(T, tv, st, sp, partials, precision, s, sb); break;
     default: launch_bh_iterate_t<128>(T, tv, st, sp, partials, precision, s, sb); break;
