@@ -422,44 +422,48 @@ def run_ours(args, rank, world, local_rank):
 
 
 def traversal_roofline(force_s, visits, inter, m, peak_tflops, peak_src, fmax):
-    """k_bh_iterate: issue/latency-bound inside the SM (ncu), not a DRAM or
-    tensor kernel.  `achieved` = SURVEY §8(d) algorithmic bytes (32 B per
-    query-node visit + 32 B per query) per launch / live launch time, against
-    the live-measured L2 read bandwidth; `traffic` = the L2->SM bytes ncu
-    measured per launch (the node loads mostly hit L1), with DRAM bytes and
-    the issue-slot utilisation beside it."""
+    """k_bh_iterate is issue-bound inside the SM (ncu: issue slots ~80% busy,
+    a latency chain of warp-uniform L1-hit record loads), not a DRAM or
+    tensor kernel, so the headline roofline is the issue-slot one: warp
+    instructions per launch (ncu, profiles/traffic.json) / the live launch
+    time, against 148 SMs x 4 schedulers x f_max.  Beside it: the SURVEY
+    §8(d) byte model (32 B per query-node visit + 32 B per query) against the
+    live-measured L2 read bandwidth -- it counts the L1 hits as traffic, so
+    its fraction can exceed 1 -- with the L2->SM and DRAM bytes ncu measured
+    per launch as `traffic`, and an FP32 FLOP view."""
     prof = _profile("bh")
     l2_peak, l2_src = l2_peak_gbs()
     alg = BYTES_PER_VISIT * visits + BYTES_PER_QUERY * m
     ach = alg / force_s / 1e9
     flop = FLOP_PER_INTERACTION * inter + FLOP_PER_VISIT * visits
+    l2_view = {"unit": "GB/s", "achieved": ach, "peak": l2_peak,
+               "frac": ach / l2_peak if l2_peak else None, "peak_source": l2_src,
+               "work": f"SURVEY §8(d) K6: {BYTES_PER_VISIT} B/visit x {visits:.4g} visits + "
+                       f"{BYTES_PER_QUERY} B x {m} queries = {alg:.4g} B per launch (model "
+                       "bytes: most node loads are L1 hits, so frac may exceed 1)"}
+    fp32_view = {"achieved_tflops": flop / force_s / 1e12, "peak_tflops": peak_tflops,
+                 "frac": flop / force_s / 1e12 / peak_tflops,
+                 "peak_source": f"2*148*128*sm_max_mhz ({peak_src} {fmax} MHz)",
+                 "work": f"{FLOP_PER_INTERACTION} FLOP/interaction + {FLOP_PER_VISIT} FLOP/visit"}
     out = {"kernel": "k_bh_iterate<float> (+k_qbound, k_node_bands, k_reduce)",
-           "bound": "issue/L1TEX (latency of the per-step record loads)", "unit": "GB/s",
-           "achieved": ach, "peak": l2_peak, "frac": ach / l2_peak if l2_peak else None,
-           "peak_source": l2_src,
-           "work": f"SURVEY §8(d) K6: {BYTES_PER_VISIT} B/visit x {visits:.4g} visits + "
-                   f"{BYTES_PER_QUERY} B x {m} queries = {alg:.4g} B per launch (model bytes: "
-                   "most node loads are L1 hits)",
            "ms_per_launch": force_s * 1e3,
            "traffic": prof.get("lts_bytes"),
            "traffic_source": "ncu lts__t_sectors_srcunit_tex x 32 B per launch (L2->SM), "
                              "profiles/traffic.json",
-           "dram_bytes": prof.get("dram_bytes"),
-           "l1_hit_pct": prof.get("l1_hit_pct"),
-           "fp32_view": {"achieved_tflops": flop / force_s / 1e12, "peak_tflops": peak_tflops,
-                         "frac": flop / force_s / 1e12 / peak_tflops,
-                         "peak_source": f"2*148*128*sm_max_mhz ({peak_src} {fmax} MHz)",
-                         "work": f"{FLOP_PER_INTERACTION} FLOP/interaction + {FLOP_PER_VISIT} "
-                                 "FLOP/visit"}}
+           "dram_bytes": prof.get("dram_bytes"), "l1_hit_pct": prof.get("l1_hit_pct"),
+           "l2_model_view": l2_view, "fp32_view": fp32_view}
     if prof.get("inst_executed"):
         issue_peak = 148 * 4 * fmax * 1e6  # warp-instructions per second
-        out["issue_view"] = {
-            "achieved_winst_per_s": prof["inst_executed"] / force_s,
-            "peak_winst_per_s": issue_peak,
-            "frac": prof["inst_executed"] / force_s / issue_peak,
-            "ncu_issue_active_pct": prof.get("issue_active_pct"),
-            "note": "warp instructions per launch (ncu) / live launch time vs 148 SMs x 4 "
-                    "schedulers x f_max"}
+        achieved = prof["inst_executed"] / force_s
+        out.update({"bound": "issue (latency-bound L1 record loads; not DRAM or tensor)",
+                    "unit": "warp-inst/s", "achieved": achieved, "peak": issue_peak,
+                    "frac": achieved / issue_peak,
+                    "peak_source": f"148 SMs x 4 schedulers x {fmax} MHz",
+                    "work": f"{prof['inst_executed']:.4g} warp instructions per launch (ncu)",
+                    "ncu_issue_active_pct": prof.get("issue_active_pct"),
+                    "ncu_warps_active_pct": prof.get("warps_active_pct")})
+    else:
+        out.update({"bound": "issue/L1TEX (no ncu profile: the byte model)", **l2_view})
     return out
 
 
