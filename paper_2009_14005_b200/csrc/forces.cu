@@ -295,22 +295,22 @@ __global__ void __launch_bounds__(kT) k_bh_split_epi(TemplateView tv, const Iter
 }
 
 // ---------------------------------------------------------------- BH operator
-template <typename Real, bool kGuardZero>
+template <typename Real, bool kGuardZero, int kT = kForceThreads>
 #ifndef FGA_BHOP_MINB
 #define FGA_BHOP_MINB 5  // 1280 threads/SM: fp64 operator 39.5 -> 38.7 ms (1M x 1M, host in/out)
 #endif
 #ifndef FGA_BHOP32_TPS
 #define FGA_BHOP32_TPS FGA_BH32_TPS
 #endif
-__global__ void __launch_bounds__(kForceThreads, sizeof(Real) == 4 ? FGA_BHOP32_TPS / kForceThreads
-                                                                   : FGA_BHOP_MINB) k_bh_operator(
+__global__ void __launch_bounds__(kT, sizeof(Real) == 4 ? FGA_BHOP32_TPS / kT
+                                                        : FGA_BHOP_MINB) k_bh_operator(
     TreeRecords tr, int n_nodes, const double* __restrict__ qx_, const double* __restrict__ qy_,
     const double* __restrict__ qz_, const double* __restrict__ qm_, const int* __restrict__ order,
     int64_t m, double theta2, double G, double eps2, F32Params f, double* __restrict__ fout,
     long long* __restrict__ visits, long long* __restrict__ accepted,
     unsigned long long* __restrict__ acc_total) {
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int64_t i = ((int64_t)blockIdx.x * kWarps + wl) * 32 + lane;
+  const int64_t i = ((int64_t)blockIdx.x * (kT / 32) + wl) * 32 + lane;
   const bool active = i < m;
   double F[3];
   int nv, na;
@@ -323,8 +323,8 @@ __global__ void __launch_bounds__(kForceThreads, sizeof(Real) == 4 ? FGA_BHOP32_
       qf[1] = (float)qy_[i];
       qf[2] = (float)qz_[i];
     }
-    __shared__ double hs[3 * kForceThreads];
-    __shared__ unsigned hc[2 * kForceThreads];
+    __shared__ double hs[3 * kT];
+    __shared__ unsigned hc[2 * kT];
     const Trav32Out o = traverse32d<kGuardZero, true>(
         tr.c32, tr.a64, tr.b64, n_nodes, qf[0], qf[1], qf[2], active, f.theta2, theta2, f.eps2,
         qx_, qy_, qz_, m, hs, 0.f, 0.f, -1, hc);
@@ -955,30 +955,39 @@ void launch_gpe(const RefPoints& ref, const double* px, const double* py, const 
                                                          (float)eps, st, partials, g.seg);
 }
 
+#ifndef FGA_OP_T
+#define FGA_OP_T 64
+#endif
+// FP32 operator threads per block (64: 13.88 -> 13.68 ms per 1M-query e2e call
+// against 256)
+constexpr int kOpT = FGA_OP_T;
+
 void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, const double* qz,
                         const double* qm, const int* order, int64_t m, double theta, double G,
                         double eps2, double* fout, long long* visits, long long* accepted,
                         unsigned long long* acc_total, int precision, cudaStream_t s) {
   if (m <= 0) return;
-  const unsigned g = grid_for(m, kForceThreads);
   const double theta2 = theta * theta;
   const F32Params f{(float)theta2, (float)eps2};
   const int nn = (int)T.n_nodes;
   const TreeRecords r = T.records();
   if (precision) {
+    const unsigned g = grid_for(m, kForceThreads);
     k_bh_operator<double, false><<<g, kForceThreads, 0, s>>>(r, nn, qx, qy, qz, qm, order, m,
                                                              theta2, G, eps2, f, fout, visits,
                                                              accepted, acc_total);
     return;
   }
   launch_node_bands(T, qx, qy, qz, m, nullptr, f.theta2, f.eps2, s);
+  const unsigned g = grid_for(m, kOpT);
   if (!(eps2 > 0.0))
-    k_bh_operator<float, true><<<g, kForceThreads, 0, s>>>(r, nn, qx, qy, qz, qm, order, m, theta2,
-                                                           G, eps2, f, fout, visits, accepted, acc_total);
+    k_bh_operator<float, true, kOpT><<<g, kOpT, 0, s>>>(r, nn, qx, qy, qz, qm, order, m, theta2,
+                                                        G, eps2, f, fout, visits, accepted,
+                                                        acc_total);
   else
-    k_bh_operator<float, false><<<g, kForceThreads, 0, s>>>(r, nn, qx, qy, qz, qm, order, m,
-                                                            theta2, G, eps2, f, fout, visits,
-                                                            accepted, acc_total);
+    k_bh_operator<float, false, kOpT><<<g, kOpT, 0, s>>>(r, nn, qx, qy, qz, qm, order, m, theta2,
+                                                         G, eps2, f, fout, visits, accepted,
+                                                         acc_total);
 }
 
 void launch_direct_operator(const RefPoints& ref, const double* qx, const double* qy,
