@@ -1214,9 +1214,25 @@ int fga_register_batch_dev(fga_ctx* c, const double* x_all, const int64_t* x_off
   TRY(launch_register_batch(a, grid, smem, s));
   if (phase_times) cudaEventRecord(pe[1], s);
   int cur = 0;
+  static const bool iter_times = phase_times && atoi(getenv("FGA_BATCH_PHASES")) == 2;
   for (int it = 0; it < params->max_iters; it++) {
+    cudaEvent_t ie[2];
+    if (iter_times) {
+      for (auto& e : ie) cudaEventCreate(&e);
+      cudaEventRecord(ie[0], s);
+    }
     TRY(launch_wide_iteration(a, cur, it, s));
     cur = 1 - cur;
+    if (iter_times) {  // (design tool: per-iteration time and active pairs)
+      cudaEventRecord(ie[1], s);
+      int act = 0;
+      cudaMemcpyAsync(&act, a.wide.counts + cur, sizeof(int), cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ie[0], ie[1]);
+      fprintf(stderr, "it %d %.3f ms active-after %d\n", it, ms, act);
+      for (auto& e : ie) cudaEventDestroy(e);
+    }
     if ((it & 3) == 3 || it + 1 == params->max_iters) {  // stop once every pair is done
       int active = 0;
       FGA_CUDA_TRY(cudaMemcpyAsync(&active, a.wide.counts + cur, sizeof(int),
