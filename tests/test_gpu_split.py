@@ -58,3 +58,34 @@ def test_split_passes_match_unsplit_and_oracle(orc):
     ref = orc.register(x.points, y.points, theta=0.5, G=66.7 * (2000 / 40000) ** 0.5,
                        max_iters=12, conv_tol=1e-300)
     assert np.abs(ta - np.array(ref.trajectory)).max() < 1e-5
+
+
+LPT_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, %r)
+import numpy as np
+import paper_2009_14005_b200 as fga
+from paper_2009_14005_b200 import synth
+rng = synth.rng_from_seed(43)
+x = synth.blob(150000, rng)
+y = synth.misalign(synth.blob(150000, synth.rng_from_seed(44)), synth.random_rigid(rng, 0.5, 0.05))
+p = fga.default_params().replace(theta=0.5, G=66.7 * (2000 / 150000) ** 0.5, max_iters=6,
+                                 conv_tol=1e-300)
+r = fga.register(x, y, params=p, options=fga.RegisterOptions(record_iterations=True))
+print(json.dumps({"traj": r.trajectory.tolist(), "inter": r.interactions.tolist()}))
+""" % ROOT
+
+
+def test_heaviest_first_order_changes_nothing():
+    """Multi-wave passes launch their blocks heaviest first after the first
+    pass (k_bh_iterate with `order`): the partial-sum slots are unchanged,
+    so the run equals the in-order one bit for bit (FGA_LPT=0)."""
+    outs = []
+    for lpt in ("1", "0"):
+        env = dict(os.environ, FGA_LPT=lpt)
+        out = subprocess.run([sys.executable, "-c", LPT_SCRIPT], env=env, capture_output=True,
+                             text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        outs.append(json.loads(out.stdout.strip().splitlines()[-1]))
+    assert outs[0]["inter"] == outs[1]["inter"]
+    assert np.array_equal(np.array(outs[0]["traj"]), np.array(outs[1]["traj"]))
