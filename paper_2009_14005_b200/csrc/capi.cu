@@ -483,11 +483,17 @@ int session_forces(fga_ctx* c, bool fuse = false) {
     if (!S.precision && S.m_local > 0) {
       const int64_t nwq = (S.m_local + 31) / 32;
       FGA_CUDA_TRY(S.split_trace.reserve(sizeof(int) * 65 * (nwq + 8)));
-      FGA_CUDA_TRY(S.split_f.reserve(sizeof(double) * 3 * kSplitPartsMax * S.m_local));
-      FGA_CUDA_TRY(S.split_a.reserve(sizeof(int) * kSplitPartsMax * S.m_local));
       sb.trace = S.split_trace.as<int>();
-      sb.fpart = S.split_f.as<double>();
-      sb.apart = S.split_a.as<int>();
+      // the split parts' buffers only where split passes can run (a pass of
+      // at most half the resident warps: forces.cu FGA_SPLIT_WAVE)
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+      if (2 * nwq <= (int64_t)sms * 64) {
+        FGA_CUDA_TRY(S.split_f.reserve(sizeof(double) * 3 * kSplitPartsMax * S.m_local));
+        FGA_CUDA_TRY(S.split_a.reserve(sizeof(int) * kSplitPartsMax * S.m_local));
+        sb.fpart = S.split_f.as<double>();
+        sb.apart = S.split_a.as<int>();
+      }
       const int64_t nblk = nwq / 2 + 8;  // >= blocks of any block size >= 64 threads
       FGA_CUDA_TRY(S.order_buf.reserve(sizeof(int) * 4 * nblk + (4 << 20)));
       sb.order = S.order_buf.as<int>();

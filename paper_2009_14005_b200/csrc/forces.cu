@@ -845,7 +845,7 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
   // small shards: record the warps' traces once, then split passes
   static const bool split_on = !(getenv("FGA_SPLIT") && atoi(getenv("FGA_SPLIT")) == 0);
   const int64_t nw = (int64_t)nb * (kT / 32);
-  if (split_on && sb && !sp.count_visits && nw >= 8 &&
+  if (split_on && sb && sb->fpart && sb->apart && !sp.count_visits && nw >= 8 &&
       FGA_SPLIT_WAVE * nw <= (int64_t)current_sms() * (FGA_BH32_TPS / 32)) {
     if (!*sb->have_trace) {
       if (gz)
