@@ -49,6 +49,7 @@ struct Session {
   bool fused_update = false;  // the last session_forces also ran the update
   bool split_traced = false;  // small shards: the warps' split trace is recorded
   bool order_ready = false;   // multi-wave passes: the heaviest-first block order is set
+  bool split_mode = false;    // the later passes run as split passes
   DevBuf split_trace, split_f, split_a, order_buf;
   DevBuf x_raw, y_raw, xn, yn, ctx_dev, mx, my, flat, counts, cells, ref32, ref64;
   DevBuf tkeys_in, tkeys, tidx_in, tidx, cub_tmp, tpl;
@@ -451,6 +452,7 @@ int session_begin_common(fga_ctx* c, int64_t n, int64_t m, int dim, const fga_pa
   S.last_pass_gpe = false;
   S.split_traced = false;
   S.order_ready = false;
+  S.split_mode = false;
   S.sums_ext = nullptr;
   return FGA_OK;
 }
@@ -486,9 +488,7 @@ int session_forces(fga_ctx* c, bool fuse = false) {
       sb.trace = S.split_trace.as<int>();
       // the split parts' buffers only where split passes can run (a pass of
       // at most half the resident warps: forces.cu FGA_SPLIT_WAVE)
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-      if (2 * nwq <= (int64_t)sms * 64) {
+      if (bh_split_possible(S.m_local)) {
         FGA_CUDA_TRY(S.split_f.reserve(sizeof(double) * 3 * kSplitPartsMax * S.m_local));
         FGA_CUDA_TRY(S.split_a.reserve(sizeof(int) * kSplitPartsMax * S.m_local));
         sb.fpart = S.split_f.as<double>();
@@ -502,6 +502,7 @@ int session_forces(fga_ctx* c, bool fuse = false) {
       sb.tmp = reinterpret_cast<void*>((t0 + 255) & ~uintptr_t(255));
       sb.tmp_bytes = (4 << 20) - 256;
       sb.have_order = &S.order_ready;
+      sb.split = &S.split_mode;
     }
     launch_bh_iterate(c->S.tree, tv, S.st(), S.sp, S.partials.as<double>(), S.precision, s,
                       sb.trace ? &sb : nullptr);

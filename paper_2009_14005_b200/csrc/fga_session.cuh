@@ -24,6 +24,7 @@ constexpr int kForceThreads = 256;
 constexpr int kDirectQPT = 4;  // queries per thread in the FP32 direct sum (2 FFMA2 packs)
 
 int64_t bh_iterate_warps(int64_t m, int precision);
+bool bh_split_possible(int64_t m);
 int64_t direct_iterate_warps(int64_t m, int precision);
 int64_t gpe_warps(int64_t m, int64_t n, int precision);
 
@@ -44,6 +45,7 @@ struct SplitBufs {
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
   bool* have_order = nullptr;
+  bool* split = nullptr;  // this session's later passes run split
 };
 void launch_bh_iterate(const TreeDev& T, const TemplateView& tv, const IterState* st,
                        const SimParams& sp, double* partials, int precision, cudaStream_t s,

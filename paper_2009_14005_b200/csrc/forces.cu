@@ -50,6 +50,9 @@ struct F32Params {
 // Measured and not kept: the query in shared memory (15.3 ms at 1792),
 // L1 prefetch of node n+1 (+1%) or of skip(n) (+7%).
 // fp64 traversal: 768 -> 35.8 ms, 1024 -> 31.5, 1280 -> 30.3, 1536 -> 38 (spills)
+#ifndef FGA_SPLIT_WAVE
+#define FGA_SPLIT_WAVE 2  // split passes when the warps fill <= 1/FGA_SPLIT_WAVE of the slots
+#endif
 #ifndef FGA_BH32_TPS
 #define FGA_BH32_TPS 1792
 #endif
@@ -166,6 +169,36 @@ __global__ void k_block_work(const int* __restrict__ trace, int nblocks, int wpb
   val[b] = b;
 }
 
+// max and sum of the warps' recorded step counts (one block)
+__global__ void k_trace_stats(const int* __restrict__ trace, int64_t nw,
+                              unsigned long long* __restrict__ out) {
+  unsigned long long mx = 0, sm = 0;
+  for (int64_t w = threadIdx.x; w < nw; w += blockDim.x) {
+    const unsigned long long v = (unsigned)trace[w * kTraceLen + 64];
+    mx = v > mx ? v : mx;
+    sm += v;
+  }
+  __shared__ unsigned long long smx[32], ssm[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = a > mx ? a : mx;
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    smx[threadIdx.x >> 5] = mx;
+    ssm[threadIdx.x >> 5] = sm;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); k++) {
+      mx = smx[k] > mx ? smx[k] : mx;
+      sm += ssm[k];
+    }
+    out[0] = mx;
+    out[1] = sm;
+  }
+}
+
 // ---------------------------------------------------------------- split passes
 // Small template shards (one wave with at most half the resident warp slots
 // used: an 8-way shard of the 1M template) end with their heaviest warps'
@@ -177,9 +210,6 @@ __global__ void k_block_work(const int* __restrict__ trace, int nblocks, int wpb
 // only the fp64 fold of the chunks is regrouped -- and a second kernel adds
 // the two parts and runs the epilogue.  Visits and accepted sets unchanged.
 constexpr int kSplitT = 128;
-#ifndef FGA_SPLIT_WAVE
-#define FGA_SPLIT_WAVE 2  // split passes when the warps fill <= 1/FGA_SPLIT_WAVE of the slots
-#endif
 #ifndef FGA_SPLIT_TPS
 #define FGA_SPLIT_TPS FGA_BH32_TPS
 #endif
@@ -679,6 +709,12 @@ static int bh_block(int64_t m, int precision) {
   const int64_t warps128 = (int64_t)grid_for(m, 128) * 4;
   return warps128 <= (int64_t)current_sms() * (FGA_BH32_TPS / 32) ? 128 : 64;
 }
+// whether a pass over m queries may run as split passes (launch_bh_iterate_t:
+// at most one wave)
+bool bh_split_possible(int64_t m) {
+  const int64_t nw = (int64_t)grid_for(m, 128) * 4;
+  return nw <= (int64_t)current_sms() * (FGA_BH32_TPS / 32);
+}
 int64_t bh_iterate_warps(int64_t m, int precision) {
   const int t = bh_block(m, precision);
   return (int64_t)grid_for(m, t) * (t / 32);
@@ -842,11 +878,21 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
       k_bh_iterate<float, false, false, kT, true><<<g, kT, tree_bytes, s>>>(r, nn, tv, st, sp, f, partials, nb);
     return;
   }
-  // small shards: record the warps' traces once, then split passes
+  }
+  // The first FP32 pass of a session records every warp's node trace and
+  // step count; later passes then run either as split passes (one wave with
+  // room to spare, or one wave whose heaviest warp exceeds FGA_SPLIT_IMB x the
+  // mean: inhomogeneous clouds) or with the blocks launched heaviest first.
   static const bool split_on = !(getenv("FGA_SPLIT") && atoi(getenv("FGA_SPLIT")) == 0);
+  static const bool order_on = !(getenv("FGA_LPT") && atoi(getenv("FGA_LPT")) == 0);
+  static const double split_imb = getenv("FGA_SPLIT_IMB") ? atof(getenv("FGA_SPLIT_IMB")) : 2.0;
+  static const bool split_log = getenv("FGA_SPLIT_LOG") != nullptr;  // (tests)
   const int64_t nw = (int64_t)nb * (kT / 32);
-  if (split_on && sb && sb->fpart && sb->apart && !sp.count_visits && nw >= 8 &&
-      FGA_SPLIT_WAVE * nw <= (int64_t)current_sms() * (FGA_BH32_TPS / 32)) {
+  const int64_t slots = (int64_t)current_sms() * (FGA_BH32_TPS / 32);
+  const bool split_cand = split_on && sb && sb->fpart && sb->apart && sb->split &&
+                          !sp.count_visits && nw >= 8 && nw <= slots;
+  const bool order_cand = order_on && sb && sb->order && !sp.count_visits;
+  if (split_cand || order_cand) {
     if (!*sb->have_trace) {
       if (gz)
         k_bh_iterate<float, true, false, kT, false, true><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f,
@@ -854,53 +900,61 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
       else
         k_bh_iterate<float, false, false, kT, false, true><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f,
                                                                           partials, nb, sb->trace);
+      bool split = false;
+      if (split_cand) {
+        if (FGA_SPLIT_WAVE * nw <= slots) {
+          split = true;
+        } else {  // a full wave: split only an imbalanced one (one sync, once per session)
+          unsigned long long* st2 = reinterpret_cast<unsigned long long*>(sb->tmp);
+          k_trace_stats<<<1, 1024, 0, s>>>(sb->trace, nw, st2);
+          unsigned long long h[2] = {0, 0};
+          if (cudaMemcpyAsync(h, st2, sizeof(h), cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+              cudaStreamSynchronize(s) == cudaSuccess && h[1] > 0)
+            split = (double)h[0] >= split_imb * ((double)h[1] / (double)nw);
+          if (split_log)
+            fprintf(stderr, "[fga] trace: %lld warps, max %llu mean %.0f -> %s\n", (long long)nw,
+                    h[0], (double)h[1] / (double)nw, split ? "split" : "unsplit");
+        }
+      }
+      *sb->split = split;
+      if (!split && order_cand) {
+        unsigned* kin = reinterpret_cast<unsigned*>(sb->okeys);
+        unsigned* kout = kin + nb;
+        int* vin = sb->okeys + 2 * nb;
+        k_block_work<<<(nb + 255) / 256, 256, 0, s>>>(sb->trace, nb, kT / 32, kin, vin);
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, kin, kout, vin, sb->order, nb,
+                                                  0, 32, s);
+        if (bytes <= sb->tmp_bytes &&
+            cub::DeviceRadixSort::SortPairsDescending(sb->tmp, bytes, kin, kout, vin, sb->order,
+                                                      nb, 0, 32, s) == cudaSuccess)
+          *sb->have_order = true;
+      }
       *sb->have_trace = true;
       return;
     }
-    static const bool split_log = getenv("FGA_SPLIT_LOG") != nullptr;  // (tests)
-    if (split_log) fprintf(stderr, "[fga] split pass: %lld warps x %d parts\n", (long long)nw, kParts);
-    const unsigned gs = (unsigned)((kParts * nw + kSplitT / 32 - 1) / (kSplitT / 32));
-    if (gz)
-      k_bh_split<true><<<gs, kSplitT, 0, s>>>(r, nn, tv, st, f, sp.theta2, sb->trace, nw,
-                                              sb->fpart, sb->apart);
-    else
-      k_bh_split<false><<<gs, kSplitT, 0, s>>>(r, nn, tv, st, f, sp.theta2, sb->trace, nw,
-                                               sb->fpart, sb->apart);
-    k_bh_split_epi<kT><<<g, kT, 0, s>>>(tv, st, sp, sb->fpart, sb->apart, partials, nb);
-    return;
-  }
-  }
-  // multi-wave passes: the first one records the warps' steps, the later
-  // ones launch the blocks heaviest first (LPT: a shorter tail)
-  static const bool order_on = !(getenv("FGA_LPT") && atoi(getenv("FGA_LPT")) == 0);
-  if (order_on && sb && sb->order && !sp.count_visits) {
-    if (!*sb->have_order) {
+    if (split_cand && *sb->split) {
+      if (split_log)
+        fprintf(stderr, "[fga] split pass: %lld warps x %d parts\n", (long long)nw, kParts);
+      const unsigned gs = (unsigned)((kParts * nw + kSplitT / 32 - 1) / (kSplitT / 32));
       if (gz)
-        k_bh_iterate<float, true, false, kT, false, true><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f,
-                                                                         partials, nb, sb->trace);
+        k_bh_split<true><<<gs, kSplitT, 0, s>>>(r, nn, tv, st, f, sp.theta2, sb->trace, nw,
+                                                sb->fpart, sb->apart);
       else
-        k_bh_iterate<float, false, false, kT, false, true><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f,
-                                                                          partials, nb, sb->trace);
-      unsigned* kin = reinterpret_cast<unsigned*>(sb->okeys);
-      unsigned* kout = kin + nb;
-      int* vin = sb->okeys + 2 * nb;
-      k_block_work<<<(nb + 255) / 256, 256, 0, s>>>(sb->trace, nb, kT / 32, kin, vin);
-      size_t bytes = 0;
-      cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, kin, kout, vin, sb->order, nb, 0,
-                                                32, s);
-      if (bytes <= sb->tmp_bytes &&
-          cub::DeviceRadixSort::SortPairsDescending(sb->tmp, bytes, kin, kout, vin, sb->order,
-                                                    nb, 0, 32, s) == cudaSuccess)
-        *sb->have_order = true;
+        k_bh_split<false><<<gs, kSplitT, 0, s>>>(r, nn, tv, st, f, sp.theta2, sb->trace, nw,
+                                                 sb->fpart, sb->apart);
+      k_bh_split_epi<kT><<<g, kT, 0, s>>>(tv, st, sp, sb->fpart, sb->apart, partials, nb);
       return;
     }
-    if (gz)
-      k_bh_iterate<float, true, false, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb,
-                                                            nullptr, sb->order);
-    else
-      k_bh_iterate<float, false, false, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb,
-                                                             nullptr, sb->order);
-    return;
+    if (order_cand && *sb->have_order) {
+      if (gz)
+        k_bh_iterate<float, true, false, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb,
+                                                              nullptr, sb->order);
+      else
+        k_bh_iterate<float, false, false, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials,
+                                                               nb, nullptr, sb->order);
+      return;
+    }
   }
   if (gz && sp.count_visits)
     k_bh_iterate<float, true, true, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb);
