@@ -482,13 +482,13 @@ int session_forces(fga_ctx* c, bool fuse = false) {
     nw = direct_iterate_warps(S.m_local, S.precision);
   } else {
     SplitBufs sb{nullptr, nullptr, nullptr, &S.split_traced};
-    if (!S.precision && S.m_local > 0) {
+    if (S.m_local > 0) {
       const int64_t nwq = (S.m_local + 31) / 32;
       FGA_CUDA_TRY(S.split_trace.reserve(sizeof(int) * 65 * (nwq + 8)));
       sb.trace = S.split_trace.as<int>();
       // the split parts' buffers only where split passes can run (a pass of
       // at most half the resident warps: forces.cu FGA_SPLIT_WAVE)
-      if (bh_split_possible(S.m_local)) {
+      if (!S.precision && bh_split_possible(S.m_local)) {
         FGA_CUDA_TRY(S.split_f.reserve(sizeof(double) * 3 * kSplitPartsMax * S.m_local));
         FGA_CUDA_TRY(S.split_a.reserve(sizeof(int) * kSplitPartsMax * S.m_local));
         sb.fpart = S.split_f.as<double>();

@@ -457,15 +457,20 @@ struct Trav64Out {
 // addresses: one L1 request per record per step; round 1 staged them through
 // a per-warp shared window that every skip past its end refilled: 30.3 ->
 // 28.6 ms at 1M).
+// trace (optional): the warp's step count -> trace[64] (the launch order of
+// later passes, forces.cu k_block_work)
 __device__ __forceinline__ Trav64Out traverse64d(const double4* __restrict__ A,
                                                  const NodeB64* __restrict__ B, int n_nodes,
                                                  double qx, double qy, double qz, double gq,
-                                                 bool active, double theta2, double eps2) {
+                                                 bool active, double theta2, double eps2,
+                                                 int* trace = nullptr) {
   Trav64Out o{0.0, 0.0, 0.0, 0, 0};
   int cursor = active ? 0 : n_nodes;
+  int steps = 0;
   while (true) {
     const int n = __reduce_min_sync(0xffffffffu, cursor);
     if (n >= n_nodes) break;
+    steps++;
     const double2 a01 = __ldg(reinterpret_cast<const double2*>(A + n));
     const double2 a23 = __ldg(reinterpret_cast<const double2*>(A + n) + 1);
     const double4 a = make_double4(a01.x, a01.y, a23.x, a23.y);
@@ -490,6 +495,7 @@ __device__ __forceinline__ Trav64Out traverse64d(const double4* __restrict__ A,
       }
     }
   }
+  if (trace && (threadIdx.x & 31) == 0) trace[64] = steps;
   return o;
 }
 

@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32
     na = o.accepted;
   } else {
     Trav64Out o = traverse64d(tr.a64, tr.b64, n_nodes, y[0], y[1], y[2], __dmul_rn(sp.G, mq),
-                              active, sp.theta2, sp.eps2);
+                              active, sp.theta2, sp.eps2,
+                              kTrace ? trace + gw * kTraceLen : nullptr);
     F[0] = o.fx;
     F[1] = o.fy;
     F[2] = o.fz;
@@ -846,6 +847,29 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
   const int nn = (int)T.n_nodes;
   const TreeRecords r = T.records();
   if (precision) {
+    // fp64: the heaviest-first block order too (the first pass records it)
+    static const bool order64 = !(getenv("FGA_LPT") && atoi(getenv("FGA_LPT")) == 0);
+    if (order64 && sb && sb->order) {
+      if (!*sb->have_order) {
+        k_bh_iterate<double, false, true, kT, false, true><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f,
+                                                                          partials, nb, sb->trace);
+        unsigned* kin = reinterpret_cast<unsigned*>(sb->okeys);
+        unsigned* kout = kin + nb;
+        int* vin = sb->okeys + 2 * nb;
+        k_block_work<<<(nb + 255) / 256, 256, 0, s>>>(sb->trace, nb, kT / 32, kin, vin);
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, kin, kout, vin, sb->order, nb,
+                                                  0, 32, s);
+        if (bytes <= sb->tmp_bytes &&
+            cub::DeviceRadixSort::SortPairsDescending(sb->tmp, bytes, kin, kout, vin, sb->order,
+                                                      nb, 0, 32, s) == cudaSuccess)
+          *sb->have_order = true;
+        return;
+      }
+      k_bh_iterate<double, false, true, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb,
+                                                             nullptr, sb->order);
+      return;
+    }
     k_bh_iterate<double, false, true, kT><<<g, kT, 0, s>>>(r, nn, tv, st, sp, f, partials, nb);
     return;
   }
