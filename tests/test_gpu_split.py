@@ -89,3 +89,39 @@ def test_heaviest_first_order_changes_nothing():
         outs.append(json.loads(out.stdout.strip().splitlines()[-1]))
     assert outs[0]["inter"] == outs[1]["inter"]
     assert np.array_equal(np.array(outs[0]["traj"]), np.array(outs[1]["traj"]))
+
+
+SWEEP_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, %r)
+import numpy as np
+import paper_2009_14005_b200 as fga
+from paper_2009_14005_b200 import synth
+out = {}
+for n, m in ((3000, 1500), (60000, 20000), (60000, 140000), (120000, 280000)):
+    rng = synth.rng_from_seed(n + m)
+    x = synth.blob(n, rng)
+    y = synth.misalign(synth.blob(m, synth.rng_from_seed(m)), synth.random_rigid(rng, 0.4, 0.05))
+    p = fga.default_params().replace(theta=0.5, G=66.7 * (2000 / n) ** 0.5, max_iters=5,
+                                     conv_tol=1e-300)
+    r = fga.register(x, y, params=p, options=fga.RegisterOptions(record_iterations=True))
+    out["%%d_%%d" %% (n, m)] = {"traj": r.trajectory.tolist(), "inter": r.interactions.tolist()}
+print(json.dumps(out))
+""" % ROOT
+
+
+def test_pass_schedules_agree_across_sizes():
+    """Every pass schedule (shared-memory small tree, split passes, heaviest-
+    first order, plain) gives the same accepted interactions and the same
+    trajectory to fp64 regrouping, across template sizes that select them."""
+    runs = []
+    for env in ({}, {"FGA_SPLIT": "0", "FGA_LPT": "0"}):
+        e = dict(os.environ, **env)
+        out = subprocess.run([sys.executable, "-c", SWEEP_SCRIPT], env=e, capture_output=True,
+                             text=True, timeout=900)
+        assert out.returncode == 0, out.stderr[-2000:]
+        runs.append(json.loads(out.stdout.strip().splitlines()[-1]))
+    for k in runs[0]:
+        assert runs[0][k]["inter"] == runs[1][k]["inter"], k
+        d = np.abs(np.array(runs[0][k]["traj"]) - np.array(runs[1][k]["traj"])).max()
+        assert d < 1e-10, (k, d)
