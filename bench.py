@@ -447,10 +447,10 @@ def traversal_roofline(force_s, visits, inter, m, peak_tflops, peak_src, fmax):
                  "work": f"{FLOP_PER_INTERACTION} FLOP/interaction + {FLOP_PER_VISIT} FLOP/visit"}
     out = {"kernel": "k_bh_iterate<float> (+k_qbound, k_node_bands, k_reduce)",
            "ms_per_launch": force_s * 1e3,
-           "traffic": prof.get("lts_bytes"),
-           "traffic_source": "ncu lts__t_sectors_srcunit_tex x 32 B per launch (L2->SM), "
+           "traffic": prof.get("dram_bytes"),
+           "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch, "
                              "profiles/traffic.json",
-           "dram_bytes": prof.get("dram_bytes"), "l1_hit_pct": prof.get("l1_hit_pct"),
+           "l2_to_sm_bytes": prof.get("lts_bytes"), "l1_hit_pct": prof.get("l1_hit_pct"),
            "l2_model_view": l2_view, "fp32_view": fp32_view}
     if prof.get("inst_executed"):
         issue_peak = 148 * 4 * fmax * 1e6  # warp-instructions per second
