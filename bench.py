@@ -556,7 +556,7 @@ def run_gpe(session, stream, n, m, peak, peak_src, fmax):
                         "peak_source": f"2*148*128*sm_max_mhz ({peak_src}, {fmax} MHz)",
                         "work": "20 FLOP-equivalent per pair (SURVEY §8(d) K11)",
                         "traffic": prof.get("dram_bytes"),
-                        "ncu_fma_pipe_pct": prof.get("fma_pipe_pct"),
+                        "ncu_fma_pipe_pct": prof.get("fma_pipe_pct"), "ncu_xu_pipe_pct": prof.get("xu_pipe_pct"),
                         "ncu_issue_active_pct": prof.get("issue_active_pct")}}
     return out
 
