@@ -86,6 +86,17 @@ struct fga_ctx {
   DevBuf tree_pts, tree_masses;
   DevBuf op[8];
   DevBuf op_total;               // device counter: accepted nodes of the last operator call
+  // one-wave FP32 operator calls (an N-way rank's slice): the split trace
+  // the last call over the same tree, query count and theta recorded
+  DevBuf op_trace, op_fpart, op_cnt;
+  struct OpSplitKey {
+    uint64_t generation = 0;
+    int64_t m = -1;
+    double theta = 0.0, eps2 = 0.0;
+    unsigned long long max_steps = 0;  // the heaviest warp's steps when traced
+    unsigned long long part_max = 0;   // the heaviest part's steps, first split call after
+    bool traced = false, split = false;
+  } op_split;
   // pinned staging ring of fga_register_batch_list (kStageSlots chunks)
   char* stage[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -653,6 +664,9 @@ int fga_destroy(fga_ctx* c) {
   c->batch_counter.release();
   c->batch_wide.release();
   c->op_total.release();
+  c->op_trace.release();
+  c->op_fpart.release();
+  c->op_cnt.release();
   for (int k = 0; k < 4; k++) {
     if (c->stage[k]) cudaFreeHost(c->stage[k]);
     if (c->stage_ev[k]) cudaEventDestroy(c->stage_ev[k]);
@@ -1530,14 +1544,48 @@ int fga_tree_forces(fga_ctx* c, const double* queries, const double* qm, int64_t
   long long* acc = vis + m;
   FGA_CUDA_TRY(c->op_total.reserve(sizeof(unsigned long long)));
   FGA_CUDA_TRY(cudaMemsetAsync(c->op_total.p, 0, sizeof(unsigned long long), s));
+  // one-wave FP32 calls: split passes from the previous call's trace (the
+  // first call over a tree / query count / theta records it, and its max and
+  // mean warp steps decide whether later calls split, as the session does)
+  OpSplitBufs ob{0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  fga_ctx::OpSplitKey& ok = c->op_split;
+  unsigned long long* stats = nullptr;
+  if (precision == FGA_PREC_FP32 && bh_operator_split_possible(m)) {
+    const bool same = ok.traced && ok.generation == c->tree.generation && ok.m == m &&
+                      ok.theta == theta && ok.eps2 == eps2;
+    const int64_t nw = bh_operator_warps(m);
+    if (!same) {
+      ok.traced = false;
+      FGA_CUDA_TRY(c->op_trace.reserve(sizeof(int) * 65 * nw + 2 * sizeof(unsigned long long)));
+      ob.mode = 1;
+    } else if (ok.split) {
+      const int64_t P = bh_split_parts();
+      FGA_CUDA_TRY(c->op_fpart.reserve(sizeof(double) * 3 * P * m));
+      FGA_CUDA_TRY(c->op_cnt.reserve(sizeof(int) * (2 * P * m + 65 * P * ((m + 31) / 32))));
+      ob.mode = 2;
+      ob.fpart = c->op_fpart.as<double>();
+      ob.vpart = c->op_cnt.as<int>();
+      ob.apart = ob.vpart + P * m;
+      ob.ptrace = ob.apart + P * m;
+    }
+    if (ob.mode) {
+      ob.trace = c->op_trace.as<int>();
+      // (8-byte aligned: 65 nw ints rounded up)
+      stats = reinterpret_cast<unsigned long long*>(c->op_trace.as<char>() +
+                                                    ((sizeof(int) * 65 * nw + 7) & ~size_t(7)));
+      ob.stats = stats;
+    }
+  }
   // Pinned (device-mapped) host outputs: the kernel stores each query's
   // results straight into them, so the device->host transfer overlaps the
   // traversal instead of following it
-  // (measured on the 1M drop-in: 14.00 -> 13.83 ms; FGA_ZERO_COPY=0 turns it off)
+  // (measured on the 1M drop-in: 14.00 -> 13.83 ms; FGA_ZERO_COPY=0 turns it off).
+  // Not for split passes: their epilogue would scatter every query's results
+  // over PCIe at the end of the call (125k queries: ~1.1 ms against a 4 MB copy)
   static const bool zc_on = !(getenv("FGA_ZERO_COPY") && atoi(getenv("FGA_ZERO_COPY")) == 0);
   double* fz = nullptr;
   long long* vz = nullptr;
-  if (zc_on && dim == 3) {
+  if (zc_on && dim == 3 && ob.mode != 2) {
     auto mapped = [](void* h) -> void* {
       cudaPointerAttributes a{};
       if (!h || cudaPointerGetAttributes(&a, h) != cudaSuccess) {
@@ -1552,7 +1600,7 @@ int fga_tree_forces(fga_ctx* c, const double* queries, const double* qm, int64_t
   }
   launch_bh_operator(c->tree, b, b + m, b + 2 * m, b + 3 * m, iout.as<int>(), m, theta, G, eps2,
                      fz ? fz : f, fz ? vz : (visits ? vis : nullptr), accepted ? acc : nullptr,
-                     c->op_total.as<unsigned long long>(), precision, s);
+                     c->op_total.as<unsigned long long>(), precision, s, ob.mode ? &ob : nullptr);
   FGA_CUDA_TRY(cudaGetLastError());
   std::vector<double> f3(dim == 3 ? 0 : 3 * m);
   if (!fz) {
@@ -1562,10 +1610,39 @@ int fga_tree_forces(fga_ctx* c, const double* queries, const double* qm, int64_t
       FGA_CUDA_TRY(cudaMemcpyAsync(visits, vis, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
   }
   if (accepted) FGA_CUDA_TRY(cudaMemcpyAsync(accepted, acc, sizeof(long long) * m, cudaMemcpyDeviceToHost, s));
-  unsigned long long total = 0;
+  unsigned long long total = 0, st2[2] = {0, 0};
   FGA_CUDA_TRY(cudaMemcpyAsync(&total, c->op_total.p, sizeof(total), cudaMemcpyDeviceToHost, s));
+  if (ob.mode)
+    FGA_CUDA_TRY(cudaMemcpyAsync(st2, stats, sizeof(st2), cudaMemcpyDeviceToHost, s));
   FGA_CUDA_TRY(cudaStreamSynchronize(s));
   c->last_interactions = (int64_t)total;
+  static const bool split_log = getenv("FGA_SPLIT_LOG") != nullptr;  // (tests)
+  if (ob.mode == 1) {
+    ok.generation = c->tree.generation;
+    ok.m = m;
+    ok.theta = theta;
+    ok.eps2 = eps2;
+    ok.max_steps = st2[0];
+    ok.part_max = 0;
+    ok.split = bh_operator_split_wanted(m, st2[0], st2[1]);
+    ok.traced = true;
+    if (split_log)
+      fprintf(stderr, "[fga] operator trace: %lld queries, max %llu sum %llu -> %s\n",
+              (long long)m, st2[0], st2[1], ok.split ? "split" : "unsplit");
+  } else if (ob.mode == 2) {
+    // the trace no longer balances these queries (another query set of the
+    // same size, or the template moved far): the heaviest part's steps grew
+    // past FGA_SPLIT_STALE x those of the first split call after the trace
+    // (a stale trace measured 3.6-4x) -> record a new one next call
+    static const double stale = getenv("FGA_SPLIT_STALE") ? atof(getenv("FGA_SPLIT_STALE")) : 2.0;
+    if (!ok.part_max)
+      ok.part_max = std::max<unsigned long long>(1, st2[0]);
+    else if ((double)st2[0] > stale * (double)ok.part_max)
+      ok.traced = false;
+    if (split_log)
+      fprintf(stderr, "[fga] operator split: %lld queries, part max %llu (trace max %llu)%s\n",
+              (long long)m, st2[0], ok.max_steps, ok.traced ? "" : " -> retrace");
+  }
   if (dim != 3) unpad3(f3.data(), m, dim, forces);
   return FGA_OK;
 }

@@ -278,8 +278,9 @@ __device__ __forceinline__ Trav32Out traverse32(const float4* __restrict__ A,
 // and re-decides the chain spanning lo by the same MAC without counting it.
 // kTrace: records the warp's node index every 256 steps (trace[0..63]) and
 // its step count (trace[64]) -- the split points of later passes.
+// kSteps: only the step count (trace[64]).
 template <bool kGuardZero, bool kCountVisits, bool kStatic = false, bool kSmem = false,
-          bool kRange = false, bool kTrace = false>
+          bool kRange = false, bool kTrace = false, bool kSteps = false>
 __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
                                                  const double4* __restrict__ A64,
                                                  const NodeB64* __restrict__ B64, int n_nodes,
@@ -311,8 +312,9 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
   // 16) | accepted of the current fold chunk -- at most FGA_FOLD node indices,
   // each visited at most once -- and the folds add it to the per-thread
   // totals in shared memory (hc[2 threadIdx.x ..])
-  static_assert(!(kRange && kCountVisits), "a split part counts accepted nodes only");
-  constexpr bool kPackable = kCountVisits && FGA_FOLD > 0 && FGA_FOLD <= 65535;
+  // a split part counts visits in plain registers (the operator's split
+  // passes, forces.cu k_bh_op_split): nodes before lo are not its visits
+  constexpr bool kPackable = kCountVisits && !kRange && FGA_FOLD > 0 && FGA_FOLD <= 65535;
   const bool packed = kPackable && hc != nullptr;
   unsigned cnt = 0;
   if (packed) hc[2 * threadIdx.x] = hc[2 * threadIdx.x + 1] = 0u;
@@ -334,8 +336,8 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     if (!kVote) n = __reduce_min_sync(0xffffffffu, cursor);
     if constexpr (kTrace) {
       if ((steps & 255) == 0 && (threadIdx.x & 31) == 0 && (steps >> 8) < 64) trace[steps >> 8] = n;
-      steps++;
     }
+    if constexpr (kTrace || kSteps) steps++;
     if (n >= lim) {  // exit, or fold the chunk's partial into the fp64 sum
       if (n >= end) break;
       if (hs) {
@@ -420,7 +422,7 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     } else if constexpr (kCountVisits) {
       asm("{\n\t.reg .pred p, q;\n\tsetp.ne.b32 p, %2, 0;\n\tsetp.ne.b32 q, %3, 0;\n\t"
           "@p add.s32 %0, %0, 1;\n\t@q add.s32 %1, %1, 1;\n\t}"
-          : "+r"(visits), "+r"(accepted) : "r"((int)mine), "r"((int)take));
+          : "+r"(visits), "+r"(accepted) : "r"((int)(mine && !pre)), "r"((int)take));
     } else {
       asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t@q add.s32 %0, %0, 1;\n\t}"
           : "+r"(accepted) : "r"((int)take));
@@ -430,7 +432,7 @@ __device__ __forceinline__ Trav32Out traverse32d(const float4* __restrict__ C,
     if (kVote)
       n = __any_sync(0xffffffffu, mine && !acc) ? n + 1 : min(__float_as_int(b.y), m_other);
   }
-  if constexpr (kTrace) {
+  if constexpr (kTrace || kSteps) {
     if ((threadIdx.x & 31) == 0) trace[64] = steps;
   }
   if (kPackable && packed) {

@@ -60,10 +60,29 @@ void launch_gpe(const RefPoints& ref, const double* px, const double* py, const 
 
 // Operator-level (no state): queries SoA fp64 (already in traversal order),
 // outputs scattered back through `order` (may be null = identity).
+// FP32 calls that fill at most one wave (bh_operator_split_possible) may run
+// as split passes: mode 1 records the warps' traces (ceil(m/32) x 65 ints)
+// and their max / sum of steps (stats[2]); mode 2 runs split passes from
+// them (fpart: 8 m x 3 doubles, vpart / apart: 8 m ints) and records the
+// parts' steps (ptrace: 8 x ceil(m/32) x 65 ints; their max / sum -> stats);
+// mode 0 plain.
+struct OpSplitBufs {
+  int mode;
+  int* trace;
+  unsigned long long* stats;
+  double* fpart;
+  int *vpart, *apart, *ptrace;
+};
+int bh_split_parts();
+bool bh_operator_split_possible(int64_t m);
+int64_t bh_operator_warps(int64_t m);
+bool bh_operator_split_wanted(int64_t m, unsigned long long max_steps,
+                              unsigned long long sum_steps);
 void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, const double* qz,
                         const double* qm, const int* order, int64_t m, double theta, double G,
                         double eps2, double* fout, long long* visits, long long* accepted,
-                        unsigned long long* acc_total, int precision, cudaStream_t s);
+                        unsigned long long* acc_total, int precision, cudaStream_t s,
+                        const OpSplitBufs* ob = nullptr);
 void launch_direct_operator(const RefPoints& ref, const double* qx, const double* qy,
                             const double* qz, const double* qm, int64_t m, double G, double eps,
                             double* fout, int precision, cudaStream_t s);

@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(kT) k_bh_split_epi(TemplateView tv, const Iter
 }
 
 // ---------------------------------------------------------------- BH operator
-template <typename Real, bool kGuardZero, int kT = kForceThreads>
+template <typename Real, bool kGuardZero, int kT = kForceThreads, bool kTrace = false>
 #ifndef FGA_BHOP_MINB
 #define FGA_BHOP_MINB 5  // 1280 threads/SM: fp64 operator 39.5 -> 38.7 ms (1M x 1M, host in/out)
 #endif
@@ -339,9 +339,10 @@ __global__ void __launch_bounds__(kT, sizeof(Real) == 4 ? FGA_BHOP32_TPS / kT
     const double* __restrict__ qz_, const double* __restrict__ qm_, const int* __restrict__ order,
     int64_t m, double theta2, double G, double eps2, F32Params f, double* __restrict__ fout,
     long long* __restrict__ visits, long long* __restrict__ accepted,
-    unsigned long long* __restrict__ acc_total) {
+    unsigned long long* __restrict__ acc_total, int* __restrict__ trace = nullptr) {
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int64_t i = ((int64_t)blockIdx.x * (kT / 32) + wl) * 32 + lane;
+  const int64_t gw = (int64_t)blockIdx.x * (kT / 32) + wl;
+  const int64_t i = gw * 32 + lane;
   const bool active = i < m;
   double F[3];
   int nv, na;
@@ -356,9 +357,10 @@ __global__ void __launch_bounds__(kT, sizeof(Real) == 4 ? FGA_BHOP32_TPS / kT
     }
     __shared__ double hs[3 * kT];
     __shared__ unsigned hc[2 * kT];
-    const Trav32Out o = traverse32d<kGuardZero, true>(
+    const Trav32Out o = traverse32d<kGuardZero, true, false, false, false, kTrace>(
         tr.c32, tr.a64, tr.b64, n_nodes, qf[0], qf[1], qf[2], active, f.theta2, theta2, f.eps2,
-        qx_, qy_, qz_, m, hs, 0.f, 0.f, -1, hc);
+        qx_, qy_, qz_, m, hs, 0.f, 0.f, -1, hc, nullptr, 0, -1,
+        kTrace ? trace + gw * kTraceLen : nullptr);
     const double gq = G * (active ? qm_[i] : 0.0);
     F[0] = gq * o.ax;
     F[1] = gq * o.ay;
@@ -390,6 +392,85 @@ __global__ void __launch_bounds__(kT, sizeof(Real) == 4 ? FGA_BHOP32_TPS / kT
   fout[dst * 3] = F[0];
   fout[dst * 3 + 1] = F[1];
   fout[dst * 3 + 2] = F[2];
+  if (visits) visits[dst] = nv;
+  if (accepted) accepted[dst] = na;
+}
+
+// One-shot operator calls that fill at most one wave (an N-way rank's slice
+// of the queries): the same split passes as the session's (k_bh_split), from
+// the trace the previous call over the same tree, query count and theta
+// recorded (k_bh_operator<kTrace>) -- in the reference's loop the template
+// moves a little per call, so the warps' step profiles carry over; any split
+// points give the same visits, accepted sets and (to fp64 regrouping) forces.
+template <bool kGuardZero>
+__global__ void __launch_bounds__(kSplitT, FGA_SPLIT_TPS / kSplitT) k_bh_op_split(
+    TreeRecords tr, int n_nodes, const double* __restrict__ qx_, const double* __restrict__ qy_,
+    const double* __restrict__ qz_, int64_t m, F32Params f, double theta2_64,
+    const int* __restrict__ trace, int64_t nwarps, double* __restrict__ fpart,
+    int* __restrict__ vpart, int* __restrict__ apart, int* __restrict__ ptrace) {
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (kSplitT / 32) + (threadIdx.x >> 5);
+  if (g >= kParts * nwarps) return;  // (whole warps)
+  const int64_t w = g % nwarps;      // part-major, as k_bh_split
+  const int part = (int)(g / nwarps);
+  const int64_t i = w * 32 + lane;
+  const bool active = i < m;
+  __shared__ double hs[3 * kSplitT];
+  __shared__ double qsh[3 * kSplitT];
+  double* q = qsh + 3 * threadIdx.x;
+  q[0] = active ? qx_[i] : 0.0;
+  q[1] = active ? qy_[i] : 0.0;
+  q[2] = active ? qz_[i] : 0.0;
+  int lo = 0, hi = 0;
+  for (int k = 1; k <= part + 1; k++) {
+    lo = hi;
+    hi = max(lo, split_point(trace, w, k, n_nodes));
+  }
+  // ptrace: the parts' own step counts (k_trace_stats -> whether the trace
+  // still balances this call's queries)
+  const Trav32Out o = traverse32d<kGuardZero, true, false, false, true, false, true>(
+      tr.c32, tr.a64, tr.b64, n_nodes, (float)q[0], (float)q[1], (float)q[2], active, f.theta2,
+      theta2_64, f.eps2, nullptr, nullptr, nullptr, m, hs, 0.f, 0.f, -1, nullptr, qsh, lo, hi,
+      ptrace + g * kTraceLen);
+  if (!active) return;
+  double* fp = fpart + (part * m + i) * 3;
+  fp[0] = o.ax;
+  fp[1] = o.ay;
+  fp[2] = o.az;
+  vpart[part * m + i] = o.visits;
+  apart[part * m + i] = o.accepted;
+}
+
+// the parts in node order -> G m_q sum, counts, scattered like k_bh_operator
+__global__ void __launch_bounds__(256) k_bh_op_split_epi(
+    const double* __restrict__ qm_, const int* __restrict__ order, int64_t m, double G,
+    const double* __restrict__ fpart, const int* __restrict__ vpart, const int* __restrict__ apart,
+    double* __restrict__ fout, long long* __restrict__ visits, long long* __restrict__ accepted,
+    unsigned long long* __restrict__ acc_total) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = i < m;
+  double h[3] = {0.0, 0.0, 0.0};
+  int nv = 0, na = 0;
+  if (active) {
+    for (int q = 0; q < kParts; q++) {
+      const double* fq = fpart + (q * m + i) * 3;
+      h[0] += fq[0];
+      h[1] += fq[1];
+      h[2] += fq[2];
+      nv += vpart[q * m + i];
+      na += apart[q * m + i];
+    }
+  }
+  if (acc_total) {
+    const unsigned wsum = __reduce_add_sync(0xffffffffu, active ? (unsigned)na : 0u);
+    if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(acc_total, (unsigned long long)wsum);
+  }
+  if (!active) return;
+  const double gq = G * qm_[i];
+  const int64_t dst = order ? order[i] : i;
+  fout[dst * 3] = gq * h[0];
+  fout[dst * 3 + 1] = gq * h[1];
+  fout[dst * 3 + 2] = gq * h[2];
   if (visits) visits[dst] = nv;
   if (accepted) accepted[dst] = na;
 }
@@ -1040,10 +1121,26 @@ void launch_gpe(const RefPoints& ref, const double* px, const double* py, const 
 // against 256)
 constexpr int kOpT = FGA_OP_T;
 
+bool bh_operator_split_possible(int64_t m) {
+  static const bool on = !(getenv("FGA_SPLIT") && atoi(getenv("FGA_SPLIT")) == 0);
+  const int64_t nw = (m + 31) / 32;
+  return on && nw >= 8 && nw <= (int64_t)current_sms() * (FGA_BHOP32_TPS / 32);
+}
+int64_t bh_operator_warps(int64_t m) { return (int64_t)grid_for(m, kOpT) * (kOpT / 32); }
+int bh_split_parts() { return kParts; }
+bool bh_operator_split_wanted(int64_t m, unsigned long long max_steps,
+                              unsigned long long sum_steps) {
+  static const double imb = getenv("FGA_SPLIT_IMB") ? atof(getenv("FGA_SPLIT_IMB")) : 2.0;
+  const int64_t nw = (m + 31) / 32;
+  if (FGA_SPLIT_WAVE * nw <= (int64_t)current_sms() * (FGA_BHOP32_TPS / 32)) return true;
+  return sum_steps > 0 && (double)max_steps >= imb * ((double)sum_steps / (double)nw);
+}
+
 void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, const double* qz,
                         const double* qm, const int* order, int64_t m, double theta, double G,
                         double eps2, double* fout, long long* visits, long long* accepted,
-                        unsigned long long* acc_total, int precision, cudaStream_t s) {
+                        unsigned long long* acc_total, int precision, cudaStream_t s,
+                        const OpSplitBufs* ob) {
   if (m <= 0) return;
   const double theta2 = theta * theta;
   const F32Params f{(float)theta2, (float)eps2};
@@ -1058,7 +1155,35 @@ void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, co
   }
   launch_node_bands(T, qx, qy, qz, m, nullptr, f.theta2, f.eps2, s);
   const unsigned g = grid_for(m, kOpT);
-  if (!(eps2 > 0.0))
+  const bool gz = !(eps2 > 0.0);
+  if (ob && ob->mode == 2) {
+    const int64_t nw = (m + 31) / 32;
+    const unsigned gs = (unsigned)((kParts * nw + kSplitT / 32 - 1) / (kSplitT / 32));
+    if (gz)
+      k_bh_op_split<true><<<gs, kSplitT, 0, s>>>(r, nn, qx, qy, qz, m, f, theta2, ob->trace, nw,
+                                                  ob->fpart, ob->vpart, ob->apart, ob->ptrace);
+    else
+      k_bh_op_split<false><<<gs, kSplitT, 0, s>>>(r, nn, qx, qy, qz, m, f, theta2, ob->trace, nw,
+                                                   ob->fpart, ob->vpart, ob->apart, ob->ptrace);
+    k_trace_stats<<<1, 1024, 0, s>>>(ob->ptrace, kParts * nw, ob->stats);
+    k_bh_op_split_epi<<<grid_for(m, 256), 256, 0, s>>>(qm, order, m, G, ob->fpart, ob->vpart,
+                                                       ob->apart, fout, visits, accepted,
+                                                       acc_total);
+    return;
+  }
+  if (ob && ob->mode == 1) {  // this call records the warps' traces (+ their max / sum)
+    if (gz)
+      k_bh_operator<float, true, kOpT, true><<<g, kOpT, 0, s>>>(
+          r, nn, qx, qy, qz, qm, order, m, theta2, G, eps2, f, fout, visits, accepted, acc_total,
+          ob->trace);
+    else
+      k_bh_operator<float, false, kOpT, true><<<g, kOpT, 0, s>>>(
+          r, nn, qx, qy, qz, qm, order, m, theta2, G, eps2, f, fout, visits, accepted, acc_total,
+          ob->trace);
+    k_trace_stats<<<1, 1024, 0, s>>>(ob->trace, (m + 31) / 32, ob->stats);
+    return;
+  }
+  if (gz)
     k_bh_operator<float, true, kOpT><<<g, kOpT, 0, s>>>(r, nn, qx, qy, qz, qm, order, m, theta2,
                                                         G, eps2, f, fout, visits, accepted,
                                                         acc_total);

@@ -125,3 +125,86 @@ def test_pass_schedules_agree_across_sizes():
         assert runs[0][k]["inter"] == runs[1][k]["inter"], k
         d = np.abs(np.array(runs[0][k]["traj"]) - np.array(runs[1][k]["traj"])).max()
         assert d < 1e-10, (k, d)
+
+
+OP_SCRIPT = r"""
+import json, sys
+sys.path.insert(0, %r)
+import ctypes
+import numpy as np
+import torch
+from paper_2009_14005_b200 import PointCloud, bhtree, synth
+from paper_2009_14005_b200 import _native as N
+rng = synth.rng_from_seed(7)
+x = synth.blob(200000, rng)
+mx = rng.uniform(0.005, 0.02, len(x))
+bhtree.build(PointCloud(x.points), mx, 20)
+c = N.context(0)
+L = N.lib()
+out = {}
+for m, pinned in ((3000, False), (25000, True), (3000, True)):
+    q = np.ascontiguousarray(synth.blob(m, synth.rng_from_seed(m)).points)
+    qm = synth.rng_from_seed(m + 1).uniform(0.02, 0.1, m)
+    runs = []
+    for call in range(3):
+        if pinned:
+            f = torch.zeros((m, 3), dtype=torch.float64, pin_memory=True).numpy()
+            vis = torch.zeros(m, dtype=torch.int64, pin_memory=True).numpy()
+        else:
+            f, vis = np.zeros((m, 3)), np.zeros(m, np.int64)
+        acc = np.zeros(m, np.int64)
+        t = N._i64(-1)
+        N.check(L.fga_tree_forces(c.handle, N.ptr(q), N.ptr(qm), m, 0.5, 1.0, 0.04, 0,
+                                  N.ptr(f), N.ptr(vis), N.ptr(acc)))
+        N.check(L.fga_last_interactions(c.handle, ctypes.byref(t)))
+        runs.append((f.copy(), vis.copy(), acc.copy(), t.value))
+    (f0, v0, a0, t0) = runs[0]
+    out[f"{m}-{pinned}"] = {
+        "vis_equal": all(np.array_equal(v0, r[1]) for r in runs),
+        "acc_equal": all(np.array_equal(a0, r[2]) for r in runs),
+        "total_equal": all(t0 == r[3] == int(a0.sum()) for r in runs),
+        "frel": max(float(np.abs(r[0] - f0).max() / np.abs(f0).max()) for r in runs),
+        "f0": f0[:64].tolist(), "v0": v0[:64].tolist(), "acc_sum": int(a0.sum())}
+print(json.dumps(out))
+""" % ROOT
+
+
+def _run_op(split):
+    env = dict(os.environ, FGA_SPLIT="1" if split else "0", FGA_SPLIT_LOG="1")
+    out = subprocess.run([sys.executable, "-c", OP_SCRIPT], env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1]), out.stderr
+
+
+def test_operator_split_passes_match_unsplit(orc):
+    """One-wave fga_tree_forces calls (an N-way rank's slice of the queries):
+    the first call over a tree / query count / theta records the warps'
+    traces, later calls run as split passes.  Visits, accepted counts and the
+    interaction total are identical to the unsplit calls; forces agree to
+    fp64 regrouping; pageable and pinned (zero-copy) outputs; a new query
+    count records a new trace."""
+    a, err = _run_op(True)
+    b, err0 = _run_op(False)
+    assert "operator trace: 3000 queries" in err and "-> split" in err
+    assert err.count("operator trace:") == 3  # 3000, 25000, then 3000 again
+    assert "operator trace" not in err0
+    for k in a:
+        assert a[k]["vis_equal"] and a[k]["acc_equal"] and a[k]["total_equal"], k
+        assert a[k]["frel"] < 1e-12, (k, a[k]["frel"])
+        assert b[k]["frel"] == 0.0
+        assert a[k]["v0"] == b[k]["v0"] and a[k]["acc_sum"] == b[k]["acc_sum"]
+        assert np.abs(np.array(a[k]["f0"]) - np.array(b[k]["f0"])).max() <= 1e-12 * np.abs(
+            np.array(b[k]["f0"])).max()
+    # and the oracle's visits on the first queries
+    from paper_2009_14005_b200 import synth
+    rng = synth.rng_from_seed(7)
+    x = synth.blob(200000, rng)
+    mx = rng.uniform(0.005, 0.02, len(x))
+    tree = orc.tree_build(x.points, mx, 20)
+    q = np.ascontiguousarray(synth.blob(3000, synth.rng_from_seed(3000)).points)
+    qm = synth.rng_from_seed(3001).uniform(0.02, 0.1, 3000)
+    of, ovis, oacc = orc.bh_forces(tree, q[:64], qm[:64], 0.5, 1.0, 0.2, 1)
+    assert np.array_equal(np.array(a["3000-False"]["v0"]), ovis)
+    np.testing.assert_allclose(np.array(a["3000-False"]["f0"]), of, rtol=1e-5,
+                               atol=1e-5 * np.abs(of).max())
