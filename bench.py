@@ -586,38 +586,55 @@ def run_e2e(args, x, y, rank, world, local_rank):
     c = N.context(local_rank)
     bhtree.build(xn, mx, 20)  # the operator tree of this context (outside the timing)
     m = len(yn)
-    lo, hi = m * rank // world, m * (rank + 1) // world
-    mm = hi - lo
+    L = N.lib()
+    total = N._i64(0)
 
     def pinned(shape, dtype):
         return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
 
-    q = pinned((mm, 3), torch.float64)
-    q[:] = yn.points[lo:hi]
-    qm = pinned((mm,), torch.float64)
-    qm[:] = my[lo:hi]
-    f = pinned((mm, 3), torch.float64)
-    vis = pinned((mm,), torch.int64)
-    L = N.lib()
-    total = N._i64(0)
+    def slice_calls(lo, hi, sync):
+        mm = hi - lo
+        q = pinned((mm, 3), torch.float64)
+        q[:] = yn.points[lo:hi]
+        qm = pinned((mm,), torch.float64)
+        qm[:] = my[lo:hi]
+        f = pinned((mm, 3), torch.float64)
+        vis = pinned((mm,), torch.int64)
 
-    def call():
-        # the reference's outputs (forces, visits); the interaction count of
-        # the call comes back as one integer (fga_last_interactions)
-        N.check(L.fga_tree_forces(c.handle, N.ptr(q), N.ptr(qm), mm, float(args.theta),
-                                  float(p.G), float(p.epsilon) ** 2, N.PREC_FP32, N.ptr(f),
-                                  N.ptr(vis), None))
-        N.check(L.fga_last_interactions(c.handle, ctypes.byref(total)))
+        def call():
+            # the reference's outputs (forces, visits); the interaction count
+            # of the call comes back as one integer (fga_last_interactions)
+            N.check(L.fga_tree_forces(c.handle, N.ptr(q), N.ptr(qm), mm, float(args.theta),
+                                      float(p.G), float(p.epsilon) ** 2, N.PREC_FP32, N.ptr(f),
+                                      N.ptr(vis), None))
+            N.check(L.fga_last_interactions(c.handle, ctypes.byref(total)))
 
-    for _ in range(2):
-        call()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        call()
-    wall = time.perf_counter() - t0
-    t = torch.tensor([wall, float(total.value)], dtype=torch.float64,
+        # two untimed calls: the first over a new query count records the
+        # warps' traces (one-wave calls then run as split passes)
+        for _ in range(2):
+            call()
+        if sync:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            call()
+        return time.perf_counter() - t0, q, qm, f, vis
+
+    lo, hi = m * rank // world, m * (rank + 1) // world
+    wall, q, qm, f, vis = slice_calls(lo, hi, world > 1)
+    inter_call = float(total.value)
+    extra = {}
+    if world == 1 and not args.no_small_m:
+        # one rank's slice of an 8-GPU run (rank 3: queries 375k..500k of
+        # the template), the same call on this GPU
+        w8, *_ = slice_calls(3 * m // 8, 4 * m // 8, False)
+        extra["rank_slice_8"] = {
+            "queries": 4 * m // 8 - 3 * m // 8, "ms_per_call": 1e3 * w8 / args.steps,
+            "interactions_per_s": float(total.value) * args.steps / w8,
+            "note": "rank 3's slice of an 8-way run (template rows m*3/8..m*4/8), "
+                    "fga_tree_forces from pinned host buffers, wall clock; a one-wave call: "
+                    "split passes from the previous call's trace (forces.cu k_bh_op_split)"}
+    t = torch.tensor([wall, inter_call], dtype=torch.float64,
                      device=torch.device("cuda", local_rank))
     if world > 1:
         tmax = t[:1].clone()
@@ -634,7 +651,7 @@ def run_e2e(args, x, y, rank, world, local_rank):
             "api": "fga_tree_forces (drop-in for _kernels.bh_forces_kernel: forces + visits "
                    "out, + fga_last_interactions for the count), pinned host buffers, initial "
                    "template state, FP32 traversal, wall clock per rank, max over ranks",
-            "visits_per_query": float(vis.mean())}
+            "visits_per_query": float(vis.mean()), **extra}
 
 
 _L2_CACHE = {}
