@@ -28,6 +28,8 @@ bool bh_split_possible(int64_t m);
 int64_t direct_iterate_warps(int64_t m, int precision);
 int64_t gpe_warps(int64_t m, int64_t n, int precision);
 
+constexpr int kTraceLen = 65;  // per-warp split trace: 64 node indices + the step count
+
 // One force pass of the iteration: applies the pending transform, evaluates
 // forces, fused Euler-Cromer step, per-warp Kabsch partials.
 // split passes of small template shards (forces.cu k_bh_split): the warps'

@@ -65,7 +65,6 @@ struct F32Params {
 // points: every step's record load is then a shared-memory load instead of an
 // L1/L2 round trip on a cold SM)
 constexpr int kSmallTreeBytes = 200 * 1024;
-constexpr int kTraceLen = 65;  // per-warp split trace: 64 node indices + the step count
 template <typename Real, bool kGuardZero, bool kCountVisits, int kT, bool kSmall = false,
           bool kTrace = false>
 __global__ void __launch_bounds__(kT, kSmall ? 1 : (sizeof(Real) == 4 ? FGA_BH32_TPS : FGA_BH64_TPS) / kT) k_bh_iterate(

@@ -21,7 +21,10 @@ xt = torch.from_numpy(np.array(x.points)).to(dev)
 yt = torch.from_numpy(np.array(y.points)).to(dev)
 st = torch.cuda.current_stream()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-for shard in ((0, 1), (0, 2), (0, 4), (0, 8), (3, 8), (7, 8)):
+ALL = os.environ.get("SMALLM_ALL")  # e.g. "2,4,8": every shard of those counts
+shards = ([(r, n) for n in map(int, ALL.split(",")) for r in range(n)] if ALL else
+          ((0, 1), (0, 2), (0, 4), (0, 8), (3, 8), (7, 8)))
+for shard in shards:
     s = Session(None, None, p, fga.RegisterOptions(compute_gpe=False), shard_rank=shard[0],
                 shard_count=shard[1], stream=st.cuda_stream,
                 device_inputs=(xt.data_ptr(), len(x), yt.data_ptr(), len(y)), ctx=N.Context(0))
