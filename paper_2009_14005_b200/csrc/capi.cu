@@ -1556,12 +1556,14 @@ int fga_tree_forces(fga_ctx* c, const double* queries, const double* qm, int64_t
     const int64_t nw = bh_operator_warps(m);
     if (!same) {
       ok.traced = false;
-      FGA_CUDA_TRY(c->op_trace.reserve(sizeof(int) * kTraceLen * nw + 2 * sizeof(unsigned long long) + 8));
+      FGA_CUDA_TRY(c->op_trace.reserve(sizeof(int) * kTraceLen * nw +
+                                       2 * sizeof(unsigned long long) + 8));
       ob.mode = 1;
     } else if (ok.split) {
       const int64_t P = bh_split_parts();
       FGA_CUDA_TRY(c->op_fpart.reserve(sizeof(double) * 3 * P * m));
-      FGA_CUDA_TRY(c->op_cnt.reserve(sizeof(int) * (2 * P * m + kTraceLen * P * ((m + 31) / 32))));
+      FGA_CUDA_TRY(
+          c->op_cnt.reserve(sizeof(int) * (2 * P * m + kTraceLen * P * ((m + 31) / 32))));
       ob.mode = 2;
       ob.fpart = c->op_fpart.as<double>();
       ob.vpart = c->op_cnt.as<int>();
@@ -1571,8 +1573,8 @@ int fga_tree_forces(fga_ctx* c, const double* queries, const double* qm, int64_t
     if (ob.mode) {
       ob.trace = c->op_trace.as<int>();
       // (8-byte aligned: kTraceLen nw ints rounded up)
-      stats = reinterpret_cast<unsigned long long*>(c->op_trace.as<char>() +
-                                                    ((sizeof(int) * kTraceLen * nw + 7) & ~size_t(7)));
+      const size_t off = (sizeof(int) * kTraceLen * nw + 7) & ~size_t(7);
+      stats = reinterpret_cast<unsigned long long*>(c->op_trace.as<char>() + off);
       ob.stats = stats;
     }
   }
