@@ -208,3 +208,31 @@ def test_operator_split_passes_match_unsplit(orc):
     assert np.array_equal(np.array(a["3000-False"]["v0"]), ovis)
     np.testing.assert_allclose(np.array(a["3000-False"]["f0"]), of, rtol=1e-5,
                                atol=1e-5 * np.abs(of).max())
+
+
+@pytest.mark.parametrize("case", ["forces", "two_d"])
+def test_operator_split_calls_match_reference_golden(golden, case):
+    """Repeated FP32 bh_forces calls over the same tree and query count: the
+    first records the warps' traces, the later ones run as split passes
+    (>= 8 warps, one wave).  Every call reproduces the REFERENCE's visits
+    (golden vectors from the reference itself) and its forces within 1e-5;
+    the split calls equal the first to 1e-12.  D=3 (500 queries) and D=2
+    (the 150 golden queries tiled to 450)."""
+    import paper_2009_14005_b200 as fga
+    from paper_2009_14005_b200 import bhtree
+    g = golden(case)
+    theta = 0.5 if case == "two_d" else 0.3
+    q, qm = g["q"], g["qm"]
+    ref_f, ref_v = g[f"bh/theta{theta}/forces"], g[f"bh/theta{theta}/visits"]
+    if case == "two_d":
+        q, qm = np.tile(q, (3, 1)), np.tile(qm, 3)
+        ref_f, ref_v = np.tile(ref_f, (3, 1)), np.tile(ref_v, 3)
+    t = bhtree.build(fga.PointCloud(g["x"]), g["xm"], 20)
+    p = fga.default_params().replace(theta=theta)
+    runs = [bhtree.bh_forces(t, q, qm, p, count_visits=True, precision="fp32")
+            for _ in range(3)]
+    for f, v in runs:
+        assert np.array_equal(v, ref_v)
+        rel = np.linalg.norm(f - ref_f, axis=1) / np.linalg.norm(ref_f, axis=1)
+        assert rel.max() < 1e-5
+        assert np.abs(f - runs[0][0]).max() <= 1e-12 * np.abs(runs[0][0]).max()
