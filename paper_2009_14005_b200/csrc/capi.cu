@@ -280,6 +280,63 @@ int morton_order(const double* pts, int64_t n, DevBuf& kin, DevBuf& kout, DevBuf
 }
 
 // -------------------------------------------------------------------- session
+
+// every stride-th entry of a permutation (balanced_cut's query sample)
+__global__ void k_capi_strided_order(const int* __restrict__ order, int64_t ms, int64_t stride,
+                                     int* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < ms) out[i] = order[i * stride];
+}
+
+// Template shards of equal COST instead of equal count (shard_count > 1, BH):
+// the per-query visit counts of every stride-th template point in Morton
+// order (one FP32 operator pass over <= 65,536 sampled queries, identical on
+// every rank: same inputs, integer counts), their running sum, and rank r's
+// chunk between the sample positions where it crosses r/N and (r+1)/N of the
+// total.  Equal-count shards of the 1M pair differed by up to 1.2x in cost
+// (tools/smallm_timing.py).  FGA_SHARD_BALANCE=0: equal counts.
+int balanced_cut(Session& S, int64_t m, cudaStream_t s) {
+  static const bool on = !(getenv("FGA_SHARD_BALANCE") && atoi(getenv("FGA_SHARD_BALANCE")) == 0);
+  if (!on || m < 2 * (int64_t)S.shard_count) return FGA_OK;
+  const int64_t stride = std::max<int64_t>(1, (m + 65535) / 65536);
+  const int64_t ms = (m + stride - 1) / stride;
+  DevBuf ord, q, out;
+  FGA_CUDA_TRY(ord.reserve(sizeof(int) * ms));
+  FGA_CUDA_TRY(q.reserve(sizeof(double) * 4 * ms));
+  FGA_CUDA_TRY(out.reserve(sizeof(double) * 3 * ms + sizeof(long long) * ms));
+  k_capi_strided_order<<<(unsigned)((ms + 255) / 256), 256, 0, s>>>(
+      S.tidx.as<int>(), ms, stride, ord.as<int>());
+  double* b = q.as<double>();
+  launch_gather_queries(S.yn.as<double>(), S.my.as<double>(), ord.as<int>(), ms, b, b + ms,
+                        b + 2 * ms, b + 3 * ms, s);
+  long long* vis = reinterpret_cast<long long*>(out.as<double>() + 3 * ms);
+  launch_bh_operator(S.tree, b, b + ms, b + 2 * ms, b + 3 * ms, nullptr, ms, S.P.theta, S.sp.G,
+                     S.sp.eps2, out.as<double>(), vis, nullptr, nullptr, FGA_PREC_FP32, s);
+  std::vector<long long> v(ms);
+  FGA_CUDA_TRY(cudaMemcpyAsync(v.data(), vis, sizeof(long long) * ms, cudaMemcpyDeviceToHost, s));
+  FGA_CUDA_TRY(cudaStreamSynchronize(s));
+  double total = 0.0;
+  for (long long x : v) total += (double)x;
+  if (!(total > 0.0)) return FGA_OK;
+  // the first sample index whose running sum reaches frac * total, as a
+  // template position (ranks 0 and N get 0 and m)
+  auto cut = [&](int r) -> int64_t {
+    if (r <= 0) return 0;
+    if (r >= S.shard_count) return m;
+    const double target = total * (double)r / (double)S.shard_count;
+    double c = 0.0;
+    for (int64_t j = 0; j < ms; j++) {
+      c += (double)v[j];
+      if (c >= target) return std::min<int64_t>(m, (j + 1) * stride);
+    }
+    return m;
+  };
+  const int64_t b0 = cut(S.shard_rank), b1 = cut(S.shard_rank + 1);
+  S.m_begin = b0;
+  S.m_local = std::max<int64_t>(0, b1 - b0);
+  return FGA_OK;
+}
+
 int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
   Session& S = c->S;
   cudaStream_t s = c->stream;
@@ -375,6 +432,7 @@ int session_setup(fga_ctx* c, const double* x_dev, const double* y_dev) {
                    S.scratch, s));
   S.m_begin = m * S.shard_rank / S.shard_count;
   S.m_local = m * (S.shard_rank + 1) / S.shard_count - S.m_begin;
+  if (S.shard_count > 1 && !S.direct) TRY(balanced_cut(S, m, s));
   FGA_CUDA_TRY(S.tpl.reserve(sizeof(double) * 7 * std::max<int64_t>(S.m_local, 1)));
   launch_gather_template(S.yn.as<double>(), S.my.as<double>(), S.tidx.as<int>(), S.m_begin,
                          S.m_local, S.view(), s);
@@ -498,7 +556,7 @@ int session_forces(fga_ctx* c, bool fuse = false) {
       FGA_CUDA_TRY(S.split_trace.reserve(sizeof(int) * kTraceLen * (nwq + 8)));
       sb.trace = S.split_trace.as<int>();
       // the split parts' buffers only where split passes can run (a pass of
-      // at most half the resident warps: forces.cu FGA_SPLIT_WAVE)
+      // at most one wave: forces.cu bh_split_possible)
       if (!S.precision && bh_split_possible(S.m_local)) {
         FGA_CUDA_TRY(S.split_f.reserve(sizeof(double) * 3 * kSplitPartsMax * S.m_local));
         FGA_CUDA_TRY(S.split_a.reserve(sizeof(int) * kSplitPartsMax * S.m_local));

@@ -50,8 +50,11 @@ struct F32Params {
 // Measured and not kept: the query in shared memory (15.3 ms at 1792),
 // L1 prefetch of node n+1 (+1%) or of skip(n) (+7%).
 // fp64 traversal: 768 -> 35.8 ms, 1024 -> 31.5, 1280 -> 30.3, 1536 -> 38 (spills)
-#ifndef FGA_SPLIT_WAVE
-#define FGA_SPLIT_WAVE 2  // split passes when the warps fill <= 1/FGA_SPLIT_WAVE of the slots
+#ifndef FGA_SPLIT_FRAC
+// split passes whenever the warps fill <= this fraction of the resident slots
+// (3,907 warps of an 8-way shard: 2.82 -> 2.30 ms; a cost-balanced shard of
+// 4,168 warps: 2.76 -> 2.25 ms; 7,813 warps of a 4-way shard: slower)
+#define FGA_SPLIT_FRAC 0.6
 #endif
 #ifndef FGA_BH32_TPS
 #define FGA_BH32_TPS 1792
@@ -1006,7 +1009,7 @@ static void launch_bh_iterate_t(const TreeDev& T, const TemplateView& tv, const 
                                                                           partials, nb, sb->trace);
       bool split = false;
       if (split_cand) {
-        if (FGA_SPLIT_WAVE * nw <= slots) {
+        if ((double)nw <= FGA_SPLIT_FRAC * (double)slots) {
           split = true;
         } else {  // a full wave: split only an imbalanced one (one sync, once per session)
           unsigned long long* st2 = reinterpret_cast<unsigned long long*>(sb->tmp);
@@ -1131,7 +1134,7 @@ bool bh_operator_split_wanted(int64_t m, unsigned long long max_steps,
                               unsigned long long sum_steps) {
   static const double imb = getenv("FGA_SPLIT_IMB") ? atof(getenv("FGA_SPLIT_IMB")) : 2.0;
   const int64_t nw = (m + 31) / 32;
-  if (FGA_SPLIT_WAVE * nw <= (int64_t)current_sms() * (FGA_BHOP32_TPS / 32)) return true;
+  if ((double)nw <= FGA_SPLIT_FRAC * (double)current_sms() * (FGA_BHOP32_TPS / 32)) return true;
   return sum_steps > 0 && (double)max_steps >= imb * ((double)sum_steps / (double)nw);
 }
 
