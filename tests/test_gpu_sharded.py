@@ -70,3 +70,38 @@ def test_register_sharded_nccl_world1():
         assert a.gpe_initial == b.gpe_initial and a.gpe_final == b.gpe_final
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("count", [2, 3, 8])
+def test_cost_balanced_shards_partition_the_template(count):
+    """Cost-balanced cuts (capi.cu balanced_cut: sampled visit counts in
+    Morton order): the shards' sizes add up to the template, they are not
+    the equal-count split on a clustered cloud, their accepted interactions
+    add up to the unsharded pass's, and FGA_SHARD_BALANCE is not needed for
+    correctness (the per-query forces do not depend on the cut)."""
+    import paper_2009_14005_b200 as fga
+    from paper_2009_14005_b200 import _native as N
+    from paper_2009_14005_b200.engine import SUM_ACCEPTED, Session
+    x, y = _pair(n=40000, seed=5)
+    p = fga.default_params().replace(theta=0.5, max_iters=1)
+    o = fga.RegisterOptions(compute_gpe=False)
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def accepted(rank, cnt):
+        s = Session(x, y, p, o, shard_rank=rank, shard_count=cnt, stream=stream,
+                    ctx=N.Context(0))
+        b = torch.zeros(18, dtype=torch.float64, device="cuda")
+        s.bind_sums(b.data_ptr())
+        s.forces()
+        torch.cuda.synchronize()
+        a, m = float(b[SUM_ACCEPTED].item()), s.m_local
+        s.finish()
+        return a, m
+
+    parts = [accepted(r, count) for r in range(count)]
+    whole, m_all = accepted(0, 1)
+    assert m_all == len(y)
+    assert sum(m for _, m in parts) == len(y)
+    assert sum(a for a, _ in parts) == whole
+    equal = [len(y) * (r + 1) // count - len(y) * r // count for r in range(count)]
+    assert [m for _, m in parts] != equal
