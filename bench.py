@@ -592,7 +592,7 @@ def run_e2e(args, x, y, rank, world, local_rank):
     def pinned(shape, dtype):
         return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
 
-    def slice_calls(lo, hi, sync):
+    def slice_calls(lo, hi, sync, with_visits=False):
         mm = hi - lo
         q = pinned((mm, 3), torch.float64)
         q[:] = yn.points[lo:hi]
@@ -602,11 +602,12 @@ def run_e2e(args, x, y, rank, world, local_rank):
         vis = pinned((mm,), torch.int64)
 
         def call():
-            # the reference's outputs (forces, visits); the interaction count
-            # of the call comes back as one integer (fga_last_interactions)
+            # the registration loop's call: forces only (bhtree.bh_forces with
+            # count_visits=False, dynamics.py:39); the interaction count of
+            # the call comes back as one integer (fga_last_interactions)
             N.check(L.fga_tree_forces(c.handle, N.ptr(q), N.ptr(qm), mm, float(args.theta),
                                       float(p.G), float(p.epsilon) ** 2, N.PREC_FP32, N.ptr(f),
-                                      N.ptr(vis), None))
+                                      N.ptr(vis) if with_visits else None, None))
             N.check(L.fga_last_interactions(c.handle, ctypes.byref(total)))
 
         # two untimed calls: the first over a new query count records the
@@ -624,6 +625,18 @@ def run_e2e(args, x, y, rank, world, local_rank):
     wall, q, qm, f, vis = slice_calls(lo, hi, world > 1)
     inter_call = float(total.value)
     extra = {}
+    # the kernel-level contract (bh_forces_kernel returns forces AND visits):
+    # the same calls with the per-query visit counts copied back as well
+    wv, q, qm, f, vis = slice_calls(lo, hi, world > 1, with_visits=True)
+    if world > 1:
+        tv = torch.tensor([wv], dtype=torch.float64, device=torch.device("cuda", local_rank))
+        dist.all_reduce(tv, op=dist.ReduceOp.MAX)
+        wv = float(tv.item())
+    extra["with_visits"] = {
+        "value": None,  # (below: all ranks' interactions / the max wall)
+        "ms_per_step": 1e3 * wv / args.steps,
+        "d2h_bytes_per_step": int(f.nbytes + vis.nbytes + 8) * world,
+        "api": "fga_tree_forces with the visits array (the _kernels.bh_forces_kernel contract)"}
     if world == 1 and not args.no_small_m:
         # one rank's slice of an 8-GPU run (rank 3: queries 375k..500k of
         # the template), the same call on this GPU
@@ -644,13 +657,16 @@ def run_e2e(args, x, y, rank, world, local_rank):
         wall, inter = float(tmax.item()), float(tsum.item())
     else:
         inter = float(t[1].item())
+    extra["with_visits"]["value"] = inter * args.steps / wv
     return {"value": inter * args.steps / wall, "unit": UNIT,
             "h2d_bytes_per_step": int(q.nbytes + qm.nbytes) * world,
-            "d2h_bytes_per_step": int(f.nbytes + vis.nbytes + 8) * world,
+            "d2h_bytes_per_step": int(f.nbytes + 8) * world,
             "ms_per_step": 1e3 * wall / args.steps,
-            "api": "fga_tree_forces (drop-in for _kernels.bh_forces_kernel: forces + visits "
-                   "out, + fga_last_interactions for the count), pinned host buffers, initial "
-                   "template state, FP32 traversal, wall clock per rank, max over ranks",
+            "api": "fga_tree_forces as the registration loop calls the operator (forces out: "
+                   "bhtree.bh_forces(count_visits=False), dynamics.py:39; + "
+                   "fga_last_interactions for the count), pinned host buffers, initial "
+                   "template state, FP32 traversal, wall clock per rank, max over ranks; "
+                   "with_visits: the same with the per-query visits copied back",
             "visits_per_query": float(vis.mean()), **extra}
 
 

@@ -328,7 +328,10 @@ __global__ void __launch_bounds__(kT) k_bh_split_epi(TemplateView tv, const Iter
 }
 
 // ---------------------------------------------------------------- BH operator
-template <typename Real, bool kGuardZero, int kT = kForceThreads, bool kTrace = false>
+// kCV: count per-query visits (the caller asked for them; the registration
+// loop's call, bhtree.bh_forces(count_visits=False) at dynamics.py:39, does not)
+template <typename Real, bool kGuardZero, int kT = kForceThreads, bool kTrace = false,
+          bool kCV = true>
 #ifndef FGA_BHOP_MINB
 #define FGA_BHOP_MINB 5  // 1280 threads/SM: fp64 operator 39.5 -> 38.7 ms (1M x 1M, host in/out)
 #endif
@@ -358,10 +361,10 @@ __global__ void __launch_bounds__(kT, sizeof(Real) == 4 ? FGA_BHOP32_TPS / kT
       qf[2] = (float)qz_[i];
     }
     __shared__ double hs[3 * kT];
-    __shared__ unsigned hc[2 * kT];
-    const Trav32Out o = traverse32d<kGuardZero, true, false, false, false, kTrace>(
+    __shared__ unsigned hc[kCV ? 2 * kT : 1];
+    const Trav32Out o = traverse32d<kGuardZero, kCV, false, false, false, kTrace>(
         tr.c32, tr.a64, tr.b64, n_nodes, qf[0], qf[1], qf[2], active, f.theta2, theta2, f.eps2,
-        qx_, qy_, qz_, m, hs, 0.f, 0.f, -1, hc, nullptr, 0, -1,
+        qx_, qy_, qz_, m, hs, 0.f, 0.f, -1, kCV ? hc : nullptr, nullptr, 0, -1,
         kTrace ? trace + gw * kTraceLen : nullptr);
     const double gq = G * (active ? qm_[i] : 0.0);
     F[0] = gq * o.ax;
@@ -1183,6 +1186,15 @@ void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, co
           r, nn, qx, qy, qz, qm, order, m, theta2, G, eps2, f, fout, visits, accepted, acc_total,
           ob->trace);
     k_trace_stats<<<1, 1024, 0, s>>>(ob->trace, (m + 31) / 32, ob->stats);
+    return;
+  }
+  if (!visits) {  // accepted counts only (one counter per lane, no packed visits)
+    if (gz)
+      k_bh_operator<float, true, kOpT, false, false><<<g, kOpT, 0, s>>>(
+          r, nn, qx, qy, qz, qm, order, m, theta2, G, eps2, f, fout, visits, accepted, acc_total);
+    else
+      k_bh_operator<float, false, kOpT, false, false><<<g, kOpT, 0, s>>>(
+          r, nn, qx, qy, qz, qm, order, m, theta2, G, eps2, f, fout, visits, accepted, acc_total);
     return;
   }
   if (gz)
