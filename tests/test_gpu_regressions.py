@@ -237,3 +237,32 @@ def test_pinned_outputs_written_in_place_equal_pageable():
         assert np.array_equal(fp, f) and np.array_equal(vp, vis)
         fp[:] = np.nan
         vp[:] = -1
+
+
+def test_operator_without_visits_same_forces_and_count():
+    """fga_tree_forces with visits=NULL runs the operator without per-query
+    visit counters (the registration loop's call): the same forces to the
+    bit and the same interaction count as with them, on a multi-wave call
+    (300k queries: no split passes)."""
+    from paper_2009_14005_b200 import PointCloud, bhtree, synth
+    from paper_2009_14005_b200 import _native as N
+    rng = synth.rng_from_seed(17)
+    x = synth.blob(50000, rng)
+    mx = rng.uniform(0.005, 0.02, len(x))
+    bhtree.build(PointCloud(x.points), mx, 20)
+    q = np.ascontiguousarray(synth.blob(300000, rng).points)
+    qm = rng.uniform(0.02, 0.1, len(q))
+    c = N.context(0)
+    L = N.lib()
+    out = []
+    for with_visits in (True, False, True):
+        f = np.zeros((len(q), 3))
+        vis = np.zeros(len(q), np.int64)
+        t = N._i64(-1)
+        N.check(L.fga_tree_forces(c.handle, N.ptr(q), N.ptr(qm), len(q), 0.5, 1.0, 0.04, 0,
+                                  N.ptr(f), N.ptr(vis) if with_visits else None, None))
+        N.check(L.fga_last_interactions(c.handle, ctypes.byref(t)))
+        out.append((f, vis, t.value))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][0], out[2][0])
+    assert out[0][2] == out[1][2] == out[2][2] > 0
+    assert np.array_equal(out[0][1], out[2][1]) and out[0][1].min() > 0
