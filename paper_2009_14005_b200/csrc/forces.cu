@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kT, sizeof(Real) == 4 ? FGA_BHOP32_TPS / kT
 // recorded (k_bh_operator<kTrace>) -- in the reference's loop the template
 // moves a little per call, so the warps' step profiles carry over; any split
 // points give the same visits, accepted sets and (to fp64 regrouping) forces.
-template <bool kGuardZero>
+template <bool kGuardZero, bool kCV>
 __global__ void __launch_bounds__(kSplitT, FGA_SPLIT_TPS / kSplitT) k_bh_op_split(
     TreeRecords tr, int n_nodes, const double* __restrict__ qx_, const double* __restrict__ qy_,
     const double* __restrict__ qz_, int64_t m, F32Params f, double theta2_64,
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(kSplitT, FGA_SPLIT_TPS / kSplitT) k_bh_op_spli
   }
   // ptrace: the parts' own step counts (k_trace_stats -> whether the trace
   // still balances this call's queries)
-  const Trav32Out o = traverse32d<kGuardZero, true, false, false, true, false, true>(
+  const Trav32Out o = traverse32d<kGuardZero, kCV, false, false, true, false, true>(
       tr.c32, tr.a64, tr.b64, n_nodes, (float)q[0], (float)q[1], (float)q[2], active, f.theta2,
       theta2_64, f.eps2, nullptr, nullptr, nullptr, m, hs, 0.f, 0.f, -1, nullptr, qsh, lo, hi,
       ptrace + g * kTraceLen);
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kSplitT, FGA_SPLIT_TPS / kSplitT) k_bh_op_spli
   fp[0] = o.ax;
   fp[1] = o.ay;
   fp[2] = o.az;
-  vpart[part * m + i] = o.visits;
+  if (kCV) vpart[part * m + i] = o.visits;
   apart[part * m + i] = o.accepted;
 }
 
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(256) k_bh_op_split_epi(
       h[0] += fq[0];
       h[1] += fq[1];
       h[2] += fq[2];
-      nv += vpart[q * m + i];
+      if (visits) nv += vpart[q * m + i];
       na += apart[q * m + i];
     }
   }
@@ -1164,12 +1164,18 @@ void launch_bh_operator(const TreeDev& T, const double* qx, const double* qy, co
   if (ob && ob->mode == 2) {
     const int64_t nw = (m + 31) / 32;
     const unsigned gs = (unsigned)((kParts * nw + kSplitT / 32 - 1) / (kSplitT / 32));
-    if (gz)
-      k_bh_op_split<true><<<gs, kSplitT, 0, s>>>(r, nn, qx, qy, qz, m, f, theta2, ob->trace, nw,
-                                                  ob->fpart, ob->vpart, ob->apart, ob->ptrace);
+#define FGA_OP_SPLIT(GZ, CV)                                                                  \
+  k_bh_op_split<GZ, CV><<<gs, kSplitT, 0, s>>>(r, nn, qx, qy, qz, m, f, theta2, ob->trace, nw,  \
+                                               ob->fpart, ob->vpart, ob->apart, ob->ptrace)
+    if (gz && visits)
+      FGA_OP_SPLIT(true, true);
+    else if (gz)
+      FGA_OP_SPLIT(true, false);
+    else if (visits)
+      FGA_OP_SPLIT(false, true);
     else
-      k_bh_op_split<false><<<gs, kSplitT, 0, s>>>(r, nn, qx, qy, qz, m, f, theta2, ob->trace, nw,
-                                                   ob->fpart, ob->vpart, ob->apart, ob->ptrace);
+      FGA_OP_SPLIT(false, false);
+#undef FGA_OP_SPLIT
     k_trace_stats<<<1, 1024, 0, s>>>(ob->ptrace, kParts * nw, ob->stats);
     k_bh_op_split_epi<<<grid_for(m, 256), 256, 0, s>>>(qm, order, m, G, ob->fpart, ob->vpart,
                                                        ob->apart, fout, visits, accepted,
